@@ -1,0 +1,227 @@
+/*
+ * lsrm_b200.h — C ABI of the B200-native LSRM sparse-attention hot path.
+ *
+ * Every entry point takes plain pointers to caller-owned DEVICE memory
+ * (unless a parameter says "host"), sizes as int64_t, and the CUDA stream to
+ * run on (cudaStream_t passed as void*).  Nothing allocates device memory
+ * behind the caller's back except the documented per-device cuBLAS handle.
+ * Calls are reentrant: no shared scratch, per-call stream, per-thread error
+ * buffer.  Outputs are deterministic (fixed reduction orders, no float
+ * atomics on outputs).
+ *
+ * Each function cites the reference interface it replaces
+ * (/root/reference/pkg/src/lsrm/<file>:<line>); INTEGRATION.md shows the
+ * ctypes binding the reference-side `lsrm` package would add.
+ *
+ * Status codes map 1:1 onto the reference exception classes
+ * (lsrm/errors.py:8-59); lsrm_last_error() returns the message of the
+ * calling thread's last failure.
+ */
+#ifndef LSRM_B200_H
+#define LSRM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum lsrm_status {
+  LSRM_OK = 0,
+  LSRM_E_CONFIG = 1,          /* ConfigurationError  (errors.py:14-17) */
+  LSRM_E_EMPTY_CONTEXT = 2,   /* EmptyContextError   (errors.py:30-31) */
+  LSRM_E_EMPTY_ROW = 3,       /* EmptyAttentionRowError (errors.py:26-27) */
+  LSRM_E_PROTOCOL = 4,        /* ProtocolError       (errors.py:42-43) */
+  LSRM_E_CUDA = 5,            /* LsrmError (internal, exit code 4) */
+  LSRM_E_OUT_OF_DOMAIN = 6    /* OutOfDomainError    (errors.py:34-35) */
+};
+
+/* ---- runtime ------------------------------------------------------------ */
+int lsrm_abi_version(void);
+const char* lsrm_last_error(void);
+/* Number of kernels this library launched on the calling thread since the
+ * last reset (evidence for bench.py's gpu_launches). */
+int64_t lsrm_launch_count(void);
+void lsrm_reset_launch_count(void);
+
+/* ---- K11 spatial block partition  (block_partition.py:54-105) ----------
+ * modality 0 = volume (coords (i,j,k), grid g0=g1=g2=S),
+ *          1 = image  (coords (view,u,v), g0 = views, g1 = g2 = S_img).
+ * Outputs sized for the worst case (n_blocks_total rows); *n_occupied (host)
+ * receives B.  centers: [B,3] (volume, object units) or [B,2] (image, patch
+ * units); block_views [B] (image only, may be NULL for volume).
+ * workspace >= lsrm_partition_workspace(n, n_blocks_total) bytes. */
+size_t lsrm_partition_workspace(int64_t n, int64_t n_blocks_total);
+int lsrm_partition(int modality, const int64_t* coords, int64_t n, int g0,
+                   int g1, int g2, int block_size, int64_t* block_of_token,
+                   int64_t* block_token_ids, int64_t* occupied_ids,
+                   int64_t* block_offsets, int64_t* occupancy,
+                   double* centers, int64_t* block_views,
+                   int64_t* n_occupied, void* workspace, size_t ws_bytes,
+                   void* stream);
+
+/* ---- K6 per-block KV compression  (block_partition.py:141-167) ---------
+ * x: [N, width] (f32, or bf16 when src_bf16) in token order, row stride ld_x;
+ * ResBlock x + W2 gelu(W1 x + b1) + b2 in f64 with the reference's f32
+ * roundings, then the in-block mean in ascending token order with an f64
+ * running sum.  out: [B, width] f32; scratch: [N, width] f32. */
+int lsrm_compress_block(int src_bf16, const void* x, int64_t ld_x, int64_t n,
+                        int width, const float* w1, const float* b1,
+                        const float* w2, const float* b2,
+                        const int64_t* block_token_ids,
+                        const int64_t* block_offsets, int64_t n_blocks,
+                        float* out, float* scratch, void* stream);
+
+/* ---- K7 volume router  (block_routing.py:115-143) ----------------------
+ * points [nq,3] f64; centers [B,3] f64.  out_rows [nq, budget] int32
+ * occupied-row indices (-1 padded), out_count [nq].  f64, no FMA:
+ * bit-exact with the reference including tie order. */
+int lsrm_route_volume(const double* points, int64_t nq, const double* centers,
+                      int64_t n_blocks, int budget, int32_t* out_rows,
+                      int32_t* out_count, void* stream);
+
+/* ---- K8 image router  (block_routing.py:150-230) -----------------------
+ * cams: [n_views, 21] f64 rows = K(9) R(9) t(3), row-major.
+ * view_row_start [n_views+1]: occupied-row range of each view.
+ * block_centers [B,2] (patch units); token_points_bm [Ni,3] f64 in
+ * block-major order; block_offsets [B+1]. */
+int lsrm_route_image(const double* points, int64_t nq, const double* cams,
+                     int n_views, const int64_t* view_row_start,
+                     const double* block_centers, int64_t n_blocks,
+                     const double* token_points_bm,
+                     const int64_t* block_offsets, int b_i, int budget,
+                     int32_t* out_rows, int32_t* out_count, void* stream);
+
+/* ---- gather table  (nsa_attention.py:123-154) -------------------------
+ * Resolves routed rows (fallback: own block row, else row 0) into padded
+ * token-id rows.  own_row may be NULL.  With fallback = 0 an empty row stays
+ * empty (resolved_count 0, length 0); the host raises EmptyAttentionRowError.
+ * resolved_rows/resolved_count receive the fallback-applied rows (the
+ * attention kernels' input).  ids/valid may be NULL (lengths only). */
+int lsrm_build_gather_table(const int32_t* rows, const int32_t* count,
+                            int64_t nq, int kmax_rows, const int32_t* own_row,
+                            int fallback, const int64_t* block_offsets,
+                            const int64_t* block_token_ids, int64_t width,
+                            int32_t* resolved_rows, int32_t* resolved_count,
+                            int64_t* ids, uint8_t* valid, int64_t* lengths,
+                            void* stream);
+
+/* ---- K9 foreground patch mask  (tokenizer.py:200-208) ------------------ */
+int lsrm_foreground_mask(const float* alpha, int n_views, int h, int w,
+                         int patch, uint8_t* mask, void* stream);
+
+/* ---- K10 informative voxel mask  (tokenizer.py:211-239) ---------------
+ * sdf: n_prims rows of 8 f64 = kind(0 sphere, 1 box), cx, cy, cz,
+ * radius | hx, hy, hz, unused.  The field is the union (min) of all
+ * primitives (camera_geometry.py:190-205). */
+int lsrm_voxel_mask(const double* sdf, int n_prims, int s_vol, double tau,
+                    int t_side, uint8_t* mask, void* stream);
+
+/* ---- compaction  (tokenizer.py:255-313) -------------------------------
+ * Stream-compacts mask-true cells in flat order and gathers parent feature +
+ * factorized fine pos-embed with the reference's two f64 roundings.
+ * volume: mask [S^3], parent grid S/factor; image: mask [V,S,S] (view, row,
+ * col), coords written as (view, u=col, v=row).  *n_out (host) = count.
+ * Call with features == NULL to only count (coords may be NULL too). */
+size_t lsrm_compact_workspace(int64_t n_cells);
+int lsrm_compact_volume(const uint8_t* mask, int s_fine, int factor,
+                        const float* x_d, int d, const float* pe0,
+                        const float* pe1, const float* pe2, int64_t* coords,
+                        float* features, int64_t max_out, int64_t* n_out,
+                        void* workspace, size_t ws_bytes, void* stream);
+int lsrm_compact_image(const uint8_t* mask, int n_views, int s_fine,
+                       int factor, const float* y_d, int d, const float* pe_u,
+                       const float* pe_v, int64_t* coords, float* features,
+                       int64_t max_out, int64_t* n_out, void* workspace,
+                       size_t ws_bytes, void* stream);
+
+/* ---- fp32 attention branches on CUDA cores  (nsa_attention.py:84-207) --
+ * q [nq, hq, dh]; keys/values [nk, hkv, dh] f32 in BLOCK-MAJOR order of the
+ * KV partition (row r = block_offsets[r]..block_offsets[r+1]).
+ * mode 0 = cmp (all nk rows are keys), 1 = sel (rows[i, :count[i]] are
+ * occupied rows, resolved), 2 = win (own_row[i]), 3 = explicit gather table
+ * (ids [nq, width] token ids into kv_token_order arrays, lengths[i]).
+ * out [nq, hq, dh]. */
+int lsrm_attention_f32(int mode, const float* q, int64_t nq, int hq, int hkv,
+                       int dh, const float* k, const float* v, int64_t nk,
+                       const int64_t* block_offsets, const int32_t* rows,
+                       const int32_t* count, int kmax_rows,
+                       const int32_t* own_row, const int64_t* ids,
+                       const int64_t* lengths, int64_t width, float* out,
+                       void* stream);
+
+/* ---- gated merge, fp32 path  (nsa_attention.py:266-284) ---------------
+ * merged[i,:] = f32( sum_b f64(sigmoid(gl[i, b*d:(b+1)*d] + gb)) * f64(o_b) )
+ * gl: gate logits [n, n_gates*d] (row stride ld_gl); o_b: [n, d] each. */
+int lsrm_gated_merge_f32(const float* gate_logits, int64_t ld_gl,
+                         const float* gate_bias, int n_gates,
+                         const float* o0, const float* o1, const float* o2,
+                         int64_t n, int d, float* merged, void* stream);
+
+/* out[n, cols] = f32(sigmoid_f64(f32(logits + bias)))  (tensor_core.py:89-94) */
+int lsrm_sigmoid_f32(const float* logits, int64_t ld, const float* bias,
+                     int64_t n, int cols, float* out, void* stream);
+
+/* ---- vanilla score top-k  (nsa_attention.py:210-232) ------------------
+ * score[i,b] = sum_h sum_d q[i,h,:] . k_cmp[b, h/group, :] in f64 (unscaled);
+ * out_rows [nq, b_sel] = stable descending top-min(b_sel, B) columns. */
+int lsrm_score_topk(const float* q, int64_t nq, int hq, int hkv, int dh,
+                    const float* k_cmp, int64_t n_blocks, int b_sel,
+                    int32_t* out_rows, int32_t* out_count, void* stream);
+
+/* ---- GEMM (plain library GEMM, cuBLAS) --------------------------------
+ * C[m,n] = A[m,k] @ B[k,n] (+ bias[n]), row-major, lda/ldb/ldc in elements.
+ * dtype 0 = fp32 (FFMA, no TF32), 1 = bf16 in / fp32 accumulate / bf16 out,
+ * 2 = bf16 in / fp32 out. */
+int lsrm_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a,
+              int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
+              void* stream);
+
+/* ---- fused bf16 three-branch NSA attention, tcgen05/TMEM  -------------
+ * (nsa_attention.py:84-112,157-207,266-284 fused)
+ * q: [nq, hq, dh] bf16 in query BLOCK-MAJOR order; kv_il: K and V in the
+ * padded interleaved layout written by lsrm_kv_interleave; kcmp_il/vcmp_il
+ * likewise for the compressed rows.  tiles: [n_tiles, 4] int32 = (first
+ * query, count, own kv row (or -1), unused).  rows/count: resolved selected
+ * rows per query.  gate_logits bf16 [nq, ld_gl] with the n_gates width-d
+ * slices at column gate_col0.  merged bf16 [nq, hq*dh]. */
+int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int hkv, int dh,
+                          const void* k_il, const void* v_il,
+                          const int64_t* pad_offsets, const int64_t* kv_offsets,
+                          int64_t n_kv_rows_pad,
+                          const void* kcmp_il, const void* vcmp_il,
+                          int64_t n_blocks, const int32_t* tiles,
+                          int64_t n_tiles, const int32_t* rows,
+                          const int32_t* count, int kmax_rows,
+                          const void* gate_logits, int64_t ld_gl,
+                          int64_t gate_col0, const float* gate_bias,
+                          int n_gates, void* merged, void* stream);
+
+/* Re-layout K or V ([n, hkv, dh] f32 or bf16, token order) into the padded,
+ * 8x8-core-matrix interleaved bf16 layout the tcgen05 kernel consumes:
+ * per kv head, per block, rows padded to a multiple of 16. */
+int lsrm_kv_interleave(int src_is_bf16, const void* src, int64_t ld_src,
+                       int64_t n, int hkv, int dh,
+                       const int64_t* block_token_ids,
+                       const int64_t* block_offsets, int64_t n_blocks,
+                       const int64_t* pad_offsets, int64_t n_rows_pad,
+                       void* dst, void* stream);
+
+/* Row permutation helpers (block-major <-> token order). */
+int lsrm_gather_rows(int elem_bytes, const void* src, int64_t ld_src,
+                     const int64_t* index, int64_t n, int64_t row_elems,
+                     void* dst, int64_t ld_dst, void* stream);
+int lsrm_scatter_rows(int elem_bytes, const void* src, int64_t ld_src,
+                      const int64_t* index, int64_t n, int64_t row_elems,
+                      void* dst, int64_t ld_dst, void* stream);
+/* f32 <-> bf16 conversion, LayerNorm (tensor_core.py:139-146). */
+int lsrm_cast(int to_bf16, const void* src, void* dst, int64_t n, void* stream);
+int lsrm_layer_norm(int in_bf16, const void* x, int64_t n, int d,
+                    const float* gamma, const float* beta, float eps,
+                    int out_bf16, void* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSRM_B200_H */

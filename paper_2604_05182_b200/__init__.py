@@ -1,0 +1,27 @@
+"""B200-native drop-in for the LSRM sparse-attention hot path (arXiv 2604.05182).
+
+Mirrors the reference `lsrm` module API for the hot path:
+NSA three-branch attention, the 3D-aware router, foreground/voxel pruning and
+compaction, block partition/compression and block-aware sequence parallelism.
+All compute runs in the in-tree C-ABI library `_lib/liblsrm_b200.so`
+(hand-written sm_100a CUDA + cuBLAS for plain GEMMs); there is no CPU fallback.
+"""
+
+from .errors import (BehindCameraError, ConfigurationError, EmptyAttentionRowError,
+                     EmptyContextError, GoldenFormatError, LsrmError, OutOfDomainError,
+                     ProtocolError, VerificationError)
+from .tensor_core import AttentionParams
+from .tokenizer import (PosEmbed, TokenSet, foreground_patch_mask, informative_voxel_mask,
+                        init_pos_embed, upsample_select_tokens)
+from .block_partition import (BlockPartition, CompressWeights, compress_block_kv,
+                              init_compress_weights, occupancy_stats, partition)
+from .nsa_attention import (GatherTable, NsaWeights, Selection, build_gather_table,
+                            cmp_attention, combine_nsa_branches, full_selection,
+                            init_nsa_weights, nsa_cross_attention, nsa_gates,
+                            read_selection, score_topk_blocks, sel_attention,
+                            win_attention, write_selection)
+from .block_routing import (RoutingBudgets, RoutingPlan, TokenCoords3D, build_routing_plan,
+                            route_to_image_blocks, route_to_volume_blocks,
+                            volume_token_coords, write_plan)
+
+__version__ = "0.1.0"

@@ -1,0 +1,97 @@
+"""ctypes binding of the in-tree C-ABI library (include/lsrm_b200.h).
+
+There is deliberately no CPU fallback: if the library is missing or no CUDA
+device is visible, every compute entry point raises.  `lib()` loads
+`_lib/liblsrm_b200.so` once per process; `call(name, *args)` maps non-zero
+status codes onto the reference exception classes.
+"""
+
+import ctypes as C
+import os
+
+from .errors import STATUS_CLASSES, LsrmError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "liblsrm_b200.so")
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int
+F32 = C.c_float
+F64 = C.c_double
+SZ = C.c_size_t
+
+# name -> (restype, argtypes); must match include/lsrm_b200.h
+SIGNATURES = {
+    "lsrm_abi_version": (I32, []),
+    "lsrm_last_error": (C.c_char_p, []),
+    "lsrm_launch_count": (I64, []),
+    "lsrm_reset_launch_count": (None, []),
+    "lsrm_partition_workspace": (SZ, [I64, I64]),
+    "lsrm_partition": (I32, [I32, P, I64, I32, I32, I32, I32, P, P, P, P, P, P, P,
+                             P, P, SZ, P]),
+    "lsrm_compress_block": (I32, [I32, P, I64, I64, I32, P, P, P, P, P, P, I64, P,
+                                  P, P]),
+    "lsrm_route_volume": (I32, [P, I64, P, I64, I32, P, P, P]),
+    "lsrm_route_image": (I32, [P, I64, P, I32, P, P, I64, P, P, I32, I32, P, P, P]),
+    "lsrm_build_gather_table": (I32, [P, P, I64, I32, P, I32, P, P, I64, P, P, P, P,
+                                      P, P]),
+    "lsrm_foreground_mask": (I32, [P, I32, I32, I32, I32, P, P]),
+    "lsrm_voxel_mask": (I32, [P, I32, I32, F64, I32, P, P]),
+    "lsrm_compact_workspace": (SZ, [I64]),
+    "lsrm_compact_volume": (I32, [P, I32, I32, P, I32, P, P, P, P, P, I64, P, P, SZ,
+                                  P]),
+    "lsrm_compact_image": (I32, [P, I32, I32, I32, P, I32, P, P, P, P, I64, P, P,
+                                 SZ, P]),
+    "lsrm_attention_f32": (I32, [I32, P, I64, I32, I32, I32, P, P, I64, P, P, P,
+                                 I32, P, P, P, I64, P, P]),
+    "lsrm_gated_merge_f32": (I32, [P, I64, P, I32, P, P, P, I64, I32, P, P]),
+    "lsrm_sigmoid_f32": (I32, [P, I64, P, I64, I32, P, P]),
+    "lsrm_score_topk": (I32, [P, I64, I32, I32, I32, P, I64, I32, P, P, P]),
+    "lsrm_gemm": (I32, [I32, I64, I64, I64, P, I64, P, I64, P, I64, P]),
+    "lsrm_nsa_attention_tc": (I32, [P, I64, I64, I32, I32, I32, P, P, P, P, I64, P, P,
+                                    I64, P, I64, P, P, I32, P, I64, I64, P, I32, P, P]),
+    "lsrm_kv_interleave": (I32, [I32, P, I64, I64, I32, I32, P, P, I64, P, I64, P,
+                                 P]),
+    "lsrm_gather_rows": (I32, [I32, P, I64, P, I64, I64, P, I64, P]),
+    "lsrm_scatter_rows": (I32, [I32, P, I64, P, I64, I64, P, I64, P]),
+    "lsrm_cast": (I32, [I32, P, P, I64, P]),
+    "lsrm_layer_norm": (I32, [I32, P, I64, I32, P, P, F32, I32, P, P]),
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise LsrmError(
+                f"CUDA extension {LIB_PATH} is missing; run "
+                "`python -m paper_2604_05182_b200.build` (there is no CPU fallback)")
+        handle = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def exported_symbols():
+    return sorted(SIGNATURES)
+
+
+def call(name, *args):
+    rc = getattr(lib(), name)(*args)
+    if rc:
+        msg = lib().lsrm_last_error().decode(errors="replace")
+        raise STATUS_CLASSES.get(rc, LsrmError)(msg)
+
+
+def launch_count() -> int:
+    return int(lib().lsrm_launch_count())
+
+
+def reset_launch_count() -> None:
+    lib().lsrm_reset_launch_count()

@@ -1,0 +1,177 @@
+"""3D-aware spatial routing on the GPU (drop-in for `lsrm/block_routing.py`).
+
+Volume KV blocks are ranked by center distance; image KV blocks by the
+two-stage rule (per-view 2D shortlist of b_i blocks, pooled, ranked by min 3D
+distance to the block's token points).  The kernels (csrc/routing.cu) are f64
+with no FMA contraction and exact lexicographic (distance, row) selection, so
+the lists equal the reference's bit for bit, tie order included.
+"""
+
+import struct
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import _dev as D
+from . import _ops
+from ._native import call
+from .block_partition import BlockPartition
+from .errors import require
+from .nsa_attention import Selection, write_selection
+
+QUERY_CHUNK = 512
+PLAN_TABLE_ORDER = ("v2v", "v2i", "i2v", "i2i")
+
+
+@dataclass
+class RoutingBudgets:
+    b_i: int = 16
+    b_v2v: int = 8
+    b_v2i: int = 8
+    b_i2v: int = 8
+    b_i2i: int = 8
+
+
+@dataclass
+class TokenCoords3D:
+    points: np.ndarray
+    miss: np.ndarray
+
+    def __post_init__(self):
+        self.points = np.asarray(self.points, dtype=np.float64)
+        self.miss = np.asarray(self.miss, dtype=bool)
+        require(self.points.ndim == 2 and self.points.shape[1] == 3, "token points must be [N,3]")
+        require(self.miss.shape == (self.points.shape[0],), "miss flags must be [N]")
+        if self.points.size:
+            require(float(self.points.min()) >= 0.0 and float(self.points.max()) <= 1.0,
+                    "token points must lie in the unit cube")
+
+
+@dataclass
+class RoutingPlan:
+    tables: dict
+    budgets: RoutingBudgets
+    fallback_queries: dict = dc_field(default_factory=dict)
+    device_rows: dict = dc_field(default_factory=dict, repr=False)   # name -> (rows, count)
+
+
+def volume_token_coords(tokens) -> TokenCoords3D:
+    """Voxel centers (c + 0.5) / S (`block_routing.py:67-70`)."""
+    side = tokens.grid_res[0]
+    c = tokens.coords if not D.is_device(tokens.coords) else D.host(tokens.coords)
+    return TokenCoords3D((c.astype(np.float64) + 0.5) / side, np.zeros(tokens.count, bool))
+
+
+def pack_cameras(cameras) -> np.ndarray:
+    """[V, 21] f64 rows K(9) R(9) t(3) from reference Camera objects or
+    (K, R, t) tuples."""
+    rows = []
+    for cam in cameras:
+        if isinstance(cam, (tuple, list)):
+            K, R, t = cam[:3]
+        else:
+            K, R, t = cam.intrinsics, cam.rotation, cam.translation
+        rows.append(np.concatenate([np.asarray(K, np.float64).ravel(),
+                                    np.asarray(R, np.float64).ravel(),
+                                    np.asarray(t, np.float64).ravel()]))
+    return np.asarray(rows, np.float64).reshape(-1, 21)
+
+
+def _rows_to_selection(rows, count, part: BlockPartition) -> Selection:
+    r = D.host(rows)
+    c = D.host(count)
+    ids = part.occupied_ids
+    return Selection([ids[r[i, :c[i]]] for i in range(r.shape[0])])
+
+
+def route_volume_rows(points, part: BlockPartition, budget: int):
+    """Device result: (rows [nq, budget] int32, count [nq] int32)."""
+    pts = D.dev(points, torch.float64)
+    nq = int(pts.shape[0])
+    rows = D.empty((nq, max(budget, 1)), torch.int32)
+    count = D.zeros((nq,), torch.int32)
+    if nq and part.n_occupied:
+        call("lsrm_route_volume", pts.data_ptr(), nq, part.dev("block_centers").data_ptr(),
+             part.n_occupied, budget, rows.data_ptr(), count.data_ptr(), D.stream())
+    else:
+        rows.fill_(-1)
+    return rows, count
+
+
+def route_image_rows(points, cameras, part: BlockPartition, token_points, b_i: int,
+                     budget: int):
+    pts = D.dev(points, torch.float64)
+    nq = int(pts.shape[0])
+    rows = D.empty((nq, max(budget, 1)), torch.int32)
+    count = D.zeros((nq,), torch.int32)
+    if nq == 0 or part.n_occupied == 0:
+        rows.fill_(-1)
+        return rows, count
+    cams = pack_cameras(cameras)
+    n_views = cams.shape[0]
+    vrs = np.searchsorted(part.block_views, np.arange(n_views + 1)).astype(np.int64)
+    tp = token_points.points if isinstance(token_points, TokenCoords3D) else token_points
+    tp_bm = _ops.gather_rows(D.dev(tp, torch.float64), part.dev("block_token_ids"))
+    call("lsrm_route_image", pts.data_ptr(), nq, D.dev(cams).data_ptr(), n_views,
+         D.dev(vrs).data_ptr(), part.dev("block_centers").data_ptr(), part.n_occupied,
+         tp_bm.data_ptr(), part.dev("block_offsets").data_ptr(), b_i, budget,
+         rows.data_ptr(), count.data_ptr(), D.stream())
+    return rows, count
+
+
+def _route_points_to_volume(points, part: BlockPartition, budget: int) -> Selection:
+    """`block_routing.py:134-143`."""
+    return _rows_to_selection(*route_volume_rows(points, part, budget), part)
+
+
+def route_to_volume_blocks(p, vol_part: BlockPartition, budget: int) -> np.ndarray:
+    """`block_routing.py:124-131`."""
+    return _route_points_to_volume(np.asarray(p, np.float64).reshape(1, 3), vol_part,
+                                   budget).lists[0]
+
+
+def _route_points_to_image(points, cameras, img_part: BlockPartition, img_coords3d,
+                           b_i: int, budget: int) -> Selection:
+    """`block_routing.py:183-220`."""
+    return _rows_to_selection(*route_image_rows(points, cameras, img_part, img_coords3d,
+                                                b_i, budget), img_part)
+
+
+def route_to_image_blocks(p, cameras, img_part, img_coords3d, b_i, budget) -> np.ndarray:
+    """`block_routing.py:223-230`."""
+    return _route_points_to_image(np.asarray(p, np.float64).reshape(1, 3), cameras,
+                                  img_part, img_coords3d, b_i, budget).lists[0]
+
+
+def build_routing_plan(vol_coords, img_coords, part_vol, part_img, cameras,
+                       budgets: RoutingBudgets, host_lists: bool = True) -> RoutingPlan:
+    """All four query->KV tables (`block_routing.py:237-258`); the device rows
+    are kept on the plan for the fused attention path."""
+    vp = vol_coords.points if isinstance(vol_coords, TokenCoords3D) else vol_coords
+    ip = img_coords.points if isinstance(img_coords, TokenCoords3D) else img_coords
+    dev_rows = {
+        "v2v": route_volume_rows(vp, part_vol, budgets.b_v2v),
+        "i2v": route_volume_rows(ip, part_vol, budgets.b_i2v),
+        "v2i": route_image_rows(vp, cameras, part_img, ip, budgets.b_i, budgets.b_v2i),
+        "i2i": route_image_rows(ip, cameras, part_img, ip, budgets.b_i, budgets.b_i2i),
+    }
+    parts = {"v2v": part_vol, "i2v": part_vol, "v2i": part_img, "i2i": part_img}
+    tables, fallback = {}, {}
+    if host_lists:
+        for name in ("v2v", "i2v", "v2i", "i2i"):
+            tables[name] = _rows_to_selection(*dev_rows[name], parts[name])
+            empty = [i for i, l in enumerate(tables[name].lists) if len(l) == 0]
+            if empty:
+                fallback[name] = empty
+    plan = RoutingPlan(tables, budgets, fallback)
+    plan.device_rows = dev_rows
+    return plan
+
+
+def write_plan(path, plan: RoutingPlan) -> None:
+    """`block_routing.py:284-290`: four tables in fixed order."""
+    with open(path, "wb") as fh:
+        fh.write(struct.pack("<I", len(PLAN_TABLE_ORDER)))
+        for name in PLAN_TABLE_ORDER:
+            write_selection(fh, plan.tables[name])

@@ -1,0 +1,238 @@
+// fp32 NSA attention branches on CUDA cores (lsrm/nsa_attention.py:84-207)
+// and the fp32 gated merge (nsa_attention.py:266-284).
+//
+// This is the exact-precision path (BASELINE config C1 "fp32 fwd", and the
+// reference API's f32 contract): one thread per (query, q-head), keys walked
+// in block order with an fp32 online softmax (accurate expf), FFMA dot
+// products.  Keys/values are in the KV partition's block-major order so each
+// selected block is one contiguous row range.
+#include "common.cuh"
+
+namespace lsrm {
+
+template <int DH>
+__device__ __forceinline__ void attend_range(const float* __restrict__ k,
+                                             const float* __restrict__ v, int hkv,
+                                             int kvh, int64_t lo, int64_t hi,
+                                             const float (&q)[DH], float scale, float& m,
+                                             float& l, float (&acc)[DH]) {
+  for (int64_t j = lo; j < hi; ++j) {
+    const float* kr = k + (j * hkv + kvh) * DH;
+    const float* vr = v + (j * hkv + kvh) * DH;
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) s = fmaf(q[c], kr[c], s);
+    s *= scale;
+    if (s > m) {
+      float corr = expf(m - s);  // m = -inf -> 0
+      l *= corr;
+#pragma unroll
+      for (int c = 0; c < DH; ++c) acc[c] *= corr;
+      m = s;
+    }
+    float p = expf(s - m);
+    l += p;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) acc[c] = fmaf(p, vr[c], acc[c]);
+  }
+}
+
+template <int DH>
+__global__ void attention_f32_kernel(int mode, const float* __restrict__ q, int64_t nq,
+                                     int hq, int hkv, const float* __restrict__ k,
+                                     const float* __restrict__ v, int64_t nk,
+                                     const int64_t* __restrict__ offs,
+                                     const int32_t* __restrict__ rows,
+                                     const int32_t* __restrict__ count, int kmax,
+                                     const int32_t* __restrict__ own_row,
+                                     const int64_t* __restrict__ ids,
+                                     const int64_t* __restrict__ lengths, int64_t width,
+                                     float* __restrict__ out) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nq * hq) return;
+  int64_t i = t / hq;
+  int h = (int)(t % hq);
+  int kvh = h / (hq / hkv);
+  float qr[DH], acc[DH];
+#pragma unroll
+  for (int c = 0; c < DH; ++c) { qr[c] = q[t * DH + c]; acc[c] = 0.f; }
+  const float scale = 1.0f / sqrtf((float)DH);
+  float m = -__builtin_huge_valf(), l = 0.f;
+  if (mode == 0) {
+    attend_range<DH>(k, v, hkv, kvh, 0, nk, qr, scale, m, l, acc);
+  } else if (mode == 1) {
+    int c = count[i];
+    for (int s = 0; s < c; ++s) {
+      int r = rows[i * kmax + s];
+      attend_range<DH>(k, v, hkv, kvh, offs[r], offs[r + 1], qr, scale, m, l, acc);
+    }
+  } else if (mode == 2) {
+    int r = own_row[i];
+    attend_range<DH>(k, v, hkv, kvh, offs[r], offs[r + 1], qr, scale, m, l, acc);
+  } else {
+    int64_t len = lengths[i];
+    for (int64_t s = 0; s < len; ++s) {
+      int64_t j = ids[i * width + s];
+      attend_range<DH>(k, v, hkv, kvh, j, j + 1, qr, scale, m, l, acc);
+    }
+  }
+  float inv = 1.0f / l;
+#pragma unroll
+  for (int c = 0; c < DH; ++c) out[t * DH + c] = acc[c] * inv;
+}
+
+__global__ void gated_merge_f32_kernel(const float* __restrict__ gl, int64_t ld,
+                                       const float* __restrict__ gb, int ng,
+                                       const float* __restrict__ o0,
+                                       const float* __restrict__ o1,
+                                       const float* __restrict__ o2, int64_t n, int d,
+                                       float* __restrict__ merged) {
+  int64_t total = n * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / d;
+    int c = (int)(e % d);
+    const float* ob[3] = {o0, o1, o2};
+    double acc = 0.0;
+    for (int b = 0; b < ng; ++b) {
+      // gate = f32(sigmoid_f64(f32(logit + bias)))   (tensor_core.py:89-94)
+      float z = gl[i * ld + b * d + c] + (gb ? gb[b * d + c] : 0.f);
+      double x = (double)z;
+      double g = x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
+      acc += (double)(float)g * (double)ob[b][e];
+    }
+    merged[e] = (float)acc;
+  }
+}
+
+__device__ __forceinline__ float sigmoid_ref(float z) {
+  double x = (double)z;
+  return (float)(x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x)));
+}
+
+__global__ void sigmoid_f32_kernel(const float* __restrict__ gl, int64_t ld,
+                                   const float* __restrict__ gb, int64_t n, int cols,
+                                   float* __restrict__ out) {
+  int64_t total = n * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / cols;
+    int c = (int)(e % cols);
+    out[e] = sigmoid_ref(gl[i * ld + c] + (gb ? gb[c] : 0.f));
+  }
+}
+
+// Vanilla selection (nsa_attention.py:210-232): score = sum_h sum_d q.k_cmp in
+// f64, unscaled; stable descending top-b_sel == lexicographic (-score, col).
+__global__ void score_topk_kernel(const float* __restrict__ q, int64_t nq, int hq, int hkv,
+                                  int dh, const float* __restrict__ kc, int nb, int b_sel,
+                                  int32_t* __restrict__ out_rows,
+                                  int32_t* __restrict__ out_count) {
+  int64_t i = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (i >= nq) return;
+  int g = hq / hkv;
+  int take = min(b_sel, nb);
+  double last_v = -__builtin_huge_val();
+  int last_i = -1;
+  for (int s = 0; s < take; ++s) {
+    double best = __builtin_huge_val();
+    int bi = 0x7fffffff;
+    for (int b = lane; b < nb; b += 32) {
+      double sc = 0.0;
+      for (int h = 0; h < hq; ++h)
+        for (int c = 0; c < dh; ++c)
+          sc += (double)q[(i * hq + h) * dh + c] * (double)kc[((int64_t)b * hkv + h / g) * dh + c];
+      double key = -sc;
+      if (lex_less(last_v, last_i, key, b) && lex_less(key, b, best, bi)) { best = key; bi = b; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (lex_less(ov, oi, best, bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) out_rows[i * b_sel + s] = bi;
+    last_v = best;
+    last_i = bi;
+  }
+  if (lane == 0) {
+    for (int s = take; s < b_sel; ++s) out_rows[i * b_sel + s] = -1;
+    out_count[i] = take;
+  }
+}
+
+}  // namespace lsrm
+
+using namespace lsrm;
+
+extern "C" {
+
+int lsrm_sigmoid_f32(const float* logits, int64_t ld, const float* bias, int64_t n, int cols,
+                     float* out, void* stream) {
+  if (n == 0) return LSRM_OK;
+  int blocks = (int)std::min<int64_t>(ceil_div(n * cols, 256), 148 * 16);
+  sigmoid_f32_kernel<<<blocks, 256, 0, as_stream(stream)>>>(logits, ld, bias, n, cols, out);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_score_topk(const float* q, int64_t nq, int hq, int hkv, int dh, const float* k_cmp,
+                    int64_t n_blocks, int b_sel, int32_t* out_rows, int32_t* out_count,
+                    void* stream) {
+  LSRM_REQUIRE(b_sel >= 1, "b_sel must be at least 1");
+  if (n_blocks == 0) return set_error(LSRM_E_EMPTY_CONTEXT, "scoring against zero compressed blocks");
+  if (nq == 0) return LSRM_OK;
+  score_topk_kernel<<<(unsigned)ceil_div(nq, 8), 256, 0, as_stream(stream)>>>(
+      q, nq, hq, hkv, dh, k_cmp, (int)n_blocks, b_sel, out_rows, out_count);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_attention_f32(int mode, const float* q, int64_t nq, int hq, int hkv, int dh,
+                       const float* k, const float* v, int64_t nk,
+                       const int64_t* block_offsets, const int32_t* rows,
+                       const int32_t* count, int kmax_rows, const int32_t* own_row,
+                       const int64_t* ids, const int64_t* lengths, int64_t width,
+                       float* out, void* stream) {
+  LSRM_REQUIRE(mode >= 0 && mode <= 3, "attention_f32: bad mode %d", mode);
+  LSRM_REQUIRE(hq >= 1 && hkv >= 1 && hq % hkv == 0,
+               "n_q_heads=%d not divisible by n_kv_heads=%d", hq, hkv);
+  if (nq == 0) return LSRM_OK;
+  if (nk == 0) return set_error(LSRM_E_EMPTY_CONTEXT, "attention over an empty key set");
+  unsigned blocks = (unsigned)ceil_div(nq * hq, 128);
+  cudaStream_t st = as_stream(stream);
+#define LSRM_ATTN_CASE(D)                                                              \
+  case D:                                                                              \
+    attention_f32_kernel<D><<<blocks, 128, 0, st>>>(mode, q, nq, hq, hkv, k, v, nk,    \
+                                                    block_offsets, rows, count,        \
+                                                    kmax_rows, own_row, ids, lengths,  \
+                                                    width, out);                       \
+    break;
+  switch (dh) {
+    LSRM_ATTN_CASE(4)
+    LSRM_ATTN_CASE(8)
+    LSRM_ATTN_CASE(16)
+    LSRM_ATTN_CASE(32)
+    LSRM_ATTN_CASE(64)
+    LSRM_ATTN_CASE(128)
+    default:
+      return set_error(LSRM_E_CONFIG, "attention_f32: head_dim %d not in {4,8,16,32,64,128}", dh);
+  }
+#undef LSRM_ATTN_CASE
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_gated_merge_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,
+                         int n_gates, const float* o0, const float* o1, const float* o2,
+                         int64_t n, int d, float* merged, void* stream) {
+  LSRM_REQUIRE(n_gates >= 1 && n_gates <= 3, "gated_merge: 1..3 gates");
+  if (n == 0) return LSRM_OK;
+  int blocks = (int)std::min<int64_t>(ceil_div(n * d, 256), 148 * 16);
+  gated_merge_f32_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      gate_logits, ld_gl, gate_bias, n_gates, o0, o1, o2, n, d, merged);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+}  // extern "C"

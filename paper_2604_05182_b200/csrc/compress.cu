@@ -1,0 +1,100 @@
+// K6 per-block KV compression (lsrm/block_partition.py:141-167).
+//
+// Pass 1 (token-parallel): ResBlock r = x + W2 gelu(W1 x + b1) + b2 per token,
+// evaluated in f64 with the reference's f32 roundings after each affine/gelu.
+// Pass 2 (block-parallel): mean over the block's tokens in ascending token id
+// order with an f64 running sum (fixed order: bit-stable across workers).
+#include "common.cuh"
+
+namespace lsrm {
+
+constexpr int kTokTile = 16;
+
+__device__ __forceinline__ double load_elem(const void* x, int bf16, int64_t idx) {
+  return bf16 ? (double)__bfloat162float(((const __nv_bfloat16*)x)[idx])
+              : (double)((const float*)x)[idx];
+}
+
+// smem: W1, W2 as f32 [w*w] each, x tile f64 [kTokTile*w], h tile f64 [kTokTile*w]
+__global__ void res_block_kernel(int src_bf16, const void* __restrict__ x, int64_t ld_x,
+                                 int64_t n, int w, const float* __restrict__ w1,
+                                 const float* __restrict__ b1, const float* __restrict__ w2,
+                                 const float* __restrict__ b2, float* __restrict__ r_out) {
+  extern __shared__ double sm[];
+  double* xt = sm;                       // [kTokTile][w]
+  double* ht = xt + kTokTile * w;        // [kTokTile][w]
+  float* W1 = (float*)(ht + kTokTile * w);
+  float* W2 = W1 + w * w;
+  for (int i = threadIdx.x; i < w * w; i += blockDim.x) { W1[i] = w1[i]; W2[i] = w2[i]; }
+  int64_t t0 = (int64_t)blockIdx.x * kTokTile;
+  int nt = (int)(n - t0 < kTokTile ? n - t0 : kTokTile);
+  for (int e = threadIdx.x; e < kTokTile * w; e += blockDim.x) {
+    int t = e / w, c = e % w;
+    xt[e] = t < nt ? (double)(float)load_elem(x, src_bf16, (t0 + t) * ld_x + c) : 0.0;
+  }
+  __syncthreads();
+  // h = f32(gelu(f32(x W1 + b1)))
+  for (int e = threadIdx.x; e < nt * w; e += blockDim.x) {
+    int t = e / w, o = e % w;
+    double acc = 0.0;
+    for (int i = 0; i < w; ++i) acc += xt[t * w + i] * (double)W1[i * w + o];
+    float a = (float)(acc + (double)b1[o]);
+    double a64 = (double)a;
+    ht[e] = (double)(float)(0.5 * a64 * (1.0 + erf(a64 * 0.70710678118654752440)));
+  }
+  __syncthreads();
+  // r = f32(x + f32(h W2 + b2))
+  for (int e = threadIdx.x; e < nt * w; e += blockDim.x) {
+    int t = e / w, o = e % w;
+    double acc = 0.0;
+    for (int i = 0; i < w; ++i) acc += ht[t * w + i] * (double)W2[i * w + o];
+    float h2 = (float)(acc + (double)b2[o]);
+    r_out[(t0 + t) * w + o] = (float)(xt[e] + (double)h2);
+  }
+}
+
+__global__ void block_mean_kernel(const float* __restrict__ r, int w,
+                                  const int64_t* __restrict__ tok,
+                                  const int64_t* __restrict__ offs, int64_t nb,
+                                  float* __restrict__ out) {
+  int64_t total = nb * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = e / w;
+    int c = (int)(e % w);
+    int64_t lo = offs[b], hi = offs[b + 1];
+    double s = 0.0;
+    for (int64_t j = lo; j < hi; ++j) s += (double)r[tok[j] * w + c];
+    out[e] = (float)(s / (double)(hi - lo));
+  }
+}
+
+}  // namespace lsrm
+
+using namespace lsrm;
+
+extern "C" {
+
+int lsrm_compress_block(int src_bf16, const void* x, int64_t ld_x, int64_t n, int width,
+                        const float* w1, const float* b1, const float* w2,
+                        const float* b2, const int64_t* block_token_ids,
+                        const int64_t* block_offsets, int64_t n_blocks, float* out,
+                        float* scratch, void* stream) {
+  LSRM_REQUIRE(width >= 1 && width <= 128, "compress: width %d outside [1,128]", width);
+  if (n == 0 || n_blocks == 0) return LSRM_OK;
+  cudaStream_t st = as_stream(stream);
+  size_t smem = 2 * kTokTile * width * sizeof(double) + 2 * width * width * sizeof(float);
+  if (smem > 48 * 1024)
+    LSRM_CUDA(cudaFuncSetAttribute(res_block_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  res_block_kernel<<<(unsigned)ceil_div(n, kTokTile), 256, smem, st>>>(
+      src_bf16, x, ld_x, n, width, w1, b1, w2, b2, scratch);
+  LSRM_LAUNCHED();
+  int blocks = (int)std::min<int64_t>(ceil_div(n_blocks * width, 128), 148 * 8);
+  block_mean_kernel<<<blocks, 128, 0, st>>>(scratch, width, block_token_ids, block_offsets,
+                                            n_blocks, out);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+}  // extern "C"

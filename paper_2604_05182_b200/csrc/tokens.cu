@@ -1,0 +1,334 @@
+// K9/K10 foreground pruning + informative-voxel mask and the fine-token
+// compaction (lsrm/tokenizer.py:180-313).  Bit-exact: masks are exact f64
+// compares on correctly rounded SDF values; compaction keeps flat (argwhere)
+// order via a two-level scan; features reproduce the reference's two f64
+// roundings f32(f64(parent) + f64(f32(sum of pos-embed rows in f64))).
+#include "common.cuh"
+
+namespace lsrm {
+
+constexpr int kScanChunk = 4096;   // cells per CTA in the compaction scan
+
+__global__ void fg_mask_kernel(const float* __restrict__ alpha, int n_views, int h,
+                               int w, int patch, uint8_t* __restrict__ mask) {
+  int ph = h / patch, pw = w / patch;
+  int64_t total = (int64_t)n_views * ph * pw;
+  int lane = threadIdx.x & 31;
+  for (int64_t cell = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+       cell < total; cell += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    int64_t view = cell / (ph * pw);
+    int r = (int)((cell / pw) % ph), c = (int)(cell % pw);
+    const float* base = alpha + (view * h + (int64_t)r * patch) * w + (int64_t)c * patch;
+    bool any = false;
+    for (int e = lane; e < patch * patch; e += 32)
+      any |= base[(e / patch) * (int64_t)w + (e % patch)] > 0.5f;
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) mask[cell] = any ? 1 : 0;
+  }
+}
+
+// Float4 fast path: patch == 8, one thread per (patch row) reads 2 float4.
+__global__ void fg_mask8_kernel(const float4* __restrict__ alpha, int n_views, int h,
+                                int w, uint8_t* __restrict__ mask) {
+  int ph = h / 8, pw = w / 8;
+  int64_t total = (int64_t)n_views * ph * pw;
+  // 8 threads per patch (one per pixel row), 4 patches per warp
+  int sub = threadIdx.x & 7, lane = threadIdx.x & 31;
+  int64_t warp_g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp_g * 4; base < total; base += n_warps * 4) {  // warp-uniform
+    int64_t cell = base + (lane >> 3);
+    bool hit = false;
+    if (cell < total) {
+      int64_t view = cell / (ph * pw);
+      int r = (int)((cell / pw) % ph), c = (int)(cell % pw);
+      int64_t row = view * h + (int64_t)r * 8 + sub;
+      const float4* p = alpha + (row * w + (int64_t)c * 8) / 4;
+      float4 a = p[0], b = p[1];
+      hit = a.x > 0.5f || a.y > 0.5f || a.z > 0.5f || a.w > 0.5f || b.x > 0.5f ||
+            b.y > 0.5f || b.z > 0.5f || b.w > 0.5f;
+    }
+    unsigned ball = __ballot_sync(0xffffffffu, hit);
+    if (cell < total && sub == 0) mask[cell] = ((ball >> (lane & 24)) & 0xffu) ? 1 : 0;
+  }
+}
+
+__device__ __forceinline__ double sdf_union(const double* __restrict__ prims, int n,
+                                            double x, double y, double z) {
+  double s = 0.0;
+  for (int p = 0; p < n; ++p) {
+    const double* P = prims + 8 * p;
+    double v;
+    if (P[0] == 0.0) {  // sphere: |p - c| - r
+      v = dsub(__dsqrt_rn(dist2(x, y, z, P[1], P[2], P[3])), P[4]);
+    } else {            // box: |max(q,0)| + min(max(q), 0), q = |p - c| - h
+      double qx = dsub(fabs(dsub(x, P[1])), P[4]);
+      double qy = dsub(fabs(dsub(y, P[2])), P[5]);
+      double qz = dsub(fabs(dsub(z, P[3])), P[6]);
+      double ox = fmax(qx, 0.0), oy = fmax(qy, 0.0), oz = fmax(qz, 0.0);
+      double out = __dsqrt_rn(dadd(dadd(dmul(ox, ox), dmul(oy, oy)), dmul(oz, oz)));
+      double in = fmin(fmax(fmax(qx, qy), qz), 0.0);
+      v = dadd(out, in);
+    }
+    s = p == 0 ? v : fmin(s, v);
+  }
+  return s;
+}
+
+__global__ void voxel_mask_kernel(const double* __restrict__ prims, int n_prims, int s_vol,
+                                  double tau, int t, uint8_t* __restrict__ mask) {
+  extern __shared__ double sh_prims[];
+  for (int i = threadIdx.x; i < 8 * n_prims; i += blockDim.x) sh_prims[i] = prims[i];
+  __syncthreads();
+  int64_t total = (int64_t)s_vol * s_vol * s_vol;
+  double fine = (double)t * s_vol;
+  for (int64_t vox = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vox < total;
+       vox += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(vox / ((int64_t)s_vol * s_vol)), j = (int)((vox / s_vol) % s_vol),
+        k = (int)(vox % s_vol);
+    double smin = __builtin_huge_val(), smax = -__builtin_huge_val(),
+           amin = __builtin_huge_val();
+    for (int a = 0; a < t; ++a) {
+      double x = ddiv(dadd((double)(t * i + a), 0.5), fine);
+      for (int b = 0; b < t; ++b) {
+        double y = ddiv(dadd((double)(t * j + b), 0.5), fine);
+        for (int c = 0; c < t; ++c) {
+          double z = ddiv(dadd((double)(t * k + c), 0.5), fine);
+          double s = sdf_union(sh_prims, n_prims, x, y, z);
+          smin = fmin(smin, s);
+          smax = fmax(smax, s);
+          amin = fmin(amin, fabs(s));
+        }
+      }
+    }
+    mask[vox] = (amin <= tau) || (dmul(smin, smax) <= 0.0);
+  }
+}
+
+__device__ int block_incl_scan(int v, int* warp_sums) {
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) warp_sums[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    warp_sums[lane] = w;
+  }
+  __syncthreads();
+  int r = v + (warp ? warp_sums[warp - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
+// Pass 1: count set flags per chunk.
+__global__ void __launch_bounds__(1024)
+chunk_count_kernel(const uint8_t* __restrict__ flags, int64_t n, int* __restrict__ counts) {
+  __shared__ int warp_sums[32];
+  int64_t base = (int64_t)blockIdx.x * kScanChunk;
+  int c = 0;
+  for (int e = threadIdx.x; e < kScanChunk; e += blockDim.x)
+    c += (base + e < n && flags[base + e]) ? 1 : 0;
+  int tot = block_incl_scan(c, warp_sums);
+  if (threadIdx.x == blockDim.x - 1) counts[blockIdx.x] = tot;
+}
+
+// Pass 2: exclusive scan of chunk counts (single CTA) + total.
+__global__ void __launch_bounds__(1024)
+chunk_scan_kernel(int* __restrict__ counts, int64_t n_chunks, int64_t* __restrict__ total) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b = 0; b < n_chunks; b += blockDim.x) {
+    int64_t i = b + threadIdx.x;
+    int v = i < n_chunks ? counts[i] : 0;
+    int incl = block_incl_scan(v, warp_sums);
+    if (i < n_chunks) counts[i] = carry + incl - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry += incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+// Pass 3: write the flat cell index of every set flag at its output position.
+__global__ void __launch_bounds__(1024)
+chunk_emit_kernel(const uint8_t* __restrict__ flags, int64_t n,
+                  const int* __restrict__ starts, int32_t* __restrict__ out_cells) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = starts[blockIdx.x];
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * kScanChunk;
+  for (int e0 = 0; e0 < kScanChunk; e0 += blockDim.x) {
+    int64_t cell = base + e0 + threadIdx.x;
+    int f = (cell < n && flags[cell]) ? 1 : 0;
+    int incl = block_incl_scan(f, warp_sums);
+    if (f) out_cells[carry + incl - 1] = (int32_t)cell;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry += incl;
+    __syncthreads();
+  }
+}
+
+// One warp per output token: coords + f32(f64(parent) + f64(pe)).
+__global__ void compact_volume_rows(const int32_t* __restrict__ cells, int64_t n_out,
+                                    int s, int f, const float* __restrict__ x_d, int d,
+                                    const float* __restrict__ pe0, const float* __restrict__ pe1,
+                                    const float* __restrict__ pe2, int64_t* __restrict__ coords,
+                                    float* __restrict__ feats) {
+  int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (row >= n_out) return;
+  int64_t cell = cells[row];
+  int i = (int)(cell / ((int64_t)s * s)), j = (int)((cell / s) % s), k = (int)(cell % s);
+  if (lane == 0 && coords) {
+    coords[3 * row] = i;
+    coords[3 * row + 1] = j;
+    coords[3 * row + 2] = k;
+  }
+  if (!feats) return;
+  int sc = s / f;
+  int64_t parent = ((int64_t)(i / f) * sc + j / f) * sc + k / f;
+  for (int c = lane; c < d; c += 32) {
+    double pe = dadd(dadd(dadd(0.0, (double)pe0[(int64_t)i * d + c]), (double)pe1[(int64_t)j * d + c]),
+                     (double)pe2[(int64_t)k * d + c]);
+    float pe32 = (float)pe;
+    feats[row * d + c] = (float)dadd((double)x_d[parent * d + c], (double)pe32);
+  }
+}
+
+__global__ void compact_image_rows(const int32_t* __restrict__ cells, int64_t n_out,
+                                   int s, int f, const float* __restrict__ y_d, int d,
+                                   const float* __restrict__ pe_u, const float* __restrict__ pe_v,
+                                   int64_t* __restrict__ coords, float* __restrict__ feats) {
+  int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (row >= n_out) return;
+  int64_t cell = cells[row];
+  int64_t view = cell / ((int64_t)s * s);
+  int r = (int)((cell / s) % s), col = (int)(cell % s);
+  if (lane == 0 && coords) {
+    coords[3 * row] = view;
+    coords[3 * row + 1] = col;   // u
+    coords[3 * row + 2] = r;     // v
+  }
+  if (!feats) return;
+  int sc = s / f;
+  int64_t parent = (view * sc + r / f) * sc + col / f;
+  for (int c = lane; c < d; c += 32) {
+    double pe = dadd(dadd(0.0, (double)pe_u[(int64_t)col * d + c]), (double)pe_v[(int64_t)r * d + c]);
+    float pe32 = (float)pe;
+    feats[row * d + c] = (float)dadd((double)y_d[parent * d + c], (double)pe32);
+  }
+}
+
+static int compact_cells(const uint8_t* mask, int64_t n_cells, void* workspace,
+                         size_t ws_bytes, int32_t** cells_out, int64_t* n_out,
+                         cudaStream_t st) {
+  int64_t n_chunks = ceil_div(n_cells, kScanChunk);
+  LSRM_REQUIRE(ws_bytes >= lsrm_compact_workspace(n_cells), "compact: workspace too small");
+  char* ws = (char*)workspace;
+  int64_t* total = (int64_t*)ws;
+  int* counts = (int*)(ws + 16);
+  int32_t* cells = (int32_t*)(ws + 16 + ((n_chunks * sizeof(int) + 15) / 16) * 16);
+  chunk_count_kernel<<<(unsigned)n_chunks, 1024, 0, st>>>(mask, n_cells, counts);
+  LSRM_LAUNCHED();
+  chunk_scan_kernel<<<1, 1024, 0, st>>>(counts, n_chunks, total);
+  LSRM_LAUNCHED();
+  chunk_emit_kernel<<<(unsigned)n_chunks, 1024, 0, st>>>(mask, n_cells, counts, cells);
+  LSRM_LAUNCHED();
+  LSRM_CUDA(cudaMemcpyAsync(n_out, total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  LSRM_CUDA(cudaStreamSynchronize(st));
+  *cells_out = cells;
+  return LSRM_OK;
+}
+
+}  // namespace lsrm
+
+using namespace lsrm;
+
+extern "C" {
+
+int lsrm_foreground_mask(const float* alpha, int n_views, int h, int w, int patch,
+                         uint8_t* mask, void* stream) {
+  LSRM_REQUIRE(patch >= 1 && h % patch == 0 && w % patch == 0,
+               "alpha %dx%d not divisible by patch %d", h, w, patch);
+  int64_t total = (int64_t)n_views * (h / patch) * (w / patch);
+  if (total == 0) return LSRM_OK;
+  if (patch == 8 && ((uintptr_t)alpha % 16) == 0) {
+    int blocks = (int)std::min<int64_t>(ceil_div(total * 8, 256), 148 * 16);
+    fg_mask8_kernel<<<blocks, 256, 0, as_stream(stream)>>>((const float4*)alpha, n_views, h, w,
+                                                           mask);
+  } else {
+    int blocks = (int)std::min<int64_t>(ceil_div(total, 8), 148 * 16);
+    fg_mask_kernel<<<blocks, 256, 0, as_stream(stream)>>>(alpha, n_views, h, w, patch, mask);
+  }
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_voxel_mask(const double* sdf, int n_prims, int s_vol, double tau, int t_side,
+                    uint8_t* mask, void* stream) {
+  LSRM_REQUIRE(s_vol >= 1 && t_side >= 1, "bad mask resolution");
+  LSRM_REQUIRE(tau > 0, "tau must be positive");
+  LSRM_REQUIRE(n_prims >= 1 && n_prims <= 256, "voxel_mask: 1..256 SDF primitives");
+  int64_t total = (int64_t)s_vol * s_vol * s_vol;
+  int blocks = (int)std::min<int64_t>(ceil_div(total, 128), 148 * 32);
+  voxel_mask_kernel<<<blocks, 128, 8 * n_prims * sizeof(double), as_stream(stream)>>>(
+      sdf, n_prims, s_vol, tau, t_side, mask);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+size_t lsrm_compact_workspace(int64_t n_cells) {
+  int64_t n_chunks = ceil_div(n_cells, kScanChunk);
+  return 16 + ((n_chunks * sizeof(int) + 15) / 16) * 16 + n_cells * sizeof(int32_t) + 16;
+}
+
+int lsrm_compact_volume(const uint8_t* mask, int s_fine, int factor, const float* x_d,
+                        int d, const float* pe0, const float* pe1, const float* pe2,
+                        int64_t* coords, float* features, int64_t max_out,
+                        int64_t* n_out, void* workspace, size_t ws_bytes, void* stream) {
+  LSRM_REQUIRE(factor >= 1 && s_fine % factor == 0, "volume mask not divisible by factor");
+  cudaStream_t st = as_stream(stream);
+  int32_t* cells = nullptr;
+  int rc = compact_cells(mask, (int64_t)s_fine * s_fine * s_fine, workspace, ws_bytes,
+                         &cells, n_out, st);
+  if (rc) return rc;
+  if ((!coords && !features) || *n_out == 0) return LSRM_OK;
+  LSRM_REQUIRE(*n_out <= max_out, "compact_volume: %lld tokens exceed max_out %lld",
+               (long long)*n_out, (long long)max_out);
+  compact_volume_rows<<<(unsigned)ceil_div(*n_out, 8), 256, 0, st>>>(
+      cells, *n_out, s_fine, factor, x_d, d, pe0, pe1, pe2, coords, features);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_compact_image(const uint8_t* mask, int n_views, int s_fine, int factor,
+                       const float* y_d, int d, const float* pe_u, const float* pe_v,
+                       int64_t* coords, float* features, int64_t max_out, int64_t* n_out,
+                       void* workspace, size_t ws_bytes, void* stream) {
+  LSRM_REQUIRE(factor >= 1 && s_fine % factor == 0, "image mask not divisible by factor");
+  cudaStream_t st = as_stream(stream);
+  int32_t* cells = nullptr;
+  int rc = compact_cells(mask, (int64_t)n_views * s_fine * s_fine, workspace, ws_bytes,
+                         &cells, n_out, st);
+  if (rc) return rc;
+  if ((!coords && !features) || *n_out == 0) return LSRM_OK;
+  LSRM_REQUIRE(*n_out <= max_out, "compact_image: %lld tokens exceed max_out %lld",
+               (long long)*n_out, (long long)max_out);
+  compact_image_rows<<<(unsigned)ceil_div(*n_out, 8), 256, 0, st>>>(
+      cells, *n_out, s_fine, factor, y_d, d, pe_u, pe_v, coords, features);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+}  // extern "C"
