@@ -113,8 +113,12 @@ def route_image_rows(points, cameras, part: BlockPartition, token_points, b_i: i
     vrs = np.searchsorted(part.block_views, np.arange(n_views + 1)).astype(np.int64)
     tp = token_points.points if isinstance(token_points, TokenCoords3D) else token_points
     tp_bm = _ops.gather_rows(D.dev(tp, torch.float64), part.dev("block_token_ids"))
-    call("lsrm_route_image", pts.data_ptr(), nq, D.dev(cams).data_ptr(), n_views,
-         D.dev(vrs).data_ptr(), part.dev("block_centers").data_ptr(), part.n_occupied,
+    # keep the staging tensors referenced until the launch is enqueued: a
+    # temporary's block returns to torch's caching allocator immediately and
+    # the next H2D copy could overwrite it before the kernel reads it
+    cams_d, vrs_d = D.dev(cams), D.dev(vrs)
+    call("lsrm_route_image", pts.data_ptr(), nq, cams_d.data_ptr(), n_views,
+         vrs_d.data_ptr(), part.dev("block_centers").data_ptr(), part.n_occupied,
          tp_bm.data_ptr(), part.dev("block_offsets").data_ptr(), b_i, budget,
          rows.data_ptr(), count.data_ptr(), D.stream())
     return rows, count

@@ -1,0 +1,177 @@
+"""Public layer-level API: one LSRM sparse-attention layer (the four gated NSA
+uses of a Stage-2 block, `lsrm/recon_pipeline.py:477-488`) on the GPU.
+
+    inst  = build_instance("c3")                 # fixture geometry -> tokens, routing
+    layer = SparseAttentionLayer(inst)
+    outs  = layer.forward_host(x_hat, y_hat)     # NumPy in -> NumPy out (f32)
+
+`forward_host` is the end-to-end path a reference user calls (host buffers,
+H2D + permute/cast + fused layer + un-permute/cast + D2H).  The device path
+(`engine.forward` on block-major bf16 tensors) is what `bench.py` times as
+`value`; `time_host_path` is its `e2e`.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev as D
+from . import _ops
+from .block_partition import BlockPartition, partition
+from .block_routing import RoutingBudgets, build_routing_plan, volume_token_coords
+from .engine import USES, USE_GEOM, SparseLayerEngine
+from .tensor_core import AttentionParams
+from .tokenizer import upsample_select_tokens
+from .workloads import coarse_inputs, load_workload, nsa_use_weights, params_of
+
+
+@dataclass
+class Instance:
+    name: str
+    params: AttentionParams
+    part_vol: BlockPartition
+    part_img: BlockPartition
+    plan_rows: dict
+    weights: dict
+    x_hat: np.ndarray     # [Nv, d] f32 LayerNorm'd volume tokens (token order)
+    y_hat: np.ndarray     # [Ni, d] f32
+    n_vol: int
+    n_img: int
+
+
+def build_instance(name: str = "c3", seed: int = 0) -> Instance:
+    """GPU instance setup: compaction -> partition -> 3D routing (all on the
+    device, bit-exact with the reference), LN'd fine tokens as layer input."""
+    wl = load_workload(name)
+    params = params_of(name)
+    d = params.model_dim
+    x_d, y_d, pe_v, pe_i = coarse_inputs(wl, d, seed)
+    x_up, y_up = upsample_select_tokens(D.dev(x_d), D.dev(y_d), wl.vol_mask, wl.img_mask,
+                                        pe_v, pe_i, wl.factor_vol, wl.factor_img)
+    pv, pi = partition(x_up), partition(y_up)
+    plan = build_routing_plan(volume_token_coords(x_up), wl.img_points, pv, pi, wl.cameras,
+                              RoutingBudgets(), host_lists=False)
+    ones = D.dev(np.ones(d, np.float32))
+    zeros = D.dev(np.zeros(d, np.float32))
+    xh = _ops.layer_norm(x_up.features, ones, zeros)
+    yh = _ops.layer_norm(y_up.features, ones, zeros)
+    return Instance(name, params, pv, pi, plan.device_rows, nsa_use_weights(params, seed),
+                    D.host(xh), D.host(yh), x_up.count, y_up.count)
+
+
+class SparseAttentionLayer:
+    def __init__(self, inst: Instance):
+        self.inst = inst
+        self.engine = SparseLayerEngine(inst.part_vol, inst.part_img, inst.plan_rows,
+                                        inst.weights, inst.params)
+        self.tok = {"x": inst.part_vol.dev("block_token_ids"),
+                    "y": inst.part_img.dev("block_token_ids")}
+        d = inst.params.model_dim
+        self._stage = {"x": D.empty((inst.n_vol, d), torch.float32),
+                       "y": D.empty((inst.n_img, d), torch.float32)}
+        self._out32 = {u: D.empty((self.engine.meta[USE_GEOM[u][0]].n, d), torch.float32)
+                       for u in USES}
+        self._bm = {"x": D.empty((inst.n_vol, d), torch.bfloat16),
+                    "y": D.empty((inst.n_img, d), torch.bfloat16)}
+
+    def device_inputs(self, x_hat, y_hat):
+        """token-order f32 -> block-major bf16 (gather + cast kernels)."""
+        out = []
+        for s, a in (("x", x_hat), ("y", y_hat)):
+            t = D.dev(a, torch.float32)
+            g = _ops.gather_rows(t, self.tok[s])
+            out.append(_ops.cast(g, torch.bfloat16))
+        return out
+
+    def _forward_from_stage(self):
+        for s in ("x", "y"):
+            bm32 = _ops.gather_rows(self._stage[s], self.tok[s])
+            from ._native import call
+            call("lsrm_cast", 1, bm32.data_ptr(), self._bm[s].data_ptr(), bm32.numel(),
+                 D.stream())
+        outs = self.engine.forward(self._bm["x"], self._bm["y"])
+        res = {}
+        from ._native import call
+        for u in USES:
+            qs = USE_GEOM[u][0]
+            o32 = _ops.cast(outs[u], torch.float32)
+            _ops.scatter_rows(o32, self.tok[qs], self._out32[u])
+            res[u] = self._out32[u]
+        return res
+
+    def forward_host(self, x_hat: np.ndarray, y_hat: np.ndarray, pinned_out=None) -> dict:
+        """NumPy in -> dict use -> NumPy [Nq, d] f32 (token order)."""
+        self._stage["x"].copy_(torch.from_numpy(np.ascontiguousarray(x_hat, np.float32)),
+                               non_blocking=True)
+        self._stage["y"].copy_(torch.from_numpy(np.ascontiguousarray(y_hat, np.float32)),
+                               non_blocking=True)
+        res = self._forward_from_stage()
+        outs = {}
+        for u in USES:
+            dst = pinned_out[u] if pinned_out is not None else torch.empty(
+                tuple(res[u].shape), dtype=torch.float32, pin_memory=True)
+            dst.copy_(res[u], non_blocking=True)
+            outs[u] = dst
+        torch.cuda.current_stream().synchronize()
+        return {u: outs[u].numpy() for u in USES}
+
+    def time_host_path(self, x_hat, y_hat, steps=5):
+        """Mean ms of forward_host with pinned host buffers; H2D/D2H bytes."""
+        xp = torch.from_numpy(np.ascontiguousarray(x_hat, np.float32)).pin_memory()
+        yp = torch.from_numpy(np.ascontiguousarray(y_hat, np.float32)).pin_memory()
+        pinned = {u: torch.empty(tuple(self._out32[u].shape), dtype=torch.float32,
+                                 pin_memory=True) for u in USES}
+        st = torch.cuda.current_stream()
+
+        def once():
+            self._stage["x"].copy_(xp, non_blocking=True)
+            self._stage["y"].copy_(yp, non_blocking=True)
+            res = self._forward_from_stage()
+            for u in USES:
+                pinned[u].copy_(res[u], non_blocking=True)
+
+        once()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(steps):
+            once()
+        b.record(st)
+        torch.cuda.synchronize()
+        h2d = xp.numel() * 4 + yp.numel() * 4
+        d2h = sum(p.numel() * 4 for p in pinned.values())
+        return a.elapsed_time(b) / steps, h2d, d2h
+
+    def profile_breakdown(self, x_bm, y_bm, reps=5):
+        """Device time per kernel class (events on the launching stream)."""
+        e = self.engine
+        st = torch.cuda.current_stream()
+        names = ["project_gemm", "kv_prep", "attention", "wo_gemm"]
+        acc = {n: 0.0 for n in names}
+        per_use = {u: 0.0 for u in USES}
+        for _ in range(reps):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record(st)
+            e.project(x_bm, y_bm)
+            ev[1].record(st)
+            torch.cuda.synchronize()
+            acc["project_gemm"] += ev[0].elapsed_time(ev[1])
+            for u in USES:
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                ev[0].record(st)
+                e.prepare_kv(u)
+                ev[1].record(st)
+                e.attend(u)
+                ev[2].record(st)
+                e.output(u)
+                ev[3].record(st)
+                torch.cuda.synchronize()
+                acc["kv_prep"] += ev[0].elapsed_time(ev[1])
+                a = ev[1].elapsed_time(ev[2])
+                acc["attention"] += a
+                per_use[u] += a
+                acc["wo_gemm"] += ev[2].elapsed_time(ev[3])
+        out = {f"{n}_ms": v / reps for n, v in acc.items()}
+        out["attention_per_use_ms"] = {u: v / reps for u, v in per_use.items()}
+        return out

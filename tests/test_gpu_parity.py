@@ -264,11 +264,12 @@ def test_tc_fused_attention_vs_oracle(c1):
         rb, cb = block_major_rows(rows, cnt, pq, pk, self_use)
         tiles = D.dev(query_tiles(pq, 16, self_use))
         merged = D.empty((nq, 1024), torch.bfloat16)
+        gb_d = D.dev(gb)
         call("lsrm_nsa_attention_tc", q_bm.data_ptr(), 1024, nq, 32, 2, 32, kil.data_ptr(),
              vil.data_ptr(), mk.pad_off.data_ptr(), mk.kv_off.data_ptr(), mk.n_rows_pad,
              kcil.data_ptr(), vcil.data_ptr(), B, tiles.data_ptr(), int(tiles.shape[0]),
              rb.data_ptr(), cb.data_ptr(), int(rb.shape[1]), gl_bm.data_ptr(), ng * 1024, 0,
-             D.dev(gb).data_ptr(), ng, merged.data_ptr(), st)
+             gb_d.data_ptr(), ng, merged.data_ptr(), st)
         out = torch.empty_like(merged)
         _ops.scatter_rows(merged, tokq, out)
         got = out.float().cpu().numpy().astype(np.float64)
