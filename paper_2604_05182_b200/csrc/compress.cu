@@ -53,19 +53,29 @@ __global__ void res_block_kernel(int src_bf16, const void* __restrict__ x, int64
   }
 }
 
+// CTA per block; thread (column c, slice s) sums the block's tokens
+// s, s+S, s+2S, ... in ascending order in f64, then slice partials are
+// combined in fixed slice order: deterministic, coalesced, and no single
+// serial chain of dependent loads over a 512-token block.
 __global__ void block_mean_kernel(const float* __restrict__ r, int w,
                                   const int64_t* __restrict__ tok,
                                   const int64_t* __restrict__ offs, int64_t nb,
                                   float* __restrict__ out) {
-  int64_t total = nb * w;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t b = e / w;
-    int c = (int)(e % w);
-    int64_t lo = offs[b], hi = offs[b + 1];
-    double s = 0.0;
-    for (int64_t j = lo; j < hi; ++j) s += (double)r[tok[j] * w + c];
-    out[e] = (float)(s / (double)(hi - lo));
+  extern __shared__ double part[];
+  const int64_t b = blockIdx.x;
+  const int S = blockDim.x / w;
+  const int c = threadIdx.x % w, s = threadIdx.x / w;
+  const int64_t lo = offs[b], hi = offs[b + 1];
+  if (s < S) {
+    double acc = 0.0;
+    for (int64_t j = lo + s; j < hi; j += S) acc += (double)r[tok[j] * w + c];
+    part[s * w + c] = acc;
+  }
+  __syncthreads();
+  if (s == 0) {
+    double tot = 0.0;
+    for (int k = 0; k < S; ++k) tot += part[k * w + c];
+    out[b * w + c] = (float)(tot / (double)(hi - lo));
   }
 }
 
@@ -90,9 +100,9 @@ int lsrm_compress_block(int src_bf16, const void* x, int64_t ld_x, int64_t n, in
   res_block_kernel<<<(unsigned)ceil_div(n, kTokTile), 256, smem, st>>>(
       src_bf16, x, ld_x, n, width, w1, b1, w2, b2, scratch);
   LSRM_LAUNCHED();
-  int blocks = (int)std::min<int64_t>(ceil_div(n_blocks * width, 128), 148 * 8);
-  block_mean_kernel<<<blocks, 128, 0, st>>>(scratch, width, block_token_ids, block_offsets,
-                                            n_blocks, out);
+  int threads = width >= 256 ? width : (256 / width) * width;
+  block_mean_kernel<<<(unsigned)n_blocks, threads, threads * sizeof(double), st>>>(
+      scratch, width, block_token_ids, block_offsets, n_blocks, out);
   LSRM_LAUNCHED();
   return LSRM_OK;
 }

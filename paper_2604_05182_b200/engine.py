@@ -102,7 +102,7 @@ class SparseLayerEngine:
 
     def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
                  weights: dict, params: AttentionParams):
-        require(params.head_dim in (16, 32, 64), "bf16 engine: head_dim must be 16, 32 or 64")
+        require(params.head_dim in (32, 64), "bf16 engine: head_dim must be 32 or 64")
         G = params.group_size
         require(128 % G == 0, "bf16 engine: (n_q_heads/n_kv_heads) must divide 128")
         self.params = params
