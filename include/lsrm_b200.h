@@ -62,7 +62,9 @@ int lsrm_partition(int modality, const int64_t* coords, int64_t n, int g0,
                    void* stream);
 
 /* ---- K6 per-block KV compression  (block_partition.py:141-167) ---------
- * x: [N, width] (f32, or bf16 when src_bf16) in token order, row stride ld_x;
+ * x: [N, width] in token order, row stride ld_x.  src_bf16 flags: bit 0 =
+ * bf16 source (else f32); bit 1 = fp32 ResBlock arithmetic (bf16 engine).
+ * Default (bit 1 clear):
  * ResBlock x + W2 gelu(W1 x + b1) + b2 in f64 with the reference's f32
  * roundings, then the in-block mean in ascending token order with an f64
  * running sum.  out: [B, width] f32; scratch: [N, width] f32. */
@@ -200,9 +202,11 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
 
 /* Re-layout K or V ([n, hkv, dh] f32 or bf16, token order) into the padded,
  * 8x8-core-matrix interleaved bf16 layout the tcgen05 kernel consumes:
- * per kv head, per block, rows padded to a multiple of 16. */
+ * per kv head, per block, rows padded to a multiple of 16.  ones_cols = 16
+ * appends 16 columns holding 1 (real key) / 0 (padding): the V operand then
+ * yields the softmax row sums in the same P.V MMA. */
 int lsrm_kv_interleave(int src_is_bf16, const void* src, int64_t ld_src,
-                       int64_t n, int hkv, int dh,
+                       int64_t n, int hkv, int dh, int ones_cols,
                        const int64_t* block_token_ids,
                        const int64_t* block_offsets, int64_t n_blocks,
                        const int64_t* pad_offsets, int64_t n_rows_pad,
@@ -211,6 +215,18 @@ int lsrm_kv_interleave(int src_is_bf16, const void* src, int64_t ld_src,
 /* Debug: device buffer of 1024 x 8 int64 that CTA 0 of the fused attention
  * kernel fills with clock64() stamps per chunk/event (NULL disables). */
 int lsrm_debug_set_trace(void* buf);
+
+/* Fused K/V preparation for the bf16 engine: token rows [n, hkv*dh] bf16 in
+ * block-major order (row stride ld) -> padded interleaved layout (pad_row[i] =
+ * padded row of token i; ones_cols 16 for V) + fp32 ResBlock rows r_out
+ * [n, hkv*dh] + (if mean_out) the per-block means [n_blocks, hkv*dh] over the
+ * contiguous block ranges block_offsets (block_partition.py:141-167). */
+int lsrm_kv_prepare(const void* src, int64_t ld, int64_t n, int hkv, int dh,
+                    const int32_t* pad_row, int64_t n_rows_pad, void* il,
+                    int ones_cols, const float* w1, const float* b1,
+                    const float* w2, const float* b2, float* r_out,
+                    const int64_t* block_offsets, int64_t n_blocks,
+                    float* mean_out, void* stream);
 
 /* Row permutation helpers (block-major <-> token order). */
 int lsrm_gather_rows(int elem_bytes, const void* src, int64_t ld_src,

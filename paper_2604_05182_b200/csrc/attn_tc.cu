@@ -112,6 +112,34 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// D[tmem] (+)= A[tmem] . B[smem]: A (P) read from TMEM, 16 bf16 per lane in 8
+// packed 32-bit columns per K=16 step.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                            uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t elect_one_sync() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 %%rx;\n\t.reg .pred %%px;\n\t"
+      "elect.sync %%rx|%%px, %1;\n\t@%%px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred;
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -161,9 +189,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // Optional event trace (debug): CTA 0 stamps clock64() per chunk and event.
 __device__ long long* g_trace = nullptr;
 constexpr int kTraceEv = 8, kTraceChunks = 1024;
-__device__ __forceinline__ void trace(uint32_t c, int ev) {
-  long long* tr = g_trace;
-  if (tr && blockIdx.x == 0 && c < (uint32_t)kTraceChunks) tr[c * kTraceEv + ev] = clock64();
+__device__ __forceinline__ void trace(long long* tr, uint32_t c, int ev) {
+  if (tr && c < (uint32_t)kTraceChunks) tr[c * kTraceEv + ev] = clock64();
 }
 
 struct Params {
@@ -192,7 +219,7 @@ struct Params {
 };
 
 constexpr int kStages = 6;       // K/V ring depth
-constexpr int kOnesCols = 16;    // N of the row-sum MMA (P . ones)
+constexpr int kOnesCols = 16;    // extra V columns holding 1 (valid key) / 0 (padding)
 constexpr int kBitmapWords = 512;  // union bitmap: up to 16384 occupied KV blocks
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
@@ -219,9 +246,7 @@ template <int DH>
 struct Smem {
   __nv_bfloat16 q[2][kM * DH];
   __nv_bfloat16 k[kStages][kNK * DH];
-  __nv_bfloat16 v[kStages][kNK * DH];
-  __nv_bfloat16 p[2][kM * kNK];
-  __nv_bfloat16 ones[kNK * kOnesCols];
+  __nv_bfloat16 v[kStages][kNK * (DH + kOnesCols)];   // [V | ones] rows
   float merged[kM][DH + 1];
   float xmax[2][kParts][kM];    // per-part partial row maxima (chunk parity)
   int32_t ent[kMaxEnt];         // selected rows of the tile tokens, [t][kmax]
@@ -249,7 +274,11 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
   const int64_t n_items = P.n_tiles * P.hkv;
   if ((int64_t)blockIdx.x >= n_items) return;
   // TMEM columns: S slots [0,128) [128,256); O/L double-buffered per chunk parity
-  constexpr uint32_t kColO = 2 * kNK, kColL = 2 * kNK + 2 * DH, kOL = kOnesCols;
+  // P(c) (bf16x2 packed, 64 columns) aliases the upper half of S slot c&1:
+  // every part has loaded its S values before the max-exchange barrier, and
+  // QK(c+2) is issued after PV(c) in the in-order tensor pipe.
+  constexpr int VW = DH + kOnesCols;   // V row width incl. the ones columns
+  constexpr uint32_t kColO = 2 * kNK, kColP = kNK / 2;   // O|L slots: kColO + parity * VW
 
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -274,7 +303,6 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
   }
   if (warp < 4)
     for (int c = 0; c < DH; ++c) S.merged[tid][c] = 0.f;  // warps 0-3 cover all rows
-  for (int i = tid; i < kNK * kOnesCols; i += kThreads) S.ones[i] = __float2bfloat16_rn(1.f);
   for (int i = tid; i < kBitmapWords; i += kThreads) S.bitmap[i] = 0u;
   fence_async_smem();
   tc_before_sync();
@@ -282,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
   tc_after_sync();
   const uint32_t tmem = S.tmem_base;
   const uint32_t row_bytes_kv = DH * 2;
+  long long* const trp = blockIdx.x == 0 ? g_trace : nullptr;  // debug event trace
 
   if (warp == kProducerWarp) {
     // ===================== producer: Q tiles, unions, chunk plans, K/V copies
@@ -417,13 +446,13 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
         const int64_t total = br == 0 ? cmp_rows : (br == 1 ? total_sel : S.seg_plen[kMaxEnt]);
         const int64_t head_rows = br == 0 ? cmp_rows : P.n_rows_pad;
         const __nv_bfloat16* kb = (br == 0 ? P.kc_il : P.k_il) + (int64_t)h * head_rows * DH;
-        const __nv_bfloat16* vb = (br == 0 ? P.vc_il : P.v_il) + (int64_t)h * head_rows * DH;
+        const __nv_bfloat16* vb = (br == 0 ? P.vc_il : P.v_il) + (int64_t)h * head_rows * VW;
         int cur = 0;
         for (int64_t start = 0; start < total; start += kNK) {
           const int64_t end = lmin(start + kNK, total);
           const int st = c % kStages;
           if (c >= kStages) mbar_wait(&S.kv_empty[st], ((c / kStages) - 1) & 1);
-          if (lane == 0) trace(c, 0);
+          if (lane == 0) trace(trp, c, 0);
           ChunkDesc& D = S.desc[st];
           const int s = cur + lane;
           bool ov = false, done = false;
@@ -473,11 +502,12 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
             D.item_seq = it;
           }
           __syncwarp();
-          if (lane == 0) mbar_expect_tx(&S.kv_full[st], 2u * (uint32_t)(end - start) * row_bytes_kv);
+          if (lane == 0)
+            mbar_expect_tx(&S.kv_full[st], (uint32_t)(end - start) * (row_bytes_kv + 2u * VW));
           __syncwarp();
           if (ov) {
             bulk_g2s(&S.k[st][col * DH], kb + src * DH, ncols * row_bytes_kv, &S.kv_full[st]);
-            bulk_g2s(&S.v[st][col * DH], vb + src * DH, ncols * row_bytes_kv, &S.kv_full[st]);
+            bulk_g2s(&S.v[st][col * VW], vb + src * VW, ncols * 2u * VW, &S.kv_full[st]);
           }
           cur += __popc(__ballot_sync(0xffffffffu, done));
           ++c;
@@ -486,31 +516,32 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
       __syncwarp();
     }
   } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer
-    if (lane == 0) {
-      const uint32_t id_pv = idesc_bf16(kM, DH, 1);
-      const uint32_t id_l = idesc_bf16(kM, kOnesCols, 1);
-      const uint64_t ones_d = sdesc(smem_u32(S.ones), 256, 128);
+    // ===================== MMA issuer (warp converged; one elected lane issues)
+    {
+      const uint32_t id_pv = idesc_bf16(kM, VW, 1);   // O | rowsum = P . [V | ones]
       // S = Q K^T for chunk cc into TMEM S slot cc&1
       auto issue_qk = [&](uint32_t cc) {
         const int st = cc % kStages;
         mbar_wait(&S.kv_full[st], (cc / kStages) & 1);
-        trace(cc, 1);
+        if (lane == 0) trace(trp, cc, 1);
         const ChunkDesc& D = S.desc[st];
         if (D.first_in_item) mbar_wait(&S.q_full[D.qb], (D.item_seq >> 1) & 1);
         tc_after_sync();
         const uint32_t id = idesc_bf16(kM, D.ncols, 0);
         const uint64_t a0 = sdesc(smem_u32(S.q[D.qb]), 128, 16 * DH);
         const uint64_t b0 = sdesc(smem_u32(S.k[st]), 128, 16 * DH);
+        if (elect_one_sync()) {
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(tmem + (cc & 1) * kNK, a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16), id,
-                   kk > 0);
-        mma_commit(&S.s_full[cc & 1]);
-        trace(cc, 2);
+          for (int kk = 0; kk < DH / 16; ++kk)
+            mma_bf16(tmem + (cc & 1) * kNK, a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16),
+                     id, kk > 0);
+          mma_commit(&S.s_full[cc & 1]);
+        }
+        __syncwarp();
+        if (lane == 0) trace(trp, cc, 2);
       };
-      // QK runs two chunks ahead: QK(c+2) reuses S slot c&1 as soon as the
-      // softmax of chunk c has released it, before PV(c) is issued
+      // QK runs two chunks ahead: QK(c+2) reuses S slot c&1 once the softmax
+      // of chunk c has released it; it is issued right after PV(c)
       uint32_t c = 0;
       issue_qk(0);
       bool ahead = !S.desc[0].last_overall;  // is there a chunk 1?
@@ -525,32 +556,29 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
         const bool last_in_item = D.last_in_item;
         const int qb = D.qb;
         mbar_wait(&S.p_full[c & 1], (c >> 1) & 1);
-        trace(c, 5);
-        // O_part = P V and the row sums L = P . ones for chunk c, into the
-        // O/L slot of parity c&1 (absorbed two chunks ago: no o_empty wait on
-        // the previous chunk)
+        if (lane == 0) trace(trp, c, 5);
+        // [O | rowsum](c) = P V' into the O slot of parity c&1 (absorbed two
+        // chunks ago: no wait on the previous chunk's absorb)
         if (c >= 2) mbar_wait(&S.o_empty[c & 1], ((c >> 1) - 1) & 1);
         tc_after_sync();
-        const uint64_t pa = sdesc(smem_u32(S.p[c & 1]), 128, 8 * kNK * 2);
-        const uint64_t vb = sdesc(smem_u32(S.v[st]), 16 * DH, 128);
-        const uint32_t to = tmem + kColO + (c & 1) * DH, tl = tmem + kColL + (c & 1) * kOL;
+        const uint32_t pa = tmem + (c & 1) * kNK + kColP;   // P(c): packed bf16 in TMEM
+        const uint64_t vb = sdesc(smem_u32(S.v[st]), 16 * VW, 128);
+        const uint32_t to = tmem + kColO + (c & 1) * VW;
+        if (elect_one_sync()) {
 #pragma unroll
-        for (int kk = 0; kk < kGroups; ++kk) {
-          if (kk < nk) {
-            const uint64_t a = pa + (uint64_t)(kk * 16);
-            mma_bf16(to, a, vb + (uint64_t)(kk * 2 * DH), id_pv, kk > 0);
-            mma_bf16(tl, a, ones_d + (uint64_t)(kk * 32), id_l, kk > 0);
-          }
+          for (int kk = 0; kk < kGroups; ++kk)
+            if (kk < nk) mma_bf16_ts(to, pa + kk * 8, vb + (uint64_t)(kk * 2 * VW), id_pv, kk > 0);
+          mma_commit(&S.o_full[c & 1]);
+          if (last_in_item) mma_commit(&S.q_empty[qb]);
+          mma_commit(&S.kv_empty[st]);
         }
+        __syncwarp();
+        if (lane == 0) trace(trp, c, 6);
         if (more) {
           issue_qk(next_qk);
           more = !S.desc[next_qk % kStages].last_overall;
           ++next_qk;
         }
-        mma_commit(&S.o_full[c & 1]);
-        trace(c, 6);
-        if (last_in_item) mma_commit(&S.q_empty[qb]);
-        mma_commit(&S.kv_empty[st]);
         ++c;
         if (last) break;
       }
@@ -576,6 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
     int64_t tok_pend = 0;
     bool rowok_pend = false;
     int head_pend = 0;
+    uint4 gate_cur[HD / 8], gate_pend[HD / 8];   // gate logits, prefetched at branch start
     float o[HD];
 #pragma unroll
     for (int j = 0; j < HD; ++j) o[j] = 0.f;
@@ -584,12 +613,12 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
     // O_part / L_part of the previous chunk: o = o * alpha + O_part, same for l
     auto absorb_pv = [&]() {
       mbar_wait(&S.o_full[(c - 1) & 1], ((c - 1) >> 1) & 1);
-      if (tid == 0) trace(c - 1, 7);
+      if (tid == 0) trace(trp, c - 1, 7);
       const uint32_t ps = (c - 1) & 1;  // O/L slot of the absorbed chunk
       tc_after_sync();
       uint32_t r[HD], rl[1];
-      tmem_ld_cols<HD>(tmem + lane_base + kColO + ps * DH + half * HD, r);
-      tmem_ld_cols<1>(tmem + lane_base + kColL + ps * kOL, rl);
+      tmem_ld_cols<HD>(tmem + lane_base + kColO + ps * VW + half * HD, r);
+      tmem_ld_cols<1>(tmem + lane_base + kColO + ps * VW + DH, rl);
       tmem_wait_ld();
       tc_before_sync();
       mbar_arrive(&S.o_empty[ps]);
@@ -603,9 +632,10 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
           const int64_t col0 = (int64_t)br_pend * d_model + head_pend * DH + half * HD;
           const __nv_bfloat16* gp = P.gl + tok_pend * P.ld_gl + P.gcol0 + col0;
           const float* bp = P.gbias ? P.gbias + col0 : nullptr;
+          (void)gp;
 #pragma unroll
           for (int c0 = 0; c0 < HD; c0 += 8) {
-            uint4 raw = *reinterpret_cast<const uint4*>(gp + c0);
+            uint4 raw = gate_pend[c0 / 8];
             const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -639,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
     };
     for (;;) {
       mbar_wait(&S.s_full[c & 1], (c >> 1) & 1);
-      if (tid == 0) trace(c, 3);
+      if (tid == 0) trace(trp, c, 3);
       tc_after_sync();
       const ChunkDesc& D = S.desc[c % kStages];
       const int n_grp = D.ncols / 16;
@@ -649,7 +679,15 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
       const bool row_ok = t < D.q_cnt;
       const int64_t tok = (int64_t)D.q_first + t;
       const int head = D.h * G + g_in;
-      if (first_br) m_run = -__builtin_huge_valf();
+      if (first_br) {
+        m_run = -__builtin_huge_valf();
+        if (row_ok) {  // prefetch this branch's gate logits (used at its end)
+          const __nv_bfloat16* gp = P.gl + tok * P.ld_gl + P.gcol0 +
+                                    (int64_t)br * d_model + head * DH + half * HD;
+#pragma unroll
+          for (int c0 = 0; c0 < HD; c0 += 8) gate_cur[c0 / 8] = *reinterpret_cast<const uint4*>(gp + c0);
+        }
+      }
       // this half's S groups -> registers (all in flight, one wait)
       uint32_t sr[HG * 16];
 #pragma unroll
@@ -669,16 +707,21 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
 #pragma unroll
       for (int k = 0; k < HG; ++k) {
         gmax[k] = -__builtin_huge_valf();
-        if (nv_grp[k] > 0) {
+        if (nv_grp[k] == 16) {
+          float v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            v[j] = fmaxf(__uint_as_float(sr[k * 16 + j]), __uint_as_float(sr[k * 16 + j + 8]));
+#pragma unroll
+          for (int w = 4; w; w >>= 1)
+#pragma unroll
+            for (int j = 0; j < w; ++j) v[j] = fmaxf(v[j], v[j + w]);
+          gmax[k] = v[0];
+        } else if (nv_grp[k] > 0) {
           float v[16];
-          if (nv_grp[k] == 16) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(sr[k * 16 + j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              v[j] = j < nv_grp[k] ? __uint_as_float(sr[k * 16 + j]) : -__builtin_huge_valf();
-          }
+          for (int j = 0; j < 16; ++j)
+            v[j] = j < nv_grp[k] ? __uint_as_float(sr[k * 16 + j]) : -__builtin_huge_valf();
 #pragma unroll
           for (int w = 8; w; w >>= 1)
 #pragma unroll
@@ -698,13 +741,12 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
       for (int p2 = 0; p2 < kParts; ++p2) cmax = fmaxf(cmax, S.xmax[c & 1][p2][m]);
       const float m_new = fmaxf(m_run, cmax * sl2);
       const float alpha = (m_new == -__builtin_huge_valf()) ? 1.f : ex2(m_run - m_new);
-      unsigned char* pbase = reinterpret_cast<unsigned char*>(S.p[c & 1]) +
-                             (m / 8) * (8 * kNK * 2) + (m % 8) * 16;
+      const uint32_t pbase = tmem + lane_base + (c & 1) * kNK + kColP;
 #pragma unroll
       for (int k = 0; k < HG; ++k) {
         const int gi = half * HG + k;
         if (gi < n_grp) {
-          uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
+          uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
           const int nv = nv_grp[k];
           if (nv > 0) {
             float pv[16];
@@ -717,23 +759,16 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
               for (int j = 0; j < 16; ++j)
                 pv[j] = j < nv ? ex2(fmaf(__uint_as_float(sr[k * 16 + j]), sl2, -m_new)) : 0.f;
             }
-            w0.x = pack_bf16(pv[0], pv[1]);
-            w0.y = pack_bf16(pv[2], pv[3]);
-            w0.z = pack_bf16(pv[4], pv[5]);
-            w0.w = pack_bf16(pv[6], pv[7]);
-            w1.x = pack_bf16(pv[8], pv[9]);
-            w1.y = pack_bf16(pv[10], pv[11]);
-            w1.z = pack_bf16(pv[12], pv[13]);
-            w1.w = pack_bf16(pv[14], pv[15]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) w[j] = pack_bf16(pv[2 * j], pv[2 * j + 1]);
           }
-          *reinterpret_cast<uint4*>(pbase + (gi * 2) * 128) = w0;
-          *reinterpret_cast<uint4*>(pbase + (gi * 2 + 1) * 128) = w1;
+          tmem_st8(pbase + gi * 8, w);
         }
       }
-      fence_async_smem();
+      tmem_wait_st();
       tc_before_sync();
       mbar_arrive(&S.p_full[c & 1]);
-      if (tid == 0) trace(c, 4);
+      if (tid == 0) trace(trp, c, 4);
       // previous chunk's PV partial (its rescale factor is alpha_pend)
       if (have_pend) absorb_pv();
       m_run = m_new;
@@ -743,6 +778,10 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
       lastit_pend = last_it;
       tok_pend = tok;
       rowok_pend = row_ok;
+      if (last_br) {
+#pragma unroll
+        for (int j = 0; j < HD / 8; ++j) gate_pend[j] = gate_cur[j];
+      }
       head_pend = head;
       have_pend = true;
       ++c;
@@ -762,7 +801,8 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
 // K/V (token order, f32 or bf16, row stride ld) -> padded interleaved bf16.
 // One CTA per block (or one CTA per 128 rows of an un-partitioned row set).
 __global__ void kv_interleave_kernel(int src_bf16, const void* __restrict__ src, int64_t ld,
-                                     int hkv, int dh, const int64_t* __restrict__ tok,
+                                     int hkv, int dh, int ones_cols,
+                                     const int64_t* __restrict__ tok,
                                      const int64_t* __restrict__ offs,
                                      const int64_t* __restrict__ pad_off, int64_t n_rows_pad,
                                      int64_t n_plain, __nv_bfloat16* __restrict__ dst) {
@@ -779,14 +819,17 @@ __global__ void kv_interleave_kernel(int src_bf16, const void* __restrict__ src,
     plen = lmin(128, n_rows_pad - lo);
     occ = lmax(0, lmin(128, n_plain - lo));
   }
-  const int nchunk = dh / 8;
+  const int nchunk = (dh + ones_cols) / 8, w = dh + ones_cols;
   int64_t total = (int64_t)hkv * plen * nchunk;
   for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
     int cc = (int)(e % nchunk);
     int64_t rr = (e / nchunk) % plen;
     int h = (int)(e / (nchunk * plen));
     __align__(16) __nv_bfloat16 vals[8];
-    if (rr < occ) {
+    if (cc * 8 >= dh) {  // ones columns: 1 for a real key, 0 for padding
+#pragma unroll
+      for (int j = 0; j < 8; ++j) vals[j] = __float2bfloat16_rn(rr < occ ? 1.f : 0.f);
+    } else if (rr < occ) {
       int64_t row = tok ? tok[lo + rr] : lo + rr;
       if (src_bf16) {
         *reinterpret_cast<uint4*>(vals) = *reinterpret_cast<const uint4*>(
@@ -801,7 +844,7 @@ __global__ void kv_interleave_kernel(int src_bf16, const void* __restrict__ src,
       for (int j = 0; j < 8; ++j) vals[j] = __float2bfloat16_rn(0.f);
     }
     int64_t prow = base + rr;
-    int64_t off = (int64_t)h * n_rows_pad * dh + (prow / 8) * (8 * dh) + cc * 64 + (prow % 8) * 8;
+    int64_t off = (int64_t)h * n_rows_pad * w + (prow / 8) * (8 * w) + cc * 64 + (prow % 8) * 8;
     *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<uint4*>(vals);
   }
 }
@@ -893,21 +936,22 @@ int lsrm_debug_set_trace(void* buf) {
 }
 
 int lsrm_kv_interleave(int src_is_bf16, const void* src, int64_t ld_src, int64_t n, int hkv,
-                       int dh, const int64_t* block_token_ids, const int64_t* block_offsets,
+                       int dh, int ones_cols, const int64_t* block_token_ids, const int64_t* block_offsets,
                        int64_t n_blocks, const int64_t* pad_offsets, int64_t n_rows_pad,
                        void* dst, void* stream) {
   LSRM_REQUIRE(dh % 8 == 0, "kv_interleave: head_dim must be a multiple of 8");
   LSRM_REQUIRE(n_rows_pad % 16 == 0, "kv_interleave: padded rows must be a multiple of 16");
+  LSRM_REQUIRE(ones_cols == 0 || ones_cols == 16, "kv_interleave: ones_cols must be 0 or 16");
   cudaStream_t st = as_stream(stream);
   if (block_token_ids) {
     if (n_blocks == 0) return LSRM_OK;
     tc::kv_interleave_kernel<<<(unsigned)n_blocks, 256, 0, st>>>(
-        src_is_bf16, src, ld_src, hkv, dh, block_token_ids, block_offsets, pad_offsets,
+        src_is_bf16, src, ld_src, hkv, dh, ones_cols, block_token_ids, block_offsets, pad_offsets,
         n_rows_pad, 0, (__nv_bfloat16*)dst);
   } else {
     if (n_rows_pad == 0) return LSRM_OK;
     tc::kv_interleave_kernel<<<(unsigned)ceil_div(n_rows_pad, 128), 256, 0, st>>>(
-        src_is_bf16, src, ld_src, hkv, dh, nullptr, nullptr, nullptr, n_rows_pad, n,
+        src_is_bf16, src, ld_src, hkv, dh, ones_cols, nullptr, nullptr, nullptr, n_rows_pad, n,
         (__nv_bfloat16*)dst);
   }
   LSRM_LAUNCHED();

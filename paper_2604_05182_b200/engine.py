@@ -11,12 +11,12 @@ block-major order of each modality's own partition, so that
 Per layer and stream, ONE bf16 GEMM (cuBLAS) computes all projections that
 read that stream: the q and gate columns of its two query uses and the k/v
 columns of the two uses that read it as KV.  Then per use: ResBlock
-compression (f64, csrc/compress.cu), K/V re-layout into the padded
+compression (fp32, csrc/compress.cu), K/V re-layout into the padded
 core-matrix layout (csrc/attn_tc.cu), the fused tcgen05 three-branch
 attention with the gated merge, and the W_o GEMM.
 
 Numerics: bf16 storage, fp32 accumulation (tensor cores), fp32 softmax with
-bf16 probabilities, f64 compression.  Tolerance vs the f32/f64 reference is
+bf16 probabilities, fp32 compression.  Tolerance vs the f32/f64 reference is
 stated in DESIGN.md and enforced in tests/test_gpu_engine.py.
 """
 
@@ -37,6 +37,7 @@ USES = ("v2v", "v2i", "i2i", "i2v")
 USE_GEOM = {"v2v": ("x", "x", 3), "v2i": ("x", "y", 2), "i2i": ("y", "y", 3),
             "i2v": ("y", "x", 2)}
 ROW_PAD = 16
+ONES_COLS = 16   # extra V columns (1 = real key) that make P.V also emit row sums
 
 
 @dataclass
@@ -50,15 +51,19 @@ class StreamMeta:
     n_rows_pad: int
     ident: torch.Tensor         # [n] int64 arange (block-major token ids)
     pad_off_host: np.ndarray
+    pad_row: torch.Tensor       # [n] int32 padded row of every (block-major) token
 
 
 def stream_meta(part: BlockPartition) -> StreamMeta:
     occ = part.occupancy.astype(np.int64)
     padded = (occ + ROW_PAD - 1) // ROW_PAD * ROW_PAD
     pad_off = np.concatenate([[0], np.cumsum(padded)]).astype(np.int64)
+    blk = np.repeat(np.arange(part.n_occupied), occ)
+    pad_row = (pad_off[:-1][blk] + np.arange(part.n_tokens) - part.block_offsets[:-1][blk])
     return StreamMeta(part, part.n_tokens, part.n_occupied, part.dev("block_offsets"),
                       D.dev(pad_off), int(pad_off[-1]),
-                      D.dev(np.arange(part.n_tokens, dtype=np.int64)), pad_off)
+                      D.dev(np.arange(part.n_tokens, dtype=np.int64)), pad_off,
+                      D.dev(pad_row.astype(np.int32)))
 
 
 def query_tiles(part: BlockPartition, group: int, self_use: bool) -> np.ndarray:
@@ -148,13 +153,16 @@ class SparseLayerEngine:
         for s in ("x", "y"):
             m = self.meta[s]
             self.buf[("Y", s)] = D.empty((m.n, ncol[s]), torch.bfloat16)
-            self.buf[("k_il", s)] = D.empty((params.n_kv_heads, m.n_rows_pad, params.head_dim),
+            # zero once: padding rows (and their ones columns) are never written again
+            self.buf[("k_il", s)] = D.zeros((params.n_kv_heads, m.n_rows_pad, params.head_dim),
                                             torch.bfloat16)
-            self.buf[("v_il", s)] = torch.empty_like(self.buf[("k_il", s)])
+            self.buf[("v_il", s)] = D.zeros(
+                (params.n_kv_heads, m.n_rows_pad, params.head_dim + ONES_COLS), torch.bfloat16)
             bpad = (m.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
             self.buf[("kc_il", s)] = D.empty((params.n_kv_heads, bpad, params.head_dim),
                                              torch.bfloat16)
-            self.buf[("vc_il", s)] = torch.empty_like(self.buf[("kc_il", s)])
+            self.buf[("vc_il", s)] = D.empty(
+                (params.n_kv_heads, bpad, params.head_dim + ONES_COLS), torch.bfloat16)
             self.buf[("kc", s)] = D.empty((m.n_blocks, w), torch.float32)
             self.buf[("vc", s)] = D.empty((m.n_blocks, w), torch.float32)
             self.buf[("scratch", s)] = D.empty((m.n, w), torch.float32)
@@ -177,18 +185,18 @@ class SparseLayerEngine:
         for kind, wres in (("k", self.cmp_w[use][0]), ("v", self.cmp_w[use][1])):
             col = self.cols[(use, kind)]
             src = Y[:, col:]
-            call("lsrm_kv_interleave", 1, src.data_ptr(), ld, m.n, p.n_kv_heads, p.head_dim,
-                 m.ident.data_ptr(), m.kv_off.data_ptr(), m.n_blocks, m.pad_off.data_ptr(),
-                 m.n_rows_pad, self.buf[(kind + "_il", ks)].data_ptr(), st)
+            ones = ONES_COLS if kind == "v" else 0   # V gets the row-sum columns
             cmp = self.buf[(kind + "c", ks)]
             w1, b1, w2, b2 = wres
-            call("lsrm_compress_block", 1, src.data_ptr(), ld, m.n, self.w, w1.data_ptr(),
-                 b1.data_ptr(), w2.data_ptr(), b2.data_ptr(), m.ident.data_ptr(),
-                 m.kv_off.data_ptr(), m.n_blocks, cmp.data_ptr(),
-                 self.buf[("scratch", ks)].data_ptr(), st)
+            # fused: interleaved K/V layout + fp32 ResBlock + per-block mean
+            call("lsrm_kv_prepare", src.data_ptr(), ld, m.n, p.n_kv_heads, p.head_dim,
+                 m.pad_row.data_ptr(), m.n_rows_pad, self.buf[(kind + "_il", ks)].data_ptr(), ones,
+                 w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
+                 self.buf[("scratch", ks)].data_ptr(), m.kv_off.data_ptr(), m.n_blocks,
+                 cmp.data_ptr(), st)
             il = self.buf[(kind + "c_il", ks)]
             call("lsrm_kv_interleave", 0, cmp.data_ptr(), self.w, m.n_blocks, p.n_kv_heads,
-                 p.head_dim, None, None, 0, None, int(il.shape[1]), il.data_ptr(), st)
+                 p.head_dim, ones, None, None, 0, None, int(il.shape[1]), il.data_ptr(), st)
 
     def attend(self, use: str):
         qs, ks, ng = USE_GEOM[use]

@@ -246,20 +246,20 @@ def test_tc_fused_attention_vs_oracle(c1):
         q_bm = _ops.gather_rows(D.dev(q.reshape(nq, 1024), torch.bfloat16), tokq)
         gl_bm = _ops.gather_rows(D.dev(gl, torch.bfloat16), tokq)
         kil = D.empty((2, mk.n_rows_pad, 32), torch.bfloat16)
-        vil = torch.empty_like(kil)
+        vil = D.empty((2, mk.n_rows_pad, 48), torch.bfloat16)
         st = D.stream()
-        for src, dst in ((k, kil), (v, vil)):
+        for src, dst, ones in ((k, kil, 0), (v, vil, 16)):
             s = D.dev(src.reshape(nk, 64), torch.bfloat16)
-            call("lsrm_kv_interleave", 1, s.data_ptr(), 64, nk, 2, 32,
+            call("lsrm_kv_interleave", 1, s.data_ptr(), 64, nk, 2, 32, ones,
                  pk.dev("block_token_ids").data_ptr(), mk.kv_off.data_ptr(), B,
                  mk.pad_off.data_ptr(), mk.n_rows_pad, dst.data_ptr(), st)
         bpad = (B + 15) // 16 * 16
         kcil = D.empty((2, bpad, 32), torch.bfloat16)
-        vcil = torch.empty_like(kcil)
-        for src, dst in ((kc, kcil), (vc, vcil)):
+        vcil = D.empty((2, bpad, 48), torch.bfloat16)
+        for src, dst, ones in ((kc, kcil, 0), (vc, vcil, 16)):
             s = D.dev(src.reshape(B, 64), torch.float32)
-            call("lsrm_kv_interleave", 0, s.data_ptr(), 64, B, 2, 32, None, None, 0, None, bpad,
-                 dst.data_ptr(), st)
+            call("lsrm_kv_interleave", 0, s.data_ptr(), 64, B, 2, 32, ones, None, None, 0, None,
+                 bpad, dst.data_ptr(), st)
         rows, cnt = plan.device_rows[name]
         rb, cb = block_major_rows(rows, cnt, pq, pk, self_use)
         tiles = D.dev(query_tiles(pq, 16, self_use))
