@@ -223,13 +223,10 @@ def run_gpu(args):
     from paper_2604_05182_b200.layer import SparseAttentionLayer, build_instance
 
     rank, local_rank, ws = dist_env()
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(local_rank % torch.cuda.device_count())   # gloo tests share a GPU
     if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        from paper_2604_05182_b200.seq_parallel import run_sp_bench
-        return run_sp_bench(args)
-    wl_name = "c3"
+        return run_sp(args)
+    wl_name = args.workload or "c3"
     inst = build_instance(wl_name)
     layer = SparseAttentionLayer(inst)
     x_bm, y_bm = layer.device_inputs(inst.x_hat, inst.y_hat)
@@ -239,20 +236,33 @@ def run_gpu(args):
     for _ in range(args.warmup):
         layer.engine.forward(x_bm, y_bm)
     torch.cuda.synchronize()
+    reset_launch_count()
+    layer.engine.forward(x_bm, y_bm)      # own-kernel launches per step (cuBLAS excluded)
+    per_step_launches = launch_count()
+    use_graph = not args.no_graph
+    if use_graph:
+        try:
+            layer.engine.capture(x_bm, y_bm)
+        except Exception as exc:  # report, fall back to eager launches
+            print(f"# CUDA graph capture failed ({exc}); timing eager launches", file=sys.stderr)
+            use_graph = False
+    step = layer.engine.replay if use_graph else (lambda: layer.engine.forward(x_bm, y_bm))
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
     # -- timed region: K steps, device events per step, L2 flushed in between
     sampler = ClockSampler(local_rank)
     sampler.start()
-    reset_launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     torch.cuda.synchronize()
     for i in range(args.steps):
         flush.zero_()
         evs[i][0].record(st)
-        layer.engine.forward(x_bm, y_bm)
+        step()
         evs[i][1].record(st)
     torch.cuda.synchronize()
-    launches = launch_count()
+    launches = per_step_launches * args.steps
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms = float(np.mean(step_ms))
     # -- per-kernel breakdown (separate pass, events on the launching stream)
@@ -283,10 +293,10 @@ def run_gpu(args):
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (reference fixture geometry, tagged Philox features/weights)",
-        "config": {"workload": "C3 fine stage: 16 views, S_vol=S_img=96, heads 32/2/32, d=1024, "
-                               "3D routing b_i=16 budgets 8, one layer = 4 gated NSA uses",
+        "config": {"workload": WORKLOAD_DESC.get(wl_name, wl_name),
                    "n_vol": inst.n_vol, "n_img": inst.n_img, "global_batch": n_tok,
-                   "parallelism": "single GPU", "l2": "flushed (256 MiB write) between steps"},
+                   "parallelism": "single GPU", "l2": "flushed (256 MiB write) between steps",
+                   "cuda_graph": use_graph},
         "roofline": {"bound": "tensor", "kernel": "nsa_fused_kernel (4 launches/step)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -303,6 +313,161 @@ def run_gpu(args):
     print(json.dumps(line), flush=True)
 
 
+WORKLOAD_DESC = {
+    "c3": "C3 fine stage: 16 views, S_vol=S_img=96, heads 32/2/32, d=1024, 3D routing b_i=16 "
+          "budgets 8, one layer = 4 gated NSA uses",
+    "c4": "C4 SP stress: C3 + 12 fully occupied 8^3 volume blocks (skewed per-block sparsity), "
+          "heads 32/2/32, d=1024, one layer = 4 gated NSA uses",
+    "c1": "C1 tiny: 4 views, S_vol=32, S_img=96, heads 8/1/8, d=64",
+}
+
+
+def run_sp(args):
+    """N>1 (torchrun, one rank per GPU): block-aware sequence parallelism.
+    Strong scaling on the C4 skewed workload: every rank builds the same
+    instance, owns the query blocks LPT assigns it (routed-block workload),
+    all-gathers K/V per use over NCCL (grouped send/recv) and attends its own
+    queries.  Timed on the device, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_05182_b200._native import launch_count, reset_launch_count
+    from paper_2604_05182_b200.layer import build_instance
+    from paper_2604_05182_b200 import seq_parallel as S
+
+    rank, local_rank, ws = dist_env()
+    backend = args.sp_backend
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        transport = S.NcclTransport(rank, ws)
+        red_dev = torch.device("cuda", local_rank)
+    else:   # gloo: several ranks may share one GPU (tests)
+        dist.init_process_group("gloo")
+        transport = S.HostStagedTransport(rank, ws)
+        red_dev = torch.device("cpu")
+
+    def max_all(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_all(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    wl_name = args.workload or "c4"
+    inst = build_instance(wl_name)
+    n_tok = inst.n_vol + inst.n_img
+    sl = S.ShardedLayer(inst, rank, ws, transport=transport, by_cost=not args.token_lpt)
+    x_loc, y_loc = sl.local_inputs(inst.x_hat, inst.y_hat)
+    for _ in range(args.warmup):
+        sl.forward(x_loc, y_loc)
+    torch.cuda.synchronize()
+    reset_launch_count()
+    sl.forward(x_loc, y_loc)
+    per_step_launches = launch_count()
+    use_graph = not args.no_graph
+    if use_graph:
+        try:
+            sl.capture(x_loc, y_loc)
+        except Exception as exc:
+            print(f"# rank {rank}: CUDA graph capture failed ({exc}); eager", file=sys.stderr)
+            use_graph = False
+    if not max_all(0.0 if use_graph else 1.0) == 0.0:
+        use_graph = False            # all ranks must take the same path
+    step = sl.step if use_graph else (lambda: sl.forward(x_loc, y_loc))
+    for _ in range(2):
+        step()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(st)
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(st)
+        step()
+        evs[i][1].record(st)
+    t1.record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms_local = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    ms = max_all(ms_local)
+    attn_ms = max_all(sl.attention_ms(reps=max(3, args.steps)))
+    flops = sum(sum(v.values()) for v in sl.engine.attention_flops().values())
+    total_flops = sum_all(flops)
+    e2e_local, h2d, d2h = sl.time_host_path(inst.x_hat, inst.y_hat, steps=args.steps)
+    e2e_ms = max_all(e2e_local)
+    h2d_all, d2h_all = sum_all(h2d), sum_all(d2h)
+    launches = int(sum_all(per_step_launches * args.steps))
+    loads = np.asarray(sl.topology.loads, np.float64)
+    single = None
+    if not args.no_single_compare:
+        # the same workload on ONE GPU (rank 0), same timing rules: the
+        # denominator for strong-scaling efficiency on THIS workload
+        if rank == 0:
+            from paper_2604_05182_b200.layer import SparseAttentionLayer
+            layer = SparseAttentionLayer(inst)
+            xb, yb = layer.device_inputs(inst.x_hat, inst.y_hat)
+            for _ in range(args.warmup):
+                layer.engine.forward(xb, yb)
+            layer.engine.capture(xb, yb)
+            e = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                 for _ in range(args.steps)]
+            for i in range(args.steps):
+                flush.zero_()
+                e[i][0].record(st)
+                layer.engine.replay()
+                e[i][1].record(st)
+            torch.cuda.synchronize()
+            ms1 = float(np.mean([a.elapsed_time(b) for a, b in e]))
+            single = {"value": n_tok / (ms1 * 1e-3), "ms_per_step": ms1}
+        dist.barrier()
+    peaks, src = load_peaks()
+    peak = float(peaks["bf16_tflops"]) * ws
+    achieved = total_flops / (attn_ms * 1e-3) / 1e12
+    if rank == 0:
+        line = {
+            "metric": "LSRM sparse-attn layer tokens/s", "value": n_tok / (ms * 1e-3),
+            "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference fixture geometry, tagged Philox features/weights)",
+            "config": {"workload": WORKLOAD_DESC.get(wl_name, wl_name),
+                       "n_vol": inst.n_vol, "n_img": inst.n_img, "global_batch": n_tok,
+                       "parallelism": f"sp{ws}: block-aware sequence parallelism, "
+                                      f"{'token' if args.token_lpt else 'routed-workload'} LPT, "
+                                      f"All-gather-KV per use ({backend} grouped send/recv)",
+                       "makespan_ratio": float(loads.max() / loads.mean()) if loads.sum() else 1.0,
+                       "l2": "flushed (256 MiB write) between steps", "cuda_graph": use_graph},
+            "roofline": {"bound": "tensor", "kernel": "nsa_fused_kernel (4 launches/step/rank)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": f"{src} bf16_tflops x {ws} GPUs",
+                         "algorithmic_flops_per_step": total_flops,
+                         "attention_ms_max_over_ranks": attn_ms},
+            "single_gpu_same_workload": single,
+            "cpu_baseline": None,
+            "e2e": {"value": n_tok / (e2e_ms * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -312,6 +477,15 @@ def main():
     ap.add_argument("--ref-frac", type=float, default=1.0 / 32)
     ap.add_argument("--warmup-ref", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches")
+    ap.add_argument("--workload", default=None, choices=["c1", "c3", "c4"],
+                    help="default: c3 at N=1, c4 (skewed) under torchrun N>1")
+    ap.add_argument("--sp-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo = host-staged exchange, lets ranks share one GPU (tests)")
+    ap.add_argument("--token-lpt", action="store_true",
+                    help="shard by token counts (reference rule) instead of routed workload")
+    ap.add_argument("--no-single-compare", action="store_true",
+                    help="N>1: skip timing the same workload on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         args.steps = min(args.steps, 3)

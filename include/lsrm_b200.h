@@ -228,6 +228,12 @@ int lsrm_kv_prepare(const void* src, int64_t ld, int64_t n, int hkv, int dh,
                     const int64_t* block_offsets, int64_t n_blocks,
                     float* mean_out, void* stream);
 
+/* Byte-segment copy: segs [n_segs, 3] int64 = (src offset, dst offset,
+ * bytes), all multiples of 16.  Places all-gathered per-rank KV shards into
+ * the canonical block-major layout (seq_parallel.py All-gather-KV). */
+int lsrm_copy_segments(const void* src, void* dst, const int64_t* segs,
+                       int64_t n_segs, void* stream);
+
 /* Row permutation helpers (block-major <-> token order). */
 int lsrm_gather_rows(int elem_bytes, const void* src, int64_t ld_src,
                      const int64_t* index, int64_t n, int64_t row_elems,

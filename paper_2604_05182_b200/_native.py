@@ -54,6 +54,7 @@ SIGNATURES = {
     "lsrm_kv_interleave": (I32, [I32, P, I64, I64, I32, I32, I32, P, P, I64, P, I64,
                                  P, P]),
     "lsrm_debug_set_trace": (I32, [P]),
+    "lsrm_copy_segments": (I32, [P, P, P, I64, P]),
     "lsrm_kv_prepare": (I32, [P, I64, I64, I32, I32, P, I64, P, I32, P, P, P, P, P, P, I64,
                               P, P]),
     "lsrm_gather_rows": (I32, [I32, P, I64, P, I64, I64, P, I64, P]),

@@ -158,3 +158,32 @@ int lsrm_layer_norm(int in_bf16, const void* x, int64_t n, int d,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Segment copy: dst[d_off : d_off + n] = src[s_off : s_off + n] for a list of
+// byte segments (16-byte aligned).  Used to place all-gathered per-rank KV
+// shards into the canonical block-major layout (W-invariant attention input).
+namespace lsrm {
+__global__ void copy_segments_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                     const int64_t* __restrict__ segs, int64_t n_segs) {
+  for (int64_t sg = blockIdx.x; sg < n_segs; sg += gridDim.x) {
+    const int64_t so = segs[3 * sg], dof = segs[3 * sg + 1], nb = segs[3 * sg + 2];
+    const int4* s4 = reinterpret_cast<const int4*>(src + so);
+    int4* d4 = reinterpret_cast<int4*>(dst + dof);
+    for (int64_t i = threadIdx.x; i < nb / 16; i += blockDim.x) d4[i] = s4[i];
+  }
+}
+}  // namespace lsrm
+
+extern "C" int lsrm_copy_segments(const void* src, void* dst, const int64_t* segs,
+                                  int64_t n_segs, void* stream) {
+  using namespace lsrm;
+  if (n_segs == 0) return LSRM_OK;
+  LSRM_REQUIRE(((uintptr_t)src % 16) == 0 && ((uintptr_t)dst % 16) == 0,
+               "copy_segments: buffers must be 16-byte aligned");
+  int blocks = (int)std::min<int64_t>(n_segs, 148 * 8);
+  copy_segments_kernel<<<blocks, 128, 0, as_stream(stream)>>>((const uint8_t*)src, (uint8_t*)dst,
+                                                              segs, n_segs);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}

@@ -10,14 +10,22 @@ block-major order of each modality's own partition, so that
 
 Per layer and stream, ONE bf16 GEMM (cuBLAS) computes all projections that
 read that stream: the q and gate columns of its two query uses and the k/v
-columns of the two uses that read it as KV.  Then per use: ResBlock
-compression (fp32, csrc/compress.cu), K/V re-layout into the padded
-core-matrix layout (csrc/attn_tc.cu), the fused tcgen05 three-branch
-attention with the gated merge, and the W_o GEMM.
+columns of the two uses that read it as KV.  Then per use: the fused K/V
+preparation (interleaved layout + fp32 ResBlock + block mean,
+csrc/compress.cu), the fused tcgen05 three-branch attention with the gated
+merge (csrc/attn_tc.cu), and the W_o GEMM.
+
+Sharding (block-aware sequence parallelism, seq_parallel.py): an engine can
+own only a subset of each stream's blocks.  Its query side then works on the
+owned tokens in a rank-local compact order (owned blocks, canonical order);
+its KV side computes K/V and compression for the owned KV blocks and an
+`exchange` hook (All-gather-KV) assembles the canonical global KV buffers
+that every rank's attention reads — so each output row is computed from the
+same inputs by the same tile regardless of the number of ranks.
 
 Numerics: bf16 storage, fp32 accumulation (tensor cores), fp32 softmax with
 bf16 probabilities, fp32 compression.  Tolerance vs the f32/f64 reference is
-stated in DESIGN.md and enforced in tests/test_gpu_engine.py.
+stated in DESIGN.md and enforced in tests/test_gpu_parity.py.
 """
 
 from dataclasses import dataclass
@@ -40,45 +48,83 @@ ROW_PAD = 16
 ONES_COLS = 16   # extra V columns (1 = real key) that make P.V also emit row sums
 
 
+def _padded(occ: np.ndarray) -> np.ndarray:
+    return (occ + ROW_PAD - 1) // ROW_PAD * ROW_PAD
+
+
+class PackedShard:
+    """Byte layout of one rank's KV shard for one use: interleaved K
+    [hkv, rows_pad, dh] bf16, V [hkv, rows_pad, dh+16] bf16, compressed K and
+    V [n_blocks, w] f32 (every section a multiple of 16 bytes)."""
+
+    def __init__(self, hkv: int, dh: int, w: int, n_rows_pad: int, n_blocks: int):
+        self.rows_pad = max(int(n_rows_pad), ROW_PAD)
+        self.n_blocks = max(int(n_blocks), 1)
+        self.off_v = hkv * self.rows_pad * dh * 2
+        self.off_kc = self.off_v + hkv * self.rows_pad * (dh + ONES_COLS) * 2
+        self.off_vc = self.off_kc + self.n_blocks * w * 4
+        self.total = self.off_vc + self.n_blocks * w * 4
+
+
 @dataclass
 class StreamMeta:
-    """Device metadata of one modality in its own block-major order."""
+    """One modality: canonical (global) KV layout + this engine's owned shard.
+
+    Global: block-major token order, 16-row padded block segments in ascending
+    occupied-row order.  Local: the owned blocks' tokens, same order, compact.
+    """
     part: BlockPartition
-    n: int
+    n: int                      # global tokens
     n_blocks: int
-    kv_off: torch.Tensor        # [B+1] int64 block offsets (block-major == identity)
-    pad_off: torch.Tensor       # [B+1] int64 16-row padded offsets
-    n_rows_pad: int
-    ident: torch.Tensor         # [n] int64 arange (block-major token ids)
+    kv_off: torch.Tensor        # [B+1] int64 global block offsets
+    pad_off: torch.Tensor       # [B+1] int64 global padded offsets
     pad_off_host: np.ndarray
-    pad_row: torch.Tensor       # [n] int32 padded row of every (block-major) token
+    n_rows_pad: int
+    owned: np.ndarray           # owned occupied rows (ascending)
+    n_loc: int
+    loc2glob: torch.Tensor      # [n_loc] int64 global block-major index of local tokens
+    loc_off: torch.Tensor       # [B_loc+1] local block offsets
+    loc_off_host: np.ndarray
+    loc_pad_row: torch.Tensor   # [n_loc] int32 padded row in the local compact layout
+    loc_pad_off_host: np.ndarray
+    n_loc_rows_pad: int
+    sharded: bool
 
 
-def stream_meta(part: BlockPartition) -> StreamMeta:
-    occ = part.occupancy.astype(np.int64)
-    padded = (occ + ROW_PAD - 1) // ROW_PAD * ROW_PAD
-    pad_off = np.concatenate([[0], np.cumsum(padded)]).astype(np.int64)
-    blk = np.repeat(np.arange(part.n_occupied), occ)
-    pad_row = (pad_off[:-1][blk] + np.arange(part.n_tokens) - part.block_offsets[:-1][blk])
-    return StreamMeta(part, part.n_tokens, part.n_occupied, part.dev("block_offsets"),
-                      D.dev(pad_off), int(pad_off[-1]),
-                      D.dev(np.arange(part.n_tokens, dtype=np.int64)), pad_off,
-                      D.dev(pad_row.astype(np.int32)))
-
-
-def query_tiles(part: BlockPartition, group: int, self_use: bool) -> np.ndarray:
-    """[n_tiles, 4] int32 (first query, count, own kv row or -1, 0): tiles of
-    128/group tokens that never straddle a query block."""
-    T = 128 // group
+def stream_meta(part: BlockPartition, owned=None) -> StreamMeta:
     occ = part.occupancy.astype(np.int64)
     off = part.block_offsets.astype(np.int64)
+    pad_off = np.concatenate([[0], np.cumsum(_padded(occ))]).astype(np.int64)
+    sharded = owned is not None
+    owned = np.arange(part.n_occupied) if owned is None else np.sort(np.asarray(owned, np.int64))
+    occ_l = occ[owned]
+    loc_off = np.concatenate([[0], np.cumsum(occ_l)]).astype(np.int64)
+    loc_pad_off = np.concatenate([[0], np.cumsum(_padded(occ_l))]).astype(np.int64)
+    blk = np.repeat(np.arange(owned.size), occ_l)
+    within = np.arange(int(loc_off[-1])) - loc_off[:-1][blk]
+    loc2glob = off[:-1][owned][blk] + within
+    loc_pad_row = loc_pad_off[:-1][blk] + within
+    return StreamMeta(part, part.n_tokens, part.n_occupied, part.dev("block_offsets"),
+                      D.dev(pad_off), pad_off, int(pad_off[-1]), owned, int(loc_off[-1]),
+                      D.dev(loc2glob.astype(np.int64)), D.dev(loc_off), loc_off,
+                      D.dev(loc_pad_row.astype(np.int32)), loc_pad_off, int(loc_pad_off[-1]),
+                      sharded)
+
+
+def query_tiles(part: BlockPartition, group: int, self_use: bool, owned=None) -> np.ndarray:
+    """[n_tiles, 4] int32 (first query (local index), count, own kv row or -1,
+    0): tiles of 128/group tokens that never straddle a query block."""
+    T = 128 // group
+    rows_all = np.arange(part.n_occupied) if owned is None else np.sort(np.asarray(owned))
+    occ = part.occupancy.astype(np.int64)[rows_all]
+    loc_off = np.concatenate([[0], np.cumsum(occ)]).astype(np.int64)
     n_t = (occ + T - 1) // T
-    rows = np.repeat(np.arange(part.n_occupied), n_t)
+    idx = np.repeat(np.arange(rows_all.size), n_t)
     k = np.arange(int(n_t.sum())) - np.repeat(np.cumsum(n_t) - n_t, n_t)
-    first = off[rows] + k * T
-    cnt = np.minimum(T, occ[rows] - k * T)
-    own = rows if self_use else np.full_like(rows, -1)
-    return np.stack([first, cnt, own, np.zeros_like(rows)], axis=1).astype(np.int32)
+    first = loc_off[idx] + k * T
+    cnt = np.minimum(T, occ[idx] - k * T)
+    own = rows_all[idx] if self_use else np.full(idx.size, -1)
+    return np.stack([first, cnt, own, np.zeros_like(idx)], axis=1).astype(np.int32)
 
 
 def block_major_rows(rows_tok, count_tok, part_q: BlockPartition, part_kv: BlockPartition,
@@ -103,17 +149,25 @@ class SparseLayerEngine:
     weights: dict use -> NsaWeights (reference layout, f32 host arrays).
     plan_rows: dict use -> (rows [n, kmax] int32, count [n] int32), token
     order, as produced by `block_routing.build_routing_plan(...).device_rows`.
+    shard: optional {"x": owned vol rows, "y": owned img rows}; `exchange`
+    (seq_parallel) then fills the global KV buffers between prepare_kv and
+    attend.
     """
 
     def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
-                 weights: dict, params: AttentionParams):
+                 weights: dict, params: AttentionParams, shard: dict = None):
         require(params.head_dim in (32, 64), "bf16 engine: head_dim must be 32 or 64")
         G = params.group_size
-        require(128 % G == 0, "bf16 engine: (n_q_heads/n_kv_heads) must divide 128")
+        require(128 % G == 0 and G >= 4, "bf16 engine: (n_q_heads/n_kv_heads) must be in 4..128 "
+                "and divide 128")
         self.params = params
         d, w = params.model_dim, params.n_kv_heads * params.head_dim
         self.d, self.w = d, w
-        self.meta = {"x": stream_meta(part_vol), "y": stream_meta(part_img)}
+        shard = shard or {}
+        self.meta = {"x": stream_meta(part_vol, shard.get("x")),
+                     "y": stream_meta(part_img, shard.get("y"))}
+        self.sharded = bool(shard)
+        self.exchange = None   # set by seq_parallel for sharded engines
         parts = {"x": part_vol, "y": part_img}
         # fused projection weights per stream: [q|gates] of its query uses, then
         # [k|v] of the uses that read it as KV
@@ -139,44 +193,65 @@ class SparseLayerEngine:
         self.gate_b = {u: D.dev(weights[u].gate_b, torch.float32) for u in USES}
         self.cmp_w = {u: (_dev_res(weights[u].compress.for_k), _dev_res(weights[u].compress.for_v))
                       for u in USES}
-        # per-use routing and tiles
+        # per-use routing (local query order) and tiles
         self.rows, self.count, self.tiles, self.kmax = {}, {}, {}, {}
         for use in USES:
             qs, ks, ng = USE_GEOM[use]
             r, c = plan_rows[use]
             rb, cb = block_major_rows(r, c, parts[qs], parts[ks], ng == 3)
+            mq = self.meta[qs]
+            if mq.sharded:
+                rb = _ops.gather_rows(rb, mq.loc2glob)
+                cb = _ops.gather_rows(cb.view(-1, 1), mq.loc2glob).view(-1)
             self.rows[use], self.count[use] = rb, cb
             self.kmax[use] = int(rb.shape[1])
-            self.tiles[use] = D.dev(query_tiles(parts[qs], G, ng == 3))
+            self.tiles[use] = D.dev(query_tiles(parts[qs], G, ng == 3,
+                                                mq.owned if mq.sharded else None))
         # work buffers
+        hkv, dh = params.n_kv_heads, params.head_dim
         self.buf = {}
         for s in ("x", "y"):
             m = self.meta[s]
-            self.buf[("Y", s)] = D.empty((m.n, ncol[s]), torch.bfloat16)
-            # zero once: padding rows (and their ones columns) are never written again
-            self.buf[("k_il", s)] = D.zeros((params.n_kv_heads, m.n_rows_pad, params.head_dim),
-                                            torch.bfloat16)
-            self.buf[("v_il", s)] = D.zeros(
-                (params.n_kv_heads, m.n_rows_pad, params.head_dim + ONES_COLS), torch.bfloat16)
+            self.buf[("Y", s)] = D.empty((m.n_loc, ncol[s]), torch.bfloat16)
+            # global KV (zeroed once: padding rows and their ones columns stay 0)
+            self.buf[("k_il", s)] = D.zeros((hkv, m.n_rows_pad, dh), torch.bfloat16)
+            self.buf[("v_il", s)] = D.zeros((hkv, m.n_rows_pad, dh + ONES_COLS), torch.bfloat16)
             bpad = (m.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
-            self.buf[("kc_il", s)] = D.empty((params.n_kv_heads, bpad, params.head_dim),
-                                             torch.bfloat16)
-            self.buf[("vc_il", s)] = D.empty(
-                (params.n_kv_heads, bpad, params.head_dim + ONES_COLS), torch.bfloat16)
+            self.buf[("kc_il", s)] = D.empty((hkv, bpad, dh), torch.bfloat16)
+            self.buf[("vc_il", s)] = D.empty((hkv, bpad, dh + ONES_COLS), torch.bfloat16)
             self.buf[("kc", s)] = D.empty((m.n_blocks, w), torch.float32)
             self.buf[("vc", s)] = D.empty((m.n_blocks, w), torch.float32)
-            self.buf[("scratch", s)] = D.empty((m.n, w), torch.float32)
+            self.buf[("scratch", s)] = D.empty((max(m.n_loc, 1), w), torch.float32)
         for use in USES:
-            qs = USE_GEOM[use][0]
-            self.buf[("merged", use)] = D.empty((self.meta[qs].n, d), torch.bfloat16)
-            self.buf[("out", use)] = D.empty((self.meta[qs].n, d), torch.bfloat16)
+            qs, ks, _ = USE_GEOM[use]
+            self.buf[("merged", use)] = D.empty((self.meta[qs].n_loc, d), torch.bfloat16)
+            self.buf[("out", use)] = D.empty((self.meta[qs].n_loc, d), torch.bfloat16)
+            m = self.meta[ks]
+            if m.sharded:
+                # rank-local compact KV shard of this use, packed in ONE buffer
+                # [k_il | v_il | k_cmp | v_cmp] so the exchange sends it whole
+                lay = PackedShard(hkv, dh, w, m.n_loc_rows_pad, m.owned.size)
+                buf = D.zeros((lay.total,), torch.uint8)
+                self.buf[("packed", use)] = buf
+                self.buf[("k_loc", use)] = buf[:lay.off_v].view(torch.bfloat16).view(
+                    hkv, lay.rows_pad, dh)
+                self.buf[("v_loc", use)] = buf[lay.off_v:lay.off_kc].view(torch.bfloat16).view(
+                    hkv, lay.rows_pad, dh + ONES_COLS)
+                self.buf[("kc_loc", use)] = buf[lay.off_kc:lay.off_vc].view(torch.float32).view(
+                    lay.n_blocks, w)
+                self.buf[("vc_loc", use)] = buf[lay.off_vc:].view(torch.float32).view(
+                    lay.n_blocks, w)
 
     # -- pieces --------------------------------------------------------------
-    def project(self, x_bm: torch.Tensor, y_bm: torch.Tensor):
-        _ops.gemm(x_bm, self.w_cat["x"], out=self.buf[("Y", "x")])
-        _ops.gemm(y_bm, self.w_cat["y"], out=self.buf[("Y", "y")])
+    def project(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
+        if self.meta["x"].n_loc:
+            _ops.gemm(x_loc, self.w_cat["x"], out=self.buf[("Y", "x")])
+        if self.meta["y"].n_loc:
+            _ops.gemm(y_loc, self.w_cat["y"], out=self.buf[("Y", "y")])
 
     def prepare_kv(self, use: str):
+        """K/V of the owned KV blocks: interleaved layout + compression.
+        Unsharded engines write the global buffers directly."""
         _, ks, _ = USE_GEOM[use]
         m, p = self.meta[ks], self.params
         Y = self.buf[("Y", ks)]
@@ -186,26 +261,44 @@ class SparseLayerEngine:
             col = self.cols[(use, kind)]
             src = Y[:, col:]
             ones = ONES_COLS if kind == "v" else 0   # V gets the row-sum columns
-            cmp = self.buf[(kind + "c", ks)]
             w1, b1, w2, b2 = wres
-            # fused: interleaved K/V layout + fp32 ResBlock + per-block mean
-            call("lsrm_kv_prepare", src.data_ptr(), ld, m.n, p.n_kv_heads, p.head_dim,
-                 m.pad_row.data_ptr(), m.n_rows_pad, self.buf[(kind + "_il", ks)].data_ptr(), ones,
-                 w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
-                 self.buf[("scratch", ks)].data_ptr(), m.kv_off.data_ptr(), m.n_blocks,
-                 cmp.data_ptr(), st)
-            il = self.buf[(kind + "c_il", ks)]
+            if m.sharded:
+                il = self.buf[(kind + "_loc", use)]
+                rows_pad = int(il.shape[1])
+                cmp, offs, nb = self.buf[(kind + "c_loc", use)], m.loc_off, m.owned.size
+            else:
+                il, rows_pad = self.buf[(kind + "_il", ks)], m.n_rows_pad
+                cmp, offs, nb = self.buf[(kind + "c", ks)], m.kv_off, m.n_blocks
+            if m.n_loc:
+                # fused: interleaved K/V layout + fp32 ResBlock + per-block mean
+                call("lsrm_kv_prepare", src.data_ptr(), ld, m.n_loc, p.n_kv_heads, p.head_dim,
+                     m.loc_pad_row.data_ptr(), rows_pad, il.data_ptr(), ones, w1.data_ptr(),
+                     b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
+                     self.buf[("scratch", ks)].data_ptr(), offs.data_ptr(), nb, cmp.data_ptr(), st)
+        if not m.sharded:
+            self.finish_kv(use)
+
+    def finish_kv(self, use: str):
+        """Compressed rows (global, canonical order) -> interleaved layout."""
+        _, ks, _ = USE_GEOM[use]
+        m, p = self.meta[ks], self.params
+        st = D.stream()
+        for kind in ("k", "v"):
+            ones = ONES_COLS if kind == "v" else 0
+            cmp, il = self.buf[(kind + "c", ks)], self.buf[(kind + "c_il", ks)]
             call("lsrm_kv_interleave", 0, cmp.data_ptr(), self.w, m.n_blocks, p.n_kv_heads,
                  p.head_dim, ones, None, None, 0, None, int(il.shape[1]), il.data_ptr(), st)
 
     def attend(self, use: str):
         qs, ks, ng = USE_GEOM[use]
         mq, mk, p = self.meta[qs], self.meta[ks], self.params
+        tiles = self.tiles[use]
+        if int(tiles.shape[0]) == 0:
+            return
         Y = self.buf[("Y", qs)]
         qcol = self.cols[(use, "q")]
         q = Y[:, qcol:]
-        tiles = self.tiles[use]
-        call("lsrm_nsa_attention_tc", q.data_ptr(), Y.stride(0), mq.n, p.n_q_heads,
+        call("lsrm_nsa_attention_tc", q.data_ptr(), Y.stride(0), mq.n_loc, p.n_q_heads,
              p.n_kv_heads, p.head_dim, self.buf[("k_il", ks)].data_ptr(),
              self.buf[("v_il", ks)].data_ptr(), mk.pad_off.data_ptr(), mk.kv_off.data_ptr(),
              mk.n_rows_pad, self.buf[("kc_il", ks)].data_ptr(),
@@ -215,29 +308,73 @@ class SparseLayerEngine:
              self.gate_b[use].data_ptr(), ng, self.buf[("merged", use)].data_ptr(), D.stream())
 
     def output(self, use: str):
-        _ops.gemm(self.buf[("merged", use)], self.w_o[use], out=self.buf[("out", use)])
+        if self.buf[("merged", use)].shape[0]:
+            _ops.gemm(self.buf[("merged", use)], self.w_o[use], out=self.buf[("out", use)])
 
     # -- whole layer ---------------------------------------------------------
-    def forward(self, x_bm: torch.Tensor, y_bm: torch.Tensor) -> dict:
-        """x_bm [Nv, d], y_bm [Ni, d] bf16 (LN'd, block-major) -> dict use ->
-        [Nq, d] bf16 (block-major).  Output buffers are reused across calls."""
-        self.project(x_bm, y_bm)
+    def forward(self, x_loc: torch.Tensor, y_loc: torch.Tensor) -> dict:
+        """x_loc [Nv_loc, d], y_loc [Ni_loc, d] bf16 (LN'd; block-major, or the
+        rank-local compact order when sharded) -> dict use -> [Nq_loc, d] bf16.
+        Output buffers are reused across calls."""
+        if self.sharded:
+            self.forward_local(x_loc, y_loc)
+            return self.forward_exchange()
+        self.project(x_loc, y_loc)
         for use in USES:
             self.prepare_kv(use)
             self.attend(use)
             self.output(use)
         return {u: self.buf[("out", u)] for u in USES}
 
+    def forward_local(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
+        """Sharded phase 1: projections and this rank's KV shards of all uses."""
+        self.project(x_loc, y_loc)
+        for use in USES:
+            self.prepare_kv(use)
+
+    def forward_exchange(self) -> dict:
+        """Sharded phase 2: launch all four All-gather-KV exchanges (in flight
+        while earlier uses attend), then per use wait + place + attend."""
+        require(self.exchange is not None, "sharded engine needs an exchange (seq_parallel)")
+        handles = {use: self.exchange(self, use) for use in USES}
+        for use in USES:
+            handles[use]()          # wait + place into the canonical layout
+            self.finish_kv(use)
+            self.attend(use)
+            self.output(use)
+        return {u: self.buf[("out", u)] for u in USES}
+
+    def capture(self, x_bm: torch.Tensor, y_bm: torch.Tensor):
+        """Record one layer (all ~30 launches) as a CUDA graph over fixed
+        input/output buffers; `replay()` then re-runs it with one launch."""
+        require(not self.sharded, "CUDA-graph capture is for the single-GPU engine")
+        self._gx, self._gy = x_bm, y_bm
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):          # warm up outside capture
+            self.forward(x_bm, y_bm)
+        torch.cuda.current_stream().wait_stream(st)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.forward(x_bm, y_bm)
+        return self.graph
+
+    def replay(self) -> dict:
+        self.graph.replay()
+        return {u: self.buf[("out", u)] for u in USES}
+
     # -- accounting ------------------------------------------------------------
     def attention_flops(self) -> dict:
-        """Algorithmic attention-core FLOPs per use: useful
-        work only (no padding, union inflation or masked keys)."""
+        """Algorithmic attention-core FLOPs per use for this engine's queries
+        (SURVEY.md §8d): useful work only (no padding, union inflation or
+        masked keys)."""
         p = self.params
         out = {}
         for use in USES:
             qs, ks, ng = USE_GEOM[use]
             pk = self.meta[ks].part
-            nq = self.meta[qs].n
+            mq = self.meta[qs]
+            nq = mq.n_loc
             rows = D.host(self.rows[use])
             cnt = D.host(self.count[use])
             occ = pk.occupancy.astype(np.float64)
@@ -245,10 +382,11 @@ class SparseLayerEngine:
             L = np.where(mask, occ[np.clip(rows, 0, None)], 0.0).sum(axis=1)
             cmp = 4.0 * nq * p.n_q_heads * p.head_dim * pk.n_occupied
             sel = 4.0 * p.n_q_heads * p.head_dim * L.sum()
-            win = 4.0 * p.n_q_heads * p.head_dim * float((occ ** 2).sum()) if ng == 3 else 0.0
+            qocc = mq.part.occupancy.astype(np.float64)[mq.owned]
+            win = 4.0 * p.n_q_heads * p.head_dim * float((qocc ** 2).sum()) if ng == 3 else 0.0
             out[use] = {"cmp": cmp, "sel": sel, "win": win}
         return out
 
     def projection_flops(self) -> float:
-        return sum(2.0 * self.meta[s].n * self.d * self.ncol[s] for s in ("x", "y")) + \
-            sum(2.0 * self.meta[USE_GEOM[u][0]].n * self.d * self.d for u in USES)
+        return sum(2.0 * self.meta[s].n_loc * self.d * self.ncol[s] for s in ("x", "y")) + \
+            sum(2.0 * self.meta[USE_GEOM[u][0]].n_loc * self.d * self.d for u in USES)

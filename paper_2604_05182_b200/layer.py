@@ -40,11 +40,13 @@ class Instance:
     n_img: int
 
 
-def build_instance(name: str = "c3", seed: int = 0) -> Instance:
+def build_instance(name: str = "c3", seed: int = 0, params: AttentionParams = None) -> Instance:
     """GPU instance setup: compaction -> partition -> 3D routing (all on the
-    device, bit-exact with the reference), LN'd fine tokens as layer input."""
+    device, bit-exact with the reference), LN'd fine tokens as layer input.
+    `params` overrides the workload's head geometry (e.g. paper heads on the
+    C1 geometry, which the bf16 engine needs: head_dim 32/64)."""
     wl = load_workload(name)
-    params = params_of(name)
+    params = params or params_of(name)
     d = params.model_dim
     x_d, y_d, pe_v, pe_i = coarse_inputs(wl, d, seed)
     x_up, y_up = upsample_select_tokens(D.dev(x_d), D.dev(y_d), wl.vol_mask, wl.img_mask,

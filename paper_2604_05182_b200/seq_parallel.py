@@ -1,0 +1,609 @@
+"""Block-aware sequence parallelism with All-gather-KV (drop-in for
+`lsrm/seq_parallel.py`, plus the real multi-GPU runtime).
+
+Reference semantics (in-process simulation, `lsrm/seq_parallel.py:1-15`):
+blocks are assigned whole by greedy LPT over token counts; tokens reach their
+workers through an all-to-all; every sparse attention use all-gathers KV
+(original + compressed) while queries stay sharded; window attention is
+worker-local; collectives append (phase, kind, src, dst, bytes) records.
+
+B200 runtime (one process per GPU, NCCL over NVLink/NVSwitch):
+  * `shard_blocks` (token LPT, the reference rule) or `shard_blocks_by_cost`
+    (the north star's routed-block workload: sum of routed key counts over the
+    block's queries for all uses + occupancy^2 for the window branch);
+  * each rank runs `engine.SparseLayerEngine` on its owned blocks' tokens,
+    computes K/V + compression for its owned KV blocks into ONE packed
+    buffer per use, and `KVExchange` all-gathers the packed buffers with a
+    grouped NCCL send/recv (all-gather-v; shards are uneven), then places
+    every block into the canonical block-major layout with one segment-copy
+    kernel per tensor — so each output row sees byte-identical KV whatever
+    the number of ranks (W-invariance, `tests/test_seq_parallel.py:285-325`).
+  * exchanges of all four uses are launched before the first attention, so
+    later uses' transfers overlap earlier uses' attention.
+"""
+
+import csv
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import _dev as D
+from ._native import call
+from .block_partition import BlockPartition
+from .errors import ProtocolError, require
+
+TOKEN_COORD_BYTES = 12     # three u32 spatial coords per moved token (seq_parallel.py:34)
+
+
+# ---------------------------------------------------------------------------
+# topology and message log
+
+
+@dataclass
+class WorkerTopology:
+    """`lsrm/seq_parallel.py:37-58`."""
+    n_workers: int
+    vol_rows: list
+    img_rows: list
+    vol_tokens: list
+    img_tokens: list
+    loads: np.ndarray
+    message_log: list = dc_field(default_factory=list)
+
+    def assignment(self, part: BlockPartition, modality: str) -> np.ndarray:
+        rows = self.vol_rows if modality == "volume" else self.img_rows
+        out = np.full(part.n_blocks_total, -1, dtype=np.int64)
+        for w, rr in enumerate(rows):
+            out[part.occupied_ids[rr]] = w
+        return out
+
+    def log(self, phase: str, kind: str, src: int, dst: int, n_bytes: int) -> None:
+        self.message_log.append((phase, kind, int(src), int(dst), int(n_bytes)))
+
+
+def message_log_to_csv(log, path) -> None:
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["phase", "kind", "src", "dst", "bytes"])
+        w.writerows(log)
+
+
+def _tokens_of(part, rows_per_worker):
+    return [np.concatenate([part.tokens_in_row(r) for r in rr]) if rr.size
+            else np.zeros(0, np.int64) for rr in rows_per_worker]
+
+
+def _lpt(items, n_workers):
+    """Greedy LPT: items = [(sort key, weight, modality 0/1, row)], heaviest
+    first; each goes to the lightest worker (ties: lower worker id)."""
+    loads = np.zeros(n_workers, dtype=np.float64)
+    rows = [[[] for _ in range(n_workers)] for _ in range(2)]
+    for _key, wgt, mod, row in sorted(items):
+        w = int(np.argmin(loads))
+        loads[w] += wgt
+        rows[mod][w].append(row)
+    return [[np.array(sorted(r), dtype=np.int64) for r in rm] for rm in rows], loads
+
+
+def shard_blocks(part_vol: BlockPartition, part_img: BlockPartition,
+                 n_workers: int) -> WorkerTopology:
+    """Greedy LPT over pooled blocks by token count: occupancy descending,
+    ties volume first then lower block id; lightest worker, ties lower id
+    (`seq_parallel.py:93-131`)."""
+    require(n_workers >= 1, "need at least one worker")
+    items = [((-int(p.occupancy[r]), m, int(p.occupied_ids[r])), int(p.occupancy[r]), m, r)
+             for m, p in enumerate((part_vol, part_img)) for r in range(p.n_occupied)]
+    (vol_rows, img_rows), loads = _lpt(items, n_workers)
+    return WorkerTopology(n_workers, vol_rows, img_rows, _tokens_of(part_vol, vol_rows),
+                          _tokens_of(part_img, img_rows), loads.astype(np.int64))
+
+
+def block_costs(part_vol, part_img, lengths: dict, window_uses=("v2v", "i2i")):
+    """Routed-block workload per query block (SURVEY.md §7 hard part 7):
+    sum over the block's tokens of the routed key count L_i of every use it
+    queries, plus occupancy^2 per window use.  lengths: use -> [n_q] gathered
+    key counts in the query partition's TOKEN order."""
+    cost = {"v": np.zeros(part_vol.n_occupied), "i": np.zeros(part_img.n_occupied)}
+    parts = {"v": part_vol, "i": part_img}
+    for use, L in lengths.items():
+        q = use[0]
+        p = parts[q]
+        Lb = np.asarray(L, np.float64)[p.block_token_ids]
+        cost[q] += np.add.reduceat(Lb, p.block_offsets[:-1]) if p.n_occupied else 0.0
+        if use in window_uses:
+            cost[q] += p.occupancy.astype(np.float64) ** 2
+    # compressed branch: every query attends all compressed rows of its KV side
+    for use in lengths:
+        q, k = use[0], use[2]
+        cost[q] += parts[q].occupancy.astype(np.float64) * parts[k].n_occupied
+    return cost["v"], cost["i"]
+
+
+def shard_blocks_by_cost(part_vol, part_img, n_workers, cost_vol, cost_img) -> WorkerTopology:
+    """LPT over routed-block workload (north star item 4); same tie rules."""
+    require(n_workers >= 1, "need at least one worker")
+    items = [((-float(c[r]), m, int(p.occupied_ids[r])), float(c[r]), m, r)
+             for m, (p, c) in enumerate(((part_vol, cost_vol), (part_img, cost_img)))
+             for r in range(p.n_occupied)]
+    (vol_rows, img_rows), loads = _lpt(items, n_workers)
+    return WorkerTopology(n_workers, vol_rows, img_rows, _tokens_of(part_vol, vol_rows),
+                          _tokens_of(part_img, img_rows), loads)
+
+
+def naive_contiguous_shards(n_tokens: int, n_workers: int):
+    """`seq_parallel.py:134-139`."""
+    edges = np.linspace(0, n_tokens, n_workers + 1).astype(np.int64)
+    return [np.arange(lo, hi, dtype=np.int64) for lo, hi in zip(edges[:-1], edges[1:])]
+
+
+# ---------------------------------------------------------------------------
+# reference-API collectives (accounting + invariant checks)
+
+
+def all_to_all(shards_in, shards_out, topology: WorkerTopology, phase: str,
+               bytes_per_token: int):
+    """Re-shard tokens; conservation checks raise ProtocolError; logs bytes
+    per ordered pair (`seq_parallel.py:146-178`)."""
+    n = topology.n_workers
+    require(len(shards_in) == n and len(shards_out) == n,
+            "shard lists must have one entry per worker")
+    owner = np.concatenate([np.full(np.asarray(ids).size, w, np.int64)
+                            for w, ids in enumerate(shards_in)])
+    flat = np.concatenate([np.asarray(ids, np.int64).ravel() for ids in shards_in])
+    uniq, first, counts = np.unique(flat, return_index=True, return_counts=True)
+    if (counts > 1).any():
+        # report the first repeated occurrence in production order
+        seen = np.zeros(flat.size, bool)
+        seen[first] = True
+        raise ProtocolError(f"token {int(flat[np.flatnonzero(~seen)[0]])} produced by two workers")
+    src = owner[first]
+    moved = np.zeros((n, n), dtype=np.int64)
+    for dst, ids in enumerate(shards_out):
+        ids = np.asarray(ids, np.int64).ravel()
+        pos = np.minimum(np.searchsorted(uniq, ids), max(uniq.size - 1, 0))
+        ok = (uniq[pos] == ids) if uniq.size else np.zeros(ids.size, bool)
+        if not ok.all():
+            raise ProtocolError(f"token {int(ids[~ok][0])} requested by worker {dst} "
+                                "was never produced")
+        np.add.at(moved[:, dst], src[pos], 1)
+    if int(moved.sum()) != flat.size:
+        raise ProtocolError("all-to-all does not conserve the token set")
+    for s in range(n):
+        for d in range(n):
+            if s != d and moved[s, d]:
+                topology.log(phase, "all_to_all", s, d, int(moved[s, d]) * bytes_per_token)
+    return shards_out
+
+
+def all_gather_kv(local_parts, topology: WorkerTopology, phase: str):
+    """Replicate per-worker KV into global tensors (k, v by token id; cmp rows
+    by occupied row); ownership must tile both index spaces
+    (`seq_parallel.py:181-218`).  NumPy in -> NumPy out."""
+    n = topology.n_workers
+    block_rows = np.concatenate([np.asarray(p["block_rows"]) for p in local_parts])
+    if not np.array_equal(np.sort(block_rows), np.arange(block_rows.size)):
+        raise ProtocolError("worker block ownership does not tile the occupied blocks")
+    order = np.argsort(block_rows, kind="stable")
+    k_cmp = np.concatenate([p["k_cmp"] for p in local_parts])[order]
+    v_cmp = np.concatenate([p["v_cmp"] for p in local_parts])[order]
+    token_ids = np.concatenate([np.asarray(p["token_ids"]) for p in local_parts])
+    if not np.array_equal(np.sort(token_ids), np.arange(token_ids.size)):
+        raise ProtocolError("worker token ownership does not tile the token sequence")
+    tail = np.asarray(local_parts[0]["k"]).shape[1:]
+    k_tok = np.zeros((token_ids.size,) + tail, np.float32)
+    v_tok = np.zeros((token_ids.size,) + tail, np.float32)
+    for p in local_parts:
+        k_tok[p["token_ids"]] = p["k"]
+        v_tok[p["token_ids"]] = p["v"]
+    kv_bytes = [4 * 2 * (np.asarray(p["k"]).size + np.asarray(p["k_cmp"]).size)
+                for p in local_parts]
+    for s in range(n):
+        for d in range(n):
+            if s != d and kv_bytes[s]:
+                topology.log(phase, "all_gather_kv", s, d, kv_bytes[s])
+    return k_tok, v_tok, k_cmp, v_cmp
+
+
+# ---------------------------------------------------------------------------
+# load-balance reporting (`seq_parallel.py:441-470`)
+
+
+def makespan_ratio(loads, n_workers: int) -> float:
+    total = float(np.sum(loads))
+    return 1.0 if total == 0.0 else float(np.max(loads)) / (total / n_workers)
+
+
+def naive_split_loads(part_vol, part_img, n_workers: int) -> np.ndarray:
+    occ = np.concatenate([part_vol.occupancy, part_img.occupancy])
+    return np.array([int(r.sum()) for r in np.array_split(occ, n_workers)], dtype=np.int64)
+
+
+def imbalance_report(instances, n_workers: int):
+    out = []
+    for pv, pi in instances:
+        topo = shard_blocks(pv, pi, n_workers)
+        naive = naive_split_loads(pv, pi, n_workers)
+        out.append({"loads": topo.loads.tolist(), "naive_loads": naive.tolist(),
+                    "ratio_block_aware": makespan_ratio(topo.loads, n_workers),
+                    "ratio_naive": makespan_ratio(naive, n_workers)})
+    return out
+
+
+# ---------------------------------------------------------------------------
+# distributed All-gather-KV for the bf16 engine
+
+
+def placement_segments(occupancy, pad_off, n_rows_pad: int, shard_rows, hkv: int, dh: int,
+                       w: int):
+    """Staging layout of an all-gathered stream and the byte segments that
+    place every rank's blocks into the canonical global buffers.
+
+    Returns (stage_off [W+1] byte offsets of each rank's packed shard,
+    {"k","v","kc","vc": int64 [n_seg, 3] (src byte offset in staging, dst
+    byte offset in the global buffer, bytes)}).  Global buffers: interleaved
+    K [hkv, n_rows_pad, dh] / V [hkv, n_rows_pad, dh+16] bf16 with block b at
+    padded row pad_off[b]; compressed K/V [n_blocks, w] f32 (engine.py).
+    """
+    from .engine import ONES_COLS, ROW_PAD, PackedShard
+    occ = np.asarray(occupancy, np.int64)
+    gpo = np.asarray(pad_off, np.int64)
+    vw = dh + ONES_COLS
+    offs = [0]
+    seg = {"k": [], "v": [], "kc": [], "vc": []}
+    for rows in shard_rows:
+        rows = np.sort(np.asarray(rows, np.int64))
+        lpo = np.concatenate([[0], np.cumsum((occ[rows] + ROW_PAD - 1) // ROW_PAD * ROW_PAD)])
+        lay = PackedShard(hkv, dh, w, int(lpo[-1]), rows.size)
+        base = offs[-1]
+        j = np.arange(rows.size)
+        plen = gpo[rows + 1] - gpo[rows]
+        for h in range(hkv):
+            seg["k"].append(np.stack([base + (h * lay.rows_pad + lpo[:-1]) * dh * 2,
+                                      (h * n_rows_pad + gpo[rows]) * dh * 2, plen * dh * 2], 1))
+            seg["v"].append(np.stack([base + lay.off_v + (h * lay.rows_pad + lpo[:-1]) * vw * 2,
+                                      (h * n_rows_pad + gpo[rows]) * vw * 2, plen * vw * 2], 1))
+        seg["kc"].append(np.stack([base + lay.off_kc + j * w * 4, rows * w * 4,
+                                   np.full(rows.size, w * 4)], 1))
+        seg["vc"].append(np.stack([base + lay.off_vc + j * w * 4, rows * w * 4,
+                                   np.full(rows.size, w * 4)], 1))
+        offs.append(base + lay.total)
+    seg = {k: np.concatenate(v).astype(np.int64).reshape(-1, 3) if v else
+           np.zeros((0, 3), np.int64) for k, v in seg.items()}
+    return offs, seg
+
+
+def apply_segments(src: np.ndarray, dst: np.ndarray, segs: np.ndarray) -> None:
+    """Host restatement of lsrm_copy_segments (tests): byte arrays."""
+    for so, do, nb in segs.tolist():
+        dst[do:do + nb] = src[so:so + nb]
+
+
+class KVExchange:
+    """All-gather-KV for a sharded SparseLayerEngine.
+
+    shards: per stream, the owned occupied rows of every rank (same on all
+    ranks).  transport(send, recv_slots) moves the packed per-use shards; the
+    default is a grouped NCCL send/recv through torch.distributed
+    (all-gather-v: shards are uneven); `InProcessTransport` is used by the
+    single-GPU tests that emulate several ranks.
+    """
+
+    def __init__(self, engine, rank: int, world: int, shards: dict, transport=None,
+                 topology: WorkerTopology = None):
+        from .engine import USE_GEOM, USES
+        self.rank, self.world = rank, world
+        self.transport = transport or NcclTransport(rank, world)
+        self.topology = topology
+        self.layer_index = 0
+        p = engine.params
+        hkv, dh, w = p.n_kv_heads, p.head_dim, engine.w
+        self.stage_off, self.segs, self.stage = {}, {}, {}
+        for s in ("x", "y"):
+            m = engine.meta[s]
+            offs, seg = placement_segments(m.part.occupancy, m.pad_off_host, m.n_rows_pad,
+                                           shards[s], hkv, dh, w)
+            self.stage_off[s] = offs
+            self.segs[s] = {k: D.dev(v) for k, v in seg.items()}
+        for use in USES:
+            _, ks, _ = USE_GEOM[use]
+            require(int(engine.buf[("packed", use)].numel()) ==
+                    self.stage_off[ks][rank + 1] - self.stage_off[ks][rank],
+                    "seq_parallel: shard layout disagrees with the engine's")
+            self.stage[use] = D.zeros((self.stage_off[ks][-1],), torch.uint8)
+        self.packed = {use: engine.buf[("packed", use)] for use in USES}
+
+    def start(self, use: str):
+        """Launch the all-gather of `use`'s packed shard into its staging
+        buffer; returns the transport's wait callable (stream-ordered)."""
+        from .engine import USE_GEOM
+        _, ks, _ = USE_GEOM[use]
+        offs = self.stage_off[ks]
+        slots = [self.stage[use][offs[r]:offs[r + 1]] for r in range(self.world)]
+        if self.topology is not None:
+            nbytes = self.packed[use].numel()
+            for d in range(self.world):
+                if d != self.rank:
+                    self.topology.log(f"layer{self.layer_index}/{use}", "all_gather_kv",
+                                      self.rank, d, nbytes)
+        return self.transport(self.packed[use], slots)
+
+    def place(self, engine, use: str):
+        """Staging -> canonical global K/V and compressed rows (4 segment-copy
+        launches; capturable in a CUDA graph)."""
+        from .engine import USE_GEOM
+        _, ks, _ = USE_GEOM[use]
+        st = D.stream()
+        stage = self.stage[use]
+        for kind, dst in (("k", engine.buf[("k_il", ks)]), ("v", engine.buf[("v_il", ks)]),
+                          ("kc", engine.buf[("kc", ks)]), ("vc", engine.buf[("vc", ks)])):
+            segs = self.segs[ks][kind]
+            call("lsrm_copy_segments", stage.data_ptr(), dst.data_ptr(), segs.data_ptr(),
+                 int(segs.shape[0]), st)
+
+    def __call__(self, engine, use: str):
+        """engine hook: start the exchange; the returned callable waits and
+        places."""
+        wait = self.start(use)
+
+        def finish():
+            wait()
+            self.place(engine, use)
+        return finish
+
+
+class NcclTransport:
+    """All-gather-v of one packed buffer per rank: grouped NCCL send/recv
+    (`torch.distributed.batch_isend_irecv`), own slot copied locally."""
+
+    def __init__(self, rank, world, group=None):
+        self.rank, self.world, self.group = rank, world, group
+
+    def __call__(self, send: torch.Tensor, slots):
+        import torch.distributed as dist
+        slots[self.rank].copy_(send)
+        ops = []
+        for peer in range(self.world):
+            if peer == self.rank:
+                continue
+            ops.append(dist.P2POp(dist.isend, send, peer, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, slots[peer], peer, group=self.group))
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+
+        def wait():
+            for r in reqs:
+                r.wait()
+        return wait
+
+
+class InProcessTransport:
+    """Emulates W ranks inside one process (single-GPU tests): every
+    engine's packed buffer is visible to every other."""
+
+    def __init__(self, rank, registry: dict, use_of: dict):
+        self.rank, self.registry, self.use_of = rank, registry, use_of
+
+    def __call__(self, send: torch.Tensor, slots):
+        use = self.use_of[send.data_ptr()]
+
+        def wait():
+            for r, slot in enumerate(slots):
+                slot.copy_(self.registry[r][use])
+        return wait
+
+
+class HostStagedTransport:
+    """All-gather-v of device buffers over a CPU backend (gloo): stage through
+    host memory.  Used to run several ranks on ONE GPU in tests (NCCL refuses
+    two ranks on the same device); blocking."""
+
+    def __init__(self, rank, world, group=None):
+        self.rank, self.world, self.group = rank, world, group
+
+    def __call__(self, send: torch.Tensor, slots):
+        import torch.distributed as dist
+        host = send.cpu()
+        recv = [torch.empty(int(sl.numel()), dtype=sl.dtype) for sl in slots]
+        recv[self.rank] = host
+        ops = []
+        for peer in range(self.world):
+            if peer != self.rank:
+                ops.append(dist.P2POp(dist.isend, host, peer, group=self.group))
+                ops.append(dist.P2POp(dist.irecv, recv[peer], peer, group=self.group))
+        for r in (dist.batch_isend_irecv(ops) if ops else []):
+            r.wait()
+        for sl, h in zip(slots, recv):
+            sl.copy_(h)
+        return lambda: None
+
+
+def allgather_v(send: torch.Tensor, sizes, group=None) -> list:
+    """Generic all-gather of unevenly sized 1-D tensors via grouped P2P
+    (works on NCCL/CUDA and gloo/CPU); returns one tensor per rank."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    out = [torch.empty(int(n), dtype=send.dtype, device=send.device) for n in sizes]
+    out[rank].copy_(send)
+    ops = []
+    for peer in range(world):
+        if peer != rank:
+            ops.append(dist.P2POp(dist.isend, send, peer, group=group))
+            ops.append(dist.P2POp(dist.irecv, out[peer], peer, group=group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    return out
+
+
+def build_sharded_engines(inst, world: int, by_cost: bool = True):
+    """Single-process construction of W sharded engines wired through
+    `InProcessTransport` (tests / simulation); returns (engines, topology)."""
+    from .engine import USES, SparseLayerEngine
+    topo = sharding_for(inst, world, by_cost)
+    shards = {"x": topo.vol_rows, "y": topo.img_rows}
+    registry, engines = {}, []
+    for r in range(world):
+        eng = SparseLayerEngine(inst.part_vol, inst.part_img, inst.plan_rows, inst.weights,
+                                inst.params, shard={"x": shards["x"][r], "y": shards["y"][r]})
+        use_of = {}
+        tr = InProcessTransport(r, registry, use_of)
+        ex = KVExchange(eng, r, world, shards, transport=tr, topology=topo)
+        registry[r] = ex.packed
+        for use in USES:
+            use_of[ex.packed[use].data_ptr()] = use
+        eng.exchange = ex
+        engines.append(eng)
+    return engines, topo
+
+
+def sharding_for(inst, world: int, by_cost: bool = True) -> WorkerTopology:
+    """Token-LPT (reference rule) or routed-workload LPT for an instance."""
+    if not by_cost:
+        return shard_blocks(inst.part_vol, inst.part_img, world)
+    from .engine import USES
+    lengths = {}
+    for use in USES:
+        rows, cnt = inst.plan_rows[use]
+        pk = inst.part_vol if use[2] == "v" else inst.part_img
+        r, c = D.host(rows), D.host(cnt)
+        occ = pk.occupancy.astype(np.float64)
+        mask = np.arange(r.shape[1])[None, :] < c[:, None]
+        lengths[use] = np.where(mask, occ[np.clip(r, 0, None)], 0.0).sum(axis=1)
+    cv, ci = block_costs(inst.part_vol, inst.part_img, lengths)
+    return shard_blocks_by_cost(inst.part_vol, inst.part_img, world, cv, ci)
+
+
+class ShardedLayer:
+    """One rank's share of the LSRM sparse-attention layer under block-aware
+    sequence parallelism (the device counterpart of `_run_use` /
+    `parallel_sparse_stage`, `lsrm/seq_parallel.py:260-434`).
+
+    The rank owns whole query blocks (`topology`), computes K/V for the
+    blocks it owns, all-gathers them per use and attends its own queries.
+    `step()` replays two CUDA graphs around the exchange: A = projections +
+    the four KV shards, B = placement + attention + W_o of the four uses.
+    """
+
+    def __init__(self, inst, rank: int, world: int, topology: WorkerTopology = None,
+                 transport=None, by_cost: bool = True):
+        from .engine import SparseLayerEngine
+        self.inst, self.rank, self.world = inst, rank, world
+        self.topology = topology or sharding_for(inst, world, by_cost)
+        shards = {"x": self.topology.vol_rows, "y": self.topology.img_rows}
+        self.engine = SparseLayerEngine(inst.part_vol, inst.part_img, inst.plan_rows,
+                                        inst.weights, inst.params,
+                                        shard={"x": shards["x"][rank], "y": shards["y"][rank]})
+        self.exchange = KVExchange(self.engine, rank, world, shards, transport=transport)
+        self.engine.exchange = self.exchange
+        m = self.engine.meta
+        # reference token ids of this rank's local rows, per stream
+        self.tok_host = {s: m[s].part.block_token_ids[D.host(m[s].loc2glob)]
+                         for s in ("x", "y")}
+        self.graphs = None
+
+    @property
+    def n_local(self) -> int:
+        return self.engine.meta["x"].n_loc + self.engine.meta["y"].n_loc
+
+    def local_inputs(self, x_hat: np.ndarray, y_hat: np.ndarray):
+        """Token-order f32 host features -> this rank's rows, local order, bf16."""
+        from . import _ops
+        return [_ops.cast(D.dev(np.ascontiguousarray(a[self.tok_host[s]], np.float32)),
+                          torch.bfloat16) for s, a in (("x", x_hat), ("y", y_hat))]
+
+    def forward(self, x_loc, y_loc) -> dict:
+        """Eager: use -> [Nq_loc, d] bf16 in local order."""
+        return self.engine.forward(x_loc, y_loc)
+
+    def _phase_b(self):
+        from .engine import USES
+        for use in USES:
+            self.exchange.place(self.engine, use)
+            self.engine.finish_kv(use)
+            self.engine.attend(use)
+            self.engine.output(use)
+
+    def capture(self, x_loc, y_loc):
+        """Record graphs A and B over fixed input buffers x_loc, y_loc."""
+        self._gin = (x_loc, y_loc)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):              # warm-up outside capture
+            self.forward(x_loc, y_loc)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        ga, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ga):
+            self.engine.forward_local(x_loc, y_loc)
+        with torch.cuda.graph(gb):
+            self._phase_b()
+        self.graphs = (ga, gb)
+
+    def step(self) -> dict:
+        """Graph A -> four exchanges (all in flight) -> graph B."""
+        from .engine import USES
+        ga, gb = self.graphs
+        ga.replay()
+        waits = [self.exchange.start(u) for u in USES]
+        for w in waits:
+            w()
+        gb.replay()
+        return {u: self.engine.buf[("out", u)] for u in USES}
+
+    def outputs_token_order(self, outs: dict) -> dict:
+        """(host) use -> (token ids, [Nq_loc, d] f32) for gathering on rank 0."""
+        from .engine import USE_GEOM
+        return {u: (self.tok_host[USE_GEOM[u][0]], D.host(o.float())) for u, o in outs.items()}
+
+    def attention_ms(self, reps: int = 5) -> float:
+        """Device time of this rank's four attention launches (events on the
+        launching stream; KV already placed by the last step)."""
+        from .engine import USES
+        st = torch.cuda.current_stream()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(st)
+        for _ in range(reps):
+            for use in USES:
+                self.engine.attend(use)
+        b.record(st)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    def time_host_path(self, x_hat, y_hat, steps: int = 5):
+        """End to end on this rank: pinned host rows -> H2D -> cast -> layer
+        (graphs + exchange) -> cast -> D2H.  Returns (mean ms, h2d, d2h bytes)."""
+        from . import _ops
+        from .engine import USES
+        xs = torch.from_numpy(np.ascontiguousarray(x_hat[self.tok_host["x"]], np.float32)).pin_memory()
+        ys = torch.from_numpy(np.ascontiguousarray(y_hat[self.tok_host["y"]], np.float32)).pin_memory()
+        x32, y32 = D.empty(tuple(xs.shape), torch.float32), D.empty(tuple(ys.shape), torch.float32)
+        xb, yb = self._gin
+        outs = self.engine.buf
+        pinned = {u: torch.empty(tuple(outs[("out", u)].shape), dtype=torch.float32,
+                                 pin_memory=True) for u in USES}
+
+        def once():
+            x32.copy_(xs, non_blocking=True)
+            y32.copy_(ys, non_blocking=True)
+            if x32.numel():
+                xb.copy_(_ops.cast(x32, torch.bfloat16))
+            if y32.numel():
+                yb.copy_(_ops.cast(y32, torch.bfloat16))
+            res = self.step()
+            for u in USES:
+                if res[u].numel():
+                    pinned[u].copy_(_ops.cast(res[u], torch.float32), non_blocking=True)
+
+        once()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(steps):
+            once()
+        b.record(st)
+        torch.cuda.synchronize()
+        h2d = (xs.numel() + ys.numel()) * 4
+        d2h = sum(p.numel() * 4 for p in pinned.values())
+        return a.elapsed_time(b) / steps, h2d, d2h
