@@ -202,8 +202,8 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference fixture geometry, tagged Philox features/weights)",
-            "config": {"workload": "C3 fine stage (16 views, S_vol=S_img=96, heads 32/2/32, "
-                                   "d=1024), bounded query sample", "parallelism": "cpu"},
+            "config": {"workload": WORKLOAD_DESC["c3"], "parallelism": "cpu (host cores)",
+                       "sample": desc},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": hi["cpu_count"],
                              "kind": "port", "sample": desc, "host": hi},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,

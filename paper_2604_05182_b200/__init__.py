@@ -14,7 +14,7 @@ from .tensor_core import AttentionParams
 from .tokenizer import (PosEmbed, TokenSet, foreground_patch_mask, informative_voxel_mask,
                         init_pos_embed, upsample_select_tokens)
 from .block_partition import (BlockPartition, CompressWeights, compress_block_kv,
-                              init_compress_weights, occupancy_stats, partition)
+                              init_compress_weights, occupancy_stats, partition, res_block)
 from .nsa_attention import (GatherTable, NsaWeights, Selection, build_gather_table,
                             cmp_attention, combine_nsa_branches, full_selection,
                             init_nsa_weights, nsa_cross_attention, nsa_gates,
@@ -23,5 +23,10 @@ from .nsa_attention import (GatherTable, NsaWeights, Selection, build_gather_tab
 from .block_routing import (RoutingBudgets, RoutingPlan, TokenCoords3D, build_routing_plan,
                             route_to_image_blocks, route_to_volume_blocks,
                             volume_token_coords, write_plan)
+
+from .seq_parallel import (TOKEN_COORD_BYTES, WorkerTopology, all_gather_kv, all_to_all,
+                           imbalance_report, makespan_ratio, message_log_to_csv,
+                           naive_contiguous_shards, naive_split_loads, shard_blocks,
+                           shard_blocks_by_cost)
 
 __version__ = "0.1.0"

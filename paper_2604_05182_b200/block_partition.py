@@ -164,6 +164,25 @@ def compress_rows(x, ld, n, width, params, part: BlockPartition, src_bf16=False,
     return out
 
 
+def res_block(x, p: ResBlockParams):
+    """x + W2·gelu(W1·x + b1) + b2 per row, f64 inside, f32 out
+    (`block_partition.py:112-124`).  x [N, w] -> [N, w]."""
+    on_dev = D.is_device(x)
+    xd = D.dev(x, torch.float32)
+    n, width = (int(s) for s in xd.shape)
+    if n == 0:
+        return xd.clone() if on_dev else np.zeros((0, width), np.float32)
+    scratch = D.empty((n, width), torch.float32)
+    one = D.empty((1, width), torch.float32)
+    ids = torch.arange(n, dtype=torch.int64, device=xd.device)
+    offs = D.dev(np.array([0, n], np.int64))
+    w1, b1, w2, b2 = _dev_res(p)
+    call("lsrm_compress_block", 0, xd.data_ptr(), width, n, width, w1.data_ptr(), b1.data_ptr(),
+         w2.data_ptr(), b2.data_ptr(), ids.data_ptr(), offs.data_ptr(), 1, one.data_ptr(),
+         scratch.data_ptr(), D.stream())
+    return scratch if on_dev else D.host(scratch)
+
+
 def compress_block_kv(k, v, part: BlockPartition, w: CompressWeights):
     """Per-token ResBlock then the in-block mean in ascending token order
     (`block_partition.py:147-167`).  k, v [N, h_kv, d_h] -> [B, h_kv, d_h]."""
