@@ -6,49 +6,49 @@
 // gated sum of combine_nsa_branches (lsrm/nsa_attention.py:84-112,157-207,
 // 266-284).  The W_o projection stays a plain GEMM.
 //
-// Work item = (query tile, kv head).  A query tile is up to T = 128/G
-// consecutive tokens of ONE query block (block-major order); the MMA
-// M-dimension is the 128 rows (token, q-head-in-group) sharing kv head h.
-// Each item streams key chunks of <= 128 keys, branch after branch:
+// Work item = (query tile, group of HP kv heads).  A query tile is up to
+// T = 128/G consecutive tokens of ONE query block (block-major order); per kv
+// head, the MMA M-dimension is the 128 rows (token, q-head-in-group).  Each
+// item streams key chunks of <= 128 keys, branch after branch:
 //   cmp : all compressed rows (one per occupied KV block),
 //   sel : the sorted union of the tile tokens' selected blocks; a row only
 //         sees the blocks ITS token selected (others masked out),
 //   win : the tile's own block (self uses).
+// The HP head-tiles of an item share the chunk plan but not K/V.
 //
-// Persistent, warp-specialised CTA (one per SM, 192 threads):
-//   warps 0-3  softmax/epilogue: thread = TMEM lane = one row; masked online
-//              softmax (exp2), bf16 P to smem, rescale-accumulate O in
-//              registers, gate + merge at branch ends;
-//   warp 4     producer: union of the tile's selections, chunk plans, and
-//              cp.async.bulk K/V copies (each KV block is one contiguous
-//              16-row-padded segment of the interleaved layout) into a
-//              2-stage ring;
-//   warp 5     MMA issuer: S = Q K^T into a double-buffered TMEM S, and
-//              O_part = P V into TMEM, in the order QK(j+1), PV(j) so the
-//              tensor core runs one chunk ahead of the softmax warps.
-// mbarriers: kv_full/kv_empty (ring), s_full (S ready), p_full (P written,
-// S slot free), o_full/o_empty (PV partial).  Phases follow a chunk counter
-// that all roles advance identically.
+// Persistent, warp-specialised CTA (one per SM, 32*(4*HP+2) threads):
+//   warps 4hh..4hh+3  softmax/epilogue of head-tile hh: thread = TMEM lane =
+//              one row and ALL keys of a chunk (no cross-warp exchange);
+//              masked online softmax (exp2), bf16 P written back into TMEM
+//              over S, PV partials absorbed into registers, gate + merge at
+//              branch ends (merge accumulator in TMEM);
+//   warp 4HP   producer: union of the tile's selections, chunk plans, and
+//              cp.async.bulk K/V copies of every head (each KV block is one
+//              contiguous 16-row-padded segment) into a 4-stage ring;
+//   warp 4HP+1 MMA issuer: per head-tile, PV(c) = P(c).[V|ones] (TS mode, P
+//              from TMEM) as soon as P(c) is written, then S(c+1) = Q K^T
+//              into the same columns.  The HP softmax warpgroups therefore
+//              run out of phase (ping-pong): one computes exponentials while
+//              the tensor core serves the other.
+// mbarriers: kv_full/kv_empty (ring), s_full (S ready), p_full (P written),
+// o_full/o_empty (double-buffered PV partial), q_full/q_empty.  Phases follow
+// a chunk counter that all roles advance identically.
 //
 // SMEM operand layout: 8x8 "core matrices" of 128 contiguous bytes,
 // SWIZZLE_NONE canonical layouts (cute mma_sm100_desc.hpp):
 //   K-major  Q, K, P : element (row, k) at (row/8)*RS + (k/8)*64 + (row%8)*8 + k%8
 //   MN-major V       : the same storage read with N = head dim, K = keys.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace lsrm {
 namespace tc {
 
-constexpr int kM = 128;          // MMA rows per tile
+constexpr int kM = 128;          // MMA rows per head-tile
 constexpr int kNK = 128;         // keys per chunk
 constexpr int kGroups = kNK / 16;
-constexpr int kParts = 4;                    // softmax warps per TMEM lane quadrant
-constexpr int kSoftThreads = 128 * kParts;   // softmax warps 0 .. 4*kParts-1
-constexpr int kProducerWarp = 4 * kParts, kMmaWarp = 4 * kParts + 1;
-constexpr int kThreads = kSoftThreads + 64;
-constexpr int kTmemCols = 512;   // S0 [0,128) S1 [128,256) O [256, 256+DH)
 constexpr int kMaxEnt = 256;     // tile tokens * selected rows
-constexpr int kMaxPieces = kNK / 16;
 
 __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
@@ -80,11 +80,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@P1 bra DONE;\n\t"
       "bra LAB_WAIT;\n\t"
       "DONE:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x100000u)   // suspend (not spin) until the phase completes
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -188,7 +188,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 
 // Optional event trace (debug): CTA 0 stamps clock64() per chunk and event.
 __device__ long long* g_trace = nullptr;
-constexpr int kTraceEv = 8, kTraceChunks = 1024;
+constexpr int kTraceEv = 16, kTraceChunks = 512;
 __device__ __forceinline__ void trace(long long* tr, uint32_t c, int ev) {
   if (tr && c < (uint32_t)kTraceChunks) tr[c * kTraceEv + ev] = clock64();
 }
@@ -218,7 +218,7 @@ struct Params {
   __nv_bfloat16* out;
 };
 
-constexpr int kStages = 6;       // K/V ring depth
+constexpr int kStages = 4;       // K/V ring depth (each stage holds every head of the item)
 constexpr int kOnesCols = 16;    // extra V columns holding 1 (valid key) / 0 (padding)
 constexpr int kBitmapWords = 512;  // union bitmap: up to 16384 occupied KV blocks
 
@@ -230,86 +230,165 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t 
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
+// 32 consecutive f32 columns of this thread's TMEM lane (no wait).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
+
+// in-place mask of 16 logits (keys j >= lim get -inf) and their maximum
+__device__ __forceinline__ void mask16(uint32_t* s, int lim) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) s[j] = j < lim ? s[j] : 0xff800000u;
+}
+__device__ __forceinline__ float max16(const uint32_t* s) {
+  const float* x = reinterpret_cast<const float*>(s);
+  float a = fmaxf(fmaxf(x[0], x[1]), x[2]), b = fmaxf(fmaxf(x[3], x[4]), x[5]);
+  float d = fmaxf(fmaxf(x[6], x[7]), x[8]), e = fmaxf(fmaxf(x[9], x[10]), x[11]);
+  float f = fmaxf(fmaxf(x[12], x[13]), x[14]);
+  a = fmaxf(fmaxf(a, b), d);
+  e = fmaxf(fmaxf(e, f), x[15]);
+  return fmaxf(a, e);
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 16 logits -> 8 words of packed bf16 exp2(s * sl2 + nb)
+__device__ __forceinline__ void exp16(const uint32_t* s, float sl2, float nb, uint32_t* w) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    w[j] = pack_bf16(ex2(fmaf(__uint_as_float(s[2 * j]), sl2, nb)),
+                     ex2(fmaf(__uint_as_float(s[2 * j + 1]), sl2, nb)));
+}
+__device__ __forceinline__ void zero8(uint32_t* w) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w[j] = 0u;
+}
 
 // One chunk of <= 128 keys as the softmax and MMA warps see it.  The
 // producer resolves visibility per 16-key group: gnv = valid keys in the
 // group, gmask = tile tokens allowed to see it.
-struct ChunkDesc {
-  uint32_t gmask[kGroups];
-  int32_t gnv[kGroups];
-  int ncols, branch;
-  int first_in_branch, last_in_branch, first_in_item, last_in_item, last_overall;
-  int q_first, q_cnt, h, qb, item_seq;
+struct __align__(16) ChunkDesc {
+  int ncols, branch, flags, q_first;   // flags: kF* bits | tail-group mask << 8
+  int q_cnt, h, qb, item_seq;
+  uint32_t gmask[kGroups];             // producer scratch: tokens allowed per group
+  int32_t gnv[kGroups];                // valid keys per group (tail groups: < 16)
+  uint8_t tokvis[32];                  // per tile token: groups it sees (bit g)
 };
+constexpr int kFFirstBranch = 1, kFLastBranch = 2, kFFirstItem = 4, kFLastItem = 8,
+              kFLastOverall = 16;
 
+// TMEM columns of one head-tile: S (f32 logits), P (bf16 packed), the branch
+// accumulator [O | rowsum] of P.[V | ones], and the gated merge (f16 packed).
 template <int DH>
+struct HeadCols {
+  static constexpr int VW = DH + kOnesCols;
+  static constexpr uint32_t kS = 0, kP = kNK, kO = kNK + kNK / 2, kMerged = kO + VW;
+  static constexpr int kTotal = kNK + kNK / 2 + VW + DH / 2;
+};
+template <int DH, int HP>
+constexpr int tmem_alloc_cols() {
+  int n = HP * HeadCols<DH>::kTotal, a = 32;
+  while (a < n) a *= 2;
+  return a;
+}
+
+template <int DH, int HP>
 struct Smem {
-  __nv_bfloat16 q[2][kM * DH];
-  __nv_bfloat16 k[kStages][kNK * DH];
-  __nv_bfloat16 v[kStages][kNK * (DH + kOnesCols)];   // [V | ones] rows
-  float merged[kM][DH + 1];
-  float xmax[2][kParts][kM];    // per-part partial row maxima (chunk parity)
-  int32_t ent[kMaxEnt];         // selected rows of the tile tokens, [t][kmax]
+  __nv_bfloat16 q[2][HP][kM * DH];
+  __nv_bfloat16 k[kStages][HP][kNK * DH];
+  __nv_bfloat16 v[kStages][HP][kNK * (DH + kOnesCols)];   // [V | ones] rows
+  __nv_bfloat16 gate[HP][kM * DH];  // per row: gate logits of the branch that just ended
+  int32_t ent[kMaxEnt];          // selected rows of the tile tokens, [t][kmax]
   uint32_t bitmap[kBitmapWords]; // selected-row bitmap of the current item
   int32_t wpre[kBitmapWords];    // rank of the first set bit of each word
   int32_t uni_row[kMaxEnt];      // sorted union of selected rows
-  uint32_t uni_mask[kMaxEnt];   // per union slot: tokens that selected it
-  int64_t seg_lo[kMaxEnt + 1];  // per union slot (+1: own block) padded first row
+  uint32_t uni_mask[kMaxEnt];    // per union slot: tokens that selected it
+  int64_t seg_lo[kMaxEnt + 1];   // per union slot (+1: own block) padded first row
   int32_t seg_plen[kMaxEnt + 1];
   int32_t seg_occ[kMaxEnt + 1];
   int32_t seg_cum[kMaxEnt];
   ChunkDesc desc[kStages];
-  uint64_t kv_full[kStages], kv_empty[kStages], s_full[2], p_full[2], o_full[2], o_empty[2],
+  uint64_t kv_full[kStages], kv_empty[kStages], s_full[HP], s_free[HP], p_full[HP], o_full[HP],
       q_full[2], q_empty[2];
   uint32_t tmem_base;
 };
 
-template <int DH>
-__global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
+template <int HP>
+constexpr int threads_of() { return 32 * (4 * HP + 2); }
+
+// Work item = (query tile, group of HP kv heads).  The HP head-tiles share the
+// chunk plan (same tokens, same union of selected blocks) but not K/V, so
+// their softmax warpgroups run out of phase: while one computes
+// exponentials, the tensor core serves the other (ping-pong).
+//
+// Warps: 4*HP softmax (warpgroup hh = head-tile hh; thread = TMEM lane = one
+// row, all 128 keys of a chunk, so no cross-warp max exchange), 1 producer,
+// 1 MMA issuer.
+template <int DH, int HP>
+__global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  Smem<DH>& S = *reinterpret_cast<Smem<DH>*>(smem_raw);
+  Smem<DH, HP>& S = *reinterpret_cast<Smem<DH, HP>*>(smem_raw);
+  using HCols = HeadCols<DH>;
+  constexpr int VW = HCols::VW, HC = HCols::kTotal;
+  constexpr int kSoftWarps = 4 * HP, kProducerWarp = kSoftWarps, kMmaWarp = kSoftWarps + 1;
+  constexpr int kAlloc = tmem_alloc_cols<DH, HP>();
+  static_assert(kAlloc <= 512, "TMEM budget");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = P.hq / P.hkv, T = kM / G;
   const int d_model = P.hq * DH;
-  const int64_t n_items = P.n_tiles * P.hkv;
+  const int n_hgroups = P.hkv / HP;
+  const int64_t n_items = P.n_tiles * n_hgroups;
   if ((int64_t)blockIdx.x >= n_items) return;
-  // TMEM columns: S slots [0,128) [128,256); O/L double-buffered per chunk parity
-  // P(c) (bf16x2 packed, 64 columns) aliases the upper half of S slot c&1:
-  // every part has loaded its S values before the max-exchange barrier, and
-  // QK(c+2) is issued after PV(c) in the in-order tensor pipe.
-  constexpr int VW = DH + kOnesCols;   // V row width incl. the ones columns
-  constexpr uint32_t kColO = 2 * kNK, kColP = kNK / 2;   // O|L slots: kColO + parity * VW
 
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&S.kv_full[i], 1);
       mbar_init(&S.kv_empty[i], 1);
     }
+    for (int hh = 0; hh < HP; ++hh) {
+      mbar_init(&S.s_full[hh], 1);
+      mbar_init(&S.s_free[hh], 128);
+      mbar_init(&S.p_full[hh], 128);
+      mbar_init(&S.o_full[hh], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&S.s_full[i], 1);
-      mbar_init(&S.p_full[i], kSoftThreads);
       mbar_init(&S.q_full[i], 1);
       mbar_init(&S.q_empty[i], 1);
-      mbar_init(&S.o_full[i], 1);
-      mbar_init(&S.o_empty[i], kSoftThreads);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&S.tmem_base)),
-                 "r"(kTmemCols));
+                 "r"(kAlloc));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (warp < 4)
-    for (int c = 0; c < DH; ++c) S.merged[tid][c] = 0.f;  // warps 0-3 cover all rows
-  for (int i = tid; i < kBitmapWords; i += kThreads) S.bitmap[i] = 0u;
+  for (int i = tid; i < kBitmapWords; i += blockDim.x) S.bitmap[i] = 0u;
   fence_async_smem();
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
   const uint32_t tmem = S.tmem_base;
-  const uint32_t row_bytes_kv = DH * 2;
   long long* const trp = blockIdx.x == 0 ? g_trace : nullptr;  // debug event trace
 
   if (warp == kProducerWarp) {
@@ -318,13 +397,12 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
     int it = 0;
     const uint32_t all_tok = T >= 32 ? 0xffffffffu : ((1u << T) - 1u);
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const int tile = (int)(item / P.hkv), h = (int)(item % P.hkv);
+      const int tile = (int)(item / n_hgroups), h0 = (int)(item % n_hgroups) * HP;
       const int q_first = P.tiles[4 * tile], q_cnt = P.tiles[4 * tile + 1],
                 own = P.tiles[4 * tile + 2];
       const bool last_item = item + gridDim.x >= n_items;
       const int qb = it & 1;
-      // ---- selected rows of the tile tokens (resolved rows are -1 padded,
-      //      so no dependent load of `count`) -> bitmap; they overlap Q
+      // ---- selected rows of the tile tokens (resolved rows are -1 padded)
       const int n_ent = T * P.kmax, n_valid_ent = q_cnt * P.kmax;
       const int32_t* rows_t = P.rows + (int64_t)q_first * P.kmax;
       for (int i = lane; i < n_ent; i += 32) {
@@ -332,24 +410,27 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
         S.ent[i] = r;
         if (r >= 0) atomicOr(&S.bitmap[r >> 5], 1u << (r & 31));
       }
-      // ---- Q tile -> sQ[qb] (cp.async, zero-filled past the tile), once the
-      //      MMAs of item it-2 are done with the buffer
+      // ---- Q tiles of the HP heads -> sQ[qb] (cp.async, zero-filled past the
+      //      tile), once the MMAs of item it-2 are done with the buffer
       if (it >= 2) mbar_wait(&S.q_empty[qb], ((it >> 1) - 1) & 1);
-#pragma unroll
-      for (int i = lane; i < kM * (DH / 8); i += 32) {
-        const int m = i / (DH / 8), cc = i % (DH / 8);
+      constexpr int kQChunks = kM * (DH / 8);
+#pragma unroll 4
+      for (int i = lane; i < HP * kQChunks; i += 32) {
+        const int hh = i / kQChunks, rem = i % kQChunks;
+        const int m = rem / (DH / 8), cc = rem % (DH / 8);
         const int tt = m / G, gg = m % G;
         const bool ok = tt < q_cnt;
         const __nv_bfloat16* src =
-            P.q + (ok ? (int64_t)(q_first + tt) * P.ld_q + (h * G + gg) * DH + cc * 8 : 0);
-        cp_async16(&S.q[qb][(m / 8) * (8 * DH) + cc * 64 + (m % 8) * 8], src, ok ? 16u : 0u);
+            P.q + (ok ? (int64_t)(q_first + tt) * P.ld_q + ((h0 + hh) * G + gg) * DH + cc * 8
+                      : 0);
+        cp_async16(&S.q[qb][hh][(m / 8) * (8 * DH) + cc * 64 + (m % 8) * 8], src,
+                   ok ? 16u : 0u);
       }
       cp_async_wait_all();
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.q_full[qb]);
-      // ---- sorted union = set bits of the bitmap in order; lane l owns a
-      //      contiguous run of words, ranks by a warp prefix of popcounts
+      // ---- sorted union = set bits of the bitmap in order
       const int n_words = (int)((P.n_blocks + 31) / 32);
       const int per_w = (n_words + 31) / 32;
       int cnt_w = 0;
@@ -380,8 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
         }
       }
       __syncwarp();
-      // token masks: entry i belongs to token i / kmax
-      for (int i = lane; i < n_ent; i += 32) {
+      for (int i = lane; i < n_ent; i += 32) {   // token masks: entry i is token i / kmax
         const int r = S.ent[i];
         if (r >= 0) {
           const int w = r >> 5;
@@ -389,8 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
           atomicOr(&S.uni_mask[rank], 1u << (i / P.kmax));
         }
       }
-      // segment geometry of every union slot (independent loads, all lanes)
-      for (int u = lane; u < nu; u += 32) {
+      for (int u = lane; u < nu; u += 32) {   // segment geometry of every union slot
         const int r = S.uni_row[u];
         const int64_t a0 = P.pad_off[r], a1 = P.pad_off[r + 1];
         const int64_t b0 = P.kv_off[r], b1 = P.kv_off[r + 1];
@@ -411,8 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
         if (w < n_words) S.bitmap[w] = 0u;
       }
       __syncwarp();
-      // exclusive prefix of the union segments' padded lengths (sel branch)
-      int total_sel;
+      int total_sel;   // exclusive prefix of the union segments' padded lengths
       {
         const int per = (nu + 31) / 32;
         int local = 0;
@@ -439,14 +517,14 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
       // ---- chunk j of a branch = keys [128j, 128j+128) of the concatenation
       //      of its 16-row-padded segments; lane i turns the i-th overlapping
       //      segment into a piece, fills its groups' visibility and issues the
-      //      piece's K and V bulk copies
+      //      piece's K and V bulk copies for every head of the item
       const int64_t cmp_rows = (P.n_blocks + 15) / 16 * 16;
       for (int br = 0; br < P.n_gates; ++br) {
         const int n_seg = br == 1 ? nu : 1;
         const int64_t total = br == 0 ? cmp_rows : (br == 1 ? total_sel : S.seg_plen[kMaxEnt]);
         const int64_t head_rows = br == 0 ? cmp_rows : P.n_rows_pad;
-        const __nv_bfloat16* kb = (br == 0 ? P.kc_il : P.k_il) + (int64_t)h * head_rows * DH;
-        const __nv_bfloat16* vb = (br == 0 ? P.vc_il : P.v_il) + (int64_t)h * head_rows * VW;
+        const __nv_bfloat16* kb = (br == 0 ? P.kc_il : P.k_il) + (int64_t)h0 * head_rows * DH;
+        const __nv_bfloat16* vb = (br == 0 ? P.vc_il : P.v_il) + (int64_t)h0 * head_rows * VW;
         int cur = 0;
         for (int64_t start = 0; start < total; start += kNK) {
           const int64_t end = lmin(start + kNK, total);
@@ -487,27 +565,44 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
               D.gmask[gi] = tm;
             }
           }
+          __syncwarp();
+          const int n_grp = (int)(end - start) / 16;
           if (lane == 0) {
+            uint32_t tail = 0;
+            for (int gi = 0; gi < n_grp; ++gi)
+              if (D.gnv[gi] > 0 && D.gnv[gi] < 16) tail |= 1u << gi;
+            const bool li = end == total && br == P.n_gates - 1;
             D.ncols = (int)(end - start);
             D.branch = br;
-            D.first_in_branch = start == 0;
-            D.last_in_branch = end == total;
-            D.first_in_item = br == 0 && start == 0;
-            D.last_in_item = end == total && br == P.n_gates - 1;
-            D.last_overall = D.last_in_item && last_item;
+            D.flags = (start == 0 ? kFFirstBranch : 0) | (end == total ? kFLastBranch : 0) |
+                      (br == 0 && start == 0 ? kFFirstItem : 0) | (li ? kFLastItem : 0) |
+                      (li && last_item ? kFLastOverall : 0) | (int)(tail << 8);
             D.q_first = q_first;
             D.q_cnt = q_cnt;
-            D.h = h;
+            D.h = h0;
             D.qb = qb;
             D.item_seq = it;
           }
+          {   // per token: the groups it sees (padding rows of the tile see none)
+            uint32_t v = 0;
+            if (lane < q_cnt)
+              for (int gi = 0; gi < n_grp; ++gi)
+                if (D.gnv[gi] > 0 && ((D.gmask[gi] >> lane) & 1u)) v |= 1u << gi;
+            D.tokvis[lane] = (uint8_t)v;
+          }
           __syncwarp();
           if (lane == 0)
-            mbar_expect_tx(&S.kv_full[st], (uint32_t)(end - start) * (row_bytes_kv + 2u * VW));
+            mbar_expect_tx(&S.kv_full[st],
+                           (uint32_t)(end - start) * HP * (uint32_t)(2 * DH + 2 * VW));
           __syncwarp();
           if (ov) {
-            bulk_g2s(&S.k[st][col * DH], kb + src * DH, ncols * row_bytes_kv, &S.kv_full[st]);
-            bulk_g2s(&S.v[st][col * VW], vb + src * VW, ncols * 2u * VW, &S.kv_full[st]);
+#pragma unroll
+            for (int hh = 0; hh < HP; ++hh) {
+              bulk_g2s(&S.k[st][hh][col * DH], kb + ((int64_t)hh * head_rows + src) * DH,
+                       ncols * DH * 2u, &S.kv_full[st]);
+              bulk_g2s(&S.v[st][hh][col * VW], vb + ((int64_t)hh * head_rows + src) * VW,
+                       ncols * VW * 2u, &S.kv_full[st]);
+            }
           }
           cur += __popc(__ballot_sync(0xffffffffu, done));
           ++c;
@@ -517,284 +612,331 @@ __global__ void __launch_bounds__(kThreads, 1) nsa_fused_kernel(Params P) {
     }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (warp converged; one elected lane issues)
-    {
-      const uint32_t id_pv = idesc_bf16(kM, VW, 1);   // O | rowsum = P . [V | ones]
-      // S = Q K^T for chunk cc into TMEM S slot cc&1
-      auto issue_qk = [&](uint32_t cc) {
-        const int st = cc % kStages;
+    const uint32_t id_pv = idesc_bf16(kM, VW, 1);   // [O | rowsum] += P . [V | ones]
+    // S_hh = Q_hh K_hh^T for chunk cc into head-tile hh's S columns
+    auto issue_qk = [&](uint32_t cc, int hh) {
+      const int st = cc % kStages;
+      const ChunkDesc& D = S.desc[st];
+      if (hh == 0) {
         mbar_wait(&S.kv_full[st], (cc / kStages) & 1);
+#ifndef LSRM_TRACE_LD
         if (lane == 0) trace(trp, cc, 1);
-        const ChunkDesc& D = S.desc[st];
-        if (D.first_in_item) mbar_wait(&S.q_full[D.qb], (D.item_seq >> 1) & 1);
-        tc_after_sync();
-        const uint32_t id = idesc_bf16(kM, D.ncols, 0);
-        const uint64_t a0 = sdesc(smem_u32(S.q[D.qb]), 128, 16 * DH);
-        const uint64_t b0 = sdesc(smem_u32(S.k[st]), 128, 16 * DH);
-        if (elect_one_sync()) {
+#endif
+        if (D.flags & kFFirstItem) mbar_wait(&S.q_full[D.qb], (D.item_seq >> 1) & 1);
+      }
+      tc_after_sync();
+      const uint32_t id = idesc_bf16(kM, D.ncols, 0);
+      const uint64_t a0 = sdesc(smem_u32(S.q[D.qb][hh]), 128, 16 * DH);
+      const uint64_t b0 = sdesc(smem_u32(S.k[st][hh]), 128, 16 * DH);
+      if (elect_one_sync()) {
 #pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk)
-            mma_bf16(tmem + (cc & 1) * kNK, a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16),
-                     id, kk > 0);
-          mma_commit(&S.s_full[cc & 1]);
+        for (int kk = 0; kk < DH / 16; ++kk)
+          mma_bf16(tmem + hh * HC + HCols::kS, a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16),
+                   id, kk > 0);
+        mma_commit(&S.s_full[hh]);
+      }
+      __syncwarp();
+      if (lane == 0 && hh == 0) trace(trp, cc, 2);
+    };
+#pragma unroll
+    for (int hh = 0; hh < HP; ++hh) issue_qk(0, hh);
+    // per chunk: S(c+1) = Q K^T as soon as the softmax has S(c) in registers
+    // (s_free), then PV(c) accumulates P(c).[V|ones] into the branch's O as
+    // soon as P(c) is written (p_full)
+    uint32_t c = 0;
+    for (;;) {
+      const int st = c % kStages;
+      const ChunkDesc& D = S.desc[st];
+      const int fl = D.flags;
+      const bool last = fl & kFLastOverall, last_in_item = fl & kFLastItem;
+      const uint32_t acc0 = (fl & kFFirstBranch) ? 0u : 1u;
+      const int nk = D.ncols / 16;
+      const int qb = D.qb;
+      if (!last) {
+#pragma unroll
+        for (int hh = 0; hh < HP; ++hh) {
+          mbar_wait(&S.s_free[hh], c & 1);
+          issue_qk(c + 1, hh);
         }
-        __syncwarp();
-        if (lane == 0) trace(trp, cc, 2);
-      };
-      // QK runs two chunks ahead: QK(c+2) reuses S slot c&1 once the softmax
-      // of chunk c has released it; it is issued right after PV(c)
-      uint32_t c = 0;
-      issue_qk(0);
-      bool ahead = !S.desc[0].last_overall;  // is there a chunk 1?
-      if (ahead) issue_qk(1);
-      uint32_t next_qk = ahead ? 2 : 1;
-      bool more = ahead && !S.desc[1 % kStages].last_overall;
-      for (;;) {
-        const int st = c % kStages;
-        const ChunkDesc& D = S.desc[st];
-        const bool last = D.last_overall;
-        const int nk = D.ncols / 16;
-        const bool last_in_item = D.last_in_item;
-        const int qb = D.qb;
-        mbar_wait(&S.p_full[c & 1], (c >> 1) & 1);
-        if (lane == 0) trace(trp, c, 5);
-        // [O | rowsum](c) = P V' into the O slot of parity c&1 (absorbed two
-        // chunks ago: no wait on the previous chunk's absorb)
-        if (c >= 2) mbar_wait(&S.o_empty[c & 1], ((c >> 1) - 1) & 1);
+      }
+#pragma unroll
+      for (int hh = 0; hh < HP; ++hh) {
+        mbar_wait(&S.p_full[hh], c & 1);
+        if (lane == 0 && hh == 0) trace(trp, c, 5);
         tc_after_sync();
-        const uint32_t pa = tmem + (c & 1) * kNK + kColP;   // P(c): packed bf16 in TMEM
-        const uint64_t vb = sdesc(smem_u32(S.v[st]), 16 * VW, 128);
-        const uint32_t to = tmem + kColO + (c & 1) * VW;
+        const uint32_t pa = tmem + hh * HC + HCols::kP;
+        const uint64_t vdesc = sdesc(smem_u32(S.v[st][hh]), 16 * VW, 128);
+        const uint32_t to = tmem + hh * HC + HCols::kO;
         if (elect_one_sync()) {
 #pragma unroll
           for (int kk = 0; kk < kGroups; ++kk)
-            if (kk < nk) mma_bf16_ts(to, pa + kk * 8, vb + (uint64_t)(kk * 2 * VW), id_pv, kk > 0);
-          mma_commit(&S.o_full[c & 1]);
-          if (last_in_item) mma_commit(&S.q_empty[qb]);
-          mma_commit(&S.kv_empty[st]);
+            if (kk < nk)
+              mma_bf16_ts(to, pa + kk * 8, vdesc + (uint64_t)(kk * 2 * VW), id_pv,
+                          kk > 0 ? 1u : acc0);
+          mma_commit(&S.o_full[hh]);
+          if (hh == HP - 1) {
+            if (last_in_item) mma_commit(&S.q_empty[qb]);
+            mma_commit(&S.kv_empty[st]);
+          }
         }
         __syncwarp();
-        if (lane == 0) trace(trp, c, 6);
-        if (more) {
-          issue_qk(next_qk);
-          more = !S.desc[next_qk % kStages].last_overall;
-          ++next_qk;
-        }
-        ++c;
-        if (last) break;
+        if (lane == 0 && hh == 0) trace(trp, c, 6);
       }
+      ++c;
+      if (last) break;
     }
     __syncwarp();
   } else {
-    // ===================== softmax / epilogue (warps 0 .. 4*kParts-1)
-    // kParts warps per TMEM lane quadrant: warps q, q+4, q+8, ... share rows
-    // 32q..32q+31; part p takes key groups [p*HG, (p+1)*HG) and O columns
-    // [p*HD, (p+1)*HD).  Row maxima are exchanged through smem (named barrier
-    // per quadrant); row sums come from the tensor core (P . ones).
-    constexpr int HG = kGroups / kParts, HD = DH / kParts;
-    const int q4 = warp & 3, half = warp >> 2;   // half == part index
+    // ===================== softmax / epilogue (warpgroup hh = head-tile hh)
+    const int hh = warp >> 2, q4 = warp & 3;
     const int m = q4 * 32 + lane;
     const int t = m / G, g_in = m % G;
-    const int bar_id = 1 + q4;
-    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tS = tmem + ((uint32_t)(q4 * 32) << 16) + hh * HC;
+    const uint32_t tP = tS + HCols::kP, tO = tS + HCols::kO, tM = tS + HCols::kMerged;
     const float sl2 = 1.4426950408889634f / sqrtf((float)DH);
-    float m_run = -__builtin_huge_valf(), l_acc = 0.f;
-    // state of the chunk whose PV partial is still in flight
-    float alpha_pend = 1.f;
-    int br_pend = 0, lastbr_pend = 0, lastit_pend = 0;
+    const float kNegInf = -__builtin_huge_valf();
+    // O accumulates in TMEM over a branch relative to the running max m_run;
+    // m_run only moves (and O is rescaled) when the chunk max exceeds it by
+    // more than 2^kHeadroom, so P <= 2^kHeadroom and rescales are rare.
+    constexpr float kHeadroom = 8.f;
+    float m_run = kNegInf;
+    // finished-branch state: its epilogue runs in the next chunk, before that
+    // chunk's PV overwrites O
+    int br_pend = 0, head_pend = 0;
+    bool lastit_pend = false, rowok_pend = false, epi_pend = false;
     int64_t tok_pend = 0;
-    bool rowok_pend = false;
-    int head_pend = 0;
-    uint4 gate_cur[HD / 8], gate_pend[HD / 8];   // gate logits, prefetched at branch start
-    float o[HD];
-#pragma unroll
-    for (int j = 0; j < HD; ++j) o[j] = 0.f;
+    __nv_bfloat16* const gate_s = &S.gate[hh][m * DH];   // this row's staged gate logits
     uint32_t c = 0;
-    bool have_pend = false;
-    // O_part / L_part of the previous chunk: o = o * alpha + O_part, same for l
-    auto absorb_pv = [&]() {
-      mbar_wait(&S.o_full[(c - 1) & 1], ((c - 1) >> 1) & 1);
-      if (tid == 0) trace(trp, c - 1, 7);
-      const uint32_t ps = (c - 1) & 1;  // O/L slot of the absorbed chunk
+
+    // gate + merge of a finished branch (nsa_attention.py:266-284); the
+    // running merge is f16 in TMEM; at an item end the merged row is stored
+    auto epilogue = [&](uint32_t pc) {
+      mbar_wait(&S.o_full[hh], pc & 1);   // PV(pc) complete
+      if (tid == 0) trace(trp, pc, 7);
       tc_after_sync();
-      uint32_t r[HD], rl[1];
-      tmem_ld_cols<HD>(tmem + lane_base + kColO + ps * VW + half * HD, r);
-      tmem_ld_cols<1>(tmem + lane_base + kColO + ps * VW + DH, rl);
+      cp_async_wait_all();                // gate logits staged by this thread
+      uint32_t rl[1];
+      tmem_ld_cols<1>(tO + DH, rl);
       tmem_wait_ld();
-      tc_before_sync();
-      mbar_arrive(&S.o_empty[ps]);
+      const float inv = rowok_pend ? 1.f / __uint_as_float(rl[0]) : 0.f;
+      const int64_t col0 = (int64_t)br_pend * d_model + head_pend * DH;
+      const float* bp = P.gbias ? P.gbias + col0 : nullptr;
 #pragma unroll
-      for (int j = 0; j < HD; ++j) o[j] = o[j] * alpha_pend + __uint_as_float(r[j]);
-      l_acc = l_acc * alpha_pend + __uint_as_float(rl[0]);
-      if (lastbr_pend) {
-        if (rowok_pend) {
-          // gate + merge the finished branch (nsa_attention.py:266-284)
-          const float inv = 1.f / l_acc;
-          const int64_t col0 = (int64_t)br_pend * d_model + head_pend * DH + half * HD;
-          const __nv_bfloat16* gp = P.gl + tok_pend * P.ld_gl + P.gcol0 + col0;
-          const float* bp = P.gbias ? P.gbias + col0 : nullptr;
-          (void)gp;
+      for (int c0 = 0; c0 < DH; c0 += 16) {   // 16 columns at a time (registers)
+        uint32_t r[16], mr[8];
+        tmem_ld16_nowait(tO + c0, r);
+        if (br_pend > 0) tmem_ld_cols<8>(tM + c0 / 2, mr);
+        tmem_wait_ld();
 #pragma unroll
-          for (int c0 = 0; c0 < HD; c0 += 8) {
-            uint4 raw = gate_pend[c0 / 8];
-            const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
+        for (int k8 = 0; k8 < 2; ++k8) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(gate_s + c0 + 8 * k8);
+          const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float z = __bfloat162float(hv[j]) + (bp ? bp[c0 + j] : 0.f);
-              float gate = 1.f / (1.f + __expf(-z));
-              S.merged[m][half * HD + c0 + j] += gate * (o[c0 + j] * inv);
+          for (int j = 0; j < 8; ++j) {
+            const int cj = 8 * k8 + j;
+            const float z = __bfloat162float(hv[j]) + (bp ? __ldg(bp + c0 + cj) : 0.f);
+            float v = rowok_pend ? __uint_as_float(r[cj]) * inv *
+                                       rcp_approx(1.f + ex2(-z * 1.4426950408889634f))
+                                 : 0.f;
+            if (br_pend > 0) {
+              const __half2 hm = *reinterpret_cast<const __half2*>(&mr[cj / 2]);
+              v += (cj & 1) ? __high2float(hm) : __low2float(hm);
             }
+            r[cj] = __float_as_uint(v);
           }
         }
-#pragma unroll
-        for (int j = 0; j < HD; ++j) o[j] = 0.f;
-        l_acc = 0.f;
         if (lastit_pend) {
           if (rowok_pend) {
-            __nv_bfloat16* op = P.out + tok_pend * d_model + head_pend * DH + half * HD;
+            __nv_bfloat16* op = P.out + tok_pend * d_model + head_pend * DH + c0;
 #pragma unroll
-            for (int c0 = 0; c0 < HD; c0 += 8) {
-              const float* mr = &S.merged[m][half * HD + c0];
+            for (int k8 = 0; k8 < 2; ++k8) {
+              const float* v = reinterpret_cast<const float*>(r + 8 * k8);
               uint4 w;
-              w.x = pack_bf16(mr[0], mr[1]);
-              w.y = pack_bf16(mr[2], mr[3]);
-              w.z = pack_bf16(mr[4], mr[5]);
-              w.w = pack_bf16(mr[6], mr[7]);
-              *reinterpret_cast<uint4*>(op + c0) = w;
+              w.x = pack_bf16(v[0], v[1]);
+              w.y = pack_bf16(v[2], v[3]);
+              w.z = pack_bf16(v[4], v[5]);
+              w.w = pack_bf16(v[6], v[7]);
+              *reinterpret_cast<uint4*>(op + 8 * k8) = w;
             }
           }
+        } else {
+          uint32_t w[8];
 #pragma unroll
-          for (int j = 0; j < HD; ++j) S.merged[m][half * HD + j] = 0.f;
+          for (int j = 0; j < 8; ++j) {
+            const __half2 h2 = __floats2half2_rn(__uint_as_float(r[2 * j]),
+                                                 __uint_as_float(r[2 * j + 1]));
+            w[j] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          tmem_st8(tM + c0 / 2, w);
         }
       }
+      if (!lastit_pend) tmem_wait_st();
     };
+
     for (;;) {
-      mbar_wait(&S.s_full[c & 1], (c >> 1) & 1);
+      mbar_wait(&S.s_full[hh], c & 1);
       if (tid == 0) trace(trp, c, 3);
       tc_after_sync();
+      // chunk plan (a few wide shared loads) and S pieces 0,1 in flight together
       const ChunkDesc& D = S.desc[c % kStages];
-      const int n_grp = D.ncols / 16;
-      const int br = D.branch;
-      const bool first_br = D.first_in_branch, last_br = D.last_in_branch,
-                 last_it = D.last_in_item, last_all = D.last_overall;
-      const bool row_ok = t < D.q_cnt;
-      const int64_t tok = (int64_t)D.q_first + t;
-      const int head = D.h * G + g_in;
-      if (first_br) {
-        m_run = -__builtin_huge_valf();
-        if (row_ok) {  // prefetch this branch's gate logits (used at its end)
-          const __nv_bfloat16* gp = P.gl + tok * P.ld_gl + P.gcol0 +
-                                    (int64_t)br * d_model + head * DH + half * HD;
-#pragma unroll
-          for (int c0 = 0; c0 < HD; c0 += 8) gate_cur[c0 / 8] = *reinterpret_cast<const uint4*>(gp + c0);
-        }
-      }
-      // this half's S groups -> registers (all in flight, one wait)
-      uint32_t sr[HG * 16];
-#pragma unroll
-      for (int k = 0; k < HG; ++k)
-        if (half * HG + k < n_grp)
-          tmem_ld16_nowait(tmem + lane_base + (c & 1) * kNK + (half * HG + k) * 16, sr + k * 16);
-      // group visibility (producer-resolved) while the loads are in flight
-      int nv_grp[HG];
-#pragma unroll
-      for (int k = 0; k < HG; ++k) {
-        const int gi = half * HG + k;
-        nv_grp[k] = (gi < n_grp && row_ok && ((D.gmask[gi] >> t) & 1u)) ? D.gnv[gi] : 0;
-      }
+      const int4 hdr0 = *reinterpret_cast<const int4*>(&D.ncols);
+      const int4 hdr1 = *reinterpret_cast<const int4*>(&D.q_cnt);
+      const uint32_t visb = D.tokvis[t];
+      const int ncols = hdr0.x;
+      uint32_t sa[32], sb[32];
+      tmem_ld32(tS + HCols::kS, sa);
+      if (ncols > 32) tmem_ld32(tS + HCols::kS + 32, sb);
+#ifdef LSRM_TRACE_LD
       tmem_wait_ld();
-      // masked group maxima (log-depth trees)
-      float gmax[HG];
+      if (tid == 0) trace(trp, c, 1);
+#endif
+      const int br = hdr0.y, fl = hdr0.z;
+      const bool first_br = fl & kFFirstBranch, last_br = fl & kFLastBranch,
+                 last_it = fl & kFLastItem, last_all = fl & kFLastOverall;
+      const bool row_ok = t < hdr1.x;
+      const int64_t tok = (int64_t)hdr0.w + t;
+      const int head = (hdr1.y + hh) * G + g_in;
+      // `live` groups are seen by some row of this warp (others are skipped,
+      // P = 0); a row sees a group if its token selected it (visb); `tail`
+      // groups end a block segment (keys j >= gnv are padding)
+      const uint32_t live = __reduce_or_sync(0xffffffffu, visb);
+      const uint32_t tail = ((uint32_t)fl >> 8) & live;
+      if (first_br) m_run = kNegInf;
+      float mx = kNegInf;
+      tmem_wait_ld();
+      if (tid == 0) trace(trp, c, 8);
+#define LSRM_MAX(arr, off, gi)                                  \
+  if ((live >> (gi)) & 1u) {                                    \
+    if ((tail >> (gi)) & 1u) mask16(arr + (off), D.gnv[gi]);    \
+    const float g_ = max16(arr + (off));                        \
+    mx = ((visb >> (gi)) & 1u) ? fmaxf(mx, g_) : mx;            \
+  }
+      LSRM_MAX(sa, 0, 0)
+      LSRM_MAX(sa, 16, 1)
+      LSRM_MAX(sb, 0, 2)
+      LSRM_MAX(sb, 16, 3)
+      const bool hi = ncols > 64;   // pieces 2,3 end up in registers
+      if (tid == 0) trace(trp, c, 9);
+      if (hi) {
+        tmem_ld32(tS + HCols::kS + 64, sa);
+        if (ncols > 96) tmem_ld32(tS + HCols::kS + 96, sb);
+        tmem_wait_ld();
+        LSRM_MAX(sa, 0, 4)
+        LSRM_MAX(sa, 16, 5)
+        LSRM_MAX(sb, 0, 6)
+        LSRM_MAX(sb, 16, 7)
+      } else {
+        tc_before_sync();
+        mbar_arrive(&S.s_free[hh]);   // S(c) fully in registers: QK(c+1) may overwrite it
+      }
+#undef LSRM_MAX
+      if (tid == 0) trace(trp, c, 10);
+      // running max with headroom; rescale O (and its row sum) if it moves
+      const float m_cand = fmaxf(m_run, mx * sl2);
+      float m_use = m_run, scale = 1.f;
+      bool need = false;
+      if (m_run == kNegInf) {
+        m_use = m_cand;
+      } else if (m_cand > m_run + kHeadroom) {
+        m_use = m_cand;
+        scale = ex2(m_run - m_cand);
+        need = true;
+      }
+      // PV(c-1) must be complete before P(c) overwrites P(c-1) and before O is
+      // rescaled or read
+      if (c > 0) mbar_wait(&S.o_full[hh], (c - 1) & 1);
+      tc_after_sync();
+      if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
-      for (int k = 0; k < HG; ++k) {
-        gmax[k] = -__builtin_huge_valf();
-        if (nv_grp[k] == 16) {
-          float v[8];
+        for (int c0 = 0; c0 < DH; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16_nowait(tO + c0, r);
+          tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            v[j] = fmaxf(__uint_as_float(sr[k * 16 + j]), __uint_as_float(sr[k * 16 + j + 8]));
-#pragma unroll
-          for (int w = 4; w; w >>= 1)
-#pragma unroll
-            for (int j = 0; j < w; ++j) v[j] = fmaxf(v[j], v[j + w]);
-          gmax[k] = v[0];
-        } else if (nv_grp[k] > 0) {
-          float v[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            v[j] = j < nv_grp[k] ? __uint_as_float(sr[k * 16 + j]) : -__builtin_huge_valf();
-#pragma unroll
-          for (int w = 8; w; w >>= 1)
-#pragma unroll
-            for (int j = 0; j < w; ++j) v[j] = fmaxf(v[j], v[j + w]);
-          gmax[k] = v[0];
+          for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
+          tmem_st16(tO + c0, r);
+        }
+        uint32_t rl[1];
+        tmem_ld_cols<1>(tO + DH, rl);
+        tmem_wait_ld();
+        rl[0] = __float_as_uint(__uint_as_float(rl[0]) * scale);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tO + DH),
+                     "r"(rl[0])
+                     : "memory");
+      }
+      m_run = m_use;
+      if (tid == 0) trace(trp, c, 11);
+      // pass 2: P = exp2(S * scale - m) as packed bf16; rows that do not see a
+      // group get a -inf bias (P = 0); fully masked rows so far use m = 0
+      const float nbv = m_use == kNegInf ? 0.f : -m_use;
+#define LSRM_EXP_PIECE(arr, pc)                                                           \
+  {                                                                                       \
+    uint32_t w[16];                                                                       \
+    if ((live >> (2 * (pc))) & 1u)                                                        \
+      exp16(arr, sl2, ((visb >> (2 * (pc))) & 1u) ? nbv : kNegInf, w);                    \
+    else                                                                                  \
+      zero8(w);                                                                           \
+    if ((live >> (2 * (pc) + 1)) & 1u)                                                    \
+      exp16(arr + 16, sl2, ((visb >> (2 * (pc) + 1)) & 1u) ? nbv : kNegInf, w + 8);       \
+    else                                                                                  \
+      zero8(w + 8);                                                                       \
+    tmem_st16(tP + 16 * (pc), w);                                                         \
+  }
+      if (hi) {
+        LSRM_EXP_PIECE(sa, 2)
+        if (ncols > 96) LSRM_EXP_PIECE(sb, 3)
+        tmem_ld32(tS + HCols::kS, sa);   // pieces 0,1 again (both full: ncols > 64)
+        tmem_ld32(tS + HCols::kS + 32, sb);
+        tmem_wait_ld();
+        tc_before_sync();
+        mbar_arrive(&S.s_free[hh]);
+        if (tid == 0) trace(trp, c, 12);
+        if (tail & 15u) {
+          if (tail & 1u) mask16(sa, D.gnv[0]);
+          if (tail & 2u) mask16(sa + 16, D.gnv[1]);
+          if (tail & 4u) mask16(sb, D.gnv[2]);
+          if (tail & 8u) mask16(sb + 16, D.gnv[3]);
         }
       }
-#pragma unroll
-      for (int w = HG / 2; w; w >>= 1)
-#pragma unroll
-        for (int j = 0; j < w; ++j) gmax[j] = fmaxf(gmax[j], gmax[j + w]);
-      // row max across the two halves
-      S.xmax[c & 1][half][m] = gmax[0];
-      named_sync(bar_id, 32 * kParts);
-      float cmax = gmax[0];
-#pragma unroll
-      for (int p2 = 0; p2 < kParts; ++p2) cmax = fmaxf(cmax, S.xmax[c & 1][p2][m]);
-      const float m_new = fmaxf(m_run, cmax * sl2);
-      const float alpha = (m_new == -__builtin_huge_valf()) ? 1.f : ex2(m_run - m_new);
-      const uint32_t pbase = tmem + lane_base + (c & 1) * kNK + kColP;
-#pragma unroll
-      for (int k = 0; k < HG; ++k) {
-        const int gi = half * HG + k;
-        if (gi < n_grp) {
-          uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          const int nv = nv_grp[k];
-          if (nv > 0) {
-            float pv[16];
-            if (nv == 16) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                pv[j] = ex2(fmaf(__uint_as_float(sr[k * 16 + j]), sl2, -m_new));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                pv[j] = j < nv ? ex2(fmaf(__uint_as_float(sr[k * 16 + j]), sl2, -m_new)) : 0.f;
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) w[j] = pack_bf16(pv[2 * j], pv[2 * j + 1]);
-          }
-          tmem_st8(pbase + gi * 8, w);
-        }
-      }
+      LSRM_EXP_PIECE(sa, 0)
+      if (ncols > 32) LSRM_EXP_PIECE(sb, 1)
+#undef LSRM_EXP_PIECE
+      if (tid == 0) trace(trp, c, 13);
       tmem_wait_st();
-      tc_before_sync();
-      mbar_arrive(&S.p_full[c & 1]);
-      if (tid == 0) trace(trp, c, 4);
-      // previous chunk's PV partial (its rescale factor is alpha_pend)
-      if (have_pend) absorb_pv();
-      m_run = m_new;
-      alpha_pend = alpha;
-      br_pend = br;
-      lastbr_pend = last_br;
-      lastit_pend = last_it;
-      tok_pend = tok;
-      rowok_pend = row_ok;
-      if (last_br) {
-#pragma unroll
-        for (int j = 0; j < HD / 8; ++j) gate_pend[j] = gate_cur[j];
+      if (tid == 0) trace(trp, c, 14);
+      if (epi_pend) {   // the previous branch's O must be read before PV(c) overwrites it
+        epilogue(c - 1);
+        epi_pend = false;
       }
-      head_pend = head;
-      have_pend = true;
+      if (tid == 0) trace(trp, c, 15);
+      tc_before_sync();
+      mbar_arrive(&S.p_full[hh]);
+      if (tid == 0) trace(trp, c, 4);
+      if (last_br) {
+        if (row_ok) {   // stage this branch's gate logits for its epilogue
+          const __nv_bfloat16* gp = P.gl + tok * P.ld_gl + P.gcol0 + (int64_t)br * d_model +
+                                    head * DH;
+#pragma unroll
+          for (int c0 = 0; c0 < DH; c0 += 8) cp_async16(gate_s + c0, gp + c0, 16u);
+        }
+        br_pend = br;
+        head_pend = head;
+        tok_pend = tok;
+        rowok_pend = row_ok;
+        lastit_pend = last_it;
+        epi_pend = true;
+      }
       ++c;
       if (last_all) break;
     }
-    absorb_pv();
+    epilogue(c - 1);
   }
   tc_before_sync();
   __syncthreads();
   if (warp == 0) {
     tc_after_sync();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(kTmemCols));
+                 "r"(kAlloc));
   }
 }
 
@@ -909,22 +1051,21 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
   int dev = 0, n_sm = 148;
   LSRM_CUDA(cudaGetDevice(&dev));
   LSRM_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  int64_t n_items = n_tiles * hkv;
+  // two head-tiles per item (ping-pong) when the kv heads pair up and TMEM fits
+  const int hp = (dh == 32 && hkv % 2 == 0) ? 2 : 1;
+  int64_t n_items = n_tiles * (hkv / hp);
   unsigned grid = (unsigned)(n_items < n_sm ? n_items : n_sm);
-#define LSRM_TC_CASE(D)                                                                     \
-  case D: {                                                                                 \
-    size_t smem = sizeof(tc::Smem<D>) + 1024;                                               \
-    LSRM_CUDA(cudaFuncSetAttribute(tc::nsa_fused_kernel<D>,                                 \
+#define LSRM_TC_CASE(D, HP)                                                                 \
+  if (dh == D && hp == HP) {                                                                \
+    size_t smem = sizeof(tc::Smem<D, HP>) + 1024;                                           \
+    LSRM_CUDA(cudaFuncSetAttribute(tc::nsa_fused_kernel<D, HP>,                             \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    tc::nsa_fused_kernel<D><<<grid, tc::kThreads, smem, st>>>(p);                           \
-    break;                                                                                  \
-  }
-  switch (dh) {
-    LSRM_TC_CASE(32)
-    LSRM_TC_CASE(64)
-    default:
-      return set_error(LSRM_E_CONFIG, "tcgen05 path: head_dim %d not in {32,64}", dh);
-  }
+    tc::nsa_fused_kernel<D, HP><<<grid, tc::threads_of<HP>(), smem, st>>>(p);               \
+  } else
+  LSRM_TC_CASE(32, 2)
+  LSRM_TC_CASE(32, 1)
+  LSRM_TC_CASE(64, 1)
+  return set_error(LSRM_E_CONFIG, "tcgen05 path: head_dim %d not in {32,64}", dh);
 #undef LSRM_TC_CASE
   LSRM_LAUNCHED();
   return LSRM_OK;

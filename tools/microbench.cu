@@ -1,0 +1,117 @@
+// Microbenchmarks that decide the softmax design of the fused attention
+// kernel on B200: MUFU ex2 throughput for f32 / f16x2 / bf16x2, and TMEM
+// load throughput (tcgen05.ld 32x32b.x32) per SM.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb tools/microbench.cu && /tmp/mb
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+constexpr int kIters = 4096;
+
+template <int MODE>
+__global__ void ex2_kernel(float* out, long long* clk) {
+  uint32_t v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = 0x3c003c00u + threadIdx.x + i;   // f16x2 (1,1)-ish
+  float f[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = -0.001f * (threadIdx.x + i);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (MODE == 0) {
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(f[i]));
+      } else if (MODE == 1) {
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(v[i]));
+      } else {
+        asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(v[i]));
+      }
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += f[i] + __uint_as_float(v[i]);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+}
+
+__global__ void tmem_ld_kernel(float* out, long long* clk, int nwarps_active) {
+  __shared__ uint32_t base;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = base + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 128;
+  uint32_t acc = 0;
+  long long t0 = clock64();
+  if (warp < nwarps_active) {
+    for (int it = 0; it < kIters / 16; ++it) {
+      uint32_t r[32];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+            "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+            "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+            "=r"(r[31])
+          : "r"(tm + (it & 3) * 32));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc ^= r[i];
+    }
+  }
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)acc;
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base));
+}
+
+int main() {
+  float* out;
+  long long* clk;
+  cudaMalloc(&out, 148 * 1024 * sizeof(float));
+  cudaMalloc(&clk, 148 * sizeof(long long));
+  long long h[148];
+  const char* names[3] = {"ex2.approx.ftz.f32", "ex2.approx.f16x2", "ex2.approx.ftz.bf16x2"};
+  for (int warps = 4; warps <= 16; warps *= 2) {
+    for (int mode = 0; mode < 3; ++mode) {
+      for (int rep = 0; rep < 2; ++rep) {
+        if (mode == 0) ex2_kernel<0><<<148, 32 * warps>>>(out, clk);
+        if (mode == 1) ex2_kernel<1><<<148, 32 * warps>>>(out, clk);
+        if (mode == 2) ex2_kernel<2><<<148, 32 * warps>>>(out, clk);
+      }
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, clk, sizeof(h), cudaMemcpyDeviceToHost);
+      double ops = (double)kIters * 8 * 32 * warps;   // lane-ops per SM
+      printf("%-22s warps/SM %2d: %.2f lane-ops/clk/SM (%lld clk)\n", names[mode], warps,
+             ops / h[0], h[0]);
+    }
+  }
+  for (int w = 1; w <= 16; w *= 2) {
+    for (int rep = 0; rep < 2; ++rep) tmem_ld_kernel<<<148, 512>>>(out, clk, w);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      printf("tmem kernel failed: %s\n", cudaGetErrorString(e));
+      return 1;
+    }
+    cudaMemcpy(h, clk, sizeof(h), cudaMemcpyDeviceToHost);
+    double bytes = (double)(kIters / 16) * 32 * 32 * 4 * w;
+    printf("tcgen05.ld x32, %2d warps: %.1f B/clk/SM (%lld clk)\n", w, bytes / h[0], h[0]);
+  }
+  return 0;
+}
