@@ -212,7 +212,7 @@ int lsrm_kv_interleave(int src_is_bf16, const void* src, int64_t ld_src,
                        const int64_t* pad_offsets, int64_t n_rows_pad,
                        void* dst, void* stream);
 
-/* Debug: device buffer of 512 x 16 int64 that CTA 0 of the fused attention
+/* Debug: device buffer of 256 x 32 int64 that CTA 0 of the fused attention
  * kernel fills with clock64() stamps per chunk/event (NULL disables). */
 int lsrm_debug_set_trace(void* buf);
 

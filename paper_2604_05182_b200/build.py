@@ -24,6 +24,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
           "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 EXACT_TUS = {"routing.cu", "tokens.cu", "partition.cu"}
+# LSRM_NVCC_FLAGS="-DLSRM_TRACE" builds the per-chunk event trace of the fused
+# attention kernel (tools/attn_trace.py); off by default.
+EXTRA = os.environ.get("LSRM_NVCC_FLAGS", "").split()
 
 
 def _sources():
@@ -36,13 +39,18 @@ def _compile(src):
     deps = [path, os.path.join(CSRC, "common.cuh"),
             os.path.join(HERE, "..", "include", "lsrm_b200.h")]
     deps += [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
-    if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
+    stamp = obj + ".flags"
+    same_flags = os.path.exists(stamp) and open(stamp).read() == " ".join(EXTRA)
+    if same_flags and os.path.exists(obj) and \
+            os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj, ""
-    flags = ARCH + COMMON + (["--fmad=false"] if src in EXACT_TUS else [])
+    flags = ARCH + COMMON + EXTRA + (["--fmad=false"] if src in EXACT_TUS else [])
     cmd = [NVCC, *flags, "-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+    with open(stamp, "w") as fh:
+        fh.write(" ".join(EXTRA))
     return obj, r.stderr
 
 

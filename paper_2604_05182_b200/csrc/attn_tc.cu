@@ -145,6 +145,9 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -188,9 +191,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 
 // Optional event trace (debug): CTA 0 stamps clock64() per chunk and event.
 __device__ long long* g_trace = nullptr;
-constexpr int kTraceEv = 16, kTraceChunks = 512;
+constexpr int kTraceEv = 32, kTraceChunks = 256;
 __device__ __forceinline__ void trace(long long* tr, uint32_t c, int ev) {
+#ifdef LSRM_TRACE
   if (tr && c < (uint32_t)kTraceChunks) tr[c * kTraceEv + ev] = clock64();
+#endif
 }
 
 struct Params {
@@ -218,7 +223,24 @@ struct Params {
   __nv_bfloat16* out;
 };
 
-constexpr int kStages = 4;       // K/V ring depth (each stage holds every head of the item)
+// Build-time variants (kept switchable so they can be measured against each
+// other on the GPU): ring depth, one-pass streaming softmax, and strict
+// alternation of the two head-tiles' exponential bursts (ping-pong).
+#ifndef LSRM_STAGES
+#define LSRM_STAGES 3
+#endif
+#ifndef LSRM_ONEPASS
+#define LSRM_ONEPASS 0
+#endif
+#ifndef LSRM_PINGPONG
+#define LSRM_PINGPONG 0
+#endif
+constexpr int kStages = LSRM_STAGES;   // K/V ring depth (each stage holds every head of the item)
+constexpr bool kOnePass = LSRM_ONEPASS;
+constexpr bool kPingPong = LSRM_PINGPONG;
+// gate biases staged in shared memory as [n_gates * hq][DH + 1] (padded rows:
+// the 16 heads of a warp hit 16 banks) when they fit, else read from global
+constexpr int kBiasMax = LSRM_STAGES <= 3 ? 3328 : 4;
 constexpr int kOnesCols = 16;    // extra V columns holding 1 (valid key) / 0 (padding)
 constexpr int kBitmapWords = 512;  // union bitmap: up to 16384 occupied KV blocks
 
@@ -266,6 +288,11 @@ __device__ __forceinline__ float max16(const uint32_t* s) {
   a = fmaxf(fmaxf(a, b), d);
   e = fmaxf(fmaxf(e, f), x[15]);
   return fmaxf(a, e);
+}
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
@@ -318,6 +345,7 @@ struct Smem {
   __nv_bfloat16 k[kStages][HP][kNK * DH];
   __nv_bfloat16 v[kStages][HP][kNK * (DH + kOnesCols)];   // [V | ones] rows
   __nv_bfloat16 gate[HP][kM * DH];  // per row: gate logits of the branch that just ended
+  float bias[kBiasMax];             // gate biases, padded rows (if they fit)
   int32_t ent[kMaxEnt];          // selected rows of the tile tokens, [t][kmax]
   uint32_t bitmap[kBitmapWords]; // selected-row bitmap of the current item
   int32_t wpre[kBitmapWords];    // rank of the first set bit of each word
@@ -334,7 +362,7 @@ struct Smem {
 };
 
 template <int HP>
-constexpr int threads_of() { return 32 * (4 * HP + 2); }
+constexpr int threads_of() { return 32 * (5 * HP + 1); }   // softmax, producer, MMA per head
 
 // Work item = (query tile, group of HP kv heads).  The HP head-tiles share the
 // chunk plan (same tokens, same union of selected blocks) but not K/V, so
@@ -350,7 +378,7 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
   Smem<DH, HP>& S = *reinterpret_cast<Smem<DH, HP>*>(smem_raw);
   using HCols = HeadCols<DH>;
   constexpr int VW = HCols::VW, HC = HCols::kTotal;
-  constexpr int kSoftWarps = 4 * HP, kProducerWarp = kSoftWarps, kMmaWarp = kSoftWarps + 1;
+  constexpr int kSoftWarps = 4 * HP, kProducerWarp = kSoftWarps;
   constexpr int kAlloc = tmem_alloc_cols<DH, HP>();
   static_assert(kAlloc <= 512, "TMEM budget");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -363,7 +391,7 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&S.kv_full[i], 1);
-      mbar_init(&S.kv_empty[i], 1);
+      mbar_init(&S.kv_empty[i], HP);   // one commit per head-tile's MMA warp
     }
     for (int hh = 0; hh < HP; ++hh) {
       mbar_init(&S.s_full[hh], 1);
@@ -373,7 +401,7 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.q_full[i], 1);
-      mbar_init(&S.q_empty[i], 1);
+      mbar_init(&S.q_empty[i], HP);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -384,6 +412,12 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   for (int i = tid; i < kBitmapWords; i += blockDim.x) S.bitmap[i] = 0u;
+  const bool bias_smem = P.gbias && P.n_gates * P.hq * (DH + 1) <= kBiasMax;
+  if (bias_smem)
+    for (int i = tid; i < P.n_gates * d_model; i += blockDim.x)
+      S.bias[(i / DH) * (DH + 1) + i % DH] = P.gbias[i];
+  const float* const bias_all = bias_smem ? S.bias : P.gbias;
+  const int bias_ld = bias_smem ? DH + 1 : DH;   // floats per (branch, head) row
   fence_async_smem();
   tc_before_sync();
   __syncthreads();
@@ -610,20 +644,22 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       }
       __syncwarp();
     }
-  } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer (warp converged; one elected lane issues)
+  } else if (warp > kProducerWarp) {
+    // ===================== MMA issuer of head-tile hh (one warp per head-tile,
+    // so neither head-tile's MMAs wait behind the other's barriers)
+    const int hh = warp - kProducerWarp - 1;
     const uint32_t id_pv = idesc_bf16(kM, VW, 1);   // [O | rowsum] += P . [V | ones]
-    // S_hh = Q_hh K_hh^T for chunk cc into head-tile hh's S columns
-    auto issue_qk = [&](uint32_t cc, int hh) {
+    const uint32_t t_s = tmem + hh * HC + HCols::kS, t_p = tmem + hh * HC + HCols::kP,
+                   t_o = tmem + hh * HC + HCols::kO;
+    // S = Q K^T for chunk cc into this head-tile's S columns
+    auto issue_qk = [&](uint32_t cc) {
       const int st = cc % kStages;
       const ChunkDesc& D = S.desc[st];
-      if (hh == 0) {
-        mbar_wait(&S.kv_full[st], (cc / kStages) & 1);
+      mbar_wait(&S.kv_full[st], (cc / kStages) & 1);
 #ifndef LSRM_TRACE_LD
-        if (lane == 0) trace(trp, cc, 1);
+      if (lane == 0 && hh == 0) trace(trp, cc, 1);
 #endif
-        if (D.flags & kFFirstItem) mbar_wait(&S.q_full[D.qb], (D.item_seq >> 1) & 1);
-      }
+      if (D.flags & kFFirstItem) mbar_wait(&S.q_full[D.qb], (D.item_seq >> 1) & 1);
       tc_after_sync();
       const uint32_t id = idesc_bf16(kM, D.ncols, 0);
       const uint64_t a0 = sdesc(smem_u32(S.q[D.qb][hh]), 128, 16 * DH);
@@ -631,15 +667,13 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       if (elect_one_sync()) {
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(tmem + hh * HC + HCols::kS, a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16),
-                   id, kk > 0);
+          mma_bf16(t_s, a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16), id, kk > 0);
         mma_commit(&S.s_full[hh]);
       }
       __syncwarp();
       if (lane == 0 && hh == 0) trace(trp, cc, 2);
     };
-#pragma unroll
-    for (int hh = 0; hh < HP; ++hh) issue_qk(0, hh);
+    issue_qk(0);
     // per chunk: S(c+1) = Q K^T as soon as the softmax has S(c) in registers
     // (s_free), then PV(c) accumulates P(c).[V|ones] into the branch's O as
     // soon as P(c) is written (p_full)
@@ -653,35 +687,25 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       const int nk = D.ncols / 16;
       const int qb = D.qb;
       if (!last) {
-#pragma unroll
-        for (int hh = 0; hh < HP; ++hh) {
-          mbar_wait(&S.s_free[hh], c & 1);
-          issue_qk(c + 1, hh);
-        }
+        mbar_wait(&S.s_free[hh], c & 1);
+        issue_qk(c + 1);
       }
+      mbar_wait(&S.p_full[hh], c & 1);
+      if (lane == 0 && hh == 0) trace(trp, c, 5);
+      tc_after_sync();
+      const uint64_t vdesc = sdesc(smem_u32(S.v[st][hh]), 16 * VW, 128);
+      if (elect_one_sync()) {
 #pragma unroll
-      for (int hh = 0; hh < HP; ++hh) {
-        mbar_wait(&S.p_full[hh], c & 1);
-        if (lane == 0 && hh == 0) trace(trp, c, 5);
-        tc_after_sync();
-        const uint32_t pa = tmem + hh * HC + HCols::kP;
-        const uint64_t vdesc = sdesc(smem_u32(S.v[st][hh]), 16 * VW, 128);
-        const uint32_t to = tmem + hh * HC + HCols::kO;
-        if (elect_one_sync()) {
-#pragma unroll
-          for (int kk = 0; kk < kGroups; ++kk)
-            if (kk < nk)
-              mma_bf16_ts(to, pa + kk * 8, vdesc + (uint64_t)(kk * 2 * VW), id_pv,
-                          kk > 0 ? 1u : acc0);
-          mma_commit(&S.o_full[hh]);
-          if (hh == HP - 1) {
-            if (last_in_item) mma_commit(&S.q_empty[qb]);
-            mma_commit(&S.kv_empty[st]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0 && hh == 0) trace(trp, c, 6);
+        for (int kk = 0; kk < kGroups; ++kk)
+          if (kk < nk)
+            mma_bf16_ts(t_o, t_p + kk * 8, vdesc + (uint64_t)(kk * 2 * VW), id_pv,
+                        kk > 0 ? 1u : acc0);
+        mma_commit(&S.o_full[hh]);
+        if (last_in_item) mma_commit(&S.q_empty[qb]);
+        mma_commit(&S.kv_empty[st]);
       }
+      __syncwarp();
+      if (lane == 0 && hh == 0) trace(trp, c, 6);
       ++c;
       if (last) break;
     }
@@ -707,6 +731,19 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
     int64_t tok_pend = 0;
     __nv_bfloat16* const gate_s = &S.gate[hh][m * DH];   // this row's staged gate logits
     uint32_t c = 0;
+    // ping-pong: the HP=2 warpgroups take turns on the exponential phase
+    // (named barriers 1, 2), so one's MUFU stream covers the other's loads,
+    // maxima and epilogue; warpgroup 1 lets warpgroup 0 go first
+    const int bar_mine = 1 + hh, bar_other = 2 - hh;
+    if (kPingPong && HP == 2 && hh == 1) named_arrive(bar_other, 256);
+    // one turn per 32-key piece: wait for ours, run the piece's exponentials,
+    // hand over (the very last hand-over of warpgroup 1 has no taker)
+    auto pp_turn = [&]() {
+      if (kPingPong && HP == 2) named_sync(bar_mine, 256);
+    };
+    auto pp_pass = [&](bool last_piece) {
+      if (kPingPong && HP == 2 && !(hh == 1 && last_piece)) named_arrive(bar_other, 256);
+    };
 
     // gate + merge of a finished branch (nsa_attention.py:266-284); the
     // running merge is f16 in TMEM; at an item end the merged row is stored
@@ -719,8 +756,8 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       tmem_ld_cols<1>(tO + DH, rl);
       tmem_wait_ld();
       const float inv = rowok_pend ? 1.f / __uint_as_float(rl[0]) : 0.f;
-      const int64_t col0 = (int64_t)br_pend * d_model + head_pend * DH;
-      const float* bp = P.gbias ? P.gbias + col0 : nullptr;
+      const float* bp =
+          bias_all ? bias_all + ((int64_t)br_pend * P.hq + head_pend) * bias_ld : nullptr;
 #pragma unroll
       for (int c0 = 0; c0 < DH; c0 += 16) {   // 16 columns at a time (registers)
         uint32_t r[16], mr[8];
@@ -734,9 +771,10 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int cj = 8 * k8 + j;
-            const float z = __bfloat162float(hv[j]) + (bp ? __ldg(bp + c0 + cj) : 0.f);
+            const float z = __bfloat162float(hv[j]) + (bp ? bp[c0 + cj] : 0.f);
+            // sigmoid(z) = 0.5 + 0.5 tanh(z / 2): one MUFU op
             float v = rowok_pend ? __uint_as_float(r[cj]) * inv *
-                                       rcp_approx(1.f + ex2(-z * 1.4426950408889634f))
+                                       fmaf(0.5f, tanh_approx(0.5f * z), 0.5f)
                                  : 0.f;
             if (br_pend > 0) {
               const __half2 hm = *reinterpret_cast<const __half2*>(&mr[cj / 2]);
@@ -803,104 +841,209 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       const uint32_t tail = ((uint32_t)fl >> 8) & live;
       if (first_br) m_run = kNegInf;
       float mx = kNegInf;
+      const int n_pc = (ncols + 31) / 32;   // 32-key pieces (ping-pong turns) of this chunk
+      int pdone = 0;
       tmem_wait_ld();
       if (tid == 0) trace(trp, c, 8);
+      // Exponentials against the running max need it defined for every row
+      // that sees this chunk: the first chunk of a branch takes two passes
+      // (max, then exponentials); later chunks stream once.
+      const bool two_pass =
+          !kOnePass || __any_sync(0xffffffffu, m_run == kNegInf && visb != 0u);
+      if (two_pass) {
 #define LSRM_MAX(arr, off, gi)                                  \
-  if ((live >> (gi)) & 1u) {                                    \
-    if ((tail >> (gi)) & 1u) mask16(arr + (off), D.gnv[gi]);    \
-    const float g_ = max16(arr + (off));                        \
-    mx = ((visb >> (gi)) & 1u) ? fmaxf(mx, g_) : mx;            \
-  }
-      LSRM_MAX(sa, 0, 0)
-      LSRM_MAX(sa, 16, 1)
-      LSRM_MAX(sb, 0, 2)
-      LSRM_MAX(sb, 16, 3)
-      const bool hi = ncols > 64;   // pieces 2,3 end up in registers
-      if (tid == 0) trace(trp, c, 9);
-      if (hi) {
-        tmem_ld32(tS + HCols::kS + 64, sa);
-        if (ncols > 96) tmem_ld32(tS + HCols::kS + 96, sb);
-        tmem_wait_ld();
-        LSRM_MAX(sa, 0, 4)
-        LSRM_MAX(sa, 16, 5)
-        LSRM_MAX(sb, 0, 6)
-        LSRM_MAX(sb, 16, 7)
-      } else {
-        tc_before_sync();
-        mbar_arrive(&S.s_free[hh]);   // S(c) fully in registers: QK(c+1) may overwrite it
-      }
-#undef LSRM_MAX
-      if (tid == 0) trace(trp, c, 10);
-      // running max with headroom; rescale O (and its row sum) if it moves
-      const float m_cand = fmaxf(m_run, mx * sl2);
-      float m_use = m_run, scale = 1.f;
-      bool need = false;
-      if (m_run == kNegInf) {
-        m_use = m_cand;
-      } else if (m_cand > m_run + kHeadroom) {
-        m_use = m_cand;
-        scale = ex2(m_run - m_cand);
-        need = true;
-      }
-      // PV(c-1) must be complete before P(c) overwrites P(c-1) and before O is
-      // rescaled or read
-      if (c > 0) mbar_wait(&S.o_full[hh], (c - 1) & 1);
-      tc_after_sync();
-      if (__any_sync(0xffffffffu, need)) {
-#pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16_nowait(tO + c0, r);
+    if ((live >> (gi)) & 1u) {                                    \
+      if ((tail >> (gi)) & 1u) mask16(arr + (off), D.gnv[gi]);    \
+      const float g_ = max16(arr + (off));                        \
+      mx = ((visb >> (gi)) & 1u) ? fmaxf(mx, g_) : mx;            \
+    }
+        LSRM_MAX(sa, 0, 0)
+        LSRM_MAX(sa, 16, 1)
+        LSRM_MAX(sb, 0, 2)
+        LSRM_MAX(sb, 16, 3)
+        const bool hi = ncols > 64;   // pieces 2,3 end up in registers
+        if (tid == 0) trace(trp, c, 9);
+        if (hi) {
+          tmem_ld32(tS + HCols::kS + 64, sa);
+          if (ncols > 96) tmem_ld32(tS + HCols::kS + 96, sb);
           tmem_wait_ld();
+          LSRM_MAX(sa, 0, 4)
+          LSRM_MAX(sa, 16, 5)
+          LSRM_MAX(sb, 0, 6)
+          LSRM_MAX(sb, 16, 7)
+        } else {
+          tc_before_sync();
+          mbar_arrive(&S.s_free[hh]);   // S(c) fully in registers: QK(c+1) may overwrite it
+        }
+#undef LSRM_MAX
+        if (tid == 0) trace(trp, c, 10);
+        // running max with headroom; rescale O (and its row sum) if it moves
+        const float m_cand = fmaxf(m_run, mx * sl2);
+        float m_use = m_run, scale = 1.f;
+        bool need = false;
+        if (m_run == kNegInf) {
+          m_use = m_cand;
+        } else if (m_cand > m_run + kHeadroom) {
+          m_use = m_cand;
+          scale = ex2(m_run - m_cand);
+          need = true;
+        }
+        // PV(c-1) must be complete before P(c) overwrites P(c-1) and before O is
+        // rescaled or read
+        if (c > 0) mbar_wait(&S.o_full[hh], (c - 1) & 1);
+        tc_after_sync();
+        if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
-          tmem_st16(tO + c0, r);
+          for (int c0 = 0; c0 < DH; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16_nowait(tO + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
+            tmem_st16(tO + c0, r);
+          }
+          uint32_t rl[1];
+          tmem_ld_cols<1>(tO + DH, rl);
+          tmem_wait_ld();
+          rl[0] = __float_as_uint(__uint_as_float(rl[0]) * scale);
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tO + DH),
+                       "r"(rl[0])
+                       : "memory");
         }
-        uint32_t rl[1];
-        tmem_ld_cols<1>(tO + DH, rl);
-        tmem_wait_ld();
-        rl[0] = __float_as_uint(__uint_as_float(rl[0]) * scale);
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tO + DH),
-                     "r"(rl[0])
-                     : "memory");
-      }
-      m_run = m_use;
-      if (tid == 0) trace(trp, c, 11);
-      // pass 2: P = exp2(S * scale - m) as packed bf16; rows that do not see a
-      // group get a -inf bias (P = 0); fully masked rows so far use m = 0
-      const float nbv = m_use == kNegInf ? 0.f : -m_use;
-#define LSRM_EXP_PIECE(arr, pc)                                                           \
-  {                                                                                       \
-    uint32_t w[16];                                                                       \
-    if ((live >> (2 * (pc))) & 1u)                                                        \
-      exp16(arr, sl2, ((visb >> (2 * (pc))) & 1u) ? nbv : kNegInf, w);                    \
-    else                                                                                  \
-      zero8(w);                                                                           \
-    if ((live >> (2 * (pc) + 1)) & 1u)                                                    \
-      exp16(arr + 16, sl2, ((visb >> (2 * (pc) + 1)) & 1u) ? nbv : kNegInf, w + 8);       \
-    else                                                                                  \
-      zero8(w + 8);                                                                       \
-    tmem_st16(tP + 16 * (pc), w);                                                         \
+        m_run = m_use;
+        if (tid == 0) trace(trp, c, 11);
+        // pass 2: P = exp2(S * scale - m) as packed bf16; rows that do not see a
+        // group get a -inf bias (P = 0); fully masked rows so far use m = 0
+        const float nbv = m_use == kNegInf ? 0.f : -m_use;
+#define LSRM_EXP_PIECE(arr, pc)                                                \
+  {                                                                            \
+    uint32_t w[16];                                                            \
+    const bool lp_ = last_all && ++pdone == n_pc;                              \
+    pp_turn();                                                                 \
+    if ((live >> (2 * (pc))) & 3u) {                                           \
+      exp16(arr, sl2, ((visb >> (2 * (pc))) & 1u) ? nbv : kNegInf, w);         \
+      exp16(arr + 16, sl2, ((visb >> (2 * (pc) + 1)) & 1u) ? nbv : kNegInf, w + 8); \
+    } else {                                                                   \
+      zero8(w);                                                                \
+      zero8(w + 8);                                                            \
+    }                                                                          \
+    pp_pass(lp_);                                                              \
+    tmem_st16(tP + 16 * (pc), w);                                              \
   }
-      if (hi) {
-        LSRM_EXP_PIECE(sa, 2)
-        if (ncols > 96) LSRM_EXP_PIECE(sb, 3)
-        tmem_ld32(tS + HCols::kS, sa);   // pieces 0,1 again (both full: ncols > 64)
-        tmem_ld32(tS + HCols::kS + 32, sb);
-        tmem_wait_ld();
-        tc_before_sync();
-        mbar_arrive(&S.s_free[hh]);
-        if (tid == 0) trace(trp, c, 12);
-        if (tail & 15u) {
-          if (tail & 1u) mask16(sa, D.gnv[0]);
-          if (tail & 2u) mask16(sa + 16, D.gnv[1]);
-          if (tail & 4u) mask16(sb, D.gnv[2]);
-          if (tail & 8u) mask16(sb + 16, D.gnv[3]);
+        if (hi) {
+          LSRM_EXP_PIECE(sa, 2)
+          if (ncols > 96) LSRM_EXP_PIECE(sb, 3)
+          tmem_ld32(tS + HCols::kS, sa);   // pieces 0,1 again (both full: ncols > 64)
+          tmem_ld32(tS + HCols::kS + 32, sb);
+          tmem_wait_ld();
+          tc_before_sync();
+          mbar_arrive(&S.s_free[hh]);
+          if (tid == 0) trace(trp, c, 12);
+          if (tail & 15u) {
+            if (tail & 1u) mask16(sa, D.gnv[0]);
+            if (tail & 2u) mask16(sa + 16, D.gnv[1]);
+            if (tail & 4u) mask16(sb, D.gnv[2]);
+            if (tail & 8u) mask16(sb + 16, D.gnv[3]);
+          }
         }
-      }
-      LSRM_EXP_PIECE(sa, 0)
-      if (ncols > 32) LSRM_EXP_PIECE(sb, 1)
+        LSRM_EXP_PIECE(sa, 0)
+        if (ncols > 32) LSRM_EXP_PIECE(sb, 1)
 #undef LSRM_EXP_PIECE
+      } else {
+        // ---- one pass: exponentials against m_run while the chunk max is
+        //      gathered; a rare fixup handles a max that leaves the headroom
+        if (c > 0) mbar_wait(&S.o_full[hh], (c - 1) & 1);   // PV(c-1) has read P(c-1)
+        tc_after_sync();
+        if (tid == 0) trace(trp, c, 11);
+        const float nbv = -m_run;
+// one 32-key piece, straight-line (no per-group branches, so the MUFU stream
+// of its 32 exponentials is scheduled back to back); groups the warp does not
+// see inside a live piece just get a -inf bias
+#define LSRM_STREAM_PIECE(arr, pc)                                            \
+  {                                                                           \
+    uint32_t w[16];                                                           \
+    if ((live >> (2 * (pc))) & 3u) {                                          \
+      if ((tail >> (2 * (pc))) & 1u) mask16(arr, D.gnv[2 * (pc)]);            \
+      if ((tail >> (2 * (pc) + 1)) & 1u) mask16(arr + 16, D.gnv[2 * (pc) + 1]); \
+      const bool v0 = (visb >> (2 * (pc))) & 1u, v1 = (visb >> (2 * (pc) + 1)) & 1u; \
+      if (tid == 0) trace(trp, c, 16 + 4 * (pc));                             \
+      const float g0 = max16(arr), g1 = max16(arr + 16);                      \
+      mx = fmaxf(mx, fmaxf(v0 ? g0 : kNegInf, v1 ? g1 : kNegInf));            \
+      if (tid == 0) trace(trp, c, 17 + 4 * (pc));                             \
+      pp_turn();                                                              \
+      exp16(arr, sl2, v0 ? nbv : kNegInf, w);                                 \
+      exp16(arr + 16, sl2, v1 ? nbv : kNegInf, w + 8);                        \
+    } else {                                                                  \
+      pp_turn();                                                              \
+      zero8(w);                                                               \
+      zero8(w + 8);                                                           \
+    }                                                                         \
+    pp_pass(last_all && ++pdone == n_pc);                                     \
+    if (tid == 0) trace(trp, c, 18 + 4 * (pc));                               \
+    tmem_st16(tP + 16 * (pc), w);                                             \
+    if (tid == 0) trace(trp, c, 19 + 4 * (pc));                               \
+  }
+        LSRM_STREAM_PIECE(sa, 0)
+        if (tid == 0) trace(trp, c, 9);
+        if (ncols > 64) tmem_ld32(tS + HCols::kS + 64, sa);
+        if (ncols > 32) LSRM_STREAM_PIECE(sb, 1)
+        if (tid == 0) trace(trp, c, 10);
+        if (ncols > 96) tmem_ld32(tS + HCols::kS + 96, sb);
+        if (ncols > 64) {
+          tmem_wait_ld();
+          if (tid == 0) trace(trp, c, 12);
+          LSRM_STREAM_PIECE(sa, 2)
+          if (ncols > 96) LSRM_STREAM_PIECE(sb, 3)
+        }
+#undef LSRM_STREAM_PIECE
+        const float m_cand = fmaxf(m_run, mx * sl2);
+        const bool need = m_cand > m_run + kHeadroom;
+        if (__any_sync(0xffffffffu, need)) {
+          // the chunk max left the headroom: rescale O, recompute P(c)
+          const float m_use = need ? m_cand : m_run;
+          const float scale = need ? ex2(m_run - m_cand) : 1.f;
+          tmem_wait_st();
+#pragma unroll
+          for (int c0 = 0; c0 < DH; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16_nowait(tO + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
+            tmem_st16(tO + c0, r);
+          }
+          uint32_t rl[1];
+          tmem_ld_cols<1>(tO + DH, rl);
+          tmem_wait_ld();
+          rl[0] = __float_as_uint(__uint_as_float(rl[0]) * scale);
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tO + DH),
+                       "r"(rl[0])
+                       : "memory");
+          const float nb2 = -m_use;
+#pragma unroll
+          for (int pc = 0; pc < kGroups / 2; ++pc) {
+            if (pc * 32 < ncols) {
+              tmem_ld32(tS + HCols::kS + 32 * pc, sa);
+              tmem_wait_ld();
+              uint32_t w[16];
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                const int gi = 2 * pc + hf;
+                if ((live >> gi) & 1u) {
+                  if ((tail >> gi) & 1u) mask16(sa + 16 * hf, D.gnv[gi]);
+                  exp16(sa + 16 * hf, sl2, ((visb >> gi) & 1u) ? nb2 : kNegInf, w + 8 * hf);
+                } else {
+                  zero8(w + 8 * hf);
+                }
+              }
+              tmem_st16(tP + 16 * pc, w);
+            }
+          }
+          m_run = m_use;
+        }
+        tc_before_sync();
+        mbar_arrive(&S.s_free[hh]);   // S(c) no longer read: QK(c+1) may overwrite it
+      }
       if (tid == 0) trace(trp, c, 13);
       tmem_wait_st();
       if (tid == 0) trace(trp, c, 14);

@@ -49,7 +49,7 @@ def main():
             tot += ms
             print(f"attention {use}: {ms * 1e3:8.1f} us")
         print(f"attention total: {tot * 1e3:8.1f} us")
-    buf = torch.zeros((512, 16), dtype=torch.int64, device="cuda")
+    buf = torch.zeros((256, 32), dtype=torch.int64, device="cuda")
     call("lsrm_debug_set_trace", buf.data_ptr())
     eng.attend(args.use)
     torch.cuda.synchronize()
@@ -90,6 +90,12 @@ def main():
     sub = [(3, 1, "S seen -> first ld done (LSRM_TRACE_LD)"), (3, 8, "S seen -> ld wait done"), (8, 9, "vis+max pass1"), (9, 10, "ld 2,3 + max"),
            (10, 11, "rescale"), (11, 13, "exps (+reload)"), (13, 14, "wait st"),
            (14, 15, "epilogue"), (15, 4, "arrive")]
+    one = tr[c, 11] > tr[c, 8]   # one-pass chunks: 11 is stamped after the turn barrier
+    sub += [(8, 11, "1-pass: wait turn"), (11, 9, "1-pass: piece 0"), (9, 10, "1-pass: piece 1"),
+            (10, 12, "1-pass: ld 2,3 wait"), (12, 13, "1-pass: pieces 2,3 + check"),
+            (11, 16, "p0: enter+mask"), (16, 17, "p0: max"), (17, 18, "p0: exps"),
+            (18, 19, "p0: st"), (19, 20, "p1: enter+mask"), (20, 21, "p1: max"),
+            (21, 22, "p1: exps"), (22, 23, "p1: st")]
     for a, b, nm in sub:
         v = tr[c, b] - tr[c, a]
         v = v[(tr[c, a] > 0) & (tr[c, b] > 0)]

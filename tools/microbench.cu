@@ -3,6 +3,7 @@
 // load throughput (tcgen05.ld 32x32b.x32) per SM.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb tools/microbench.cu && /tmp/mb
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -81,6 +82,88 @@ __global__ void tmem_ld_kernel(float* out, long long* clk, int nwarps_active) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base));
 }
 
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pk(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
+// softmax exp-phase pattern: per iteration 128 keys per thread (4 pieces of
+// 32): [ld S piece] -> 32 x (FFMA + MUFU) -> 16 F2FP -> st P piece
+template <int MODE>
+__global__ void exp_phase_kernel(float* out, long long* clk, int active_warps) {
+  __shared__ uint32_t base;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = base + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 256;
+  float acc = 0.f;
+  const float sl2 = 0.25f, nb = -1.f;
+  long long t0 = clock64();
+  if (warp < active_warps) {
+    uint32_t sa[32];
+    if (MODE != 0) { ld32(tm, sa); asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+    else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sa[j] = __float_as_uint(-0.01f * j);
+    }
+    for (int it = 0; it < 64; ++it) {
+#pragma unroll 1
+      for (int pc = 0; pc < 4; ++pc) {
+        if (MODE == 2) { ld32(tm + 32 * pc, sa); asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+        uint32_t w[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          w[j] = pk(ex2f(fmaf(__uint_as_float(sa[2 * j]), sl2, nb)),
+                    ex2f(fmaf(__uint_as_float(sa[2 * j + 1]), sl2, nb)));
+        if (MODE >= 1) st16(tm + 128 + 16 * pc, w);
+        else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc += __uint_as_float(w[j]);
+        }
+      }
+    }
+    if (MODE >= 1) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base));
+}
+
 int main() {
   float* out;
   long long* clk;
@@ -113,5 +196,20 @@ int main() {
     double bytes = (double)(kIters / 16) * 32 * 32 * 4 * w;
     printf("tcgen05.ld x32, %2d warps: %.1f B/clk/SM (%lld clk)\n", w, bytes / h[0], h[0]);
   }
+  const char* en[3] = {"regs only", "+st P", "+ld S +st P"};
+  for (int mode = 0; mode < 3; ++mode)
+    for (int w = 4; w <= 8; w += 4) {
+      for (int rep = 0; rep < 2; ++rep) {
+        if (mode == 0) exp_phase_kernel<0><<<148, 256>>>(out, clk, w);
+        if (mode == 1) exp_phase_kernel<1><<<148, 256>>>(out, clk, w);
+        if (mode == 2) exp_phase_kernel<2><<<148, 256>>>(out, clk, w);
+      }
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("exp_phase failed: %s\n", cudaGetErrorString(e)); return 1; }
+      cudaMemcpy(h, clk, sizeof(h), cudaMemcpyDeviceToHost);
+      double elems = 64.0 * 128 * 32 * w;
+      printf("exp phase %-12s warps %d: %.2f exp/clk/SM (%.0f clk per 128x128-per-warp-group chunk-equivalent)\n",
+             en[mode], w, elems / h[0], (double)h[0] / 64);
+    }
   return 0;
 }
