@@ -216,17 +216,35 @@ int lsrm_kv_interleave(int src_is_bf16, const void* src, int64_t ld_src,
  * kernel fills with clock64() stamps per chunk/event (NULL disables). */
 int lsrm_debug_set_trace(void* buf);
 
-/* Fused K/V preparation for the bf16 engine: token rows [n, hkv*dh] bf16 in
- * block-major order (row stride ld) -> padded interleaved layout (pad_row[i] =
- * padded row of token i; ones_cols 16 for V) + fp32 ResBlock rows r_out
- * [n, hkv*dh] + (if mean_out) the per-block means [n_blocks, hkv*dh] over the
- * contiguous block ranges block_offsets (block_partition.py:141-167). */
-int lsrm_kv_prepare(const void* src, int64_t ld, int64_t n, int hkv, int dh,
-                    const int32_t* pad_row, int64_t n_rows_pad, void* il,
-                    int ones_cols, const float* w1, const float* b1,
-                    const float* w2, const float* b2, float* r_out,
-                    const int64_t* block_offsets, int64_t n_blocks,
-                    float* mean_out, void* stream);
+/* K/V preparation of the bf16 engine, every (use, K|V) tensor of a layer in
+ * ONE launch (nsa_attention.py:305-312 with block_partition.py:141-167 fused
+ * in).  One job per tensor: token rows src [n, hkv*dh] bf16 (row stride ld) in
+ * block-major order; blk_off [n_blocks+1] token offsets and pad_off
+ * [n_blocks+1] 16-row-padded offsets into il.  Writes the interleaved layout
+ * il [hkv][rows_pad][dh+ones_cols] (ones_cols = 16 for V: row-sum columns), the
+ * ResBlock block means (tensor-core bf16 MLP, fp32 accumulation, fixed-order
+ * sums) to mean_out [n_blocks][hkv*dh] f32 and/or, interleaved, to cmp_il
+ * [hkv][cmp_rows_pad][dh+ones_cols] (either may be NULL).  jobs points to
+ * DEVICE memory; hkv*dh must be 64 or 128. */
+typedef struct lsrm_kv_job {
+  const void* src;
+  int64_t ld;
+  const int64_t* blk_off;
+  const int64_t* pad_off;
+  int64_t n_blocks;
+  int64_t rows_pad;
+  void* il;
+  int64_t ones_cols;
+  const float* w1;
+  const float* b1;
+  const float* w2;
+  const float* b2;
+  float* mean_out;
+  void* cmp_il;
+  int64_t cmp_rows_pad;
+} lsrm_kv_job;
+int lsrm_kv_prepare_jobs(const lsrm_kv_job* jobs, int n_jobs, int64_t max_blocks, int hkv,
+                         int dh, void* stream);
 
 /* Byte-segment copy: segs [n_segs, 3] int64 = (src offset, dst offset,
  * bytes), all multiples of 16.  Places all-gathered per-rank KV shards into

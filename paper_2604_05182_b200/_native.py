@@ -55,8 +55,7 @@ SIGNATURES = {
                                  P, P]),
     "lsrm_debug_set_trace": (I32, [P]),
     "lsrm_copy_segments": (I32, [P, P, P, I64, P]),
-    "lsrm_kv_prepare": (I32, [P, I64, I64, I32, I32, P, I64, P, I32, P, P, P, P, P, P, I64,
-                              P, P]),
+    "lsrm_kv_prepare_jobs": (I32, [P, I32, I64, I32, I32, P]),
     "lsrm_gather_rows": (I32, [I32, P, I64, P, I64, I64, P, I64, P]),
     "lsrm_scatter_rows": (I32, [I32, P, I64, P, I64, I64, P, I64, P]),
     "lsrm_cast": (I32, [I32, P, P, I64, P]),

@@ -10,10 +10,11 @@ block-major order of each modality's own partition, so that
 
 Per layer and stream, ONE bf16 GEMM (cuBLAS) computes all projections that
 read that stream: the q and gate columns of its two query uses and the k/v
-columns of the two uses that read it as KV.  Then per use: the fused K/V
-preparation (interleaved layout + fp32 ResBlock + block mean,
-csrc/compress.cu), the fused tcgen05 three-branch attention with the gated
-merge (csrc/attn_tc.cu), and the W_o GEMM.
+columns of the two uses that read it as KV.  Then ONE launch prepares the K/V
+of all four uses (interleaved layout + tensor-core ResBlock + block mean,
+written straight into the compressed layout; csrc/kv_prep.cu), and per use
+the fused tcgen05 three-branch attention with the gated merge
+(csrc/attn_tc.cu) and the W_o GEMM.
 
 Sharding (block-aware sequence parallelism, seq_parallel.py): an engine can
 own only a subset of each stream's blocks.  Its query side then works on the
@@ -29,6 +30,8 @@ stated in DESIGN.md and enforced in tests/test_gpu_parity.py.
 """
 
 from dataclasses import dataclass
+
+import ctypes as C
 
 import numpy as np
 import torch
@@ -50,6 +53,15 @@ ONES_COLS = 16   # extra V columns (1 = real key) that make P.V also emit row su
 
 def _padded(occ: np.ndarray) -> np.ndarray:
     return (occ + ROW_PAD - 1) // ROW_PAD * ROW_PAD
+
+
+class KvJob(C.Structure):
+    """Mirror of `lsrm_kv_job` (include/lsrm_b200.h)."""
+    _fields_ = [("src", C.c_void_p), ("ld", C.c_int64), ("blk_off", C.c_void_p),
+                ("pad_off", C.c_void_p), ("n_blocks", C.c_int64), ("rows_pad", C.c_int64),
+                ("il", C.c_void_p), ("ones_cols", C.c_int64), ("w1", C.c_void_p),
+                ("b1", C.c_void_p), ("w2", C.c_void_p), ("b2", C.c_void_p),
+                ("mean_out", C.c_void_p), ("cmp_il", C.c_void_p), ("cmp_rows_pad", C.c_int64)]
 
 
 class PackedShard:
@@ -87,6 +99,7 @@ class StreamMeta:
     loc_off_host: np.ndarray
     loc_pad_row: torch.Tensor   # [n_loc] int32 padded row in the local compact layout
     loc_pad_off_host: np.ndarray
+    loc_pad_off: torch.Tensor   # [B_loc+1] int64 padded offsets in the local compact layout
     n_loc_rows_pad: int
     sharded: bool
 
@@ -107,8 +120,8 @@ def stream_meta(part: BlockPartition, owned=None) -> StreamMeta:
     return StreamMeta(part, part.n_tokens, part.n_occupied, part.dev("block_offsets"),
                       D.dev(pad_off), pad_off, int(pad_off[-1]), owned, int(loc_off[-1]),
                       D.dev(loc2glob.astype(np.int64)), D.dev(loc_off), loc_off,
-                      D.dev(loc_pad_row.astype(np.int32)), loc_pad_off, int(loc_pad_off[-1]),
-                      sharded)
+                      D.dev(loc_pad_row.astype(np.int32)), loc_pad_off, D.dev(loc_pad_off),
+                      int(loc_pad_off[-1]), sharded)
 
 
 def query_tiles(part: BlockPartition, group: int, self_use: bool, owned=None) -> np.ndarray:
@@ -213,17 +226,18 @@ class SparseLayerEngine:
         for s in ("x", "y"):
             m = self.meta[s]
             self.buf[("Y", s)] = D.empty((m.n_loc, ncol[s]), torch.bfloat16)
-            # global KV (zeroed once: padding rows and their ones columns stay 0)
-            self.buf[("k_il", s)] = D.zeros((hkv, m.n_rows_pad, dh), torch.bfloat16)
-            self.buf[("v_il", s)] = D.zeros((hkv, m.n_rows_pad, dh + ONES_COLS), torch.bfloat16)
-            bpad = (m.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
-            self.buf[("kc_il", s)] = D.empty((hkv, bpad, dh), torch.bfloat16)
-            self.buf[("vc_il", s)] = D.empty((hkv, bpad, dh + ONES_COLS), torch.bfloat16)
-            self.buf[("kc", s)] = D.empty((m.n_blocks, w), torch.float32)
-            self.buf[("vc", s)] = D.empty((m.n_blocks, w), torch.float32)
-            self.buf[("scratch", s)] = D.empty((max(m.n_loc, 1), w), torch.float32)
         for use in USES:
             qs, ks, _ = USE_GEOM[use]
+            m = self.meta[ks]
+            # global KV of this use (zeroed once: padding rows, their ones
+            # columns and the compressed padding rows stay 0)
+            self.buf[("k_il", use)] = D.zeros((hkv, m.n_rows_pad, dh), torch.bfloat16)
+            self.buf[("v_il", use)] = D.zeros((hkv, m.n_rows_pad, dh + ONES_COLS), torch.bfloat16)
+            bpad = (m.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
+            self.buf[("kc_il", use)] = D.zeros((hkv, bpad, dh), torch.bfloat16)
+            self.buf[("vc_il", use)] = D.zeros((hkv, bpad, dh + ONES_COLS), torch.bfloat16)
+            self.buf[("kc", use)] = D.empty((m.n_blocks, w), torch.float32)
+            self.buf[("vc", use)] = D.empty((m.n_blocks, w), torch.float32)
             self.buf[("merged", use)] = D.empty((self.meta[qs].n_loc, d), torch.bfloat16)
             self.buf[("out", use)] = D.empty((self.meta[qs].n_loc, d), torch.bfloat16)
             m = self.meta[ks]
@@ -241,6 +255,40 @@ class SparseLayerEngine:
                     lay.n_blocks, w)
                 self.buf[("vc_loc", use)] = buf[lay.off_vc:].view(torch.float32).view(
                     lay.n_blocks, w)
+        self._build_kv_jobs()
+
+    def _build_kv_jobs(self):
+        """Device array of `lsrm_kv_job`: K and V of every use (one launch)."""
+        p = self.params
+        jobs, self._job_refs = [], []
+        max_blocks = 0
+        for use in USES:
+            _, ks, _ = USE_GEOM[use]
+            m = self.meta[ks]
+            if not m.n_loc:
+                continue
+            Y = self.buf[("Y", ks)]
+            for kind, wres in (("k", self.cmp_w[use][0]), ("v", self.cmp_w[use][1])):
+                src = Y[:, self.cols[(use, kind)]:]
+                w1, b1, w2, b2 = wres
+                if m.sharded:   # rank-local compact shard; means go to the packed buffer
+                    il = self.buf[(kind + "_loc", use)]
+                    blk, pad, nb = m.loc_off, m.loc_pad_off, m.owned.size
+                    mean, cmp_il = self.buf[(kind + "c_loc", use)], None
+                else:           # global layout; compressed rows straight to the kernel layout
+                    il = self.buf[(kind + "_il", use)]
+                    blk, pad, nb = m.kv_off, m.pad_off, m.n_blocks
+                    mean, cmp_il = None, self.buf[(kind + "c_il", use)]
+                jobs.append(KvJob(src.data_ptr(), Y.stride(0), blk.data_ptr(), pad.data_ptr(), nb,
+                                  int(il.shape[1]), il.data_ptr(),
+                                  ONES_COLS if kind == "v" else 0, w1.data_ptr(), b1.data_ptr(),
+                                  w2.data_ptr(), b2.data_ptr(), D.ptr(mean), D.ptr(cmp_il),
+                                  int(cmp_il.shape[1]) if cmp_il is not None else 0))
+                self._job_refs += [src, il, blk, pad, mean, cmp_il]
+                max_blocks = max(max_blocks, nb)
+        raw = b"".join(C.string_at(C.addressof(j), C.sizeof(j)) for j in jobs)
+        self.kv_jobs = D.dev(np.frombuffer(raw, dtype=np.uint8).copy()) if jobs else None
+        self.n_kv_jobs, self.kv_max_blocks = len(jobs), max_blocks
 
     # -- pieces --------------------------------------------------------------
     def project(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
@@ -249,34 +297,13 @@ class SparseLayerEngine:
         if self.meta["y"].n_loc:
             _ops.gemm(y_loc, self.w_cat["y"], out=self.buf[("Y", "y")])
 
-    def prepare_kv(self, use: str):
-        """K/V of the owned KV blocks: interleaved layout + compression.
-        Unsharded engines write the global buffers directly."""
-        _, ks, _ = USE_GEOM[use]
-        m, p = self.meta[ks], self.params
-        Y = self.buf[("Y", ks)]
-        ld = Y.stride(0)
-        st = D.stream()
-        for kind, wres in (("k", self.cmp_w[use][0]), ("v", self.cmp_w[use][1])):
-            col = self.cols[(use, kind)]
-            src = Y[:, col:]
-            ones = ONES_COLS if kind == "v" else 0   # V gets the row-sum columns
-            w1, b1, w2, b2 = wres
-            if m.sharded:
-                il = self.buf[(kind + "_loc", use)]
-                rows_pad = int(il.shape[1])
-                cmp, offs, nb = self.buf[(kind + "c_loc", use)], m.loc_off, m.owned.size
-            else:
-                il, rows_pad = self.buf[(kind + "_il", ks)], m.n_rows_pad
-                cmp, offs, nb = self.buf[(kind + "c", ks)], m.kv_off, m.n_blocks
-            if m.n_loc:
-                # fused: interleaved K/V layout + fp32 ResBlock + per-block mean
-                call("lsrm_kv_prepare", src.data_ptr(), ld, m.n_loc, p.n_kv_heads, p.head_dim,
-                     m.loc_pad_row.data_ptr(), rows_pad, il.data_ptr(), ones, w1.data_ptr(),
-                     b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
-                     self.buf[("scratch", ks)].data_ptr(), offs.data_ptr(), nb, cmp.data_ptr(), st)
-        if not m.sharded:
-            self.finish_kv(use)
+    def prepare_kv(self):
+        """K/V of all four uses in one launch (owned KV blocks when sharded;
+        unsharded engines write the global buffers, compressed rows included)."""
+        if self.n_kv_jobs:
+            p = self.params
+            call("lsrm_kv_prepare_jobs", self.kv_jobs.data_ptr(), self.n_kv_jobs,
+                 self.kv_max_blocks, p.n_kv_heads, p.head_dim, D.stream())
 
     def finish_kv(self, use: str):
         """Compressed rows (global, canonical order) -> interleaved layout."""
@@ -285,7 +312,7 @@ class SparseLayerEngine:
         st = D.stream()
         for kind in ("k", "v"):
             ones = ONES_COLS if kind == "v" else 0
-            cmp, il = self.buf[(kind + "c", ks)], self.buf[(kind + "c_il", ks)]
+            cmp, il = self.buf[(kind + "c", use)], self.buf[(kind + "c_il", use)]
             call("lsrm_kv_interleave", 0, cmp.data_ptr(), self.w, m.n_blocks, p.n_kv_heads,
                  p.head_dim, ones, None, None, 0, None, int(il.shape[1]), il.data_ptr(), st)
 
@@ -299,10 +326,10 @@ class SparseLayerEngine:
         qcol = self.cols[(use, "q")]
         q = Y[:, qcol:]
         call("lsrm_nsa_attention_tc", q.data_ptr(), Y.stride(0), mq.n_loc, p.n_q_heads,
-             p.n_kv_heads, p.head_dim, self.buf[("k_il", ks)].data_ptr(),
-             self.buf[("v_il", ks)].data_ptr(), mk.pad_off.data_ptr(), mk.kv_off.data_ptr(),
-             mk.n_rows_pad, self.buf[("kc_il", ks)].data_ptr(),
-             self.buf[("vc_il", ks)].data_ptr(), mk.n_blocks, tiles.data_ptr(),
+             p.n_kv_heads, p.head_dim, self.buf[("k_il", use)].data_ptr(),
+             self.buf[("v_il", use)].data_ptr(), mk.pad_off.data_ptr(), mk.kv_off.data_ptr(),
+             mk.n_rows_pad, self.buf[("kc_il", use)].data_ptr(),
+             self.buf[("vc_il", use)].data_ptr(), mk.n_blocks, tiles.data_ptr(),
              int(tiles.shape[0]), self.rows[use].data_ptr(), self.count[use].data_ptr(),
              self.kmax[use], Y.data_ptr(), Y.stride(0), qcol + self.d,
              self.gate_b[use].data_ptr(), ng, self.buf[("merged", use)].data_ptr(), D.stream())
@@ -320,8 +347,8 @@ class SparseLayerEngine:
             self.forward_local(x_loc, y_loc)
             return self.forward_exchange()
         self.project(x_loc, y_loc)
+        self.prepare_kv()
         for use in USES:
-            self.prepare_kv(use)
             self.attend(use)
             self.output(use)
         return {u: self.buf[("out", u)] for u in USES}
@@ -329,8 +356,7 @@ class SparseLayerEngine:
     def forward_local(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
         """Sharded phase 1: projections and this rank's KV shards of all uses."""
         self.project(x_loc, y_loc)
-        for use in USES:
-            self.prepare_kv(use)
+        self.prepare_kv()
 
     def forward_exchange(self) -> dict:
         """Sharded phase 2: launch all four All-gather-KV exchanges (in flight

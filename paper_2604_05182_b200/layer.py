@@ -159,21 +159,24 @@ class SparseAttentionLayer:
             ev[1].record(st)
             torch.cuda.synchronize()
             acc["project_gemm"] += ev[0].elapsed_time(ev[1])
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record(st)
+            e.prepare_kv()
+            ev[1].record(st)
+            torch.cuda.synchronize()
+            acc["kv_prep"] += ev[0].elapsed_time(ev[1])
             for u in USES:
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 ev[0].record(st)
-                e.prepare_kv(u)
-                ev[1].record(st)
                 e.attend(u)
-                ev[2].record(st)
+                ev[1].record(st)
                 e.output(u)
-                ev[3].record(st)
+                ev[2].record(st)
                 torch.cuda.synchronize()
-                acc["kv_prep"] += ev[0].elapsed_time(ev[1])
-                a = ev[1].elapsed_time(ev[2])
+                a = ev[0].elapsed_time(ev[1])
                 acc["attention"] += a
                 per_use[u] += a
-                acc["wo_gemm"] += ev[2].elapsed_time(ev[3])
+                acc["wo_gemm"] += ev[1].elapsed_time(ev[2])
         out = {f"{n}_ms": v / reps for n, v in acc.items()}
         out["attention_per_use_ms"] = {u: v / reps for u, v in per_use.items()}
         return out

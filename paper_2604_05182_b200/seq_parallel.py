@@ -335,8 +335,8 @@ class KVExchange:
         _, ks, _ = USE_GEOM[use]
         st = D.stream()
         stage = self.stage[use]
-        for kind, dst in (("k", engine.buf[("k_il", ks)]), ("v", engine.buf[("v_il", ks)]),
-                          ("kc", engine.buf[("kc", ks)]), ("vc", engine.buf[("vc", ks)])):
+        for kind, dst in (("k", engine.buf[("k_il", use)]), ("v", engine.buf[("v_il", use)]),
+                          ("kc", engine.buf[("kc", use)]), ("vc", engine.buf[("vc", use)])):
             segs = self.segs[ks][kind]
             call("lsrm_copy_segments", stage.data_ptr(), dst.data_ptr(), segs.data_ptr(),
                  int(segs.shape[0]), st)
