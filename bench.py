@@ -301,7 +301,10 @@ def run_gpu(args):
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{src} bf16_tflops (burst)",
-                     "algorithmic_flops_per_step": attn_flops},
+                     "algorithmic_flops_per_step": attn_flops,
+                     # d_h = 32: 4*d_h flops per (row, key) pair against one exp2 on
+                     # the MUFU (16/clk/SM), so the special-function unit binds first
+                     "mufu": mufu_roofline(attn_flops, attn_ms, layer.inst.params, peaks)},
         "breakdown_ms": brk,
         "layer_tflops": (attn_flops + proj_flops) / (ms * 1e-3) / 1e12,
         "cpu_baseline": cpu,
@@ -311,6 +314,18 @@ def run_gpu(args):
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
+
+
+def mufu_roofline(attn_flops, attn_ms, params, peaks):
+    """Exponentials of the useful (row, key) pairs (4*d_h flops each) per second
+    against the MUFU ex2 peak (16 per clock per SM, measured in
+    tools/microbench.cu) x SMs x max SM clock."""
+    import torch
+    exps = attn_flops / (4.0 * params.head_dim)
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    peak = 16.0 * n_sm * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    ach = exps / (attn_ms * 1e-3)
+    return {"achieved": ach / 1e9, "peak": peak / 1e9, "unit": "Gexp/s", "frac": ach / peak}
 
 
 WORKLOAD_DESC = {
