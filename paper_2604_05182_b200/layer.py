@@ -119,31 +119,24 @@ class SparseAttentionLayer:
         return {u: outs[u].numpy() for u in USES}
 
     def time_host_path(self, x_hat, y_hat, steps=5):
-        """Mean ms of forward_host with pinned host buffers; H2D/D2H bytes."""
+        """End-to-end throughput of the host API path over `steps` layer calls.
+
+        Every step copies its f32 inputs from pinned host memory, runs the
+        layer (permute/cast, four NSA uses, un-permute/cast) and copies the
+        four f32 outputs back to pinned host memory. Steps are pipelined two
+        deep: H2D, compute and D2H run on their own streams, with double-
+        buffered device staging. Step k's D2H therefore overlaps step k+1's
+        H2D and compute. Returns (mean ms per step from the first H2D to the
+        last D2H, H2D bytes per step, D2H bytes per step)."""
         xp = torch.from_numpy(np.ascontiguousarray(x_hat, np.float32)).pin_memory()
         yp = torch.from_numpy(np.ascontiguousarray(y_hat, np.float32)).pin_memory()
-        pinned = {u: torch.empty(tuple(self._out32[u].shape), dtype=torch.float32,
-                                 pin_memory=True) for u in USES}
-        st = torch.cuda.current_stream()
-
-        def once():
-            self._stage["x"].copy_(xp, non_blocking=True)
-            self._stage["y"].copy_(yp, non_blocking=True)
-            res = self._forward_from_stage()
-            for u in USES:
-                pinned[u].copy_(res[u], non_blocking=True)
-
-        once()
+        pipe = HostPipeline(self, n_slots=2)
+        pipe.run(xp, yp, 2)          # warm-up (graph capture inside)
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        for _ in range(steps):
-            once()
-        b.record(st)
-        torch.cuda.synchronize()
+        ms = pipe.run(xp, yp, steps)
         h2d = xp.numel() * 4 + yp.numel() * 4
-        d2h = sum(p.numel() * 4 for p in pinned.values())
-        return a.elapsed_time(b) / steps, h2d, d2h
+        d2h = sum(t.numel() * 4 for t in pipe.host_out[0].values())
+        return ms, h2d, d2h
 
     def profile_breakdown(self, x_bm, y_bm, reps=5):
         """Device time per kernel class (events on the launching stream)."""
@@ -180,3 +173,85 @@ class SparseAttentionLayer:
         out = {f"{n}_ms": v / reps for n, v in acc.items()}
         out["attention_per_use_ms"] = {u: v / reps for u, v in per_use.items()}
         return out
+
+
+class HostPipeline:
+    """Two-deep pipeline of host-API layer calls (H2D | compute | D2H streams).
+
+    Slot s owns device staging (f32 inputs, f32 outputs) and pinned host
+    outputs. Its compute is one CUDA graph: gather/cast to block-major bf16,
+    the engine's four NSA uses, cast/scatter back to token order. Engine
+    buffers are shared, because compute is serialised on one stream."""
+
+    def __init__(self, layer: SparseAttentionLayer, n_slots: int = 2):
+        self.layer, self.n = layer, n_slots
+        inst, eng = layer.inst, layer.engine
+        d = inst.params.model_dim
+        self.stage = [{"x": D.empty((inst.n_vol, d), torch.float32),
+                       "y": D.empty((inst.n_img, d), torch.float32)} for _ in range(n_slots)]
+        self.dev_out = [{u: D.empty((eng.meta[USE_GEOM[u][0]].n, d), torch.float32) for u in USES}
+                        for _ in range(n_slots)]
+        self.host_out = [{u: torch.empty(tuple(t.shape), dtype=torch.float32, pin_memory=True)
+                          for u, t in slot.items()} for slot in self.dev_out]
+        self.s_in, self.s_comp, self.s_out = (torch.cuda.Stream() for _ in range(3))
+        self.graphs = None
+
+    def _compute(self, slot: int):
+        lay, eng = self.layer, self.layer.engine
+        from ._native import call
+        for s in ("x", "y"):
+            bm32 = _ops.gather_rows(self.stage[slot][s], lay.tok[s])
+            call("lsrm_cast", 1, bm32.data_ptr(), lay._bm[s].data_ptr(), bm32.numel(), D.stream())
+        outs = eng.forward(lay._bm["x"], lay._bm["y"])
+        for u in USES:
+            o32 = _ops.cast(outs[u], torch.float32)
+            _ops.scatter_rows(o32, lay.tok[USE_GEOM[u][0]], self.dev_out[slot][u])
+
+    def _capture(self):
+        self.graphs = []
+        with torch.cuda.stream(self.s_comp):
+            for slot in range(self.n):          # warm-up outside capture
+                self._compute(slot)
+        torch.cuda.synchronize()
+        for slot in range(self.n):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.s_comp):
+                self._compute(slot)
+            self.graphs.append(g)
+        torch.cuda.synchronize()
+
+    def run(self, xp: torch.Tensor, yp: torch.Tensor, steps: int) -> float:
+        if self.graphs is None:
+            self._capture()
+        ev = lambda: torch.cuda.Event(enable_timing=False)   # noqa: E731
+        consumed = [None] * self.n     # compute finished with the slot's staging
+        drained = [None] * self.n      # D2H finished with the slot's outputs
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(self.s_in)
+        for k in range(steps):
+            s = k % self.n
+            with torch.cuda.stream(self.s_in):
+                if consumed[s] is not None:
+                    self.s_in.wait_event(consumed[s])
+                self.stage[s]["x"].copy_(xp, non_blocking=True)
+                self.stage[s]["y"].copy_(yp, non_blocking=True)
+                e_in = ev()
+                e_in.record(self.s_in)
+            with torch.cuda.stream(self.s_comp):   # replay() launches on the current stream
+                self.s_comp.wait_event(e_in)
+                if drained[s] is not None:
+                    self.s_comp.wait_event(drained[s])
+                self.graphs[s].replay()
+                e_c = ev()
+                e_c.record(self.s_comp)
+            consumed[s] = e_c
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(e_c)
+                for u in USES:
+                    self.host_out[s][u].copy_(self.dev_out[s][u], non_blocking=True)
+                e_o = ev()
+                e_o.record(self.s_out)
+                drained[s] = e_o
+        t1.record(self.s_out)
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1) / steps
