@@ -287,6 +287,7 @@ def run_gpu(args):
         cpu = {"value": tok / secs, "unit": "tokens/s", "cores": hi["cpu_count"],
                "kind": "port", "sample": desc}
     proj_flops = layer.engine.projection_flops()
+    block = time_sparse_block(inst, n_tok, args.steps)
     line = {
         "metric": "LSRM sparse-attn layer tokens/s", "value": n_tok / (ms * 1e-3),
         "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -307,6 +308,7 @@ def run_gpu(args):
                      "mufu": mufu_roofline(attn_flops, attn_ms, layer.inst.params, peaks)},
         "breakdown_ms": brk,
         "layer_tflops": (attn_flops + proj_flops) / (ms * 1e-3) / 1e12,
+        "sparse_block": block,
         "cpu_baseline": cpu,
         "e2e": {"value": n_tok / (e2e_ms * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
@@ -314,6 +316,50 @@ def run_gpu(args):
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
+
+
+def time_sparse_block(inst, n_tok, steps):
+    """The full Stage-2 block around the four uses (injection + LayerNorm,
+    use-gate mixture, FFN 4d, residuals; recon_pipeline.py:461-497) on the
+    bf16 engine, CUDA graph, device events, L2 flushed between steps.
+    Reported next to the layer metric."""
+    import torch
+    from paper_2604_05182_b200 import _dev as D, _ops
+    from paper_2604_05182_b200.recon_pipeline import SparseBlockEngine, init_sparse_block
+    w = init_sparse_block(0, inst.params, 0)
+    eng = SparseBlockEngine(inst.part_vol, inst.part_img, inst.plan_rows, w, inst.params)
+    d = inst.params.model_dim
+    g = torch.Generator(device="cuda").manual_seed(0)
+    ins = [torch.randn((n, d), generator=g, device="cuda", dtype=torch.float32)
+           for n in (inst.n_vol, inst.n_img, inst.n_vol, inst.n_img)]
+    st = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    side.wait_stream(st)
+    with torch.cuda.stream(side):
+        eng.forward(*ins)
+    st.wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        eng.forward(*ins)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    for a, b in evs:
+        flush.zero_()
+        a.record(st)
+        graph.replay()
+        b.record(st)
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    ffn_flops = 2.0 * n_tok * d * 4 * d * 2
+    gate_flops = 2.0 * n_tok * d * 2 * d
+    return {"ms_per_step": ms, "tokens_per_s": n_tok / (ms * 1e-3),
+            "what": "one Stage-2 sparse block: 4 gated NSA uses + injection/LayerNorm, "
+                    "use-gate mixture, FFN 4d (erf gelu), residuals; bf16 engine",
+            "ffn_and_gate_gflop": (ffn_flops + gate_flops) / 1e9}
 
 
 def mufu_roofline(attn_flops, attn_ms, params, peaks):

@@ -265,6 +265,28 @@ int lsrm_layer_norm(int in_bf16, const void* x, int64_t n, int d,
                     const float* gamma, const float* beta, float eps,
                     int out_bf16, void* y, void* stream);
 
+/* ---- Stage-2 sparse block around the NSA uses (recon_pipeline.py:461-497) --
+ * exact = 1: the reference's f32 storage with f64 arithmetic (reference API);
+ * exact = 0: fp32 arithmetic (bf16 engine).  Row kernels run a warp per row
+ * with f64 LayerNorm statistics (tensor_core.py:139-146).
+ * add_layer_norm: sum_out = f32(a + b) (b may be NULL), y = LN(sum_out). */
+int lsrm_add_layer_norm(const float* a, const void* b, int b_bf16, int64_t n, int d,
+                        const float* gamma, const float* beta, float eps,
+                        float* sum_out, int out_bf16, void* y, void* stream);
+/* x1 = f32(xe + sigmoid(gl[:, :d] + gb[:d]) * o_self
+ *           + sigmoid(gl[:, d:2d] + gb[d:]) * o_cross),  h = LN(x1). */
+int lsrm_gate_mix_layer_norm(int exact, const float* xe, const void* gate_logits,
+                             int64_t ld_gl, int gl_bf16, const float* gate_b,
+                             const void* o_self, const void* o_cross, int o_bf16,
+                             int64_t n, int d, float* x1, const float* gamma,
+                             const float* beta, float eps, int out_bf16, void* h,
+                             void* stream);
+/* out = f32(act(f32(h + bias))) (+ residual f32 [n, cols]); act 0 = identity,
+ * 1 = exact-erf gelu (tensor_core.py:82-86). */
+int lsrm_bias_act(int exact, const void* h, int h_bf16, int64_t ld, const float* bias,
+                  int64_t n, int cols, int act, const float* residual, void* out,
+                  int out_bf16, int64_t ld_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

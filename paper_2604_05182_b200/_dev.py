@@ -54,3 +54,19 @@ def host(t):
 
 def is_device(x):
     return isinstance(x, torch.Tensor) and x.device.type == "cuda"
+
+
+_WCACHE = {}
+
+
+def weight(arr, dtype=torch.float32):
+    """Device copy of a host weight array, made once per (array, dtype,
+    device). Works for any weight container (this package's dataclasses or the
+    reference's), which is what the drop-in needs."""
+    key = (id(arr), dtype, torch.cuda.current_device())
+    hit = _WCACHE.get(key)
+    if hit is not None and hit[0] is arr:
+        return hit[1]
+    t = dev(arr, dtype)
+    _WCACHE[key] = (arr, t)
+    return t

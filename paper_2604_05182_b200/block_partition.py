@@ -147,7 +147,7 @@ def init_compress_weights(seed, width, *tags) -> CompressWeights:
 
 
 def _dev_res(p: ResBlockParams):
-    return [D.dev(a, torch.float32) for a in (p.w1, p.b1, p.w2, p.b2)]
+    return [D.weight(a) for a in (p.w1, p.b1, p.w2, p.b2)]
 
 
 def compress_rows(x, ld, n, width, params, part: BlockPartition, src_bf16=False, out=None,

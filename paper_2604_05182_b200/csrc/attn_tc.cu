@@ -736,6 +736,9 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
     // maxima and epilogue; warpgroup 1 lets warpgroup 0 go first
     const int bar_mine = 1 + hh, bar_other = 2 - hh;
     if (kPingPong && HP == 2 && hh == 1) named_arrive(bar_other, 256);
+#ifdef LSRM_WG1_DELAY_NS
+    if (HP == 2 && hh == 1) __nanosleep(LSRM_WG1_DELAY_NS);   // start out of phase
+#endif
     // one turn per 32-key piece: wait for ours, run the piece's exponentials,
     // hand over (the very last hand-over of warpgroup 1 has no taker)
     auto pp_turn = [&]() {

@@ -1,0 +1,169 @@
+// Stage-2 sparse residual block around the four NSA uses
+// (lsrm/recon_pipeline.py:461-497): injection + pre-norm, the two-gate
+// mixture of the self/cross NSA outputs with the residual, and the FFN
+// (affine-gelu-affine) with its residual.  The GEMMs are library GEMMs
+// (lsrm_gemm); these kernels are the fused row-wise / element-wise steps.
+//
+// exact = 1 reproduces the reference's f32 storage with f64 arithmetic (the
+// reference-API path, parity <= 1e-5); exact = 0 is the bf16 engine's fp32
+// arithmetic.
+#include "common.cuh"
+
+namespace lsrm {
+
+__device__ __forceinline__ double ld_any(const void* p, int bf16, int64_t i) {
+  return bf16 ? (double)__bfloat162float(((const __nv_bfloat16*)p)[i])
+              : (double)((const float*)p)[i];
+}
+__device__ __forceinline__ void st_any(void* p, int bf16, int64_t i, float v) {
+  if (bf16)
+    ((__nv_bfloat16*)p)[i] = __float2bfloat16_rn(v);
+  else
+    ((float*)p)[i] = v;
+}
+// sigmoid in f64, branch on sign as tensor_core.py:89-94
+__device__ __forceinline__ double sigmoid64(double x) {
+  return x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
+}
+
+// Warp per row: LayerNorm of the f32 row r (already in `row`, length d) with
+// f64 statistics (tensor_core.py:139-146) -> y.
+__device__ __forceinline__ void ln_row(const float* row, int d, const float* gamma,
+                                       const float* beta, float eps, int out_bf16, void* y,
+                                       int64_t yoff, int lane) {
+  double s = 0.0;
+  for (int c = lane; c < d; c += 32) s += (double)row[c];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const double mu = s / d;
+  double v = 0.0;
+  for (int c = lane; c < d; c += 32) {
+    const double t = (double)row[c] - mu;
+    v += t * t;
+  }
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const double inv = 1.0 / sqrt(v / d + (double)eps);
+  for (int c = lane; c < d; c += 32)
+    st_any(y, out_bf16, yoff + c,
+           (float)(((double)row[c] - mu) * inv * (double)gamma[c] + (double)beta[c]));
+}
+
+// sum = f32(a + b) (b optional), y = LayerNorm(sum)
+__global__ void add_ln_kernel(const float* __restrict__ a, const void* __restrict__ b,
+                              int b_bf16, int64_t n, int d, const float* __restrict__ gamma,
+                              const float* __restrict__ beta, float eps,
+                              float* __restrict__ sum_out, int out_bf16, void* y) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  float* row = sum_out + r * d;
+  for (int c = lane; c < d; c += 32)
+    row[c] = b ? (float)((double)a[r * d + c] + ld_any(b, b_bf16, r * d + c)) : a[r * d + c];
+  __syncwarp();
+  ln_row(row, d, gamma, beta, eps, out_bf16, y, r * d, lane);
+}
+
+// Two-gate mixture with the residual (recon_pipeline.py:474-490):
+//   g_self, g_cross = f32(sigmoid(f32(logit + bias)))     (logits [n, 2d])
+//   x1 = f32(xe + g_self * o_self + g_cross * o_cross)     (f64 sums)
+// then h = LayerNorm(x1) for the FFN.
+__global__ void gate_mix_ln_kernel(int exact, const float* __restrict__ xe,
+                                   const void* __restrict__ gl, int64_t ld_gl, int gl_bf16,
+                                   const float* __restrict__ gate_b,
+                                   const void* __restrict__ o_self,
+                                   const void* __restrict__ o_cross, int o_bf16, int64_t n,
+                                   int d, float* __restrict__ x1,
+                                   const float* __restrict__ gamma,
+                                   const float* __restrict__ beta, float eps, int out_bf16,
+                                   void* h) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  float* row = x1 + r * d;
+  for (int c = lane; c < d; c += 32) {
+    const double zs = (double)(float)(ld_any(gl, gl_bf16, r * ld_gl + c) + (double)gate_b[c]);
+    const double zc =
+        (double)(float)(ld_any(gl, gl_bf16, r * ld_gl + d + c) + (double)gate_b[d + c]);
+    double gs, gc;
+    if (exact) {
+      gs = (double)(float)sigmoid64(zs);
+      gc = (double)(float)sigmoid64(zc);
+    } else {
+      gs = (double)(1.f / (1.f + __expf(-(float)zs)));
+      gc = (double)(1.f / (1.f + __expf(-(float)zc)));
+    }
+    const double o = gs * ld_any(o_self, o_bf16, r * d + c) + gc * ld_any(o_cross, o_bf16, r * d + c);
+    row[c] = (float)((double)xe[r * d + c] + o);
+  }
+  __syncwarp();
+  ln_row(row, d, gamma, beta, eps, out_bf16, h, r * d, lane);
+}
+
+// out = f32(act(f32(h + bias)) [+ residual])   act: 0 identity, 1 exact-erf gelu
+__global__ void bias_act_kernel(int exact, const void* __restrict__ hin, int h_bf16, int64_t ld,
+                                const float* __restrict__ bias, int64_t n, int cols, int act,
+                                const float* __restrict__ residual, void* out, int out_bf16,
+                                int64_t ld_out) {
+  const int64_t total = n * (int64_t)cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols;
+    const int c = (int)(e % cols);
+    float v = (float)(ld_any(hin, h_bf16, r * ld + c) + (bias ? (double)bias[c] : 0.0));
+    if (act == 1) {
+      if (exact) {
+        const double x = (double)v;
+        v = (float)(0.5 * x * (1.0 + erf(x * 0.70710678118654752440)));
+      } else {
+        v = 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+      }
+    }
+    if (residual) v = (float)((double)residual[r * cols + c] + (double)v);
+    st_any(out, out_bf16, r * ld_out + c, v);
+  }
+}
+
+}  // namespace lsrm
+
+using namespace lsrm;
+
+extern "C" {
+
+int lsrm_add_layer_norm(const float* a, const void* b, int b_bf16, int64_t n, int d,
+                        const float* gamma, const float* beta, float eps, float* sum_out,
+                        int out_bf16, void* y, void* stream) {
+  LSRM_REQUIRE(d > 0, "add_layer_norm: d must be positive");
+  if (n == 0) return LSRM_OK;
+  add_ln_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, as_stream(stream)>>>(
+      a, b, b_bf16, n, d, gamma, beta, eps, sum_out, out_bf16, y);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_gate_mix_layer_norm(int exact, const float* xe, const void* gate_logits, int64_t ld_gl,
+                             int gl_bf16, const float* gate_b, const void* o_self,
+                             const void* o_cross, int o_bf16, int64_t n, int d, float* x1,
+                             const float* gamma, const float* beta, float eps, int out_bf16,
+                             void* h, void* stream) {
+  LSRM_REQUIRE(d > 0 && ld_gl >= 2 * d, "gate_mix: logits need 2*d columns");
+  if (n == 0) return LSRM_OK;
+  gate_mix_ln_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, as_stream(stream)>>>(
+      exact, xe, gate_logits, ld_gl, gl_bf16, gate_b, o_self, o_cross, o_bf16, n, d, x1, gamma,
+      beta, eps, out_bf16, h);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_bias_act(int exact, const void* h, int h_bf16, int64_t ld, const float* bias, int64_t n,
+                  int cols, int act, const float* residual, void* out, int out_bf16,
+                  int64_t ld_out, void* stream) {
+  LSRM_REQUIRE(act == 0 || act == 1, "bias_act: act must be 0 (identity) or 1 (gelu)");
+  if (n == 0 || cols == 0) return LSRM_OK;
+  int64_t total = n * (int64_t)cols;
+  unsigned grid = (unsigned)(ceil_div(total, 256) < 148 * 16 ? ceil_div(total, 256) : 148 * 16);
+  bias_act_kernel<<<grid, 256, 0, as_stream(stream)>>>(exact, h, h_bf16, ld, bias, n, cols, act,
+                                                       residual, out, out_bf16, ld_out);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+}  // extern "C"

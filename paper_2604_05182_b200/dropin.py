@@ -25,6 +25,7 @@ HOT_PATH = {
                       "_route_points_to_volume", "_route_points_to_image"),
     "tokenizer": ("informative_voxel_mask", "foreground_patch_mask", "upsample_select_tokens"),
     "seq_parallel": ("shard_blocks", "all_to_all", "all_gather_kv", "naive_contiguous_shards"),
+    "recon_pipeline": ("sparse_block_forward", "build_sparse_context", "ffn_forward"),
 }
 
 _saved = []

@@ -165,10 +165,14 @@ class SparseLayerEngine:
     shard: optional {"x": owned vol rows, "y": owned img rows}; `exchange`
     (seq_parallel) then fills the global KV buffers between prepare_kv and
     attend.
+    extra_cols: optional {"x": W [d, m], "y": ...} appended to a stream's fused
+    projection GEMM (the Stage-2 block's use gates); their output columns start
+    at `self.cols[("extra", stream)]` of `buf[("Y", stream)]`.
     """
 
     def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
-                 weights: dict, params: AttentionParams, shard: dict = None):
+                 weights: dict, params: AttentionParams, shard: dict = None,
+                 extra_cols: dict = None):
         require(params.head_dim in (32, 64), "bf16 engine: head_dim must be 32 or 64")
         G = params.group_size
         require(128 % G == 0 and G >= 4, "bf16 engine: (n_q_heads/n_kv_heads) must be in 4..128 "
@@ -200,6 +204,10 @@ class SparseLayerEngine:
             self.cols[(use, "v")] = ncol[ks] + w
             wcat[ks] += [wu.w_k, wu.w_v]
             ncol[ks] += 2 * w
+        for s_, wx in (extra_cols or {}).items():
+            self.cols[("extra", s_)] = ncol[s_]
+            wcat[s_].append(np.asarray(wx, np.float32))
+            ncol[s_] += int(wx.shape[1])
         self.ncol = ncol
         self.w_cat = {s: D.dev(np.concatenate(wcat[s], axis=1), torch.bfloat16) for s in wcat}
         self.w_o = {u: D.dev(weights[u].w_o, torch.bfloat16) for u in USES}

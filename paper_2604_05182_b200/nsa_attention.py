@@ -282,13 +282,6 @@ class NsaWeights:
     gate_b: np.ndarray
     compress: CompressWeights
     n_gates: int
-    _dev: dict = field(default_factory=dict, repr=False, compare=False)
-
-    def d(self, name, dtype=torch.float32):
-        key = (name, dtype, torch.cuda.current_device())
-        if key not in self._dev:
-            self._dev[key] = D.dev(getattr(self, name), dtype)
-        return self._dev[key]
 
 
 def init_nsa_weights(seed: int, params: AttentionParams, n_gates: int, *tags,
@@ -313,9 +306,9 @@ def nsa_gates(x, w: NsaWeights):
     on_dev = D.is_device(x)
     xd = D.dev(x, torch.float32)
     n, d = xd.shape
-    logits = _ops.gemm(xd, w.d("gate_w"))
+    logits = _ops.gemm(xd, D.weight(w.gate_w))
     g = D.empty((n, w.n_gates * d), torch.float32)
-    call("lsrm_sigmoid_f32", logits.data_ptr(), logits.stride(0), w.d("gate_b").data_ptr(),
+    call("lsrm_sigmoid_f32", logits.data_ptr(), logits.stride(0), D.weight(w.gate_b).data_ptr(),
          n, w.n_gates * d, g.data_ptr(), D.stream())
     g = g if on_dev else D.host(g)
     return tuple(g[:, i * d:(i + 1) * d] for i in range(w.n_gates))
@@ -323,13 +316,13 @@ def nsa_gates(x, w: NsaWeights):
 
 def _combine_dev(xd, outs, w: NsaWeights):
     n, d = xd.shape
-    logits = _ops.gemm(xd, w.d("gate_w"))
+    logits = _ops.gemm(xd, D.weight(w.gate_w))
     merged = D.empty((n, d), torch.float32)
     o = [t.reshape(n, d) for t in outs] + [None] * (3 - len(outs))
-    call("lsrm_gated_merge_f32", logits.data_ptr(), logits.stride(0), w.d("gate_b").data_ptr(),
+    call("lsrm_gated_merge_f32", logits.data_ptr(), logits.stride(0), D.weight(w.gate_b).data_ptr(),
          w.n_gates, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]), n, d, merged.data_ptr(),
          D.stream())
-    return _ops.gemm(merged, w.d("w_o"))
+    return _ops.gemm(merged, D.weight(w.w_o))
 
 
 def combine_nsa_branches(x, branch_outs, w: NsaWeights):
@@ -354,9 +347,9 @@ def nsa_cross_attention(x, kv_feats, part_q: BlockPartition, part_kv: BlockParti
     kvd = D.dev(kv_feats, torch.float32)
     n = int(xd.shape[0])
     hq, hkv, dh = params.n_q_heads, params.n_kv_heads, params.head_dim
-    q = _ops.gemm(xd, w.d("w_q")).reshape(n, hq, dh)
-    k = _ops.gemm(kvd, w.d("w_k"))
-    v = _ops.gemm(kvd, w.d("w_v"))
+    q = _ops.gemm(xd, D.weight(w.w_q)).reshape(n, hq, dh)
+    k = _ops.gemm(kvd, D.weight(w.w_k))
+    v = _ops.gemm(kvd, D.weight(w.w_v))
     nkv = int(kvd.shape[0])
     width = hkv * dh
     require(nkv == part_kv.n_tokens, "partition does not index these tokens")
@@ -372,7 +365,7 @@ def nsa_cross_attention(x, kv_feats, part_q: BlockPartition, part_kv: BlockParti
         sel_obj = None
     else:
         sel_obj = sel
-    if table is not None and table.rows is not None:
+    if getattr(table, "rows", None) is not None:   # this package's GatherTable
         rows, count = table.rows, table.count
     else:
         if sel_obj is not None:
