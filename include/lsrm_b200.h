@@ -204,7 +204,10 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
  * 8x8-core-matrix interleaved bf16 layout the tcgen05 kernel consumes:
  * per kv head, per block, rows padded to a multiple of 16.  ones_cols = 16
  * appends 16 columns holding 1 (real key) / 0 (padding): the V operand then
- * yields the softmax row sums in the same P.V MMA. */
+ * yields the softmax row sums in the same P.V MMA.  Padding rows of V are
+ * zero; padding rows of K (ones_cols = 0) repeat the block's first key, so
+ * they can neither raise a row max nor contribute (the attention kernel
+ * needs no padding masks). */
 int lsrm_kv_interleave(int src_is_bf16, const void* src, int64_t ld_src,
                        int64_t n, int hkv, int dh, int ones_cols,
                        const int64_t* block_token_ids,

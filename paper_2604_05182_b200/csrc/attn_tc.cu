@@ -332,20 +332,21 @@ struct HeadCols {
   static constexpr uint32_t kS = 0, kP = kNK, kO = kNK + kNK / 2, kMerged = kO + VW;
   static constexpr int kTotal = kNK + kNK / 2 + VW + DH / 2;
 };
-template <int DH, int HP>
+template <int DH, int HP, int NP>
 constexpr int tmem_alloc_cols() {
-  int n = HP * HeadCols<DH>::kTotal, a = 32;
+  int n = NP * HP * HeadCols<DH>::kTotal, a = 32;
   while (a < n) a *= 2;
   return a;
 }
 
+// Shared memory of one pipeline (producer + MMA warp(s) + softmax warps that
+// stream their own items).
 template <int DH, int HP>
-struct Smem {
+struct Pipe {
   __nv_bfloat16 q[2][HP][kM * DH];
   __nv_bfloat16 k[kStages][HP][kNK * DH];
   __nv_bfloat16 v[kStages][HP][kNK * (DH + kOnesCols)];   // [V | ones] rows
   __nv_bfloat16 gate[HP][kM * DH];  // per row: gate logits of the branch that just ended
-  float bias[kBiasMax];             // gate biases, padded rows (if they fit)
   int32_t ent[kMaxEnt];          // selected rows of the tile tokens, [t][kmax]
   uint32_t bitmap[kBitmapWords]; // selected-row bitmap of the current item
   int32_t wpre[kBitmapWords];    // rank of the first set bit of each word
@@ -358,11 +359,18 @@ struct Smem {
   ChunkDesc desc[kStages];
   uint64_t kv_full[kStages], kv_empty[kStages], s_full[HP], s_free[HP], p_full[HP], o_full[HP],
       q_full[2], q_empty[2];
+};
+
+template <int DH, int HP, int NP>
+struct Smem {
+  Pipe<DH, HP> pipe[NP];
+  float bias[kBiasMax];             // gate biases, padded rows (if they fit)
   uint32_t tmem_base;
 };
 
-template <int HP>
-constexpr int threads_of() { return 32 * (5 * HP + 1); }   // softmax, producer, MMA per head
+// per pipeline: 4 softmax warps per head-tile, 1 producer, 1 MMA warp per head-tile
+template <int HP, int NP>
+constexpr int threads_of() { return 32 * NP * (5 * HP + 1); }
 
 // Work item = (query tile, group of HP kv heads).  The HP head-tiles share the
 // chunk plan (same tokens, same union of selected blocks) but not K/V, so
@@ -372,23 +380,41 @@ constexpr int threads_of() { return 32 * (5 * HP + 1); }   // softmax, producer,
 // Warps: 4*HP softmax (warpgroup hh = head-tile hh; thread = TMEM lane = one
 // row, all 128 keys of a chunk, so no cross-warp max exchange), 1 producer,
 // 1 MMA issuer.
-template <int DH, int HP>
-__global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P) {
+//
+// NP independent pipelines per CTA (own items, producer, ring, MMA warp(s),
+// softmax warps, TMEM columns): their warps share each SMSP but not a chunk
+// plan, so one pipeline's loads / maxima / epilogue overlap the other's
+// exponentials instead of running in lockstep.  Odd pipelines walk their item
+// list backwards so the two of a CTA start on different tiles.
+template <int DH, int HP, int NP>
+__global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Params P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  Smem<DH, HP>& S = *reinterpret_cast<Smem<DH, HP>*>(smem_raw);
+  Smem<DH, HP, NP>& SM = *reinterpret_cast<Smem<DH, HP, NP>*>(smem_raw);
   using HCols = HeadCols<DH>;
   constexpr int VW = HCols::VW, HC = HCols::kTotal;
-  constexpr int kSoftWarps = 4 * HP, kProducerWarp = kSoftWarps;
-  constexpr int kAlloc = tmem_alloc_cols<DH, HP>();
+  constexpr int kSoftWarps = 4 * HP * NP, kProducerWarp = kSoftWarps;
+  constexpr int kAlloc = tmem_alloc_cols<DH, HP, NP>();
   static_assert(kAlloc <= 512, "TMEM budget");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = P.hq / P.hkv, T = kM / G;
   const int d_model = P.hq * DH;
   const int n_hgroups = P.hkv / HP;
   const int64_t n_items = P.n_tiles * n_hgroups;
-  if ((int64_t)blockIdx.x >= n_items) return;
+  // role -> pipeline: softmax warps [0, 4*HP*NP), producers, then MMA warps
+  const int pipe_id = warp < kSoftWarps ? warp / (4 * HP)
+                      : (warp < kSoftWarps + NP ? warp - kSoftWarps
+                                                : (warp - kSoftWarps - NP) / HP);
+  Pipe<DH, HP>& S = SM.pipe[pipe_id];
+  const int64_t n_pipes = (int64_t)gridDim.x * NP;
+  const int64_t gp = (int64_t)blockIdx.x * NP + pipe_id;
+  const int64_t m_items = gp < n_items ? (n_items - gp + n_pipes - 1) / n_pipes : 0;
+  auto item_of = [&](int64_t k) -> int64_t {
+    return (pipe_id & 1) ? gp + (m_items - 1 - k) * n_pipes : gp + k * n_pipes;
+  };
 
   if (tid == 0) {
+    for (int pp = 0; pp < NP; ++pp) {
+    Pipe<DH, HP>& S = SM.pipe[pp];
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&S.kv_full[i], 1);
       mbar_init(&S.kv_empty[i], HP);   // one commit per head-tile's MMA warp
@@ -403,38 +429,43 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       mbar_init(&S.q_full[i], 1);
       mbar_init(&S.q_empty[i], HP);
     }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&S.tmem_base)),
+                     smem_u32(&SM.tmem_base)),
                  "r"(kAlloc));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int i = tid; i < kBitmapWords; i += blockDim.x) S.bitmap[i] = 0u;
+  for (int i = tid; i < NP * kBitmapWords; i += blockDim.x)
+    SM.pipe[i / kBitmapWords].bitmap[i % kBitmapWords] = 0u;
   const bool bias_smem = P.gbias && P.n_gates * P.hq * (DH + 1) <= kBiasMax;
   if (bias_smem)
     for (int i = tid; i < P.n_gates * d_model; i += blockDim.x)
-      S.bias[(i / DH) * (DH + 1) + i % DH] = P.gbias[i];
-  const float* const bias_all = bias_smem ? S.bias : P.gbias;
+      SM.bias[(i / DH) * (DH + 1) + i % DH] = P.gbias[i];
+  const float* const bias_all = bias_smem ? SM.bias : P.gbias;
   const int bias_ld = bias_smem ? DH + 1 : DH;   // floats per (branch, head) row
   fence_async_smem();
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
-  const uint32_t tmem = S.tmem_base;
-  long long* const trp = blockIdx.x == 0 ? g_trace : nullptr;  // debug event trace
+  const uint32_t tmem = SM.tmem_base + (uint32_t)(pipe_id * HP * HC);   // this pipeline's columns
+  long long* const trp = (blockIdx.x == 0 && pipe_id == 0) ? g_trace : nullptr;  // debug trace
 
-  if (warp == kProducerWarp) {
+  if (m_items == 0) {
+    // this pipeline has no work (small launches)
+  } else if (warp >= kProducerWarp && warp < kProducerWarp + NP) {
     // ===================== producer: Q tiles, unions, chunk plans, K/V copies
     uint32_t c = 0;
     int it = 0;
     const uint32_t all_tok = T >= 32 ? 0xffffffffu : ((1u << T) - 1u);
-    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    for (int64_t kk_item = 0; kk_item < m_items; ++kk_item, ++it) {
+      const int64_t item = item_of(kk_item);
       const int tile = (int)(item / n_hgroups), h0 = (int)(item % n_hgroups) * HP;
       const int q_first = P.tiles[4 * tile], q_cnt = P.tiles[4 * tile + 1],
                 own = P.tiles[4 * tile + 2];
-      const bool last_item = item + gridDim.x >= n_items;
+      const bool last_item = kk_item == m_items - 1;
       const int qb = it & 1;
       // ---- selected rows of the tile tokens (resolved rows are -1 padded)
       const int n_ent = T * P.kmax, n_valid_ent = q_cnt * P.kmax;
@@ -644,10 +675,10 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       }
       __syncwarp();
     }
-  } else if (warp > kProducerWarp) {
+  } else if (warp >= kProducerWarp + NP) {
     // ===================== MMA issuer of head-tile hh (one warp per head-tile,
     // so neither head-tile's MMAs wait behind the other's barriers)
-    const int hh = warp - kProducerWarp - 1;
+    const int hh = (warp - kProducerWarp - NP) % HP;
     const uint32_t id_pv = idesc_bf16(kM, VW, 1);   // [O | rowsum] += P . [V | ones]
     const uint32_t t_s = tmem + hh * HC + HCols::kS, t_p = tmem + hh * HC + HCols::kP,
                    t_o = tmem + hh * HC + HCols::kO;
@@ -712,7 +743,7 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
     __syncwarp();
   } else {
     // ===================== softmax / epilogue (warpgroup hh = head-tile hh)
-    const int hh = warp >> 2, q4 = warp & 3;
+    const int hh = (warp % (4 * HP)) >> 2, q4 = warp & 3;
     const int m = q4 * 32 + lane;
     const int t = m / G, g_in = m % G;
     const uint32_t tS = tmem + ((uint32_t)(q4 * 32) << 16) + hh * HC;
@@ -735,17 +766,17 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
     // (named barriers 1, 2), so one's MUFU stream covers the other's loads,
     // maxima and epilogue; warpgroup 1 lets warpgroup 0 go first
     const int bar_mine = 1 + hh, bar_other = 2 - hh;
-    if (kPingPong && HP == 2 && hh == 1) named_arrive(bar_other, 256);
+    if (kPingPong && NP == 1 && HP == 2 && hh == 1) named_arrive(bar_other, 256);
 #ifdef LSRM_WG1_DELAY_NS
     if (HP == 2 && hh == 1) __nanosleep(LSRM_WG1_DELAY_NS);   // start out of phase
 #endif
     // one turn per 32-key piece: wait for ours, run the piece's exponentials,
     // hand over (the very last hand-over of warpgroup 1 has no taker)
     auto pp_turn = [&]() {
-      if (kPingPong && HP == 2) named_sync(bar_mine, 256);
+      if (kPingPong && NP == 1 && HP == 2) named_sync(bar_mine, 256);
     };
     auto pp_pass = [&](bool last_piece) {
-      if (kPingPong && HP == 2 && !(hh == 1 && last_piece)) named_arrive(bar_other, 256);
+      if (kPingPong && NP == 1 && HP == 2 && !(hh == 1 && last_piece)) named_arrive(bar_other, 256);
     };
 
     // gate + merge of a finished branch (nsa_attention.py:266-284); the
@@ -838,10 +869,10 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       const int64_t tok = (int64_t)hdr0.w + t;
       const int head = (hdr1.y + hh) * G + g_in;
       // `live` groups are seen by some row of this warp (others are skipped,
-      // P = 0); a row sees a group if its token selected it (visb); `tail`
-      // groups end a block segment (keys j >= gnv are padding)
+      // P = 0); a row sees a group if its token selected it (visb).  Block
+      // padding needs no mask: padding K rows repeat a real key of the block
+      // (no effect on the max) and padding V rows are zero.
       const uint32_t live = __reduce_or_sync(0xffffffffu, visb);
-      const uint32_t tail = ((uint32_t)fl >> 8) & live;
       if (first_br) m_run = kNegInf;
       float mx = kNegInf;
       const int n_pc = (ncols + 31) / 32;   // 32-key pieces (ping-pong turns) of this chunk
@@ -854,16 +885,18 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       const bool two_pass =
           !kOnePass || __any_sync(0xffffffffu, m_run == kNegInf && visb != 0u);
       if (two_pass) {
+// straight-line group maxima; groups this row does not see are not selected
 #define LSRM_MAX(arr, off, gi)                                  \
-    if ((live >> (gi)) & 1u) {                                    \
-      if ((tail >> (gi)) & 1u) mask16(arr + (off), D.gnv[gi]);    \
-      const float g_ = max16(arr + (off));                        \
-      mx = ((visb >> (gi)) & 1u) ? fmaxf(mx, g_) : mx;            \
-    }
+  {                                                             \
+    const float g_ = max16(arr + (off));                        \
+    mx = ((visb >> (gi)) & 1u) ? fmaxf(mx, g_) : mx;            \
+  }
         LSRM_MAX(sa, 0, 0)
         LSRM_MAX(sa, 16, 1)
-        LSRM_MAX(sb, 0, 2)
-        LSRM_MAX(sb, 16, 3)
+        if (ncols > 32) {
+          LSRM_MAX(sb, 0, 2)
+          LSRM_MAX(sb, 16, 3)
+        }
         const bool hi = ncols > 64;   // pieces 2,3 end up in registers
         if (tid == 0) trace(trp, c, 9);
         if (hi) {
@@ -872,8 +905,10 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
           tmem_wait_ld();
           LSRM_MAX(sa, 0, 4)
           LSRM_MAX(sa, 16, 5)
-          LSRM_MAX(sb, 0, 6)
-          LSRM_MAX(sb, 16, 7)
+          if (ncols > 96) {
+            LSRM_MAX(sb, 0, 6)
+            LSRM_MAX(sb, 16, 7)
+          }
         } else {
           tc_before_sync();
           mbar_arrive(&S.s_free[hh]);   // S(c) fully in registers: QK(c+1) may overwrite it
@@ -892,10 +927,17 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
           need = true;
         }
         // PV(c-1) must be complete before P(c) overwrites P(c-1) and before O is
-        // rescaled or read
-        if (c > 0) mbar_wait(&S.o_full[hh], (c - 1) & 1);
-        tc_after_sync();
+        // rescaled or read: waited for lazily, right before the first of those
+        bool pv_done = c == 0;
+        auto wait_pv = [&]() {
+          if (!pv_done) {
+            mbar_wait(&S.o_full[hh], (c - 1) & 1);
+            tc_after_sync();
+            pv_done = true;
+          }
+        };
         if (__any_sync(0xffffffffu, need)) {
+          wait_pv();
 #pragma unroll
           for (int c0 = 0; c0 < DH; c0 += 16) {
             uint32_t r[16];
@@ -931,6 +973,7 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
       zero8(w + 8);                                                            \
     }                                                                          \
     pp_pass(lp_);                                                              \
+    wait_pv();                                                                 \
     tmem_st16(tP + 16 * (pc), w);                                              \
   }
         if (hi) {
@@ -942,12 +985,6 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
           tc_before_sync();
           mbar_arrive(&S.s_free[hh]);
           if (tid == 0) trace(trp, c, 12);
-          if (tail & 15u) {
-            if (tail & 1u) mask16(sa, D.gnv[0]);
-            if (tail & 2u) mask16(sa + 16, D.gnv[1]);
-            if (tail & 4u) mask16(sb, D.gnv[2]);
-            if (tail & 8u) mask16(sb + 16, D.gnv[3]);
-          }
         }
         LSRM_EXP_PIECE(sa, 0)
         if (ncols > 32) LSRM_EXP_PIECE(sb, 1)
@@ -966,8 +1003,6 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
   {                                                                           \
     uint32_t w[16];                                                           \
     if ((live >> (2 * (pc))) & 3u) {                                          \
-      if ((tail >> (2 * (pc))) & 1u) mask16(arr, D.gnv[2 * (pc)]);            \
-      if ((tail >> (2 * (pc) + 1)) & 1u) mask16(arr + 16, D.gnv[2 * (pc) + 1]); \
       const bool v0 = (visb >> (2 * (pc))) & 1u, v1 = (visb >> (2 * (pc) + 1)) & 1u; \
       if (tid == 0) trace(trp, c, 16 + 4 * (pc));                             \
       const float g0 = max16(arr), g1 = max16(arr + 16);                      \
@@ -1033,7 +1068,6 @@ __global__ void __launch_bounds__(threads_of<HP>(), 1) nsa_fused_kernel(Params P
               for (int hf = 0; hf < 2; ++hf) {
                 const int gi = 2 * pc + hf;
                 if ((live >> gi) & 1u) {
-                  if ((tail >> gi) & 1u) mask16(sa + 16 * hf, D.gnv[gi]);
                   exp16(sa + 16 * hf, sl2, ((visb >> gi) & 1u) ? nb2 : kNegInf, w + 8 * hf);
                 } else {
                   zero8(w + 8 * hf);
@@ -1127,6 +1161,19 @@ __global__ void kv_interleave_kernel(int src_bf16, const void* __restrict__ src,
 #pragma unroll
         for (int j = 0; j < 8; ++j) vals[j] = __float2bfloat16_rn(s[j]);
       }
+    } else if (ones_cols == 0 && (tok ? occ > 0 : n_plain > 0)) {
+      // K padding rows repeat the set's first key: a duplicate key cannot
+      // raise a row max, and its value row (V padding) is zero, so padding
+      // needs no masking in the attention kernel
+      int64_t row = tok ? tok[lo] : 0;
+      if (src_bf16) {
+        *reinterpret_cast<uint4*>(vals) = *reinterpret_cast<const uint4*>(
+            (const __nv_bfloat16*)src + row * ld + h * dh + cc * 8);
+      } else {
+        const float* s = (const float*)src + row * ld + h * dh + cc * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vals[j] = __float2bfloat16_rn(s[j]);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) vals[j] = __float2bfloat16_rn(0.f);
@@ -1197,20 +1244,28 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
   int dev = 0, n_sm = 148;
   LSRM_CUDA(cudaGetDevice(&dev));
   LSRM_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  // two head-tiles per item (ping-pong) when the kv heads pair up and TMEM fits
-  const int hp = (dh == 32 && hkv % 2 == 0) ? 2 : 1;
+  // d_h = 32: two independent single-head pipelines per CTA (or, with
+  // -DLSRM_HEADPAIR, one pipeline whose items are kv-head pairs); d_h = 64:
+  // one pipeline (TMEM)
+#ifdef LSRM_HEADPAIR
+  const int hp = (dh == 32 && hkv % 2 == 0) ? 2 : 1, np_ = 1;
+#else
+  const int hp = 1, np_ = dh == 32 ? 2 : 1;
+#endif
   int64_t n_items = n_tiles * (hkv / hp);
-  unsigned grid = (unsigned)(n_items < n_sm ? n_items : n_sm);
-#define LSRM_TC_CASE(D, HP)                                                                 \
-  if (dh == D && hp == HP) {                                                                \
-    size_t smem = sizeof(tc::Smem<D, HP>) + 1024;                                           \
-    LSRM_CUDA(cudaFuncSetAttribute(tc::nsa_fused_kernel<D, HP>,                             \
+  int64_t want = (n_items + np_ - 1) / np_;
+  unsigned grid = (unsigned)(want < n_sm ? want : n_sm);
+#define LSRM_TC_CASE(D, HP, NP)                                                             \
+  if (dh == D && hp == HP && np_ == NP) {                                                   \
+    size_t smem = sizeof(tc::Smem<D, HP, NP>) + 1024;                                       \
+    LSRM_CUDA(cudaFuncSetAttribute(tc::nsa_fused_kernel<D, HP, NP>,                         \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    tc::nsa_fused_kernel<D, HP><<<grid, tc::threads_of<HP>(), smem, st>>>(p);               \
+    tc::nsa_fused_kernel<D, HP, NP><<<grid, tc::threads_of<HP, NP>(), smem, st>>>(p);       \
   } else
-  LSRM_TC_CASE(32, 2)
-  LSRM_TC_CASE(32, 1)
-  LSRM_TC_CASE(64, 1)
+  LSRM_TC_CASE(32, 1, 2)
+  LSRM_TC_CASE(32, 2, 1)
+  LSRM_TC_CASE(32, 1, 1)
+  LSRM_TC_CASE(64, 1, 1)
   return set_error(LSRM_E_CONFIG, "tcgen05 path: head_dim %d not in {32,64}", dh);
 #undef LSRM_TC_CASE
   LSRM_LAUNCHED();

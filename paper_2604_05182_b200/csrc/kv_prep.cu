@@ -183,6 +183,18 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
       }
     }
   }
+  // K padding rows of the block segment repeat its first key (a duplicate key
+  // cannot raise a row max; the matching V rows stay zero): no padding masks
+  // in the attention kernel
+  if (!J.ones_cols) {
+    const int64_t plen = J.pad_off[b + 1] - prow0;
+    for (int e = tid; e < (plen - occ) * (W / 8); e += 128) {
+      const int64_t r = occ + e / (W / 8);
+      const int col = (e % (W / 8)) * 8, h = col / dh;
+      const uint4 v = *reinterpret_cast<const uint4*>(J.src + lo * J.ld + col);
+      *reinterpret_cast<uint4*>(J.il + il_off(h, J.rows_pad, vw, prow0 + r, col - h * dh)) = v;
+    }
+  }
   // 4. fixed-order reduction: lanes with equal t4 (xor 4, 8, 16), then warps
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
@@ -202,6 +214,9 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
     if (J.cmp_il) {
       const int h = col / dh;
       J.cmp_il[il_off(h, J.cmp_rows_pad, vw, b, col - h * dh)] = __float2bfloat16_rn(mean);
+      if (b == 0 && !J.ones_cols)   // compressed K padding rows repeat row 0
+        for (int64_t r = J.n_blocks; r < J.cmp_rows_pad; ++r)
+          J.cmp_il[il_off(h, J.cmp_rows_pad, vw, r, col - h * dh)] = __float2bfloat16_rn(mean);
     }
   }
   if (J.cmp_il && J.ones_cols)
