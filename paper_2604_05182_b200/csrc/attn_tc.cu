@@ -77,6 +77,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef LSRM_SPIN_WAIT
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "LAB_WAIT:\n\t"
@@ -86,6 +97,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "DONE:\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x100000u)   // suspend (not spin) until the phase completes
       : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
@@ -299,12 +311,34 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// exp2 on the FMA pipe: x = j + f (j = round(x), |f| <= 1/2), 2^f by a
+// degree-3 polynomial (rel. error < 7e-4, a sixth of a bf16 ulp), 2^j added to
+// the exponent bits.  x is clamped to >= -125 (masked -inf -> ~2e-38, which
+// contributes nothing measurable); x <= 8 by the softmax headroom.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;   // 1.5 * 2^23: round to integer in the mantissa
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(f, 0.0555041086648216f, 0.2402264923172690f);
+  p = fmaf(p, f, 0.6931471805599453f);
+  p = fmaf(p, f, 1.f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+// Of every 16 exponentials, kPolyPer16 go to the FMA pipe (ex2_poly) and the
+// rest to the MUFU, whose issue rate (16/clk/SM) bounds the kernel.
+#ifndef LSRM_POLY_PER16
+#define LSRM_POLY_PER16 0
+#endif
+constexpr int kPolyPer16 = LSRM_POLY_PER16;
+__device__ __forceinline__ float ex2_mixed(float x, int j) {
+  return j >= 16 - kPolyPer16 ? ex2_poly(x) : ex2(x);
+}
 // 16 logits -> 8 words of packed bf16 exp2(s * sl2 + nb)
 __device__ __forceinline__ void exp16(const uint32_t* s, float sl2, float nb, uint32_t* w) {
 #pragma unroll
   for (int j = 0; j < 8; ++j)
-    w[j] = pack_bf16(ex2(fmaf(__uint_as_float(s[2 * j]), sl2, nb)),
-                     ex2(fmaf(__uint_as_float(s[2 * j + 1]), sl2, nb)));
+    w[j] = pack_bf16(ex2_mixed(fmaf(__uint_as_float(s[2 * j]), sl2, nb), 2 * j),
+                     ex2_mixed(fmaf(__uint_as_float(s[2 * j + 1]), sl2, nb), 2 * j + 1));
 }
 __device__ __forceinline__ void zero8(uint32_t* w) {
 #pragma unroll

@@ -164,6 +164,51 @@ __global__ void exp_phase_kernel(float* out, long long* clk, int active_warps) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base));
 }
 
+// XU-pipe sharing: ex2 alone, ex2 + F2FP bf16x2 pack (1 per 2 ex2), ex2 + PRMT pack
+template <int MODE>
+__global__ void xu_kernel(float* out, long long* clk) {
+  float f[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[i] = -0.001f * (threadIdx.x + i);
+  uint32_t acc = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < kIters / 4; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(f[i]));
+    if (MODE == 1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t w;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w) : "f"(f[2 * i]), "f"(f[2 * i + 1]));
+        acc ^= w;
+      }
+    } else if (MODE == 2) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t w;
+        asm volatile("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(w) : "r"(__float_as_uint(f[2 * i])),
+                     "r"(__float_as_uint(f[2 * i + 1])));
+        acc ^= w;
+      }
+    } else if (MODE == 3) {   // pack only (no ex2 dependence chain change)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t w;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w) : "f"(f[2 * i]), "f"(f[2 * i + 1]));
+        acc ^= w;
+      }
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float a = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a += f[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a + (float)acc;
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+}
+
 int main() {
   float* out;
   long long* clk;
@@ -195,6 +240,20 @@ int main() {
     cudaMemcpy(h, clk, sizeof(h), cudaMemcpyDeviceToHost);
     double bytes = (double)(kIters / 16) * 32 * 32 * 4 * w;
     printf("tcgen05.ld x32, %2d warps: %.1f B/clk/SM (%lld clk)\n", w, bytes / h[0], h[0]);
+  }
+  {
+    const char* xn[3] = {"ex2 only", "ex2 + cvt.bf16x2 (1 per 2)", "ex2 + prmt (1 per 2)"};
+    for (int mode = 0; mode < 3; ++mode) {
+      for (int rep = 0; rep < 2; ++rep) {
+        if (mode == 0) xu_kernel<0><<<148, 256>>>(out, clk);
+        if (mode == 1) xu_kernel<1><<<148, 256>>>(out, clk);
+        if (mode == 2) xu_kernel<2><<<148, 256>>>(out, clk);
+      }
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, clk, sizeof(h), cudaMemcpyDeviceToHost);
+      double ex = (double)(kIters / 4) * 16 * 256;
+      printf("%-28s: %.2f ex2/clk/SM\n", xn[mode], ex / h[0]);
+    }
   }
   const char* en[3] = {"regs only", "+st P", "+ld S +st P"};
   for (int mode = 0; mode < 3; ++mode)
