@@ -180,6 +180,14 @@ int lsrm_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a,
               int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
               void* stream);
 
+/* C[m,n] = A[m,k] @ B[k,n] + bias[n], bf16 in / fp32 accumulate / bf16 out
+ * (cuBLASLt bias epilogue; a per-device handle and 32 MiB workspace are made
+ * on first use).  The engine uses it to fold the NSA gate biases into the
+ * fused per-stream projection. */
+int lsrm_gemm_bias_bf16(int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
+                        const void* b, int64_t ldb, const void* bias, void* c,
+                        int64_t ldc, void* stream);
+
 /* ---- fused bf16 three-branch NSA attention, tcgen05/TMEM  -------------
  * (nsa_attention.py:84-112,157-207,266-284 fused)
  * q: [nq, hq, dh] bf16 in query BLOCK-MAJOR order; kv_il: K and V in the

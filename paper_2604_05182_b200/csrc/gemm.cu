@@ -4,6 +4,7 @@
 #include "common.cuh"
 
 #include <cublas_v2.h>
+#include <cublasLt.h>
 
 namespace lsrm {
 
@@ -28,9 +29,81 @@ static int get_handle(cublasHandle_t* out) {
   return LSRM_OK;
 }
 
+// cuBLASLt (bias epilogue): one handle + 32 MiB workspace per device, made
+// on first use (the documented exception to "no hidden allocation").
+struct LtSlot {
+  cublasLtHandle_t h = nullptr;
+  void* ws = nullptr;
+};
+static LtSlot g_lt[16];
+constexpr size_t kLtWorkspace = 32u << 20;
+
+static int get_lt(int dev, LtSlot** out) {
+  if (dev < 0 || dev >= 16) return set_error(LSRM_E_CUDA, "device id %d out of range", dev);
+  LtSlot& s = g_lt[dev];
+  if (!s.h) {
+    if (cublasLtCreate(&s.h) != CUBLAS_STATUS_SUCCESS)
+      return set_error(LSRM_E_CUDA, "cublasLtCreate failed");
+    LSRM_CUDA(cudaMalloc(&s.ws, kLtWorkspace));
+  }
+  *out = &s;
+  return LSRM_OK;
+}
+
 }  // namespace lsrm
 
 using namespace lsrm;
+
+// C[m,n] = A[m,k] @ B[k,n] + bias[n], bf16 in / fp32 accumulate / bf16 out,
+// row-major (issued as the column-major C^T = B^T A^T with a row bias).
+extern "C" int lsrm_gemm_bias_bf16(int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
+                                   const void* b, int64_t ldb, const void* bias, void* c,
+                                   int64_t ldc, void* stream) {
+  if (m == 0 || n == 0) return LSRM_OK;
+  int dev = 0;
+  LSRM_CUDA(cudaGetDevice(&dev));
+  LtSlot* lt;
+  int rc = get_lt(dev, &lt);
+  if (rc) return rc;
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+  cublasLtMatmulPreference_t pref = nullptr;
+  int status = LSRM_OK;
+  cublasOperation_t tn = CUBLAS_OP_N;
+  cublasLtEpilogue_t epi = CUBLASLT_EPILOGUE_BIAS;
+  cudaDataType_t bt = CUDA_R_16BF;
+  size_t wsz = kLtWorkspace;
+  cublasLtMatmulHeuristicResult_t heur = {};
+  int n_res = 0;
+  const float one = 1.f, zero = 0.f;
+  bool ok = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tn, sizeof(tn)) == 0;
+  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tn, sizeof(tn)) == 0;
+  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi)) == 0;
+  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias,
+                                            sizeof(bias)) == 0;
+  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bt,
+                                            sizeof(bt)) == 0;
+  // column-major view: D (n x m) = B^T (n x k) . A^T (k x m)
+  ok = ok && cublasLtMatrixLayoutCreate(&la, CUDA_R_16BF, n, k, ldb) == 0;
+  ok = ok && cublasLtMatrixLayoutCreate(&lb, CUDA_R_16BF, k, m, lda) == 0;
+  ok = ok && cublasLtMatrixLayoutCreate(&lc, CUDA_R_16BF, n, m, ldc) == 0;
+  ok = ok && cublasLtMatmulPreferenceCreate(&pref) == 0;
+  ok = ok && cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
+                                                  &wsz, sizeof(wsz)) == 0;
+  ok = ok && cublasLtMatmulAlgoGetHeuristic(lt->h, op, la, lb, lc, lc, pref, 1, &heur, &n_res) == 0 &&
+       n_res > 0;
+  ok = ok && cublasLtMatmul(lt->h, op, &one, b, la, a, lb, &zero, c, lc, c, lc, &heur.algo, lt->ws,
+                            kLtWorkspace, as_stream(stream)) == CUBLAS_STATUS_SUCCESS;
+  if (!ok) status = set_error(LSRM_E_CUDA, "cublasLt bias GEMM failed (m=%lld n=%lld k=%lld)",
+                              (long long)m, (long long)n, (long long)k);
+  if (pref) cublasLtMatmulPreferenceDestroy(pref);
+  if (lc) cublasLtMatrixLayoutDestroy(lc);
+  if (lb) cublasLtMatrixLayoutDestroy(lb);
+  if (la) cublasLtMatrixLayoutDestroy(la);
+  if (op) cublasLtMatmulDescDestroy(op);
+  return status;
+}
 
 extern "C" int lsrm_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a,
                          int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,

@@ -188,14 +188,18 @@ class SparseLayerEngine:
         parts = {"x": part_vol, "y": part_img}
         # fused projection weights per stream: [q|gates] of its query uses, then
         # [k|v] of the uses that read it as KV
+        # (the gate biases ride in the same GEMM's bias epilogue, so the gate
+        # logits the attention reads are complete)
         self.cols = {}
         wcat = {"x": [], "y": []}
+        bcat = {"x": [], "y": []}
         ncol = {"x": 0, "y": 0}
         for use in USES:
             qs, _, ng = USE_GEOM[use]
             wu = weights[use]
             self.cols[(use, "q")] = ncol[qs]
             wcat[qs] += [wu.w_q, wu.gate_w]
+            bcat[qs] += [np.zeros(d, np.float32), np.asarray(wu.gate_b, np.float32)]
             ncol[qs] += d + ng * d
         for use in USES:
             _, ks, _ = USE_GEOM[use]
@@ -203,13 +207,16 @@ class SparseLayerEngine:
             self.cols[(use, "k")] = ncol[ks]
             self.cols[(use, "v")] = ncol[ks] + w
             wcat[ks] += [wu.w_k, wu.w_v]
+            bcat[ks].append(np.zeros(2 * w, np.float32))
             ncol[ks] += 2 * w
         for s_, wx in (extra_cols or {}).items():
             self.cols[("extra", s_)] = ncol[s_]
             wcat[s_].append(np.asarray(wx, np.float32))
+            bcat[s_].append(np.zeros(int(wx.shape[1]), np.float32))
             ncol[s_] += int(wx.shape[1])
         self.ncol = ncol
         self.w_cat = {s: D.dev(np.concatenate(wcat[s], axis=1), torch.bfloat16) for s in wcat}
+        self.b_cat = {s: D.dev(np.concatenate(bcat[s]), torch.bfloat16) for s in bcat}
         self.w_o = {u: D.dev(weights[u].w_o, torch.bfloat16) for u in USES}
         self.gate_b = {u: D.dev(weights[u].gate_b, torch.float32) for u in USES}
         self.cmp_w = {u: (_dev_res(weights[u].compress.for_k), _dev_res(weights[u].compress.for_v))
@@ -300,10 +307,13 @@ class SparseLayerEngine:
 
     # -- pieces --------------------------------------------------------------
     def project(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
-        if self.meta["x"].n_loc:
-            _ops.gemm(x_loc, self.w_cat["x"], out=self.buf[("Y", "x")])
-        if self.meta["y"].n_loc:
-            _ops.gemm(y_loc, self.w_cat["y"], out=self.buf[("Y", "y")])
+        for s, a in (("x", x_loc), ("y", y_loc)):
+            if self.meta[s].n_loc:
+                Y, Wc = self.buf[("Y", s)], self.w_cat[s]
+                m, k = a.shape
+                call("lsrm_gemm_bias_bf16", m, int(Wc.shape[1]), k, a.data_ptr(), a.stride(0),
+                     Wc.data_ptr(), Wc.stride(0), self.b_cat[s].data_ptr(), Y.data_ptr(),
+                     Y.stride(0), D.stream())
 
     def prepare_kv(self):
         """K/V of all four uses in one launch (owned KV blocks when sharded;
@@ -340,7 +350,7 @@ class SparseLayerEngine:
              self.buf[("vc_il", use)].data_ptr(), mk.n_blocks, tiles.data_ptr(),
              int(tiles.shape[0]), self.rows[use].data_ptr(), self.count[use].data_ptr(),
              self.kmax[use], Y.data_ptr(), Y.stride(0), qcol + self.d,
-             self.gate_b[use].data_ptr(), ng, self.buf[("merged", use)].data_ptr(), D.stream())
+             None, ng, self.buf[("merged", use)].data_ptr(), D.stream())   # bias: in the GEMM
 
     def output(self, use: str):
         if self.buf[("merged", use)].shape[0]:

@@ -295,6 +295,9 @@ def test_engine_layer_vs_fp32_path(c1):
     plan = L.build_routing_plan(L.volume_token_coords(x_up), wl.img_points, pv, pi,
                                 wl.cameras, L.RoutingBudgets())
     ws = nsa_use_weights(params)
+    g = np.random.default_rng(11)
+    for wu in ws.values():   # nonzero gate biases: the engine folds them into its GEMM
+        wu.gate_b = (g.standard_normal(wu.gate_b.shape) * 0.5).astype(np.float32)
     d = 1024
     ones, zeros = np.ones(d, np.float32), np.zeros(d, np.float32)
     xh = O.layer_norm(x_up.features, ones, zeros)
