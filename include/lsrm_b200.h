@@ -208,6 +208,39 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
                           int64_t gate_col0, const float* gate_bias,
                           int n_gates, void* merged, void* stream);
 
+/* All NSA uses of a layer (same head geometry) in ONE persistent launch, with
+ * a heaviest-first work queue.  Each use is described like the arguments of
+ * lsrm_nsa_attention_tc (uses is a HOST array); gate biases must already be
+ * folded into the gate logits.  order [n_order]: (use << 28) | item, item =
+ * tile * hkv + kv head, sorted by estimated cost, descending; counter: one
+ * int32 of device memory (zeroed by this call on `stream`). */
+typedef struct lsrm_nsa_use {
+  const void* q;
+  int64_t ld_q;
+  int64_t nq;
+  const void* k_il;
+  const void* v_il;
+  const int64_t* pad_offsets;
+  const int64_t* kv_offsets;
+  int64_t n_kv_rows_pad;
+  const void* kcmp_il;
+  const void* vcmp_il;
+  int64_t n_blocks;
+  const int32_t* tiles;
+  int64_t n_tiles;
+  const int32_t* rows;
+  const int32_t* count;
+  int64_t kmax_rows;
+  const void* gate_logits;
+  int64_t ld_gl;
+  int64_t gate_col0;
+  int64_t n_gates;
+  void* merged;
+} lsrm_nsa_use;
+int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, int hkv, int dh,
+                                const int32_t* order, int64_t n_order, int32_t* counter,
+                                void* stream);
+
 /* Re-layout K or V ([n, hkv, dh] f32 or bf16, token order) into the padded,
  * 8x8-core-matrix interleaved bf16 layout the tcgen05 kernel consumes:
  * per kv head, per block, rows padded to a multiple of 16.  ones_cols = 16

@@ -235,6 +235,19 @@ struct Params {
   __nv_bfloat16* out;
 };
 
+// One launch: up to kMaxUses NSA uses (same head geometry).  order == nullptr:
+// static round-robin over use 0's items.  Otherwise a work queue: order[i] =
+// (use << 28) | item, heaviest first (LPT); pipeline p takes item p, then
+// n_pipes + atomicAdd(counter, 1), ... (counter zeroed before the launch).
+constexpr int kMaxUses = 4;
+struct Launch {
+  Params use[kMaxUses];
+  int n_uses;
+  const int32_t* order;
+  int64_t n_order;
+  int* counter;
+};
+
 // Build-time variants (kept switchable so they can be measured against each
 // other on the GPU): ring depth, one-pass streaming softmax, and strict
 // alternation of the two head-tiles' exponential bursts (ping-pong).
@@ -349,7 +362,7 @@ __device__ __forceinline__ void zero8(uint32_t* w) {
 // producer resolves visibility per 16-key group: gnv = valid keys in the
 // group, gmask = tile tokens allowed to see it.
 struct __align__(16) ChunkDesc {
-  int ncols, branch, flags, q_first;   // flags: kF* bits | tail-group mask << 8
+  int ncols, branch, flags, q_first;   // flags: kF* bits | NSA use << 16
   int q_cnt, h, qb, item_seq;
   uint32_t gmask[kGroups];             // producer scratch: tokens allowed per group
   int32_t gnv[kGroups];                // valid keys per group (tail groups: < 16)
@@ -421,7 +434,8 @@ constexpr int threads_of() { return 32 * NP * (5 * HP + 1); }
 // exponentials instead of running in lockstep.  Odd pipelines walk their item
 // list backwards so the two of a CTA start on different tiles.
 template <int DH, int HP, int NP>
-__global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Params P) {
+__global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(const __grid_constant__ Launch L) {
+  const Params& P = L.use[0];   // head geometry (shared by all uses); static mode's use
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem<DH, HP, NP>& SM = *reinterpret_cast<Smem<DH, HP, NP>*>(smem_raw);
   using HCols = HeadCols<DH>;
@@ -433,7 +447,8 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
   const int G = P.hq / P.hkv, T = kM / G;
   const int d_model = P.hq * DH;
   const int n_hgroups = P.hkv / HP;
-  const int64_t n_items = P.n_tiles * n_hgroups;
+  const bool dyn = L.order != nullptr;
+  const int64_t n_items = dyn ? L.n_order : P.n_tiles * n_hgroups;
   // role -> pipeline: softmax warps [0, 4*HP*NP), producers, then MMA warps
   const int pipe_id = warp < kSoftWarps ? warp / (4 * HP)
                       : (warp < kSoftWarps + NP ? warp - kSoftWarps
@@ -441,7 +456,9 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
   Pipe<DH, HP>& S = SM.pipe[pipe_id];
   const int64_t n_pipes = (int64_t)gridDim.x * NP;
   const int64_t gp = (int64_t)blockIdx.x * NP + pipe_id;
-  const int64_t m_items = gp < n_items ? (n_items - gp + n_pipes - 1) / n_pipes : 0;
+  // items of this pipeline (static mode); in queue mode only "any" matters:
+  // every pipeline's first item is its own index gp
+  const int64_t m_items = gp < n_items ? (dyn ? 1 : (n_items - gp + n_pipes - 1) / n_pipes) : 0;
   auto item_of = [&](int64_t k) -> int64_t {
     return (pipe_id & 1) ? gp + (m_items - 1 - k) * n_pipes : gp + k * n_pipes;
   };
@@ -474,7 +491,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
   }
   for (int i = tid; i < NP * kBitmapWords; i += blockDim.x)
     SM.pipe[i / kBitmapWords].bitmap[i % kBitmapWords] = 0u;
-  const bool bias_smem = P.gbias && P.n_gates * P.hq * (DH + 1) <= kBiasMax;
+  const bool bias_smem = !dyn && P.gbias && P.n_gates * P.hq * (DH + 1) <= kBiasMax;
   if (bias_smem)
     for (int i = tid; i < P.n_gates * d_model; i += blockDim.x)
       SM.bias[(i / DH) * (DH + 1) + i % DH] = P.gbias[i];
@@ -494,12 +511,29 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
     uint32_t c = 0;
     int it = 0;
     const uint32_t all_tok = T >= 32 ? 0xffffffffu : ((1u << T) - 1u);
-    for (int64_t kk_item = 0; kk_item < m_items; ++kk_item, ++it) {
-      const int64_t item = item_of(kk_item);
+    int64_t cur = dyn ? gp : 0;   // queue mode: global queue position; static: k
+    for (;;) {
+      if (!dyn && cur >= m_items) break;
+      if (dyn && cur >= n_items) break;
+      int64_t nxt = cur + 1;
+      if (dyn) {   // claim the next queue entry now, so the last item is known
+        if (lane == 0) nxt = n_pipes + (int64_t)atomicAdd(L.counter, 1);
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+      }
+      const bool last_item = dyn ? nxt >= n_items : nxt >= m_items;
+      int use = 0;
+      int64_t item;
+      if (dyn) {
+        const int32_t code = L.order[cur];
+        use = code >> 28;
+        item = code & 0x0FFFFFFF;
+      } else {
+        item = item_of(cur);
+      }
+      const Params& P = L.use[use];
       const int tile = (int)(item / n_hgroups), h0 = (int)(item % n_hgroups) * HP;
       const int q_first = P.tiles[4 * tile], q_cnt = P.tiles[4 * tile + 1],
                 own = P.tiles[4 * tile + 2];
-      const bool last_item = kk_item == m_items - 1;
       const int qb = it & 1;
       // ---- selected rows of the tile tokens (resolved rows are -1 padded)
       const int n_ent = T * P.kmax, n_valid_ent = q_cnt * P.kmax;
@@ -624,14 +658,14 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
         const int64_t head_rows = br == 0 ? cmp_rows : P.n_rows_pad;
         const __nv_bfloat16* kb = (br == 0 ? P.kc_il : P.k_il) + (int64_t)h0 * head_rows * DH;
         const __nv_bfloat16* vb = (br == 0 ? P.vc_il : P.v_il) + (int64_t)h0 * head_rows * VW;
-        int cur = 0;
+        int cur_seg = 0;   // first segment not yet consumed by earlier chunks
         for (int64_t start = 0; start < total; start += kNK) {
           const int64_t end = lmin(start + kNK, total);
           const int st = c % kStages;
           if (c >= kStages) mbar_wait(&S.kv_empty[st], ((c / kStages) - 1) & 1);
           if (lane == 0) trace(trp, c, 0);
           ChunkDesc& D = S.desc[st];
-          const int s = cur + lane;
+          const int s = cur_seg + lane;
           bool ov = false, done = false;
           int col = 0, ncols = 0, nvalid = 0;
           uint32_t tm = all_tok;
@@ -667,15 +701,12 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
           __syncwarp();
           const int n_grp = (int)(end - start) / 16;
           if (lane == 0) {
-            uint32_t tail = 0;
-            for (int gi = 0; gi < n_grp; ++gi)
-              if (D.gnv[gi] > 0 && D.gnv[gi] < 16) tail |= 1u << gi;
             const bool li = end == total && br == P.n_gates - 1;
             D.ncols = (int)(end - start);
             D.branch = br;
             D.flags = (start == 0 ? kFFirstBranch : 0) | (end == total ? kFLastBranch : 0) |
                       (br == 0 && start == 0 ? kFFirstItem : 0) | (li ? kFLastItem : 0) |
-                      (li && last_item ? kFLastOverall : 0) | (int)(tail << 8);
+                      (li && last_item ? kFLastOverall : 0) | (use << 16);
             D.q_first = q_first;
             D.q_cnt = q_cnt;
             D.h = h0;
@@ -703,11 +734,13 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
                        ncols * VW * 2u, &S.kv_full[st]);
             }
           }
-          cur += __popc(__ballot_sync(0xffffffffu, done));
+          cur_seg += __popc(__ballot_sync(0xffffffffu, done));
           ++c;
         }
       }
       __syncwarp();
+      cur = nxt;
+      ++it;
     }
   } else if (warp >= kProducerWarp + NP) {
     // ===================== MMA issuer of head-tile hh (one warp per head-tile,
@@ -791,7 +824,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
     float m_run = kNegInf;
     // finished-branch state: its epilogue runs in the next chunk, before that
     // chunk's PV overwrites O
-    int br_pend = 0, head_pend = 0;
+    int br_pend = 0, head_pend = 0, use_pend = 0;
     bool lastit_pend = false, rowok_pend = false, epi_pend = false;
     int64_t tok_pend = 0;
     __nv_bfloat16* const gate_s = &S.gate[hh][m * DH];   // this row's staged gate logits
@@ -853,7 +886,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
         }
         if (lastit_pend) {
           if (rowok_pend) {
-            __nv_bfloat16* op = P.out + tok_pend * d_model + head_pend * DH + c0;
+            __nv_bfloat16* op = L.use[use_pend].out + tok_pend * d_model + head_pend * DH + c0;
 #pragma unroll
             for (int k8 = 0; k8 < 2; ++k8) {
               const float* v = reinterpret_cast<const float*>(r + 8 * k8);
@@ -896,7 +929,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
       tmem_wait_ld();
       if (tid == 0) trace(trp, c, 1);
 #endif
-      const int br = hdr0.y, fl = hdr0.z;
+      const int br = hdr0.y, fl = hdr0.z, use_c = fl >> 16;
       const bool first_br = fl & kFFirstBranch, last_br = fl & kFLastBranch,
                  last_it = fl & kFLastItem, last_all = fl & kFLastOverall;
       const bool row_ok = t < hdr1.x;
@@ -1128,12 +1161,14 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(Para
       if (tid == 0) trace(trp, c, 4);
       if (last_br) {
         if (row_ok) {   // stage this branch's gate logits for its epilogue
-          const __nv_bfloat16* gp = P.gl + tok * P.ld_gl + P.gcol0 + (int64_t)br * d_model +
+          const Params& PU = L.use[use_c];
+          const __nv_bfloat16* gp = PU.gl + tok * PU.ld_gl + PU.gcol0 + (int64_t)br * d_model +
                                     head * DH;
 #pragma unroll
           for (int c0 = 0; c0 < DH; c0 += 8) cp_async16(gate_s + c0, gp + c0, 16u);
         }
         br_pend = br;
+        use_pend = use_c;
         head_pend = head;
         tok_pend = tok;
         rowok_pend = row_ok;
@@ -1223,6 +1258,46 @@ __global__ void kv_interleave_kernel(int src_bf16, const void* __restrict__ src,
 
 using namespace lsrm;
 
+namespace lsrm {
+namespace tc {
+// Picks the variant and grid: d_h = 32 runs two independent single-head
+// pipelines per CTA (or, with -DLSRM_HEADPAIR in static mode, one pipeline
+// whose items are kv-head pairs); d_h = 64 one pipeline (TMEM budget).
+static int launch(const Launch& L, int dh, int hkv, int64_t n_tiles_static, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int dev = 0, n_sm = 148;
+  LSRM_CUDA(cudaGetDevice(&dev));
+  LSRM_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  const bool dyn = L.order != nullptr;
+#ifdef LSRM_HEADPAIR
+  const int hp = (!dyn && dh == 32 && hkv % 2 == 0) ? 2 : 1, np_ = hp == 2 ? 1 : (dh == 32 ? 2 : 1);
+#else
+  const int hp = 1, np_ = dh == 32 ? 2 : 1;
+#endif
+  const int64_t n_items = dyn ? L.n_order : n_tiles_static * (hkv / hp);
+  if (n_items == 0) return LSRM_OK;
+  if (dyn) LSRM_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(int), st));
+  const int64_t want = (n_items + np_ - 1) / np_;
+  const unsigned grid = (unsigned)(want < n_sm ? want : n_sm);
+#define LSRM_TC_CASE(D, HP, NP)                                                             \
+  if (dh == D && hp == HP && np_ == NP) {                                                   \
+    size_t smem = sizeof(Smem<D, HP, NP>) + 1024;                                           \
+    LSRM_CUDA(cudaFuncSetAttribute(nsa_fused_kernel<D, HP, NP>,                             \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    nsa_fused_kernel<D, HP, NP><<<grid, threads_of<HP, NP>(), smem, st>>>(L);               \
+  } else
+  LSRM_TC_CASE(32, 1, 2)
+  LSRM_TC_CASE(32, 2, 1)
+  LSRM_TC_CASE(32, 1, 1)
+  LSRM_TC_CASE(64, 1, 1)
+  return set_error(LSRM_E_CONFIG, "tcgen05 path: head_dim %d not in {32,64}", dh);
+#undef LSRM_TC_CASE
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+}  // namespace tc
+}  // namespace lsrm
+
 extern "C" {
 
 int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int hkv, int dh,
@@ -1274,36 +1349,65 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
   p.gbias = gate_bias;
   p.n_gates = n_gates;
   p.out = (__nv_bfloat16*)merged;
-  cudaStream_t st = as_stream(stream);
-  int dev = 0, n_sm = 148;
-  LSRM_CUDA(cudaGetDevice(&dev));
-  LSRM_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  // d_h = 32: two independent single-head pipelines per CTA (or, with
-  // -DLSRM_HEADPAIR, one pipeline whose items are kv-head pairs); d_h = 64:
-  // one pipeline (TMEM)
-#ifdef LSRM_HEADPAIR
-  const int hp = (dh == 32 && hkv % 2 == 0) ? 2 : 1, np_ = 1;
-#else
-  const int hp = 1, np_ = dh == 32 ? 2 : 1;
-#endif
-  int64_t n_items = n_tiles * (hkv / hp);
-  int64_t want = (n_items + np_ - 1) / np_;
-  unsigned grid = (unsigned)(want < n_sm ? want : n_sm);
-#define LSRM_TC_CASE(D, HP, NP)                                                             \
-  if (dh == D && hp == HP && np_ == NP) {                                                   \
-    size_t smem = sizeof(tc::Smem<D, HP, NP>) + 1024;                                       \
-    LSRM_CUDA(cudaFuncSetAttribute(tc::nsa_fused_kernel<D, HP, NP>,                         \
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    tc::nsa_fused_kernel<D, HP, NP><<<grid, tc::threads_of<HP, NP>(), smem, st>>>(p);       \
-  } else
-  LSRM_TC_CASE(32, 1, 2)
-  LSRM_TC_CASE(32, 2, 1)
-  LSRM_TC_CASE(32, 1, 1)
-  LSRM_TC_CASE(64, 1, 1)
-  return set_error(LSRM_E_CONFIG, "tcgen05 path: head_dim %d not in {32,64}", dh);
-#undef LSRM_TC_CASE
-  LSRM_LAUNCHED();
-  return LSRM_OK;
+  tc::Launch L{};
+  L.use[0] = p;
+  L.n_uses = 1;
+  return tc::launch(L, dh, hkv, n_tiles, stream);
+}
+
+int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, int hkv, int dh,
+                                const int32_t* order, int64_t n_order, int32_t* counter,
+                                void* stream) {
+  LSRM_REQUIRE(n_uses >= 1 && n_uses <= tc::kMaxUses, "tc_multi: 1..%d uses, got %d",
+               tc::kMaxUses, n_uses);
+  LSRM_REQUIRE(order && counter, "tc_multi: needs the item order and a counter");
+  LSRM_REQUIRE(hq % hkv == 0, "n_q_heads=%d not divisible by n_kv_heads=%d", hq, hkv);
+  const int G = hq / hkv;
+  LSRM_REQUIRE(G >= 4 && G <= tc::kM && tc::kM % G == 0 && tc::kM / G <= 32,
+               "tcgen05 path needs 4 <= hq/hkv, (hq/hkv) | 128, got %d", G);
+  tc::Launch L{};
+  for (int u = 0; u < n_uses; ++u) {
+    const lsrm_nsa_use& U = uses[u];
+    LSRM_REQUIRE(U.n_gates == 2 || U.n_gates == 3, "use %d: n_gates must be 2 or 3", u);
+    LSRM_REQUIRE((tc::kM / G) * U.kmax_rows <= tc::kMaxEnt,
+                 "use %d: tile tokens x selected rows exceeds %d", u, tc::kMaxEnt);
+    LSRM_REQUIRE(U.ld_q % 8 == 0 && U.ld_gl % 8 == 0 && U.gate_col0 % 8 == 0,
+                 "use %d: row strides must be multiples of 8 elements", u);
+    if (U.n_blocks == 0) return set_error(LSRM_E_EMPTY_CONTEXT, "use %d: no occupied KV blocks", u);
+    LSRM_REQUIRE(U.n_blocks <= (int64_t)tc::kBitmapWords * 32,
+                 "use %d: %lld occupied KV blocks exceed %d", u, (long long)U.n_blocks,
+                 tc::kBitmapWords * 32);
+    tc::Params& p = L.use[u];
+    p.q = (const __nv_bfloat16*)U.q;
+    p.ld_q = U.ld_q;
+    p.nq = U.nq;
+    p.hq = hq;
+    p.hkv = hkv;
+    p.k_il = (const __nv_bfloat16*)U.k_il;
+    p.v_il = (const __nv_bfloat16*)U.v_il;
+    p.pad_off = U.pad_offsets;
+    p.kv_off = U.kv_offsets;
+    p.n_rows_pad = U.n_kv_rows_pad;
+    p.kc_il = (const __nv_bfloat16*)U.kcmp_il;
+    p.vc_il = (const __nv_bfloat16*)U.vcmp_il;
+    p.n_blocks = U.n_blocks;
+    p.tiles = U.tiles;
+    p.n_tiles = U.n_tiles;
+    p.rows = U.rows;
+    p.count = U.count;
+    p.kmax = (int)U.kmax_rows;
+    p.gl = (const __nv_bfloat16*)U.gate_logits;
+    p.ld_gl = U.ld_gl;
+    p.gcol0 = U.gate_col0;
+    p.gbias = nullptr;   // folded into the gate logits by the caller
+    p.n_gates = (int)U.n_gates;
+    p.out = (__nv_bfloat16*)U.merged;
+  }
+  L.n_uses = n_uses;
+  L.order = order;
+  L.n_order = n_order;
+  L.counter = counter;
+  return tc::launch(L, dh, hkv, 0, stream);
 }
 
 int lsrm_debug_set_trace(void* buf) {

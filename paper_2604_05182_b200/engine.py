@@ -64,6 +64,18 @@ class KvJob(C.Structure):
                 ("mean_out", C.c_void_p), ("cmp_il", C.c_void_p), ("cmp_rows_pad", C.c_int64)]
 
 
+class NsaUse(C.Structure):
+    """Mirror of `lsrm_nsa_use` (include/lsrm_b200.h)."""
+    _fields_ = [("q", C.c_void_p), ("ld_q", C.c_int64), ("nq", C.c_int64),
+                ("k_il", C.c_void_p), ("v_il", C.c_void_p), ("pad_offsets", C.c_void_p),
+                ("kv_offsets", C.c_void_p), ("n_kv_rows_pad", C.c_int64),
+                ("kcmp_il", C.c_void_p), ("vcmp_il", C.c_void_p), ("n_blocks", C.c_int64),
+                ("tiles", C.c_void_p), ("n_tiles", C.c_int64), ("rows", C.c_void_p),
+                ("count", C.c_void_p), ("kmax_rows", C.c_int64), ("gate_logits", C.c_void_p),
+                ("ld_gl", C.c_int64), ("gate_col0", C.c_int64), ("n_gates", C.c_int64),
+                ("merged", C.c_void_p)]
+
+
 class PackedShard:
     """Byte layout of one rank's KV shard for one use: interleaved K
     [hkv, rows_pad, dh] bf16, V [hkv, rows_pad, dh+16] bf16, compressed K and
@@ -271,6 +283,8 @@ class SparseLayerEngine:
                 self.buf[("vc_loc", use)] = buf[lay.off_vc:].view(torch.float32).view(
                     lay.n_blocks, w)
         self._build_kv_jobs()
+        if not self.sharded:
+            self._build_attention_queue()
 
     def _build_kv_jobs(self):
         """Device array of `lsrm_kv_job`: K and V of every use (one launch)."""
@@ -304,6 +318,52 @@ class SparseLayerEngine:
         raw = b"".join(C.string_at(C.addressof(j), C.sizeof(j)) for j in jobs)
         self.kv_jobs = D.dev(np.frombuffer(raw, dtype=np.uint8).copy()) if jobs else None
         self.n_kv_jobs, self.kv_max_blocks = len(jobs), max_blocks
+
+    def _build_attention_queue(self):
+        """One launch for the four uses: per-use descriptors and a
+        heaviest-first item order. An item is (use, tile, kv head); its cost is
+        the keys it streams: compressed rows + the padded union of its tokens'
+        selected blocks + (self uses) its own block."""
+        p = self.params
+        hkv = p.n_kv_heads
+        uses, costs, codes = [], [], []
+        for ui, use in enumerate(USES):
+            qs, ks, ng = USE_GEOM[use]
+            mq, mk = self.meta[qs], self.meta[ks]
+            Y = self.buf[("Y", qs)]
+            qcol = self.cols[(use, "q")]
+            tiles = self.tiles[use]
+            uses.append(NsaUse(
+                Y[:, qcol:].data_ptr(), Y.stride(0), mq.n_loc,
+                self.buf[("k_il", use)].data_ptr(), self.buf[("v_il", use)].data_ptr(),
+                mk.pad_off.data_ptr(), mk.kv_off.data_ptr(), mk.n_rows_pad,
+                self.buf[("kc_il", use)].data_ptr(), self.buf[("vc_il", use)].data_ptr(),
+                mk.n_blocks, tiles.data_ptr(), int(tiles.shape[0]), self.rows[use].data_ptr(),
+                self.count[use].data_ptr(), self.kmax[use], Y.data_ptr(), Y.stride(0),
+                qcol + self.d, ng, self.buf[("merged", use)].data_ptr()))
+            th = D.host(tiles)
+            rows = D.host(self.rows[use])
+            padlen = np.diff(mk.pad_off_host)
+            cmp_rows = (mk.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
+            for t, (first, cnt, own, _) in enumerate(th):
+                r = rows[first:first + cnt].ravel()
+                r = np.unique(r[r >= 0])
+                c = cmp_rows + int(padlen[r].sum()) + (int(padlen[own]) if own >= 0 else 0)
+                for h in range(hkv):
+                    costs.append(c)
+                    codes.append((ui << 28) | (t * hkv + h))
+        costs, codes = np.asarray(costs, np.int64), np.asarray(codes, np.int64)
+        order = codes[np.lexsort((codes, -costs))].astype(np.int32)
+        self.attn_uses = (NsaUse * len(uses))(*uses)
+        self.attn_order = D.dev(order)
+        self.attn_counter = D.zeros((1,), torch.int32)
+
+    def attend_all(self):
+        """The four uses' fused attention in one persistent launch (LPT queue)."""
+        p = self.params
+        call("lsrm_nsa_attention_tc_multi", C.cast(self.attn_uses, C.c_void_p), len(USES),
+             p.n_q_heads, p.n_kv_heads, p.head_dim, self.attn_order.data_ptr(),
+             int(self.attn_order.shape[0]), self.attn_counter.data_ptr(), D.stream())
 
     # -- pieces --------------------------------------------------------------
     def project(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
@@ -366,8 +426,8 @@ class SparseLayerEngine:
             return self.forward_exchange()
         self.project(x_loc, y_loc)
         self.prepare_kv()
+        self.attend_all()
         for use in USES:
-            self.attend(use)
             self.output(use)
         return {u: self.buf[("out", u)] for u in USES}
 

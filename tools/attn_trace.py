@@ -49,6 +49,14 @@ def main():
             tot += ms
             print(f"attention {use}: {ms * 1e3:8.1f} us")
         print(f"attention total: {tot * 1e3:8.1f} us")
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng.attend_all()
+        a.record()
+        for _ in range(10):
+            eng.attend_all()
+        b.record()
+        torch.cuda.synchronize()
+        print(f"attention merged launch (4 uses, LPT queue): {a.elapsed_time(b) / 10 * 1e3:8.1f} us")
     buf = torch.zeros((256, 32), dtype=torch.int64, device="cuda")
     call("lsrm_debug_set_trace", buf.data_ptr())
     eng.attend(args.use)
