@@ -211,7 +211,9 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
 /* All NSA uses of a layer (same head geometry) in ONE persistent launch, with
  * a heaviest-first work queue.  Each use is described like the arguments of
  * lsrm_nsa_attention_tc (uses is a HOST array); gate biases must already be
- * folded into the gate logits.  order [n_order]: (use << 28) | item, item =
+ * folded into the gate logits.  A use may regroup its query tiles through
+ * `perm` (e.g. tokens of a block sorted by selection signature, so a tile's
+ * union of selected blocks shrinks).  order [n_order]: (use << 28) | item, item =
  * tile * hkv + kv head, sorted by estimated cost, descending; counter: one
  * int32 of device memory (zeroed by this call on `stream`). */
 typedef struct lsrm_nsa_use {
@@ -236,6 +238,9 @@ typedef struct lsrm_nsa_use {
   int64_t gate_col0;
   int64_t n_gates;
   void* merged;
+  const int32_t* perm;   /* optional [nq]: tile position -> query row; tiles,
+                            rows and count are then in permuted (tile) order,
+                            q / gate_logits / merged stay in query-row order */
 } lsrm_nsa_use;
 int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, int hkv, int dh,
                                 const int32_t* order, int64_t n_order, int32_t* counter,

@@ -226,6 +226,7 @@ struct Params {
   const int32_t* tiles;
   int64_t n_tiles;
   const int32_t* rows;
+  const int32_t* perm;   // optional: tile position -> query row (rows[] are in tile order)
   const int32_t* count;
   int kmax;
   const __nv_bfloat16* gl;
@@ -367,6 +368,7 @@ struct __align__(16) ChunkDesc {
   uint32_t gmask[kGroups];             // producer scratch: tokens allowed per group
   int32_t gnv[kGroups];                // valid keys per group (tail groups: < 16)
   uint8_t tokvis[32];                  // per tile token: groups it sees (bit g)
+  int32_t tok[32];                     // per tile token: its query row (output / gates)
 };
 constexpr int kFFirstBranch = 1, kFLastBranch = 2, kFFirstItem = 4, kFLastItem = 8,
               kFLastOverall = 16;
@@ -553,9 +555,9 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
         const int m = rem / (DH / 8), cc = rem % (DH / 8);
         const int tt = m / G, gg = m % G;
         const bool ok = tt < q_cnt;
+        const int64_t qrow = ok ? (P.perm ? P.perm[q_first + tt] : q_first + tt) : 0;
         const __nv_bfloat16* src =
-            P.q + (ok ? (int64_t)(q_first + tt) * P.ld_q + ((h0 + hh) * G + gg) * DH + cc * 8
-                      : 0);
+            P.q + (ok ? qrow * P.ld_q + ((h0 + hh) * G + gg) * DH + cc * 8 : 0);
         cp_async16(&S.q[qb][hh][(m / 8) * (8 * DH) + cc * 64 + (m % 8) * 8], src,
                    ok ? 16u : 0u);
       }
@@ -719,6 +721,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
               for (int gi = 0; gi < n_grp; ++gi)
                 if (D.gnv[gi] > 0 && ((D.gmask[gi] >> lane) & 1u)) v |= 1u << gi;
             D.tokvis[lane] = (uint8_t)v;
+            D.tok[lane] = lane < q_cnt ? (P.perm ? P.perm[q_first + lane] : q_first + lane) : 0;
           }
           __syncwarp();
           if (lane == 0)
@@ -933,7 +936,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const bool first_br = fl & kFFirstBranch, last_br = fl & kFLastBranch,
                  last_it = fl & kFLastItem, last_all = fl & kFLastOverall;
       const bool row_ok = t < hdr1.x;
-      const int64_t tok = (int64_t)hdr0.w + t;
+      const int64_t tok = D.tok[t];
       const int head = (hdr1.y + hh) * G + g_in;
       // `live` groups are seen by some row of this warp (others are skipped,
       // P = 0); a row sees a group if its token selected it (visb).  Block
@@ -1342,6 +1345,7 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
   p.n_tiles = n_tiles;
   p.rows = rows;
   p.count = count;
+  p.perm = nullptr;
   p.kmax = kmax_rows;
   p.gl = (const __nv_bfloat16*)gate_logits;
   p.ld_gl = ld_gl;
@@ -1395,6 +1399,7 @@ int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, in
     p.n_tiles = U.n_tiles;
     p.rows = U.rows;
     p.count = U.count;
+    p.perm = U.perm;
     p.kmax = (int)U.kmax_rows;
     p.gl = (const __nv_bfloat16*)U.gate_logits;
     p.ld_gl = U.ld_gl;

@@ -73,7 +73,7 @@ class NsaUse(C.Structure):
                 ("tiles", C.c_void_p), ("n_tiles", C.c_int64), ("rows", C.c_void_p),
                 ("count", C.c_void_p), ("kmax_rows", C.c_int64), ("gate_logits", C.c_void_p),
                 ("ld_gl", C.c_int64), ("gate_col0", C.c_int64), ("n_gates", C.c_int64),
-                ("merged", C.c_void_p)]
+                ("merged", C.c_void_p), ("perm", C.c_void_p)]
 
 
 class PackedShard:
@@ -333,16 +333,26 @@ class SparseLayerEngine:
             Y = self.buf[("Y", qs)]
             qcol = self.cols[(use, "q")]
             tiles = self.tiles[use]
+            # tokens of each query block sorted by selection signature: tiles of
+            # similar tokens have smaller unions of selected blocks
+            rows_h = D.host(self.rows[use])
+            cnt_h = D.host(self.count[use])
+            blk = np.repeat(np.arange(mq.loc_off_host.size - 1), np.diff(mq.loc_off_host))
+            key = np.sort(np.where(rows_h >= 0, rows_h, np.iinfo(np.int32).max), axis=1)
+            perm = np.lexsort(tuple(key[:, j] for j in reversed(range(key.shape[1]))) + (blk,))
+            rows = np.ascontiguousarray(rows_h[perm])
+            perm_d = D.dev(perm.astype(np.int32))
+            rows_d, cnt_d = D.dev(rows), D.dev(np.ascontiguousarray(cnt_h[perm]))
+            self._job_refs += [perm_d, rows_d, cnt_d]
             uses.append(NsaUse(
                 Y[:, qcol:].data_ptr(), Y.stride(0), mq.n_loc,
                 self.buf[("k_il", use)].data_ptr(), self.buf[("v_il", use)].data_ptr(),
                 mk.pad_off.data_ptr(), mk.kv_off.data_ptr(), mk.n_rows_pad,
                 self.buf[("kc_il", use)].data_ptr(), self.buf[("vc_il", use)].data_ptr(),
-                mk.n_blocks, tiles.data_ptr(), int(tiles.shape[0]), self.rows[use].data_ptr(),
-                self.count[use].data_ptr(), self.kmax[use], Y.data_ptr(), Y.stride(0),
-                qcol + self.d, ng, self.buf[("merged", use)].data_ptr()))
+                mk.n_blocks, tiles.data_ptr(), int(tiles.shape[0]), rows_d.data_ptr(),
+                cnt_d.data_ptr(), self.kmax[use], Y.data_ptr(), Y.stride(0),
+                qcol + self.d, ng, self.buf[("merged", use)].data_ptr(), perm_d.data_ptr()))
             th = D.host(tiles)
-            rows = D.host(self.rows[use])
             padlen = np.diff(mk.pad_off_host)
             cmp_rows = (mk.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
             for t, (first, cnt, own, _) in enumerate(th):
