@@ -283,8 +283,7 @@ class SparseLayerEngine:
                 self.buf[("vc_loc", use)] = buf[lay.off_vc:].view(torch.float32).view(
                     lay.n_blocks, w)
         self._build_kv_jobs()
-        if not self.sharded:
-            self._build_attention_queue()
+        self._build_attention_queue()
 
     def _build_kv_jobs(self):
         """Device array of `lsrm_kv_job`: K and V of every use (one launch)."""
@@ -454,7 +453,8 @@ class SparseLayerEngine:
         for use in USES:
             handles[use]()          # wait + place into the canonical layout
             self.finish_kv(use)
-            self.attend(use)
+        self.attend_all()
+        for use in USES:
             self.output(use)
         return {u: self.buf[("out", u)] for u in USES}
 

@@ -520,7 +520,8 @@ class ShardedLayer:
         for use in USES:
             self.exchange.place(self.engine, use)
             self.engine.finish_kv(use)
-            self.engine.attend(use)
+        self.engine.attend_all()
+        for use in USES:
             self.engine.output(use)
 
     def capture(self, x_loc, y_loc):
@@ -556,16 +557,14 @@ class ShardedLayer:
         return {u: (self.tok_host[USE_GEOM[u][0]], D.host(o.float())) for u, o in outs.items()}
 
     def attention_ms(self, reps: int = 5) -> float:
-        """Device time of this rank's four attention launches (events on the
-        launching stream; KV already placed by the last step)."""
-        from .engine import USES
+        """Device time of this rank's attention launch (all four uses; events
+        on the launching stream; KV already placed by the last step)."""
         st = torch.cuda.current_stream()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record(st)
         for _ in range(reps):
-            for use in USES:
-                self.engine.attend(use)
+            self.engine.attend_all()
         b.record(st)
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
