@@ -272,7 +272,8 @@ int lsrm_debug_set_trace(void* buf);
  * [n_blocks+1] 16-row-padded offsets into il.  Writes the interleaved layout
  * il [hkv][rows_pad][dh+ones_cols] (ones_cols = 16 for V: row-sum columns), the
  * ResBlock block means (tensor-core bf16 MLP, fp32 accumulation, fixed-order
- * sums) to mean_out [n_blocks][hkv*dh] f32 and/or, interleaved, to cmp_il
+ * sums; one CTA per 64-token sub-tile, the block's last-arriving CTA adds
+ * the sub-tiles' partials in order) to mean_out [n_blocks][hkv*dh] f32 and/or, interleaved, to cmp_il
  * [hkv][cmp_rows_pad][dh+ones_cols] (either may be NULL).  jobs points to
  * DEVICE memory; hkv*dh must be 64 or 128. */
 typedef struct lsrm_kv_job {
@@ -284,15 +285,21 @@ typedef struct lsrm_kv_job {
   int64_t rows_pad;
   void* il;
   int64_t ones_cols;
-  const float* w1;
+  const void* w1;        /* [w][w] bf16, r = x W1 (w = hkv*dh) */
   const float* b1;
-  const float* w2;
+  const void* w2;        /* [w][w] bf16 */
   const float* b2;
   float* mean_out;
   void* cmp_il;
   int64_t cmp_rows_pad;
+  const int32_t* work;   /* [n_work]: block * 16 + 64-token sub-tile, by block;
+                            one CTA each */
+  int64_t n_work;
+  float* partial;        /* [n_work][hkv*dh] scratch: per-sub-tile column sums */
+  int32_t* arrive;       /* [n_blocks] counters, zero between launches (the
+                            block's last-arriving CTA resets its entry) */
 } lsrm_kv_job;
-int lsrm_kv_prepare_jobs(const lsrm_kv_job* jobs, int n_jobs, int64_t max_blocks, int hkv,
+int lsrm_kv_prepare_jobs(const lsrm_kv_job* jobs, int n_jobs, int64_t max_work, int hkv,
                          int dh, void* stream);
 
 /* Byte-segment copy: segs [n_segs, 3] int64 = (src offset, dst offset,

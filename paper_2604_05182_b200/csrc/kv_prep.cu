@@ -5,13 +5,14 @@
 //
 // Job j = one K or V tensor of one NSA use: token rows [n, w = hkv*dh] bf16
 // (a column slice of the fused projection output, block-major order).
-// CTA (block b, job j), 4 warps, loops over 64-token sub-tiles of the block:
+// CTA (64-token sub-tile of a block, job j), 4 warps:
 //   1. rows -> shared memory, and -> the padded 8x8-core-matrix interleaved
 //      layout of the tcgen05 attention (plus the 16 ones columns for V);
 //   2. ResBlock r = x + W2 gelu(W1 x + b1) + b2 on the tensor cores
 //      (mma.sync m16n8k16 bf16, fp32 accumulation; warp = 16 tokens);
-//   3. per-column sums of r over the block's tokens, reduced in a fixed order
-//      (deterministic), -> the block mean (the compressed K/V row).
+//   3. per-column sums of r over the sub-tile's tokens (fixed order) -> a
+//      partial row; the block's last-arriving CTA adds its sub-tiles' partials
+//      in sub-tile order (deterministic) -> the block mean (compressed row).
 // The compressed row goes to mean_out (f32, for the All-gather-KV shard) and/or
 // directly into the interleaved compressed layout cmp_il.
 #include "common.cuh"
@@ -27,10 +28,17 @@ struct KvJob {
   int64_t n_blocks, rows_pad;
   __nv_bfloat16* il;
   int64_t ones_cols;
-  const float *w1, *b1, *w2, *b2;
+  const __nv_bfloat16* w1;   // [W][W] bf16 (r = x W1)
+  const float* b1;
+  const __nv_bfloat16* w2;
+  const float* b2;
   float* mean_out;
   __nv_bfloat16* cmp_il;
   int64_t cmp_rows_pad;
+  const int32_t* work;   // per CTA: block * 16 + 64-token sub-tile, ordered by block
+  int64_t n_work;
+  float* partial;        // [n_work][W] per-sub-tile column sums
+  int32_t* arrive;       // [n_blocks] arrival counters (zero between launches)
 };
 static_assert(sizeof(KvJob) == sizeof(lsrm_kv_job), "KvJob must mirror lsrm_kv_job");
 
@@ -77,25 +85,31 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
   __nv_bfloat16* const w1s = hs + kSub * LDS;                             // [W][LDS]
   __nv_bfloat16* const w2s = w1s + W * LDS;                               // [W][LDS]
   float (*csum)[W] = reinterpret_cast<float (*)[W]>(w2s + W * LDS);       // [4][W]
+  __shared__ int s_last;
   const KvJob& J = jobs[blockIdx.y];
-  const int64_t b = blockIdx.x;
-  if (b >= J.n_blocks) return;
+  const int64_t wi = blockIdx.x;
+  if (wi >= J.n_work) return;
+  const int code = J.work[wi];
+  const int64_t b = code >> 4, sub = code & 15;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int hkv = W / dh, vw = dh + (int)J.ones_cols;
   const int64_t lo = J.blk_off[b], occ = J.blk_off[b + 1] - lo, prow0 = J.pad_off[b];
-  // weights -> bf16 smem (W1, W2 are [in][out] row-major: r = x W)
-  for (int i = tid; i < W * W; i += 128) {
-    w1s[(i / W) * LDS + i % W] = __float2bfloat16_rn(J.w1[i]);
-    w2s[(i / W) * LDS + i % W] = __float2bfloat16_rn(J.w2[i]);
+  const int64_t n_sub = (occ + kSub - 1) / kSub;
+  // bf16 weights -> smem (16-byte chunks; W1, W2 are [in][out]: r = x W)
+  for (int i = tid; i < W * W / 8; i += 128) {
+    const int r = i / (W / 8), c8 = (i % (W / 8)) * 8;
+    *reinterpret_cast<uint4*>(&w1s[r * LDS + c8]) = *reinterpret_cast<const uint4*>(J.w1 + r * W + c8);
+    *reinterpret_cast<uint4*>(&w2s[r * LDS + c8]) = *reinterpret_cast<const uint4*>(J.w2 + r * W + c8);
   }
   // this thread's accumulator columns: n-tile nt, cols 8nt + 2(lane%4) + {0,1}
   const int g = lane >> 2, t4 = lane & 3;
   float cs[NT][2];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) cs[nt][0] = cs[nt][1] = 0.f;
-  for (int64_t s0 = 0; s0 < occ; s0 += kSub) {
+  {
+    const int64_t s0 = sub * kSub;
     const int nt_valid = (int)(occ - s0 < kSub ? occ - s0 : kSub);
-    __syncthreads();   // previous sub-tile done with xs / hs (and weights staged)
+    __syncthreads();   // weights staged
     // 1. rows -> smem + interleaved layout
     for (int e = tid; e < kSub * (W / 8); e += 128) {
       const int r = e / (W / 8), ch = e % (W / 8);
@@ -183,18 +197,6 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
       }
     }
   }
-  // K padding rows of the block segment repeat its first key (a duplicate key
-  // cannot raise a row max; the matching V rows stay zero): no padding masks
-  // in the attention kernel
-  if (!J.ones_cols) {
-    const int64_t plen = J.pad_off[b + 1] - prow0;
-    for (int e = tid; e < (plen - occ) * (W / 8); e += 128) {
-      const int64_t r = occ + e / (W / 8);
-      const int col = (e % (W / 8)) * 8, h = col / dh;
-      const uint4 v = *reinterpret_cast<const uint4*>(J.src + lo * J.ld + col);
-      *reinterpret_cast<uint4*>(J.il + il_off(h, J.rows_pad, vw, prow0 + r, col - h * dh)) = v;
-    }
-  }
   // 4. fixed-order reduction: lanes with equal t4 (xor 4, 8, 16), then warps
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
@@ -207,9 +209,33 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
       if (g == 0) csum[warp][8 * nt + 2 * t4 + e] = v;
     }
   __syncthreads();
+  for (int col = tid; col < W; col += 128)
+    J.partial[wi * W + col] = ((csum[0][col] + csum[1][col]) + csum[2][col]) + csum[3][col];
+  // 5. the block's last-arriving CTA finishes it
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&J.arrive[b], 1) == (int)n_sub - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t w0 = wi - sub;   // partial row of the block's sub-tile 0
+  // K padding rows of the block segment repeat its first key (a duplicate key
+  // cannot raise a row max; the matching V rows stay zero): no padding masks
+  // in the attention kernel
+  if (!J.ones_cols) {
+    const int64_t plen = J.pad_off[b + 1] - prow0;
+    for (int e = tid; e < (plen - occ) * (W / 8); e += 128) {
+      const int64_t r = occ + e / (W / 8);
+      const int col = (e % (W / 8)) * 8, h = col / dh;
+      const uint4 v = *reinterpret_cast<const uint4*>(J.src + lo * J.ld + col);
+      *reinterpret_cast<uint4*>(J.il + il_off(h, J.rows_pad, vw, prow0 + r, col - h * dh)) = v;
+    }
+  }
   const float inv = 1.f / (float)occ;
   for (int col = tid; col < W; col += 128) {
-    const float mean = (((csum[0][col] + csum[1][col]) + csum[2][col]) + csum[3][col]) * inv;
+    float tot = 0.f;
+    for (int64_t k = 0; k < n_sub; ++k) tot += __ldcg(J.partial + (w0 + k) * W + col);
+    const float mean = tot * inv;
     if (J.mean_out) J.mean_out[b * W + col] = mean;
     if (J.cmp_il) {
       const int h = col / dh;
@@ -219,6 +245,7 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
           J.cmp_il[il_off(h, J.cmp_rows_pad, vw, r, col - h * dh)] = __float2bfloat16_rn(mean);
     }
   }
+  if (tid == 0) J.arrive[b] = 0;   // ready for the next launch
   if (J.cmp_il && J.ones_cols)
     for (int e = tid; e < hkv * (int)J.ones_cols; e += 128) {
       const int h = e / (int)J.ones_cols, cc = e % (int)J.ones_cols;
@@ -230,14 +257,14 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
 
 using namespace lsrm;
 
-extern "C" int lsrm_kv_prepare_jobs(const lsrm_kv_job* jobs, int n_jobs, int64_t max_blocks,
+extern "C" int lsrm_kv_prepare_jobs(const lsrm_kv_job* jobs, int n_jobs, int64_t max_work,
                                     int hkv, int dh, void* stream) {
   const int w = hkv * dh;
   LSRM_REQUIRE(w == 64 || w == 128, "kv_prepare_jobs: width hkv*dh must be 64 or 128, got %d", w);
   LSRM_REQUIRE(dh % 8 == 0, "kv_prepare_jobs: head_dim must be a multiple of 8");
-  if (n_jobs == 0 || max_blocks == 0) return LSRM_OK;
+  if (n_jobs == 0 || max_work == 0) return LSRM_OK;
   cudaStream_t st = as_stream(stream);
-  const dim3 grid((unsigned)max_blocks, (unsigned)n_jobs);
+  const dim3 grid((unsigned)max_work, (unsigned)n_jobs);
   const size_t smem = (size_t)(2 * kSub + 2 * w) * (w + 8) * 2 + 4 * w * sizeof(float);
   if (w == 64) {
     LSRM_CUDA(cudaFuncSetAttribute(kv_prep_kernel<64>,

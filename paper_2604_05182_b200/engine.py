@@ -61,7 +61,9 @@ class KvJob(C.Structure):
                 ("pad_off", C.c_void_p), ("n_blocks", C.c_int64), ("rows_pad", C.c_int64),
                 ("il", C.c_void_p), ("ones_cols", C.c_int64), ("w1", C.c_void_p),
                 ("b1", C.c_void_p), ("w2", C.c_void_p), ("b2", C.c_void_p),
-                ("mean_out", C.c_void_p), ("cmp_il", C.c_void_p), ("cmp_rows_pad", C.c_int64)]
+                ("mean_out", C.c_void_p), ("cmp_il", C.c_void_p), ("cmp_rows_pad", C.c_int64),
+                ("work", C.c_void_p), ("n_work", C.c_int64), ("partial", C.c_void_p),
+                ("arrive", C.c_void_p)]
 
 
 class NsaUse(C.Structure):
@@ -299,6 +301,8 @@ class SparseLayerEngine:
             for kind, wres in (("k", self.cmp_w[use][0]), ("v", self.cmp_w[use][1])):
                 src = Y[:, self.cols[(use, kind)]:]
                 w1, b1, w2, b2 = wres
+                w1, w2 = w1.to(torch.bfloat16).contiguous(), w2.to(torch.bfloat16).contiguous()
+                self._job_refs += [w1, w2]
                 if m.sharded:   # rank-local compact shard; means go to the packed buffer
                     il = self.buf[(kind + "_loc", use)]
                     blk, pad, nb = m.loc_off, m.loc_pad_off, m.owned.size
@@ -307,13 +311,21 @@ class SparseLayerEngine:
                     il = self.buf[(kind + "_il", use)]
                     blk, pad, nb = m.kv_off, m.pad_off, m.n_blocks
                     mean, cmp_il = None, self.buf[(kind + "c_il", use)]
+                occ = np.diff(m.loc_off_host)
+                nsub = (occ + 63) // 64
+                work = np.concatenate([b * 16 + np.arange(k) for b, k in enumerate(nsub)])
+                work_d = D.dev(work.astype(np.int32))
+                partial = D.empty((work.size, self.w), torch.float32)
+                arrive = D.zeros((max(nb, 1),), torch.int32)
                 jobs.append(KvJob(src.data_ptr(), Y.stride(0), blk.data_ptr(), pad.data_ptr(), nb,
                                   int(il.shape[1]), il.data_ptr(),
                                   ONES_COLS if kind == "v" else 0, w1.data_ptr(), b1.data_ptr(),
                                   w2.data_ptr(), b2.data_ptr(), D.ptr(mean), D.ptr(cmp_il),
-                                  int(cmp_il.shape[1]) if cmp_il is not None else 0))
-                self._job_refs += [src, il, blk, pad, mean, cmp_il]
-                max_blocks = max(max_blocks, nb)
+                                  int(cmp_il.shape[1]) if cmp_il is not None else 0,
+                                  work_d.data_ptr(), work.size, partial.data_ptr(),
+                                  arrive.data_ptr()))
+                self._job_refs += [src, il, blk, pad, mean, cmp_il, work_d, partial, arrive]
+                max_blocks = max(max_blocks, int(work.size))
         raw = b"".join(C.string_at(C.addressof(j), C.sizeof(j)) for j in jobs)
         self.kv_jobs = D.dev(np.frombuffer(raw, dtype=np.uint8).copy()) if jobs else None
         self.n_kv_jobs, self.kv_max_blocks = len(jobs), max_blocks
