@@ -95,6 +95,21 @@ int lsrm_route_image(const double* points, int64_t nq, const double* cams,
                      const int64_t* block_offsets, int b_i, int budget,
                      int32_t* out_rows, int32_t* out_count, void* stream);
 
+/* ---- router input producer  (block_routing.py:73-108,
+ *      camera_geometry.py:236-302) ------------------------------------------
+ * Surface point of every image token's patch-center ray: 128-sample Laplace
+ * opacity march through [0,1]^3 of the analytic scene (sdf rows as in
+ * lsrm_voxel_mask), peak of transmittance x alpha, cube-entry / closest-
+ * approach fallbacks with miss flags.  coords [n,3] int64 (view, u, v);
+ * cams [n_views,21] K R t; image_wh [n_views,2] pixels; rows_f = patch grid
+ * side.  points [n,3] f64 clipped to [0,1]; miss [n].  f64, no FMA; exp and
+ * the reference's BLAS rotation are not bit-identical, so points match the
+ * reference to a stated tolerance. */
+int lsrm_image_token_points(const int64_t* coords, int64_t n, const double* cams,
+                            const int32_t* image_wh, int n_views, int rows_f,
+                            const double* sdf, int n_prims, double beta,
+                            double* points, uint8_t* miss, void* stream);
+
 /* ---- gather table  (nsa_attention.py:123-154) -------------------------
  * Resolves routed rows (fallback: own block row, else row 0) into padded
  * token-id rows.  own_row may be NULL.  With fallback = 0 an empty row stays

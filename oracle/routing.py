@@ -116,3 +116,81 @@ def build_routing_plan(vol_points, img_points, part_vol, part_img, cameras,
     }
     fb = {k: [i for i, l in enumerate(v) if len(l) == 0] for k, v in tables.items()}
     return RoutingPlan(tables, dict(budgets), {k: v for k, v in fb.items() if v})
+
+
+# ---------------------------------------------------------------------------
+# router input producer: image-token surface points (the step before K8)
+
+N_MARCH = 128          # camera_geometry.py:18
+LAPLACE_BETA = 0.02    # camera_geometry.py:19
+NO_PEAK_MARGIN = 3.0   # camera_geometry.py:20
+
+
+def ray_cube_intersection(o, d):
+    """Slab method against [0,1]^3 (`camera_geometry.py:236-252`)."""
+    t0, t1 = -np.inf, np.inf
+    for ax in range(3):
+        if abs(d[ax]) < 1e-12:
+            if o[ax] < 0.0 or o[ax] > 1.0:
+                return None
+            continue
+        a = (0.0 - o[ax]) / d[ax]
+        b = (1.0 - o[ax]) / d[ax]
+        t0 = max(t0, min(a, b))
+        t1 = min(t1, max(a, b))
+    if t1 <= t0 or t1 <= 0.0:
+        return None
+    return max(t0, 0.0), t1
+
+
+def surface_peak(scene, o, d, beta=LAPLACE_BETA):
+    """Opacity peak of one ray (`camera_geometry.py:264-302`): 128 mid-segment
+    samples between cube entry and exit, Laplace density, peak of
+    transmittance x alpha.  None if the ray misses the cube or min s > 3 beta."""
+    from .tokens import eval_sdf
+    d = d / np.linalg.norm(d)
+    span = ray_cube_intersection(o, d)
+    if span is None:
+        return None, d
+    t0, t1 = span
+    step = (t1 - t0) / N_MARCH
+    ts = t0 + (np.arange(N_MARCH) + 0.5) * step
+    pts = o[None, :] + ts[:, None] * d[None, :]
+    s = eval_sdf(scene, pts)
+    if s.min() > NO_PEAK_MARGIN * beta:
+        return None, d
+    psi = np.where(s >= 0.0, 0.5 * np.exp(-s / beta), 1.0 - 0.5 * np.exp(s / beta))
+    alpha = 1.0 - np.exp(-(psi / beta) * step)
+    trans = np.concatenate([[1.0], np.cumprod(1.0 - alpha)[:-1]])
+    return pts[int(np.argmax(trans * alpha))], d
+
+
+def image_token_coords(coords, cameras, image_size, rows_f, scene, beta=LAPLACE_BETA):
+    """Surface point per image token's patch-center ray, with cube-entry /
+    closest-approach fallbacks and miss flags (`block_routing.py:73-108`).
+    coords [N,3] (view, u=col, v=row); cameras [(K, R, t)]; image_size (W, H)."""
+    n = coords.shape[0]
+    pts = np.zeros((n, 3), np.float64)
+    miss = np.zeros(n, bool)
+    W, H = image_size
+    for i in range(n):
+        view, u, v = (int(c) for c in coords[i])
+        K, R, t = cameras[view]
+        px = ((u + 0.5) * (W / rows_f), (v + 0.5) * (H / rows_f))
+        d_cam = np.array([(px[0] - K[0, 2]) / K[0, 0], (px[1] - K[1, 2]) / K[1, 1], 1.0])
+        d = R @ d_cam
+        d /= np.linalg.norm(d)
+        o = np.asarray(t, np.float64)
+        peak, dn = surface_peak(scene, o, d, beta)
+        if peak is not None:
+            p = np.asarray(peak)
+        else:
+            miss[i] = True
+            span = ray_cube_intersection(o, dn)
+            if span is not None:
+                p = o + span[0] * dn
+            else:
+                t_near = float(np.dot(np.array([0.5, 0.5, 0.5]) - o, dn))
+                p = o + max(t_near, 0.0) * dn
+        pts[i] = np.clip(p, 0.0, 1.0)
+    return pts, miss

@@ -22,7 +22,7 @@ from .nsa_attention import (GatherTable, NsaWeights, Selection, build_gather_tab
                             win_attention, write_selection)
 from .block_routing import (RoutingBudgets, RoutingPlan, TokenCoords3D, build_routing_plan,
                             route_to_image_blocks, route_to_volume_blocks,
-                            volume_token_coords, write_plan)
+                            image_token_coords, volume_token_coords, write_plan)
 
 from .seq_parallel import (TOKEN_COORD_BYTES, WorkerTopology, all_gather_kv, all_to_all,
                            imbalance_report, makespan_ratio, message_log_to_csv,

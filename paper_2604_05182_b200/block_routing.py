@@ -63,6 +63,37 @@ def volume_token_coords(tokens) -> TokenCoords3D:
     return TokenCoords3D((c.astype(np.float64) + 0.5) / side, np.zeros(tokens.count, bool))
 
 
+LAPLACE_BETA = 0.02   # camera_geometry.py:19
+
+
+def image_token_coords(tokens, cameras, field, beta: float = LAPLACE_BETA) -> TokenCoords3D:
+    """Surface point of each image token's patch-center ray
+    (`block_routing.py:73-108`): 128-sample Laplace opacity march
+    (`camera_geometry.py:264-302`) on the GPU, f64; rays with no opacity peak
+    fall back to their cube-entry point, rays missing the cube to the clamped
+    closest approach to the cube center, both flagged in `miss`."""
+    from .tokenizer import sdf_primitives
+    n_views, rows_f, _ = tokens.grid_res
+    require(len(cameras) == n_views, "camera count != view count")
+    wh = []
+    for cam in cameras:
+        size = getattr(cam, "image_size", None)
+        if size is None and isinstance(cam, (tuple, list)) and len(cam) > 3:
+            size = cam[3]
+        wh.append(size if size is not None else (8 * rows_f, 8 * rows_f))
+    n = tokens.count
+    coords = D.dev(tokens.coords, torch.int64)
+    cams = D.dev(pack_cameras(cameras))
+    whd = D.dev(np.asarray(wh, np.int32).reshape(-1, 2))
+    prims = D.dev(sdf_primitives(field))
+    pts = D.empty((max(n, 1), 3), torch.float64)
+    miss = D.empty((max(n, 1),), torch.uint8)
+    call("lsrm_image_token_points", coords.data_ptr(), n, cams.data_ptr(), whd.data_ptr(),
+         n_views, rows_f, prims.data_ptr(), int(prims.shape[0]), float(beta), pts.data_ptr(),
+         miss.data_ptr(), D.stream())
+    return TokenCoords3D(D.host(pts)[:n], D.host(miss)[:n].astype(bool))
+
+
 def pack_cameras(cameras) -> np.ndarray:
     """[V, 21] f64 rows K(9) R(9) t(3) from reference Camera objects or
     (K, R, t) tuples."""

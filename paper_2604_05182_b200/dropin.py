@@ -22,7 +22,8 @@ HOT_PATH = {
                       "combine_nsa_branches"),
     "block_partition": ("partition", "compress_block_kv", "res_block"),
     "block_routing": ("build_routing_plan", "route_to_volume_blocks", "route_to_image_blocks",
-                      "_route_points_to_volume", "_route_points_to_image"),
+                      "_route_points_to_volume", "_route_points_to_image",
+                      "image_token_coords"),
     "tokenizer": ("informative_voxel_mask", "foreground_patch_mask", "upsample_select_tokens"),
     "seq_parallel": ("shard_blocks", "all_to_all", "all_gather_kv", "naive_contiguous_shards"),
     "recon_pipeline": ("sparse_block_forward", "build_sparse_context", "ffn_forward"),
