@@ -110,6 +110,18 @@ int lsrm_image_token_points(const int64_t* coords, int64_t n, const double* cams
                             const double* sdf, int n_prims, double beta,
                             double* points, uint8_t* miss, void* stream);
 
+/* Plücker rays (camera_geometry.py:91-107): [n_views, gh, gw, 6] float32
+ * rows (unit direction d, moment t x d) through the centers of a gw x gh grid
+ * over each view's image. */
+int lsrm_pluecker_rays(const double* cams, const int32_t* image_wh, int n_views, int gw,
+                       int gh, float* out, void* stream);
+/* Silhouettes (camera_geometry.py:308-350): alpha [n_views, max_h, max_w]
+ * float32, 1 where the pixel ray (float32 Plücker direction, as the
+ * reference) hits the analytic scene (sdf rows as in lsrm_voxel_mask). */
+int lsrm_silhouette_alpha(const double* cams, const int32_t* image_wh, int n_views,
+                          int max_w, int max_h, const double* sdf, int n_prims,
+                          float* alpha, void* stream);
+
 /* ---- gather table  (nsa_attention.py:123-154) -------------------------
  * Resolves routed rows (fallback: own block row, else row 0) into padded
  * token-id rows.  own_row may be NULL.  With fallback = 0 an empty row stays

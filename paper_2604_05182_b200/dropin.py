@@ -27,6 +27,7 @@ HOT_PATH = {
     "tokenizer": ("informative_voxel_mask", "foreground_patch_mask", "upsample_select_tokens"),
     "seq_parallel": ("shard_blocks", "all_to_all", "all_gather_kv", "naive_contiguous_shards"),
     "recon_pipeline": ("sparse_block_forward", "build_sparse_context", "ffn_forward"),
+    "camera_geometry": ("pluecker_rays", "silhouette_alpha"),
 }
 
 _saved = []

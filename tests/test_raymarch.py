@@ -59,3 +59,35 @@ def test_gpu_image_points_vs_reference(cuda, name):
     assert np.array_equal(got.miss, _miss(name))
     assert exact >= 0.99
     assert err.max() <= np.sqrt(3.0) / 128
+
+
+@pytest.mark.gpu
+def test_gpu_silhouette_vs_reference_c1(cuda):
+    """Silhouette of view 0 (the foreground-mask input) against the reference's
+    own alpha map (fixture), bit for bit."""
+    import os
+    from paper_2604_05182_b200.camera_geometry import silhouettes
+    wl = load_workload("c1")
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "workload_c1.npz"))
+    want = np.unpackbits(z["alpha0"])[:768 * 768].reshape(768, 768).astype(bool)
+    cams = [(K, R, t, (768, 768)) for K, R, t in wl.cameras]
+    got = silhouettes(SCENE, cams)
+    print(f"silhouette view 0: {int((got[0] > 0.5).sum())} hit pixels, "
+          f"{int(((got[0] > 0.5) != want).sum())} differ")
+    assert np.array_equal(got[0] > 0.5, want)
+
+
+@pytest.mark.gpu
+def test_gpu_pluecker_rays(cuda):
+    """Patch-center rays against a NumPy restatement of camera_geometry.py:91-107."""
+    from paper_2604_05182_b200.camera_geometry import pluecker_rays
+    wl = load_workload("c1")
+    K, R, t = wl.cameras[1]
+    got = pluecker_rays((K, R, t, (768, 768)), (96, 96))
+    u = (np.arange(96) + 0.5) * 8.0
+    uu, vv = np.meshgrid(u, u)
+    d = np.stack([(uu - K[0, 2]) / K[0, 0], (vv - K[1, 2]) / K[1, 1], np.ones_like(uu)], -1)
+    d = d @ R.T
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    want = np.concatenate([d, np.cross(np.broadcast_to(t, d.shape), d)], -1).astype(np.float32)
+    assert np.max(np.abs(got - want)) <= 1e-6
