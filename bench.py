@@ -298,7 +298,7 @@ def run_gpu(args):
                    "n_vol": inst.n_vol, "n_img": inst.n_img, "global_batch": n_tok,
                    "parallelism": "single GPU", "l2": "flushed (256 MiB write) between steps",
                    "cuda_graph": use_graph},
-        "roofline": {"bound": "tensor", "kernel": "nsa_fused_kernel (4 launches/step)",
+        "roofline": {"bound": "tensor", "kernel": "nsa_fused_kernel (one launch per step: four uses, LPT queue)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{src} bf16_tflops (burst)",
@@ -510,7 +510,7 @@ def run_sp(args):
                                       f"All-gather-KV per use ({backend} grouped send/recv)",
                        "makespan_ratio": float(loads.max() / loads.mean()) if loads.sum() else 1.0,
                        "l2": "flushed (256 MiB write) between steps", "cuda_graph": use_graph},
-            "roofline": {"bound": "tensor", "kernel": "nsa_fused_kernel (4 launches/step/rank)",
+            "roofline": {"bound": "tensor", "kernel": "nsa_fused_kernel (one launch per step per rank: four uses, LPT queue)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "peak_source": f"{src} bf16_tflops x {ws} GPUs",

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round profile on one GPU: ncu launch list of a short bench run, `--set full`
-# of the four fused-attention launches and the K/V-prep launch of one layer,
+# of one layer's K/V-prep launch and its (merged, four-use) attention launch,
 # and the attention DRAM traffic per launch that bench.py reports.
 #   bash tools/profile_round.sh <tag>      (outputs under gpurun_out/; on the
 #   workstation, `bash tools/profile_round.sh <tag> --summarise` turns them into
@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k "regex:nsa_fused|kv_prep" \
-    --launch-count 5 -o gpurun_out/layer_full_$TAG -f \
+    --launch-count 2 -o gpurun_out/layer_full_$TAG -f \
     python tools/attn_trace.py --use v2v > /dev/null 2>&1
 exit 0
 fi
