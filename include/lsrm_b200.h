@@ -370,6 +370,36 @@ int lsrm_bias_act(int exact, const void* h, int h_bf16, int64_t ld, const float*
                   int64_t n, int cols, int act, const float* residual, void* out,
                   int out_bf16, int64_t ld_out, void* stream);
 
+/* ---- backward of one gated NSA use (training) -----
+ * fp32, recompute-based; the reference has no backward (oracle:
+ * oracle/torch_nsa.py, f64 autograd).  dK/dV accumulate with atomics (not
+ * bit-deterministic); callers zero dq/dk/dv first.
+ * attention_bwd: same key-set arguments as lsrm_attention_f32 (mode 0 cmp,
+ * 1 sel, 2 win); q/dO/O [nq, hq, dh] token order; dq += ...; dk/dv += ... */
+int lsrm_attention_bwd_f32(int mode, const float* q, const float* dO, const float* O,
+                           int64_t nq, int hq, int hkv, int dh, const float* k,
+                           const float* v, int64_t nk, const int64_t* block_offsets,
+                           const int32_t* rows, const int32_t* count, int kmax_rows,
+                           const int32_t* own_row, float* dq, float* dk, float* dv,
+                           void* stream);
+/* merged = sum_b sigmoid(gl[:, b*d:(b+1)*d] + gb[b*d:]) * o_b:
+ * do_b = dM g_b,  dz[:, b*d + c] = dM o_b g_b (1 - g_b)   (dz [n, n_gates*d]). */
+int lsrm_gate_merge_bwd_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,
+                            int n_gates, const float* o0, const float* o1, const float* o2,
+                            const float* dmerged, int64_t n, int d, float* do0, float* do1,
+                            float* do2, float* dz, void* stream);
+/* Compression ResBlock under the block mean (block_partition.py:141-158):
+ * dr_t = dcmp[row(t)] / occupancy[row(t)];  dx_t += dr_t + (dr_t W2^T * gelu'(z1_t)) W1^T;
+ * writes dr, dz1, h = gelu(z1) rows [n, width] for the weight-gradient GEMMs. */
+int lsrm_res_block_bwd_f32(const float* x, int64_t n, int width, const float* w1,
+                           const float* b1, const float* w2, const float* dcmp,
+                           const int32_t* row_of_token, const int64_t* occupancy, float* dx,
+                           float* dr_out, float* dz1_out, float* h_out, void* stream);
+/* Row-major fp32 C[m,n] = alpha op(A) op(B) + beta C (op = transpose if trans_*). */
+int lsrm_gemm_f32_ex(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, float alpha,
+                     const float* a, int64_t lda, const float* b, int64_t ldb, float beta,
+                     float* c, int64_t ldc, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,3 +60,19 @@ def layer_norm(x: torch.Tensor, gamma, beta, eps=1e-5, out_dtype=None) -> torch.
          gamma.data_ptr(), beta.data_ptr(), float(eps), int(odt == torch.bfloat16),
          out.data_ptr(), D.stream())
     return out
+
+
+def gemm_ex(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, out=None,
+            beta=0.0, alpha=1.0) -> torch.Tensor:
+    """fp32 out = alpha op(a) @ op(b) + beta out (op = transpose when asked)."""
+    m, k = (a.shape[1], a.shape[0]) if trans_a else a.shape
+    k2, n = (b.shape[1], b.shape[0]) if trans_b else b.shape
+    assert k == k2 and a.stride(1) == 1 and b.stride(1) == 1
+    assert a.dtype == b.dtype == torch.float32
+    if out is None:
+        out = D.empty((m, n), torch.float32)
+        beta = 0.0
+    call("lsrm_gemm_f32_ex", int(trans_a), int(trans_b), m, n, k, float(alpha), a.data_ptr(),
+         a.stride(0), b.data_ptr(), b.stride(0), float(beta), out.data_ptr(), out.stride(0),
+         D.stream())
+    return out

@@ -1,0 +1,257 @@
+// Backward of one gated NSA use, fp32 on CUDA cores (SURVEY.md §8f rank 2:
+// the reference has no backward; the oracle is a float64 torch autograd
+// restatement, oracle/torch_nsa.py).
+//
+//   * attention_bwd: per (query, q-head) thread, the branch's key set walked
+//     like the forward (attn_f32.cu): pass 1 recomputes max / sum, pass 2
+//     forms P, dS = P (dO.V - rowsum(dO O)) and accumulates dQ locally, dK and
+//     dV with atomics (keys are shared by many queries).
+//   * gate_merge_bwd: merged = sum_b sigmoid(z_b) * O_b  ->  dO_b, dz_b.
+//   * res_block_bwd: the compression's per-token ResBlock under the block
+//     mean, r = x + gelu(x W1 + b1) W2 + b2, k_cmp[b] = mean_{t in b} r_t;
+//     emits dx (accumulated), dz1 and h for the weight-gradient GEMMs.
+// Gradients with atomics are not bit-deterministic run to run (training path).
+#include "common.cuh"
+
+namespace lsrm {
+
+template <int DH>
+__device__ __forceinline__ void range_stats(const float* __restrict__ k, int hkv, int kvh,
+                                            int64_t lo, int64_t hi, const float (&q)[DH],
+                                            float scale, float& m, float& l) {
+  for (int64_t j = lo; j < hi; ++j) {
+    const float* kr = k + (j * hkv + kvh) * DH;
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) s = fmaf(q[c], kr[c], s);
+    s *= scale;
+    if (s > m) {
+      l *= expf(m - s);
+      m = s;
+    }
+    l += expf(s - m);
+  }
+}
+
+template <int DH>
+__device__ __forceinline__ void range_grad(const float* __restrict__ k, const float* __restrict__ v,
+                                           float* __restrict__ dk, float* __restrict__ dv,
+                                           int hkv, int kvh, int64_t lo, int64_t hi,
+                                           const float (&q)[DH], const float (&dout)[DH],
+                                           float dsum, float scale, float m, float inv_l,
+                                           float (&dq)[DH]) {
+  for (int64_t j = lo; j < hi; ++j) {
+    const int64_t base = (j * hkv + kvh) * DH;
+    const float* kr = k + base;
+    const float* vr = v + base;
+    float s = 0.f, dp = 0.f;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) {
+      s = fmaf(q[c], kr[c], s);
+      dp = fmaf(dout[c], vr[c], dp);
+    }
+    const float p = expf(s * scale - m) * inv_l;
+    const float ds = p * (dp - dsum) * scale;
+#pragma unroll
+    for (int c = 0; c < DH; ++c) {
+      dq[c] = fmaf(ds, kr[c], dq[c]);
+      atomicAdd(dk + base + c, ds * q[c]);
+      atomicAdd(dv + base + c, p * dout[c]);
+    }
+  }
+}
+
+template <int DH>
+__global__ void attention_bwd_f32_kernel(int mode, const float* __restrict__ q,
+                                         const float* __restrict__ dO,
+                                         const float* __restrict__ O, int64_t nq, int hq,
+                                         int hkv, const float* __restrict__ k,
+                                         const float* __restrict__ v, int64_t nk,
+                                         const int64_t* __restrict__ offs,
+                                         const int32_t* __restrict__ rows,
+                                         const int32_t* __restrict__ count, int kmax,
+                                         const int32_t* __restrict__ own_row,
+                                         float* __restrict__ dq, float* __restrict__ dk,
+                                         float* __restrict__ dv) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nq * hq) return;
+  const int64_t i = t / hq;
+  const int h = (int)(t % hq);
+  const int kvh = h / (hq / hkv);
+  float qr[DH], dor[DH], dqa[DH];
+  float dsum = 0.f;
+#pragma unroll
+  for (int c = 0; c < DH; ++c) {
+    qr[c] = q[t * DH + c];
+    dor[c] = dO[t * DH + c];
+    dsum = fmaf(dor[c], O[t * DH + c], dsum);
+    dqa[c] = 0.f;
+  }
+  const float scale = 1.0f / sqrtf((float)DH);
+  float m = -__builtin_huge_valf(), l = 0.f;
+  auto walk = [&](auto&& f) {
+    if (mode == 0) {
+      f((int64_t)0, nk);
+    } else if (mode == 1) {
+      const int cnt = count[i];
+      for (int s = 0; s < cnt; ++s) {
+        const int r = rows[i * kmax + s];
+        f(offs[r], offs[r + 1]);
+      }
+    } else {
+      const int r = own_row[i];
+      f(offs[r], offs[r + 1]);
+    }
+  };
+  walk([&](int64_t lo, int64_t hi) { range_stats<DH>(k, hkv, kvh, lo, hi, qr, scale, m, l); });
+  const float inv_l = 1.f / l;
+  walk([&](int64_t lo, int64_t hi) {
+    range_grad<DH>(k, v, dk, dv, hkv, kvh, lo, hi, qr, dor, dsum, scale, m, inv_l, dqa);
+  });
+#pragma unroll
+  for (int c = 0; c < DH; ++c) dq[t * DH + c] += dqa[c];
+}
+
+__device__ __forceinline__ double sigmoid_d(double x) {
+  return x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
+}
+
+// merged = sum_b g_b * O_b, g_b = sigmoid(z_b + bias_b):  dO_b = dM g_b,
+// dz_b = dM O_b g_b (1 - g_b)
+__global__ void gate_merge_bwd_kernel(const float* __restrict__ gl, int64_t ld,
+                                      const float* __restrict__ gb, int ng,
+                                      const float* __restrict__ o0, const float* __restrict__ o1,
+                                      const float* __restrict__ o2,
+                                      const float* __restrict__ dm, int64_t n, int d,
+                                      float* __restrict__ do0, float* __restrict__ do1,
+                                      float* __restrict__ do2, float* __restrict__ dz) {
+  const int64_t total = n * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / d;
+    const int c = (int)(e % d);
+    const float* ob[3] = {o0, o1, o2};
+    float* dob[3] = {do0, do1, do2};
+    const float g_m = dm[e];
+    for (int b = 0; b < ng; ++b) {
+      const float z = gl[i * ld + b * d + c] + (gb ? gb[b * d + c] : 0.f);
+      const float g = (float)sigmoid_d((double)z);
+      dob[b][e] = g_m * g;
+      dz[i * (int64_t)ng * d + b * d + c] = g_m * ob[b][e] * g * (1.f - g);
+    }
+  }
+}
+
+// One CTA per token (w threads): r = x + gelu(z1) W2 + b2, z1 = x W1 + b1.
+// dr = dcmp[row(t)] / occ[row(t)];  dz1 = (dr W2^T) * gelu'(z1);
+// dx += dr + dz1 W1^T;  dR, dZ1, H (= gelu(z1)) rows for the weight GEMMs.
+__global__ void res_block_bwd_kernel(const float* __restrict__ x, int64_t n, int w,
+                                     const float* __restrict__ w1, const float* __restrict__ b1,
+                                     const float* __restrict__ w2,
+                                     const float* __restrict__ dcmp,
+                                     const int32_t* __restrict__ row_of_token,
+                                     const int64_t* __restrict__ occupancy,
+                                     float* __restrict__ dx, float* __restrict__ dr_out,
+                                     float* __restrict__ dz1_out, float* __restrict__ h_out) {
+  extern __shared__ float sm[];
+  float* xs = sm;          // [w]
+  float* drs = xs + w;     // [w]
+  float* dz1s = drs + w;   // [w]
+  const int64_t t = blockIdx.x;
+  const int o = threadIdx.x;
+  if (t >= n) return;
+  const int r = row_of_token[t];
+  const float inv = 1.f / (float)occupancy[r];
+  if (o < w) {
+    xs[o] = x[t * w + o];
+    drs[o] = dcmp[(int64_t)r * w + o] * inv;
+  }
+  __syncthreads();
+  if (o < w) {
+    float z = b1[o];
+    for (int i = 0; i < w; ++i) z = fmaf(xs[i], w1[i * w + o], z);
+    const float cdf = 0.5f * (1.f + erff(z * 0.70710678118654752f));
+    const float pdf = 0.39894228040143268f * expf(-0.5f * z * z);
+    h_out[t * w + o] = z * cdf;
+    // (dr W2^T)[o] = sum_j dr[j] W2[o][j]
+    float dh = 0.f;
+    for (int j = 0; j < w; ++j) dh = fmaf(drs[j], w2[o * w + j], dh);
+    const float dz = dh * (cdf + z * pdf);
+    dz1s[o] = dz;
+    dz1_out[t * w + o] = dz;
+    dr_out[t * w + o] = drs[o];
+  }
+  __syncthreads();
+  if (o < w) {
+    float acc = drs[o];
+    for (int j = 0; j < w; ++j) acc = fmaf(dz1s[j], w1[o * w + j], acc);
+    dx[t * w + o] += acc;
+  }
+}
+
+}  // namespace lsrm
+
+using namespace lsrm;
+
+extern "C" {
+
+int lsrm_attention_bwd_f32(int mode, const float* q, const float* dO, const float* O, int64_t nq,
+                           int hq, int hkv, int dh, const float* k, const float* v, int64_t nk,
+                           const int64_t* block_offsets, const int32_t* rows,
+                           const int32_t* count, int kmax_rows, const int32_t* own_row,
+                           float* dq, float* dk, float* dv, void* stream) {
+  LSRM_REQUIRE(mode >= 0 && mode <= 2, "attention_bwd: mode must be 0 (cmp), 1 (sel), 2 (win)");
+  LSRM_REQUIRE(hq % hkv == 0, "n_q_heads=%d not divisible by n_kv_heads=%d", hq, hkv);
+  if (nq == 0) return LSRM_OK;
+  const int64_t threads = nq * hq;
+  const unsigned grid = (unsigned)ceil_div(threads, 128);
+  cudaStream_t st = as_stream(stream);
+#define LSRM_BWD_CASE(D)                                                                  \
+  case D:                                                                                 \
+    attention_bwd_f32_kernel<D><<<grid, 128, 0, st>>>(mode, q, dO, O, nq, hq, hkv, k, v,  \
+                                                      nk, block_offsets, rows, count,     \
+                                                      kmax_rows, own_row, dq, dk, dv);    \
+    break;
+  switch (dh) {
+    LSRM_BWD_CASE(4)
+    LSRM_BWD_CASE(8)
+    LSRM_BWD_CASE(16)
+    LSRM_BWD_CASE(32)
+    LSRM_BWD_CASE(64)
+    default:
+      return set_error(LSRM_E_CONFIG, "attention_bwd: head_dim %d not in {4,8,16,32,64}", dh);
+  }
+#undef LSRM_BWD_CASE
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_gate_merge_bwd_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,
+                            int n_gates, const float* o0, const float* o1, const float* o2,
+                            const float* dmerged, int64_t n, int d, float* do0, float* do1,
+                            float* do2, float* dz, void* stream) {
+  LSRM_REQUIRE(n_gates >= 1 && n_gates <= 3, "n_gates must be 1..3");
+  if (n == 0) return LSRM_OK;
+  const int64_t total = n * d;
+  const unsigned grid = (unsigned)(ceil_div(total, 256) < 148 * 16 ? ceil_div(total, 256) : 148 * 16);
+  gate_merge_bwd_kernel<<<grid, 256, 0, as_stream(stream)>>>(gate_logits, ld_gl, gate_bias,
+                                                             n_gates, o0, o1, o2, dmerged, n, d,
+                                                             do0, do1, do2, dz);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_res_block_bwd_f32(const float* x, int64_t n, int width, const float* w1,
+                           const float* b1, const float* w2, const float* dcmp,
+                           const int32_t* row_of_token, const int64_t* occupancy, float* dx,
+                           float* dr_out, float* dz1_out, float* h_out, void* stream) {
+  LSRM_REQUIRE(width >= 1 && width <= 1024, "res_block_bwd: width %d out of range", width);
+  if (n == 0) return LSRM_OK;
+  const int threads = (width + 31) / 32 * 32;
+  res_block_bwd_kernel<<<(unsigned)n, threads, 3 * width * sizeof(float), as_stream(stream)>>>(
+      x, n, width, w1, b1, w2, dcmp, row_of_token, occupancy, dx, dr_out, dz1_out, h_out);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+}  // extern "C"

@@ -129,3 +129,24 @@ extern "C" int lsrm_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void*
   if (s != CUBLAS_STATUS_SUCCESS) return set_error(LSRM_E_CUDA, "cublas gemm failed: %d", (int)s);
   return LSRM_OK;
 }
+
+// Row-major fp32 C[m,n] = alpha op(A) op(B) + beta C, op = transpose when
+// trans_* != 0 (op(A) is [m,k], op(B) is [k,n]; lda/ldb are the row strides of
+// the stored A/B).  The backward's weight / input gradients.
+extern "C" int lsrm_gemm_f32_ex(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                                float alpha, const float* a, int64_t lda, const float* b,
+                                int64_t ldb, float beta, float* c, int64_t ldc, void* stream) {
+  if (m == 0 || n == 0) return LSRM_OK;
+  cublasHandle_t h;
+  int rc = get_handle(&h);
+  if (rc) return rc;
+  cublasSetStream(h, as_stream(stream));
+  // column-major: C^T (n x m) = op(B)^T op(A)^T; a row-major stored matrix is
+  // its own transpose in column-major, so the flags carry over unchanged.
+  const cublasOperation_t ob = trans_b ? CUBLAS_OP_T : CUBLAS_OP_N;
+  const cublasOperation_t oa = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;
+  cublasStatus_t s = cublasSgemm(h, ob, oa, (int)n, (int)m, (int)k, &alpha, b, (int)ldb, a,
+                                 (int)lda, &beta, c, (int)ldc);
+  if (s != CUBLAS_STATUS_SUCCESS) return set_error(LSRM_E_CUDA, "cublas gemm_ex failed: %d", (int)s);
+  return LSRM_OK;
+}

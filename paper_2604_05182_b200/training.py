@@ -1,0 +1,209 @@
+"""Training step of one gated NSA use.
+
+The reference is inference-only: its NSA use (`nsa_attention.py:287-327`) has
+no backward.  This module adds one on the GPU path: an fp32
+forward that keeps its intermediates (same kernels as `nsa_cross_attention`)
+and a backward built from
+
+  * `lsrm_attention_bwd_f32`  - the three branches (recompute, dK/dV atomics),
+  * `lsrm_gate_merge_bwd_f32` - the sigmoid-gated merge,
+  * `lsrm_res_block_bwd_f32`  - the compression ResBlock under the block mean,
+  * `lsrm_gemm_f32_ex`        - every projection / weight gradient (cuBLAS),
+
+wrapped in a `torch.autograd.Function` so a `torch.optim` optimizer can step
+the weights.  Gradients are checked against the float64 autograd restatement
+`oracle/torch_nsa.py` (tests/test_training.py).
+
+Inputs and selections are fixed per call: routing (which blocks each query
+attends to) is not differentiated, exactly as in NSA training.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev as D
+from . import _ops
+from ._native import call
+from .block_partition import BlockPartition, compress_rows
+from .errors import require
+from .nsa_attention import NsaWeights, _attn, resolve_rows, selection_rows
+from .tensor_core import AttentionParams
+
+PARAM_NAMES = ("w_q", "w_k", "w_v", "w_o", "gate_w", "gate_b",
+               "ck_w1", "ck_b1", "ck_w2", "ck_b2", "cv_w1", "cv_b1", "cv_w2", "cv_b2")
+
+
+@dataclass
+class _Spec:
+    params: AttentionParams
+    n_gates: int
+    part_q: BlockPartition
+    part_kv: BlockPartition
+    rows: torch.Tensor
+    count: torch.Tensor
+
+
+def _forward(spec: _Spec, x, kv, P):
+    p = spec.params
+    n, d = x.shape
+    m = int(kv.shape[0])
+    hq, hkv, dh = p.n_q_heads, p.n_kv_heads, p.head_dim
+    width = hkv * dh
+    part = spec.part_kv
+    q = _ops.gemm(x, P["w_q"])
+    k = _ops.gemm(kv, P["w_k"])
+    v = _ops.gemm(kv, P["w_v"])
+    ck = [P[f"ck_{s}"] for s in ("w1", "b1", "w2", "b2")]
+    cv = [P[f"cv_{s}"] for s in ("w1", "b1", "w2", "b2")]
+    kc = compress_rows(k, width, m, width, ck, part)
+    vc = compress_rows(v, width, m, width, cv, part)
+    tok, offs = part.dev("block_token_ids"), part.dev("block_offsets")
+    k_bm, v_bm = _ops.gather_rows(k, tok), _ops.gather_rows(v, tok)
+    q3 = q.view(n, hq, dh)
+    B = part.n_occupied
+    outs = [_attn(0, q3, kc.view(B, hkv, dh), vc.view(B, hkv, dh), p),
+            _attn(1, q3, k_bm.view(m, hkv, dh), v_bm.view(m, hkv, dh), p, offs=offs,
+                  rows=spec.rows, count=spec.count)]
+    if spec.n_gates == 3:
+        outs.append(_attn(2, q3, k_bm.view(m, hkv, dh), v_bm.view(m, hkv, dh), p, offs=offs,
+                          own_row=spec.part_q.dev("row_of_token")))
+    logits = _ops.gemm(x, P["gate_w"])
+    merged = D.empty((n, d), torch.float32)
+    o = [t.view(n, d) for t in outs] + [None] * (3 - len(outs))
+    call("lsrm_gated_merge_f32", logits.data_ptr(), logits.stride(0), P["gate_b"].data_ptr(),
+         spec.n_gates, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]), n, d, merged.data_ptr(),
+         D.stream())
+    out = _ops.gemm(merged, P["w_o"])
+    saved = dict(x=x, kv=kv, q=q, k=k, v=v, kc=kc, vc=vc, k_bm=k_bm, v_bm=v_bm, outs=o,
+                 logits=logits, merged=merged, ck=ck, cv=cv)
+    return out, saved
+
+
+def _colsum(t):
+    ones = torch.ones((1, t.shape[0]), dtype=torch.float32, device=t.device)
+    return _ops.gemm_ex(ones, t).view(-1)
+
+
+def _backward(spec: _Spec, P, s, dout):
+    """Gradients of every input and parameter (dict keyed like PARAM_NAMES
+    plus "x", "kv")."""
+    p = spec.params
+    n, d = s["x"].shape
+    m = int(s["kv"].shape[0])
+    hq, hkv, dh = p.n_q_heads, p.n_kv_heads, p.head_dim
+    width = hkv * dh
+    ng = spec.n_gates
+    part = spec.part_kv
+    B = part.n_occupied
+    st = D.stream()
+    g = {}
+    # out = merged W_o
+    dmerged = _ops.gemm_ex(dout, P["w_o"], trans_b=True)
+    g["w_o"] = _ops.gemm_ex(s["merged"], dout, trans_a=True)
+    # gated merge
+    do = [D.empty((n, d), torch.float32) for _ in range(ng)] + [None] * (3 - ng)
+    dz = D.empty((n, ng * d), torch.float32)
+    o = s["outs"]
+    call("lsrm_gate_merge_bwd_f32", s["logits"].data_ptr(), s["logits"].stride(0),
+         P["gate_b"].data_ptr(), ng, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]),
+         dmerged.data_ptr(), n, d, D.ptr(do[0]), D.ptr(do[1]), D.ptr(do[2]), dz.data_ptr(), st)
+    g["gate_w"] = _ops.gemm_ex(s["x"], dz, trans_a=True)
+    g["gate_b"] = _colsum(dz)
+    dx = _ops.gemm_ex(dz, P["gate_w"], trans_b=True)
+    # branches
+    dq = D.zeros((n, d), torch.float32)
+    dkc, dvc = D.zeros((B, width), torch.float32), D.zeros((B, width), torch.float32)
+    dk_bm, dv_bm = D.zeros((m, width), torch.float32), D.zeros((m, width), torch.float32)
+    offs = part.dev("block_offsets")
+    kmax = int(spec.rows.shape[1])
+
+    def bwd(mode, b, k, v, nk, dk, dv, rows=None, count=None, own=None):
+        call("lsrm_attention_bwd_f32", mode, s["q"].data_ptr(), do[b].data_ptr(),
+             o[b].data_ptr(), n, hq, hkv, dh, k.data_ptr(), v.data_ptr(), nk,
+             offs.data_ptr() if mode else None, D.ptr(rows), D.ptr(count), kmax, D.ptr(own),
+             dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), st)
+    bwd(0, 0, s["kc"], s["vc"], B, dkc, dvc)
+    bwd(1, 1, s["k_bm"], s["v_bm"], m, dk_bm, dv_bm, rows=spec.rows, count=spec.count)
+    if ng == 3:
+        bwd(2, 2, s["k_bm"], s["v_bm"], m, dk_bm, dv_bm, own=spec.part_q.dev("row_of_token"))
+    tok = part.dev("block_token_ids")
+    dk = _ops.scatter_rows(dk_bm, tok, D.empty((m, width), torch.float32))
+    dv = _ops.scatter_rows(dv_bm, tok, D.empty((m, width), torch.float32))
+    # compression ResBlocks under the block mean (accumulate into dk / dv)
+    row_of = part.dev("row_of_token")
+    occ = part.dev("occupancy")
+    require(occ.dtype == torch.int64, "occupancy must be int64")
+    for tag, t, dc, dt, cw in (("ck", s["k"], dkc, dk, s["ck"]), ("cv", s["v"], dvc, dv, s["cv"])):
+        dr, dz1, h = (D.empty((m, width), torch.float32) for _ in range(3))
+        call("lsrm_res_block_bwd_f32", t.data_ptr(), m, width, cw[0].data_ptr(),
+             cw[1].data_ptr(), cw[2].data_ptr(), dc.data_ptr(), row_of.data_ptr(),
+             occ.data_ptr(), dt.data_ptr(), dr.data_ptr(), dz1.data_ptr(), h.data_ptr(), st)
+        g[f"{tag}_w1"] = _ops.gemm_ex(t, dz1, trans_a=True)
+        g[f"{tag}_b1"] = _colsum(dz1)
+        g[f"{tag}_w2"] = _ops.gemm_ex(h, dr, trans_a=True)
+        g[f"{tag}_b2"] = _colsum(dr)
+    # projections
+    g["w_k"] = _ops.gemm_ex(s["kv"], dk, trans_a=True)
+    g["w_v"] = _ops.gemm_ex(s["kv"], dv, trans_a=True)
+    dkv = _ops.gemm_ex(dk, P["w_k"], trans_b=True)
+    _ops.gemm_ex(dv, P["w_v"], trans_b=True, out=dkv, beta=1.0)
+    g["w_q"] = _ops.gemm_ex(s["x"], dq, trans_a=True)
+    _ops.gemm_ex(dq, P["w_q"], trans_b=True, out=dx, beta=1.0)
+    g["x"], g["kv"] = dx, dkv
+    return g
+
+
+class _NsaUseFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, spec, x, kv, *params):
+        P = dict(zip(PARAM_NAMES, (t.detach().contiguous() for t in params)))
+        out, saved = _forward(spec, x.detach().contiguous(), kv.detach().contiguous(), P)
+        ctx.spec, ctx.P, ctx.saved = spec, P, saved
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        g = _backward(ctx.spec, ctx.P, ctx.saved, dout.contiguous())
+        ctx.saved = None
+        return (None, g["x"], g["kv"], *(g[name] for name in PARAM_NAMES))
+
+
+class NsaUseModule(torch.nn.Module):
+    """One trainable gated NSA use (fp32).  Parameters mirror `NsaWeights`
+    (`nsa_attention.py:239-263`); compression ResBlocks are ck_* / cv_*."""
+
+    def __init__(self, params: AttentionParams, n_gates: int, weights: NsaWeights = None,
+                 seed: int = 0):
+        super().__init__()
+        require(n_gates in (2, 3), "n_gates must be 2 (cross) or 3 (self)")
+        self.params, self.n_gates = params, n_gates
+        if weights is None:
+            from .nsa_attention import init_nsa_weights
+            weights = init_nsa_weights(seed, params, n_gates, "train")
+        for name, arr in _weight_arrays(weights).items():
+            self.register_parameter(name, torch.nn.Parameter(D.dev(arr, torch.float32).clone()))
+
+    def forward(self, x, kv, part_q: BlockPartition, part_kv: BlockPartition, sel=None,
+                table=None):
+        n = int(x.shape[0])
+        require(x.shape[1] == self.params.model_dim, "query width != model dim")
+        require(int(kv.shape[0]) == part_kv.n_tokens, "partition does not index these tokens")
+        if getattr(table, "rows", None) is not None:
+            rows, count = table.rows, table.count
+        else:
+            require(sel is not None and sel.n_queries == n, "a Selection covering every query "
+                    "is required")
+            rows, count = selection_rows(sel, part_kv)
+            own = part_kv.block_of_token if self.n_gates == 3 else None
+            rows, count, _, _, _ = resolve_rows(rows, count, part_kv, own, True)
+        spec = _Spec(self.params, self.n_gates, part_q, part_kv, rows, count)
+        return _NsaUseFn.apply(spec, x, kv, *(getattr(self, nm) for nm in PARAM_NAMES))
+
+
+def _weight_arrays(w: NsaWeights) -> dict:
+    ck, cv = w.compress.for_k, w.compress.for_v
+    return {"w_q": w.w_q, "w_k": w.w_k, "w_v": w.w_v, "w_o": w.w_o, "gate_w": w.gate_w,
+            "gate_b": w.gate_b, "ck_w1": ck.w1, "ck_b1": ck.b1, "ck_w2": ck.w2, "ck_b2": ck.b2,
+            "cv_w1": cv.w1, "cv_b1": cv.b1, "cv_w2": cv.w2, "cv_b2": cv.b2}

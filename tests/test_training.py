@@ -1,0 +1,192 @@
+"""Backward of one gated NSA use (the reference has no
+backward).  The oracle is `oracle/torch_nsa.py` (float64 torch autograd):
+
+  * CPU: its forward is pinned to the NumPy oracle's `nsa_use` (which follows
+    `nsa_attention.py:287-327`) and its gradients to finite differences
+    (`torch.autograd.gradcheck`);
+  * GPU: `training.NsaUseModule` (fp32 kernels) matches its forward and every
+    gradient (inputs, projections, gate, compression ResBlocks) within
+    GRAD_RTOL of the largest entry, for self (3 gates) and cross (2 gates) uses.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from oracle import torch_nsa as TN
+
+GRAD_RTOL = 2e-4      # fp32 kernels vs f64 autograd, relative to max |grad|
+FWD_ATOL = 2e-5       # NumPy oracle stores f32 between steps
+
+
+def _coords(seed, side, keep):
+    g = np.random.default_rng(seed)
+    return np.argwhere(g.random((side, side, side)) < keep)
+
+
+def _weights(seed, hq, hkv, dh, n_gates, scale=0.3):
+    g = np.random.default_rng(seed)
+    d, w = hq * dh, hkv * dh
+    f = lambda *s: (g.standard_normal(s) * scale).astype(np.float32)   # noqa: E731
+    rb = lambda: (f(w, w), f(w), f(w, w), f(w))                        # noqa: E731
+    return dict(w_q=f(d, d), w_k=f(d, w), w_v=f(d, w), w_o=f(d, d), gate_w=f(d, n_gates * d),
+                gate_b=f(n_gates * d), ck=rb(), cv=rb())
+
+
+def _oracle_weights(w, n_gates):
+    return O.NsaWeights(w["w_q"], w["w_k"], w["w_v"], w["w_o"], w["gate_w"], w["gate_b"],
+                        (w["ck"], w["cv"]), n_gates)
+
+
+def _t64(w, requires_grad=False):
+    out = {}
+    for k, v in w.items():
+        if isinstance(v, tuple):
+            out[k] = tuple(torch.tensor(a, dtype=torch.float64, requires_grad=requires_grad)
+                           for a in v)
+        else:
+            out[k] = torch.tensor(v, dtype=torch.float64, requires_grad=requires_grad)
+    return out
+
+
+def _lists(seed, n, occupied, kmax=3):
+    g = np.random.default_rng(seed)
+    return [np.sort(g.choice(occupied, size=int(g.integers(1, min(kmax, occupied.size) + 1)),
+                             replace=False)) for _ in range(n)]
+
+
+def _instance(seed, self_use, side=16, keep=0.03, heads=(4, 2, 8)):
+    hq, hkv, dh = heads
+    params = O.AttentionParams(hq, hkv, dh)
+    cq = _coords(seed, side, keep)
+    ckv = cq if self_use else _coords(seed + 100, side, keep)
+    pq = O.partition_tokens("volume", cq, (side,) * 3)
+    pkv = pq if self_use else O.partition_tokens("volume", ckv, (side,) * 3)
+    g = np.random.default_rng(seed + 7)
+    d = params.model_dim
+    x = g.standard_normal((cq.shape[0], d)).astype(np.float32)
+    kv = x if self_use else g.standard_normal((ckv.shape[0], d)).astype(np.float32)
+    n_gates = 3 if self_use else 2
+    w = _weights(seed + 3, hq, hkv, dh, n_gates)
+    lists = _lists(seed + 5, cq.shape[0], pkv.occupied_ids)
+    return params, cq, ckv, pq, pkv, x, kv, w, lists, n_gates
+
+
+@pytest.mark.parametrize("self_use", [True, False])
+def test_torch_oracle_forward_matches_numpy_oracle(self_use):
+    params, _, _, pq, pkv, x, kv, w, lists, ng = _instance(11, self_use)
+    want = O.nsa_use(x, kv, pq, pkv, lists, _oracle_weights(w, ng), params)
+    sel, win = TN.key_masks(pq, pkv, lists, self_use)
+    got = TN.nsa_use(torch.tensor(x, dtype=torch.float64), torch.tensor(kv, dtype=torch.float64),
+                     _t64(w), params, pkv, sel, win)
+    err = np.max(np.abs(got.numpy() - want))
+    assert err < FWD_ATOL * max(1.0, np.max(np.abs(want))), err
+
+
+@pytest.mark.parametrize("self_use", [True, False])
+def test_torch_oracle_gradcheck(self_use):
+    """Finite differences on a tiny instance (2 q-heads, 1 kv-head, dh 2)."""
+    params, _, _, pq, pkv, x, kv, w, lists, _ = _instance(12, self_use, side=8, keep=0.025,
+                                                          heads=(2, 1, 2))
+    sel, win = TN.key_masks(pq, pkv, lists, self_use)
+    tw = _t64(w)
+    xt = torch.tensor(x, dtype=torch.float64, requires_grad=True)
+    kvt = xt if self_use else torch.tensor(kv, dtype=torch.float64, requires_grad=True)
+    flat = [tw["w_q"], tw["w_k"], tw["gate_b"], *tw["ck"], tw["cv"][2]]
+    for t in flat:
+        t.requires_grad_(True)
+
+    def f(xx, kk, *ws):
+        ww = dict(tw)
+        ww["w_q"], ww["w_k"], ww["gate_b"] = ws[0], ws[1], ws[2]
+        ww["ck"] = tuple(ws[3:7])
+        ww["cv"] = (tw["cv"][0], tw["cv"][1], ws[7], tw["cv"][3])
+        return TN.nsa_use(xx, xx if self_use else kk, ww, params, pkv, sel, win)
+    assert torch.autograd.gradcheck(f, (xt, kvt, *flat), eps=1e-6, atol=1e-6, rtol=1e-4)
+
+
+# ---------------------------------------------------------------------------
+# GPU
+
+
+def _our_weights(w, n_gates):
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200.block_partition import CompressWeights, ResBlockParams
+    return L.NsaWeights(w["w_q"], w["w_k"], w["w_v"], w["w_o"], w["gate_w"], w["gate_b"],
+                        CompressWeights(ResBlockParams(*w["ck"]), ResBlockParams(*w["cv"])),
+                        n_gates)
+
+
+def _rel(a, b, floor=1e-30):
+    """max |a - b| / max(max |b|, floor)."""
+    a = a.detach().double().cpu()
+    b = b.detach().double().cpu()
+    return float((a - b).abs().max() / max(float(b.abs().max()), floor))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("self_use", [True, False])
+def test_gpu_backward_matches_f64_autograd(cuda, self_use):
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200.training import NsaUseModule
+    params, cq, ckv, pq, pkv, x, kv, w, lists, ng = _instance(21, self_use, keep=0.05)
+    p = L.AttentionParams(*(params.n_q_heads, params.n_kv_heads, params.head_dim))
+    side = 16
+    tq = L.TokenSet("volume", x, cq, (side,) * 3)
+    part_q = L.partition(tq)
+    part_kv = part_q if self_use else L.partition(L.TokenSet("volume", kv, ckv, (side,) * 3))
+    mod = NsaUseModule(p, ng, weights=_our_weights(w, ng))
+    xg = torch.tensor(x, device="cuda", requires_grad=True)
+    kvg = xg if self_use else torch.tensor(kv, device="cuda", requires_grad=True)
+    out = mod(xg, kvg, part_q, part_kv, sel=L.Selection(lists))
+    g = np.random.default_rng(5)
+    dout = g.standard_normal(out.shape).astype(np.float32)
+    out.backward(torch.tensor(dout, device="cuda"))
+
+    sel, win = TN.key_masks(pq, pkv, lists, self_use)
+    tw = _t64(w, requires_grad=True)
+    xt = torch.tensor(x, dtype=torch.float64, requires_grad=True)
+    kvt = xt if self_use else torch.tensor(kv, dtype=torch.float64, requires_grad=True)
+    want = TN.nsa_use(xt, kvt, tw, params, pkv, sel, win)
+    want.backward(torch.tensor(dout, dtype=torch.float64))
+    assert _rel(out, want) < 1e-5
+    pairs = [("x", xg.grad, xt.grad)]
+    if not self_use:
+        pairs.append(("kv", kvg.grad, kvt.grad))
+    for name in ("w_q", "w_k", "w_v", "w_o", "gate_w", "gate_b"):
+        pairs.append((name, getattr(mod, name).grad, tw[name].grad))
+    for tag in ("ck", "cv"):
+        for i, s in enumerate(("w1", "b1", "w2", "b2")):
+            pairs.append((f"{tag}_{s}", getattr(mod, f"{tag}_{s}").grad, tw[tag][i].grad))
+    # floor: 1% of the largest gradient, for gradients that vanish exactly
+    # (the K compression's b2 shifts every compressed key of a head equally, so
+    # the cmp softmax is invariant to it; fp32 leaves cancellation noise)
+    floor = 1e-2 * max(float(b.abs().max()) for _, _, b in pairs)
+    errs = {n: _rel(a, b, floor) for n, a, b in pairs}
+    bad = {n: e for n, e in errs.items() if e > GRAD_RTOL}
+    assert not bad, bad
+
+
+@pytest.mark.gpu
+def test_gpu_training_steps_reduce_loss(cuda):
+    """A few Adam steps on a fixed regression target lower the loss."""
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200.training import NsaUseModule
+    params, cq, _, _, _, x, _, w, lists, ng = _instance(31, True, keep=0.05)
+    p = L.AttentionParams(params.n_q_heads, params.n_kv_heads, params.head_dim)
+    part = L.partition(L.TokenSet("volume", x, cq, (16,) * 3))
+    mod = NsaUseModule(p, ng, weights=_our_weights(w, ng))
+    xg = torch.tensor(x, device="cuda")
+    target = torch.tensor(np.random.default_rng(2).standard_normal(x.shape).astype(np.float32),
+                          device="cuda")
+    opt = torch.optim.Adam(mod.parameters(), lr=1e-2)
+    sel = L.Selection(lists)
+    losses = []
+    for _ in range(20):
+        opt.zero_grad()
+        loss = ((mod(xg, xg, part, part, sel=sel) - target) ** 2).mean()
+        loss.backward()
+        opt.step()
+        losses.append(float(loss.detach()))
+    assert losses[-1] < 0.9 * losses[0], losses
