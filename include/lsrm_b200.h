@@ -371,17 +371,24 @@ int lsrm_bias_act(int exact, const void* h, int h_bf16, int64_t ld, const float*
                   int out_bf16, int64_t ld_out, void* stream);
 
 /* ---- backward of one gated NSA use (training) -----
- * fp32, recompute-based; the reference has no backward (oracle:
- * oracle/torch_nsa.py, f64 autograd).  dK/dV accumulate with atomics (not
- * bit-deterministic); callers zero dq/dk/dv first.
- * attention_bwd: same key-set arguments as lsrm_attention_f32 (mode 0 cmp,
- * 1 sel, 2 win); q/dO/O [nq, hq, dh] token order; dq += ...; dk/dv += ... */
+ * fp32, recompute-based, deterministic (fixed summation orders, no float
+ * atomics); the reference has no backward (oracle: oracle/torch_nsa.py, f64
+ * autograd).
+ * attention_bwd: key sets as lsrm_attention_f32 (mode 0 cmp over all nk
+ * rows, 1 sel over the resolved rows, 2 win over own_row), q/dO/O
+ * [nq, hq, dh] and k/v [nk, hkv, dh] (block-major for sel/win).  n_rows and
+ * max_row_keys describe block_offsets (sel/win).  The key pass splits the
+ * queries into n_slices ranges (more CTAs for few keys); workspace holds the
+ * per-slice partials.  Accumulates: dq += ..., dk += ..., dv += .... */
+size_t lsrm_attention_bwd_workspace(int64_t nq, int hq, int64_t nk, int hkv, int dh,
+                                    int n_slices);
 int lsrm_attention_bwd_f32(int mode, const float* q, const float* dO, const float* O,
                            int64_t nq, int hq, int hkv, int dh, const float* k,
                            const float* v, int64_t nk, const int64_t* block_offsets,
-                           const int32_t* rows, const int32_t* count, int kmax_rows,
-                           const int32_t* own_row, float* dq, float* dk, float* dv,
-                           void* stream);
+                           int n_rows, int max_row_keys, const int32_t* rows,
+                           const int32_t* count, int kmax_rows, const int32_t* own_row,
+                           int n_slices, float* dq, float* dk, float* dv, void* workspace,
+                           size_t ws_bytes, void* stream);
 /* merged = sum_b sigmoid(gl[:, b*d:(b+1)*d] + gb[b*d:]) * o_b:
  * do_b = dM g_b,  dz[:, b*d + c] = dM o_b g_b (1 - g_b)   (dz [n, n_gates*d]). */
 int lsrm_gate_merge_bwd_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,

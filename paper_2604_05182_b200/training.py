@@ -5,7 +5,8 @@ no backward.  This module adds one on the GPU path: an fp32
 forward that keeps its intermediates (same kernels as `nsa_cross_attention`)
 and a backward built from
 
-  * `lsrm_attention_bwd_f32`  - the three branches (recompute, dK/dV atomics),
+  * `lsrm_attention_bwd_f32`  - the three branches (recompute; a query-major
+                                dQ pass and a key-major dK/dV pass, no atomics),
   * `lsrm_gate_merge_bwd_f32` - the sigmoid-gated merge,
   * `lsrm_res_block_bwd_f32`  - the compression ResBlock under the block mean,
   * `lsrm_gemm_f32_ex`        - every projection / weight gradient (cuBLAS),
@@ -25,7 +26,7 @@ import torch
 
 from . import _dev as D
 from . import _ops
-from ._native import call
+from ._native import call, lib
 from .block_partition import BlockPartition, compress_rows
 from .errors import require
 from .nsa_attention import NsaWeights, _attn, resolve_rows, selection_rows
@@ -119,11 +120,18 @@ def _backward(spec: _Spec, P, s, dout):
     offs = part.dev("block_offsets")
     kmax = int(spec.rows.shape[1])
 
+    max_occ = int(np.max(part.occupancy)) if B else 1
+
     def bwd(mode, b, k, v, nk, dk, dv, rows=None, count=None, own=None):
+        # cmp has few keys and every query: slice the queries for parallelism
+        n_slices = max(1, min(64, n // 256)) if mode == 0 else max(1, min(4, n // 1024))
+        ws_bytes = lib().lsrm_attention_bwd_workspace(n, hq, nk, hkv, dh, n_slices)
+        ws = D.empty((ws_bytes,), torch.uint8)
         call("lsrm_attention_bwd_f32", mode, s["q"].data_ptr(), do[b].data_ptr(),
              o[b].data_ptr(), n, hq, hkv, dh, k.data_ptr(), v.data_ptr(), nk,
-             offs.data_ptr() if mode else None, D.ptr(rows), D.ptr(count), kmax, D.ptr(own),
-             dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), st)
+             offs.data_ptr() if mode else None, B, max_occ, D.ptr(rows), D.ptr(count), kmax,
+             D.ptr(own), n_slices, dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr(),
+             ws_bytes, st)
     bwd(0, 0, s["kc"], s["vc"], B, dkc, dvc)
     bwd(1, 1, s["k_bm"], s["v_bm"], m, dk_bm, dv_bm, rows=spec.rows, count=spec.count)
     if ng == 3:
@@ -207,3 +215,45 @@ def _weight_arrays(w: NsaWeights) -> dict:
     return {"w_q": w.w_q, "w_k": w.w_k, "w_v": w.w_v, "w_o": w.w_o, "gate_w": w.gate_w,
             "gate_b": w.gate_b, "ck_w1": ck.w1, "ck_b1": ck.b1, "ck_w2": ck.w2, "ck_b2": ck.b2,
             "cv_w1": cv.w1, "cv_b1": cv.b1, "cv_w2": cv.w2, "cv_b2": cv.b2}
+
+
+USE_STREAMS = {"v2v": ("x", "x", 3), "v2i": ("x", "y", 2), "i2i": ("y", "y", 3),
+               "i2v": ("y", "x", 2)}
+
+
+@dataclass
+class ResolvedRows:
+    rows: torch.Tensor
+    count: torch.Tensor
+
+
+def resolve_plan_rows(plan_rows: dict, part_vol: BlockPartition, part_img: BlockPartition):
+    """Routing-plan device rows -> fallback-resolved rows per use
+    (`nsa_attention.py:123-154`), reusable across training steps."""
+    parts = {"x": part_vol, "y": part_img}
+    out = {}
+    for use, (qs, ks, ng) in USE_STREAMS.items():
+        rows, count = plan_rows[use]
+        own = parts[ks].block_of_token if ng == 3 else None
+        r, c, _, _, _ = resolve_rows(rows, count, parts[ks], own, True)
+        out[use] = ResolvedRows(r, c)
+    return out
+
+
+class NsaLayerModule(torch.nn.Module):
+    """The four NSA uses of one Stage-2 layer (`recon_pipeline.py:477-488`):
+    v2v and v2i read the volume stream x as queries, i2i and i2v the image
+    stream y; returns each use's output."""
+
+    def __init__(self, params: AttentionParams, weights: dict = None, seed: int = 0):
+        super().__init__()
+        self.uses = torch.nn.ModuleDict({
+            u: NsaUseModule(params, ng, weights=(weights or {}).get(u), seed=seed)
+            for u, (_, _, ng) in USE_STREAMS.items()})
+
+    def forward(self, x, y, part_vol, part_img, resolved: dict) -> dict:
+        streams = {"x": x, "y": y}
+        parts = {"x": part_vol, "y": part_img}
+        return {u: self.uses[u](streams[qs], streams[ks], parts[qs], parts[ks],
+                                table=resolved[u])
+                for u, (qs, ks, _) in USE_STREAMS.items()}
