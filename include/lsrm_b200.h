@@ -407,6 +407,24 @@ int lsrm_gemm_f32_ex(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, 
                      const float* a, int64_t lda, const float* b, int64_t ldb, float beta,
                      float* c, int64_t ldc, void* stream);
 
+/* ---- feature decode around the sparse stage (recon_pipeline.py:209-348) --
+ * f64 arithmetic, the reference's f32 rounding points, NumPy operation order.
+ * decode_scatter: vec [side^3, t^3*d_f] (token-major, slice [dz,dy,dx,c]) ->
+ * grid [(t*side)^3, d_f]. */
+int lsrm_decode_scatter(const float* vec, int side, int t, int d_f, float* grid, void* stream);
+/* sparse fine features: rows [n*t^3, d_f] and index [s_f^3] int64 (-1 absent). */
+int lsrm_sparse_features(const float* vec, const int64_t* coords, int64_t n, int t, int d_f,
+                         int64_t s_f, int64_t* index, float* rows, void* stream);
+/* Blended field query (sparse_index NULL: dense trilinear only) at f64 points
+ * [n,3] in [0,1]^3, then the z (gelu, sigmoid) and s (gelu, identity) heads
+ * + the bounding-sphere offset.  head_w: host array of 8 device pointers
+ * (z w1 b1 w2 b2, s w1 b1 w2 b2) or NULL for the field only; field_out
+ * [n, d_f] optional. */
+int lsrm_decode_points(const float* grid, int s_df, const int64_t* sparse_index,
+                       const float* sparse_rows, int s_f, int d_f, const double* points,
+                       int64_t n, const float* const* head_w, int hidden, int z_channels,
+                       float* z_out, float* s_out, float* field_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,7 +10,7 @@ All compute runs in the in-tree C-ABI library `_lib/liblsrm_b200.so`
 from .errors import (BehindCameraError, ConfigurationError, EmptyAttentionRowError,
                      EmptyContextError, GoldenFormatError, LsrmError, OutOfDomainError,
                      ProtocolError, VerificationError)
-from .tensor_core import AttentionParams
+from .tensor_core import AttentionParams, read_goldens, write_goldens
 from .tokenizer import (PosEmbed, TokenSet, foreground_patch_mask, informative_voxel_mask,
                         init_pos_embed, upsample_select_tokens)
 from .block_partition import (BlockPartition, CompressWeights, compress_block_kv,
@@ -28,5 +28,11 @@ from .seq_parallel import (TOKEN_COORD_BYTES, WorkerTopology, all_gather_kv, all
                            imbalance_report, makespan_ratio, message_log_to_csv,
                            naive_contiguous_shards, naive_split_loads, shard_blocks,
                            shard_blocks_by_cost)
+from .recon_pipeline import (DecodeWeights, DecoderHeads, DenseBlockWeights, FeatureVolume,
+                             MhaWeights, build_sparse_context, build_sparse_features,
+                             decode_feature_volume, decode_point, decode_points,
+                             dense_block_forward, dense_stage_forward, init_decode,
+                             init_decoder_heads, init_dense_block, mha_forward, query_field,
+                             sparse_block_forward, sparse_stage_forward)
 
 __version__ = "0.1.0"

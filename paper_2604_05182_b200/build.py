@@ -23,7 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
           "-Xptxas", "-v", "--expt-relaxed-constexpr"]
-EXACT_TUS = {"routing.cu", "tokens.cu", "partition.cu", "raymarch.cu", "camera.cu"}
+EXACT_TUS = {"routing.cu", "tokens.cu", "partition.cu", "raymarch.cu", "camera.cu",
+             "decode.cu"}
 # LSRM_NVCC_FLAGS="-DLSRM_TRACE" builds the per-chunk event trace of the fused
 # attention kernel (tools/attn_trace.py); off by default.
 EXTRA = os.environ.get("LSRM_NVCC_FLAGS", "").split()

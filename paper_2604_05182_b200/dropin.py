@@ -26,8 +26,12 @@ HOT_PATH = {
                       "image_token_coords"),
     "tokenizer": ("informative_voxel_mask", "foreground_patch_mask", "upsample_select_tokens"),
     "seq_parallel": ("shard_blocks", "all_to_all", "all_gather_kv", "naive_contiguous_shards"),
-    "recon_pipeline": ("sparse_block_forward", "build_sparse_context", "ffn_forward"),
+    "recon_pipeline": ("sparse_block_forward", "build_sparse_context", "ffn_forward",
+                       "mha_forward", "dense_block_forward", "dense_stage_forward",
+                       "decode_feature_volume", "build_sparse_features", "query_field",
+                       "decode_points"),
     "camera_geometry": ("pluecker_rays", "silhouette_alpha"),
+    "tensor_core": ("write_goldens", "read_goldens"),
 }
 
 _saved = []

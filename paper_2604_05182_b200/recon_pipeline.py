@@ -10,6 +10,7 @@ LayerNorm, gate mixture + LayerNorm and the FFN residual as fused kernels
 (csrc/block.cu) around bf16 cuBLAS GEMMs.
 """
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -272,3 +273,280 @@ class SparseBlockEngine:
             u = _ops.gemm(t, self.bf[k2], out_dtype=torch.float32)
             res.append(_bias_act(0, u, D.weight(ffn.b2), 0, residual=x1))
         return tuple(res)
+
+
+# ---------------------------------------------------------------------------
+# Stage 1: dense blocks (recon_pipeline.py:113-193; §8f rank 4)
+
+
+@dataclass
+class MhaWeights:
+    """`recon_pipeline.py:45-49`."""
+    w_q: np.ndarray
+    w_k: np.ndarray
+    w_v: np.ndarray
+    w_o: np.ndarray
+
+
+@dataclass
+class DenseBlockWeights:
+    """`recon_pipeline.py:117-131`."""
+    x_self: MhaWeights
+    x_cross: MhaWeights
+    y_self: MhaWeights
+    y_cross: MhaWeights
+    gate_x_w: np.ndarray
+    gate_x_b: np.ndarray
+    gate_y_w: np.ndarray
+    gate_y_b: np.ndarray
+    ln_attn_x: NormParams
+    ln_attn_y: NormParams
+    ln_ffn_x: NormParams
+    ln_ffn_y: NormParams
+    ffn_x: FfnWeights
+    ffn_y: FfnWeights
+
+
+def init_mha(seed: int, params: AttentionParams, *tags, scale: float = 0.02) -> MhaWeights:
+    """`recon_pipeline.py:66-74` (same tags, so identical weights)."""
+    d = params.model_dim
+    kv_w = params.n_kv_heads * params.head_dim
+    return MhaWeights(normal_f32(seed, (d, d), scale, *tags, "wq"),
+                      normal_f32(seed, (d, kv_w), scale, *tags, "wk"),
+                      normal_f32(seed, (d, kv_w), scale, *tags, "wv"),
+                      normal_f32(seed, (d, d), scale, *tags, "wo"))
+
+
+def init_dense_block(seed: int, params: AttentionParams, layer: int,
+                     scale: float = 0.02) -> DenseBlockWeights:
+    """`recon_pipeline.py:134-151`."""
+    d = params.model_dim
+    tag = f"dense{layer}"
+    return DenseBlockWeights(
+        x_self=init_mha(seed, params, tag, "xs", scale=scale),
+        x_cross=init_mha(seed, params, tag, "xc", scale=scale),
+        y_self=init_mha(seed, params, tag, "ys", scale=scale),
+        y_cross=init_mha(seed, params, tag, "yc", scale=scale),
+        gate_x_w=normal_f32(seed, (d, 2 * d), scale, tag, "gx"),
+        gate_x_b=np.zeros(2 * d, dtype=DTYPE),
+        gate_y_w=normal_f32(seed, (d, 2 * d), scale, tag, "gy"),
+        gate_y_b=np.zeros(2 * d, dtype=DTYPE),
+        ln_attn_x=init_norm(d), ln_attn_y=init_norm(d),
+        ln_ffn_x=init_norm(d), ln_ffn_y=init_norm(d),
+        ffn_x=init_ffn(seed, d, tag, "fx", scale=scale),
+        ffn_y=init_ffn(seed, d, tag, "fy", scale=scale))
+
+
+def mha_forward(q_in, kv_in, w: MhaWeights, params: AttentionParams):
+    """Full multi-head attention with the output projection
+    (`recon_pipeline.py:90-98`): fp32 projections, dense GQA softmax
+    (`tensor_core.py:164-206`, csrc/attn_f32.cu mode 0), W_o."""
+    from .errors import EmptyContextError
+    from .nsa_attention import _attn
+    on_dev = D.is_device(q_in)
+    qd, kd = D.dev(q_in, torch.float32), D.dev(kv_in, torch.float32)
+    if kd.shape[0] == 0:
+        raise EmptyContextError("attention over an empty key set")
+    n = int(qd.shape[0])
+    hq, hkv, dh = params.n_q_heads, params.n_kv_heads, params.head_dim
+    q = _ops.gemm(qd, D.weight(w.w_q)).view(n, hq, dh)
+    k = _ops.gemm(kd, D.weight(w.w_k)).view(-1, hkv, dh)
+    v = _ops.gemm(kd, D.weight(w.w_v)).view(-1, hkv, dh)
+    o = _attn(0, q, k, v, params)
+    out = _ops.gemm(o.view(n, params.model_dim), D.weight(w.w_o))
+    return out if on_dev else D.host(out)
+
+
+def dense_block_forward(x, y, w: DenseBlockWeights, params: AttentionParams):
+    """Pre-norm residual dense block (`recon_pipeline.py:154-184`): both
+    streams update from the same pre-block state. Returns (x', y')."""
+    require(x.shape[0] > 0 and y.shape[0] > 0, "dense block needs nonempty token streams")
+    d = params.model_dim
+    require(x.shape[1] == d and y.shape[1] == d, "token width mismatch")
+    on_dev = D.is_device(x)
+    xd, yd = D.dev(x, torch.float32), D.dev(y, torch.float32)
+    _, xh = _add_ln(xd, None, w.ln_attn_x)
+    _, yh = _add_ln(yd, None, w.ln_attn_y)
+    lx = _ops.gemm(xh, D.weight(w.gate_x_w))
+    ly = _ops.gemm(yh, D.weight(w.gate_y_w))
+    o = {"xs": mha_forward(xh, xh, w.x_self, params), "xc": mha_forward(xh, yh, w.x_cross, params),
+         "ys": mha_forward(yh, yh, w.y_self, params), "yc": mha_forward(yh, xh, w.y_cross, params)}
+    outs = []
+    for base, lg, gb, os_, oc, ln, ffn in ((xd, lx, w.gate_x_b, o["xs"], o["xc"], w.ln_ffn_x, w.ffn_x),
+                                          (yd, ly, w.gate_y_b, o["ys"], o["yc"], w.ln_ffn_y, w.ffn_y)):
+        x1, h = _gate_mix_ln(1, base, lg, lg.stride(0), D.weight(gb), os_, oc, ln)
+        t = _bias_act(1, _ops.gemm(h, D.weight(ffn.w1)), D.weight(ffn.b1), 1)
+        outs.append(_bias_act(1, _ops.gemm(t, D.weight(ffn.w2)), D.weight(ffn.b2), 0,
+                              residual=x1))
+    return tuple(a if on_dev else D.host(a) for a in outs)
+
+
+def dense_stage_forward(x0, y0, weights, params: AttentionParams):
+    """`recon_pipeline.py:187-193`."""
+    on_dev = D.is_device(x0)
+    x, y = D.dev(x0, torch.float32), D.dev(y0, torch.float32)
+    for w in weights:
+        x, y = dense_block_forward(x, y, w, params)
+    return (x, y) if on_dev else (D.host(x), D.host(y))
+
+
+# ---------------------------------------------------------------------------
+# feature decode (recon_pipeline.py:196-348; csrc/decode.cu)
+
+T_SIDE = 4          # per-axis decode upsampling (recon_pipeline.py:36)
+FEATURE_DIM = 32    # decoded feature channels (recon_pipeline.py:37)
+
+
+@dataclass
+class DecodeWeights:
+    """`recon_pipeline.py:197-199`: weight [d, T^3 * d_f], bias."""
+    weight: np.ndarray
+    bias: np.ndarray
+
+
+def init_decode(seed: int, d: int, *tags, d_f: int = FEATURE_DIM,
+                scale: float = 0.02) -> DecodeWeights:
+    """`recon_pipeline.py:202-206`."""
+    out = (T_SIDE ** 3) * d_f
+    return DecodeWeights(normal_f32(seed, (d, out), scale, *tags, "dec"),
+                         np.zeros(out, dtype=DTYPE))
+
+
+@dataclass
+class FeatureVolume:
+    """`recon_pipeline.py:271-283`; arrays may be NumPy or CUDA tensors."""
+    dense: object
+    sparse_index: object = None
+    sparse_rows: object = None
+
+    @property
+    def s_df(self) -> int:
+        return int(self.dense.shape[0])
+
+    @property
+    def s_f(self):
+        return None if self.sparse_index is None else int(self.sparse_index.shape[0])
+
+
+@dataclass
+class DecoderHeads:
+    """`recon_pipeline.py:286-289`: [(w, b, act), ...] per head."""
+    z_layers: list
+    s_layers: list
+
+
+def init_decoder_heads(seed: int, d_f: int = FEATURE_DIM, z_channels: int = 3,
+                       hidden: int = 64, scale: float = 0.02) -> DecoderHeads:
+    """`recon_pipeline.py:292-301`."""
+    def head(tag, out_dim, act):
+        w1 = normal_f32(seed, (d_f, hidden), scale, "head", tag, "w1")
+        w2 = normal_f32(seed, (hidden, out_dim), scale, "head", tag, "w2")
+        return [(w1, np.zeros(hidden, dtype=DTYPE), "gelu"),
+                (w2, np.zeros(out_dim, dtype=DTYPE), act)]
+    return DecoderHeads(head("z", z_channels, "sigmoid"), head("s", 1, "identity"))
+
+
+def _affine_dec(x, w: DecodeWeights):
+    """f32(x W + b), fp32 GEMM + bias (the reference: f64 accumulation)."""
+    v = _ops.gemm(x, D.weight(w.weight))
+    return _bias_act(1, v, D.weight(w.bias), 0)
+
+
+def decode_feature_volume(x_d, w: DecodeWeights, d_f: int = FEATURE_DIM):
+    """Dense feature grid [4s, 4s, 4s, d_f] from the coarse token cube
+    (`recon_pipeline.py:223-231`)."""
+    on_dev = D.is_device(x_d)
+    xd = D.dev(x_d, torch.float32)
+    n = int(xd.shape[0])
+    side = round(n ** (1.0 / 3.0))
+    if side ** 3 != n:
+        from .errors import ConfigurationError
+        raise ConfigurationError(f"{n} tokens is not a cubic grid")
+    require(w.weight.shape[1] == (T_SIDE ** 3) * d_f, "decode width mismatch")
+    vec = _affine_dec(xd, w)
+    s = side * T_SIDE
+    grid = D.empty((s, s, s, d_f), torch.float32)
+    call("lsrm_decode_scatter", vec.data_ptr(), side, T_SIDE, d_f, grid.data_ptr(), D.stream())
+    return grid if on_dev else D.host(grid)
+
+
+def build_sparse_features(tokens, w: DecodeWeights, d_f: int = FEATURE_DIM):
+    """(index [S_f^3] int64 with -1 for absent cells, rows [M, d_f]) over the
+    4^3 cells of every active volume token (`recon_pipeline.py:234-268`)."""
+    require(tokens.modality == "volume", "sparse decode needs volume tokens")
+    on_dev = D.is_device(tokens.features)
+    s_f = T_SIDE * int(tokens.grid_res[0])
+    index = D.empty((s_f, s_f, s_f), torch.int64)
+    n = int(tokens.count)
+    rows = D.empty((n * T_SIDE ** 3, d_f), torch.float32)
+    vec = _affine_dec(D.dev(tokens.features, torch.float32), w) if n else rows
+    coords = D.dev(tokens.coords, torch.int64)
+    call("lsrm_sparse_features", vec.data_ptr(), coords.data_ptr(), n, T_SIDE, d_f, s_f,
+         index.data_ptr(), rows.data_ptr(), D.stream())
+    return (index, rows) if on_dev else (D.host(index), D.host(rows))
+
+
+def _points(points):
+    from .errors import OutOfDomainError
+    pts = D.dev(points, torch.float64).reshape(-1, 3)
+    bad = (pts < 0.0) | (pts > 1.0)
+    if bool(bad.any()):
+        p = D.host(pts[bad.any(dim=1)][0])
+        raise OutOfDomainError(f"point outside the unit cube: {p.tolist()}")
+    return pts
+
+
+def _decode(fv: FeatureVolume, points, heads: DecoderHeads = None, want_field=False):
+    dense = D.dev(fv.dense, torch.float32)
+    s_df, d_f = int(dense.shape[0]), int(dense.shape[3])
+    require(s_df >= 2, "trilinear needs side >= 2")
+    pts = _points(points)
+    n = int(pts.shape[0])
+    idx = rows = None
+    s_f = 0
+    if fv.sparse_index is not None:
+        idx = D.dev(fv.sparse_index, torch.int64)
+        rows = D.dev(fv.sparse_rows, torch.float32)
+        s_f = int(idx.shape[0])
+    field = D.empty((n, d_f), torch.float32) if want_field else None
+    z = s = hw = None
+    hidden = zc = 1
+    if heads is not None:
+        (zw1, zb1, _), (zw2, zb2, _) = heads.z_layers
+        (sw1, sb1, _), (sw2, sb2, _) = heads.s_layers
+        ws = [D.weight(a) for a in (zw1, zb1, zw2, zb2, sw1, sb1, sw2, sb2)]
+        hw = (ctypes.c_void_p * 8)(*[t.data_ptr() for t in ws])
+        hidden, zc = int(zw1.shape[1]), int(zw2.shape[1])
+        z = D.empty((n, zc), torch.float32)
+        s = D.empty((n,), torch.float32)
+    call("lsrm_decode_points", dense.data_ptr(), s_df, D.ptr(idx), D.ptr(rows), s_f, d_f,
+         pts.data_ptr(), n, hw, hidden, zc, D.ptr(z), D.ptr(s), D.ptr(field), D.stream())
+    return z, s, field
+
+
+def query_field(fv: FeatureVolume, mask, points):
+    """Blended sparse/dense feature lookup (`recon_pipeline.py:304-346`)."""
+    require(fv.sparse_index is not None, "feature volume has no sparse part")
+    require(mask.shape[0] * T_SIDE == fv.s_f, "mask resolution does not match the sparse grid")
+    on_dev = D.is_device(points)
+    _, _, f = _decode(fv, points, want_field=True)
+    return f if on_dev else D.host(f)
+
+
+def decode_points(fv: FeatureVolume, heads: DecoderHeads, points, mask=None):
+    """(z, s) at query points (`recon_pipeline.py:349-365`): the blended
+    sparse query when the volume has a sparse part, else dense trilinear; z
+    through the sigmoid head, s through the SDF head + bounding-sphere offset."""
+    if fv.sparse_index is not None:
+        require(mask is not None, "sparse field query needs the voxel mask")
+        require(mask.shape[0] * T_SIDE == fv.s_f,
+                "mask resolution does not match the sparse grid")
+    on_dev = D.is_device(points)
+    z, s, _ = _decode(fv, points, heads)
+    return (z, s) if on_dev else (D.host(z), D.host(s))
+
+
+def decode_point(fv: FeatureVolume, heads: DecoderHeads, p, mask=None):
+    """`recon_pipeline.py:368-371`."""
+    z, s = decode_points(fv, heads, np.asarray(p, np.float64).reshape(1, 3), mask)
+    return z[0], float(s[0])
