@@ -215,6 +215,12 @@ int lsrm_gemm_bias_bf16(int64_t m, int64_t n, int64_t k, const void* a, int64_t 
                         const void* b, int64_t ldb, const void* bias, void* c,
                         int64_t ldc, void* stream);
 
+/* D[m,n] = A[m,k] @ B[k,n] + bias[n] + R[m,n]: bf16 A/B, f32 bias, residual R
+ * (may be NULL, may alias D) and output; cuBLASLt epilogue. */
+int lsrm_gemm_bias_res_f32(int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
+                           const void* b, int64_t ldb, const float* bias, const float* res,
+                           int64_t ldr, float* d, int64_t ldd, void* stream);
+
 /* ---- fused bf16 three-branch NSA attention, tcgen05/TMEM  -------------
  * (nsa_attention.py:84-112,157-207,266-284 fused)
  * q: [nq, hq, dh] bf16 in query BLOCK-MAJOR order; kv_il: K and V in the
@@ -352,8 +358,9 @@ int lsrm_layer_norm(int in_bf16, const void* x, int64_t n, int d,
  * exact = 1: the reference's f32 storage with f64 arithmetic (reference API);
  * exact = 0: fp32 arithmetic (bf16 engine).  Row kernels run a warp per row
  * with f64 LayerNorm statistics (tensor_core.py:139-146).
- * add_layer_norm: sum_out = f32(a + b) (b may be NULL), y = LN(sum_out). */
-int lsrm_add_layer_norm(const float* a, const void* b, int b_bf16, int64_t n, int d,
+ * add_layer_norm: sum_out = f32(a + b) (b may be NULL), y = LN(sum_out);
+ * exact = 0 keeps the row in registers with fp32 statistics (d = 1024). */
+int lsrm_add_layer_norm(int exact, const float* a, const void* b, int b_bf16, int64_t n, int d,
                         const float* gamma, const float* beta, float eps,
                         float* sum_out, int out_bf16, void* y, void* stream);
 /* x1 = f32(xe + sigmoid(gl[:, :d] + gb[:d]) * o_self

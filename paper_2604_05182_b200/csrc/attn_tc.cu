@@ -262,8 +262,23 @@ struct Launch {
 #define LSRM_PINGPONG 0
 #endif
 constexpr int kStages = LSRM_STAGES;   // K/V ring depth (each stage holds every head of the item)
+#ifndef LSRM_SPLIT
+#define LSRM_SPLIT 1
+#endif
+#ifndef LSRM_SPLIT_RELOAD
+#define LSRM_SPLIT_RELOAD 1
+#endif
 constexpr bool kOnePass = LSRM_ONEPASS;
 constexpr bool kPingPong = LSRM_PINGPONG;
+// kSplit softmax warps per TMEM lane quadrant: warp `half` of a pair owns
+// key columns [64*half, 64*half+64) of every chunk and output columns
+// [DH/2*half, ...) of the epilogue; the pair exchanges row maxima through
+// shared memory.  Doubles the softmax warps per SMSP without more TMEM.
+constexpr int kSplit = LSRM_SPLIT;
+static_assert(kSplit == 1 || kSplit == 2, "LSRM_SPLIT must be 1 or 2");
+
+static_assert(kSplit == 1 || (!LSRM_ONEPASS && !LSRM_PINGPONG),
+              "the split softmax is two-pass only");
 // gate biases staged in shared memory as [n_gates * hq][DH + 1] (padded rows:
 // the 16 heads of a warp hit 16 banks) when they fit, else read from global
 constexpr int kBiasMax = LSRM_STAGES <= 3 ? 3328 : 4;
@@ -406,6 +421,7 @@ struct Pipe {
   int32_t seg_occ[kMaxEnt + 1];
   int32_t seg_cum[kMaxEnt];
   ChunkDesc desc[kStages];
+  float xmax[kSplit > 1 ? 2 : 1][HP][kSplit][kM];   // split: partial row maxima, by chunk parity
   uint64_t kv_full[kStages], kv_empty[kStages], s_full[HP], s_free[HP], p_full[HP], o_full[HP],
       q_full[2], q_empty[2];
 };
@@ -419,7 +435,7 @@ struct Smem {
 
 // per pipeline: 4 softmax warps per head-tile, 1 producer, 1 MMA warp per head-tile
 template <int HP, int NP>
-constexpr int threads_of() { return 32 * NP * (5 * HP + 1); }
+constexpr int threads_of() { return 32 * NP * (4 * kSplit * HP + HP + 1); }
 
 // Work item = (query tile, group of HP kv heads).  The HP head-tiles share the
 // chunk plan (same tokens, same union of selected blocks) but not K/V, so
@@ -442,7 +458,8 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
   Smem<DH, HP, NP>& SM = *reinterpret_cast<Smem<DH, HP, NP>*>(smem_raw);
   using HCols = HeadCols<DH>;
   constexpr int VW = HCols::VW, HC = HCols::kTotal;
-  constexpr int kSoftWarps = 4 * HP * NP, kProducerWarp = kSoftWarps;
+  constexpr int kSoftPerPipe = 4 * HP * kSplit;
+  constexpr int kSoftWarps = kSoftPerPipe * NP, kProducerWarp = kSoftWarps;
   constexpr int kAlloc = tmem_alloc_cols<DH, HP, NP>();
   static_assert(kAlloc <= 512, "TMEM budget");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -452,7 +469,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
   const bool dyn = L.order != nullptr;
   const int64_t n_items = dyn ? L.n_order : P.n_tiles * n_hgroups;
   // role -> pipeline: softmax warps [0, 4*HP*NP), producers, then MMA warps
-  const int pipe_id = warp < kSoftWarps ? warp / (4 * HP)
+  const int pipe_id = warp < kSoftWarps ? warp / kSoftPerPipe
                       : (warp < kSoftWarps + NP ? warp - kSoftWarps
                                                 : (warp - kSoftWarps - NP) / HP);
   Pipe<DH, HP>& S = SM.pipe[pipe_id];
@@ -474,8 +491,8 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     }
     for (int hh = 0; hh < HP; ++hh) {
       mbar_init(&S.s_full[hh], 1);
-      mbar_init(&S.s_free[hh], 128);
-      mbar_init(&S.p_full[hh], 128);
+      mbar_init(&S.s_free[hh], 128 * kSplit);
+      mbar_init(&S.p_full[hh], 128 * kSplit);
       mbar_init(&S.o_full[hh], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -813,7 +830,12 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     __syncwarp();
   } else {
     // ===================== softmax / epilogue (warpgroup hh = head-tile hh)
-    const int hh = (warp % (4 * HP)) >> 2, q4 = warp & 3;
+    const int wi = warp % kSoftPerPipe;
+    const int hh = wi / (4 * kSplit), half = (wi >> 2) % kSplit, q4 = warp & 3;
+    // epilogue / rescale columns of this warp, and the pair's named barrier
+    constexpr int kOCols = DH / kSplit;
+    const int oc0 = half * kOCols;
+    const int pair_bar = 1 + (pipe_id * HP + hh) * 4 + q4;
     const int m = q4 * 32 + lane;
     const int t = m / G, g_in = m % G;
     const uint32_t tS = tmem + ((uint32_t)(q4 * 32) << 16) + hh * HC;
@@ -863,7 +885,8 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const float* bp =
           bias_all ? bias_all + ((int64_t)br_pend * P.hq + head_pend) * bias_ld : nullptr;
 #pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 16) {   // 16 columns at a time (registers)
+      for (int cq = 0; cq < kOCols; cq += 16) {   // 16 columns at a time (registers)
+        const int c0 = oc0 + cq;
         uint32_t r[16], mr[8];
         tmem_ld16_nowait(tO + c0, r);
         if (br_pend > 0) tmem_ld_cols<8>(tM + c0 / 2, mr);
@@ -926,8 +949,9 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const uint32_t visb = D.tokvis[t];
       const int ncols = hdr0.x;
       uint32_t sa[32], sb[32];
-      tmem_ld32(tS + HCols::kS, sa);
-      if (ncols > 32) tmem_ld32(tS + HCols::kS + 32, sb);
+      const int pcb = 2 * half;   // first 32-key piece of this warp (split: 0 or 2)
+      if (kSplit == 1 || ncols > 32 * pcb) tmem_ld32(tS + HCols::kS + 32 * pcb, sa);
+      if (ncols > 32 * (pcb + 1)) tmem_ld32(tS + HCols::kS + 32 * (pcb + 1), sb);
 #ifdef LSRM_TRACE_LD
       tmem_wait_ld();
       if (tid == 0) trace(trp, c, 1);
@@ -954,7 +978,117 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       // (max, then exponentials); later chunks stream once.
       const bool two_pass =
           !kOnePass || __any_sync(0xffffffffu, m_run == kNegInf && visb != 0u);
-      if (two_pass) {
+      if constexpr (kSplit == 2) {
+        // ---- split softmax: this warp's two pieces stay in registers
+        const bool has0 = ncols > 32 * pcb, has1 = ncols > 32 * (pcb + 1);
+#define LSRM_MAX(arr, off, gi)                                  \
+  {                                                             \
+    const float g_ = max16(arr + (off));                        \
+    mx = ((visb >> (gi)) & 1u) ? fmaxf(mx, g_) : mx;            \
+  }
+        if (has0) {
+          LSRM_MAX(sa, 0, 2 * pcb)
+          LSRM_MAX(sa, 16, 2 * pcb + 1)
+        }
+        if (has1) {
+          LSRM_MAX(sb, 0, 2 * pcb + 2)
+          LSRM_MAX(sb, 16, 2 * pcb + 3)
+        }
+#undef LSRM_MAX
+#if LSRM_SPLIT_RELOAD
+        // pass 2 reloads S piece by piece (fewer live registers)
+#else
+        tc_before_sync();
+        mbar_arrive(&S.s_free[hh]);   // S(c) in registers: QK(c+1) may overwrite it
+#endif
+        // row max across the pair (double-buffered by chunk parity)
+        S.xmax[c & 1][hh][half][m] = mx;
+        named_sync(pair_bar, 64);
+        mx = fmaxf(mx, S.xmax[c & 1][hh][half ^ 1][m]);
+        if (tid == 0) trace(trp, c, 10);
+        const float m_cand = fmaxf(m_run, mx * sl2);
+        float m_use = m_run, scale = 1.f;
+        bool need = false;
+        if (m_run == kNegInf) {
+          m_use = m_cand;
+        } else if (m_cand > m_run + kHeadroom) {
+          m_use = m_cand;
+          scale = ex2(m_run - m_cand);
+          need = true;
+        }
+        bool pv_done = c == 0;
+        auto wait_pv = [&]() {
+          if (!pv_done) {
+            mbar_wait(&S.o_full[hh], (c - 1) & 1);
+            tc_after_sync();
+            pv_done = true;
+          }
+        };
+        if (__any_sync(0xffffffffu, need)) {   // the pair decides identically
+          wait_pv();
+#pragma unroll
+          for (int cq = 0; cq < kOCols; cq += 16) {
+            uint32_t r[16];
+            tmem_ld16_nowait(tO + oc0 + cq, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
+            tmem_st16(tO + oc0 + cq, r);
+          }
+          if (half == 0) {
+            uint32_t rl[1];
+            tmem_ld_cols<1>(tO + DH, rl);
+            tmem_wait_ld();
+            rl[0] = __float_as_uint(__uint_as_float(rl[0]) * scale);
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tO + DH),
+                         "r"(rl[0])
+                         : "memory");
+          }
+        }
+        m_run = m_use;
+        if (tid == 0) trace(trp, c, 11);
+        const float nbv = m_use == kNegInf ? 0.f : -m_use;
+#define LSRM_SPLIT_PIECE(arr, pc)                                              \
+  {                                                                            \
+    uint32_t w[16];                                                            \
+    if ((live >> (2 * (pc))) & 3u) {                                           \
+      exp16(arr, sl2, ((visb >> (2 * (pc))) & 1u) ? nbv : kNegInf, w);         \
+      exp16(arr + 16, sl2, ((visb >> (2 * (pc) + 1)) & 1u) ? nbv : kNegInf, w + 8); \
+    } else {                                                                   \
+      zero8(w);                                                                \
+      zero8(w + 8);                                                            \
+    }                                                                          \
+    wait_pv();                                                                 \
+    tmem_st16(tP + 16 * (pc), w);                                              \
+  }
+#if LSRM_SPLIT_RELOAD
+        if (has0) {
+          tmem_ld32(tS + HCols::kS + 32 * pcb, sa);
+          tmem_wait_ld();
+          if (!has1) {
+            tc_before_sync();
+            mbar_arrive(&S.s_free[hh]);
+          }
+          LSRM_SPLIT_PIECE(sa, pcb)
+        }
+        if (has1) {
+          tmem_ld32(tS + HCols::kS + 32 * (pcb + 1), sa);
+          tmem_wait_ld();
+          tc_before_sync();
+          mbar_arrive(&S.s_free[hh]);
+          LSRM_SPLIT_PIECE(sa, pcb + 1)
+        }
+        if (!has0) {
+          tc_before_sync();
+          mbar_arrive(&S.s_free[hh]);
+        }
+#else
+        if (has0) LSRM_SPLIT_PIECE(sa, pcb)
+        if (has1) LSRM_SPLIT_PIECE(sb, pcb + 1)
+#endif
+#undef LSRM_SPLIT_PIECE
+        wait_pv();   // PV(c-1) read O before this chunk's epilogue may run
+      } else if (two_pass) {
 // straight-line group maxima; groups this row does not see are not selected
 #define LSRM_MAX(arr, off, gi)                                  \
   {                                                             \
@@ -1168,7 +1302,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           const __nv_bfloat16* gp = PU.gl + tok * PU.ld_gl + PU.gcol0 + (int64_t)br * d_model +
                                     head * DH;
 #pragma unroll
-          for (int c0 = 0; c0 < DH; c0 += 8) cp_async16(gate_s + c0, gp + c0, 16u);
+          for (int cq = 0; cq < kOCols; cq += 8) cp_async16(gate_s + oc0 + cq, gp + oc0 + cq, 16u);
         }
         br_pend = br;
         use_pend = use_c;

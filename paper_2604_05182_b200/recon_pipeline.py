@@ -137,12 +137,12 @@ def build_sparse_context(part_vol: BlockPartition, part_img: BlockPartition,
 # fused row / element steps (csrc/block.cu)
 
 
-def _add_ln(a, b, norm: NormParams, out_dtype=torch.float32):
+def _add_ln(a, b, norm: NormParams, out_dtype=torch.float32, exact=True):
     """sum = f32(a + b), LayerNorm(sum) -> (sum f32, normalised)."""
     n, d = a.shape
     s = D.empty((n, d), torch.float32)
     y = D.empty((n, d), out_dtype)
-    call("lsrm_add_layer_norm", a.data_ptr(), D.ptr(b), int(b is not None and
+    call("lsrm_add_layer_norm", int(exact), a.data_ptr(), D.ptr(b), int(b is not None and
                                                            b.dtype == torch.bfloat16),
          n, d, D.weight(norm.gamma).data_ptr(), D.weight(norm.beta).data_ptr(), LN_EPS, s.data_ptr(),
          int(out_dtype == torch.bfloat16), y.data_ptr(), D.stream())
@@ -257,8 +257,8 @@ class SparseBlockEngine:
 
     def forward(self, x, y, x_inj, y_inj):
         w, L = self.w, self.layer
-        xe, xh = _add_ln(x, x_inj, w.ln_attn_x, torch.bfloat16)
-        ye, yh = _add_ln(y, y_inj, w.ln_attn_y, torch.bfloat16)
+        xe, xh = _add_ln(x, x_inj, w.ln_attn_x, torch.bfloat16, exact=False)
+        ye, yh = _add_ln(y, y_inj, w.ln_attn_y, torch.bfloat16, exact=False)
         outs = L.forward(xh, yh)
         res = []
         for s, e, gb, us, uc, ln, k1, k2, ffn in (
@@ -270,8 +270,13 @@ class SparseBlockEngine:
                                  torch.bfloat16)
             t = _ops.gemm(h, self.bf[k1])
             _bias_act(0, t, D.weight(ffn.b1), 1)
-            u = _ops.gemm(t, self.bf[k2], out_dtype=torch.float32)
-            res.append(_bias_act(0, u, D.weight(ffn.b2), 0, residual=x1))
+            # second FFN GEMM with its bias and the residual in the epilogue
+            u = D.empty(tuple(x1.shape), torch.float32)
+            w2 = self.bf[k2]
+            call("lsrm_gemm_bias_res_f32", t.shape[0], w2.shape[1], t.shape[1], t.data_ptr(),
+                 t.stride(0), w2.data_ptr(), w2.stride(0), D.weight(ffn.b2).data_ptr(),
+                 x1.data_ptr(), x1.stride(0), u.data_ptr(), u.stride(0), D.stream())
+            res.append(u)
         return tuple(res)
 
 
