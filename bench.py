@@ -380,6 +380,8 @@ WORKLOAD_DESC = {
     "c4": "C4 SP stress: C3 + 12 fully occupied 8^3 volume blocks (skewed per-block sparsity), "
           "heads 32/2/32, d=1024, one layer = 4 gated NSA uses",
     "c1": "C1 tiny: 4 views, S_vol=32, S_img=96, heads 8/1/8, d=64",
+    "c5": "C5 scaled context: 18 views, S_vol=408, S_img=288 (fixture scene, masks and points "
+          "generated on the GPU), heads 32/2/32, d=1024, one layer = 4 gated NSA uses",
 }
 
 
@@ -539,7 +541,7 @@ def main():
     ap.add_argument("--warmup-ref", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches")
-    ap.add_argument("--workload", default=None, choices=["c1", "c3", "c4"],
+    ap.add_argument("--workload", default=None, choices=["c1", "c3", "c4", "c5"],
                     help="default: c3 at N=1, c4 (skewed) under torchrun N>1")
     ap.add_argument("--sp-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = host-staged exchange, lets ranks share one GPU (tests)")

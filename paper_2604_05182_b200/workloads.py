@@ -22,12 +22,20 @@ from .tokenizer import init_pos_embed
 FIXTURE_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                            "tests", "golden")
 
-# BASELINE.json configs: C1 tiny (desk heads, fp32), C3 fine stage, C4 skewed
+# BASELINE.json configs: C1 tiny (desk heads, fp32), C3 fine stage, C4 skewed,
+# C5 scaled context (~20x object tokens, 18 views; "raise the
+# object radius or S with the same recipe"; generated on the GPU)
 CONFIGS = {
     "c1": {"params": (8, 1, 8), "dtype": "f32"},
     "c3": {"params": (32, 2, 32), "dtype": "bf16"},
     "c4": {"params": (32, 2, 32), "dtype": "bf16"},
+    "c5": {"params": (32, 2, 32), "dtype": "bf16", "views": 18, "s_vol": 408, "s_img": 288},
 }
+# the fixture scene (tests/test_acceptance.py:299-300 of the reference)
+SCENE = {"kind": "union", "parts": [
+    {"kind": "sphere", "center": [0.42, 0.5, 0.55], "radius": 0.18},
+    {"kind": "box", "center": [0.6, 0.45, 0.4], "half_sizes": [0.12, 0.12, 0.12]}]}
+CUBE_CENTER = np.array([0.5, 0.5, 0.5])
 USE_TAGS = {"v2v": (3, "xs"), "v2i": (2, "xc"), "i2i": (3, "ys"), "i2v": (2, "yc")}
 
 
@@ -47,7 +55,70 @@ class Workload:
     n_img: int
 
 
+def look_at_camera(eye, target, image_size, focal, world_up=(0.0, 0.0, 1.0)):
+    """(K, R, t, (W, H)) of a pinhole camera at eye looking at target,
+    principal point at the image center (`camera_geometry.py:110-126`)."""
+    eye = np.asarray(eye, dtype=np.float64)
+    fwd = np.asarray(target, dtype=np.float64) - eye
+    fwd = fwd / np.linalg.norm(fwd)
+    up = np.asarray(world_up, dtype=np.float64)
+    if abs(np.dot(fwd, up)) > 0.999:
+        up = np.array([1.0, 0.0, 0.0])
+    right = np.cross(fwd, up)
+    right /= np.linalg.norm(right)
+    down = np.cross(fwd, right)
+    R = np.stack([right, down, fwd], axis=1)
+    W, H = image_size
+    K = np.array([[focal, 0.0, W / 2.0], [0.0, focal, H / 2.0], [0.0, 0.0, 1.0]])
+    return (K, R, eye, (int(W), int(H)))
+
+
+def orbit_cameras(count, radius, elevation_deg, image_size, fov_deg=50.0, phase=0.0):
+    """Ring of cameras around the cube center (`camera_geometry.py:129-144`)."""
+    import math
+    focal = 0.5 * image_size[0] / math.tan(math.radians(fov_deg) / 2.0)
+    el = math.radians(elevation_deg)
+    cams = []
+    for k in range(count):
+        az = phase + 2.0 * math.pi * k / count
+        eye = CUBE_CENTER + radius * np.array([math.cos(az) * math.cos(el),
+                                               math.sin(az) * math.cos(el), math.sin(el)])
+        cams.append(look_at_camera(eye, CUBE_CENTER, image_size, focal))
+    return cams
+
+
+def generate_workload(name: str, views: int, s_vol: int, s_img: int) -> Workload:
+    """The fixture recipe (tests/golden/make_golden.py) on the GPU: orbit
+    cameras, the informative-voxel mask, silhouettes -> foreground patches,
+    compaction and the image-token surface points, all with this package's
+    kernels (bit-exact with the reference for masks and coords)."""
+    from . import _dev as D
+    from .block_routing import LAPLACE_BETA, image_token_coords
+    from .camera_geometry import silhouettes
+    from .tokenizer import foreground_patch_mask, informative_voxel_mask, upsample_select_tokens
+    cams = orbit_cameras(views, 1.7, 20.0, (8 * s_img, 8 * s_img))
+    vol_mask = informative_voxel_mask(SCENE, s_vol)
+    img_mask = foreground_patch_mask(silhouettes(SCENE, cams, as_device=True))
+    img_mask = D.host(img_mask) if D.is_device(img_mask) else img_mask
+    fv = 6 if s_vol % 6 == 0 else 4
+    fi = 3
+    d = 8   # features do not affect coords; image points depend on coords only
+    g = stream(0, "hot")
+    x_d = g.standard_normal(((s_vol // fv) ** 3, d)).astype(np.float32)
+    y_d = g.standard_normal((views * (s_img // fi) ** 2, d)).astype(np.float32)
+    x_up, y_up = upsample_select_tokens(D.dev(x_d), D.dev(y_d), vol_mask, img_mask,
+                                        init_pos_embed(6, 3, s_vol, d, label="v"),
+                                        init_pos_embed(6, 2, s_img, d, label="i"), fv, fi)
+    ic = image_token_coords(y_up, cams, SCENE, LAPLACE_BETA)
+    return Workload(name, views, s_vol, s_img, fv, fi, np.asarray(vol_mask, bool),
+                    np.asarray(img_mask, bool), [c[:3] for c in cams], ic.points,
+                    int(x_up.count), int(y_up.count))
+
+
 def load_workload(name: str) -> Workload:
+    if name in CONFIGS and "views" in CONFIGS[name]:
+        c = CONFIGS[name]
+        return generate_workload(name, c["views"], c["s_vol"], c["s_img"])
     z = np.load(os.path.join(FIXTURE_DIR, f"workload_{name}.npz"))
     s, si, v = int(z["s_vol"]), int(z["s_img"]), int(z["views"])
     vm = np.unpackbits(z["vol_mask"])[: s ** 3].astype(bool).reshape(s, s, s)
