@@ -270,6 +270,10 @@ def run_gpu(args):
     clocks = sampler.stop()
     # -- end to end through the public host API (pinned host buffers)
     e2e_ms, h2d, d2h = layer.time_host_path(inst.x_hat, inst.y_hat, steps=args.steps)
+    pcie = pcie_bandwidth()
+    # e2e roofline: the duplex copy of one step's inputs and outputs
+    e2e_bound_ms = max(h2d / (pcie["duplex_h2d_gbps"] * 1e9),
+                       d2h / (pcie["duplex_d2h_gbps"] * 1e9)) * 1e3
     peaks, src = load_peaks()
     attn_flops = sum(sum(v.values()) for v in layer.engine.attention_flops().values())
     attn_ms = brk["attention_ms"]
@@ -311,11 +315,49 @@ def run_gpu(args):
         "sparse_block": block,
         "cpu_baseline": cpu,
         "e2e": {"value": n_tok / (e2e_ms * 1e-3), "unit": "tokens/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "roofline": {"bound": "pcie", "pcie_measured": pcie,
+                             "bound_ms": e2e_bound_ms, "frac": e2e_bound_ms / e2e_ms}},
         "gpu_launches": launches,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
+
+
+def pcie_bandwidth(nbytes=256 << 20, reps=3):
+    """Pinned host <-> device copy bandwidth on this box (GB/s): H2D alone,
+    D2H alone, and both directions at once (the e2e pipeline overlaps them).
+    The e2e roofline is the slower direction of the duplex copy."""
+    import torch
+    h_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn_list):
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            evs = []
+            for s, fn in fn_list:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(s):
+                    a.record(s)
+                    fn()
+                    b.record(s)
+                evs.append((a, b))
+            torch.cuda.synchronize()
+            ms = [a.elapsed_time(b) for a, b in evs]
+            best = ms if best is None or max(ms) < max(best) else best
+        return best
+    h2d = timed([(s1, lambda: d_a.copy_(h_in, non_blocking=True))])[0]
+    d2h = timed([(s1, lambda: h_out.copy_(d_b, non_blocking=True))])[0]
+    both = timed([(s1, lambda: d_a.copy_(h_in, non_blocking=True)),
+                  (s2, lambda: h_out.copy_(d_b, non_blocking=True))])
+    gb = nbytes / 1e9
+    return {"h2d_gbps": gb / (h2d * 1e-3), "d2h_gbps": gb / (d2h * 1e-3),
+            "duplex_h2d_gbps": gb / (both[0] * 1e-3), "duplex_d2h_gbps": gb / (both[1] * 1e-3)}
 
 
 def time_sparse_block(inst, n_tok, steps):
