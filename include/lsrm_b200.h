@@ -396,6 +396,17 @@ int lsrm_attention_bwd_f32(int mode, const float* q, const float* dO, const floa
                            const int32_t* count, int kmax_rows, const int32_t* own_row,
                            int n_slices, float* dq, float* dk, float* dv, void* workspace,
                            size_t ws_bytes, void* stream);
+/* Tensor-core variant (mma.sync bf16, fp32 accumulation), same contract and
+ * workspace: bf16 copies of q, dO and k, v feed the MMAs; dO and O in f32
+ * give D = rowsum(dO * O); lse_in (optional, from lsrm_attention_fwd_mma)
+ * skips the statistics pass.  head_dim in {16, 32, 64}, hq / hkv <= 16. */
+int lsrm_attention_bwd_mma(int mode, const void* q_bf16, const void* dO_bf16, const float* dO,
+                           const float* O, const float* lse_in, int64_t nq, int hq, int hkv, int dh,
+                           const void* k_bf16, const void* v_bf16, int64_t nk,
+                           const int64_t* block_offsets, int n_rows, int max_row_keys,
+                           const int32_t* rows, const int32_t* count, int kmax_rows,
+                           const int32_t* own_row, int n_slices, float* dq, float* dk,
+                           float* dv, void* workspace, size_t ws_bytes, void* stream);
 /* merged = sum_b sigmoid(gl[:, b*d:(b+1)*d] + gb[b*d:]) * o_b:
  * do_b = dM g_b,  dz[:, b*d + c] = dM o_b g_b (1 - g_b)   (dz [n, n_gates*d]). */
 int lsrm_gate_merge_bwd_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,
@@ -409,10 +420,19 @@ int lsrm_res_block_bwd_f32(const float* x, int64_t n, int width, const float* w1
                            const float* b1, const float* w2, const float* dcmp,
                            const int32_t* row_of_token, const int64_t* occupancy, float* dx,
                            float* dr_out, float* dz1_out, float* h_out, void* stream);
-/* Row-major fp32 C[m,n] = alpha op(A) op(B) + beta C (op = transpose if trans_*). */
+/* Row-major fp32 C[m,n] = alpha op(A) op(B) + beta C (op = transpose if
+ * trans_*); tf32 = 1 allows TF32 tensor cores (the fast training mode). */
 int lsrm_gemm_f32_ex(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, float alpha,
                      const float* a, int64_t lda, const float* b, int64_t ldb, float beta,
-                     float* c, int64_t ldc, void* stream);
+                     float* c, int64_t ldc, int tf32, void* stream);
+/* Training forward of one branch on tensor cores (mma.sync bf16): out f32
+ * [nq, hq, dh] and lse [nq, hq] (natural log) for the backward.  Key-set
+ * arguments as lsrm_attention_f32. */
+int lsrm_attention_fwd_mma(int mode, const void* q_bf16, int64_t nq, int hq, int hkv, int dh,
+                           const void* k_bf16, const void* v_bf16, int64_t nk,
+                           const int64_t* block_offsets, const int32_t* rows,
+                           const int32_t* count, int kmax_rows, const int32_t* own_row,
+                           float* out, float* lse, void* stream);
 
 /* ---- feature decode around the sparse stage (recon_pipeline.py:209-348) --
  * f64 arithmetic, the reference's f32 rounding points, NumPy operation order.

@@ -73,12 +73,17 @@ SIGNATURES = {
     "lsrm_attention_bwd_workspace": (SZ, [I64, I32, I64, I32, I32, I32]),
     "lsrm_attention_bwd_f32": (I32, [I32, P, P, P, I64, I32, I32, I32, P, P, I64, P, I32, I32,
                                      P, P, I32, P, I32, P, P, P, P, SZ, P]),
+    "lsrm_attention_bwd_mma": (I32, [I32, P, P, P, P, P, I64, I32, I32, I32, P, P, I64, P, I32, I32,
+                                     P, P, I32, P, I32, P, P, P, P, SZ, P]),
     "lsrm_gate_merge_bwd_f32": (I32, [P, I64, P, I32, P, P, P, P, I64, I32, P, P, P, P, P]),
     "lsrm_res_block_bwd_f32": (I32, [P, I64, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "lsrm_decode_scatter": (I32, [P, I32, I32, I32, P, P]),
     "lsrm_sparse_features": (I32, [P, P, I64, I32, I32, I64, P, P, P]),
     "lsrm_decode_points": (I32, [P, I32, P, P, I32, I32, P, I64, P, I32, I32, P, P, P, P]),
-    "lsrm_gemm_f32_ex": (I32, [I32, I32, I64, I64, I64, F32, P, I64, P, I64, F32, P, I64, P]),
+    "lsrm_gemm_f32_ex": (I32, [I32, I32, I64, I64, I64, F32, P, I64, P, I64, F32, P, I64, I32,
+                               P]),
+    "lsrm_attention_fwd_mma": (I32, [I32, P, I64, I32, I32, I32, P, P, I64, P, P, P, I32, P, P, P,
+                                     P]),
 }
 
 _lib = None

@@ -63,8 +63,9 @@ def layer_norm(x: torch.Tensor, gamma, beta, eps=1e-5, out_dtype=None) -> torch.
 
 
 def gemm_ex(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, out=None,
-            beta=0.0, alpha=1.0) -> torch.Tensor:
-    """fp32 out = alpha op(a) @ op(b) + beta out (op = transpose when asked)."""
+            beta=0.0, alpha=1.0, tf32=False) -> torch.Tensor:
+    """fp32 out = alpha op(a) @ op(b) + beta out (op = transpose when asked;
+    tf32 allows TF32 tensor cores)."""
     m, k = (a.shape[1], a.shape[0]) if trans_a else a.shape
     k2, n = (b.shape[1], b.shape[0]) if trans_b else b.shape
     assert k == k2 and a.stride(1) == 1 and b.stride(1) == 1
@@ -74,5 +75,5 @@ def gemm_ex(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, out=
         beta = 0.0
     call("lsrm_gemm_f32_ex", int(trans_a), int(trans_b), m, n, k, float(alpha), a.data_ptr(),
          a.stride(0), b.data_ptr(), b.stride(0), float(beta), out.data_ptr(), out.stride(0),
-         D.stream())
+         int(tf32), D.stream())
     return out

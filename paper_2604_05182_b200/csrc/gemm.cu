@@ -159,7 +159,8 @@ extern "C" int lsrm_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void*
 // the stored A/B).  The backward's weight / input gradients.
 extern "C" int lsrm_gemm_f32_ex(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
                                 float alpha, const float* a, int64_t lda, const float* b,
-                                int64_t ldb, float beta, float* c, int64_t ldc, void* stream) {
+                                int64_t ldb, float beta, float* c, int64_t ldc, int tf32,
+                                void* stream) {
   if (m == 0 || n == 0) return LSRM_OK;
   cublasHandle_t h;
   int rc = get_handle(&h);
@@ -169,8 +170,10 @@ extern "C" int lsrm_gemm_f32_ex(int trans_a, int trans_b, int64_t m, int64_t n, 
   // its own transpose in column-major, so the flags carry over unchanged.
   const cublasOperation_t ob = trans_b ? CUBLAS_OP_T : CUBLAS_OP_N;
   const cublasOperation_t oa = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;
+  if (tf32) cublasSetMathMode(h, CUBLAS_TF32_TENSOR_OP_MATH);
   cublasStatus_t s = cublasSgemm(h, ob, oa, (int)n, (int)m, (int)k, &alpha, b, (int)ldb, a,
                                  (int)lda, &beta, c, (int)ldc);
+  if (tf32) cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
   if (s != CUBLAS_STATUS_SUCCESS) return set_error(LSRM_E_CUDA, "cublas gemm_ex failed: %d", (int)s);
   return LSRM_OK;
 }

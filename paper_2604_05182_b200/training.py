@@ -44,6 +44,12 @@ class _Spec:
     part_kv: BlockPartition
     rows: torch.Tensor
     count: torch.Tensor
+    fast: bool = False    # tensor-core (bf16) attention backward
+
+
+def _mma_ok(spec: _Spec) -> bool:
+    p = spec.params
+    return spec.fast and p.head_dim in (16, 32, 64) and p.n_q_heads // p.n_kv_heads <= 16
 
 
 def _forward(spec: _Spec, x, kv, P):
@@ -53,32 +59,53 @@ def _forward(spec: _Spec, x, kv, P):
     hq, hkv, dh = p.n_q_heads, p.n_kv_heads, p.head_dim
     width = hkv * dh
     part = spec.part_kv
-    q = _ops.gemm(x, P["w_q"])
-    k = _ops.gemm(kv, P["w_k"])
-    v = _ops.gemm(kv, P["w_v"])
+    fast = _mma_ok(spec)
+    mm = lambda a, b: _ops.gemm_ex(a, b, tf32=fast)   # noqa: E731
+    q = mm(x, P["w_q"])
+    k = mm(kv, P["w_k"])
+    v = mm(kv, P["w_v"])
     ck = [P[f"ck_{s}"] for s in ("w1", "b1", "w2", "b2")]
     cv = [P[f"cv_{s}"] for s in ("w1", "b1", "w2", "b2")]
     kc = compress_rows(k, width, m, width, ck, part)
     vc = compress_rows(v, width, m, width, cv, part)
     tok, offs = part.dev("block_token_ids"), part.dev("block_offsets")
     k_bm, v_bm = _ops.gather_rows(k, tok), _ops.gather_rows(v, tok)
-    q3 = q.view(n, hq, dh)
     B = part.n_occupied
-    outs = [_attn(0, q3, kc.view(B, hkv, dh), vc.view(B, hkv, dh), p),
-            _attn(1, q3, k_bm.view(m, hkv, dh), v_bm.view(m, hkv, dh), p, offs=offs,
-                  rows=spec.rows, count=spec.count)]
-    if spec.n_gates == 3:
-        outs.append(_attn(2, q3, k_bm.view(m, hkv, dh), v_bm.view(m, hkv, dh), p, offs=offs,
-                          own_row=spec.part_q.dev("row_of_token")))
-    logits = _ops.gemm(x, P["gate_w"])
+    own = spec.part_q.dev("row_of_token") if spec.n_gates == 3 else None
+    saved = dict(x=x, kv=kv, q=q, k=k, v=v, kc=kc, vc=vc, k_bm=k_bm, v_bm=v_bm, ck=ck, cv=cv)
+    if fast:
+        # branches on tensor cores (bf16 operands); lse kept for the backward
+        bf = {name: _ops.cast(saved[name], torch.bfloat16)
+              for name in ("q", "kc", "vc", "k_bm", "v_bm")}
+        outs, lses = [], []
+        for mode, kn, vn, nk in ((0, "kc", "vc", B), (1, "k_bm", "v_bm", m),
+                                 (2, "k_bm", "v_bm", m))[:spec.n_gates]:
+            o_b = D.empty((n, hq, dh), torch.float32)
+            lse = D.empty((n, hq), torch.float32)
+            call("lsrm_attention_fwd_mma", mode, bf["q"].data_ptr(), n, hq, hkv, dh,
+                 bf[kn].data_ptr(), bf[vn].data_ptr(), nk, offs.data_ptr() if mode else None,
+                 D.ptr(spec.rows) if mode == 1 else None,
+                 D.ptr(spec.count) if mode == 1 else None, int(spec.rows.shape[1]),
+                 D.ptr(own) if mode == 2 else None, o_b.data_ptr(), lse.data_ptr(), D.stream())
+            outs.append(o_b)
+            lses.append(lse)
+        saved.update(bf=bf, lse=lses)
+    else:
+        q3 = q.view(n, hq, dh)
+        outs = [_attn(0, q3, kc.view(B, hkv, dh), vc.view(B, hkv, dh), p),
+                _attn(1, q3, k_bm.view(m, hkv, dh), v_bm.view(m, hkv, dh), p, offs=offs,
+                      rows=spec.rows, count=spec.count)]
+        if spec.n_gates == 3:
+            outs.append(_attn(2, q3, k_bm.view(m, hkv, dh), v_bm.view(m, hkv, dh), p,
+                              offs=offs, own_row=own))
+    logits = mm(x, P["gate_w"])
     merged = D.empty((n, d), torch.float32)
     o = [t.view(n, d) for t in outs] + [None] * (3 - len(outs))
     call("lsrm_gated_merge_f32", logits.data_ptr(), logits.stride(0), P["gate_b"].data_ptr(),
          spec.n_gates, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]), n, d, merged.data_ptr(),
          D.stream())
-    out = _ops.gemm(merged, P["w_o"])
-    saved = dict(x=x, kv=kv, q=q, k=k, v=v, kc=kc, vc=vc, k_bm=k_bm, v_bm=v_bm, outs=o,
-                 logits=logits, merged=merged, ck=ck, cv=cv)
+    out = mm(merged, P["w_o"])
+    saved.update(outs=o, logits=logits, merged=merged)
     return out, saved
 
 
@@ -100,9 +127,13 @@ def _backward(spec: _Spec, P, s, dout):
     B = part.n_occupied
     st = D.stream()
     g = {}
+    fast = _mma_ok(spec)
+
+    def gx(a, b, **kw):
+        return _ops.gemm_ex(a, b, tf32=fast, **kw)
     # out = merged W_o
-    dmerged = _ops.gemm_ex(dout, P["w_o"], trans_b=True)
-    g["w_o"] = _ops.gemm_ex(s["merged"], dout, trans_a=True)
+    dmerged = gx(dout, P["w_o"], trans_b=True)
+    g["w_o"] = gx(s["merged"], dout, trans_a=True)
     # gated merge
     do = [D.empty((n, d), torch.float32) for _ in range(ng)] + [None] * (3 - ng)
     dz = D.empty((n, ng * d), torch.float32)
@@ -110,9 +141,9 @@ def _backward(spec: _Spec, P, s, dout):
     call("lsrm_gate_merge_bwd_f32", s["logits"].data_ptr(), s["logits"].stride(0),
          P["gate_b"].data_ptr(), ng, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]),
          dmerged.data_ptr(), n, d, D.ptr(do[0]), D.ptr(do[1]), D.ptr(do[2]), dz.data_ptr(), st)
-    g["gate_w"] = _ops.gemm_ex(s["x"], dz, trans_a=True)
+    g["gate_w"] = gx(s["x"], dz, trans_a=True)
     g["gate_b"] = _colsum(dz)
-    dx = _ops.gemm_ex(dz, P["gate_w"], trans_b=True)
+    dx = gx(dz, P["gate_w"], trans_b=True)
     # branches
     dq = D.zeros((n, d), torch.float32)
     dkc, dvc = D.zeros((B, width), torch.float32), D.zeros((B, width), torch.float32)
@@ -122,20 +153,30 @@ def _backward(spec: _Spec, P, s, dout):
 
     max_occ = int(np.max(part.occupancy)) if B else 1
 
+    use_mma = fast
+    bf = s.get("bf")
+
     def bwd(mode, b, k, v, nk, dk, dv, rows=None, count=None, own=None):
         # cmp has few keys and every query: slice the queries for parallelism
         n_slices = max(1, min(64, n // 256)) if mode == 0 else max(1, min(4, n // 1024))
         ws_bytes = lib().lsrm_attention_bwd_workspace(n, hq, nk, hkv, dh, n_slices)
         ws = D.empty((ws_bytes,), torch.uint8)
-        call("lsrm_attention_bwd_f32", mode, s["q"].data_ptr(), do[b].data_ptr(),
-             o[b].data_ptr(), n, hq, hkv, dh, k.data_ptr(), v.data_ptr(), nk,
-             offs.data_ptr() if mode else None, B, max_occ, D.ptr(rows), D.ptr(count), kmax,
-             D.ptr(own), n_slices, dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr(),
-             ws_bytes, st)
-    bwd(0, 0, s["kc"], s["vc"], B, dkc, dvc)
-    bwd(1, 1, s["k_bm"], s["v_bm"], m, dk_bm, dv_bm, rows=spec.rows, count=spec.count)
+        common = (nk, offs.data_ptr() if mode else None, B, max_occ, D.ptr(rows), D.ptr(count),
+                  kmax, D.ptr(own), n_slices, dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                  ws.data_ptr(), ws_bytes, st)
+        if use_mma:
+            dob = _ops.cast(do[b], torch.bfloat16)
+            call("lsrm_attention_bwd_mma", mode, bf["q"].data_ptr(), dob.data_ptr(),
+                 do[b].data_ptr(), o[b].data_ptr(), s["lse"][b].data_ptr(), n, hq, hkv, dh,
+                 bf[k].data_ptr(),
+                 bf[v].data_ptr(), *common)
+        else:
+            call("lsrm_attention_bwd_f32", mode, s["q"].data_ptr(), do[b].data_ptr(),
+                 o[b].data_ptr(), n, hq, hkv, dh, s[k].data_ptr(), s[v].data_ptr(), *common)
+    bwd(0, 0, "kc", "vc", B, dkc, dvc)
+    bwd(1, 1, "k_bm", "v_bm", m, dk_bm, dv_bm, rows=spec.rows, count=spec.count)
     if ng == 3:
-        bwd(2, 2, s["k_bm"], s["v_bm"], m, dk_bm, dv_bm, own=spec.part_q.dev("row_of_token"))
+        bwd(2, 2, "k_bm", "v_bm", m, dk_bm, dv_bm, own=spec.part_q.dev("row_of_token"))
     tok = part.dev("block_token_ids")
     dk = _ops.scatter_rows(dk_bm, tok, D.empty((m, width), torch.float32))
     dv = _ops.scatter_rows(dv_bm, tok, D.empty((m, width), torch.float32))
@@ -148,17 +189,17 @@ def _backward(spec: _Spec, P, s, dout):
         call("lsrm_res_block_bwd_f32", t.data_ptr(), m, width, cw[0].data_ptr(),
              cw[1].data_ptr(), cw[2].data_ptr(), dc.data_ptr(), row_of.data_ptr(),
              occ.data_ptr(), dt.data_ptr(), dr.data_ptr(), dz1.data_ptr(), h.data_ptr(), st)
-        g[f"{tag}_w1"] = _ops.gemm_ex(t, dz1, trans_a=True)
+        g[f"{tag}_w1"] = gx(t, dz1, trans_a=True)
         g[f"{tag}_b1"] = _colsum(dz1)
-        g[f"{tag}_w2"] = _ops.gemm_ex(h, dr, trans_a=True)
+        g[f"{tag}_w2"] = gx(h, dr, trans_a=True)
         g[f"{tag}_b2"] = _colsum(dr)
     # projections
-    g["w_k"] = _ops.gemm_ex(s["kv"], dk, trans_a=True)
-    g["w_v"] = _ops.gemm_ex(s["kv"], dv, trans_a=True)
-    dkv = _ops.gemm_ex(dk, P["w_k"], trans_b=True)
-    _ops.gemm_ex(dv, P["w_v"], trans_b=True, out=dkv, beta=1.0)
-    g["w_q"] = _ops.gemm_ex(s["x"], dq, trans_a=True)
-    _ops.gemm_ex(dq, P["w_q"], trans_b=True, out=dx, beta=1.0)
+    g["w_k"] = gx(s["kv"], dk, trans_a=True)
+    g["w_v"] = gx(s["kv"], dv, trans_a=True)
+    dkv = gx(dk, P["w_k"], trans_b=True)
+    gx(dv, P["w_v"], trans_b=True, out=dkv, beta=1.0)
+    g["w_q"] = gx(s["x"], dq, trans_a=True)
+    gx(dq, P["w_q"], trans_b=True, out=dx, beta=1.0)
     g["x"], g["kv"] = dx, dkv
     return g
 
@@ -183,10 +224,11 @@ class NsaUseModule(torch.nn.Module):
     (`nsa_attention.py:239-263`); compression ResBlocks are ck_* / cv_*."""
 
     def __init__(self, params: AttentionParams, n_gates: int, weights: NsaWeights = None,
-                 seed: int = 0):
+                 seed: int = 0, fast_backward: bool = False):
         super().__init__()
         require(n_gates in (2, 3), "n_gates must be 2 (cross) or 3 (self)")
         self.params, self.n_gates = params, n_gates
+        self.fast_backward = fast_backward
         if weights is None:
             from .nsa_attention import init_nsa_weights
             weights = init_nsa_weights(seed, params, n_gates, "train")
@@ -206,7 +248,7 @@ class NsaUseModule(torch.nn.Module):
             rows, count = selection_rows(sel, part_kv)
             own = part_kv.block_of_token if self.n_gates == 3 else None
             rows, count, _, _, _ = resolve_rows(rows, count, part_kv, own, True)
-        spec = _Spec(self.params, self.n_gates, part_q, part_kv, rows, count)
+        spec = _Spec(self.params, self.n_gates, part_q, part_kv, rows, count, self.fast_backward)
         return _NsaUseFn.apply(spec, x, kv, *(getattr(self, nm) for nm in PARAM_NAMES))
 
 
@@ -245,10 +287,12 @@ class NsaLayerModule(torch.nn.Module):
     v2v and v2i read the volume stream x as queries, i2i and i2v the image
     stream y; returns each use's output."""
 
-    def __init__(self, params: AttentionParams, weights: dict = None, seed: int = 0):
+    def __init__(self, params: AttentionParams, weights: dict = None, seed: int = 0,
+                 fast_backward: bool = False):
         super().__init__()
         self.uses = torch.nn.ModuleDict({
-            u: NsaUseModule(params, ng, weights=(weights or {}).get(u), seed=seed)
+            u: NsaUseModule(params, ng, weights=(weights or {}).get(u), seed=seed,
+                            fast_backward=fast_backward)
             for u, (_, _, ng) in USE_STREAMS.items()})
 
     def forward(self, x, y, part_vol, part_img, resolved: dict) -> dict:

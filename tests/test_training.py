@@ -18,6 +18,7 @@ from oracle import torch_nsa as TN
 
 GRAD_RTOL = 2e-4      # fp32 kernels vs f64 autograd, relative to max |grad|
 FWD_ATOL = 2e-5       # NumPy oracle stores f32 between steps
+FAST_RTOL = 3e-2      # tensor-core backward: bf16 q/k/v/dO/P/dS operands
 
 
 def _coords(seed, side, keep):
@@ -56,7 +57,7 @@ def _lists(seed, n, occupied, kmax=3):
                              replace=False)) for _ in range(n)]
 
 
-def _instance(seed, self_use, side=16, keep=0.03, heads=(4, 2, 8)):
+def _instance(seed, self_use, side=16, keep=0.03, heads=(4, 2, 8), wscale=0.3):
     hq, hkv, dh = heads
     params = O.AttentionParams(hq, hkv, dh)
     cq = _coords(seed, side, keep)
@@ -68,7 +69,7 @@ def _instance(seed, self_use, side=16, keep=0.03, heads=(4, 2, 8)):
     x = g.standard_normal((cq.shape[0], d)).astype(np.float32)
     kv = x if self_use else g.standard_normal((ckv.shape[0], d)).astype(np.float32)
     n_gates = 3 if self_use else 2
-    w = _weights(seed + 3, hq, hkv, dh, n_gates)
+    w = _weights(seed + 3, hq, hkv, dh, n_gates, scale=wscale)
     lists = _lists(seed + 5, cq.shape[0], pkv.occupied_ids)
     return params, cq, ckv, pq, pkv, x, kv, w, lists, n_gates
 
@@ -125,18 +126,17 @@ def _rel(a, b, floor=1e-30):
     return float((a - b).abs().max() / max(float(b.abs().max()), floor))
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("self_use", [True, False])
-def test_gpu_backward_matches_f64_autograd(cuda, self_use):
+def _gpu_vs_oracle(self_use, heads, wscale, fast):
     import paper_2604_05182_b200 as L
     from paper_2604_05182_b200.training import NsaUseModule
-    params, cq, ckv, pq, pkv, x, kv, w, lists, ng = _instance(21, self_use, keep=0.05)
+    params, cq, ckv, pq, pkv, x, kv, w, lists, ng = _instance(21, self_use, keep=0.05,
+                                                              heads=heads, wscale=wscale)
     p = L.AttentionParams(*(params.n_q_heads, params.n_kv_heads, params.head_dim))
     side = 16
     tq = L.TokenSet("volume", x, cq, (side,) * 3)
     part_q = L.partition(tq)
     part_kv = part_q if self_use else L.partition(L.TokenSet("volume", kv, ckv, (side,) * 3))
-    mod = NsaUseModule(p, ng, weights=_our_weights(w, ng))
+    mod = NsaUseModule(p, ng, weights=_our_weights(w, ng), fast_backward=fast)
     xg = torch.tensor(x, device="cuda", requires_grad=True)
     kvg = xg if self_use else torch.tensor(kv, device="cuda", requires_grad=True)
     out = mod(xg, kvg, part_q, part_kv, sel=L.Selection(lists))
@@ -150,7 +150,7 @@ def test_gpu_backward_matches_f64_autograd(cuda, self_use):
     kvt = xt if self_use else torch.tensor(kv, dtype=torch.float64, requires_grad=True)
     want = TN.nsa_use(xt, kvt, tw, params, pkv, sel, win)
     want.backward(torch.tensor(dout, dtype=torch.float64))
-    assert _rel(out, want) < 1e-5
+    assert _rel(out, want) < (FAST_RTOL if fast else 1e-5)
     pairs = [("x", xg.grad, xt.grad)]
     if not self_use:
         pairs.append(("kv", kvg.grad, kvt.grad))
@@ -163,9 +163,28 @@ def test_gpu_backward_matches_f64_autograd(cuda, self_use):
     # (the K compression's b2 shifts every compressed key of a head equally, so
     # the cmp softmax is invariant to it; fp32 leaves cancellation noise)
     floor = 1e-2 * max(float(b.abs().max()) for _, _, b in pairs)
-    errs = {n: _rel(a, b, floor) for n, a, b in pairs}
+    return {n: _rel(a, b, floor) for n, a, b in pairs}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("self_use", [True, False])
+def test_gpu_backward_matches_f64_autograd(cuda, self_use):
+    errs = _gpu_vs_oracle(self_use, (4, 2, 8), 0.3, False)
     bad = {n: e for n, e in errs.items() if e > GRAD_RTOL}
     assert not bad, bad
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("self_use", [True, False])
+@pytest.mark.parametrize("fast", [False, True])
+def test_gpu_backward_paper_heads(cuda, self_use, fast):
+    """Paper heads (32/2/32, group 16): the fp32 path within GRAD_RTOL, the
+    fast path (mma.sync bf16 branch forward/backward, TF32 GEMMs) within
+    FAST_RTOL."""
+    errs = _gpu_vs_oracle(self_use, (32, 2, 32), 0.03, fast)
+    tol = FAST_RTOL if fast else GRAD_RTOL
+    bad = {n: e for n, e in errs.items() if e > tol}
+    assert not bad, (bad, errs)
 
 
 @pytest.mark.gpu

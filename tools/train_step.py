@@ -20,13 +20,14 @@ def main():
     ap.add_argument("--workload", default="c3")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--fast", action="store_true", help="tensor-core (bf16) attention backward")
     a = ap.parse_args()
     import torch
     from paper_2604_05182_b200.layer import build_instance
     from paper_2604_05182_b200.training import NsaLayerModule, resolve_plan_rows
     inst = build_instance(a.workload)
     res = resolve_plan_rows(inst.plan_rows, inst.part_vol, inst.part_img)
-    mod = NsaLayerModule(inst.params, weights=inst.weights)
+    mod = NsaLayerModule(inst.params, weights=inst.weights, fast_backward=a.fast)
     x = torch.tensor(inst.x_hat, device="cuda", requires_grad=True)
     y = torch.tensor(inst.y_hat, device="cuda", requires_grad=True)
 
@@ -53,6 +54,7 @@ def main():
     n_tok = inst.n_vol + inst.n_img
     ms = sum(fw) / len(fw) + sum(bw) / len(bw)
     print(json.dumps({"workload": a.workload, "n_tokens": n_tok, "dtype": "f32",
+                      "backward": "mma.sync bf16" if a.fast else "fp32 CUDA cores",
                       "forward_ms": sum(fw) / len(fw), "backward_ms": sum(bw) / len(bw),
                       "step_ms": ms, "tokens_per_s": n_tok / (ms * 1e-3)}))
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
