@@ -292,6 +292,7 @@ def run_gpu(args):
                "kind": "port", "sample": desc}
     proj_flops = layer.engine.projection_flops()
     block = time_sparse_block(inst, n_tok, args.steps)
+    train = time_train_step(inst) if wl_name != "c5" else None
     line = {
         "metric": "LSRM sparse-attn layer tokens/s", "value": n_tok / (ms * 1e-3),
         "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -313,6 +314,7 @@ def run_gpu(args):
         "breakdown_ms": brk,
         "layer_tflops": (attn_flops + proj_flops) / (ms * 1e-3) / 1e12,
         "sparse_block": block,
+        "train_step": train,
         "cpu_baseline": cpu,
         "e2e": {"value": n_tok / (e2e_ms * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
@@ -322,6 +324,44 @@ def run_gpu(args):
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
+
+
+def time_train_step(inst, steps=3):
+    """Training step of the four NSA uses of one layer (SURVEY §8f rank 2,
+    BASELINE config 5's fwd+bwd): training.NsaLayerModule, fast path
+    (mma.sync bf16 branches, TF32 GEMMs), loss = sum of squares of the four
+    outputs; device events around forward and backward."""
+    import torch
+    from paper_2604_05182_b200.training import NsaLayerModule, resolve_plan_rows
+    res = resolve_plan_rows(inst.plan_rows, inst.part_vol, inst.part_img)
+    mod = NsaLayerModule(inst.params, weights=inst.weights, fast_backward=True)
+    x = torch.tensor(inst.x_hat, device="cuda", requires_grad=True)
+    y = torch.tensor(inst.y_hat, device="cuda", requires_grad=True)
+
+    def fwd():
+        outs = mod(x, y, inst.part_vol, inst.part_img, res)
+        return sum((o * o).sum() for o in outs.values())
+    fwd().backward()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    fw, bw = [], []
+    for _ in range(steps):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(st)
+        loss = fwd()
+        e[1].record(st)
+        loss.backward()
+        e[2].record(st)
+        torch.cuda.synchronize()
+        fw.append(e[0].elapsed_time(e[1]))
+        bw.append(e[1].elapsed_time(e[2]))
+    f, b = float(np.mean(fw)), float(np.mean(bw))
+    n_tok = inst.n_vol + inst.n_img
+    return {"ms_per_step": f + b, "forward_ms": f, "backward_ms": b,
+            "tokens_per_s": n_tok / ((f + b) * 1e-3),
+            "what": "fwd+bwd of the 4 gated NSA uses of one layer incl. projections, "
+                    "compression and gates (mma.sync bf16 branches, TF32 GEMMs, fp32 master "
+                    "weights)"}
 
 
 def pcie_bandwidth(nbytes=256 << 20, reps=3):

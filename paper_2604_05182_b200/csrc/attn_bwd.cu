@@ -274,9 +274,12 @@ __global__ void gate_merge_bwd_kernel(const float* __restrict__ gl, int64_t ld,
   }
 }
 
-// One CTA per token (w threads): r = x + gelu(z1) W2 + b2, z1 = x W1 + b1.
+// kTokB tokens per CTA (w threads each), W1 / W2 staged in shared memory:
+// r = x + gelu(z1) W2 + b2, z1 = x W1 + b1.
 // dr = dcmp[row(t)] / occ[row(t)];  dz1 = (dr W2^T) * gelu'(z1);
 // dx += dr + dz1 W1^T;  dR, dZ1, H (= gelu(z1)) rows for the weight GEMMs.
+constexpr int kTokB = 4;
+
 __global__ void res_block_bwd_kernel(const float* __restrict__ x, int64_t n, int w,
                                      const float* __restrict__ w1, const float* __restrict__ b1,
                                      const float* __restrict__ w2,
@@ -286,37 +289,46 @@ __global__ void res_block_bwd_kernel(const float* __restrict__ x, int64_t n, int
                                      float* __restrict__ dx, float* __restrict__ dr_out,
                                      float* __restrict__ dz1_out, float* __restrict__ h_out) {
   extern __shared__ float sm[];
-  float* xs = sm;          // [w]
-  float* drs = xs + w;     // [w]
-  float* dz1s = drs + w;   // [w]
-  const int64_t t = blockIdx.x;
-  const int o = threadIdx.x;
-  if (t >= n) return;
-  const int r = row_of_token[t];
-  const float inv = 1.f / (float)occupancy[r];
-  if (o < w) {
-    xs[o] = x[t * w + o];
-    drs[o] = dcmp[(int64_t)r * w + o] * inv;
+  const int ws = w + 1;           // padded row stride: row and column walks conflict-free
+  float* W1 = sm;                 // [w][w + 1]
+  float* W2 = W1 + w * ws;        // [w][w + 1]
+  float* xs = W2 + w * ws;        // [kTokB][w]
+  float* drs = xs + kTokB * w;    // [kTokB][w]
+  float* dz1s = drs + kTokB * w;  // [kTokB][w]
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    W1[(e / w) * ws + e % w] = w1[e];
+    W2[(e / w) * ws + e % w] = w2[e];
+  }
+  const int tl = threadIdx.x / w, o = threadIdx.x % w;
+  const int64_t t = (int64_t)blockIdx.x * kTokB + tl;
+  const bool ok = tl < kTokB && t < n;
+  if (ok) {
+    const int r = row_of_token[t];
+    xs[tl * w + o] = x[t * w + o];
+    drs[tl * w + o] = dcmp[(int64_t)r * w + o] / (float)occupancy[r];
   }
   __syncthreads();
-  if (o < w) {
+  if (ok) {
+    const float* xr = xs + tl * w;
+    const float* dr = drs + tl * w;
     float z = b1[o];
-    for (int i = 0; i < w; ++i) z = fmaf(xs[i], w1[i * w + o], z);
+    for (int i = 0; i < w; ++i) z = fmaf(xr[i], W1[i * ws + o], z);
     const float cdf = 0.5f * (1.f + erff(z * 0.70710678118654752f));
     const float pdf = 0.39894228040143268f * expf(-0.5f * z * z);
     h_out[t * w + o] = z * cdf;
     // (dr W2^T)[o] = sum_j dr[j] W2[o][j]
     float dh = 0.f;
-    for (int j = 0; j < w; ++j) dh = fmaf(drs[j], w2[o * w + j], dh);
+    for (int j = 0; j < w; ++j) dh = fmaf(dr[j], W2[o * ws + j], dh);
     const float dz = dh * (cdf + z * pdf);
-    dz1s[o] = dz;
+    dz1s[tl * w + o] = dz;
     dz1_out[t * w + o] = dz;
-    dr_out[t * w + o] = drs[o];
+    dr_out[t * w + o] = dr[o];
   }
   __syncthreads();
-  if (o < w) {
-    float acc = drs[o];
-    for (int j = 0; j < w; ++j) acc = fmaf(dz1s[j], w1[o * w + j], acc);
+  if (ok) {
+    const float* dz = dz1s + tl * w;
+    float acc = drs[tl * w + o];
+    for (int j = 0; j < w; ++j) acc = fmaf(dz[j], W1[o * ws + j], acc);
     dx[t * w + o] += acc;
   }
 }
@@ -413,10 +425,14 @@ int lsrm_res_block_bwd_f32(const float* x, int64_t n, int width, const float* w1
                            const float* b1, const float* w2, const float* dcmp,
                            const int32_t* row_of_token, const int64_t* occupancy, float* dx,
                            float* dr_out, float* dz1_out, float* h_out, void* stream) {
-  LSRM_REQUIRE(width >= 1 && width <= 1024, "res_block_bwd: width %d out of range", width);
+  LSRM_REQUIRE(width >= 1 && width <= 256, "res_block_bwd: width %d out of range", width);
   if (n == 0) return LSRM_OK;
-  const int threads = (width + 31) / 32 * 32;
-  res_block_bwd_kernel<<<(unsigned)n, threads, 3 * width * sizeof(float), as_stream(stream)>>>(
+  LSRM_REQUIRE(width * kTokB <= 1024, "res_block_bwd: width %d too large", width);
+  const size_t smem = (2 * (size_t)width * (width + 1) + 3 * kTokB * (size_t)width) * sizeof(float);
+  if (smem > 48 * 1024)
+    LSRM_CUDA(cudaFuncSetAttribute(res_block_bwd_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  res_block_bwd_kernel<<<(unsigned)ceil_div(n, kTokB), kTokB * width, smem, as_stream(stream)>>>(
       x, n, width, w1, b1, w2, dcmp, row_of_token, occupancy, dx, dr_out, dz1_out, h_out);
   LSRM_LAUNCHED();
   return LSRM_OK;
