@@ -113,9 +113,10 @@ struct KeySet {
 };
 
 constexpr int kDqWarps = 4;
+constexpr int kCmpKeys = 64;   // CMP: keys per CTA-shared K/V tile
 
 // dQ pass: warp per (query, kv head).
-template <int DH>
+template <int DH, bool CMP>
 __global__ void __launch_bounds__(32 * kDqWarps)
 dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dob,
               const float* __restrict__ dO, const float* __restrict__ O,
@@ -123,23 +124,36 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
               int hkv, const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
               float* __restrict__ dq, float* __restrict__ lse_out, float* __restrict__ dsum_out) {
   constexpr int LD = DH + 8;
-  __shared__ __align__(16) __nv_bfloat16 sm[kDqWarps][4][16 * LD];   // Q, dO, K, V tiles
+  __shared__ __align__(16) __nv_bfloat16 sm[kDqWarps][CMP ? 2 : 4][16 * LD];   // Q, dO (, K, V)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t wid = (int64_t)blockIdx.x * kDqWarps + warp;
-  if (wid >= nq * hkv) return;
-  const int64_t i = wid / hkv;
-  const int g = (int)(wid % hkv);
+  // CMP: the CTA's warps take kDqWarps queries of one kv head, which share
+  // every key (the compressed rows), so K/V tiles are loaded once per CTA
+  int64_t i;
+  int g;
+  bool valid = true;
+  if constexpr (CMP) {
+    i = (int64_t)(blockIdx.x / hkv) * kDqWarps + warp;
+    g = (int)(blockIdx.x % hkv);
+    valid = i < nq;
+  } else {
+    const int64_t wid = (int64_t)blockIdx.x * kDqWarps + warp;
+    if (wid >= nq * hkv) return;
+    i = wid / hkv;
+    g = (int)(wid % hkv);
+  }
   const int G = hq / hkv;
+  __shared__ __align__(16) __nv_bfloat16 shK[CMP ? kCmpKeys * LD : 8];
+  __shared__ __align__(16) __nv_bfloat16 shV[CMP ? kCmpKeys * LD : 8];
   __nv_bfloat16* sQ = sm[warp][0];
   __nv_bfloat16* sO = sm[warp][1];
-  __nv_bfloat16* sK = sm[warp][2];
-  __nv_bfloat16* sV = sm[warp][3];
+  __nv_bfloat16* sK = sm[warp][CMP ? 0 : 2];   // private K / V tiles (unused with CMP)
+  __nv_bfloat16* sV = sm[warp][CMP ? 1 : 3];
   const int gq = lane >> 2, cq = lane & 3;
   // Q and dO rows of the G heads (rows >= G zero)
   for (int e = lane; e < 16 * (DH / 8); e += 32) {
     const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
     uint4 vq = make_uint4(0, 0, 0, 0), vo = make_uint4(0, 0, 0, 0);
-    if (r < G) {
+    if (valid && r < G) {
       const int64_t base = ((i * hq) + (int64_t)g * G + r) * DH + c8;
       vq = *reinterpret_cast<const uint4*>(q + base);
       vo = *reinterpret_cast<const uint4*>(dob + base);
@@ -152,7 +166,7 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
 #pragma unroll
   for (int hr = 0; hr < 2; ++hr) {
     const int r = gq + 8 * hr;
-    if (r < G) {
+    if (valid && r < G) {
       const int64_t base = ((i * hq) + (int64_t)g * G + r) * DH;
       for (int c = cq; c < DH; c += 4) dsum[hr] = fmaf(dO[base + c], O[base + c], dsum[hr]);
     }
@@ -180,10 +194,47 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
     }
     __syncwarp();
   };
+  const __nv_bfloat16* tK = sK;   // current 16-key K / V tile
+  const __nv_bfloat16* tV = sV;
+  auto for_tiles = [&](auto&& body) {
+    if constexpr (CMP) {
+      for (int64_t kb = 0; kb < ks.nk; kb += kCmpKeys) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kCmpKeys * (DH / 8); e += blockDim.x) {
+          const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
+          uint4 vk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+          if (kb + r < ks.nk) {
+            const int64_t base = (kb + r) * kstride + (int64_t)g * DH + c8;
+            vk = *reinterpret_cast<const uint4*>(k + base);
+            vv = *reinterpret_cast<const uint4*>(v + base);
+          }
+          *reinterpret_cast<uint4*>(shK + r * LD + c8) = vk;
+          *reinterpret_cast<uint4*>(shV + r * LD + c8) = vv;
+        }
+        __syncthreads();
+        if (valid)
+          for (int sub = 0; sub < kCmpKeys / 16 && kb + 16 * sub < ks.nk; ++sub) {
+            tK = shK + sub * 16 * LD;
+            tV = shV + sub * 16 * LD;
+            body(kb + 16 * sub, ks.nk);
+          }
+      }
+    } else {
+      const int nr = ks.n_ranges(i);
+      for (int sidx = 0; sidx < nr; ++sidx) {
+        int64_t lo, hi;
+        ks.range(i, sidx, lo, hi);
+        for (int64_t k0 = lo; k0 < hi; k0 += 16) {
+          load_kv(k0, hi);
+          body(k0, hi);
+        }
+      }
+    }
+  };
   // S tile (16 rows x 16 keys) = Q K^T, keys past hi masked to -inf
   auto s_tile = [&](int64_t k0, int64_t hi, float (*s)[4]) {
     uint32_t bk[DH / 16][4];
-    load_b_nt<DH>(sK, lane, bk);
+    load_b_nt<DH>(tK, lane, bk);
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
@@ -199,12 +250,7 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
   };
   // pass 1: row max and sum (rows gq, gq + 8), unless the forward saved lse
   float m[2] = {-__builtin_huge_valf(), -__builtin_huge_valf()}, l[2] = {0.f, 0.f};
-  const int nr = ks.n_ranges(i);
-  for (int sidx = 0; sidx < (lse_in ? 0 : nr); ++sidx) {
-    int64_t lo, hi;
-    ks.range(i, sidx, lo, hi);
-    for (int64_t k0 = lo; k0 < hi; k0 += 16) {
-      load_kv(k0, hi);
+  if (!lse_in) for_tiles([&](int64_t k0, int64_t hi) {
       float s[2][4];
       s_tile(k0, hi, s);
 #pragma unroll
@@ -220,14 +266,13 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
         l[hr] = l[hr] * __expf(m[hr] - mn) + add;
         m[hr] = mn;
       }
-    }
-  }
+  });
   float lse[2];
 #pragma unroll
   for (int hr = 0; hr < 2; ++hr) {
     const int r = gq + 8 * hr;
     if (lse_in)
-      lse[hr] = r < G ? lse_in[i * hq + (int64_t)g * G + r] : 0.f;
+      lse[hr] = (valid && r < G) ? lse_in[i * hq + (int64_t)g * G + r] : 0.f;
     else
       lse[hr] = m[hr] + __logf(l[hr]);
   }
@@ -237,15 +282,11 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
   for (int nt = 0; nt < DH / 8; ++nt)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-  for (int sidx = 0; sidx < nr; ++sidx) {
-    int64_t lo, hi;
-    ks.range(i, sidx, lo, hi);
-    for (int64_t k0 = lo; k0 < hi; k0 += 16) {
-      load_kv(k0, hi);
+  for_tiles([&](int64_t k0, int64_t hi) {
       float s[2][4], dp[2][4];
       s_tile(k0, hi, s);
       uint32_t bv[DH / 16][4];
-      load_b_nt<DH>(sV, lane, bv);
+      load_b_nt<DH>(tV, lane, bv);
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
@@ -269,19 +310,18 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
       }
       // dQ += dS K  (B(k = key, n = dim) from the K tile rows, transposed loads)
       uint32_t bk[DH / 16][4];
-      load_b_nn<DH>(sK, lane, bk);
+      load_b_nn<DH>(tK, lane, bk);
 #pragma unroll
       for (int np = 0; np < DH / 16; ++np) {
         mma(acc[2 * np], ads, bk[np][0], bk[np][1]);
         mma(acc[2 * np + 1], ads, bk[np][2], bk[np][3]);
       }
-    }
-  }
+  });
   // write dq rows (< G), lse, D
 #pragma unroll
   for (int hr = 0; hr < 2; ++hr) {
     const int r = gq + 8 * hr;
-    if (r < G) {
+    if (valid && r < G) {
       const int64_t t = i * hq + (int64_t)g * G + r;
 #pragma unroll
       for (int nt = 0; nt < DH / 8; ++nt) {
@@ -300,27 +340,41 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
 // Forward of one branch for training: warp per (query, kv head), online
 // softmax over the key set in 16-key tiles; writes the branch output (fp32)
 // and lse per (query, head) for the backward.
-template <int DH>
+template <int DH, bool CMP>
 __global__ void __launch_bounds__(32 * kDqWarps)
 fwd_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, int64_t nq, int hq, int hkv,
                const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                float* __restrict__ out, float* __restrict__ lse_out) {
   constexpr int LD = DH + 8;
-  __shared__ __align__(16) __nv_bfloat16 sm[kDqWarps][3][16 * LD];   // Q, K, V tiles
+  __shared__ __align__(16) __nv_bfloat16 sm[kDqWarps][CMP ? 1 : 3][16 * LD];   // Q (, K, V)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t wid = (int64_t)blockIdx.x * kDqWarps + warp;
-  if (wid >= nq * hkv) return;
-  const int64_t i = wid / hkv;
-  const int g = (int)(wid % hkv);
+  // CMP: the CTA's warps take kDqWarps queries of one kv head, which share
+  // every key (the compressed rows), so K/V tiles are loaded once per CTA
+  int64_t i;
+  int g;
+  bool valid = true;
+  if constexpr (CMP) {
+    i = (int64_t)(blockIdx.x / hkv) * kDqWarps + warp;
+    g = (int)(blockIdx.x % hkv);
+    valid = i < nq;
+  } else {
+    const int64_t wid = (int64_t)blockIdx.x * kDqWarps + warp;
+    if (wid >= nq * hkv) return;
+    i = wid / hkv;
+    g = (int)(wid % hkv);
+  }
   const int G = hq / hkv;
+  __shared__ __align__(16) __nv_bfloat16 shK[CMP ? kCmpKeys * LD : 8];
+  __shared__ __align__(16) __nv_bfloat16 shV[CMP ? kCmpKeys * LD : 8];
   __nv_bfloat16* sQ = sm[warp][0];
-  __nv_bfloat16* sK = sm[warp][1];
-  __nv_bfloat16* sV = sm[warp][2];
+  __nv_bfloat16* sK = sm[warp][CMP ? 0 : 1];   // private K / V tiles (unused with CMP)
+  __nv_bfloat16* sV = sm[warp][CMP ? 0 : 2];
   const int gq = lane >> 2, cq = lane & 3;
   for (int e = lane; e < 16 * (DH / 8); e += 32) {
     const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
     uint4 vq = make_uint4(0, 0, 0, 0);
-    if (r < G) vq = *reinterpret_cast<const uint4*>(q + ((i * hq) + (int64_t)g * G + r) * DH + c8);
+    if (valid && r < G)
+      vq = *reinterpret_cast<const uint4*>(q + ((i * hq) + (int64_t)g * G + r) * DH + c8);
     *reinterpret_cast<uint4*>(sQ + r * LD + c8) = vq;
   }
   __syncwarp();
@@ -334,26 +388,11 @@ fwd_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, int64_t nq, int h
   for (int nt = 0; nt < DH / 8; ++nt)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-  const int nr = ks.n_ranges(i);
-  for (int sidx = 0; sidx < nr; ++sidx) {
-    int64_t lo, hi;
-    ks.range(i, sidx, lo, hi);
-    for (int64_t k0 = lo; k0 < hi; k0 += 16) {
-      __syncwarp();
-      for (int e = lane; e < 16 * (DH / 8); e += 32) {
-        const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
-        uint4 vk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-        if (k0 + r < hi) {
-          const int64_t base = (k0 + r) * kstride + (int64_t)g * DH + c8;
-          vk = *reinterpret_cast<const uint4*>(k + base);
-          vv = *reinterpret_cast<const uint4*>(v + base);
-        }
-        *reinterpret_cast<uint4*>(sK + r * LD + c8) = vk;
-        *reinterpret_cast<uint4*>(sV + r * LD + c8) = vv;
-      }
-      __syncwarp();
+  const __nv_bfloat16* tK = sK;   // current 16-key K / V tile
+  const __nv_bfloat16* tV = sV;
+  auto body = [&](int64_t k0, int64_t hi) {
       uint32_t bk[DH / 16][4];
-      load_b_nt<DH>(sK, lane, bk);
+      load_b_nt<DH>(tK, lane, bk);
       float s[2][4];
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
@@ -401,18 +440,62 @@ fwd_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, int64_t nq, int h
         ap[2 * nt + 1] = pk(p4[nt][2], p4[nt][3]);
       }
       uint32_t bv[DH / 16][4];
-      load_b_nn<DH>(sV, lane, bv);
+      load_b_nn<DH>(tV, lane, bv);
 #pragma unroll
       for (int np = 0; np < DH / 16; ++np) {
         mma(acc[2 * np], ap, bv[np][0], bv[np][1]);
         mma(acc[2 * np + 1], ap, bv[np][2], bv[np][3]);
+      }
+  };
+  if constexpr (CMP) {
+    for (int64_t kb = 0; kb < ks.nk; kb += kCmpKeys) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < kCmpKeys * (DH / 8); e += blockDim.x) {
+        const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
+        uint4 vk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+        if (kb + r < ks.nk) {
+          const int64_t base = (kb + r) * kstride + (int64_t)g * DH + c8;
+          vk = *reinterpret_cast<const uint4*>(k + base);
+          vv = *reinterpret_cast<const uint4*>(v + base);
+        }
+        *reinterpret_cast<uint4*>(shK + r * LD + c8) = vk;
+        *reinterpret_cast<uint4*>(shV + r * LD + c8) = vv;
+      }
+      __syncthreads();
+      if (valid)
+        for (int sub = 0; sub < kCmpKeys / 16 && kb + 16 * sub < ks.nk; ++sub) {
+          tK = shK + sub * 16 * LD;
+          tV = shV + sub * 16 * LD;
+          body(kb + 16 * sub, ks.nk);
+        }
+    }
+  } else {
+    const int nr = ks.n_ranges(i);
+    for (int sidx = 0; sidx < nr; ++sidx) {
+      int64_t lo, hi;
+      ks.range(i, sidx, lo, hi);
+      for (int64_t k0 = lo; k0 < hi; k0 += 16) {
+        __syncwarp();
+        for (int e = lane; e < 16 * (DH / 8); e += 32) {
+          const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
+          uint4 vk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+          if (k0 + r < hi) {
+            const int64_t base = (k0 + r) * kstride + (int64_t)g * DH + c8;
+            vk = *reinterpret_cast<const uint4*>(k + base);
+            vv = *reinterpret_cast<const uint4*>(v + base);
+          }
+          *reinterpret_cast<uint4*>(sK + r * LD + c8) = vk;
+          *reinterpret_cast<uint4*>(sV + r * LD + c8) = vv;
+        }
+        __syncwarp();
+        body(k0, hi);
       }
     }
   }
 #pragma unroll
   for (int hr = 0; hr < 2; ++hr) {
     const int r = gq + 8 * hr;
-    if (r < G) {
+    if (valid && r < G) {
       const int64_t t = i * hq + (int64_t)g * G + r;
       const float inv = 1.f / l[hr];
 #pragma unroll
@@ -428,6 +511,10 @@ fwd_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, int64_t nq, int h
 
 // dK/dV pass: CTA of 4 warps per (64-key tile, kv head, query slice).
 constexpr int kKvKeys = 64;
+#ifndef LSRM_BWD_QB
+#define LSRM_BWD_QB 8
+#endif
+constexpr int kQB = LSRM_BWD_QB;   // matched queries staged per shared-memory round
 
 template <int DH>
 __global__ void __launch_bounds__(128)
@@ -438,9 +525,9 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
                 float* __restrict__ part_dv) {
   constexpr int LD = DH + 8;
   __shared__ __align__(16) __nv_bfloat16 sKV[2][kKvKeys * LD];
-  __shared__ __align__(16) __nv_bfloat16 sQ[16 * LD];
-  __shared__ __align__(16) __nv_bfloat16 sO[16 * LD];
-  __shared__ float sL[16], sD[16];
+  __shared__ __align__(16) __nv_bfloat16 sQ[kQB][16 * LD];   // kQB matched queries per round
+  __shared__ __align__(16) __nv_bfloat16 sO[kQB][16 * LD];
+  __shared__ float sL[kQB][16], sD[kQB][16];
   __shared__ int qlist[128];
   __shared__ int wsum[4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -500,68 +587,74 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
     const int n_match = wsum[0] + wsum[1] + wsum[2] + wsum[3];
     if (match) qlist[before] = (int)(i - base);
     __syncthreads();
-    for (int mi = 0; mi < n_match; ++mi) {
-      const int64_t qi = base + qlist[mi];
-      // Q and dO rows of the G heads (rows >= G zero; lse = +inf -> P = 0)
-      for (int e2 = tid; e2 < 16 * (DH / 8) * 2; e2 += 128) {
-        const int which = e2 / (16 * (DH / 8)), e = e2 % (16 * (DH / 8));
+    for (int mb = 0; mb < n_match; mb += kQB) {
+      const int nb = min(kQB, n_match - mb);
+      // Q and dO rows of the G heads of nb queries (rows >= G zero; lse = +inf -> P = 0)
+      for (int e2 = tid; e2 < kQB * 2 * 16 * (DH / 8); e2 += 128) {
+        const int qb = e2 / (2 * 16 * (DH / 8)), rem = e2 % (2 * 16 * (DH / 8));
+        const int which = rem / (16 * (DH / 8)), e = rem % (16 * (DH / 8));
         const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
         uint4 val = make_uint4(0, 0, 0, 0);
-        if (r < G) {
+        if (qb < nb && r < G) {
+          const int64_t qi = base + qlist[mb + qb];
           const int64_t src = ((qi * hq) + (int64_t)g * G + r) * DH + c8;
           val = *reinterpret_cast<const uint4*>((which ? dob : q) + src);
         }
-        *reinterpret_cast<uint4*>((which ? sO : sQ) + r * LD + c8) = val;
+        *reinterpret_cast<uint4*>((which ? sO[qb] : sQ[qb]) + r * LD + c8) = val;
       }
-      if (tid < 16) {
-        const int64_t t = qi * hq + (int64_t)g * G + tid;
-        sL[tid] = tid < G ? lse[t] : __builtin_huge_valf();
-        sD[tid] = tid < G ? dsum[t] : 0.f;
+      for (int e = tid; e < kQB * 16; e += 128) {
+        const int qb = e / 16, h = e % 16;
+        const bool ok = qb < nb && h < G;
+        const int64_t t = ok ? (base + qlist[mb + qb]) * hq + (int64_t)g * G + h : 0;
+        sL[qb][h] = ok ? lse[t] : __builtin_huge_valf();
+        sD[qb][h] = ok ? dsum[t] : 0.f;
       }
       __syncthreads();
-      uint32_t bq[DH / 16][4], bo[DH / 16][4];
-      load_b_nt<DH>(sQ, lane, bq);
-      load_b_nt<DH>(sO, lane, bo);
-      // S^T, dP^T: 16 keys x 16 heads (two n-tiles of 8 heads)
-      float st[2][4], dpt[2][4];
+      for (int qb = 0; qb < nb; ++qb) {
+        uint32_t bq[DH / 16][4], bo[DH / 16][4];
+        load_b_nt<DH>(sQ[qb], lane, bq);
+        load_b_nt<DH>(sO[qb], lane, bo);
+        // S^T, dP^T: 16 keys x 16 heads (two n-tiles of 8 heads)
+        float st[2][4], dpt[2][4];
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+        for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) st[nt][e] = dpt[nt][e] = 0.f;
+          for (int e = 0; e < 4; ++e) st[nt][e] = dpt[nt][e] = 0.f;
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          mma(st[nt], ak[kk], bq[kk][2 * nt], bq[kk][2 * nt + 1]);
-          mma(dpt[nt], av[kk], bo[kk][2 * nt], bo[kk][2 * nt + 1]);
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            mma(st[nt], ak[kk], bq[kk][2 * nt], bq[kk][2 * nt + 1]);
+            mma(dpt[nt], av[kk], bo[kk][2 * nt], bo[kk][2 * nt + 1]);
+          }
+        }
+        uint32_t ap[4], ads[4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          float p4[4], d4[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int h = nt * 8 + 2 * cq + (e & 1);
+            const float p = __expf(st[nt][e] * scale - sL[qb][h]);
+            p4[e] = p;
+            d4[e] = p * (dpt[nt][e] - sD[qb][h]) * scale;
+          }
+          ap[2 * nt] = pk(p4[0], p4[1]);
+          ap[2 * nt + 1] = pk(p4[2], p4[3]);
+          ads[2 * nt] = pk(d4[0], d4[1]);
+          ads[2 * nt + 1] = pk(d4[2], d4[3]);
+        }
+        // dV += P^T dO, dK += dS^T Q  (B(k = head, n = dim): transposed loads)
+        uint32_t bo2[DH / 16][4], bq2[DH / 16][4];
+        load_b_nn<DH>(sO[qb], lane, bo2);
+        load_b_nn<DH>(sQ[qb], lane, bq2);
+#pragma unroll
+        for (int np = 0; np < DH / 16; ++np) {
+          mma(dv[2 * np], ap, bo2[np][0], bo2[np][1]);
+          mma(dv[2 * np + 1], ap, bo2[np][2], bo2[np][3]);
+          mma(dk[2 * np], ads, bq2[np][0], bq2[np][1]);
+          mma(dk[2 * np + 1], ads, bq2[np][2], bq2[np][3]);
         }
       }
-      uint32_t ap[4], ads[4];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        float p4[4], d4[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int h = nt * 8 + 2 * cq + (e & 1);
-          const float p = __expf(st[nt][e] * scale - sL[h]);
-          p4[e] = p;
-          d4[e] = p * (dpt[nt][e] - sD[h]) * scale;
-        }
-        ap[2 * nt] = pk(p4[0], p4[1]);
-        ap[2 * nt + 1] = pk(p4[2], p4[3]);
-        ads[2 * nt] = pk(d4[0], d4[1]);
-        ads[2 * nt + 1] = pk(d4[2], d4[3]);
-      }
-      // dV += P^T dO, dK += dS^T Q  (B(k = head, n = dim): transposed loads)
-      uint32_t bo2[DH / 16][4], bq2[DH / 16][4];
-      load_b_nn<DH>(sO, lane, bo2);
-      load_b_nn<DH>(sQ, lane, bq2);
-#pragma unroll
-      for (int np = 0; np < DH / 16; ++np) {
-        mma(dv[2 * np], ap, bo2[np][0], bo2[np][1]);
-        mma(dv[2 * np + 1], ap, bo2[np][2], bo2[np][3]);
-        mma(dk[2 * np], ads, bq2[np][0], bq2[np][1]);
-        mma(dk[2 * np + 1], ads, bq2[np][2], bq2[np][3]);
-      }
-      __syncthreads();   // sQ / sO reused by the next query
+      __syncthreads();   // staging reused by the next round
     }
   }
   // partials of this warp's 16 keys
@@ -634,7 +727,8 @@ int lsrm_attention_bwd_mma(int mode, const void* q_bf16, const void* dO_bf16, co
   float* pv_ = (float*)((char*)pk_ + align256((size_t)n_slices * nk * hkv * dh * sizeof(float)));
   cudaStream_t st = as_stream(stream);
   KeySet ks{mode, nk, block_offsets, rows, count, kmax_rows, own_row};
-  const unsigned g1 = (unsigned)ceil_div(nq * hkv, kDqWarps);
+  const unsigned g1 = mode == 0 ? (unsigned)(ceil_div(nq, kDqWarps) * hkv)
+                                : (unsigned)ceil_div(nq * hkv, kDqWarps);
   const int tiles_per_row = mode == 0 ? 0 : (int)ceil_div(max_row_keys, kKvKeys);
   const dim3 g2(mode == 0 ? (unsigned)ceil_div(nk, kKvKeys) : (unsigned)(n_rows * tiles_per_row),
                 (unsigned)hkv, (unsigned)n_slices);
@@ -644,9 +738,12 @@ int lsrm_attention_bwd_mma(int mode, const void* q_bf16, const void* dO_bf16, co
                       *kb = (const __nv_bfloat16*)k_bf16, *vb = (const __nv_bfloat16*)v_bf16;
 #define LSRM_BWD_MMA_CASE(D)                                                                   \
   case D:                                                                                      \
-    dq_mma_kernel<D><<<g1, 32 * kDqWarps, 0, st>>>(ks, qb, ob, dO, O, lse_in, nq, hq, hkv, kb, \
-                                                    vb, dq,                                    \
-                                                    lse, dsum);                                \
+    if (mode == 0)                                                                             \
+      dq_mma_kernel<D, true><<<g1, 32 * kDqWarps, 0, st>>>(ks, qb, ob, dO, O, lse_in, nq, hq,  \
+                                                           hkv, kb, vb, dq, lse, dsum);        \
+    else                                                                                       \
+      dq_mma_kernel<D, false><<<g1, 32 * kDqWarps, 0, st>>>(ks, qb, ob, dO, O, lse_in, nq, hq, \
+                                                            hkv, kb, vb, dq, lse, dsum);       \
     dkdv_mma_kernel<D><<<g2, 128, 0, st>>>(ks, qb, ob, lse, dsum, nq, hq, hkv, kb, vb, n_rows,  \
                                            tiles_per_row, n_slices, pk_, pv_);                  \
     break;
@@ -680,14 +777,22 @@ int lsrm_attention_fwd_mma(int mode, const void* q_bf16, int64_t nq, int hq, int
   if (nq == 0) return LSRM_OK;
   LSRM_REQUIRE(nk > 0, "attention over an empty key set");
   KeySet ks{mode, nk, block_offsets, rows, count, kmax_rows, own_row};
-  const unsigned g1 = (unsigned)ceil_div(nq * hkv, kDqWarps);
+  const unsigned g1 = mode == 0 ? (unsigned)(ceil_div(nq, kDqWarps) * hkv)
+                                : (unsigned)ceil_div(nq * hkv, kDqWarps);
   cudaStream_t st = as_stream(stream);
   const __nv_bfloat16 *qb = (const __nv_bfloat16*)q_bf16, *kb = (const __nv_bfloat16*)k_bf16,
                       *vb = (const __nv_bfloat16*)v_bf16;
+#define LSRM_FWD_MMA(D)                                                                      \
+  if (mode == 0)                                                                             \
+    fwd_mma_kernel<D, true><<<g1, 32 * kDqWarps, 0, st>>>(ks, qb, nq, hq, hkv, kb, vb, out,  \
+                                                          lse);                              \
+  else                                                                                       \
+    fwd_mma_kernel<D, false><<<g1, 32 * kDqWarps, 0, st>>>(ks, qb, nq, hq, hkv, kb, vb, out, \
+                                                           lse);
   switch (dh) {
-    case 16: fwd_mma_kernel<16><<<g1, 32 * kDqWarps, 0, st>>>(ks, qb, nq, hq, hkv, kb, vb, out, lse); break;
-    case 32: fwd_mma_kernel<32><<<g1, 32 * kDqWarps, 0, st>>>(ks, qb, nq, hq, hkv, kb, vb, out, lse); break;
-    case 64: fwd_mma_kernel<64><<<g1, 32 * kDqWarps, 0, st>>>(ks, qb, nq, hq, hkv, kb, vb, out, lse); break;
+    case 16: LSRM_FWD_MMA(16) break;
+    case 32: LSRM_FWD_MMA(32) break;
+    case 64: LSRM_FWD_MMA(64) break;
     default:
       return set_error(LSRM_E_CONFIG, "attention_fwd_mma: head_dim %d not in {16,32,64}", dh);
   }
