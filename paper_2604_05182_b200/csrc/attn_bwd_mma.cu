@@ -524,10 +524,11 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
                 int n_rows, int tiles_per_row, int n_slices, float* __restrict__ part_dk,
                 float* __restrict__ part_dv) {
   constexpr int LD = DH + 8;
+  constexpr int QB = DH <= 32 ? kQB : 4;   // staging rounds fit the 48 KB static limit
   __shared__ __align__(16) __nv_bfloat16 sKV[2][kKvKeys * LD];
-  __shared__ __align__(16) __nv_bfloat16 sQ[kQB][16 * LD];   // kQB matched queries per round
-  __shared__ __align__(16) __nv_bfloat16 sO[kQB][16 * LD];
-  __shared__ float sL[kQB][16], sD[kQB][16];
+  __shared__ __align__(16) __nv_bfloat16 sQ[QB][16 * LD];   // QB matched queries per round
+  __shared__ __align__(16) __nv_bfloat16 sO[QB][16 * LD];
+  __shared__ float sL[QB][16], sD[QB][16];
   __shared__ int qlist[128];
   __shared__ int wsum[4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -587,10 +588,10 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
     const int n_match = wsum[0] + wsum[1] + wsum[2] + wsum[3];
     if (match) qlist[before] = (int)(i - base);
     __syncthreads();
-    for (int mb = 0; mb < n_match; mb += kQB) {
-      const int nb = min(kQB, n_match - mb);
+    for (int mb = 0; mb < n_match; mb += QB) {
+      const int nb = min(QB, n_match - mb);
       // Q and dO rows of the G heads of nb queries (rows >= G zero; lse = +inf -> P = 0)
-      for (int e2 = tid; e2 < kQB * 2 * 16 * (DH / 8); e2 += 128) {
+      for (int e2 = tid; e2 < QB * 2 * 16 * (DH / 8); e2 += 128) {
         const int qb = e2 / (2 * 16 * (DH / 8)), rem = e2 % (2 * 16 * (DH / 8));
         const int which = rem / (16 * (DH / 8)), e = rem % (16 * (DH / 8));
         const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
@@ -602,7 +603,7 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
         }
         *reinterpret_cast<uint4*>((which ? sO[qb] : sQ[qb]) + r * LD + c8) = val;
       }
-      for (int e = tid; e < kQB * 16; e += 128) {
+      for (int e = tid; e < QB * 16; e += 128) {
         const int qb = e / 16, h = e % 16;
         const bool ok = qb < nb && h < G;
         const int64_t t = ok ? (base + qlist[mb + qb]) * hq + (int64_t)g * G + h : 0;
