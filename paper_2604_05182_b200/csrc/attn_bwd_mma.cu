@@ -512,7 +512,7 @@ fwd_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, int64_t nq, int h
 // dK/dV pass: CTA of 4 warps per (64-key tile, kv head, query slice).
 constexpr int kKvKeys = 64;
 #ifndef LSRM_BWD_QB
-#define LSRM_BWD_QB 8
+#define LSRM_BWD_QB 4
 #endif
 constexpr int kQB = LSRM_BWD_QB;   // matched queries staged per shared-memory round
 
