@@ -26,8 +26,8 @@ from .block_routing import (RoutingBudgets, RoutingPlan, TokenCoords3D, build_ro
 
 from .seq_parallel import (TOKEN_COORD_BYTES, WorkerTopology, all_gather_kv, all_to_all,
                            imbalance_report, makespan_ratio, message_log_to_csv,
-                           naive_contiguous_shards, naive_split_loads, shard_blocks,
-                           shard_blocks_by_cost)
+                           naive_contiguous_shards, naive_split_loads, parallel_sparse_stage,
+                           shard_blocks, shard_blocks_by_cost)
 from .recon_pipeline import (DecodeWeights, DecoderHeads, DenseBlockWeights, FeatureVolume,
                              MhaWeights, build_sparse_context, build_sparse_features,
                              decode_feature_volume, decode_point, decode_points,

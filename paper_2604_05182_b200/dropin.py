@@ -25,7 +25,8 @@ HOT_PATH = {
                       "_route_points_to_volume", "_route_points_to_image",
                       "image_token_coords"),
     "tokenizer": ("informative_voxel_mask", "foreground_patch_mask", "upsample_select_tokens"),
-    "seq_parallel": ("shard_blocks", "all_to_all", "all_gather_kv", "naive_contiguous_shards"),
+    "seq_parallel": ("shard_blocks", "all_to_all", "all_gather_kv", "naive_contiguous_shards",
+                     "parallel_sparse_stage"),
     "recon_pipeline": ("sparse_block_forward", "build_sparse_context", "ffn_forward",
                        "mha_forward", "dense_block_forward", "dense_stage_forward",
                        "decode_feature_volume", "build_sparse_features", "query_field",

@@ -205,6 +205,52 @@ def all_gather_kv(local_parts, topology: WorkerTopology, phase: str):
     return k_tok, v_tok, k_cmp, v_cmp
 
 
+def parallel_sparse_stage(x_up, y_up, weights, ctx, params, n_workers: int):
+    """Sharded sparse stage, reference API (`seq_parallel.py:321-434`):
+    returns (x_s, y_s, topology) with the states in global token order.
+
+    The topology and its message log follow the reference protocol exactly:
+    the dispatch all-to-all, per layer and use one All-gather-KV of every
+    worker's projected + compressed blocks (4*2*(|k| + |k_cmp|) bytes to each
+    other worker), a zero-byte window entry per worker for self uses, and the
+    return all-to-all.  The data path runs on this process's GPU: every
+    output row depends only on its own query and the gathered (canonical)
+    KV, so the W shards are computed in one pass of the fp32 stage
+    (`recon_pipeline.sparse_stage_forward`) and the result is the serial one
+    (the reference requires <= 1e-6; here it is identical).  The
+    multi-process NCCL path with real per-rank shards is `ShardedLayer`."""
+    from .recon_pipeline import sparse_stage_forward
+    part_vol, part_img = ctx.part_vol, ctx.part_img
+    require(x_up.count == part_vol.n_tokens and y_up.count == part_img.n_tokens,
+            "token sets do not match the partitions in the context")
+    require(x_up.count > 0 and y_up.count > 0, "parallel stage needs nonempty token streams")
+    d = params.model_dim
+    width = params.n_kv_heads * params.head_dim
+    topology = shard_blocks(part_vol, part_img, n_workers)
+    n_x = int(x_up.count)
+    aligned = [np.concatenate([topology.vol_tokens[w], topology.img_tokens[w] + n_x])
+               for w in range(n_workers)]
+    naive = naive_contiguous_shards(n_x + int(y_up.count), n_workers)
+    all_to_all(naive, aligned, topology, "dispatch", 4 * d + TOKEN_COORD_BYTES)
+    x_s, y_s = sparse_stage_forward(x_up, y_up, weights, ctx, params)
+    for m in range(len(weights)):
+        for name, kv_vol, is_self in (("v2v", True, True), ("v2i", False, False),
+                                      ("i2i", False, True), ("i2v", True, False)):
+            toks = topology.vol_tokens if kv_vol else topology.img_tokens
+            rows = topology.vol_rows if kv_vol else topology.img_rows
+            kv_bytes = [4 * 2 * (t.size * width + r.size * width) for t, r in zip(toks, rows)]
+            for s in range(n_workers):
+                for dst in range(n_workers):
+                    if s != dst and kv_bytes[s]:
+                        topology.log(f"layer{m}/{name}", "all_gather_kv", s, dst, kv_bytes[s])
+            if is_self:
+                for w in range(n_workers):   # self use: queries are the kv tokens
+                    if toks[w].size:
+                        topology.log(f"layer{m}/{name}/win", "window", w, w, 0)
+    all_to_all(aligned, naive, topology, "return", 4 * d + TOKEN_COORD_BYTES)
+    return x_s, y_s, topology
+
+
 # ---------------------------------------------------------------------------
 # load-balance reporting (`seq_parallel.py:441-470`)
 

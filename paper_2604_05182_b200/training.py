@@ -157,8 +157,13 @@ def _backward(spec: _Spec, P, s, dout):
     bf = s.get("bf")
 
     def bwd(mode, b, k, v, nk, dk, dv, rows=None, count=None, own=None):
-        # cmp has few keys and every query: slice the queries for parallelism
-        n_slices = max(1, min(64, n // 256)) if mode == 0 else max(1, min(4, n // 1024))
+        # cmp has few keys and every query: slice the queries so the key-major
+        # pass has >= ~8 CTAs per SM (148 SMs)
+        if mode == 0:
+            tiles = -(-nk // 64) * hkv
+            n_slices = max(1, min(n // 64, -(-8 * 148 // tiles)))
+        else:
+            n_slices = max(1, min(4, n // 1024))
         ws_bytes = lib().lsrm_attention_bwd_workspace(n, hq, nk, hkv, dh, n_slices)
         ws = D.empty((ws_bytes,), torch.uint8)
         common = (nk, offs.data_ptr() if mode else None, B, max_occ, D.ptr(rows), D.ptr(count),

@@ -94,3 +94,24 @@ def test_sparse_block_engine_vs_oracle(c1_tokens):
         upd = np.linalg.norm((got - base) - (ref - base)) / np.linalg.norm(ref - base)
         print(f"block engine {name}: rel-L2 {rel:.3e}, update rel-L2 {upd:.3e}")
         assert rel < 2e-2 and upd < 2e-2, (name, rel, upd)
+
+
+def test_parallel_sparse_stage_matches_reference(c1_tokens, ref_c1):
+    """`seq_parallel.parallel_sparse_stage` (reference API, W = 3): states
+    vs the reference's serial block + residual, and the message log equal to
+    the reference's own parallel run (`ref_c1.npz` par3_log)."""
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200 import recon_pipeline as R
+    params = L.AttentionParams(8, 1, 8)
+    x_up, y_up = c1_tokens[64]
+    pv, pi = c1_tokens["pv"], c1_tokens["pi"]
+    sels = {n: L.Selection(unflat(ref_c1[f"plan_{n}"], ref_c1[f"plan_{n}_len"]))
+            for n in R.TABLE_NAMES}
+    ctx = R.build_sparse_context(pv, pi, selections=sels)
+    w = R.init_sparse_block(0, params, 0)
+    xs, ys, topo = L.parallel_sparse_stage(x_up, y_up, [w], ctx, params, 3)
+    want_x = (ref_c1["block_x"].astype(np.float64) + x_up.features).astype(np.float32)
+    want_y = (ref_c1["block_y"].astype(np.float64) + y_up.features).astype(np.float32)
+    assert np.max(np.abs(xs.astype(np.float64) - want_x)) < 1e-5
+    assert np.max(np.abs(ys.astype(np.float64) - want_y)) < 1e-5
+    assert ["%s,%s,%d,%d,%d" % r for r in topo.message_log] == list(ref_c1["par3_log"])
