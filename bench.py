@@ -341,7 +341,8 @@ def time_train_step(inst, steps=3):
     def fwd():
         outs = mod(x, y, inst.part_vol, inst.part_img, res)
         return sum((o * o).sum() for o in outs.values())
-    fwd().backward()
+    for _ in range(3):   # warm-up (lazy module loading of the sort kernels, allocator)
+        fwd().backward()
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     fw, bw = [], []

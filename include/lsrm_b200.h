@@ -405,8 +405,18 @@ int lsrm_attention_bwd_mma(int mode, const void* q_bf16, const void* dO_bf16, co
                            const void* k_bf16, const void* v_bf16, int64_t nk,
                            const int64_t* block_offsets, int n_rows, int max_row_keys,
                            const int32_t* rows, const int32_t* count, int kmax_rows,
-                           const int32_t* own_row, int n_slices, float* dq, float* dk,
-                           float* dv, void* workspace, size_t ws_bytes, void* stream);
+                           const int32_t* own_row, int n_slices, const int64_t* t_offs,
+                           const int32_t* t_q, float* dq, float* dk, float* dv,
+                           void* workspace, size_t ws_bytes, void* stream);
+/* Transposed routing index for the key-major pass: offs [n_rows + 1] and
+ * q [nq * kmax] (the first offs[n_rows] used): per kv row, the queries whose
+ * resolved selection holds it, ascending (stable radix sort of (row, query)
+ * keys).  The backward takes it as t_offs / t_q (sel), or the query
+ * partition's block offsets / token ids (win). */
+size_t lsrm_transpose_rows_workspace(int64_t nq, int kmax);
+int lsrm_transpose_rows(const int32_t* rows, const int32_t* count, int64_t nq, int kmax,
+                        int n_rows, int64_t* offs, int32_t* q_out, void* workspace,
+                        size_t ws_bytes, void* stream);
 /* merged = sum_b sigmoid(gl[:, b*d:(b+1)*d] + gb[b*d:]) * o_b:
  * do_b = dM g_b,  dz[:, b*d + c] = dM o_b g_b (1 - g_b)   (dz [n, n_gates*d]). */
 int lsrm_gate_merge_bwd_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,

@@ -17,6 +17,8 @@
 // B "col" 16x8, C 16x8 f32 (rows lane/4 and lane/4 + 8, columns 2(lane%4)).
 #include <cuda_bf16.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 
 namespace lsrm {
@@ -521,8 +523,9 @@ __global__ void __launch_bounds__(128)
 dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dob,
                 const float* __restrict__ lse, const float* __restrict__ dsum, int64_t nq, int hq,
                 int hkv, const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
-                int n_rows, int tiles_per_row, int n_slices, float* __restrict__ part_dk,
-                float* __restrict__ part_dv) {
+                int n_rows, int tiles_per_row, int n_slices,
+                const int64_t* __restrict__ t_offs, const int32_t* __restrict__ t_q,
+                float* __restrict__ part_dk, float* __restrict__ part_dv) {
   constexpr int LD = DH + 8;
   constexpr int QB = DH <= 32 ? kQB : 4;   // staging rounds fit the 48 KB static limit
   __shared__ __align__(16) __nv_bfloat16 sKV[2][kKvKeys * LD];
@@ -565,11 +568,25 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
   for (int nt = 0; nt < DH / 8; ++nt)
 #pragma unroll
     for (int e = 0; e < 4; ++e) dk[nt][e] = dv[nt][e] = 0.f;
-  const int64_t q_lo = nq * slice / n_slices, q_hi = nq * (slice + 1) / n_slices;
+  // queries that see this row: with a transposed index (t_offs / t_q: per
+  // row, its queries in ascending order) this slice's share of the row's
+  // list; otherwise scan the slice of all queries and test membership
+  const bool listed = t_offs != nullptr && mode != 0;
+  int64_t q_lo, q_hi;
+  if (listed) {
+    const int64_t l0 = t_offs[row], len = t_offs[row + 1] - l0;
+    q_lo = l0 + len * slice / n_slices;
+    q_hi = l0 + len * (slice + 1) / n_slices;
+  } else {
+    q_lo = nq * slice / n_slices;
+    q_hi = nq * (slice + 1) / n_slices;
+  }
   for (int64_t base = q_lo; base < q_hi; base += 128) {
-    const int64_t i = base + tid;
+    const int64_t i = listed ? (base + tid < q_hi ? (int64_t)t_q[base + tid] : 0) : base + tid;
     bool match = false;
-    if (i < q_hi) {
+    if (listed) {
+      match = base + tid < q_hi;
+    } else if (i < q_hi) {
       if (mode == 0) {
         match = true;
       } else if (mode == 1) {
@@ -586,7 +603,7 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
     int before = __popc(bal & ((1u << lane) - 1u));
     for (int w = 0; w < warp; ++w) before += wsum[w];
     const int n_match = wsum[0] + wsum[1] + wsum[2] + wsum[3];
-    if (match) qlist[before] = (int)(i - base);
+    if (match) qlist[before] = (int)i;   // absolute query index
     __syncthreads();
     for (int mb = 0; mb < n_match; mb += QB) {
       const int nb = min(QB, n_match - mb);
@@ -597,7 +614,7 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
         const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
         uint4 val = make_uint4(0, 0, 0, 0);
         if (qb < nb && r < G) {
-          const int64_t qi = base + qlist[mb + qb];
+          const int64_t qi = qlist[mb + qb];
           const int64_t src = ((qi * hq) + (int64_t)g * G + r) * DH + c8;
           val = *reinterpret_cast<const uint4*>((which ? dob : q) + src);
         }
@@ -606,7 +623,7 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
       for (int e = tid; e < QB * 16; e += 128) {
         const int qb = e / 16, h = e % 16;
         const bool ok = qb < nb && h < G;
-        const int64_t t = ok ? (base + qlist[mb + qb]) * hq + (int64_t)g * G + h : 0;
+        const int64_t t = ok ? (int64_t)qlist[mb + qb] * hq + (int64_t)g * G + h : 0;
         sL[qb][h] = ok ? lse[t] : __builtin_huge_valf();
         sD[qb][h] = ok ? dsum[t] : 0.f;
       }
@@ -693,6 +710,37 @@ __global__ void reduce_kernel(const float* __restrict__ pk_, const float* __rest
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+__global__ void transpose_keys_kernel(const int32_t* __restrict__ rows,
+                                      const int32_t* __restrict__ count, int64_t nq, int kmax,
+                                      uint64_t* __restrict__ keys) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= nq * kmax) return;
+  const int64_t i = e / kmax;
+  const int s = (int)(e % kmax);
+  const uint64_t r = s < count[i] ? (uint64_t)(uint32_t)rows[e] : 0xffffffffull;
+  keys[e] = (r << 32) | (uint64_t)i;
+}
+
+// offs[r] = first sorted position with row >= r (binary search)
+__global__ void transpose_offsets_kernel(const uint64_t* __restrict__ sorted, int64_t n,
+                                         int n_rows, int64_t* __restrict__ offs) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > n_rows) return;
+  const uint64_t key = (uint64_t)(uint32_t)r << 32;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sorted[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  offs[r] = lo;
+}
+
+__global__ void transpose_fill_kernel(const uint64_t* __restrict__ sorted, int64_t n,
+                                      int32_t* __restrict__ q_out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < n) q_out[e] = (int32_t)(sorted[e] & 0xffffffffull);
+}
+
 }  // namespace bwdmma
 }  // namespace lsrm
 
@@ -710,10 +758,12 @@ int lsrm_attention_bwd_mma(int mode, const void* q_bf16, const void* dO_bf16, co
                            const void* k_bf16, const void* v_bf16, int64_t nk,
                            const int64_t* block_offsets, int n_rows, int max_row_keys,
                            const int32_t* rows, const int32_t* count, int kmax_rows,
-                           const int32_t* own_row, int n_slices, float* dq, float* dk, float* dv,
+                           const int32_t* own_row, int n_slices, const int64_t* t_offs,
+                           const int32_t* t_q, float* dq, float* dk, float* dv,
                            void* workspace, size_t ws_bytes, void* stream) {
   LSRM_REQUIRE(mode >= 0 && mode <= 2, "attention_bwd: mode must be 0 (cmp), 1 (sel), 2 (win)");
   LSRM_REQUIRE(hq % hkv == 0 && hq / hkv <= 16, "attention_bwd_mma: group size must be <= 16");
+  LSRM_REQUIRE((t_offs == nullptr) == (t_q == nullptr), "attention_bwd_mma: t_offs and t_q go together");
   LSRM_REQUIRE(n_slices >= 1 && n_slices <= 65535, "attention_bwd: n_slices out of range");
   LSRM_REQUIRE(mode == 0 || (block_offsets && n_rows >= 1 && max_row_keys >= 1),
                "attention_bwd: sel/win need block offsets");
@@ -746,7 +796,7 @@ int lsrm_attention_bwd_mma(int mode, const void* q_bf16, const void* dO_bf16, co
       dq_mma_kernel<D, false><<<g1, 32 * kDqWarps, 0, st>>>(ks, qb, ob, dO, O, lse_in, nq, hq, \
                                                             hkv, kb, vb, dq, lse, dsum);       \
     dkdv_mma_kernel<D><<<g2, 128, 0, st>>>(ks, qb, ob, lse, dsum, nq, hq, hkv, kb, vb, n_rows,  \
-                                           tiles_per_row, n_slices, pk_, pv_);                  \
+                                           tiles_per_row, n_slices, t_offs, t_q, pk_, pv_);     \
     break;
   switch (dh) {
     LSRM_BWD_MMA_CASE(16)
@@ -760,6 +810,45 @@ int lsrm_attention_bwd_mma(int mode, const void* q_bf16, const void* dO_bf16, co
   const int64_t n = nk * hkv * dh;
   const unsigned g3 = (unsigned)(ceil_div(n, 256) < 148 * 8 ? ceil_div(n, 256) : 148 * 8);
   reduce_kernel<<<g3, 256, 0, st>>>(pk_, pv_, n_slices, n, dk, dv);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+// Transposed routing index: for every kv row, the queries whose resolved
+// selection holds it, in ascending query order (deterministic: one stable
+// radix sort of (row, query) keys).  offs [n_rows + 1], q [sum(count)].
+size_t lsrm_transpose_rows_workspace(int64_t nq, int kmax) {
+  size_t tmp = 0;
+  const int64_t n = nq * kmax;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                 (int)n);
+  return 2 * align256((size_t)n * sizeof(uint64_t)) + align256(sizeof(int)) + align256(tmp);
+}
+
+int lsrm_transpose_rows(const int32_t* rows, const int32_t* count, int64_t nq, int kmax,
+                        int n_rows, int64_t* offs, int32_t* q_out, void* workspace,
+                        size_t ws_bytes, void* stream) {
+  LSRM_REQUIRE(ws_bytes >= lsrm_transpose_rows_workspace(nq, kmax),
+               "transpose_rows: workspace too small");
+  LSRM_REQUIRE(nq * (int64_t)kmax < (1ll << 31), "transpose_rows: too many entries");
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = nq * kmax;
+  char* ws = (char*)workspace;
+  uint64_t* keys = (uint64_t*)ws;
+  uint64_t* sorted = (uint64_t*)(ws + align256((size_t)n * sizeof(uint64_t)));
+  void* tmp = ws + 2 * align256((size_t)n * sizeof(uint64_t)) + align256(sizeof(int));
+  size_t tmp_bytes = ws_bytes - (2 * align256((size_t)n * sizeof(uint64_t)) + align256(sizeof(int)));
+  // entry (i, s): key = row << 32 | i; unused slots sort last (row = all ones)
+  transpose_keys_kernel<<<(unsigned)ceil_div(n > 0 ? n : 1, 256), 256, 0, st>>>(rows, count, nq,
+                                                                               kmax, keys);
+  LSRM_LAUNCHED();
+  if (n > 0 &&
+      cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, (int)n, 0, 64, st) !=
+          cudaSuccess)
+    return set_error(LSRM_E_CUDA, "transpose_rows: radix sort failed");
+  transpose_offsets_kernel<<<(unsigned)ceil_div(n_rows + 1, 256), 256, 0, st>>>(sorted, n, n_rows,
+                                                                              offs);
+  transpose_fill_kernel<<<(unsigned)ceil_div(n > 0 ? n : 1, 256), 256, 0, st>>>(sorted, n, q_out);
   LSRM_LAUNCHED();
   return LSRM_OK;
 }

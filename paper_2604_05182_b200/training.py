@@ -45,6 +45,7 @@ class _Spec:
     rows: torch.Tensor
     count: torch.Tensor
     fast: bool = False    # tensor-core (bf16) attention backward
+    transposed: tuple = None   # (offs, queries) per kv row, built on first use
 
 
 def _mma_ok(spec: _Spec) -> bool:
@@ -155,6 +156,22 @@ def _backward(spec: _Spec, P, s, dout):
 
     use_mma = fast
     bf = s.get("bf")
+    # key-major pass of the mma path walks each kv row's own query list:
+    # sel through the transposed routing index, win through the block's tokens
+    lists = {0: (None, None), 1: (None, None), 2: (None, None)}
+    if use_mma:
+        if spec.transposed is None:
+            kmx = int(spec.rows.shape[1])
+            t_offs = D.empty((B + 1,), torch.int64)
+            t_q = D.empty((max(n * kmx, 1),), torch.int32)
+            wsb = lib().lsrm_transpose_rows_workspace(n, kmx)
+            tws = D.empty((max(wsb, 1),), torch.uint8)
+            call("lsrm_transpose_rows", spec.rows.data_ptr(), spec.count.data_ptr(), n, kmx, B,
+                 t_offs.data_ptr(), t_q.data_ptr(), tws.data_ptr(), wsb, st)
+            spec.transposed = (t_offs, t_q)
+        lists[1] = spec.transposed
+        if ng == 3:
+            lists[2] = (part.dev("block_offsets"), part.dev("block_token_ids").to(torch.int32))
 
     def bwd(mode, b, k, v, nk, dk, dv, rows=None, count=None, own=None):
         # cmp has few keys and every query: slice the queries so the key-major
@@ -166,18 +183,19 @@ def _backward(spec: _Spec, P, s, dout):
             n_slices = max(1, min(4, n // 1024))
         ws_bytes = lib().lsrm_attention_bwd_workspace(n, hq, nk, hkv, dh, n_slices)
         ws = D.empty((ws_bytes,), torch.uint8)
-        common = (nk, offs.data_ptr() if mode else None, B, max_occ, D.ptr(rows), D.ptr(count),
-                  kmax, D.ptr(own), n_slices, dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
-                  ws.data_ptr(), ws_bytes, st)
+        head = (nk, offs.data_ptr() if mode else None, B, max_occ, D.ptr(rows), D.ptr(count),
+                kmax, D.ptr(own), n_slices)
+        tail = (dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws_bytes, st)
         if use_mma:
             dob = _ops.cast(do[b], torch.bfloat16)
             call("lsrm_attention_bwd_mma", mode, bf["q"].data_ptr(), dob.data_ptr(),
                  do[b].data_ptr(), o[b].data_ptr(), s["lse"][b].data_ptr(), n, hq, hkv, dh,
-                 bf[k].data_ptr(),
-                 bf[v].data_ptr(), *common)
+                 bf[k].data_ptr(), bf[v].data_ptr(), *head, D.ptr(lists[mode][0]),
+                 D.ptr(lists[mode][1]), *tail)
         else:
             call("lsrm_attention_bwd_f32", mode, s["q"].data_ptr(), do[b].data_ptr(),
-                 o[b].data_ptr(), n, hq, hkv, dh, s[k].data_ptr(), s[v].data_ptr(), *common)
+                 o[b].data_ptr(), n, hq, hkv, dh, s[k].data_ptr(), s[v].data_ptr(), *head,
+                 *tail)
     bwd(0, 0, "kc", "vc", B, dkc, dvc)
     bwd(1, 1, "k_bm", "v_bm", m, dk_bm, dv_bm, rows=spec.rows, count=spec.count)
     if ng == 3:

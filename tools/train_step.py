@@ -19,7 +19,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c3")
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--fast", action="store_true", help="tensor-core (bf16) attention backward")
     a = ap.parse_args()
     import torch
@@ -56,7 +56,8 @@ def main():
     print(json.dumps({"workload": a.workload, "n_tokens": n_tok, "dtype": "f32",
                       "backward": "mma.sync bf16" if a.fast else "fp32 CUDA cores",
                       "forward_ms": sum(fw) / len(fw), "backward_ms": sum(bw) / len(bw),
-                      "step_ms": ms, "tokens_per_s": n_tok / (ms * 1e-3)}))
+                      "step_ms": ms, "tokens_per_s": n_tok / (ms * 1e-3),
+                      "per_step_ms": [round(a + b, 3) for a, b in zip(fw, bw)]}))
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
         step().backward()
         torch.cuda.synchronize()
