@@ -268,6 +268,9 @@ constexpr int kStages = LSRM_STAGES;   // K/V ring depth (each stage holds every
 #ifndef LSRM_SPLIT_RELOAD
 #define LSRM_SPLIT_RELOAD 1
 #endif
+#ifndef LSRM_SKIP_DEAD_MAX
+#define LSRM_SKIP_DEAD_MAX 0
+#endif
 constexpr bool kOnePass = LSRM_ONEPASS;
 constexpr bool kPingPong = LSRM_PINGPONG;
 // kSplit softmax warps per TMEM lane quadrant: warp `half` of a pair owns
@@ -1095,9 +1098,17 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     const float g_ = max16(arr + (off));                        \
     mx = ((visb >> (gi)) & 1u) ? fmaxf(mx, g_) : mx;            \
   }
-        LSRM_MAX(sa, 0, 0)
-        LSRM_MAX(sa, 16, 1)
-        if (ncols > 32) {
+// pieces no row of the warp sees are skipped (warp-uniform `live` bits)
+#if LSRM_SKIP_DEAD_MAX
+#define LSRM_LIVE(pc) ((live >> (2 * (pc))) & 3u)
+#else
+#define LSRM_LIVE(pc) true
+#endif
+        if (LSRM_LIVE(0)) {
+          LSRM_MAX(sa, 0, 0)
+          LSRM_MAX(sa, 16, 1)
+        }
+        if (ncols > 32 && LSRM_LIVE(1)) {
           LSRM_MAX(sb, 0, 2)
           LSRM_MAX(sb, 16, 3)
         }
@@ -1107,9 +1118,11 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           tmem_ld32(tS + HCols::kS + 64, sa);
           if (ncols > 96) tmem_ld32(tS + HCols::kS + 96, sb);
           tmem_wait_ld();
-          LSRM_MAX(sa, 0, 4)
-          LSRM_MAX(sa, 16, 5)
-          if (ncols > 96) {
+          if (LSRM_LIVE(2)) {
+            LSRM_MAX(sa, 0, 4)
+            LSRM_MAX(sa, 16, 5)
+          }
+          if (ncols > 96 && LSRM_LIVE(3)) {
             LSRM_MAX(sb, 0, 6)
             LSRM_MAX(sb, 16, 7)
           }
