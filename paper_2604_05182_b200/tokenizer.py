@@ -193,8 +193,9 @@ def upsample_select_tokens(x_d, y_d, vol_mask, img_mask, pe_fine_vol, pe_fine_im
     yd = D.dev(y_d, torch.float32)
     vm = D.dev(vol_mask).to(torch.uint8).contiguous()
     im = D.dev(img_mask).to(torch.uint8).contiguous()
-    tv = [D.dev(t, torch.float32) for t in pe_fine_vol.tables]
-    ti = [D.dev(t, torch.float32) for t in pe_fine_img.tables]
+    # positional tables are weights: uploaded once per array (device cache)
+    tv = [D.dev(t, torch.float32) if D.is_device(t) else D.weight(t) for t in pe_fine_vol.tables]
+    ti = [D.dev(t, torch.float32) if D.is_device(t) else D.weight(t) for t in pe_fine_img.tables]
     vc, vf = _compact("volume", vm, xd, d, tv, 1, s_fine, factor_vol)
     ic, ifeat = _compact("image", im, yd, d, ti, n_views, rows_f, factor_img)
     if not on_dev:
