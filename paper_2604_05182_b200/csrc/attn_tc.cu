@@ -271,6 +271,12 @@ constexpr int kStages = LSRM_STAGES;   // K/V ring depth (each stage holds every
 #ifndef LSRM_SKIP_DEAD_MAX
 #define LSRM_SKIP_DEAD_MAX 0
 #endif
+#ifndef LSRM_GROUP_SKIP
+#define LSRM_GROUP_SKIP 0
+#endif
+// skip exponentials per 16-key group no row of the warp sees (instead of per
+// 32-key piece)
+constexpr bool kGroupSkip = LSRM_GROUP_SKIP;
 constexpr bool kOnePass = LSRM_ONEPASS;
 constexpr bool kPingPong = LSRM_PINGPONG;
 // kSplit softmax warps per TMEM lane quadrant: warp `half` of a pair owns
@@ -1182,7 +1188,16 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     uint32_t w[16];                                                            \
     const bool lp_ = last_all && ++pdone == n_pc;                              \
     pp_turn();                                                                 \
-    if ((live >> (2 * (pc))) & 3u) {                                           \
+    if (kGroupSkip) {   /* warp-uniform skip per 16-key group */             \
+      if ((live >> (2 * (pc))) & 1u)                                           \
+        exp16(arr, sl2, ((visb >> (2 * (pc))) & 1u) ? nbv : kNegInf, w);       \
+      else                                                                     \
+        zero8(w);                                                              \
+      if ((live >> (2 * (pc) + 1)) & 1u)                                       \
+        exp16(arr + 16, sl2, ((visb >> (2 * (pc) + 1)) & 1u) ? nbv : kNegInf, w + 8); \
+      else                                                                     \
+        zero8(w + 8);                                                          \
+    } else if ((live >> (2 * (pc))) & 3u) {                                    \
       exp16(arr, sl2, ((visb >> (2 * (pc))) & 1u) ? nbv : kNegInf, w);         \
       exp16(arr + 16, sl2, ((visb >> (2 * (pc) + 1)) & 1u) ? nbv : kNegInf, w + 8); \
     } else {                                                                   \
