@@ -317,3 +317,28 @@ def test_engine_layer_vs_fp32_path(c1):
         rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         print(f"engine {use}: rel-L2 {rel:.3e}")
         assert rel < 2e-2, (use, rel)
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_engine_layer_vs_fp32_path_full_size(cuda, name):
+    """The bf16 layer at BASELINE sizes (C3; C4 with twelve fully occupied
+    512-token volume blocks, the maximum block size) against the fp32
+    reference-API path on the same inputs and routing, every use."""
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200.engine import USES
+    from paper_2604_05182_b200.layer import SparseAttentionLayer, build_instance
+    inst = build_instance(name)
+    layer = SparseAttentionLayer(inst)
+    outs = layer.forward_host(inst.x_hat, inst.y_hat)
+    pv, pi = inst.part_vol, inst.part_img
+    parts = {"v2v": (inst.x_hat, inst.x_hat, pv, pv), "v2i": (inst.x_hat, inst.y_hat, pv, pi),
+             "i2i": (inst.y_hat, inst.y_hat, pi, pi), "i2v": (inst.y_hat, inst.x_hat, pi, pv)}
+    from paper_2604_05182_b200.block_routing import _rows_to_selection
+    for use in USES:
+        xq, xkv, pq, pk = parts[use]
+        sel = _rows_to_selection(*inst.plan_rows[use], pk)
+        ref = L.nsa_cross_attention(xq, xkv, pq, pk, sel, inst.weights[use], inst.params)
+        got = np.asarray(outs[use], np.float64)
+        rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        print(f"{name} engine {use}: rel-L2 {rel:.3e}")
+        assert rel < 2e-2, (use, rel)
