@@ -274,6 +274,19 @@ constexpr int kStages = LSRM_STAGES;   // K/V ring depth (each stage holds every
 #ifndef LSRM_GROUP_SKIP
 #define LSRM_GROUP_SKIP 0
 #endif
+#ifndef LSRM_HOLD4
+#define LSRM_HOLD4 0
+#endif
+#ifndef LSRM_DBUF
+#define LSRM_DBUF 0
+#endif
+// Double-buffered S (one pipeline per CTA): QK(c+2) is issued right after
+// PV(c) into the buffer chunk c used, so S(c+1) is ready before the softmax
+// finishes chunk c.  P(c) is written into the consumed half of S(c)'s buffer
+// (columns [kNK/2, kNK)), so a pipeline needs 2*kNK + VW + DH/2 columns.
+constexpr bool kDbuf = LSRM_DBUF;
+static_assert(!kDbuf || (LSRM_SPLIT == 1 && !LSRM_ONEPASS && !LSRM_PINGPONG),
+              "double-buffered S is two-pass, unsplit only");
 // skip exponentials per 16-key group no row of the warp sees (instead of per
 // 32-key piece)
 constexpr bool kGroupSkip = LSRM_GROUP_SKIP;
@@ -402,8 +415,10 @@ constexpr int kFFirstBranch = 1, kFLastBranch = 2, kFFirstItem = 4, kFLastItem =
 template <int DH>
 struct HeadCols {
   static constexpr int VW = DH + kOnesCols;
-  static constexpr uint32_t kS = 0, kP = kNK, kO = kNK + kNK / 2, kMerged = kO + VW;
-  static constexpr int kTotal = kNK + kNK / 2 + VW + DH / 2;
+  // kDbuf: S buffers at 0 and kNK, P at +kNK/2 inside the chunk's S buffer
+  static constexpr uint32_t kS = 0, kP = kDbuf ? kNK / 2 : kNK,
+                            kO = kDbuf ? 2 * kNK : kNK + kNK / 2, kMerged = kO + VW;
+  static constexpr int kTotal = (kDbuf ? 2 * kNK : kNK + kNK / 2) + VW + DH / 2;
 };
 template <int DH, int HP, int NP>
 constexpr int tmem_alloc_cols() {
@@ -431,7 +446,8 @@ struct Pipe {
   int32_t seg_cum[kMaxEnt];
   ChunkDesc desc[kStages];
   float xmax[kSplit > 1 ? 2 : 1][HP][kSplit][kM];   // split: partial row maxima, by chunk parity
-  uint64_t kv_full[kStages], kv_empty[kStages], s_full[HP], s_free[HP], p_full[HP], o_full[HP],
+  uint64_t kv_full[kStages], kv_empty[kStages], s_full[2 * HP], s_free[HP], p_full[2 * HP],
+      o_full[HP],
       q_full[2], q_empty[2];
 };
 
@@ -499,9 +515,11 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       mbar_init(&S.kv_empty[i], HP);   // one commit per head-tile's MMA warp
     }
     for (int hh = 0; hh < HP; ++hh) {
-      mbar_init(&S.s_full[hh], 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&S.s_full[2 * hh + b], 1);
+        mbar_init(&S.p_full[2 * hh + b], 128 * kSplit);
+      }
       mbar_init(&S.s_free[hh], 128 * kSplit);
-      mbar_init(&S.p_full[hh], 128 * kSplit);
       mbar_init(&S.o_full[hh], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -778,6 +796,11 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     const uint32_t id_pv = idesc_bf16(kM, VW, 1);   // [O | rowsum] += P . [V | ones]
     const uint32_t t_s = tmem + hh * HC + HCols::kS, t_p = tmem + hh * HC + HCols::kP,
                    t_o = tmem + hh * HC + HCols::kO;
+    // S / P of chunk cc (kDbuf: the chunk's buffer) and its barriers
+    auto sbuf = [&](uint32_t cc) { return kDbuf ? (cc & 1u) * (uint32_t)kNK : 0u; };
+    auto sfull = [&](uint32_t cc) { return &S.s_full[kDbuf ? 2 * hh + (cc & 1) : 2 * hh]; };
+    auto pfull = [&](uint32_t cc) { return &S.p_full[kDbuf ? 2 * hh + (cc & 1) : 2 * hh]; };
+    auto bpar = [&](uint32_t cc) { return kDbuf ? (cc >> 1) & 1u : cc & 1u; };
     // S = Q K^T for chunk cc into this head-tile's S columns
     auto issue_qk = [&](uint32_t cc) {
       const int st = cc % kStages;
@@ -794,13 +817,20 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       if (elect_one_sync()) {
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(t_s, a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16), id, kk > 0);
-        mma_commit(&S.s_full[hh]);
+          mma_bf16(t_s + sbuf(cc), a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16), id,
+                   kk > 0);
+        mma_commit(sfull(cc));
       }
       __syncwarp();
       if (lane == 0 && hh == 0) trace(trp, cc, 2);
     };
     issue_qk(0);
+    // kDbuf: QK(1) now; afterwards QK(c+2) right after PV(c)
+    bool next_last = (S.desc[0].flags & kFLastOverall) != 0;   // is chunk c+1 past the end?
+    if (kDbuf && !next_last) {
+      issue_qk(1);
+      next_last = (S.desc[1 % kStages].flags & kFLastOverall) != 0;
+    }
     // per chunk: S(c+1) = Q K^T as soon as the softmax has S(c) in registers
     // (s_free), then PV(c) accumulates P(c).[V|ones] into the branch's O as
     // soon as P(c) is written (p_full)
@@ -813,11 +843,11 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const uint32_t acc0 = (fl & kFFirstBranch) ? 0u : 1u;
       const int nk = D.ncols / 16;
       const int qb = D.qb;
-      if (!last) {
+      if (!kDbuf && !last) {
         mbar_wait(&S.s_free[hh], c & 1);
         issue_qk(c + 1);
       }
-      mbar_wait(&S.p_full[hh], c & 1);
+      mbar_wait(pfull(c), bpar(c));
       if (lane == 0 && hh == 0) trace(trp, c, 5);
       tc_after_sync();
       const uint64_t vdesc = sdesc(smem_u32(S.v[st][hh]), 16 * VW, 128);
@@ -825,7 +855,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
 #pragma unroll
         for (int kk = 0; kk < kGroups; ++kk)
           if (kk < nk)
-            mma_bf16_ts(t_o, t_p + kk * 8, vdesc + (uint64_t)(kk * 2 * VW), id_pv,
+            mma_bf16_ts(t_o, t_p + sbuf(c) + kk * 8, vdesc + (uint64_t)(kk * 2 * VW), id_pv,
                         kk > 0 ? 1u : acc0);
         mma_commit(&S.o_full[hh]);
         if (last_in_item) mma_commit(&S.q_empty[qb]);
@@ -833,6 +863,14 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       }
       __syncwarp();
       if (lane == 0 && hh == 0) trace(trp, c, 6);
+      if (kDbuf && !last && !next_last) {
+        // chunk c+2 exists: its S goes into the buffer PV(c) just read (in
+        // issue order, so after PV(c)); the softmax released S(c) before P(c)
+        issue_qk(c + 2);
+        next_last = (S.desc[(c + 2) % kStages].flags & kFLastOverall) != 0;
+      } else if (kDbuf) {
+        next_last = true;
+      }
       ++c;
       if (last) break;
     }
@@ -948,7 +986,10 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     };
 
     for (;;) {
-      mbar_wait(&S.s_full[hh], c & 1);
+      mbar_wait(&S.s_full[kDbuf ? 2 * hh + (c & 1) : 2 * hh], kDbuf ? (c >> 1) & 1 : c & 1);
+      // this chunk's S (and, kDbuf, P) columns
+      const uint32_t tSc = tS + (kDbuf ? (c & 1u) * (uint32_t)kNK : 0u);
+      const uint32_t tPc = kDbuf ? tSc + HCols::kP : tP;
       if (tid == 0) trace(trp, c, 3);
       tc_after_sync();
       // chunk plan (a few wide shared loads) and S pieces 0,1 in flight together
@@ -959,8 +1000,8 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const int ncols = hdr0.x;
       uint32_t sa[32], sb[32];
       const int pcb = 2 * half;   // first 32-key piece of this warp (split: 0 or 2)
-      if (kSplit == 1 || ncols > 32 * pcb) tmem_ld32(tS + HCols::kS + 32 * pcb, sa);
-      if (ncols > 32 * (pcb + 1)) tmem_ld32(tS + HCols::kS + 32 * (pcb + 1), sb);
+      if (kSplit == 1 || ncols > 32 * pcb) tmem_ld32(tSc + HCols::kS + 32 * pcb, sa);
+      if (ncols > 32 * (pcb + 1)) tmem_ld32(tSc + HCols::kS + 32 * (pcb + 1), sb);
 #ifdef LSRM_TRACE_LD
       tmem_wait_ld();
       if (tid == 0) trace(trp, c, 1);
@@ -1068,11 +1109,11 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       zero8(w + 8);                                                            \
     }                                                                          \
     wait_pv();                                                                 \
-    tmem_st16(tP + 16 * (pc), w);                                              \
+    tmem_st16(tPc + 16 * (pc), w);                                              \
   }
 #if LSRM_SPLIT_RELOAD
         if (has0) {
-          tmem_ld32(tS + HCols::kS + 32 * pcb, sa);
+          tmem_ld32(tSc + HCols::kS + 32 * pcb, sa);
           tmem_wait_ld();
           if (!has1) {
             tc_before_sync();
@@ -1081,7 +1122,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           LSRM_SPLIT_PIECE(sa, pcb)
         }
         if (has1) {
-          tmem_ld32(tS + HCols::kS + 32 * (pcb + 1), sa);
+          tmem_ld32(tSc + HCols::kS + 32 * (pcb + 1), sa);
           tmem_wait_ld();
           tc_before_sync();
           mbar_arrive(&S.s_free[hh]);
@@ -1120,9 +1161,29 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
         }
         const bool hi = ncols > 64;   // pieces 2,3 end up in registers
         if (tid == 0) trace(trp, c, 9);
+#if LSRM_HOLD4
+        // all four pieces stay in registers: S(c) is released to QK(c+1)
+        // right after the max pass instead of after a reload mid-exp-phase
+        uint32_t sc[32], sd[32];
         if (hi) {
-          tmem_ld32(tS + HCols::kS + 64, sa);
-          if (ncols > 96) tmem_ld32(tS + HCols::kS + 96, sb);
+          tmem_ld32(tSc + HCols::kS + 64, sc);
+          if (ncols > 96) tmem_ld32(tSc + HCols::kS + 96, sd);
+          tmem_wait_ld();
+          tc_before_sync();
+          mbar_arrive(&S.s_free[hh]);
+          if (LSRM_LIVE(2)) {
+            LSRM_MAX(sc, 0, 4)
+            LSRM_MAX(sc, 16, 5)
+          }
+          if (ncols > 96 && LSRM_LIVE(3)) {
+            LSRM_MAX(sd, 0, 6)
+            LSRM_MAX(sd, 16, 7)
+          }
+        } else {
+#else
+        if (hi) {
+          tmem_ld32(tSc + HCols::kS + 64, sa);
+          if (ncols > 96) tmem_ld32(tSc + HCols::kS + 96, sb);
           tmem_wait_ld();
           if (LSRM_LIVE(2)) {
             LSRM_MAX(sa, 0, 4)
@@ -1133,6 +1194,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
             LSRM_MAX(sb, 16, 7)
           }
         } else {
+#endif
           tc_before_sync();
           mbar_arrive(&S.s_free[hh]);   // S(c) fully in registers: QK(c+1) may overwrite it
         }
@@ -1206,18 +1268,25 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     }                                                                          \
     pp_pass(lp_);                                                              \
     wait_pv();                                                                 \
-    tmem_st16(tP + 16 * (pc), w);                                              \
+    tmem_st16(tPc + 16 * (pc), w);                                              \
   }
+#if LSRM_HOLD4
+        if (hi) {
+          LSRM_EXP_PIECE(sc, 2)
+          if (ncols > 96) LSRM_EXP_PIECE(sd, 3)
+        }
+#else
         if (hi) {
           LSRM_EXP_PIECE(sa, 2)
           if (ncols > 96) LSRM_EXP_PIECE(sb, 3)
-          tmem_ld32(tS + HCols::kS, sa);   // pieces 0,1 again (both full: ncols > 64)
-          tmem_ld32(tS + HCols::kS + 32, sb);
+          tmem_ld32(tSc + HCols::kS, sa);   // pieces 0,1 again (both full: ncols > 64)
+          tmem_ld32(tSc + HCols::kS + 32, sb);
           tmem_wait_ld();
           tc_before_sync();
           mbar_arrive(&S.s_free[hh]);
           if (tid == 0) trace(trp, c, 12);
         }
+#endif
         LSRM_EXP_PIECE(sa, 0)
         if (ncols > 32) LSRM_EXP_PIECE(sb, 1)
 #undef LSRM_EXP_PIECE
@@ -1250,15 +1319,15 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     }                                                                         \
     pp_pass(last_all && ++pdone == n_pc);                                     \
     if (tid == 0) trace(trp, c, 18 + 4 * (pc));                               \
-    tmem_st16(tP + 16 * (pc), w);                                             \
+    tmem_st16(tPc + 16 * (pc), w);                                             \
     if (tid == 0) trace(trp, c, 19 + 4 * (pc));                               \
   }
         LSRM_STREAM_PIECE(sa, 0)
         if (tid == 0) trace(trp, c, 9);
-        if (ncols > 64) tmem_ld32(tS + HCols::kS + 64, sa);
+        if (ncols > 64) tmem_ld32(tSc + HCols::kS + 64, sa);
         if (ncols > 32) LSRM_STREAM_PIECE(sb, 1)
         if (tid == 0) trace(trp, c, 10);
-        if (ncols > 96) tmem_ld32(tS + HCols::kS + 96, sb);
+        if (ncols > 96) tmem_ld32(tSc + HCols::kS + 96, sb);
         if (ncols > 64) {
           tmem_wait_ld();
           if (tid == 0) trace(trp, c, 12);
@@ -1293,7 +1362,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
 #pragma unroll
           for (int pc = 0; pc < kGroups / 2; ++pc) {
             if (pc * 32 < ncols) {
-              tmem_ld32(tS + HCols::kS + 32 * pc, sa);
+              tmem_ld32(tSc + HCols::kS + 32 * pc, sa);
               tmem_wait_ld();
               uint32_t w[16];
 #pragma unroll
@@ -1305,7 +1374,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
                   zero8(w + 8 * hf);
                 }
               }
-              tmem_st16(tP + 16 * pc, w);
+              tmem_st16(tPc + 16 * pc, w);
             }
           }
           m_run = m_use;
@@ -1322,7 +1391,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       }
       if (tid == 0) trace(trp, c, 15);
       tc_before_sync();
-      mbar_arrive(&S.p_full[hh]);
+      mbar_arrive(&S.p_full[kDbuf ? 2 * hh + (c & 1) : 2 * hh]);
       if (tid == 0) trace(trp, c, 4);
       if (last_br) {
         if (row_ok) {   // stage this branch's gate logits for its epilogue
@@ -1437,7 +1506,7 @@ static int launch(const Launch& L, int dh, int hkv, int64_t n_tiles_static, void
 #ifdef LSRM_HEADPAIR
   const int hp = (!dyn && dh == 32 && hkv % 2 == 0) ? 2 : 1, np_ = hp == 2 ? 1 : (dh == 32 ? 2 : 1);
 #else
-  const int hp = 1, np_ = dh == 32 ? 2 : 1;
+  const int hp = 1, np_ = (dh == 32 && !kDbuf) ? 2 : 1;
 #endif
   const int64_t n_items = dyn ? L.n_order : n_tiles_static * (hkv / hp);
   if (n_items == 0) return LSRM_OK;
@@ -1451,8 +1520,10 @@ static int launch(const Launch& L, int dh, int hkv, int64_t n_tiles_static, void
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     nsa_fused_kernel<D, HP, NP><<<grid, threads_of<HP, NP>(), smem, st>>>(L);               \
   } else
+#if !LSRM_DBUF
   LSRM_TC_CASE(32, 1, 2)
   LSRM_TC_CASE(32, 2, 1)
+#endif
   LSRM_TC_CASE(32, 1, 1)
   LSRM_TC_CASE(64, 1, 1)
   return set_error(LSRM_E_CONFIG, "tcgen05 path: head_dim %d not in {32,64}", dh);
