@@ -46,7 +46,15 @@ namespace lsrm {
 namespace tc {
 
 constexpr int kM = 128;          // MMA rows per head-tile
-constexpr int kNK = 128;         // keys per chunk
+#ifndef LSRM_DBUF
+#define LSRM_DBUF 0
+#endif
+#ifndef LSRM_DBUF_NK
+#define LSRM_DBUF_NK 96
+#endif
+// keys per chunk; double-buffered S (LSRM_DBUF) uses 96 so that two S
+// buffers (P inside) + [O | rowsum] + merge fit 256 TMEM columns per pipeline
+constexpr int kNK = LSRM_DBUF ? LSRM_DBUF_NK : 128;
 constexpr int kGroups = kNK / 16;
 constexpr int kMaxEnt = 256;     // tile tokens * selected rows
 
@@ -276,9 +284,6 @@ constexpr int kStages = LSRM_STAGES;   // K/V ring depth (each stage holds every
 #endif
 #ifndef LSRM_HOLD4
 #define LSRM_HOLD4 0
-#endif
-#ifndef LSRM_DBUF
-#define LSRM_DBUF 0
 #endif
 // Double-buffered S (one pipeline per CTA): QK(c+2) is issued right after
 // PV(c) into the buffer chunk c used, so S(c+1) is ready before the softmax
@@ -1506,7 +1511,7 @@ static int launch(const Launch& L, int dh, int hkv, int64_t n_tiles_static, void
 #ifdef LSRM_HEADPAIR
   const int hp = (!dyn && dh == 32 && hkv % 2 == 0) ? 2 : 1, np_ = hp == 2 ? 1 : (dh == 32 ? 2 : 1);
 #else
-  const int hp = 1, np_ = (dh == 32 && !kDbuf) ? 2 : 1;
+  const int hp = 1, np_ = dh == 32 ? 2 : 1;
 #endif
   const int64_t n_items = dyn ? L.n_order : n_tiles_static * (hkv / hp);
   if (n_items == 0) return LSRM_OK;
@@ -1520,8 +1525,8 @@ static int launch(const Launch& L, int dh, int hkv, int64_t n_tiles_static, void
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     nsa_fused_kernel<D, HP, NP><<<grid, threads_of<HP, NP>(), smem, st>>>(L);               \
   } else
-#if !LSRM_DBUF
   LSRM_TC_CASE(32, 1, 2)
+#if !LSRM_DBUF
   LSRM_TC_CASE(32, 2, 1)
 #endif
   LSRM_TC_CASE(32, 1, 1)
