@@ -200,6 +200,35 @@ def test_fp32_nsa_uses_c1(c1, ref_c1):
         assert agree > 0.999, agree
 
 
+def test_fp32_nsa_uses_score_mode_c1(c1):
+    """Score-mode routing (`recon_pipeline.py:457-458`: b_sel instead of a
+    3D selection) through the whole use, vs the oracle's score-mode use."""
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200.workloads import nsa_use_weights
+    params = L.AttentionParams(8, 1, 8)
+    ws = nsa_use_weights(params)
+    ows = {n: O.NsaWeights(w.w_q, w.w_k, w.w_v, w.w_o, w.gate_w, w.gate_b,
+                           ((w.compress.for_k.w1, w.compress.for_k.b1, w.compress.for_k.w2,
+                             w.compress.for_k.b2),
+                            (w.compress.for_v.w1, w.compress.for_v.b1, w.compress.for_v.w2,
+                             w.compress.for_v.b2)), w.n_gates) for n, w in ws.items()}
+    d = 64
+    ones, zeros = np.ones(d, np.float32), np.zeros(d, np.float32)
+    xh = O.layer_norm(c1["x_up"].features, ones, zeros)
+    yh = O.layer_norm(c1["y_up"].features, ones, zeros)
+    pv, pi = c1["pv"], c1["pi"]
+    opv = O.partition_tokens("volume", c1["x_up"].coords, c1["x_up"].grid_res)
+    opi = O.partition_tokens("image", c1["y_up"].coords, c1["y_up"].grid_res)
+    uses = {"v2v": (xh, xh, pv, pv, opv, opv), "v2i": (xh, yh, pv, pi, opv, opi),
+            "i2i": (yh, yh, pi, pi, opi, opi), "i2v": (yh, xh, pi, pv, opi, opv)}
+    for name, (xq, xkv, pq, pkv, oq, okv) in uses.items():
+        got = L.nsa_cross_attention(xq, xkv, pq, pkv, None, ws[name], params, b_sel=4)
+        want = O.nsa_use(xq, xkv, oq, okv, None, ows[name], O.AttentionParams(8, 1, 8),
+                         b_sel=4)
+        err = np.max(np.abs(got.astype(np.float64) - want))
+        assert err < 1e-5, (name, err)
+
+
 def _bf(a):
     return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).float().numpy()
 
