@@ -285,6 +285,11 @@ constexpr int kStages = LSRM_STAGES;   // K/V ring depth (each stage holds every
 #ifndef LSRM_HOLD4
 #define LSRM_HOLD4 0
 #endif
+#ifndef LSRM_EPI_SPLIT
+#define LSRM_EPI_SPLIT 0
+#endif
+// branch epilogue: only the O read precedes the P(c) hand-over
+constexpr bool kEpiSplit = LSRM_EPI_SPLIT;
 // Double-buffered S (one pipeline per CTA): QK(c+2) is issued right after
 // PV(c) into the buffer chunk c used, so S(c+1) is ready before the softmax
 // finishes chunk c.  P(c) is written into the consumed half of S(c)'s buffer
@@ -925,24 +930,33 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
 
     // gate + merge of a finished branch (nsa_attention.py:266-284); the
     // running merge is f16 in TMEM; at an item end the merged row is stored
-    auto epilogue = [&](uint32_t pc) {
+    // The epilogue in two halves: epi_load reads the branch's O (this warp's
+    // columns) and row sum into registers - the part that must precede PV(c),
+    // which overwrites O; epi_finish does the gate, the merge and the stores.
+    auto epi_load = [&](uint32_t pc, uint32_t* eo) {
       mbar_wait(&S.o_full[hh], pc & 1);   // PV(pc) complete
       if (tid == 0) trace(trp, pc, 7);
       tc_after_sync();
-      cp_async_wait_all();                // gate logits staged by this thread
-      uint32_t rl[1];
-      tmem_ld_cols<1>(tO + DH, rl);
+      tmem_ld_cols<1>(tO + DH, eo + kOCols);
+#pragma unroll
+      for (int cq = 0; cq < kOCols; cq += 16) tmem_ld16_nowait(tO + oc0 + cq, eo + cq);
       tmem_wait_ld();
-      const float inv = rowok_pend ? 1.f / __uint_as_float(rl[0]) : 0.f;
+    };
+    auto epi_finish = [&](const uint32_t* eo) {
+      cp_async_wait_all();                // gate logits staged by this thread
+      const float inv = rowok_pend ? 1.f / __uint_as_float(eo[kOCols]) : 0.f;
       const float* bp =
           bias_all ? bias_all + ((int64_t)br_pend * P.hq + head_pend) * bias_ld : nullptr;
 #pragma unroll
       for (int cq = 0; cq < kOCols; cq += 16) {   // 16 columns at a time (registers)
         const int c0 = oc0 + cq;
         uint32_t r[16], mr[8];
-        tmem_ld16_nowait(tO + c0, r);
-        if (br_pend > 0) tmem_ld_cols<8>(tM + c0 / 2, mr);
-        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r[j] = eo[cq + j];
+        if (br_pend > 0) {
+          tmem_ld_cols<8>(tM + c0 / 2, mr);
+          tmem_wait_ld();
+        }
 #pragma unroll
         for (int k8 = 0; k8 < 2; ++k8) {
           const uint4 raw = *reinterpret_cast<const uint4*>(gate_s + c0 + 8 * k8);
@@ -988,6 +1002,11 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
         }
       }
       if (!lastit_pend) tmem_wait_st();
+    };
+    auto epilogue = [&](uint32_t pc) {
+      uint32_t eo[kOCols + 1];
+      epi_load(pc, eo);
+      epi_finish(eo);
     };
 
     for (;;) {
@@ -1390,13 +1409,24 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       if (tid == 0) trace(trp, c, 13);
       tmem_wait_st();
       if (tid == 0) trace(trp, c, 14);
-      if (epi_pend) {   // the previous branch's O must be read before PV(c) overwrites it
-        epilogue(c - 1);
+      if (epi_pend && kEpiSplit) {
+        // the previous branch's O into registers, release P(c) to PV(c), then
+        // gate / merge / store off the MMA's critical path
+        uint32_t eo[kOCols + 1];
+        epi_load(c - 1, eo);
+        tc_before_sync();
+        mbar_arrive(&S.p_full[kDbuf ? 2 * hh + (c & 1) : 2 * hh]);
+        epi_finish(eo);
         epi_pend = false;
+      } else {
+        if (epi_pend) {   // the previous branch's O must be read before PV(c) overwrites it
+          epilogue(c - 1);
+          epi_pend = false;
+        }
+        if (tid == 0) trace(trp, c, 15);
+        tc_before_sync();
+        mbar_arrive(&S.p_full[kDbuf ? 2 * hh + (c & 1) : 2 * hh]);
       }
-      if (tid == 0) trace(trp, c, 15);
-      tc_before_sync();
-      mbar_arrive(&S.p_full[kDbuf ? 2 * hh + (c & 1) : 2 * hh]);
       if (tid == 0) trace(trp, c, 4);
       if (last_br) {
         if (row_ok) {   // stage this branch's gate logits for its epilogue
