@@ -149,7 +149,7 @@ def cpu_oracle_sample(wl_name="c3", frac=1.0 / 32, seed=0):
         O.combine_branches(xq[qids], outs, w)
         t_total += time.perf_counter() - t0
         done += n
-    desc = (f"oracle 4 NSA uses, C3 paper heads 32/2/32 d=1024, first query blocks holding "
+    desc = (f"oracle 4 NSA uses, {wl_name.upper()} paper heads 32/2/32 d=1024, first query blocks holding "
             f"~{frac:.4f} of each use's queries ({done} queries) against the full KV side")
     return done, t_total, desc
 
@@ -189,11 +189,11 @@ def run_reference(args):
     rank, _, ws = dist_env()
     if rank != 0:
         return
-    for _ in range(args.warmup_ref):
-        pass
+    # the same workload our arm runs at this N (C3 on one GPU, C4 under torchrun)
+    wl_name = args.workload or ("c4" if ws > 1 else "c3")
     times, tokens, desc = [], 0, ""
     for _ in range(args.steps):
-        tokens, secs, desc = cpu_oracle_sample(frac=args.ref_frac)
+        tokens, secs, desc = cpu_oracle_sample(wl_name=wl_name, frac=args.ref_frac)
         times.append(secs)
     v = tokens / float(np.mean(times))
     hi = host_info()
@@ -202,8 +202,8 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference fixture geometry, tagged Philox features/weights)",
-            "config": {"workload": WORKLOAD_DESC["c3"], "parallelism": "cpu (host cores)",
-                       "sample": desc},
+            "config": {"workload": WORKLOAD_DESC.get(wl_name, wl_name),
+                       "parallelism": "cpu (host cores)", "sample": desc},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": hi["cpu_count"],
                              "kind": "port", "sample": desc, "host": hi},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
