@@ -421,8 +421,13 @@ int lsrm_transpose_rows(const int32_t* rows, const int32_t* count, int64_t nq, i
  * do_b = dM g_b,  dz[:, b*d + c] = dM o_b g_b (1 - g_b)   (dz [n, n_gates*d]). */
 int lsrm_gate_merge_bwd_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,
                             int n_gates, const float* o0, const float* o1, const float* o2,
-                            const float* dmerged, int64_t n, int d, float* do0, float* do1,
-                            float* do2, float* dz, void* stream);
+                            const float* dmerged, int64_t n, int d, int fast, float* do0,
+                            float* do1, float* do2, float* dz, void* stream);
+/* Training forward of the gated merge in fp32 (fp32 sigmoid and sum; the
+ * reference-API lsrm_gated_merge_f32 keeps f64): merged = sum_b g_b * o_b. */
+int lsrm_gated_merge_fast_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,
+                              int n_gates, const float* o0, const float* o1, const float* o2,
+                              int64_t n, int d, float* merged, void* stream);
 /* Compression ResBlock under the block mean (block_partition.py:141-158):
  * dr_t = dcmp[row(t)] / occupancy[row(t)];  dx_t += dr_t + (dr_t W2^T * gelu'(z1_t)) W1^T;
  * writes dr, dz1, h = gelu(z1) rows [n, width] for the weight-gradient GEMMs. */

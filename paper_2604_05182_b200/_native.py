@@ -77,7 +77,9 @@ SIGNATURES = {
                                      P, P, I32, P, I32, P, P, P, P, P, P, SZ, P]),
     "lsrm_transpose_rows_workspace": (SZ, [I64, I32]),
     "lsrm_transpose_rows": (I32, [P, P, I64, I32, I32, P, P, P, SZ, P]),
-    "lsrm_gate_merge_bwd_f32": (I32, [P, I64, P, I32, P, P, P, P, I64, I32, P, P, P, P, P]),
+    "lsrm_gate_merge_bwd_f32": (I32, [P, I64, P, I32, P, P, P, P, I64, I32, I32, P, P, P, P,
+                                      P]),
+    "lsrm_gated_merge_fast_f32": (I32, [P, I64, P, I32, P, P, P, I64, I32, P, P]),
     "lsrm_res_block_bwd_f32": (I32, [P, I64, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "lsrm_decode_scatter": (I32, [P, I32, I32, I32, P, P]),
     "lsrm_sparse_features": (I32, [P, P, I64, I32, I32, I64, P, P, P]),

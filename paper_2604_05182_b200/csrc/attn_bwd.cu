@@ -250,11 +250,18 @@ __device__ __forceinline__ double sigmoid_d(double x) {
 
 // merged = sum_b g_b * O_b, g_b = sigmoid(z_b + bias_b):  dO_b = dM g_b,
 // dz_b = dM O_b g_b (1 - g_b)
+template <int NG>
+__device__ __forceinline__ float gate_sig(float z, int fast) {
+  return fast ? 1.f / (1.f + __expf(-z)) : (float)sigmoid_d((double)z);
+}
+
+// dO_b = dM g_b, dz_b = dM O_b g_b (1 - g_b); fast = fp32 sigmoid (training)
+template <int NG>
 __global__ void gate_merge_bwd_kernel(const float* __restrict__ gl, int64_t ld,
-                                      const float* __restrict__ gb, int ng,
+                                      const float* __restrict__ gb,
                                       const float* __restrict__ o0, const float* __restrict__ o1,
                                       const float* __restrict__ o2,
-                                      const float* __restrict__ dm, int64_t n, int d,
+                                      const float* __restrict__ dm, int64_t n, int d, int fast,
                                       float* __restrict__ do0, float* __restrict__ do1,
                                       float* __restrict__ do2, float* __restrict__ dz) {
   const int64_t total = n * d;
@@ -262,15 +269,40 @@ __global__ void gate_merge_bwd_kernel(const float* __restrict__ gl, int64_t ld,
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / d;
     const int c = (int)(e % d);
-    const float* ob[3] = {o0, o1, o2};
-    float* dob[3] = {do0, do1, do2};
     const float g_m = dm[e];
-    for (int b = 0; b < ng; ++b) {
+#pragma unroll
+    for (int b = 0; b < NG; ++b) {
+      const float* ob = b == 0 ? o0 : (b == 1 ? o1 : o2);
+      float* dob = b == 0 ? do0 : (b == 1 ? do1 : do2);
       const float z = gl[i * ld + b * d + c] + (gb ? gb[b * d + c] : 0.f);
-      const float g = (float)sigmoid_d((double)z);
-      dob[b][e] = g_m * g;
-      dz[i * (int64_t)ng * d + b * d + c] = g_m * ob[b][e] * g * (1.f - g);
+      const float g = gate_sig<NG>(z, fast);
+      dob[e] = g_m * g;
+      dz[i * (int64_t)NG * d + b * d + c] = g_m * ob[e] * g * (1.f - g);
     }
+  }
+}
+
+// training forward of the gated merge in fp32: merged = sum_b sigmoid(z_b) O_b
+template <int NG>
+__global__ void gated_merge_fast_kernel(const float* __restrict__ gl, int64_t ld,
+                                        const float* __restrict__ gb,
+                                        const float* __restrict__ o0,
+                                        const float* __restrict__ o1,
+                                        const float* __restrict__ o2, int64_t n, int d,
+                                        float* __restrict__ merged) {
+  const int64_t total = n * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / d;
+    const int c = (int)(e % d);
+    float acc = 0.f;
+#pragma unroll
+    for (int b = 0; b < NG; ++b) {
+      const float* ob = b == 0 ? o0 : (b == 1 ? o1 : o2);
+      const float z = gl[i * ld + b * d + c] + (gb ? gb[b * d + c] : 0.f);
+      acc = fmaf(1.f / (1.f + __expf(-z)), ob[e], acc);
+    }
+    merged[e] = acc;
   }
 }
 
@@ -408,15 +440,43 @@ int lsrm_attention_bwd_f32(int mode, const float* q, const float* dO, const floa
 
 int lsrm_gate_merge_bwd_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,
                             int n_gates, const float* o0, const float* o1, const float* o2,
-                            const float* dmerged, int64_t n, int d, float* do0, float* do1,
-                            float* do2, float* dz, void* stream) {
+                            const float* dmerged, int64_t n, int d, int fast, float* do0,
+                            float* do1, float* do2, float* dz, void* stream) {
   LSRM_REQUIRE(n_gates >= 1 && n_gates <= 3, "n_gates must be 1..3");
   if (n == 0) return LSRM_OK;
   const int64_t total = n * d;
   const unsigned grid = (unsigned)(ceil_div(total, 256) < 148 * 16 ? ceil_div(total, 256) : 148 * 16);
-  gate_merge_bwd_kernel<<<grid, 256, 0, as_stream(stream)>>>(gate_logits, ld_gl, gate_bias,
-                                                             n_gates, o0, o1, o2, dmerged, n, d,
-                                                             do0, do1, do2, dz);
+  cudaStream_t st = as_stream(stream);
+  if (n_gates == 3)
+    gate_merge_bwd_kernel<3><<<grid, 256, 0, st>>>(gate_logits, ld_gl, gate_bias, o0, o1, o2,
+                                                   dmerged, n, d, fast, do0, do1, do2, dz);
+  else if (n_gates == 2)
+    gate_merge_bwd_kernel<2><<<grid, 256, 0, st>>>(gate_logits, ld_gl, gate_bias, o0, o1, o2,
+                                                   dmerged, n, d, fast, do0, do1, do2, dz);
+  else
+    gate_merge_bwd_kernel<1><<<grid, 256, 0, st>>>(gate_logits, ld_gl, gate_bias, o0, o1, o2,
+                                                   dmerged, n, d, fast, do0, do1, do2, dz);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_gated_merge_fast_f32(const float* gate_logits, int64_t ld_gl, const float* gate_bias,
+                              int n_gates, const float* o0, const float* o1, const float* o2,
+                              int64_t n, int d, float* merged, void* stream) {
+  LSRM_REQUIRE(n_gates >= 1 && n_gates <= 3, "n_gates must be 1..3");
+  if (n == 0) return LSRM_OK;
+  const int64_t total = n * d;
+  const unsigned grid = (unsigned)(ceil_div(total, 256) < 148 * 16 ? ceil_div(total, 256) : 148 * 16);
+  cudaStream_t st = as_stream(stream);
+  if (n_gates == 3)
+    gated_merge_fast_kernel<3><<<grid, 256, 0, st>>>(gate_logits, ld_gl, gate_bias, o0, o1, o2,
+                                                     n, d, merged);
+  else if (n_gates == 2)
+    gated_merge_fast_kernel<2><<<grid, 256, 0, st>>>(gate_logits, ld_gl, gate_bias, o0, o1, o2,
+                                                     n, d, merged);
+  else
+    gated_merge_fast_kernel<1><<<grid, 256, 0, st>>>(gate_logits, ld_gl, gate_bias, o0, o1, o2,
+                                                     n, d, merged);
   LSRM_LAUNCHED();
   return LSRM_OK;
 }

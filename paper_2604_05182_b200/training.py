@@ -102,9 +102,9 @@ def _forward(spec: _Spec, x, kv, P):
     logits = mm(x, P["gate_w"])
     merged = D.empty((n, d), torch.float32)
     o = [t.view(n, d) for t in outs] + [None] * (3 - len(outs))
-    call("lsrm_gated_merge_f32", logits.data_ptr(), logits.stride(0), P["gate_b"].data_ptr(),
-         spec.n_gates, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]), n, d, merged.data_ptr(),
-         D.stream())
+    call("lsrm_gated_merge_fast_f32" if fast else "lsrm_gated_merge_f32", logits.data_ptr(),
+         logits.stride(0), P["gate_b"].data_ptr(), spec.n_gates, D.ptr(o[0]), D.ptr(o[1]),
+         D.ptr(o[2]), n, d, merged.data_ptr(), D.stream())
     out = mm(merged, P["w_o"])
     saved.update(outs=o, logits=logits, merged=merged)
     return out, saved
@@ -141,7 +141,8 @@ def _backward(spec: _Spec, P, s, dout):
     o = s["outs"]
     call("lsrm_gate_merge_bwd_f32", s["logits"].data_ptr(), s["logits"].stride(0),
          P["gate_b"].data_ptr(), ng, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]),
-         dmerged.data_ptr(), n, d, D.ptr(do[0]), D.ptr(do[1]), D.ptr(do[2]), dz.data_ptr(), st)
+         dmerged.data_ptr(), n, d, int(fast), D.ptr(do[0]), D.ptr(do[1]), D.ptr(do[2]),
+         dz.data_ptr(), st)
     g["gate_w"] = gx(s["x"], dz, trans_a=True)
     g["gate_b"] = _colsum(dz)
     dx = gx(dz, P["gate_w"], trans_b=True)
