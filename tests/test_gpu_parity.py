@@ -308,16 +308,18 @@ def test_tc_fused_attention_vs_oracle(c1):
         assert rel < 1e-2 and mx < 2e-2, (name, rel, mx)
 
 
-def test_engine_layer_vs_fp32_path(c1):
+@pytest.mark.parametrize("heads", [(32, 2, 32), (16, 2, 64), (16, 4, 32)])
+def test_engine_layer_vs_fp32_path(c1, heads):
     """Whole bf16 layer (4 uses: GEMMs + compression + fused attention + W_o)
-    vs the fp32 reference-API path on the same inputs, paper heads."""
+    vs the fp32 reference-API path on the same inputs: paper heads, head_dim
+    64 (one pipeline per CTA) and group size 4 (32-token query tiles)."""
     import paper_2604_05182_b200 as L
     from paper_2604_05182_b200 import _dev as D, _ops
     from paper_2604_05182_b200.engine import SparseLayerEngine, USES
     from paper_2604_05182_b200.workloads import coarse_inputs, nsa_use_weights
-    params = L.AttentionParams(32, 2, 32)
+    params = L.AttentionParams(*heads)
     wl = c1["wl"]
-    x_d, y_d, pe_v, pe_i = coarse_inputs(wl, 1024)
+    x_d, y_d, pe_v, pe_i = coarse_inputs(wl, params.model_dim)
     x_up, y_up = L.upsample_select_tokens(x_d, y_d, wl.vol_mask, wl.img_mask, pe_v, pe_i,
                                           wl.factor_vol, wl.factor_img)
     pv, pi = L.partition(x_up), L.partition(y_up)
@@ -327,7 +329,7 @@ def test_engine_layer_vs_fp32_path(c1):
     g = np.random.default_rng(11)
     for wu in ws.values():   # nonzero gate biases: the engine folds them into its GEMM
         wu.gate_b = (g.standard_normal(wu.gate_b.shape) * 0.5).astype(np.float32)
-    d = 1024
+    d = params.model_dim
     ones, zeros = np.ones(d, np.float32), np.zeros(d, np.float32)
     xh = O.layer_norm(x_up.features, ones, zeros)
     yh = O.layer_norm(y_up.features, ones, zeros)
