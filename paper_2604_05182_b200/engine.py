@@ -186,7 +186,7 @@ class SparseLayerEngine:
 
     def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
                  weights: dict, params: AttentionParams, shard: dict = None,
-                 extra_cols: dict = None):
+                 extra_cols: dict = None, pool: dict = None):
         require(params.head_dim in (32, 64), "bf16 engine: head_dim must be 32 or 64")
         G = params.group_size
         require(128 % G == 0 and G >= 4, "bf16 engine: (n_q_heads/n_kv_heads) must be in 4..128 "
@@ -249,26 +249,38 @@ class SparseLayerEngine:
             self.kmax[use] = int(rb.shape[1])
             self.tiles[use] = D.dev(query_tiles(parts[qs], G, ng == 3,
                                                 mq.owned if mq.sharded else None))
-        # work buffers
+        # work buffers (a `pool` shared by engines that run one after another,
+        # e.g. the layers of a stage, hands out the same tensors by key)
         hkv, dh = params.n_kv_heads, params.head_dim
         self.buf = {}
+
+        def alloc(key, shape, dtype, zero=False):
+            t = pool.get(key) if pool is not None else None
+            if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+                t = D.zeros(shape, dtype) if zero else D.empty(shape, dtype)
+                if pool is not None:
+                    pool[key] = t
+            return t
         for s in ("x", "y"):
             m = self.meta[s]
-            self.buf[("Y", s)] = D.empty((m.n_loc, ncol[s]), torch.bfloat16)
+            self.buf[("Y", s)] = alloc(("Y", s), (m.n_loc, ncol[s]), torch.bfloat16)
         for use in USES:
             qs, ks, _ = USE_GEOM[use]
             m = self.meta[ks]
             # global KV of this use (zeroed once: padding rows, their ones
             # columns and the compressed padding rows stay 0)
-            self.buf[("k_il", use)] = D.zeros((hkv, m.n_rows_pad, dh), torch.bfloat16)
-            self.buf[("v_il", use)] = D.zeros((hkv, m.n_rows_pad, dh + ONES_COLS), torch.bfloat16)
-            bpad = (m.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
-            self.buf[("kc_il", use)] = D.zeros((hkv, bpad, dh), torch.bfloat16)
-            self.buf[("vc_il", use)] = D.zeros((hkv, bpad, dh + ONES_COLS), torch.bfloat16)
-            self.buf[("kc", use)] = D.empty((m.n_blocks, w), torch.float32)
-            self.buf[("vc", use)] = D.empty((m.n_blocks, w), torch.float32)
-            self.buf[("merged", use)] = D.empty((self.meta[qs].n_loc, d), torch.bfloat16)
-            self.buf[("out", use)] = D.empty((self.meta[qs].n_loc, d), torch.bfloat16)
+            for key, shape, zero in (
+                    (("k_il", use), (hkv, m.n_rows_pad, dh), True),
+                    (("v_il", use), (hkv, m.n_rows_pad, dh + ONES_COLS), True),
+                    (("kc_il", use), (hkv, (m.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD, dh),
+                     True),
+                    (("vc_il", use), (hkv, (m.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD,
+                                      dh + ONES_COLS), True),
+                    (("merged", use), (self.meta[qs].n_loc, d), False),
+                    (("out", use), (self.meta[qs].n_loc, d), False)):
+                self.buf[key] = alloc(key, shape, torch.bfloat16, zero)
+            self.buf[("kc", use)] = alloc(("kc", use), (m.n_blocks, w), torch.float32)
+            self.buf[("vc", use)] = alloc(("vc", use), (m.n_blocks, w), torch.float32)
             m = self.meta[ks]
             if m.sharded:
                 # rank-local compact KV shard of this use, packed in ONE buffer

@@ -247,10 +247,10 @@ class SparseBlockEngine:
     logits."""
 
     def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
-                 w: SparseBlockWeights, params: AttentionParams):
+                 w: SparseBlockWeights, params: AttentionParams, pool: dict = None):
         self.w, self.params = w, params
         self.layer = SparseLayerEngine(part_vol, part_img, plan_rows, w.uses(), params,
-                                       extra_cols={"x": w.gate_x_w, "y": w.gate_y_w})
+                                       extra_cols={"x": w.gate_x_w, "y": w.gate_y_w}, pool=pool)
         self.bf = {name: D.weight(getattr(getattr(w, f), n), torch.bfloat16)
                    for name, f, n in (("fx1", "ffn_x", "w1"), ("fx2", "ffn_x", "w2"),
                                       ("fy1", "ffn_y", "w1"), ("fy2", "ffn_y", "w2"))}
@@ -555,3 +555,31 @@ def decode_point(fv: FeatureVolume, heads: DecoderHeads, p, mask=None):
     """`recon_pipeline.py:368-371`."""
     z, s = decode_points(fv, heads, np.asarray(p, np.float64).reshape(1, 3), mask)
     return z[0], float(s[0])
+
+
+class SparseStageEngine:
+    """The Stage-2 sparse stage (`recon_pipeline.py:500-512`) on the bf16
+    engine: `depth` SparseBlockEngines over one routing, sharing their work
+    buffers (layers run one after another; only the weights are per layer).
+    forward(x_up, y_up) takes the fine tokens' f32 features in block-major
+    order and returns the stage output x_s, y_s (f32, block-major): zero
+    state, per-layer injection of the frozen inputs, inputs added at the end."""
+
+    def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
+                 weights: list, params: AttentionParams):
+        self.pool = {}
+        self.blocks = [SparseBlockEngine(part_vol, part_img, plan_rows, w, params, pool=self.pool)
+                       for w in weights]
+        self.inj = [(D.weight(w.inj_x, torch.bfloat16), D.weight(w.inj_y, torch.bfloat16))
+                    for w in weights]
+
+    def forward(self, x_up: torch.Tensor, y_up: torch.Tensor):
+        xb, yb = _ops.cast(x_up, torch.bfloat16), _ops.cast(y_up, torch.bfloat16)
+        x, y = torch.zeros_like(x_up), torch.zeros_like(y_up)
+        for blk, (ix, iy) in zip(self.blocks, self.inj):
+            xi = _ops.gemm(xb, ix, out_dtype=torch.float32)
+            yi = _ops.gemm(yb, iy, out_dtype=torch.float32)
+            x, y = blk.forward(x, y, xi, yi)
+        zero = torch.zeros(x_up.shape[1], dtype=torch.float32, device=x_up.device)
+        return (_bias_act(0, x, zero, 0, residual=x_up, out_dtype=torch.float32),
+                _bias_act(0, y, zero, 0, residual=y_up, out_dtype=torch.float32))

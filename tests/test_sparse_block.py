@@ -115,3 +115,34 @@ def test_parallel_sparse_stage_matches_reference(c1_tokens, ref_c1):
     assert np.max(np.abs(xs.astype(np.float64) - want_x)) < 1e-5
     assert np.max(np.abs(ys.astype(np.float64) - want_y)) < 1e-5
     assert ["%s,%s,%d,%d,%d" % r for r in topo.message_log] == list(ref_c1["par3_log"])
+
+
+def test_sparse_stage_engine_vs_fp32_stage(c1_tokens):
+    """Two-layer bf16 SparseStageEngine (shared work buffers) against the
+    fp32 reference-API `sparse_stage_forward` on the same routing, paper
+    heads at C1 geometry."""
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200 import _dev as D, _ops
+    from paper_2604_05182_b200 import recon_pipeline as R
+    params = L.AttentionParams(32, 2, 32)
+    wl = c1_tokens["wl"]
+    x_up, y_up = c1_tokens[1024]
+    pv, pi = L.partition(x_up), L.partition(y_up)
+    plan = L.build_routing_plan(L.volume_token_coords(x_up), wl.img_points, pv, pi,
+                                wl.cameras, L.RoutingBudgets())
+    ws = [R.init_sparse_block(0, params, m) for m in range(2)]
+    eng = R.SparseStageEngine(pv, pi, plan.device_rows, ws, params)
+    tv, ti = pv.dev("block_token_ids"), pi.dev("block_token_ids")
+    xs_b, ys_b = eng.forward(_ops.gather_rows(D.dev(x_up.features), tv),
+                             _ops.gather_rows(D.dev(y_up.features), ti))
+    xs, ys = torch.empty_like(xs_b), torch.empty_like(ys_b)
+    _ops.scatter_rows(xs_b, tv, xs)
+    _ops.scatter_rows(ys_b, ti, ys)
+    ctx = R.build_sparse_context(pv, pi, selections=plan.tables)
+    rx, ry = R.sparse_stage_forward(x_up, y_up, ws, ctx, params)
+    for name, got, ref, base in (("x", xs, rx, x_up.features), ("y", ys, ry, y_up.features)):
+        got = D.host(got).astype(np.float64)
+        ref = np.asarray(ref, np.float64)
+        upd = np.linalg.norm((got - base) - (ref - base)) / np.linalg.norm(ref - base)
+        print(f"stage engine {name}: update rel-L2 {upd:.3e}")
+        assert upd < 2e-2, (name, upd)
