@@ -1,22 +1,32 @@
-"""Deterministic tagged Philox streams, identical to `lsrm/rng.py:16-41`, so
-weights and synthetic inputs built here equal the reference's bit for bit."""
+"""Tagged counter-based random streams, draw-for-draw equal to the
+reference's (`lsrm/rng.py:16-41`), so synthetic weights and inputs built
+here are the reference's bit for bit.
+
+A stream is NumPy's Philox keyed by the integer seed, with counter word 0
+set to the first 8 bytes (little-endian) of sha256 over the "/"-joined tag
+path; the other counter words are 0.
+"""
 
 import hashlib
 
 import numpy as np
 
+_KEY_MASK = (1 << 64) - 1
+
 
 def tag_counter(*tags) -> int:
-    h = hashlib.sha256("/".join(str(t) for t in tags).encode("utf-8")).digest()
-    return int.from_bytes(h[:8], "little")
+    path = "/".join(map(str, tags)).encode("utf-8")
+    return int.from_bytes(hashlib.sha256(path).digest()[:8], "little")
 
 
 def stream(seed: int, *tags) -> np.random.Generator:
     if not isinstance(seed, (int, np.integer)):
-        raise TypeError(f"seed must be an int, got {type(seed).__name__}")
-    return np.random.Generator(np.random.Philox(
-        key=int(seed) & 0xFFFFFFFFFFFFFFFF, counter=[tag_counter(*tags), 0, 0, 0]))
+        raise TypeError(f"stream seed has to be an integer (got {type(seed).__name__})")
+    philox = np.random.Philox(key=int(seed) & _KEY_MASK, counter=(tag_counter(*tags), 0, 0, 0))
+    return np.random.Generator(philox)
 
 
 def normal_f32(seed: int, shape, scale: float = 1.0, *tags) -> np.ndarray:
-    return (stream(seed, *tags).standard_normal(shape) * scale).astype(np.float32)
+    """N(0, scale^2) draws of `shape`, stored as float32."""
+    draws = stream(seed, *tags).standard_normal(shape)
+    return (draws * scale).astype(np.float32)
