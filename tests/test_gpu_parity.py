@@ -373,3 +373,32 @@ def test_engine_layer_vs_fp32_path_full_size(cuda, name):
         rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         print(f"{name} engine {use}: rel-L2 {rel:.3e}")
         assert rel < 2e-2, (use, rel)
+
+
+def test_routing_bit_exact_c5_sample(cuda):
+    """Maximum size (C5: 333K volume + 99K image tokens, workload generated on
+    the GPU): the four routing tables for a strided sample of queries equal
+    the oracle's (bit-exact f64 distances, stable ties)."""
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200.workloads import coarse_inputs, load_workload
+    wl = load_workload("c5")
+    x_d, y_d, pe_v, pe_i = coarse_inputs(wl, 8)
+    x_up, y_up = L.upsample_select_tokens(x_d, y_d, wl.vol_mask, wl.img_mask, pe_v, pe_i,
+                                          wl.factor_vol, wl.factor_img)
+    c = dict(x_up=x_up, pv=L.partition(x_up), pi=L.partition(y_up))
+    plan = _plan(c, wl)
+    opv = O.partition_tokens("volume", x_up.coords, x_up.grid_res)
+    opi = O.partition_tokens("image", y_up.coords, y_up.grid_res)
+    assert np.array_equal(c["pv"].occupied_ids, opv.occupied_ids)
+    assert np.array_equal(c["pi"].occupied_ids, opi.occupied_ids)
+    vpts = (x_up.coords.astype(np.float64) + 0.5) / wl.s_vol
+    ipts = np.asarray(wl.img_points, np.float64)
+    sv = np.arange(0, vpts.shape[0], max(1, vpts.shape[0] // 192))
+    si = np.arange(0, ipts.shape[0], max(1, ipts.shape[0] // 192))
+    want = {"v2v": O.route_volume(vpts[sv], opv, 8), "i2v": O.route_volume(ipts[si], opv, 8),
+            "v2i": O.route_image(vpts[sv], wl.cameras, opi, ipts, 16, 8),
+            "i2i": O.route_image(ipts[si], wl.cameras, opi, ipts, 16, 8)}
+    for name, idx in (("v2v", sv), ("i2v", si), ("v2i", sv), ("i2i", si)):
+        got = [plan.tables[name].lists[i] for i in idx]
+        bad = [k for k, (a, b) in enumerate(zip(got, want[name])) if not np.array_equal(a, b)]
+        assert not bad, (name, len(bad), len(idx))
