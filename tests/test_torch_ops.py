@@ -76,10 +76,11 @@ def test_branch_attention_fp32(cuda, mode):
     assert float((got.double().cpu() - want).abs().max()) < 1e-5
 
 
+@pytest.mark.parametrize("heads", [(4, 2, 16), (32, 2, 32), (8, 1, 64)])
 @pytest.mark.parametrize("mode", [0, 1, 2])
-def test_sparse_attention_forward_backward(cuda, mode):
+def test_sparse_attention_forward_backward(cuda, mode, heads):
     import paper_2604_05182_b200.torch_ops  # noqa: F401
-    inst = _instance(10 + mode)
+    inst = _instance(10 + mode, *heads)
     k, v, *rest = _args(inst, mode)
     q = inst["q"].clone().requires_grad_(True)
     kk = k.clone().requires_grad_(True)
