@@ -32,6 +32,7 @@ stated in DESIGN.md and enforced in tests/test_gpu_parity.py.
 from dataclasses import dataclass
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -48,7 +49,9 @@ USES = ("v2v", "v2i", "i2i", "i2v")
 USE_GEOM = {"v2v": ("x", "x", 3), "v2i": ("x", "y", 2), "i2i": ("y", "y", 3),
             "i2v": ("y", "x", 2)}
 ROW_PAD = 16
-ONES_COLS = 16   # extra V columns (1 = real key) that make P.V also emit row sums
+ONES_COLS = 16
+# cross uses (v2i, i2v) tile their signature-sorted tokens across query blocks
+CROSS_GLOBAL_TILES = os.environ.get("LSRM_CROSS_GLOBAL_TILES", "1") != "0"   # extra V columns (1 = real key) that make P.V also emit row sums
 
 
 def _padded(occ: np.ndarray) -> np.ndarray:
@@ -362,7 +365,20 @@ class SparseLayerEngine:
             cnt_h = D.host(self.count[use])
             blk = np.repeat(np.arange(mq.loc_off_host.size - 1), np.diff(mq.loc_off_host))
             key = np.sort(np.where(rows_h >= 0, rows_h, np.iinfo(np.int32).max), axis=1)
-            perm = np.lexsort(tuple(key[:, j] for j in reversed(range(key.shape[1]))) + (blk,))
+            # cross uses have no window branch, so their tiles need not stay
+            # inside one query block: sort ALL their tokens by signature and
+            # tile the sorted order (tokens of neighbouring blocks often share
+            # a selection), which shrinks the unions further
+            cross_global = ng == 2 and not mq.sharded and CROSS_GLOBAL_TILES
+            sig = tuple(key[:, j] for j in reversed(range(key.shape[1])))
+            perm = np.lexsort(sig if cross_global else sig + (blk,))
+            if cross_global:
+                T = 128 // p.group_size
+                n_q = int(rows_h.shape[0])
+                first = np.arange(0, n_q, T, dtype=np.int64)
+                tiles = D.dev(np.stack([first, np.minimum(T, n_q - first), np.full_like(first, -1),
+                                        np.zeros_like(first)], axis=1).astype(np.int32))
+                self._job_refs.append(tiles)
             rows = np.ascontiguousarray(rows_h[perm])
             perm_d = D.dev(perm.astype(np.int32))
             rows_d, cnt_d = D.dev(rows), D.dev(np.ascontiguousarray(cnt_h[perm]))
