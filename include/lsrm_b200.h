@@ -274,6 +274,9 @@ typedef struct lsrm_nsa_use {
   const int32_t* perm;   /* optional [nq]: tile position -> query row; tiles,
                             rows and count are then in permuted (tile) order,
                             q / gate_logits / merged stay in query-row order */
+  int64_t branch_first;  /* first branch the items run: 0, or 2 for window-only
+                            items (self uses split over two launches) */
+  int64_t accumulate;    /* 1: add the gated result to `merged` (second launch) */
 } lsrm_nsa_use;
 int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, int hkv, int dh,
                                 const int32_t* order, int64_t n_order, int32_t* counter,

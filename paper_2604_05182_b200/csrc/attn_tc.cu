@@ -242,6 +242,8 @@ struct Params {
   const float* gbias;
   int n_gates;
   __nv_bfloat16* out;
+  int br_first;   // first branch this use's items run (2: window only)
+  int accum;      // add the gated merge to `out` instead of storing it
 };
 
 // One launch: up to kMaxUses NSA uses (same head geometry).  order == nullptr:
@@ -592,7 +594,8 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
                 own = P.tiles[4 * tile + 2];
       const int qb = it & 1;
       // ---- selected rows of the tile tokens (resolved rows are -1 padded)
-      const int n_ent = T * P.kmax, n_valid_ent = q_cnt * P.kmax;
+      // (window-only items need no union of selected blocks)
+      const int n_ent = P.br_first <= 1 ? T * P.kmax : 0, n_valid_ent = q_cnt * P.kmax;
       const int32_t* rows_t = P.rows + (int64_t)q_first * P.kmax;
       for (int i = lane; i < n_ent; i += 32) {
         const int r = i < n_valid_ent ? rows_t[i] : -1;
@@ -708,7 +711,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       //      segment into a piece, fills its groups' visibility and issues the
       //      piece's K and V bulk copies for every head of the item
       const int64_t cmp_rows = (P.n_blocks + 15) / 16 * 16;
-      for (int br = 0; br < P.n_gates; ++br) {
+      for (int br = P.br_first; br < P.n_gates; ++br) {
         const int n_seg = br == 1 ? nu : 1;
         const int64_t total = br == 0 ? cmp_rows : (br == 1 ? total_sel : S.seg_plen[kMaxEnt]);
         const int64_t head_rows = br == 0 ? cmp_rows : P.n_rows_pad;
@@ -761,7 +764,8 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
             D.ncols = (int)(end - start);
             D.branch = br;
             D.flags = (start == 0 ? kFFirstBranch : 0) | (end == total ? kFLastBranch : 0) |
-                      (br == 0 && start == 0 ? kFFirstItem : 0) | (li ? kFLastItem : 0) |
+                      (br == P.br_first && start == 0 ? kFFirstItem : 0) |
+                      (li ? kFLastItem : 0) |
                       (li && last_item ? kFLastOverall : 0) | (use << 16);
             D.q_first = q_first;
             D.q_cnt = q_cnt;
@@ -907,6 +911,10 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     // finished-branch state: its epilogue runs in the next chunk, before that
     // chunk's PV overwrites O
     int br_pend = 0, head_pend = 0, use_pend = 0;
+    // the item's first branch (items may start at the window branch); a
+    // branch that is its item's first starts the merge instead of adding
+    int item_br0 = 0;
+    bool firstbr_pend = true;
     bool lastit_pend = false, rowok_pend = false, epi_pend = false;
     int64_t tok_pend = 0;
     __nv_bfloat16* const gate_s = &S.gate[hh][m * DH];   // this row's staged gate logits
@@ -953,7 +961,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
         uint32_t r[16], mr[8];
 #pragma unroll
         for (int j = 0; j < 16; ++j) r[j] = eo[cq + j];
-        if (br_pend > 0) {
+        if (!firstbr_pend) {
           tmem_ld_cols<8>(tM + c0 / 2, mr);
           tmem_wait_ld();
         }
@@ -969,7 +977,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
             float v = rowok_pend ? __uint_as_float(r[cj]) * inv *
                                        fmaf(0.5f, tanh_approx(0.5f * z), 0.5f)
                                  : 0.f;
-            if (br_pend > 0) {
+            if (!firstbr_pend) {
               const __half2 hm = *reinterpret_cast<const __half2*>(&mr[cj / 2]);
               v += (cj & 1) ? __high2float(hm) : __low2float(hm);
             }
@@ -981,7 +989,13 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
             __nv_bfloat16* op = L.use[use_pend].out + tok_pend * d_model + head_pend * DH + c0;
 #pragma unroll
             for (int k8 = 0; k8 < 2; ++k8) {
-              const float* v = reinterpret_cast<const float*>(r + 8 * k8);
+              float* v = reinterpret_cast<float*>(r + 8 * k8);
+              if (L.use[use_pend].accum) {   // second launch: add to the first's merge
+                const uint4 old = *reinterpret_cast<const uint4*>(op + 8 * k8);
+                const __nv_bfloat16* ov = reinterpret_cast<const __nv_bfloat16*>(&old);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] += __bfloat162float(ov[j]);
+              }
               uint4 w;
               w.x = pack_bf16(v[0], v[1]);
               w.y = pack_bf16(v[2], v[3]);
@@ -1033,6 +1047,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const int br = hdr0.y, fl = hdr0.z, use_c = fl >> 16;
       const bool first_br = fl & kFFirstBranch, last_br = fl & kFLastBranch,
                  last_it = fl & kFLastItem, last_all = fl & kFLastOverall;
+      if (fl & kFFirstItem) item_br0 = br;
       const bool row_ok = t < hdr1.x;
       const int64_t tok = D.tok[t];
       const int head = (hdr1.y + hh) * G + g_in;
@@ -1437,6 +1452,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           for (int cq = 0; cq < kOCols; cq += 8) cp_async16(gate_s + oc0 + cq, gp + oc0 + cq, 16u);
         }
         br_pend = br;
+        firstbr_pend = br == item_br0;
         use_pend = use_c;
         head_pend = head;
         tok_pend = tok;
@@ -1621,6 +1637,8 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
   p.gbias = gate_bias;
   p.n_gates = n_gates;
   p.out = (__nv_bfloat16*)merged;
+  p.br_first = 0;
+  p.accum = 0;
   tc::Launch L{};
   L.use[0] = p;
   L.n_uses = 1;
@@ -1675,6 +1693,8 @@ int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, in
     p.gbias = nullptr;   // folded into the gate logits by the caller
     p.n_gates = (int)U.n_gates;
     p.out = (__nv_bfloat16*)U.merged;
+    p.br_first = (int)U.branch_first;
+    p.accum = (int)U.accumulate;
   }
   L.n_uses = n_uses;
   L.order = order;

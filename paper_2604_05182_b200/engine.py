@@ -51,7 +51,10 @@ USE_GEOM = {"v2v": ("x", "x", 3), "v2i": ("x", "y", 2), "i2i": ("y", "y", 3),
 ROW_PAD = 16
 ONES_COLS = 16
 # cross uses (v2i, i2v) tile their signature-sorted tokens across query blocks
-CROSS_GLOBAL_TILES = os.environ.get("LSRM_CROSS_GLOBAL_TILES", "1") != "0"   # extra V columns (1 = real key) that make P.V also emit row sums
+CROSS_GLOBAL_TILES = os.environ.get("LSRM_CROSS_GLOBAL_TILES", "1") != "0"
+# self uses run cmp + sel on such tiles and the window branch in a second,
+# accumulating launch (correct, measured slower: 1.23 -> 1.31 ms; off)
+SPLIT_SELF_WINDOW = os.environ.get("LSRM_SPLIT_SELF_WINDOW", "0") != "0"   # extra V columns (1 = real key) that make P.V also emit row sums
 
 
 def _padded(occ: np.ndarray) -> np.ndarray:
@@ -78,7 +81,8 @@ class NsaUse(C.Structure):
                 ("tiles", C.c_void_p), ("n_tiles", C.c_int64), ("rows", C.c_void_p),
                 ("count", C.c_void_p), ("kmax_rows", C.c_int64), ("gate_logits", C.c_void_p),
                 ("ld_gl", C.c_int64), ("gate_col0", C.c_int64), ("n_gates", C.c_int64),
-                ("merged", C.c_void_p), ("perm", C.c_void_p)]
+                ("merged", C.c_void_p), ("perm", C.c_void_p), ("branch_first", C.c_int64),
+                ("accumulate", C.c_int64)]
 
 
 class PackedShard:
@@ -346,43 +350,34 @@ class SparseLayerEngine:
         self.n_kv_jobs, self.kv_max_blocks = len(jobs), max_blocks
 
     def _build_attention_queue(self):
-        """One launch for the four uses: per-use descriptors and a
-        heaviest-first item order. An item is (use, tile, kv head); its cost is
-        the keys it streams: compressed rows + the padded union of its tokens'
-        selected blocks + (self uses) its own block."""
+        """The four uses' attention as heaviest-first item queues. An item is
+        (use, tile, kv head); its cost is the keys it streams: compressed rows
+        + the padded union of its tokens' selected blocks + (window) its own
+        block.
+
+        Tokens are sorted by selection signature before tiling, so a tile's
+        tokens share most of their selected blocks. Only the window branch
+        ties a tile to one query block, so (SPLIT_SELF_WINDOW) the cmp and sel
+        branches of every use run on tiles of the signature order across
+        blocks in launch A, and the self uses' window branch runs on block
+        tiles in launch B, which adds its gated output to A's."""
         p = self.params
         hkv = p.n_kv_heads
-        uses, costs, codes = [], [], []
-        for ui, use in enumerate(USES):
-            qs, ks, ng = USE_GEOM[use]
+        T = 128 // p.group_size
+        queues = {"A": ([], [], []), "B": ([], [], [])}   # uses, costs, codes
+
+        def add(qname, use, tiles, rows_h, cnt_h, perm, n_gates, br_first, accum):
+            qs, ks, _ = USE_GEOM[use]
             mq, mk = self.meta[qs], self.meta[ks]
             Y = self.buf[("Y", qs)]
             qcol = self.cols[(use, "q")]
-            tiles = self.tiles[use]
-            # tokens of each query block sorted by selection signature: tiles of
-            # similar tokens have smaller unions of selected blocks
-            rows_h = D.host(self.rows[use])
-            cnt_h = D.host(self.count[use])
-            blk = np.repeat(np.arange(mq.loc_off_host.size - 1), np.diff(mq.loc_off_host))
-            key = np.sort(np.where(rows_h >= 0, rows_h, np.iinfo(np.int32).max), axis=1)
-            # cross uses have no window branch, so their tiles need not stay
-            # inside one query block: sort ALL their tokens by signature and
-            # tile the sorted order (tokens of neighbouring blocks often share
-            # a selection), which shrinks the unions further
-            cross_global = ng == 2 and not mq.sharded and CROSS_GLOBAL_TILES
-            sig = tuple(key[:, j] for j in reversed(range(key.shape[1])))
-            perm = np.lexsort(sig if cross_global else sig + (blk,))
-            if cross_global:
-                T = 128 // p.group_size
-                n_q = int(rows_h.shape[0])
-                first = np.arange(0, n_q, T, dtype=np.int64)
-                tiles = D.dev(np.stack([first, np.minimum(T, n_q - first), np.full_like(first, -1),
-                                        np.zeros_like(first)], axis=1).astype(np.int32))
-                self._job_refs.append(tiles)
-            rows = np.ascontiguousarray(rows_h[perm])
-            perm_d = D.dev(perm.astype(np.int32))
-            rows_d, cnt_d = D.dev(rows), D.dev(np.ascontiguousarray(cnt_h[perm]))
-            self._job_refs += [perm_d, rows_d, cnt_d]
+            rows = np.ascontiguousarray(rows_h if perm is None else rows_h[perm])
+            cnt = np.ascontiguousarray(cnt_h if perm is None else cnt_h[perm])
+            perm_d = D.dev(perm.astype(np.int32)) if perm is not None else None
+            rows_d, cnt_d = D.dev(rows), D.dev(cnt)
+            self._job_refs += [t for t in (perm_d, rows_d, cnt_d, tiles) if t is not None]
+            uses, costs, codes = queues[qname]
+            ui = len(uses)
             uses.append(NsaUse(
                 Y[:, qcol:].data_ptr(), Y.stride(0), mq.n_loc,
                 self.buf[("k_il", use)].data_ptr(), self.buf[("v_il", use)].data_ptr(),
@@ -390,29 +385,62 @@ class SparseLayerEngine:
                 self.buf[("kc_il", use)].data_ptr(), self.buf[("vc_il", use)].data_ptr(),
                 mk.n_blocks, tiles.data_ptr(), int(tiles.shape[0]), rows_d.data_ptr(),
                 cnt_d.data_ptr(), self.kmax[use], Y.data_ptr(), Y.stride(0),
-                qcol + self.d, ng, self.buf[("merged", use)].data_ptr(), perm_d.data_ptr()))
+                qcol + self.d, n_gates, self.buf[("merged", use)].data_ptr(), D.ptr(perm_d),
+                br_first, accum))
             th = D.host(tiles)
             padlen = np.diff(mk.pad_off_host)
             cmp_rows = (mk.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
-            for t, (first, cnt, own, _) in enumerate(th):
-                r = rows[first:first + cnt].ravel()
-                r = np.unique(r[r >= 0])
-                c = cmp_rows + int(padlen[r].sum()) + (int(padlen[own]) if own >= 0 else 0)
+            for t, (first, tc, own, _) in enumerate(th):
+                c = int(padlen[own]) if (own >= 0 and n_gates == 3) else 0
+                if br_first == 0:
+                    r = rows[first:first + tc].ravel()
+                    r = np.unique(r[r >= 0])
+                    c += cmp_rows + int(padlen[r].sum())
                 for h in range(hkv):
                     costs.append(c)
                     codes.append((ui << 28) | (t * hkv + h))
-        costs, codes = np.asarray(costs, np.int64), np.asarray(codes, np.int64)
-        order = codes[np.lexsort((codes, -costs))].astype(np.int32)
-        self.attn_uses = (NsaUse * len(uses))(*uses)
-        self.attn_order = D.dev(order)
-        self.attn_counter = D.zeros((1,), torch.int32)
+
+        for use in USES:
+            qs, ks, ng = USE_GEOM[use]
+            mq = self.meta[qs]
+            rows_h = D.host(self.rows[use])
+            cnt_h = D.host(self.count[use])
+            blk = np.repeat(np.arange(mq.loc_off_host.size - 1), np.diff(mq.loc_off_host))
+            key = np.sort(np.where(rows_h >= 0, rows_h, np.iinfo(np.int32).max), axis=1)
+            sig = tuple(key[:, j] for j in reversed(range(key.shape[1])))
+            across = not mq.sharded and (SPLIT_SELF_WINDOW if ng == 3 else CROSS_GLOBAL_TILES)
+            if across:
+                perm = np.lexsort(sig)
+                n_q = int(rows_h.shape[0])
+                first = np.arange(0, n_q, T, dtype=np.int64)
+                tiles = D.dev(np.stack([first, np.minimum(T, n_q - first),
+                                        np.full_like(first, -1), np.zeros_like(first)],
+                                       axis=1).astype(np.int32))
+                add("A", use, tiles, rows_h, cnt_h, perm, 2, 0, 0)
+                if ng == 3:   # window branch on block tiles, added to A's output
+                    add("B", use, self.tiles[use], rows_h, cnt_h, None, 3, 2, 1)
+            else:
+                add("A", use, self.tiles[use], rows_h, cnt_h, np.lexsort(sig + (blk,)), ng, 0, 0)
+
+        self.attn_queues = []
+        for qname in ("A", "B"):
+            uses, costs, codes = queues[qname]
+            if not uses:
+                continue
+            costs, codes = np.asarray(costs, np.int64), np.asarray(codes, np.int64)
+            order = codes[np.lexsort((codes, -costs))].astype(np.int32)
+            self.attn_queues.append(((NsaUse * len(uses))(*uses), len(uses), D.dev(order),
+                                     D.zeros((1,), torch.int32)))
 
     def attend_all(self):
-        """The four uses' fused attention in one persistent launch (LPT queue)."""
+        """The four uses' fused attention: persistent launches over LPT queues
+        (A: every use's cmp + sel (+ window when not split); B: the self uses'
+        window branch, accumulating into A's output)."""
         p = self.params
-        call("lsrm_nsa_attention_tc_multi", C.cast(self.attn_uses, C.c_void_p), len(USES),
-             p.n_q_heads, p.n_kv_heads, p.head_dim, self.attn_order.data_ptr(),
-             int(self.attn_order.shape[0]), self.attn_counter.data_ptr(), D.stream())
+        for uses, n_uses, order, counter in self.attn_queues:
+            call("lsrm_nsa_attention_tc_multi", C.cast(uses, C.c_void_p), n_uses,
+                 p.n_q_heads, p.n_kv_heads, p.head_dim, order.data_ptr(),
+                 int(order.shape[0]), counter.data_ptr(), D.stream())
 
     # -- pieces --------------------------------------------------------------
     def project(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
