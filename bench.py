@@ -191,12 +191,16 @@ def run_reference(args):
         return
     # the same workload our arm runs at this N (C3 on one GPU, C4 under torchrun)
     wl_name = args.workload or ("c4" if ws > 1 else "c3")
+    # every host thread (torchrun sets OMP_NUM_THREADS=1 for its workers)
+    from threadpoolctl import threadpool_limits
     times, tokens, desc = [], 0, ""
-    for _ in range(args.steps):
-        tokens, secs, desc = cpu_oracle_sample(wl_name=wl_name, frac=args.ref_frac)
-        times.append(secs)
+    with threadpool_limits(limits=os.cpu_count()):
+        for _ in range(args.steps):
+            tokens, secs, desc = cpu_oracle_sample(wl_name=wl_name, frac=args.ref_frac)
+            times.append(secs)
     v = tokens / float(np.mean(times))
-    hi = host_info()
+    with threadpool_limits(limits=os.cpu_count()):
+        hi = host_info()
     line = {"impl": "reference", "metric": "LSRM sparse-attn layer tokens/s",
             "value": v, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
