@@ -277,6 +277,9 @@ typedef struct lsrm_nsa_use {
   int64_t branch_first;  /* first branch the items run: 0, or 2 for window-only
                             items (self uses split over two launches) */
   int64_t accumulate;    /* 1: add the gated result to `merged` (second launch) */
+  const int32_t* own_rows; /* optional [nq] (tile order): each token's own kv row;
+                              the window branch then spans the tile's distinct own
+                              blocks, so self-use tiles may cross query blocks */
 } lsrm_nsa_use;
 int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, int hkv, int dh,
                                 const int32_t* order, int64_t n_order, int32_t* counter,

@@ -244,6 +244,8 @@ struct Params {
   __nv_bfloat16* out;
   int br_first;   // first branch this use's items run (2: window only)
   int accum;      // add the gated merge to `out` instead of storing it
+  const int32_t* own_rows;   // optional [nq] (tile order): each token's own kv row;
+                             // the window branch then spans the tile's distinct own blocks
 };
 
 // One launch: up to kMaxUses NSA uses (same head geometry).  order == nullptr:
@@ -456,6 +458,9 @@ struct Pipe {
   int32_t seg_plen[kMaxEnt + 1];
   int32_t seg_occ[kMaxEnt + 1];
   int32_t seg_cum[kMaxEnt];
+  int64_t wseg_lo[32];            // window segments: the tile tokens' distinct own blocks
+  int32_t wseg_plen[32], wseg_occ[32], wseg_cum[32];
+  uint32_t wseg_mask[32];
   ChunkDesc desc[kStages];
   float xmax[kSplit > 1 ? 2 : 1][HP][kSplit][kM];   // split: partial row maxima, by chunk parity
   uint64_t kv_full[kStages], kv_empty[kStages], s_full[2 * HP], s_free[HP], p_full[2 * HP],
@@ -676,6 +681,37 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
         S.seg_plen[kMaxEnt] = (int)(a1 - a0);
         S.seg_occ[kMaxEnt] = (int)(b1 - b0);
       }
+      // per-token own rows: one window segment per distinct own block of the
+      // tile (in token order), each seen by the tokens that own it
+      int n_wseg = 1;
+      int64_t total_win = 0;
+      if (P.own_rows && P.n_gates == 3) {
+        const bool tv = lane < q_cnt;
+        const int r = tv ? P.own_rows[q_first + lane] : -1;
+        const uint32_t vmask = __ballot_sync(0xffffffffu, tv);
+        const uint32_t same = __match_any_sync(0xffffffffu, r) & vmask;
+        const bool leader = tv && (__ffs(same) - 1) == lane;
+        const uint32_t leaders = __ballot_sync(0xffffffffu, leader);
+        n_wseg = __popc(leaders);
+        const int idx = __popc(leaders & ((1u << lane) - 1u));
+        int plen = 0;
+        if (leader) {
+          const int64_t a0 = P.pad_off[r], a1 = P.pad_off[r + 1];
+          S.wseg_lo[idx] = a0;
+          plen = (int)(a1 - a0);
+          S.wseg_plen[idx] = plen;
+          S.wseg_occ[idx] = (int)(P.kv_off[r + 1] - P.kv_off[r]);
+          S.wseg_mask[idx] = same;
+        }
+        // segment starts: exclusive prefix over the leaders in token order
+        int incl = plen;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        if (leader) S.wseg_cum[idx] = incl - plen;
+        total_win = __shfl_sync(0xffffffffu, incl, 31);
+      }
       __syncwarp();
       for (int k = 0; k < per_w; ++k) {  // clear the bitmap for the next item
         const int w = lane * per_w + k;
@@ -712,8 +748,10 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       //      piece's K and V bulk copies for every head of the item
       const int64_t cmp_rows = (P.n_blocks + 15) / 16 * 16;
       for (int br = P.br_first; br < P.n_gates; ++br) {
-        const int n_seg = br == 1 ? nu : 1;
-        const int64_t total = br == 0 ? cmp_rows : (br == 1 ? total_sel : S.seg_plen[kMaxEnt]);
+        const bool win_tok = br == 2 && P.own_rows != nullptr;
+        const int n_seg = br == 1 ? nu : (win_tok ? n_wseg : 1);
+        const int64_t total = br == 0 ? cmp_rows
+                              : (br == 1 ? total_sel : (win_tok ? total_win : S.seg_plen[kMaxEnt]));
         const int64_t head_rows = br == 0 ? cmp_rows : P.n_rows_pad;
         const __nv_bfloat16* kb = (br == 0 ? P.kc_il : P.k_il) + (int64_t)h0 * head_rows * DH;
         const __nv_bfloat16* vb = (br == 0 ? P.vc_il : P.v_il) + (int64_t)h0 * head_rows * VW;
@@ -736,6 +774,9 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
             } else if (br == 1) {
               lo = S.seg_lo[s]; plen = S.seg_plen[s]; occ = S.seg_occ[s]; cs = S.seg_cum[s];
               tm = S.uni_mask[s];
+            } else if (win_tok) {
+              lo = S.wseg_lo[s]; plen = S.wseg_plen[s]; occ = S.wseg_occ[s]; cs = S.wseg_cum[s];
+              tm = S.wseg_mask[s];
             } else {
               lo = S.seg_lo[kMaxEnt]; plen = S.seg_plen[kMaxEnt]; occ = S.seg_occ[kMaxEnt];
               cs = 0;
@@ -1639,6 +1680,7 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
   p.out = (__nv_bfloat16*)merged;
   p.br_first = 0;
   p.accum = 0;
+  p.own_rows = nullptr;
   tc::Launch L{};
   L.use[0] = p;
   L.n_uses = 1;
@@ -1695,6 +1737,7 @@ int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, in
     p.out = (__nv_bfloat16*)U.merged;
     p.br_first = (int)U.branch_first;
     p.accum = (int)U.accumulate;
+    p.own_rows = U.own_rows;
   }
   L.n_uses = n_uses;
   L.order = order;

@@ -52,6 +52,10 @@ ROW_PAD = 16
 ONES_COLS = 16
 # cross uses (v2i, i2v) tile their signature-sorted tokens across query blocks
 CROSS_GLOBAL_TILES = os.environ.get("LSRM_CROSS_GLOBAL_TILES", "1") != "0"
+# self uses tile across blocks too; their window branch then spans each tile's
+# distinct own blocks (per-token own rows). Correct, measured neutral
+# (1.230 -> 1.236 ms), so off.
+SELF_GLOBAL_TILES = os.environ.get("LSRM_SELF_GLOBAL_TILES", "0") != "0"
 # self uses run cmp + sel on such tiles and the window branch in a second,
 # accumulating launch (correct, measured slower: 1.23 -> 1.31 ms; off)
 SPLIT_SELF_WINDOW = os.environ.get("LSRM_SPLIT_SELF_WINDOW", "0") != "0"   # extra V columns (1 = real key) that make P.V also emit row sums
@@ -82,7 +86,7 @@ class NsaUse(C.Structure):
                 ("count", C.c_void_p), ("kmax_rows", C.c_int64), ("gate_logits", C.c_void_p),
                 ("ld_gl", C.c_int64), ("gate_col0", C.c_int64), ("n_gates", C.c_int64),
                 ("merged", C.c_void_p), ("perm", C.c_void_p), ("branch_first", C.c_int64),
-                ("accumulate", C.c_int64)]
+                ("accumulate", C.c_int64), ("own_rows", C.c_void_p)]
 
 
 class PackedShard:
@@ -366,7 +370,8 @@ class SparseLayerEngine:
         T = 128 // p.group_size
         queues = {"A": ([], [], []), "B": ([], [], [])}   # uses, costs, codes
 
-        def add(qname, use, tiles, rows_h, cnt_h, perm, n_gates, br_first, accum):
+        def add(qname, use, tiles, rows_h, cnt_h, perm, n_gates, br_first, accum,
+                own_rows=None):
             qs, ks, _ = USE_GEOM[use]
             mq, mk = self.meta[qs], self.meta[ks]
             Y = self.buf[("Y", qs)]
@@ -375,7 +380,8 @@ class SparseLayerEngine:
             cnt = np.ascontiguousarray(cnt_h if perm is None else cnt_h[perm])
             perm_d = D.dev(perm.astype(np.int32)) if perm is not None else None
             rows_d, cnt_d = D.dev(rows), D.dev(cnt)
-            self._job_refs += [t for t in (perm_d, rows_d, cnt_d, tiles) if t is not None]
+            own_d = D.dev(own_rows.astype(np.int32)) if own_rows is not None else None
+            self._job_refs += [t for t in (perm_d, rows_d, cnt_d, tiles, own_d) if t is not None]
             uses, costs, codes = queues[qname]
             ui = len(uses)
             uses.append(NsaUse(
@@ -386,12 +392,14 @@ class SparseLayerEngine:
                 mk.n_blocks, tiles.data_ptr(), int(tiles.shape[0]), rows_d.data_ptr(),
                 cnt_d.data_ptr(), self.kmax[use], Y.data_ptr(), Y.stride(0),
                 qcol + self.d, n_gates, self.buf[("merged", use)].data_ptr(), D.ptr(perm_d),
-                br_first, accum))
+                br_first, accum, D.ptr(own_d)))
             th = D.host(tiles)
             padlen = np.diff(mk.pad_off_host)
             cmp_rows = (mk.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
             for t, (first, tc, own, _) in enumerate(th):
                 c = int(padlen[own]) if (own >= 0 and n_gates == 3) else 0
+                if own_rows is not None:   # the tile's distinct own blocks
+                    c += int(padlen[np.unique(own_rows[first:first + tc])].sum())
                 if br_first == 0:
                     r = rows[first:first + tc].ravel()
                     r = np.unique(r[r >= 0])
@@ -409,7 +417,17 @@ class SparseLayerEngine:
             key = np.sort(np.where(rows_h >= 0, rows_h, np.iinfo(np.int32).max), axis=1)
             sig = tuple(key[:, j] for j in reversed(range(key.shape[1])))
             across = not mq.sharded and (SPLIT_SELF_WINDOW if ng == 3 else CROSS_GLOBAL_TILES)
-            if across:
+            if ng == 3 and not mq.sharded and SELF_GLOBAL_TILES and not SPLIT_SELF_WINDOW:
+                # signature order across blocks (own block as the minor key);
+                # the window branch follows each token's own block
+                perm = np.lexsort((blk,) + sig)
+                n_q = int(rows_h.shape[0])
+                first = np.arange(0, n_q, T, dtype=np.int64)
+                tiles = D.dev(np.stack([first, np.minimum(T, n_q - first),
+                                        np.full_like(first, -1), np.zeros_like(first)],
+                                       axis=1).astype(np.int32))
+                add("A", use, tiles, rows_h, cnt_h, perm, 3, 0, 0, own_rows=blk[perm])
+            elif across:
                 perm = np.lexsort(sig)
                 n_q = int(rows_h.shape[0])
                 first = np.arange(0, n_q, T, dtype=np.int64)
