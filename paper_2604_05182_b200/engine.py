@@ -56,6 +56,10 @@ CROSS_GLOBAL_TILES = os.environ.get("LSRM_CROSS_GLOBAL_TILES", "1") != "0"
 # distinct own blocks (per-token own rows). Correct, measured neutral
 # (1.230 -> 1.236 ms), so off.
 SELF_GLOBAL_TILES = os.environ.get("LSRM_SELF_GLOBAL_TILES", "0") != "0"
+# self uses keep block tiles but pool every block's partial last tile with the
+# others' into full tiles (per-token own rows for the window branch).
+# Correct, measured neutral (the LPT queue already hides the small items): off.
+PACK_SELF_TAILS = os.environ.get("LSRM_PACK_SELF_TAILS", "0") != "0"
 # self uses run cmp + sel on such tiles and the window branch in a second,
 # accumulating launch (correct, measured slower: 1.23 -> 1.31 ms; off)
 SPLIT_SELF_WINDOW = os.environ.get("LSRM_SPLIT_SELF_WINDOW", "0") != "0"   # extra V columns (1 = real key) that make P.V also emit row sums
@@ -417,7 +421,24 @@ class SparseLayerEngine:
             key = np.sort(np.where(rows_h >= 0, rows_h, np.iinfo(np.int32).max), axis=1)
             sig = tuple(key[:, j] for j in reversed(range(key.shape[1])))
             across = not mq.sharded and (SPLIT_SELF_WINDOW if ng == 3 else CROSS_GLOBAL_TILES)
-            if ng == 3 and not mq.sharded and SELF_GLOBAL_TILES and not SPLIT_SELF_WINDOW:
+            if ng == 3 and not mq.sharded and PACK_SELF_TAILS and not SELF_GLOBAL_TILES:
+                # block tiles (signature order inside each block), except that
+                # each block's partial last tile is pooled with the other
+                # blocks' into full tiles; the window branch follows each
+                # token's own block (per-token own rows)
+                order = np.lexsort(sig + (blk,))
+                occ = np.diff(mq.loc_off_host).astype(np.int64)
+                full = (occ // T) * T
+                pos_in_blk = np.arange(order.size) - np.repeat(mq.loc_off_host[:-1], occ)
+                is_full = pos_in_blk < np.repeat(full, occ)
+                perm = np.concatenate([order[is_full], order[~is_full]])
+                n_q = int(rows_h.shape[0])
+                first = np.arange(0, n_q, T, dtype=np.int64)
+                tiles = D.dev(np.stack([first, np.minimum(T, n_q - first),
+                                        np.full_like(first, -1), np.zeros_like(first)],
+                                       axis=1).astype(np.int32))
+                add("A", use, tiles, rows_h, cnt_h, perm, 3, 0, 0, own_rows=blk[perm])
+            elif ng == 3 and not mq.sharded and SELF_GLOBAL_TILES and not SPLIT_SELF_WINDOW:
                 # signature order across blocks (own block as the minor key);
                 # the window branch follows each token's own block
                 perm = np.lexsort((blk,) + sig)
