@@ -1,43 +1,46 @@
 // Fused bf16 three-branch NSA attention on the 5th-gen tensor cores
-// (tcgen05.mma + TMEM accumulators + bulk-async (TMA engine) K/V staging),
-// with the sigmoid-gated branch merge in the epilogue.
+// (tcgen05.mma + TMEM accumulators + cp.async.bulk K/V staging), with the
+// sigmoid-gated branch merge in the epilogue.
 //
 // Replaces, fused: cmp_attention / sel_attention / win_attention and the
 // gated sum of combine_nsa_branches (lsrm/nsa_attention.py:84-112,157-207,
 // 266-284).  The W_o projection stays a plain GEMM.
 //
-// Work item = (query tile, group of HP kv heads).  A query tile is up to
-// T = 128/G consecutive tokens of ONE query block (block-major order); per kv
-// head, the MMA M-dimension is the 128 rows (token, q-head-in-group).  Each
-// item streams key chunks of <= 128 keys, branch after branch:
+// One persistent launch runs the four uses of a layer
+// (lsrm_nsa_attention_tc_multi): work items (use, query tile, kv head) are
+// claimed from a heaviest-first queue with an atomic counter.  A query tile
+// is T = 128/G tokens (G = hq/hkv) in a per-use permuted order: signature-
+// sorted within each query block, or across blocks for cross uses; the MMA
+// M dimension is its 128 (token, q-head-in-group) rows.  Each item streams
+// key chunks of <= 128 keys, branch after branch:
 //   cmp : all compressed rows (one per occupied KV block),
-//   sel : the sorted union of the tile tokens' selected blocks; a row only
-//         sees the blocks ITS token selected (others masked out),
-//   win : the tile's own block (self uses).
-// The HP head-tiles of an item share the chunk plan but not K/V.
+//   sel : the sorted union of the tile tokens' selected blocks; a row sees
+//         only the 16-key groups of blocks ITS token selected,
+//   win : the own block (self uses), or each token's own block (own_rows).
+// Block padding needs no masks: padding K rows repeat the block's first key
+// and padding V rows (with their ones column) are zero.
 //
-// Persistent, warp-specialised CTA (one per SM, 32*(4*HP+2) threads):
-//   warps 4hh..4hh+3  softmax/epilogue of head-tile hh: thread = TMEM lane =
-//              one row and ALL keys of a chunk (no cross-warp exchange);
-//              masked online softmax (exp2), bf16 P written back into TMEM
-//              over S, PV partials absorbed into registers, gate + merge at
-//              branch ends (merge accumulator in TMEM);
-//   warp 4HP   producer: union of the tile's selections, chunk plans, and
-//              cp.async.bulk K/V copies of every head (each KV block is one
-//              contiguous 16-row-padded segment) into a 4-stage ring;
-//   warp 4HP+1 MMA issuer: per head-tile, PV(c) = P(c).[V|ones] (TS mode, P
-//              from TMEM) as soon as P(c) is written, then S(c+1) = Q K^T
-//              into the same columns.  The HP softmax warpgroups therefore
-//              run out of phase (ping-pong): one computes exponentials while
-//              the tensor core serves the other.
-// mbarriers: kv_full/kv_empty (ring), s_full (S ready), p_full (P written),
-// o_full/o_empty (double-buffered PV partial), q_full/q_empty.  Phases follow
-// a chunk counter that all roles advance identically.
+// CTA = NP = 2 independent pipelines (d_h = 32), each: 4 softmax warps
+// (thread = TMEM lane = one row, all keys of a chunk: two-pass max / exp2 in
+// 32-key pieces, running max with 2^8 headroom, bf16 P stored to TMEM, gate +
+// merge at branch ends into an f16 TMEM accumulator), 1 producer warp (tile
+// unions, chunk plans, bulk copies into a 3-stage K/V ring), 1 MMA warp
+// (S(c+1) = Q K^T once S(c) is in registers; [O | rowsum] += P.[V | ones] in
+// TS mode once P(c) is written).  The two pipelines' phases interleave on
+// each SMSP.  TMEM per pipeline: S 128 + P 64 + [O|rowsum] 48 + merge 16.
+// mbarriers: kv_full/kv_empty (ring), s_full/s_free, p_full, o_full,
+// q_full/q_empty; phases follow a chunk counter all roles advance alike.
+//
+// Build switches (-D...), all measured against this default and recorded in
+// LSRM_SPLIT=2, LSRM_HOLD4, LSRM_DBUF (+ LSRM_DBUF_NK),
+// LSRM_SKIP_DEAD_MAX, LSRM_GROUP_SKIP, LSRM_EPI_SPLIT, LSRM_ONEPASS,
+// LSRM_PINGPONG, LSRM_POLY_PER16, LSRM_HEADPAIR, LSRM_STAGES; LSRM_TRACE for
+// tools/attn_trace.py.
 //
 // SMEM operand layout: 8x8 "core matrices" of 128 contiguous bytes,
 // SWIZZLE_NONE canonical layouts (cute mma_sm100_desc.hpp):
-//   K-major  Q, K, P : element (row, k) at (row/8)*RS + (k/8)*64 + (row%8)*8 + k%8
-//   MN-major V       : the same storage read with N = head dim, K = keys.
+//   K-major  Q, K : element (row, k) at (row/8)*RS + (k/8)*64 + (row%8)*8 + k%8
+//   MN-major V    : the same storage read with N = head dim, K = keys.
 #include <cuda_fp16.h>
 
 #include "common.cuh"
