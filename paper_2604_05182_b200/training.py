@@ -276,6 +276,20 @@ class NsaUseModule(torch.nn.Module):
         return _NsaUseFn.apply(spec, x, kv, *(getattr(self, nm) for nm in PARAM_NAMES))
 
 
+def module_weights(mod: "NsaUseModule") -> NsaWeights:
+    """The module's current parameters as host `NsaWeights` (f32 arrays), so
+    trained weights feed the reference-API forward (`nsa_cross_attention`)
+    and the bf16 engine."""
+    from .block_partition import CompressWeights, ResBlockParams
+    h = {n: getattr(mod, n).detach().float().cpu().numpy() for n in PARAM_NAMES}
+    return NsaWeights(h["w_q"], h["w_k"], h["w_v"], h["w_o"], h["gate_w"], h["gate_b"],
+                      CompressWeights(ResBlockParams(h["ck_w1"], h["ck_b1"], h["ck_w2"],
+                                                     h["ck_b2"]),
+                                      ResBlockParams(h["cv_w1"], h["cv_b1"], h["cv_w2"],
+                                                     h["cv_b2"])),
+                      mod.n_gates)
+
+
 def _weight_arrays(w: NsaWeights) -> dict:
     ck, cv = w.compress.for_k, w.compress.for_v
     return {"w_q": w.w_q, "w_k": w.w_k, "w_v": w.w_v, "w_o": w.w_o, "gate_w": w.gate_w,

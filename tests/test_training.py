@@ -209,3 +209,21 @@ def test_gpu_training_steps_reduce_loss(cuda):
         opt.step()
         losses.append(float(loss.detach()))
     assert losses[-1] < 0.9 * losses[0], losses
+
+
+@pytest.mark.gpu
+def test_trained_weights_round_trip_to_reference_api(cuda):
+    """module_weights() exports the module's parameters as NsaWeights; the
+    reference-API forward with them equals the module's forward."""
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200.training import NsaUseModule, module_weights
+    params, cq, _, _, _, x, _, w, lists, ng = _instance(41, True, keep=0.05)
+    p = L.AttentionParams(params.n_q_heads, params.n_kv_heads, params.head_dim)
+    part = L.partition(L.TokenSet("volume", x, cq, (16,) * 3))
+    mod = NsaUseModule(p, ng, weights=_our_weights(w, ng))
+    with torch.no_grad():
+        mod.w_o.mul_(1.5)                      # "trained": differs from the initial weights
+    xg = torch.tensor(x, device="cuda")
+    got = mod(xg, xg, part, part, sel=L.Selection(lists)).detach().cpu().numpy()
+    ref = L.nsa_cross_attention(x, x, part, part, L.Selection(lists), module_weights(mod), p)
+    assert np.max(np.abs(got - ref)) < 1e-5
