@@ -115,6 +115,60 @@ struct KeySet {
 };
 
 constexpr int kDqWarps = 4;
+
+// Walks the 16-key tiles of query i's key set (one warp, warp-private smem
+// tiles sK / sV): the next tile's K / V rows are loaded into registers while
+// body(k0, hi) computes on the current one.
+template <int DH, class Body>
+__device__ __forceinline__ void walk_tiles(const KeySet& ks, int64_t i,
+                                           const __nv_bfloat16* __restrict__ k,
+                                           const __nv_bfloat16* __restrict__ v, int64_t kstride,
+                                           int g, int lane, __nv_bfloat16* sK,
+                                           __nv_bfloat16* sV, Body&& body) {
+  constexpr int LD = DH + 8, PER = 16 * (DH / 8) / 32;
+  const int nr = ks.n_ranges(i);
+  int sidx = -1;
+  int64_t k0 = 0, hi = 0;
+  auto advance = [&]() -> bool {
+    k0 += 16;
+    while (k0 >= hi) {
+      if (++sidx >= nr) return false;
+      int64_t lo;
+      ks.range(i, sidx, lo, hi);
+      k0 = lo;
+    }
+    return true;
+  };
+  uint4 rk[PER], rv[PER];
+  auto fetch = [&]() {
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int e = lane + 32 * p, r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
+      rk[p] = rv[p] = make_uint4(0, 0, 0, 0);
+      if (k0 + r < hi) {
+        const int64_t base = (k0 + r) * kstride + (int64_t)g * DH + c8;
+        rk[p] = *reinterpret_cast<const uint4*>(k + base);
+        rv[p] = *reinterpret_cast<const uint4*>(v + base);
+      }
+    }
+  };
+  bool have = advance();
+  if (have) fetch();
+  while (have) {
+    const int64_t ck0 = k0, chi = hi;
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int e = lane + 32 * p, r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
+      *reinterpret_cast<uint4*>(sK + r * LD + c8) = rk[p];
+      *reinterpret_cast<uint4*>(sV + r * LD + c8) = rv[p];
+    }
+    __syncwarp();
+    have = advance();
+    if (have) fetch();   // in flight while the current tile is computed
+    body(ck0, chi);
+  }
+}
 constexpr int kCmpKeys = 64;   // CMP: keys per CTA-shared K/V tile
 
 // dQ pass: warp per (query, kv head).
@@ -222,15 +276,7 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
           }
       }
     } else {
-      const int nr = ks.n_ranges(i);
-      for (int sidx = 0; sidx < nr; ++sidx) {
-        int64_t lo, hi;
-        ks.range(i, sidx, lo, hi);
-        for (int64_t k0 = lo; k0 < hi; k0 += 16) {
-          load_kv(k0, hi);
-          body(k0, hi);
-        }
-      }
+      walk_tiles<DH>(ks, i, k, v, kstride, g, lane, sK, sV, body);
     }
   };
   // S tile (16 rows x 16 keys) = Q K^T, keys past hi masked to -inf
@@ -472,27 +518,7 @@ fwd_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, int64_t nq, int h
         }
     }
   } else {
-    const int nr = ks.n_ranges(i);
-    for (int sidx = 0; sidx < nr; ++sidx) {
-      int64_t lo, hi;
-      ks.range(i, sidx, lo, hi);
-      for (int64_t k0 = lo; k0 < hi; k0 += 16) {
-        __syncwarp();
-        for (int e = lane; e < 16 * (DH / 8); e += 32) {
-          const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
-          uint4 vk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-          if (k0 + r < hi) {
-            const int64_t base = (k0 + r) * kstride + (int64_t)g * DH + c8;
-            vk = *reinterpret_cast<const uint4*>(k + base);
-            vv = *reinterpret_cast<const uint4*>(v + base);
-          }
-          *reinterpret_cast<uint4*>(sK + r * LD + c8) = vk;
-          *reinterpret_cast<uint4*>(sV + r * LD + c8) = vv;
-        }
-        __syncwarp();
-        body(k0, hi);
-      }
-    }
+    walk_tiles<DH>(ks, i, k, v, kstride, g, lane, sK, sV, body);
   }
 #pragma unroll
   for (int hr = 0; hr < 2; ++hr) {
