@@ -171,6 +171,47 @@ __device__ __forceinline__ void walk_tiles(const KeySet& ks, int64_t i,
 }
 constexpr int kCmpKeys = 64;   // CMP: keys per CTA-shared K/V tile
 
+// CMP: the CTA's warps share 64-key K / V tiles of all compressed rows; each
+// thread prefetches its share of the next tile into registers while the
+// current one is computed.  sub(k0, tk, tv) runs per 16-key sub-tile (valid
+// warps only; every thread joins the barriers).
+template <int DH, class Sub>
+__device__ __forceinline__ void walk_cmp_tiles(int64_t nk, const __nv_bfloat16* __restrict__ k,
+                                               const __nv_bfloat16* __restrict__ v,
+                                               int64_t kstride, int g, bool valid,
+                                               __nv_bfloat16* shK, __nv_bfloat16* shV,
+                                               Sub&& sub) {
+  constexpr int LD = DH + 8, PER = kCmpKeys * (DH / 8) / (32 * kDqWarps);
+  uint4 rk[PER], rv[PER];
+  auto fetch = [&](int64_t kb) {
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int e = threadIdx.x + 32 * kDqWarps * p, r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
+      rk[p] = rv[p] = make_uint4(0, 0, 0, 0);
+      if (kb + r < nk) {
+        const int64_t base = (kb + r) * kstride + (int64_t)g * DH + c8;
+        rk[p] = *reinterpret_cast<const uint4*>(k + base);
+        rv[p] = *reinterpret_cast<const uint4*>(v + base);
+      }
+    }
+  };
+  if (nk > 0) fetch(0);
+  for (int64_t kb = 0; kb < nk; kb += kCmpKeys) {
+    __syncthreads();   // the previous tile is no longer read
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int e = threadIdx.x + 32 * kDqWarps * p, r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
+      *reinterpret_cast<uint4*>(shK + r * LD + c8) = rk[p];
+      *reinterpret_cast<uint4*>(shV + r * LD + c8) = rv[p];
+    }
+    __syncthreads();
+    if (kb + kCmpKeys < nk) fetch(kb + kCmpKeys);   // in flight during the compute
+    if (valid)
+      for (int t = 0; t < kCmpKeys / 16 && kb + 16 * t < nk; ++t)
+        sub(kb + 16 * t, shK + t * 16 * LD, shV + t * 16 * LD);
+  }
+}
+
 // dQ pass: warp per (query, kv head).
 template <int DH, bool CMP>
 __global__ void __launch_bounds__(32 * kDqWarps)
@@ -254,27 +295,12 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
   const __nv_bfloat16* tV = sV;
   auto for_tiles = [&](auto&& body) {
     if constexpr (CMP) {
-      for (int64_t kb = 0; kb < ks.nk; kb += kCmpKeys) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < kCmpKeys * (DH / 8); e += blockDim.x) {
-          const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
-          uint4 vk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-          if (kb + r < ks.nk) {
-            const int64_t base = (kb + r) * kstride + (int64_t)g * DH + c8;
-            vk = *reinterpret_cast<const uint4*>(k + base);
-            vv = *reinterpret_cast<const uint4*>(v + base);
-          }
-          *reinterpret_cast<uint4*>(shK + r * LD + c8) = vk;
-          *reinterpret_cast<uint4*>(shV + r * LD + c8) = vv;
-        }
-        __syncthreads();
-        if (valid)
-          for (int sub = 0; sub < kCmpKeys / 16 && kb + 16 * sub < ks.nk; ++sub) {
-            tK = shK + sub * 16 * LD;
-            tV = shV + sub * 16 * LD;
-            body(kb + 16 * sub, ks.nk);
-          }
-      }
+      walk_cmp_tiles<DH>(ks.nk, k, v, kstride, g, valid, shK, shV,
+                         [&](int64_t k0, const __nv_bfloat16* tk, const __nv_bfloat16* tv) {
+                           tK = tk;
+                           tV = tv;
+                           body(k0, ks.nk);
+                         });
     } else {
       walk_tiles<DH>(ks, i, k, v, kstride, g, lane, sK, sV, body);
     }
@@ -496,27 +522,12 @@ fwd_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, int64_t nq, int h
       }
   };
   if constexpr (CMP) {
-    for (int64_t kb = 0; kb < ks.nk; kb += kCmpKeys) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < kCmpKeys * (DH / 8); e += blockDim.x) {
-        const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
-        uint4 vk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-        if (kb + r < ks.nk) {
-          const int64_t base = (kb + r) * kstride + (int64_t)g * DH + c8;
-          vk = *reinterpret_cast<const uint4*>(k + base);
-          vv = *reinterpret_cast<const uint4*>(v + base);
-        }
-        *reinterpret_cast<uint4*>(shK + r * LD + c8) = vk;
-        *reinterpret_cast<uint4*>(shV + r * LD + c8) = vv;
-      }
-      __syncthreads();
-      if (valid)
-        for (int sub = 0; sub < kCmpKeys / 16 && kb + 16 * sub < ks.nk; ++sub) {
-          tK = shK + sub * 16 * LD;
-          tV = shV + sub * 16 * LD;
-          body(kb + 16 * sub, ks.nk);
-        }
-    }
+    walk_cmp_tiles<DH>(ks.nk, k, v, kstride, g, valid, shK, shV,
+                       [&](int64_t k0, const __nv_bfloat16* tk, const __nv_bfloat16* tv) {
+                         tK = tk;
+                         tV = tv;
+                         body(k0, ks.nk);
+                       });
   } else {
     walk_tiles<DH>(ks, i, k, v, kstride, g, lane, sK, sV, body);
   }
