@@ -642,29 +642,52 @@ dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloa
     const int n_match = wsum[0] + wsum[1] + wsum[2] + wsum[3];
     if (match) qlist[before] = (int)i;   // absolute query index
     __syncthreads();
-    for (int mb = 0; mb < n_match; mb += QB) {
+    // Q / dO rows of the G heads of QB queries (rows >= G zero; lse = +inf ->
+    // P = 0), staged through registers: round mb+QB is fetched while round mb
+    // is computed
+    constexpr int PERQ = QB * 2 * 16 * (DH / 8) / 128;
+    static_assert(PERQ * 128 == QB * 2 * 16 * (DH / 8) && QB * 16 <= 128, "staging shape");
+    uint4 rq[PERQ];
+    float rl = __builtin_huge_valf(), rd = 0.f;
+    auto fetch = [&](int mb) {
       const int nb = min(QB, n_match - mb);
-      // Q and dO rows of the G heads of nb queries (rows >= G zero; lse = +inf -> P = 0)
-      for (int e2 = tid; e2 < QB * 2 * 16 * (DH / 8); e2 += 128) {
+#pragma unroll
+      for (int p = 0; p < PERQ; ++p) {
+        const int e2 = tid + 128 * p;
         const int qb = e2 / (2 * 16 * (DH / 8)), rem = e2 % (2 * 16 * (DH / 8));
         const int which = rem / (16 * (DH / 8)), e = rem % (16 * (DH / 8));
         const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
-        uint4 val = make_uint4(0, 0, 0, 0);
+        rq[p] = make_uint4(0, 0, 0, 0);
         if (qb < nb && r < G) {
-          const int64_t qi = qlist[mb + qb];
-          const int64_t src = ((qi * hq) + (int64_t)g * G + r) * DH + c8;
-          val = *reinterpret_cast<const uint4*>((which ? dob : q) + src);
+          const int64_t src = (((int64_t)qlist[mb + qb] * hq) + (int64_t)g * G + r) * DH + c8;
+          rq[p] = *reinterpret_cast<const uint4*>((which ? dob : q) + src);
         }
-        *reinterpret_cast<uint4*>((which ? sO[qb] : sQ[qb]) + r * LD + c8) = val;
       }
-      for (int e = tid; e < QB * 16; e += 128) {
-        const int qb = e / 16, h = e % 16;
+      if (tid < QB * 16) {
+        const int qb = tid / 16, h = tid % 16;
         const bool ok = qb < nb && h < G;
         const int64_t t = ok ? (int64_t)qlist[mb + qb] * hq + (int64_t)g * G + h : 0;
-        sL[qb][h] = ok ? lse[t] : __builtin_huge_valf();
-        sD[qb][h] = ok ? dsum[t] : 0.f;
+        rl = ok ? lse[t] : __builtin_huge_valf();
+        rd = ok ? dsum[t] : 0.f;
+      }
+    };
+    if (n_match > 0) fetch(0);
+    for (int mb = 0; mb < n_match; mb += QB) {
+      const int nb = min(QB, n_match - mb);
+#pragma unroll
+      for (int p = 0; p < PERQ; ++p) {
+        const int e2 = tid + 128 * p;
+        const int qb = e2 / (2 * 16 * (DH / 8)), rem = e2 % (2 * 16 * (DH / 8));
+        const int which = rem / (16 * (DH / 8)), e = rem % (16 * (DH / 8));
+        const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
+        *reinterpret_cast<uint4*>((which ? sO[qb] : sQ[qb]) + r * LD + c8) = rq[p];
+      }
+      if (tid < QB * 16) {
+        sL[tid / 16][tid % 16] = rl;
+        sD[tid / 16][tid % 16] = rd;
       }
       __syncthreads();
+      if (mb + QB < n_match) fetch(mb + QB);   // in flight during this round
       for (int qb = 0; qb < nb; ++qb) {
         uint32_t bq[DH / 16][4], bo[DH / 16][4];
         load_b_nt<DH>(sQ[qb], lane, bq);
