@@ -276,21 +276,6 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
   load_a<DH>(sO, lane, ao);
   const float scale = 1.0f / sqrtf((float)DH);
   const int64_t kstride = (int64_t)hkv * DH;
-  auto load_kv = [&](int64_t k0, int64_t hi) {
-    __syncwarp();
-    for (int e = lane; e < 16 * (DH / 8); e += 32) {
-      const int r = e / (DH / 8), c8 = (e % (DH / 8)) * 8;
-      uint4 vk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (k0 + r < hi) {
-        const int64_t base = (k0 + r) * kstride + (int64_t)g * DH + c8;
-        vk = *reinterpret_cast<const uint4*>(k + base);
-        vv = *reinterpret_cast<const uint4*>(v + base);
-      }
-      *reinterpret_cast<uint4*>(sK + r * LD + c8) = vk;
-      *reinterpret_cast<uint4*>(sV + r * LD + c8) = vv;
-    }
-    __syncwarp();
-  };
   const __nv_bfloat16* tK = sK;   // current 16-key K / V tile
   const __nv_bfloat16* tV = sV;
   auto for_tiles = [&](auto&& body) {
