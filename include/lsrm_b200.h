@@ -331,7 +331,7 @@ typedef struct lsrm_kv_job {
   float* mean_out;
   void* cmp_il;
   int64_t cmp_rows_pad;
-  const int32_t* work;   /* [n_work]: block * 16 + 64-token sub-tile, by block;
+  const int32_t* work;   /* [n_work]: (block << 12) | 64-token sub-tile, by block;
                             one CTA each */
   int64_t n_work;
   float* partial;        /* [n_work][hkv*dh] scratch: per-sub-tile column sums */

@@ -56,17 +56,15 @@ def is_device(x):
     return isinstance(x, torch.Tensor) and x.device.type == "cuda"
 
 
-_WCACHE = {}
-
-
 def weight(arr, dtype=torch.float32):
-    """Device copy of a host weight array, made once per (array, dtype,
-    device). Works for any weight container (this package's dataclasses or the
+    """Device copy of a host weight array for one reference-API call.
+
+    The reference functions are pure functions of their arguments, so the
+    weights are read afresh on every call: a caller that updates a NumPy
+    weight in place sees the update, and nothing outlives the call.  (The
+    device-resident engines upload their weights once, at construction.)
+    Works for any weight container (this package's dataclasses or the
     reference's), which is what the drop-in needs."""
-    key = (id(arr), dtype, torch.cuda.current_device())
-    hit = _WCACHE.get(key)
-    if hit is not None and hit[0] is arr:
-        return hit[1]
-    t = dev(arr, dtype)
-    _WCACHE[key] = (arr, t)
-    return t
+    if is_device(arr):
+        return arr if arr.dtype == dtype else arr.to(dtype)
+    return dev(arr, dtype)

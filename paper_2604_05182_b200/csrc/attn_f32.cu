@@ -122,8 +122,41 @@ __global__ void sigmoid_f32_kernel(const float* __restrict__ gl, int64_t ld,
   }
 }
 
+// The reference's score is np.einsum("xhd,yhd->xy", q64, k64) over C-contiguous
+// operands (nsa_attention.py:226-227).  NumPy's einsum coalesces (h, d) into
+// one contiguous inner loop of n = h_q*d_h products and reduces it with its
+// baseline-SIMD sum-of-products kernel (x86-64 baseline SSE2: 2 f64 lanes, no
+// FMA): per group of 8 elements each lane l adds the products of elements
+// 6+l, 4+l, 2+l, l in that order, the tail is added pair by pair, then lane 0
+// + lane 1.  Restated here with explicit round-to-nearest mul/add so the f64
+// scores -- and therefore the ranked block ids, ties included -- are bit-equal.
+__device__ __forceinline__ double einsum_score(const float* __restrict__ qi,
+                                               const float* __restrict__ kb, int hq, int g,
+                                               int dh) {
+  const int n = hq * dh;
+  auto prod = [&](int e) {
+    int h = e / dh, c = e - h * dh;
+    return __dmul_rn((double)qi[e], (double)kb[(h / g) * dh + c]);
+  };
+  double v0 = 0.0, v1 = 0.0;
+  int i = 0;
+  for (; n - i >= 8; i += 8) {
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+      v0 = __dadd_rn(prod(i + 2 * j), v0);
+      v1 = __dadd_rn(prod(i + 2 * j + 1), v1);
+    }
+  }
+  for (; i < n; i += 2) {
+    v0 = __dadd_rn(prod(i), v0);
+    if (i + 1 < n) v1 = __dadd_rn(prod(i + 1), v1);
+  }
+  return __dadd_rn(0.0, __dadd_rn(v0, v1));
+}
+
 // Vanilla selection (nsa_attention.py:210-232): score = sum_h sum_d q.k_cmp in
-// f64, unscaled; stable descending top-b_sel == lexicographic (-score, col).
+// f64, unscaled, in einsum's order; stable descending top-b_sel ==
+// lexicographic (-score, col).
 __global__ void score_topk_kernel(const float* __restrict__ q, int64_t nq, int hq, int hkv,
                                   int dh, const float* __restrict__ kc, int nb, int b_sel,
                                   int32_t* __restrict__ out_rows,
@@ -139,11 +172,7 @@ __global__ void score_topk_kernel(const float* __restrict__ q, int64_t nq, int h
     double best = __builtin_huge_val();
     int bi = 0x7fffffff;
     for (int b = lane; b < nb; b += 32) {
-      double sc = 0.0;
-      for (int h = 0; h < hq; ++h)
-        for (int c = 0; c < dh; ++c)
-          sc += (double)q[(i * hq + h) * dh + c] * (double)kc[((int64_t)b * hkv + h / g) * dh + c];
-      double key = -sc;
+      double key = -einsum_score(q + i * hq * dh, kc + (int64_t)b * hkv * dh, hq, g, dh);
       if (lex_less(last_v, last_i, key, b) && lex_less(key, b, best, bi)) { best = key; bi = b; }
     }
     for (int o = 16; o; o >>= 1) {

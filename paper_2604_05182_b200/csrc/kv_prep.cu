@@ -35,7 +35,7 @@ struct KvJob {
   float* mean_out;
   __nv_bfloat16* cmp_il;
   int64_t cmp_rows_pad;
-  const int32_t* work;   // per CTA: block * 16 + 64-token sub-tile, ordered by block
+  const int32_t* work;   // per CTA: (block << 12) | 64-token sub-tile, ordered by block
   int64_t n_work;
   float* partial;        // [n_work][W] per-sub-tile column sums
   int32_t* arrive;       // [n_blocks] arrival counters (zero between launches)
@@ -43,6 +43,7 @@ struct KvJob {
 static_assert(sizeof(KvJob) == sizeof(lsrm_kv_job), "KvJob must mirror lsrm_kv_job");
 
 constexpr int kSub = 64;   // tokens per sub-tile (4 warps x 16 rows)
+constexpr int kSubBits = 12;   // work code = (block << kSubBits) | sub-tile
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
   const int64_t wi = blockIdx.x;
   if (wi >= J.n_work) return;
   const int code = J.work[wi];
-  const int64_t b = code >> 4, sub = code & 15;
+  const int64_t b = code >> kSubBits, sub = code & ((1 << kSubBits) - 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int hkv = W / dh, vw = dh + (int)J.ones_cols;
   const int64_t lo = J.blk_off[b], occ = J.blk_off[b + 1] - lo, prow0 = J.pad_off[b];

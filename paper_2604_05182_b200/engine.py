@@ -50,8 +50,14 @@ USE_GEOM = {"v2v": ("x", "x", 3), "v2i": ("x", "y", 2), "i2i": ("y", "y", 3),
             "i2v": ("y", "x", 2)}
 ROW_PAD = 16
 ONES_COLS = 16
-# cross uses (v2i, i2v) tile their signature-sorted tokens across query blocks
-CROSS_GLOBAL_TILES = os.environ.get("LSRM_CROSS_GLOBAL_TILES", "1") != "0"
+# cross uses (v2i, i2v) may tile their signature-sorted tokens across query
+# blocks (LSRM_CROSS_GLOBAL_TILES=1: ~5% faster attention).  Off by default: a
+# row's online-softmax rescale points depend on how its keys fall into the
+# tile's chunks, so tiles that mix blocks make results depend on tile-mates,
+# and a sharded rank (which owns whole blocks) could not reproduce them.  With
+# block tiles every output row is bit-identical for every world size W
+# (the reference's serial == parallel contract, tests/test_seq_parallel.py).
+CROSS_GLOBAL_TILES = os.environ.get("LSRM_CROSS_GLOBAL_TILES", "0") != "0"
 # self uses tile across blocks too; their window branch then spans each tile's
 # distinct own blocks (per-token own rows). Correct, measured neutral
 # (1.230 -> 1.236 ms), so off.
@@ -340,7 +346,12 @@ class SparseLayerEngine:
                     mean, cmp_il = None, self.buf[(kind + "c_il", use)]
                 occ = np.diff(m.loc_off_host)
                 nsub = (occ + 63) // 64
-                work = np.concatenate([b * 16 + np.arange(k) for b, k in enumerate(nsub)])
+                # work code = (block << 12) | 64-token sub-tile (kv_prep.cu kSubBits)
+                require(int(nsub.max(initial=0)) <= 1 << 12 and nb < 1 << 19,
+                        f"kv_prepare: blocks of up to {64 << 12} tokens and fewer than "
+                        f"{1 << 19} occupied blocks are supported (got {int(occ.max(initial=0))} "
+                        f"tokens, {nb} blocks)")
+                work = np.concatenate([(b << 12) + np.arange(k) for b, k in enumerate(nsub)])
                 work_d = D.dev(work.astype(np.int32))
                 partial = D.empty((work.size, self.w), torch.float32)
                 arrive = D.zeros((max(nb, 1),), torch.int32)

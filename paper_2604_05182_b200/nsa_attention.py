@@ -382,8 +382,14 @@ def nsa_cross_attention(x, kv_feats, part_q: BlockPartition, part_kv: BlockParti
             _attn(1, q, k3, v3, params, offs=part_kv.dev("block_offsets"), rows=rows,
                   count=count)]
     if is_self:
+        # win_attention's contract (`nsa_attention.py:92-112`): self pairs only
+        if part_q is not part_kv and not np.array_equal(part_q.block_of_token,
+                                                        part_kv.block_of_token):
+            raise ConfigurationError("window attention requires the query and key partitions "
+                                     "to be the same (self-attention only)")
+        require(n == part_kv.n_tokens, "window attention needs one query per key token")
         outs.append(_attn(2, q, k3, v3, params, offs=part_kv.dev("block_offsets"),
-                          own_row=part_q.dev("row_of_token")))
+                          own_row=part_kv.dev("row_of_token")))
     out = _combine_dev(xd, outs, w)
     out = out if on_dev else D.host(out)
     if return_selection:

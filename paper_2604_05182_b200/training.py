@@ -248,14 +248,16 @@ class NsaUseModule(torch.nn.Module):
     (`nsa_attention.py:239-263`); compression ResBlocks are ck_* / cv_*."""
 
     def __init__(self, params: AttentionParams, n_gates: int, weights: NsaWeights = None,
-                 seed: int = 0, fast_backward: bool = False):
+                 seed: int = 0, fast_backward: bool = False, tags: tuple = ("train",)):
         super().__init__()
         require(n_gates in (2, 3), "n_gates must be 2 (cross) or 3 (self)")
         self.params, self.n_gates = params, n_gates
         self.fast_backward = fast_backward
         if weights is None:
+            # tagged Philox streams (`rng.py`): distinct tags give distinct
+            # parameters, like the reference's per-use tags (xs/xc/ys/yc)
             from .nsa_attention import init_nsa_weights
-            weights = init_nsa_weights(seed, params, n_gates, "train")
+            weights = init_nsa_weights(seed, params, n_gates, *tags)
         for name, arr in _weight_arrays(weights).items():
             self.register_parameter(name, torch.nn.Parameter(D.dev(arr, torch.float32).clone()))
 
@@ -326,11 +328,11 @@ class NsaLayerModule(torch.nn.Module):
     stream y; returns each use's output."""
 
     def __init__(self, params: AttentionParams, weights: dict = None, seed: int = 0,
-                 fast_backward: bool = False):
+                 fast_backward: bool = False, layer: int = 0):
         super().__init__()
         self.uses = torch.nn.ModuleDict({
             u: NsaUseModule(params, ng, weights=(weights or {}).get(u), seed=seed,
-                            fast_backward=fast_backward)
+                            fast_backward=fast_backward, tags=("train", f"layer{layer}", u))
             for u, (_, _, ng) in USE_STREAMS.items()})
 
     def forward(self, x, y, part_vol, part_img, resolved: dict) -> dict:

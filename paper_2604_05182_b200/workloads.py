@@ -1,14 +1,17 @@
 """Synthetic BASELINE workloads, built without the reference.
 
-The scene-dependent inputs (masks, cameras, image-token surface points) were
-produced once by the REAL reference geometry and committed as fixtures
-(`tests/golden/workload_<cfg>.npz`, script `tests/golden/make_golden.py`).
-Features, positional tables and weights are regenerated here from the same
-tagged Philox streams the reference uses (`rng.py`), so the GPU path and the
-CPU oracle see identical inputs.
+Every config is generated on the GPU with this package's own kernels from the
+reference's fixture recipe (`tests/test_acceptance.py:293-322` of the
+reference): orbit cameras, the informative-voxel mask (plus C4's seeded
+fully occupied blocks), silhouettes -> foreground patches, compaction and the
+image-token surface points.  The tests pin the result against fixtures the
+real reference produced (`tests/golden/workload_<cfg>.npz`,
+`tests/test_workload_gen.py`); the package itself never reads them.
+Features, positional tables and weights come from the same tagged Philox
+streams the reference uses (`rng.py`), so the GPU path and the CPU oracle see
+identical inputs.
 """
 
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -19,16 +22,14 @@ from .rng import stream
 from .tensor_core import AttentionParams
 from .tokenizer import init_pos_embed
 
-FIXTURE_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                           "tests", "golden")
-
 # BASELINE.json configs: C1 tiny (desk heads, fp32), C3 fine stage, C4 skewed,
 # C5 scaled context (~20x object tokens, 18 views; "raise the
 # object radius or S with the same recipe"; generated on the GPU)
 CONFIGS = {
-    "c1": {"params": (8, 1, 8), "dtype": "f32"},
-    "c3": {"params": (32, 2, 32), "dtype": "bf16"},
-    "c4": {"params": (32, 2, 32), "dtype": "bf16"},
+    "c1": {"params": (8, 1, 8), "dtype": "f32", "views": 4, "s_vol": 32, "s_img": 96},
+    "c3": {"params": (32, 2, 32), "dtype": "bf16", "views": 16, "s_vol": 96, "s_img": 96},
+    "c4": {"params": (32, 2, 32), "dtype": "bf16", "views": 16, "s_vol": 96, "s_img": 96,
+           "skew": 12},
     "c5": {"params": (32, 2, 32), "dtype": "bf16", "views": 18, "s_vol": 408, "s_img": 288},
 }
 # the fixture scene (tests/test_acceptance.py:299-300 of the reference)
@@ -87,7 +88,19 @@ def orbit_cameras(count, radius, elevation_deg, image_size, fov_deg=50.0, phase=
     return cams
 
 
-def generate_workload(name: str, views: int, s_vol: int, s_img: int) -> Workload:
+def skew_blocks(vol_mask: np.ndarray, skew: int) -> np.ndarray:
+    """C4's load-balance stress: `skew` seeded 8^3 volume blocks made fully
+    occupied (stream(0, "skew"), the recipe of tests/golden/make_golden.py)."""
+    vol_mask = np.array(vol_mask, dtype=bool, copy=True)
+    g = stream(0, "skew")
+    sb = vol_mask.shape[0] // 8
+    for b in g.choice(sb ** 3, size=skew, replace=False):
+        i, j, k = b // (sb * sb), (b // sb) % sb, b % sb
+        vol_mask[8 * i:8 * i + 8, 8 * j:8 * j + 8, 8 * k:8 * k + 8] = True
+    return vol_mask
+
+
+def generate_workload(name: str, views: int, s_vol: int, s_img: int, skew: int = 0) -> Workload:
     """The fixture recipe (tests/golden/make_golden.py) on the GPU: orbit
     cameras, the informative-voxel mask, silhouettes -> foreground patches,
     compaction and the image-token surface points, all with this package's
@@ -98,6 +111,8 @@ def generate_workload(name: str, views: int, s_vol: int, s_img: int) -> Workload
     from .tokenizer import foreground_patch_mask, informative_voxel_mask, upsample_select_tokens
     cams = orbit_cameras(views, 1.7, 20.0, (8 * s_img, 8 * s_img))
     vol_mask = informative_voxel_mask(SCENE, s_vol)
+    if skew:
+        vol_mask = skew_blocks(D.host(vol_mask) if D.is_device(vol_mask) else vol_mask, skew)
     img_mask = foreground_patch_mask(silhouettes(SCENE, cams, as_device=True))
     img_mask = D.host(img_mask) if D.is_device(img_mask) else img_mask
     fv = 6 if s_vol % 6 == 0 else 4
@@ -116,16 +131,15 @@ def generate_workload(name: str, views: int, s_vol: int, s_img: int) -> Workload
 
 
 def load_workload(name: str) -> Workload:
-    if name in CONFIGS and "views" in CONFIGS[name]:
+    """The named BASELINE config, generated on the GPU (cached per process)."""
+    if name not in _CACHE:
         c = CONFIGS[name]
-        return generate_workload(name, c["views"], c["s_vol"], c["s_img"])
-    z = np.load(os.path.join(FIXTURE_DIR, f"workload_{name}.npz"))
-    s, si, v = int(z["s_vol"]), int(z["s_img"]), int(z["views"])
-    vm = np.unpackbits(z["vol_mask"])[: s ** 3].astype(bool).reshape(s, s, s)
-    im = np.unpackbits(z["img_mask"])[: v * si * si].astype(bool).reshape(v, si, si)
-    cams = [(z["cam_K"][i], z["cam_R"][i], z["cam_t"][i]) for i in range(v)]
-    return Workload(name, v, s, si, int(z["factor_vol"]), int(z["factor_img"]), vm, im, cams,
-                    z["img_points"], int(z["n_vol"]), int(z["n_img"]))
+        _CACHE[name] = generate_workload(name, c["views"], c["s_vol"], c["s_img"],
+                                         c.get("skew", 0))
+    return _CACHE[name]
+
+
+_CACHE = {}
 
 
 def coarse_inputs(wl: Workload, d: int, seed: int = 0):

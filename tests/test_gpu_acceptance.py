@@ -51,7 +51,8 @@ def test_03_residual_identity(cuda):
     x + injection exactly in its residual stream (recon_pipeline.py:461-497)."""
     import paper_2604_05182_b200 as L
     from paper_2604_05182_b200 import recon_pipeline as R
-    from paper_2604_05182_b200.workloads import coarse_inputs, load_workload
+    from paper_2604_05182_b200.workloads import coarse_inputs
+    from fixtures import load_workload
     wl = load_workload("c1")
     params = L.AttentionParams(8, 1, 8)
     x_d, y_d, pe_v, pe_i = coarse_inputs(wl, 64)

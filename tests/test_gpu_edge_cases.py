@@ -106,7 +106,7 @@ def test_query_behind_all_cameras_gets_empty_image_list(cuda):
     """`tests/test_block_routing.py:165-174`: a point behind every camera sees
     no image block."""
     import paper_2604_05182_b200 as L
-    from paper_2604_05182_b200.workloads import load_workload
+    from fixtures import load_workload
     wl = load_workload("c1")
     x_d = np.zeros(((wl.vol_mask.shape[0] // wl.factor_vol) ** 3, 8), np.float32)
     ic = np.argwhere(wl.img_mask)
@@ -130,7 +130,8 @@ def test_query_behind_all_cameras_gets_empty_image_list(cuda):
 
 def test_empty_masks_give_empty_token_sets(cuda):
     import paper_2604_05182_b200 as L
-    from paper_2604_05182_b200.workloads import coarse_inputs, load_workload
+    from paper_2604_05182_b200.workloads import coarse_inputs
+    from fixtures import load_workload
     wl = load_workload("c1")
     x_d, y_d, pe_v, pe_i = coarse_inputs(wl, 64)
     vm = np.zeros_like(wl.vol_mask)
@@ -150,3 +151,27 @@ def test_c_abi_status_maps_to_reference_errors(cuda):
         call("lsrm_nsa_attention_tc", None, 8, 1, 6, 4, 32, None, None, None, None, 16,
              None, None, 1, None, 1, None, None, 8, None, 8, 0, None, 2, None,
              torch.cuda.current_stream().cuda_stream)
+
+
+def test_reference_api_reads_current_weights(cuda):
+    """The reference functions are pure: a NumPy weight updated in place
+    between two calls must be seen by the second call (no stale device
+    copies), and self uses reject mismatched partitions like win_attention."""
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200.errors import ConfigurationError
+    g = np.random.default_rng(5)
+    params = L.AttentionParams(4, 2, 8)
+    coords = np.stack(np.meshgrid(np.arange(12), np.arange(12), np.arange(4), indexing="ij"),
+                      -1).reshape(-1, 3)[g.permutation(576)[:300]]
+    toks = L.TokenSet("volume", np.zeros((300, 32), np.float32), coords, (16,) * 3)
+    part = L.partition(toks)
+    x = g.standard_normal((300, 32)).astype(np.float32)
+    w = L.init_nsa_weights(0, params, 3, "t")
+    sel = L.Selection([part.occupied_ids[:2].copy() for _ in range(300)])
+    a = L.nsa_cross_attention(x, x, part, part, sel, w, params)
+    w.w_o *= 2.0                       # in-place update of the caller's array
+    b = L.nsa_cross_attention(x, x, part, part, sel, w, params)
+    assert np.allclose(b, 2.0 * a, rtol=1e-6, atol=1e-7)
+    toks2 = L.TokenSet("volume", np.zeros((300, 32), np.float32), coords[::-1].copy(), (16,) * 3)
+    with pytest.raises(ConfigurationError):
+        L.nsa_cross_attention(x, x, L.partition(toks2), part, sel, w, params)

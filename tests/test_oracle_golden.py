@@ -10,7 +10,8 @@ import pytest
 
 import oracle as O
 from conftest import GOLDEN, golden, unflat
-from paper_2604_05182_b200.workloads import coarse_inputs, load_workload
+from paper_2604_05182_b200.workloads import coarse_inputs
+from fixtures import load_workload
 
 pytestmark = pytest.mark.filterwarnings("ignore::RuntimeWarning")
 
@@ -42,7 +43,7 @@ def test_compaction_bit_exact(ref_c1, c1_instance):
 
 
 def test_voxel_mask_bit_exact(ref_c1):
-    from paper_2604_05182_b200.workloads import load_workload
+    from fixtures import load_workload
     scene = {"kind": "union", "parts": [
         {"kind": "sphere", "center": [0.42, 0.5, 0.55], "radius": 0.18},
         {"kind": "box", "center": [0.6, 0.45, 0.4], "half_sizes": [0.12, 0.12, 0.12]}]}

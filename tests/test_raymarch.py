@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import oracle.routing as OR
-from paper_2604_05182_b200.workloads import load_workload
+from fixtures import load_workload
 
 SCENE = {"kind": "union", "parts": [
     {"kind": "sphere", "center": [0.42, 0.5, 0.55], "radius": 0.18},

@@ -24,7 +24,8 @@ from paper_2604_05182_b200.errors import ConfigurationError, ProtocolError
 
 @pytest.fixture(scope="module")
 def c1_parts():
-    from paper_2604_05182_b200.workloads import coarse_inputs, load_workload
+    from paper_2604_05182_b200.workloads import coarse_inputs
+    from fixtures import load_workload
     wl = load_workload("c1")
     x_d, y_d, pe_v, pe_i = coarse_inputs(wl, 64)
     x_up, y_up = O.upsample_select_tokens(x_d, y_d, wl.vol_mask, wl.img_mask, pe_v.tables,
@@ -334,10 +335,12 @@ def test_gloo_world2_all_gather_kv():
 @pytest.mark.parametrize("W,by_cost", [(2, True), (3, False)])
 @pytest.mark.parametrize("cross_global", [True, False])
 def test_sharded_engine_matches_unsharded(cuda, W, by_cost, cross_global, monkeypatch):
-    """Sharded engines (block tiles everywhere) vs the single-GPU engine.
-    Self uses are bit-identical; cross uses too when the single-GPU engine
-    also keeps block tiles (cross_global=False); with its default
-    across-block cross tiles they differ by bf16 rounding only."""
+    """Sharded engines vs the single-GPU engine.  With the default block
+    tiles (cross_global=False) EVERY use is bit-identical for every W (the
+    reference's serial == parallel contract, `tests/test_seq_parallel.py:
+    285-325` of the reference).  The opt-in across-block cross tiles
+    (LSRM_CROSS_GLOBAL_TILES=1) are not W-invariant: cross uses then differ
+    by bf16 rounding only."""
     from paper_2604_05182_b200 import engine as E
     monkeypatch.setattr(E, "CROSS_GLOBAL_TILES", cross_global)
     from paper_2604_05182_b200 import _ops

@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(scope="module")
 def c1_tokens(cuda):
     import paper_2604_05182_b200 as L
-    from paper_2604_05182_b200.workloads import coarse_inputs, load_workload
+    from paper_2604_05182_b200.workloads import coarse_inputs
+    from fixtures import load_workload
     wl = load_workload("c1")
     out = {"wl": wl}
     for d in (64, 1024):

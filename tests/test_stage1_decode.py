@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 
 from conftest import golden
-from paper_2604_05182_b200.workloads import coarse_inputs, load_workload
+from paper_2604_05182_b200.workloads import coarse_inputs
+from fixtures import load_workload
 
 FLOAT_TOL = 1e-5      # the reference's own golden tolerance
 DECODE_RTOL = 1e-6    # f64 decode arithmetic, f32 outputs

@@ -1,11 +1,13 @@
-"""The GPU workload generator (workloads.generate_workload, used for C5) must
+"""The GPU workload generator (workloads.generate_workload, every config) must
 reproduce the reference-made fixtures: cameras bit-exact on the CPU; masks,
 token counts and image-token surface points on the GPU."""
 
 import numpy as np
 import pytest
 
-from paper_2604_05182_b200.workloads import load_workload, orbit_cameras
+from paper_2604_05182_b200.workloads import orbit_cameras
+
+from fixtures import load_workload
 
 
 @pytest.mark.parametrize("name,views,s_img", [("c1", 4, 96), ("c3", 16, 96)])
@@ -21,10 +23,14 @@ def test_orbit_cameras_bit_exact(name, views, s_img):
 
 
 @pytest.mark.gpu
-def test_generated_c3_matches_fixture(cuda):
-    from paper_2604_05182_b200.workloads import generate_workload
-    ref = load_workload("c3")
-    got = generate_workload("c3", 16, 96, 96)
+@pytest.mark.parametrize("name", ["c1", "c3", "c4"])
+def test_generated_workload_matches_fixture(cuda, name):
+    """The package's own workloads (what build_instance and bench.py use) are
+    the reference-made fixtures: masks (C4 skew blocks included) and token
+    counts bit-exact, surface points within 1e-12."""
+    from paper_2604_05182_b200 import workloads as W
+    ref = load_workload(name)
+    got = W.load_workload(name)
     assert np.array_equal(got.vol_mask, ref.vol_mask)
     assert np.array_equal(got.img_mask, ref.img_mask)
     assert (got.n_vol, got.n_img) == (ref.n_vol, ref.n_img)
