@@ -95,6 +95,36 @@ int lsrm_route_image(const double* points, int64_t nq, const double* cams,
                      const int64_t* block_offsets, int b_i, int budget,
                      int32_t* out_rows, int32_t* out_count, void* stream);
 
+/* ---- SDF fields  (camera_geometry.py:151-205, runner.py:301-306) -------
+ * kind 0 analytic: prims = n_prims rows of 8 f64 (as lsrm_voxel_mask);
+ * kind 1 decoded: the coarse dense feature grid [side^3, d_f] f32 through the
+ *   decoder's SDF head (w1 [d_f, hidden], b1 [hidden], gelu, w2 [hidden, 1],
+ *   b2 [1]) plus |p - c| - radius, with the reference's f32 rounding points
+ *   and NumPy's einsum reduction order (decode_points(...)[1] of
+ *   recon_pipeline.py:349-365 on FeatureVolume(grid));
+ * kind 2 values: s of each sample precomputed (an opaque callable evaluated
+ *   by the host at the points lsrm_voxel_sample_points /
+ *   lsrm_ray_sample_points produce), indexed by sample id. */
+typedef struct lsrm_sdf_field {
+  int32_t kind;
+  int32_t n_prims;
+  const double* prims;
+  const float* grid;
+  int32_t side;
+  int32_t d_f;
+  int32_t hidden;
+  int32_t pad_;
+  const float* w1;
+  const float* b1;
+  const float* w2;
+  const float* b2;
+  double radius;
+  const double* values;
+} lsrm_sdf_field;
+
+/* LSRM_OK if the descriptor is usable, else LSRM_E_CONFIG with a message. */
+int lsrm_check_field(const lsrm_sdf_field* field);
+
 /* ---- router input producer  (block_routing.py:73-108,
  *      camera_geometry.py:236-302) ------------------------------------------
  * Surface point of every image token's patch-center ray: 128-sample Laplace
@@ -109,6 +139,19 @@ int lsrm_image_token_points(const int64_t* coords, int64_t n, const double* cams
                             const int32_t* image_wh, int n_views, int rows_f,
                             const double* sdf, int n_prims, double beta,
                             double* points, uint8_t* miss, void* stream);
+
+/* The same for any field (analytic, decoded, or values with sample id
+ * ray * 128 + k). */
+int lsrm_image_token_points_field(const int64_t* coords, int64_t n, const double* cams,
+                                  const int32_t* image_wh, int n_views, int rows_f,
+                                  const lsrm_sdf_field* field, double beta, double* points,
+                                  uint8_t* miss, void* stream);
+/* The 128 march sample points of every ray, points [n, 128, 3] f64, for an
+ * opaque field the host evaluates; has_span [n] = 0 for rays missing the cube
+ * (their samples are placeholders the march never reads). */
+int lsrm_ray_sample_points(const int64_t* coords, int64_t n, const double* cams,
+                           const int32_t* image_wh, int n_views, int rows_f, double* points,
+                           uint8_t* has_span, void* stream);
 
 /* Plücker rays (camera_geometry.py:91-107): [n_views, gh, gw, 6] float32
  * rows (unit direction d, moment t x d) through the centers of a gw x gh grid
@@ -146,6 +189,16 @@ int lsrm_foreground_mask(const float* alpha, int n_views, int h, int w,
  * primitives (camera_geometry.py:190-205). */
 int lsrm_voxel_mask(const double* sdf, int n_prims, int s_vol, double tau,
                     int t_side, uint8_t* mask, void* stream);
+
+/* Eq. 11 for any field over the voxels of x-slabs [i0, i1) (mask is the full
+ * [s_vol^3] array; other slabs untouched).  For kind 2 the values cover
+ * exactly those slabs in the layout of lsrm_voxel_sample_points. */
+int lsrm_voxel_mask_field(const lsrm_sdf_field* field, int s_vol, double tau, int t_side,
+                          int i0, int i1, uint8_t* mask, void* stream);
+/* Cell-center sample points of x-slabs [i0, i1), the reference's layout
+ * (tokenizer.py:227-235): points [(i1-i0) * t * (t s)^2, 3] f64. */
+int lsrm_voxel_sample_points(int s_vol, int t_side, int i0, int i1, double* points,
+                             void* stream);
 
 /* ---- compaction  (tokenizer.py:255-313) -------------------------------
  * Stream-compacts mask-true cells in flat order and gathers parent feature +
@@ -459,6 +512,13 @@ int lsrm_attention_fwd_mma(int mode, const void* q_bf16, int64_t nq, int hq, int
  * f64 arithmetic, the reference's f32 rounding points, NumPy operation order.
  * decode_scatter: vec [side^3, t^3*d_f] (token-major, slice [dz,dy,dx,c]) ->
  * grid [(t*side)^3, d_f]. */
+/* y[n, dout] (row stride ldy) = f32(act(f32(x W + bias))): the reference's
+ * affine (tensor_core.py:100-116: f64 accumulation in np.einsum's order) and
+ * activation (act 0 identity, 1 erf-gelu, 2 sigmoid; tensor_core.py:82-94).
+ * x [n, din] f32 (row stride ldx), W [din, dout] f32, bias [dout] or NULL. */
+int lsrm_affine_exact(const float* x, int64_t ldx, int64_t n, int din, const float* w,
+                      const float* bias, int dout, int act, float* y, int64_t ldy,
+                      void* stream);
 int lsrm_decode_scatter(const float* vec, int side, int t, int d_f, float* grid, void* stream);
 /* sparse fine features: rows [n*t^3, d_f] and index [s_f^3] int64 (-1 absent). */
 int lsrm_sparse_features(const float* vec, const int64_t* coords, int64_t n, int t, int d_f,

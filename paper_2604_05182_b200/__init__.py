@@ -33,6 +33,7 @@ from .recon_pipeline import (DecodeWeights, DecoderHeads, DenseBlockWeights, Fea
                              decode_feature_volume, decode_point, decode_points,
                              dense_block_forward, dense_stage_forward, init_decode,
                              init_decoder_heads, init_dense_block, mha_forward, query_field,
-                             sparse_block_forward, sparse_stage_forward)
+                             sparse_block_forward, sparse_stage_forward, affine_exact)
+from .sdf import DecodedSdf, callable_field, decoded_sdf_field
 
 __version__ = "0.1.0"

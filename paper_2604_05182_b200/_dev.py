@@ -1,6 +1,9 @@
 """Device plumbing: torch owns device memory and streams; compute goes through
 the C ABI.  No CPU fallback: `require_cuda()` raises without a GPU."""
 
+import weakref
+from collections import OrderedDict
+
 import numpy as np
 import torch
 
@@ -56,15 +59,38 @@ def is_device(x):
     return isinstance(x, torch.Tensor) and x.device.type == "cuda"
 
 
-def weight(arr, dtype=torch.float32):
-    """Device copy of a host weight array for one reference-API call.
+_WCACHE = OrderedDict()   # (id, dtype, device) -> (weakref to the array, snapshot, tensor)
+_WCACHE_MAX = 256
 
-    The reference functions are pure functions of their arguments, so the
-    weights are read afresh on every call: a caller that updates a NumPy
-    weight in place sees the update, and nothing outlives the call.  (The
-    device-resident engines upload their weights once, at construction.)
-    Works for any weight container (this package's dataclasses or the
-    reference's), which is what the drop-in needs."""
+
+def weight(arr, dtype=torch.float32):
+    """Device copy of a host weight array.
+
+    The reference functions are pure functions of their arguments, so a
+    cached copy is only reused while the caller's array is alive AND still
+    holds the same values (compared against a host snapshot: a weight updated
+    in place is re-uploaded).  The cache is a bounded LRU, and it keeps the
+    device copy alive past the launch that reads it.  Works for any weight
+    container (this package's dataclasses or the reference's), which is what
+    the drop-in needs."""
     if is_device(arr):
         return arr if arr.dtype == dtype else arr.to(dtype)
-    return dev(arr, dtype)
+    a = np.asarray(arr)
+    key = (id(arr), dtype, torch.cuda.current_device())
+    hit = _WCACHE.get(key)
+    if hit is not None:
+        ref, snap, t = hit
+        if ref() is arr and snap.shape == a.shape and snap.dtype == a.dtype and \
+                np.array_equal(snap, a, equal_nan=snap.dtype.kind == "f"):
+            _WCACHE.move_to_end(key)
+            return t
+        del _WCACHE[key]
+    t = dev(a, dtype)
+    try:
+        ref = weakref.ref(arr)
+    except TypeError:      # not weak-referenceable: no caching
+        return t
+    _WCACHE[key] = (ref, a.copy(), t)
+    while len(_WCACHE) > _WCACHE_MAX:
+        _WCACHE.popitem(last=False)
+    return t

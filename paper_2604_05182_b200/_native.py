@@ -88,6 +88,12 @@ SIGNATURES = {
                                P]),
     "lsrm_attention_fwd_mma": (I32, [I32, P, I64, I32, I32, I32, P, P, I64, P, P, P, I32, P, P, P,
                                      P]),
+    "lsrm_check_field": (I32, [P]),
+    "lsrm_image_token_points_field": (I32, [P, I64, P, P, I32, I32, P, F64, P, P, P]),
+    "lsrm_ray_sample_points": (I32, [P, I64, P, P, I32, I32, P, P, P]),
+    "lsrm_voxel_mask_field": (I32, [P, I32, F64, I32, I32, I32, P, P]),
+    "lsrm_voxel_sample_points": (I32, [I32, I32, I32, I32, P, P]),
+    "lsrm_affine_exact": (I32, [P, I64, I64, I32, P, P, I32, I32, P, I64, P]),
 }
 
 _lib = None

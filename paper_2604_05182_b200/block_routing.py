@@ -69,12 +69,16 @@ LAPLACE_BETA = 0.02   # camera_geometry.py:19
 def image_token_coords(tokens, cameras, field, beta: float = LAPLACE_BETA) -> TokenCoords3D:
     """Surface point of each image token's patch-center ray
     (`block_routing.py:73-108`): 128-sample Laplace opacity march
-    (`camera_geometry.py:264-302`) on the GPU, f64; rays with no opacity peak
-    fall back to their cube-entry point, rays missing the cube to the clamped
-    closest approach to the cube center, both flagged in `miss`."""
-    from .tokenizer import sdf_primitives
+    (`camera_geometry.py:264-302`) on the GPU, f64, warp per ray; rays with
+    no opacity peak fall back to their cube-entry point, rays missing the cube
+    to the clamped closest approach to the cube center, both flagged in
+    `miss`.  `field` as in `informative_voxel_mask`: analytic, the decoded
+    coarse volume (in-kernel), or any callable field (called on the
+    GPU-generated sample points of the rays that enter the cube)."""
+    from .sdf import DeviceField, ptr as sdf_ptr
     n_views, rows_f, _ = tokens.grid_res
     require(len(cameras) == n_views, "camera count != view count")
+    require(beta > 0, "beta must be positive")
     wh = []
     for cam in cameras:
         size = getattr(cam, "image_size", None)
@@ -85,12 +89,25 @@ def image_token_coords(tokens, cameras, field, beta: float = LAPLACE_BETA) -> To
     coords = D.dev(tokens.coords, torch.int64)
     cams = D.dev(pack_cameras(cameras))
     whd = D.dev(np.asarray(wh, np.int32).reshape(-1, 2))
-    prims = D.dev(sdf_primitives(field))
+    f = DeviceField(field)
     pts = D.empty((max(n, 1), 3), torch.float64)
     miss = D.empty((max(n, 1),), torch.uint8)
-    call("lsrm_image_token_points", coords.data_ptr(), n, cams.data_ptr(), whd.data_ptr(),
-         n_views, rows_f, prims.data_ptr(), int(prims.shape[0]), float(beta), pts.data_ptr(),
-         miss.data_ptr(), D.stream())
+    st = D.stream()
+    desc = f.desc
+    if f.opaque and n:
+        samples = D.empty((n * 128, 3), torch.float64)
+        span = D.empty((n,), torch.uint8)
+        call("lsrm_ray_sample_points", coords.data_ptr(), n, cams.data_ptr(), whd.data_ptr(),
+             n_views, rows_f, samples.data_ptr(), span.data_ptr(), st)
+        live = span.bool().repeat_interleave(128)
+        vals = torch.zeros((n * 128,), dtype=torch.float64, device=samples.device)
+        if bool(live.any()):
+            vals[live] = f.eval_host(samples[live])
+        desc = f.values_desc(vals)
+    if n:
+        call("lsrm_image_token_points_field", coords.data_ptr(), n, cams.data_ptr(),
+             whd.data_ptr(), n_views, rows_f, sdf_ptr(desc), float(beta), pts.data_ptr(),
+             miss.data_ptr(), st)
     return TokenCoords3D(D.host(pts)[:n], D.host(miss)[:n].astype(bool))
 
 

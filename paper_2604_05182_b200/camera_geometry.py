@@ -10,7 +10,7 @@ from . import _dev as D
 from ._native import call
 from .block_routing import pack_cameras
 from .errors import require
-from .tokenizer import sdf_primitives
+from .sdf import callable_field, decoded_sdf_field, sdf_primitives  # noqa: F401
 
 
 def _image_sizes(cameras):

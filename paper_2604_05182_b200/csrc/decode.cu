@@ -3,12 +3,12 @@
 // feature rows + cell index, and the blended field query feeding the two
 // decoder heads.  f64 arithmetic with the reference's f32 rounding points
 // and NumPy's unfused operation order (compiled with --fmad=false).
-#include "common.cuh"
+#include "field.cuh"
 
 namespace lsrm {
 
-constexpr int kMaxDf = 64;
-constexpr int kMaxHidden = 128;
+constexpr int kMaxDf = kFieldMaxDf;
+constexpr int kMaxHidden = kFieldMaxHidden;
 
 // grid[(t*side)^3, d_f]: fine cell (t*i+dx, t*j+dy, t*k+dz) takes slice
 // [dz, dy, dx] of token (i, j, k)'s vector (recon_pipeline.py:209-220)
@@ -48,59 +48,6 @@ __global__ void sparse_features_kernel(const float* __restrict__ vec,
                     z = coords[3 * tok + 2] * t + dz;
       index[(x * s_f + y) * s_f + z] = r;
     }
-  }
-}
-
-__device__ __forceinline__ void tri_prepare(const double* p, int side, int64_t* i0,
-                                            double* frac) {
-  for (int a = 0; a < 3; ++a) {
-    const double t = p[a] * side - 0.5;
-    double f = floor(t);
-    f = f < 0.0 ? 0.0 : (f > (double)(side - 2) ? (double)(side - 2) : f);
-    i0[a] = (int64_t)f;
-    frac[a] = t - (double)i0[a];
-  }
-}
-
-// trilinear_interpolate_many (tensor_core.py:228-247): f64 accumulation in
-// (dx, dy, dz) corner order, weight ((wx*wy)*wz), result rounded to f32.
-__device__ void trilinear_dense(const float* __restrict__ grid, int side, int d_f,
-                                const double* p, float* out) {
-  int64_t i0[3];
-  double fr[3];
-  tri_prepare(p, side, i0, fr);
-  double acc[kMaxDf];
-  for (int c = 0; c < d_f; ++c) acc[c] = 0.0;
-  for (int dx = 0; dx < 2; ++dx) {
-    const double wx = dx ? fr[0] : 1.0 - fr[0];
-    for (int dy = 0; dy < 2; ++dy) {
-      const double wy = dy ? fr[1] : 1.0 - fr[1];
-      for (int dz = 0; dz < 2; ++dz) {
-        const double wz = dz ? fr[2] : 1.0 - fr[2];
-        const double w = dmul(dmul(wx, wy), wz);
-        const float* cr =
-            grid + (((i0[0] + dx) * side + (i0[1] + dy)) * side + (i0[2] + dz)) * d_f;
-        for (int c = 0; c < d_f; ++c) acc[c] = dadd(acc[c], dmul(w, (double)cr[c]));
-      }
-    }
-  }
-  for (int c = 0; c < d_f; ++c) out[c] = (float)acc[c];
-}
-
-// f32(act(f32(x W + b))) for one row, f64 accumulation (tensor_core.py:100-136)
-__device__ void affine_act(const float* x, int din, const float* __restrict__ w,
-                           const float* __restrict__ b, int dout, int act, float* y) {
-  for (int o = 0; o < dout; ++o) {
-    double s = 0.0;
-    for (int i = 0; i < din; ++i) s = dadd(s, dmul((double)x[i], (double)w[i * dout + o]));
-    if (b) s = dadd(s, (double)b[o]);
-    float v = (float)s;
-    const double z = (double)v;
-    if (act == 1)
-      v = (float)dmul(dmul(0.5, z), dadd(1.0, erf(z / 1.4142135623730951)));
-    else if (act == 2)
-      v = (float)(z >= 0.0 ? 1.0 / (1.0 + exp(-z)) : exp(z) / (1.0 + exp(z)));
-    y[o] = v;
   }
 }
 
@@ -160,15 +107,41 @@ __global__ void decode_points_kernel(const float* __restrict__ grid, int s_df,
     for (int c = 0; c < d_f; ++c) f_out[i * d_f + c] = f[c];
   if (!H.zw1) return;   // field query only
   float h[kMaxHidden], o[kMaxHidden];
-  affine_act(f, d_f, H.zw1, H.zb1, H.hidden, 1, h);
-  affine_act(h, H.hidden, H.zw2, H.zb2, H.zc, 2, o);
+  affine_act_row(f, d_f, H.zw1, H.zb1, H.hidden, 1, h);
+  affine_act_row(h, H.hidden, H.zw2, H.zb2, H.zc, 2, o);
   for (int c = 0; c < H.zc; ++c) z_out[i * H.zc + c] = o[c];
-  affine_act(f, d_f, H.sw1, H.sb1, H.hidden, 1, h);
-  affine_act(h, H.hidden, H.sw2, H.sb2, 1, 0, o);
+  affine_act_row(f, d_f, H.sw1, H.sb1, H.hidden, 1, h);
+  affine_act_row(h, H.hidden, H.sw2, H.sb2, 1, 0, o);
   // + bounding-sphere offset |p - c| - r (camera_geometry.py:219-221)
-  const double dx = p[0] - 0.5, dy = p[1] - 0.5, dz = p[2] - 0.5;
-  const double nrm = sqrt(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
-  s_out[i] = (float)dadd((double)o[0], nrm - 0.45);
+  s_out[i] = s_with_bias(o[0], p, 0.45);
+}
+
+// y = f32(act(f32(x W + b))): tensor_core.affine (+ activation) in f64 with
+// np.einsum's reduction order (field.cuh), one thread per output element;
+// consecutive threads take consecutive output columns (coalesced W reads,
+// broadcast x reads).
+__global__ void affine_exact_kernel(const float* __restrict__ x, int64_t ldx, int64_t n, int din,
+                                    const float* __restrict__ w, const float* __restrict__ b,
+                                    int dout, int act, float* __restrict__ y, int64_t ldy) {
+  const int64_t total = n * dout;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / dout;
+    const int o = (int)(e % dout);
+    const float* xr = x + r * ldx;
+    double s;
+    if (dout == 1) {
+      s = einsum_dot(xr, w, 1, din);
+    } else {
+      s = 0.0;
+      for (int i = 0; i < din; ++i) s = dadd(s, dmul((double)xr[i], (double)w[(int64_t)i * dout + o]));
+    }
+    if (b) s = dadd(s, (double)b[o]);
+    float v = (float)s;
+    if (act == 1) v = gelu_ref(v);
+    else if (act == 2) v = sigmoid_ref_f(v);
+    y[r * ldy + o] = v;
+  }
 }
 
 }  // namespace lsrm
@@ -176,6 +149,20 @@ __global__ void decode_points_kernel(const float* __restrict__ grid, int s_df,
 using namespace lsrm;
 
 extern "C" {
+
+int lsrm_affine_exact(const float* x, int64_t ldx, int64_t n, int din, const float* w,
+                      const float* bias, int dout, int act, float* y, int64_t ldy,
+                      void* stream) {
+  LSRM_REQUIRE(din >= 1 && dout >= 1, "affine: bad widths %d x %d", din, dout);
+  LSRM_REQUIRE(act >= 0 && act <= 2, "affine: activation %d not in {0 identity, 1 gelu, "
+               "2 sigmoid}", act);
+  if (n == 0) return LSRM_OK;
+  const int64_t total = n * dout;
+  const unsigned g = (unsigned)(ceil_div(total, 256) < 148 * 64 ? ceil_div(total, 256) : 148 * 64);
+  affine_exact_kernel<<<g, 256, 0, as_stream(stream)>>>(x, ldx, n, din, w, bias, dout, act, y, ldy);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
 
 int lsrm_decode_scatter(const float* vec, int side, int t, int d_f, float* grid, void* stream) {
   LSRM_REQUIRE(side >= 1 && t >= 1 && d_f >= 1, "decode_scatter: bad sizes");

@@ -3,7 +3,7 @@
 // compares on correctly rounded SDF values; compaction keeps flat (argwhere)
 // order via a two-level scan; features reproduce the reference's two f64
 // roundings f32(f64(parent) + f64(f32(sum of pos-embed rows in f64))).
-#include "common.cuh"
+#include "field.cuh"
 
 namespace lsrm {
 
@@ -53,28 +53,6 @@ __global__ void fg_mask8_kernel(const float4* __restrict__ alpha, int n_views, i
   }
 }
 
-__device__ __forceinline__ double sdf_union(const double* __restrict__ prims, int n,
-                                            double x, double y, double z) {
-  double s = 0.0;
-  for (int p = 0; p < n; ++p) {
-    const double* P = prims + 8 * p;
-    double v;
-    if (P[0] == 0.0) {  // sphere: |p - c| - r
-      v = dsub(__dsqrt_rn(dist2(x, y, z, P[1], P[2], P[3])), P[4]);
-    } else {            // box: |max(q,0)| + min(max(q), 0), q = |p - c| - h
-      double qx = dsub(fabs(dsub(x, P[1])), P[4]);
-      double qy = dsub(fabs(dsub(y, P[2])), P[5]);
-      double qz = dsub(fabs(dsub(z, P[3])), P[6]);
-      double ox = fmax(qx, 0.0), oy = fmax(qy, 0.0), oz = fmax(qz, 0.0);
-      double out = __dsqrt_rn(dadd(dadd(dmul(ox, ox), dmul(oy, oy)), dmul(oz, oz)));
-      double in = fmin(fmax(fmax(qx, qy), qz), 0.0);
-      v = dadd(out, in);
-    }
-    s = p == 0 ? v : fmin(s, v);
-  }
-  return s;
-}
-
 __global__ void voxel_mask_kernel(const double* __restrict__ prims, int n_prims, int s_vol,
                                   double tau, int t, uint8_t* __restrict__ mask) {
   extern __shared__ double sh_prims[];
@@ -94,7 +72,7 @@ __global__ void voxel_mask_kernel(const double* __restrict__ prims, int n_prims,
         double y = ddiv(dadd((double)(t * j + b), 0.5), fine);
         for (int c = 0; c < t; ++c) {
           double z = ddiv(dadd((double)(t * k + c), 0.5), fine);
-          double s = sdf_union(sh_prims, n_prims, x, y, z);
+          double s = sdf_prims(sh_prims, n_prims, x, y, z);
           smin = fmin(smin, s);
           smax = fmax(smax, s);
           amin = fmin(amin, fabs(s));
@@ -102,6 +80,66 @@ __global__ void voxel_mask_kernel(const double* __restrict__ prims, int n_prims,
       }
     }
     mask[vox] = (amin <= tau) || (dmul(smin, smax) <= 0.0);
+  }
+}
+
+// Eq. 11 for a general field (decoded coarse volume, or values of an opaque
+// callable), one warp per voxel: the lanes evaluate the t^3 samples, exact
+// f64 min / max / min|s| by shuffles.  Voxels of x-slabs [i0, i1).  For the
+// values kind, sample ids follow the reference's slab layout
+// (tokenizer.py:227-235): ((i - i0) * t + a) * fine^2 + (t j + b) * fine + t k + c.
+__global__ void voxel_mask_field_kernel(FieldDev F, int s_vol, double tau, int t, int i0,
+                                        int i1, uint8_t* __restrict__ mask) {
+  const int lane = threadIdx.x & 31;
+  const int64_t plane = (int64_t)s_vol * s_vol;
+  const int64_t total = (int64_t)(i1 - i0) * plane;
+  const int fine = t * s_vol;
+  const double finef = (double)fine;
+  const int t3 = t * t * t;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < total;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int i = i0 + (int)(v / plane), j = (int)((v / s_vol) % s_vol), k = (int)(v % s_vol);
+    double smin = __builtin_huge_val(), smax = -__builtin_huge_val(),
+           amin = __builtin_huge_val();
+    for (int e = lane; e < t3; e += 32) {
+      const int a = e / (t * t), b = (e / t) % t, c = e % t;
+      const int xa = t * i + a, yb = t * j + b, zc = t * k + c;
+      const double x = ddiv(dadd((double)xa, 0.5), finef);
+      const double y = ddiv(dadd((double)yb, 0.5), finef);
+      const double z = ddiv(dadd((double)zc, 0.5), finef);
+      const int64_t id = ((int64_t)(i - i0) * t + a) * fine * (int64_t)fine +
+                         (int64_t)yb * fine + zc;
+      const double s = field_sdf(F, id, x, y, z);
+      smin = fmin(smin, s);
+      smax = fmax(smax, s);
+      amin = fmin(amin, fabs(s));
+    }
+    for (int o = 16; o; o >>= 1) {
+      smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+      smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+      amin = fmin(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+    }
+    if (lane == 0) mask[(int64_t)i * plane + (int64_t)j * s_vol + k] =
+        (amin <= tau) || (dmul(smin, smax) <= 0.0);
+  }
+}
+
+// sample points of x-slabs [i0, i1) in the reference's layout (for an opaque
+// field evaluated on the host): pts [(i1-i0) * t * fine^2, 3]
+__global__ void voxel_samples_kernel(int s_vol, int t, int i0, int i1,
+                                     double* __restrict__ pts) {
+  const int fine = t * s_vol;
+  const int64_t per_slab = (int64_t)t * fine * fine;
+  const int64_t total = (int64_t)(i1 - i0) * per_slab;
+  const double finef = (double)fine;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int sl = (int)(e / per_slab);
+    const int a = (int)((e / ((int64_t)fine * fine)) % t);
+    const int yb = (int)((e / fine) % fine), zc = (int)(e % fine);
+    pts[3 * e] = ddiv(dadd((double)(t * (i0 + sl) + a), 0.5), finef);
+    pts[3 * e + 1] = ddiv(dadd((double)yb, 0.5), finef);
+    pts[3 * e + 2] = ddiv(dadd((double)zc, 0.5), finef);
   }
 }
 
@@ -284,6 +322,52 @@ int lsrm_voxel_mask(const double* sdf, int n_prims, int s_vol, double tau, int t
   int blocks = (int)std::min<int64_t>(ceil_div(total, 128), 148 * 32);
   voxel_mask_kernel<<<blocks, 128, 8 * n_prims * sizeof(double), as_stream(stream)>>>(
       sdf, n_prims, s_vol, tau, t_side, mask);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_voxel_mask_field(const lsrm_sdf_field* field, int s_vol, double tau, int t_side,
+                          int i0, int i1, uint8_t* mask, void* stream) {
+  LSRM_REQUIRE(s_vol >= 1 && t_side >= 1, "bad mask resolution");
+  LSRM_REQUIRE(tau > 0, "tau must be positive");
+  LSRM_REQUIRE(0 <= i0 && i0 <= i1 && i1 <= s_vol, "voxel mask: slab range [%d, %d) out of "
+               "[0, %d)", i0, i1, s_vol);
+  int rc = lsrm_check_field(field);
+  if (rc) return rc;
+  if (i0 == i1) return LSRM_OK;
+  if (field->kind == kFieldAnalytic && i0 == 0 && i1 == s_vol)
+    return lsrm_voxel_mask(field->prims, field->n_prims, s_vol, tau, t_side, mask, stream);
+  FieldDev F{};
+  F.kind = field->kind;
+  F.prims = field->prims;
+  F.n_prims = field->n_prims;
+  F.grid = field->grid;
+  F.side = field->side;
+  F.d_f = field->d_f;
+  F.hidden = field->hidden;
+  F.w1 = field->w1;
+  F.b1 = field->b1;
+  F.w2 = field->w2;
+  F.b2 = field->b2;
+  F.radius = field->radius;
+  F.values = field->values;
+  const int64_t voxels = (int64_t)(i1 - i0) * s_vol * s_vol;
+  const int blocks = (int)std::min<int64_t>(ceil_div(voxels, 4), 148 * 64);
+  voxel_mask_field_kernel<<<blocks, 128, 0, as_stream(stream)>>>(F, s_vol, tau, t_side, i0, i1,
+                                                                 mask);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_voxel_sample_points(int s_vol, int t_side, int i0, int i1, double* points,
+                             void* stream) {
+  LSRM_REQUIRE(s_vol >= 1 && t_side >= 1, "bad mask resolution");
+  LSRM_REQUIRE(0 <= i0 && i0 <= i1 && i1 <= s_vol, "voxel samples: bad slab range");
+  const int64_t fine = (int64_t)t_side * s_vol;
+  const int64_t total = (int64_t)(i1 - i0) * t_side * fine * fine;
+  if (total == 0) return LSRM_OK;
+  const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 32);
+  voxel_samples_kernel<<<blocks, 256, 0, as_stream(stream)>>>(s_vol, t_side, i0, i1, points);
   LSRM_LAUNCHED();
   return LSRM_OK;
 }

@@ -308,7 +308,8 @@ def nsa_gates(x, w: NsaWeights):
     n, d = xd.shape
     logits = _ops.gemm(xd, D.weight(w.gate_w))
     g = D.empty((n, w.n_gates * d), torch.float32)
-    call("lsrm_sigmoid_f32", logits.data_ptr(), logits.stride(0), D.weight(w.gate_b).data_ptr(),
+    gb = D.weight(w.gate_b)
+    call("lsrm_sigmoid_f32", logits.data_ptr(), logits.stride(0), gb.data_ptr(),
          n, w.n_gates * d, g.data_ptr(), D.stream())
     g = g if on_dev else D.host(g)
     return tuple(g[:, i * d:(i + 1) * d] for i in range(w.n_gates))
@@ -319,7 +320,8 @@ def _combine_dev(xd, outs, w: NsaWeights):
     logits = _ops.gemm(xd, D.weight(w.gate_w))
     merged = D.empty((n, d), torch.float32)
     o = [t.reshape(n, d) for t in outs] + [None] * (3 - len(outs))
-    call("lsrm_gated_merge_f32", logits.data_ptr(), logits.stride(0), D.weight(w.gate_b).data_ptr(),
+    gb = D.weight(w.gate_b)
+    call("lsrm_gated_merge_f32", logits.data_ptr(), logits.stride(0), gb.data_ptr(),
          w.n_gates, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]), n, d, merged.data_ptr(),
          D.stream())
     return _ops.gemm(merged, D.weight(w.w_o))

@@ -142,9 +142,10 @@ def _add_ln(a, b, norm: NormParams, out_dtype=torch.float32, exact=True):
     n, d = a.shape
     s = D.empty((n, d), torch.float32)
     y = D.empty((n, d), out_dtype)
+    gamma, beta = D.weight(norm.gamma), D.weight(norm.beta)   # alive across the launch
     call("lsrm_add_layer_norm", int(exact), a.data_ptr(), D.ptr(b), int(b is not None and
                                                            b.dtype == torch.bfloat16),
-         n, d, D.weight(norm.gamma).data_ptr(), D.weight(norm.beta).data_ptr(), LN_EPS, s.data_ptr(),
+         n, d, gamma.data_ptr(), beta.data_ptr(), LN_EPS, s.data_ptr(),
          int(out_dtype == torch.bfloat16), y.data_ptr(), D.stream())
     return s, y
 
@@ -156,10 +157,11 @@ def _gate_mix_ln(exact, xe, logits, ld, gate_b, o_self, o_cross, norm: NormParam
     n, d = xe.shape
     x1 = D.empty((n, d), torch.float32)
     h = D.empty((n, d), out_dtype)
+    gamma, beta = D.weight(norm.gamma), D.weight(norm.beta)   # alive across the launch
     call("lsrm_gate_mix_layer_norm", int(exact), xe.data_ptr(), logits.data_ptr(), ld,
          int(logits.dtype == torch.bfloat16), gate_b.data_ptr(), o_self.data_ptr(),
          o_cross.data_ptr(), int(o_self.dtype == torch.bfloat16), n, d, x1.data_ptr(),
-         D.weight(norm.gamma).data_ptr(), D.weight(norm.beta).data_ptr(), LN_EPS,
+         gamma.data_ptr(), beta.data_ptr(), LN_EPS,
          int(out_dtype == torch.bfloat16), h.data_ptr(), D.stream())
     return x1, h
 
@@ -452,9 +454,27 @@ def init_decoder_heads(seed: int, d_f: int = FEATURE_DIM, z_channels: int = 3,
 
 
 def _affine_dec(x, w: DecodeWeights):
-    """f32(x W + b), fp32 GEMM + bias (the reference: f64 accumulation)."""
-    v = _ops.gemm(x, D.weight(w.weight))
-    return _bias_act(1, v, D.weight(w.bias), 0)
+    """f32(x W + b) with the reference's f64 einsum accumulation
+    (`tensor_core.py:100-116`; csrc/decode.cu `lsrm_affine_exact`), so the
+    decoded grid -- which the decoded-geometry voxel mask thresholds -- is
+    the reference's bit for bit."""
+    return affine_exact(x, w.weight, w.bias)
+
+
+def affine_exact(x, weight, bias=None, act: int = 0):
+    """`tensor_core.affine` (+ activation 0 identity / 1 gelu / 2 sigmoid):
+    f32 storage, f64 accumulation in np.einsum's order, on the GPU."""
+    xd = D.dev(x, torch.float32)
+    n, din = int(xd.shape[0]), int(xd.shape[1])
+    wd = D.weight(weight)
+    require(int(wd.shape[0]) == din, f"affine dim mismatch: x has {din}, weight expects "
+            f"{int(wd.shape[0])}")
+    dout = int(wd.shape[1])
+    bd = D.weight(bias) if bias is not None else None
+    y = D.empty((n, dout), torch.float32)
+    call("lsrm_affine_exact", xd.data_ptr(), xd.stride(0), n, din, wd.data_ptr(), D.ptr(bd),
+         dout, act, y.data_ptr(), y.stride(0), D.stream())
+    return y
 
 
 def decode_feature_volume(x_d, w: DecodeWeights, d_f: int = FEATURE_DIM):

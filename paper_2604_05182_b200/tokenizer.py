@@ -14,6 +14,8 @@ import torch
 
 from . import _dev as D
 from ._native import call, lib
+from .sdf import DeviceField, sdf_primitives  # noqa: F401 (re-export)
+from .sdf import ptr as sdf_ptr
 from .errors import ConfigurationError, require
 
 PATCH = 8
@@ -100,43 +102,36 @@ def foreground_patch_mask(alpha, patch: int = PATCH):
     return _ret(m, on_dev)
 
 
-def sdf_primitives(field) -> np.ndarray:
-    """Flatten an SDF union tree into [n,8] rows (kind, center, radius |
-    half sizes).  Accepts the reference SdfField objects or scene-json dicts;
-    union is min, which is associative, so flattening is exact."""
-    rows = []
-
-    def visit(node):
-        get = (lambda k: node.get(k)) if isinstance(node, dict) else (lambda k: getattr(node, k))
-        kind = get("kind")
-        if kind == "union":
-            for p in get("parts"):
-                visit(p)
-        elif kind == "sphere":
-            c = np.asarray(get("center"), np.float64)
-            rows.append([0.0, c[0], c[1], c[2], float(get("radius")), 0.0, 0.0, 0.0])
-        elif kind == "box":
-            c = np.asarray(get("center"), np.float64)
-            h = np.asarray(get("half_sizes"), np.float64)
-            rows.append([1.0, c[0], c[1], c[2], h[0], h[1], h[2], 0.0])
-        else:
-            raise ConfigurationError(f"voxel mask: unsupported SDF kind {kind!r}")
-    visit(field)
-    return np.asarray(rows, np.float64)
-
-
 def informative_voxel_mask(field, s_vol: int, tau: float = None, t_side: int = 4,
                            as_device: bool = False):
     """[S,S,S] bool, Eq. 11 over t_side^3 cell-center samples per voxel
-    (`tokenizer.py:211-239`)."""
+    (`tokenizer.py:211-239`).  `field`: the analytic scene (reference
+    SdfField or scene-json dict), the decoded coarse volume
+    (`sdf.decoded_sdf_field`, evaluated in-kernel), or any callable field
+    (`callable_field(fn)`: fn is called on the GPU-generated sample points of
+    each x-slab batch, in the reference's layout; the reduction runs on the
+    GPU)."""
     require(s_vol >= 1 and t_side >= 1, "bad mask resolution")
     if tau is None:
         tau = 1.0 / s_vol
     require(tau > 0, "tau must be positive")
-    prims = D.dev(sdf_primitives(field))
-    m = D.empty((s_vol, s_vol, s_vol), torch.uint8)
-    call("lsrm_voxel_mask", prims.data_ptr(), prims.shape[0], s_vol, float(tau), t_side,
-         m.data_ptr(), D.stream())
+    f = DeviceField(field)
+    m = D.zeros((s_vol, s_vol, s_vol), torch.uint8)
+    st = D.stream()
+    if not f.opaque:
+        call("lsrm_voxel_mask_field", sdf_ptr(f.desc), s_vol, float(tau), t_side, 0, s_vol,
+             m.data_ptr(), st)
+        return _ret(m.bool(), as_device)
+    fine = t_side * s_vol
+    per_slab = t_side * fine * fine
+    step = max(1, (1 << 22) // per_slab)
+    for i0 in range(0, s_vol, step):
+        i1 = min(s_vol, i0 + step)
+        pts = D.empty(((i1 - i0) * per_slab, 3), torch.float64)
+        call("lsrm_voxel_sample_points", s_vol, t_side, i0, i1, pts.data_ptr(), st)
+        vals = f.eval_host(pts)
+        call("lsrm_voxel_mask_field", sdf_ptr(f.values_desc(vals)), s_vol, float(tau), t_side,
+             i0, i1, m.data_ptr(), st)
     return _ret(m.bool(), as_device)
 
 

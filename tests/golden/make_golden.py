@@ -227,8 +227,55 @@ def ref_goldenrun():
                 os.path.join(HERE, "ref_goldenrun_messages.csv"))
 
 
+def ref_decoded():
+    """The reference's coarse-to-fine path with geometry_source="decoded"
+    (`runner.py:301-335`) at the golden-run config: the decoded coarse SDF
+    drives the informative-voxel mask and the image-token surface points."""
+    import dataclasses
+    import json
+    gdir = "/root/reference/pkg/tests/goldens"
+    cfg = lsrm.config_from_json(json.load(open(os.path.join(gdir, "config.json"))))
+    cfg = dataclasses.replace(cfg, geometry_source="decoded")
+    cams, f = lsrm.scene_from_json(json.load(open(os.path.join(gdir, "scene.json"))))
+    res = lsrm.run_pipeline(cfg, cams, f)
+    w = res["weights"]
+    fv_coarse = lsrm.FeatureVolume(res["dense_grid"])
+    from lsrm.camera_geometry import callable_field
+    geo = callable_field(
+        lambda pts: lsrm.decode_points(fv_coarse, w.heads, pts)[1].astype(np.float64))
+    ic = lsrm.image_token_coords(res["y_up"], res["fine_cams"], geo, LAPLACE_BETA)
+    (sw1, sb1, _), (sw2, sb2, _) = w.heads.s_layers
+    plan = res["plan"]
+    out = dict(
+        seed=cfg.seed, d=cfg.d, heads=np.array([cfg.n_q_heads, cfg.n_kv_heads]),
+        s_vol_fine=cfg.s_vol_fine, s_img_fine=cfg.s_img_fine,
+        factor_vol=cfg.factor_vol, factor_img=cfg.factor_img, workers=cfg.workers,
+        depth_sparse=cfg.depth_sparse,
+        budgets=np.array([cfg.budgets.b_i, cfg.budgets.b_v2v, cfg.budgets.b_v2i,
+                          cfg.budgets.b_i2v, cfg.budgets.b_i2i]),
+        x_d=res["x_d"], y_d=res["y_d"], dense_grid=res["dense_grid"],
+        s_w1=sw1, s_b1=sb1, s_w2=sw2, s_b2=sb2,
+        vol_mask=res["vol_mask"], img_mask=res["img_mask"],
+        cam_K=np.stack([c.intrinsics for c in res["fine_cams"]]),
+        cam_R=np.stack([c.rotation for c in res["fine_cams"]]),
+        cam_t=np.stack([c.translation for c in res["fine_cams"]]),
+        cam_wh=np.array([c.image_size for c in res["fine_cams"]]),
+        x_coords=res["x_up"].coords, y_coords=res["y_up"].coords,
+        img_points=ic.points, img_miss=ic.miss,
+        x_s=res["x_s"], y_s=res["y_s"],
+        probe=res["probe"], probe_z=res["probe_z"], probe_s=res["probe_s"])
+    for name, selx in plan.tables.items():
+        out[f"plan_{name}"], out[f"plan_{name}_len"] = flat(selx.lists)
+    np.savez_compressed(os.path.join(HERE, "ref_decoded.npz"), **out)
+    lsrm.message_log_to_csv(res["topology"].message_log,
+                            os.path.join(HERE, "ref_decoded_messages.csv"))
+    print("decoded", int(res["vol_mask"].sum()), res["x_up"].count, res["y_up"].count)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["work", "small", "goldenrun"]
+    which = sys.argv[1:] or ["work", "small", "goldenrun", "decoded"]
+    if "decoded" in which:
+        ref_decoded()
     if "small" in which:
         ref_small()
     if "goldenrun" in which:
