@@ -274,6 +274,33 @@ int lsrm_gemm_bias_res_f32(int64_t m, int64_t n, int64_t k, const void* a, int64
                            const void* b, int64_t ldb, const float* bias, const float* res,
                            int64_t ldr, float* d, int64_t ldd, void* stream);
 
+/* ---- grouped bf16 GEMM on tcgen05 (hand-written; TMA + TMEM) ----------
+ * Replaces the library GEMMs of the layer's hot path: the per-stream fused
+ * projection (q/k/v `affine` + gate GEMM, nsa_attention.py:266-273,303-307
+ * over tensor_core.py:100-116), W_o (nsa_attention.py:284) and the Stage-2
+ * FFN (recon_pipeline.py:497-512).  For every problem:
+ *   C[m,n] = act(A[m,k] . Bt[n,k]^T + bias[n]) + res[m,n]
+ * A bf16 [m,k] and Bt bf16 [n,k] (the weight stored TRANSPOSED) both with K
+ * contiguous; fp32 accumulation in TMEM; bias/res/C dtypes per flags.
+ * k, n and every row stride must be multiples of 8 elements and pointers
+ * 16-byte aligned.  One persistent launch runs all problems (<= 8). */
+#define LSRM_GEMM_OUT_F32  1   /* C is f32 (else bf16) */
+#define LSRM_GEMM_BIAS_F32 2   /* bias is f32 (else bf16) */
+#define LSRM_GEMM_RES_F32  4   /* res is f32 (else bf16) */
+#define LSRM_GEMM_GELU     8   /* act = exact-erf gelu, applied before res */
+typedef struct lsrm_gemm_problem {
+  int64_t m, n, k;
+  const void* a;  int64_t lda;
+  const void* bt; int64_t ldb;
+  void* c;        int64_t ldc;
+  const void* bias;             /* [n] or NULL */
+  const void* res; int64_t ldr; /* [m,n] or NULL; may alias c */
+  int32_t flags;
+  int32_t reserved;
+} lsrm_gemm_problem;
+/* problems: HOST array of n_problems descriptors. */
+int lsrm_gemm_tc(const lsrm_gemm_problem* problems, int n_problems, void* stream);
+
 /* ---- fused bf16 three-branch NSA attention, tcgen05/TMEM  -------------
  * (nsa_attention.py:84-112,157-207,266-284 fused)
  * q: [nq, hq, dh] bf16 in query BLOCK-MAJOR order; kv_il: K and V in the

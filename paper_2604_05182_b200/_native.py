@@ -94,6 +94,7 @@ SIGNATURES = {
     "lsrm_voxel_mask_field": (I32, [P, I32, F64, I32, I32, I32, P, P]),
     "lsrm_voxel_sample_points": (I32, [I32, I32, I32, I32, P, P]),
     "lsrm_affine_exact": (I32, [P, I64, I64, I32, P, P, I32, I32, P, I64, P]),
+    "lsrm_gemm_tc": (I32, [P, I32, P]),
 }
 
 _lib = None

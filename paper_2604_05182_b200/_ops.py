@@ -1,5 +1,7 @@
 """Thin device-op wrappers over the C ABI used by the host modules."""
 
+import ctypes as C
+
 import torch
 
 from . import _dev as D
@@ -76,4 +78,52 @@ def gemm_ex(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, out=
     call("lsrm_gemm_f32_ex", int(trans_a), int(trans_b), m, n, k, float(alpha), a.data_ptr(),
          a.stride(0), b.data_ptr(), b.stride(0), float(beta), out.data_ptr(), out.stride(0),
          int(tf32), D.stream())
+    return out
+
+
+class GemmProblem(C.Structure):
+    """Mirror of `lsrm_gemm_problem` (include/lsrm_b200.h)."""
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
+                ("a", C.c_void_p), ("lda", C.c_int64), ("bt", C.c_void_p), ("ldb", C.c_int64),
+                ("c", C.c_void_p), ("ldc", C.c_int64), ("bias", C.c_void_p),
+                ("res", C.c_void_p), ("ldr", C.c_int64), ("flags", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+GEMM_OUT_F32, GEMM_BIAS_F32, GEMM_RES_F32, GEMM_GELU = 1, 2, 4, 8
+
+
+def gemm_problem(a: torch.Tensor, bt: torch.Tensor, out: torch.Tensor, bias=None, res=None,
+                 gelu=False) -> GemmProblem:
+    """One tcgen05 GEMM problem: out = act(a @ bt^T + bias) + res, with a
+    [m,k] and bt [n,k] bf16 (K contiguous: bt is the weight transposed)."""
+    m, k = a.shape
+    n, k2 = bt.shape
+    assert k == k2 and a.dtype == bt.dtype == torch.bfloat16
+    assert a.stride(1) == 1 and bt.stride(1) == 1 and out.stride(1) == 1
+    assert tuple(out.shape) == (m, n)
+    flags = (GEMM_OUT_F32 if out.dtype == torch.float32 else 0) | (GEMM_GELU if gelu else 0)
+    if bias is not None:
+        flags |= GEMM_BIAS_F32 if bias.dtype == torch.float32 else 0
+    if res is not None:
+        assert res.stride(1) == 1 and tuple(res.shape) == (m, n)
+        flags |= GEMM_RES_F32 if res.dtype == torch.float32 else 0
+    prob = GemmProblem(m, n, k, a.data_ptr(), a.stride(0), bt.data_ptr(), bt.stride(0),
+                       out.data_ptr(), out.stride(0), D.ptr(bias), D.ptr(res),
+                       res.stride(0) if res is not None else 0, flags, 0)
+    prob.keep = (a, bt, out, bias, res)   # the descriptor holds raw pointers
+    return prob
+
+
+def gemm_tc(problems) -> None:
+    """Run GemmProblems as ONE persistent tcgen05 launch (csrc/gemm_tc.cu)."""
+    arr = (GemmProblem * len(problems))(*problems)
+    call("lsrm_gemm_tc", C.cast(arr, C.c_void_p), len(problems), D.stream())
+
+
+def gemm_bf16(a: torch.Tensor, bt: torch.Tensor, out=None, out_dtype=torch.bfloat16, bias=None,
+              res=None, gelu=False) -> torch.Tensor:
+    """a [m,k] @ bt[n,k]^T on the tcgen05 GEMM."""
+    out = D.empty((a.shape[0], bt.shape[0]), out_dtype) if out is None else out
+    gemm_tc([gemm_problem(a, bt, out, bias, res, gelu)])
     return out
