@@ -8,13 +8,13 @@ block-major order of each modality's own partition, so that
   * query tiles never straddle blocks (window branch + W-invariance),
   * the routed selections are expressed as occupied-row indices.
 
-Per layer and stream, ONE bf16 GEMM (cuBLAS) computes all projections that
-read that stream: the q and gate columns of its two query uses and the k/v
-columns of the two uses that read it as KV.  Then ONE launch prepares the K/V
+Per layer, ONE grouped tcgen05 GEMM launch (csrc/gemm_tc.cu) computes, for
+each stream, all projections that read it: the q and gate columns of its two
+query uses and the k/v columns of the two uses that read it as KV.  Then ONE launch prepares the K/V
 of all four uses (interleaved layout + tensor-core ResBlock + block mean,
 written straight into the compressed layout; csrc/kv_prep.cu), and per use
 the fused tcgen05 three-branch attention with the gated merge
-(csrc/attn_tc.cu) and the W_o GEMM.
+(csrc/attn_tc.cu) and the four W_o GEMMs (one grouped launch).
 
 Sharding (block-aware sequence parallelism, seq_parallel.py): an engine can
 own only a subset of each stream's blocks.  Its query side then works on the
@@ -250,9 +250,11 @@ class SparseLayerEngine:
             bcat[s_].append(np.zeros(int(wx.shape[1]), np.float32))
             ncol[s_] += int(wx.shape[1])
         self.ncol = ncol
-        self.w_cat = {s: D.dev(np.concatenate(wcat[s], axis=1), torch.bfloat16) for s in wcat}
+        # weights stored transposed ([n, k], K contiguous): both tcgen05 GEMM
+        # operands K-major (csrc/gemm_tc.cu)
+        self.w_cat = {s: D.dev(np.concatenate(wcat[s], axis=1).T, torch.bfloat16) for s in wcat}
         self.b_cat = {s: D.dev(np.concatenate(bcat[s]), torch.bfloat16) for s in bcat}
-        self.w_o = {u: D.dev(weights[u].w_o, torch.bfloat16) for u in USES}
+        self.w_o = {u: D.dev(np.asarray(weights[u].w_o).T, torch.bfloat16) for u in USES}
         self.gate_b = {u: D.dev(weights[u].gate_b, torch.float32) for u in USES}
         self.cmp_w = {u: (_dev_res(weights[u].compress.for_k), _dev_res(weights[u].compress.for_v))
                       for u in USES}
@@ -494,13 +496,12 @@ class SparseLayerEngine:
 
     # -- pieces --------------------------------------------------------------
     def project(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
-        for s, a in (("x", x_loc), ("y", y_loc)):
-            if self.meta[s].n_loc:
-                Y, Wc = self.buf[("Y", s)], self.w_cat[s]
-                m, k = a.shape
-                call("lsrm_gemm_bias_bf16", m, int(Wc.shape[1]), k, a.data_ptr(), a.stride(0),
-                     Wc.data_ptr(), Wc.stride(0), self.b_cat[s].data_ptr(), Y.data_ptr(),
-                     Y.stride(0), D.stream())
+        """Both streams' fused projections (q | gate logits + bias | k | v)
+        as ONE grouped tcgen05 GEMM launch."""
+        probs = [_ops.gemm_problem(a, self.w_cat[s], self.buf[("Y", s)], bias=self.b_cat[s])
+                 for s, a in (("x", x_loc), ("y", y_loc)) if self.meta[s].n_loc]
+        if probs:
+            _ops.gemm_tc(probs)
 
     def prepare_kv(self):
         """K/V of all four uses in one launch (owned KV blocks when sharded;
@@ -541,7 +542,15 @@ class SparseLayerEngine:
 
     def output(self, use: str):
         if self.buf[("merged", use)].shape[0]:
-            _ops.gemm(self.buf[("merged", use)], self.w_o[use], out=self.buf[("out", use)])
+            _ops.gemm_tc([_ops.gemm_problem(self.buf[("merged", use)], self.w_o[use],
+                                            self.buf[("out", use)])])
+
+    def output_all(self):
+        """The four uses' W_o projections as ONE grouped tcgen05 GEMM launch."""
+        probs = [_ops.gemm_problem(self.buf[("merged", u)], self.w_o[u], self.buf[("out", u)])
+                 for u in USES if self.buf[("merged", u)].shape[0]]
+        if probs:
+            _ops.gemm_tc(probs)
 
     # -- whole layer ---------------------------------------------------------
     def forward(self, x_loc: torch.Tensor, y_loc: torch.Tensor) -> dict:
@@ -554,8 +563,7 @@ class SparseLayerEngine:
         self.project(x_loc, y_loc)
         self.prepare_kv()
         self.attend_all()
-        for use in USES:
-            self.output(use)
+        self.output_all()
         return {u: self.buf[("out", u)] for u in USES}
 
     def forward_local(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
@@ -572,8 +580,7 @@ class SparseLayerEngine:
             handles[use]()          # wait + place into the canonical layout
             self.finish_kv(use)
         self.attend_all()
-        for use in USES:
-            self.output(use)
+        self.output_all()
         return {u: self.buf[("out", u)] for u in USES}
 
     def capture(self, x_bm: torch.Tensor, y_bm: torch.Tensor):

@@ -253,7 +253,8 @@ class SparseBlockEngine:
         self.w, self.params = w, params
         self.layer = SparseLayerEngine(part_vol, part_img, plan_rows, w.uses(), params,
                                        extra_cols={"x": w.gate_x_w, "y": w.gate_y_w}, pool=pool)
-        self.bf = {name: D.weight(getattr(getattr(w, f), n), torch.bfloat16)
+        # FFN weights transposed ([n, k], K contiguous) for the tcgen05 GEMM
+        self.bf = {name: D.dev(np.asarray(getattr(getattr(w, f), n)).T, torch.bfloat16)
                    for name, f, n in (("fx1", "ffn_x", "w1"), ("fx2", "ffn_x", "w2"),
                                       ("fy1", "ffn_y", "w1"), ("fy2", "ffn_y", "w2"))}
 
@@ -262,23 +263,31 @@ class SparseBlockEngine:
         xe, xh = _add_ln(x, x_inj, w.ln_attn_x, torch.bfloat16, exact=False)
         ye, yh = _add_ln(y, y_inj, w.ln_attn_y, torch.bfloat16, exact=False)
         outs = L.forward(xh, yh)
-        res = []
-        for s, e, gb, us, uc, ln, k1, k2, ffn in (
-                ("x", xe, D.weight(w.gate_x_b), "v2v", "v2i", w.ln_ffn_x, "fx1", "fx2", w.ffn_x),
-                ("y", ye, D.weight(w.gate_y_b), "i2i", "i2v", w.ln_ffn_y, "fy1", "fy2", w.ffn_y)):
+        x1s, hs = [], []
+        for s, e, gb, us, uc, ln in (
+                ("x", xe, D.weight(w.gate_x_b), "v2v", "v2i", w.ln_ffn_x),
+                ("y", ye, D.weight(w.gate_y_b), "i2i", "i2v", w.ln_ffn_y)):
             Y = L.buf[("Y", s)]
             lg = Y[:, L.cols[("extra", s)]:]
             x1, h = _gate_mix_ln(0, e, lg, Y.stride(0), gb, outs[us], outs[uc], ln,
                                  torch.bfloat16)
-            t = _ops.gemm(h, self.bf[k1])
-            _bias_act(0, t, D.weight(ffn.b1), 1)
-            # second FFN GEMM with its bias and the residual in the epilogue
+            x1s.append(x1)
+            hs.append(h)
+        # FFN on the tcgen05 GEMM, both streams per launch: gelu(h W1 + b1)
+        # (bias + erf-gelu in the epilogue, bf16), then t W2 + b2 + x1 (bias
+        # and residual in the epilogue, f32)
+        ts, p1 = [], []
+        for h, k1, ffn in zip(hs, ("fx1", "fy1"), (w.ffn_x, w.ffn_y)):
+            t = D.empty((h.shape[0], self.bf[k1].shape[0]), torch.bfloat16)
+            ts.append(t)
+            p1.append(_ops.gemm_problem(h, self.bf[k1], t, bias=D.weight(ffn.b1), gelu=True))
+        _ops.gemm_tc([p for p, h in zip(p1, hs) if h.shape[0]])
+        res, p2 = [], []
+        for t, x1, k2, ffn in zip(ts, x1s, ("fx2", "fy2"), (w.ffn_x, w.ffn_y)):
             u = D.empty(tuple(x1.shape), torch.float32)
-            w2 = self.bf[k2]
-            call("lsrm_gemm_bias_res_f32", t.shape[0], w2.shape[1], t.shape[1], t.data_ptr(),
-                 t.stride(0), w2.data_ptr(), w2.stride(0), D.weight(ffn.b2).data_ptr(),
-                 x1.data_ptr(), x1.stride(0), u.data_ptr(), u.stride(0), D.stream())
             res.append(u)
+            p2.append(_ops.gemm_problem(t, self.bf[k2], u, bias=D.weight(ffn.b2), res=x1))
+        _ops.gemm_tc([p for p, t in zip(p2, ts) if t.shape[0]])
         return tuple(res)
 
 
@@ -590,15 +599,18 @@ class SparseStageEngine:
         self.pool = {}
         self.blocks = [SparseBlockEngine(part_vol, part_img, plan_rows, w, params, pool=self.pool)
                        for w in weights]
-        self.inj = [(D.weight(w.inj_x, torch.bfloat16), D.weight(w.inj_y, torch.bfloat16))
-                    for w in weights]
+        # injection weights transposed for the tcgen05 GEMM
+        self.inj = [(D.dev(np.asarray(w.inj_x).T, torch.bfloat16),
+                     D.dev(np.asarray(w.inj_y).T, torch.bfloat16)) for w in weights]
 
     def forward(self, x_up: torch.Tensor, y_up: torch.Tensor):
         xb, yb = _ops.cast(x_up, torch.bfloat16), _ops.cast(y_up, torch.bfloat16)
         x, y = torch.zeros_like(x_up), torch.zeros_like(y_up)
+        xi = D.empty(tuple(x_up.shape), torch.float32)
+        yi = D.empty(tuple(y_up.shape), torch.float32)
         for blk, (ix, iy) in zip(self.blocks, self.inj):
-            xi = _ops.gemm(xb, ix, out_dtype=torch.float32)
-            yi = _ops.gemm(yb, iy, out_dtype=torch.float32)
+            _ops.gemm_tc([_ops.gemm_problem(a, wt, o) for a, wt, o in ((xb, ix, xi), (yb, iy, yi))
+                          if a.shape[0]])
             x, y = blk.forward(x, y, xi, yi)
         zero = torch.zeros(x_up.shape[1], dtype=torch.float32, device=x_up.device)
         return (_bias_act(0, x, zero, 0, residual=x_up, out_dtype=torch.float32),

@@ -567,8 +567,7 @@ class ShardedLayer:
             self.exchange.place(self.engine, use)
             self.engine.finish_kv(use)
         self.engine.attend_all()
-        for use in USES:
-            self.engine.output(use)
+        self.engine.output_all()
 
     def capture(self, x_loc, y_loc):
         """Record graphs A and B over fixed input buffers x_loc, y_loc."""
