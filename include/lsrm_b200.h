@@ -4,7 +4,8 @@
  * Every entry point takes plain pointers to caller-owned DEVICE memory
  * (unless a parameter says "host"), sizes as int64_t, and the CUDA stream to
  * run on (cudaStream_t passed as void*).  Nothing allocates device memory
- * behind the caller's back except the documented per-device cuBLAS handle.
+ * behind the caller's back except the per-thread cuBLAS handle of the fp32
+ * library GEMM (lsrm_gemm / lsrm_gemm_f32_ex).
  * Calls are reentrant: no shared scratch, per-call stream, per-thread error
  * buffer.  Outputs are deterministic (fixed reduction orders, no float
  * atomics on outputs).
@@ -252,27 +253,13 @@ int lsrm_score_topk(const float* q, int64_t nq, int hq, int hkv, int dh,
                     const float* k_cmp, int64_t n_blocks, int b_sel,
                     int32_t* out_rows, int32_t* out_count, void* stream);
 
-/* ---- GEMM (plain library GEMM, cuBLAS) --------------------------------
+/* ---- GEMM (plain library GEMM, cuBLAS; fp32 reference-API path) --------
  * C[m,n] = A[m,k] @ B[k,n] (+ bias[n]), row-major, lda/ldb/ldc in elements.
  * dtype 0 = fp32 (FFMA, no TF32), 1 = bf16 in / fp32 accumulate / bf16 out,
  * 2 = bf16 in / fp32 out. */
 int lsrm_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a,
               int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
               void* stream);
-
-/* C[m,n] = A[m,k] @ B[k,n] + bias[n], bf16 in / fp32 accumulate / bf16 out
- * (cuBLASLt bias epilogue; a per-device handle and 32 MiB workspace are made
- * on first use).  The engine uses it to fold the NSA gate biases into the
- * fused per-stream projection. */
-int lsrm_gemm_bias_bf16(int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
-                        const void* b, int64_t ldb, const void* bias, void* c,
-                        int64_t ldc, void* stream);
-
-/* D[m,n] = A[m,k] @ B[k,n] + bias[n] + R[m,n]: bf16 A/B, f32 bias, residual R
- * (may be NULL, may alias D) and output; cuBLASLt epilogue. */
-int lsrm_gemm_bias_res_f32(int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
-                           const void* b, int64_t ldb, const float* bias, const float* res,
-                           int64_t ldr, float* d, int64_t ldd, void* stream);
 
 /* ---- grouped bf16 GEMM on tcgen05 (hand-written; TMA + TMEM) ----------
  * Replaces the library GEMMs of the layer's hot path: the per-stream fused

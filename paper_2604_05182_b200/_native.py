@@ -56,8 +56,6 @@ SIGNATURES = {
     "lsrm_debug_set_trace": (I32, [P]),
     "lsrm_copy_segments": (I32, [P, P, P, I64, P]),
     "lsrm_kv_prepare_jobs": (I32, [P, I32, I64, I32, I32, P]),
-    "lsrm_gemm_bias_bf16": (I32, [I64, I64, I64, P, I64, P, I64, P, P, I64, P]),
-    "lsrm_gemm_bias_res_f32": (I32, [I64, I64, I64, P, I64, P, I64, P, P, I64, P, I64, P]),
     "lsrm_nsa_attention_tc_multi": (I32, [P, I32, I32, I32, I32, P, I64, P, P]),
     "lsrm_image_token_points": (I32, [P, I64, P, P, I32, I32, P, I32, F64, P, P, P]),
     "lsrm_pluecker_rays": (I32, [P, P, I32, I32, I32, P, P]),

@@ -68,7 +68,7 @@ def build(verbose: bool = False) -> str:
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", LIB, *objs,
-               "-lcublas", "-lcublasLt", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+               "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -1,10 +1,12 @@
-// Plain projection GEMMs through cuBLAS (library GEMM; the fused hot ops are
-// hand-written).  Row-major C[m,n] = A[m,k] @ B[k,n] is issued as the
-// column-major product C^T = B^T A^T.  fp32 mode never uses TF32.
+// Plain library GEMMs through cuBLAS for the fp32 reference-precision API path
+// and the fp32 training GEMMs (the bf16 hot path runs on the hand-written
+// tcgen05 GEMM, gemm_tc.cu).  Row-major C[m,n] = A[m,k] @ B[k,n] is issued as
+// the column-major product C^T = B^T A^T.  fp32 mode never uses TF32 unless
+// asked.  The cuBLAS handle is per thread and device (thread_local), so
+// concurrent callers on different streams share no state.
 #include "common.cuh"
 
 #include <cublas_v2.h>
-#include <cublasLt.h>
 
 namespace lsrm {
 
@@ -29,105 +31,9 @@ static int get_handle(cublasHandle_t* out) {
   return LSRM_OK;
 }
 
-// cuBLASLt (bias epilogue): one handle + 32 MiB workspace per device, made
-// on first use (the documented exception to "no hidden allocation").
-struct LtSlot {
-  cublasLtHandle_t h = nullptr;
-  void* ws = nullptr;
-};
-static LtSlot g_lt[16];
-constexpr size_t kLtWorkspace = 32u << 20;
-
-static int get_lt(int dev, LtSlot** out) {
-  if (dev < 0 || dev >= 16) return set_error(LSRM_E_CUDA, "device id %d out of range", dev);
-  LtSlot& s = g_lt[dev];
-  if (!s.h) {
-    if (cublasLtCreate(&s.h) != CUBLAS_STATUS_SUCCESS)
-      return set_error(LSRM_E_CUDA, "cublasLtCreate failed");
-    LSRM_CUDA(cudaMalloc(&s.ws, kLtWorkspace));
-  }
-  *out = &s;
-  return LSRM_OK;
-}
-
 }  // namespace lsrm
 
 using namespace lsrm;
-
-// Row-major D[m,n] = A[m,k] @ B[k,n] (bf16 in, fp32 accumulate) + bias[n]
-// (optional) + beta * C, issued as the column-major D^T = B^T A^T with a row
-// bias.  C may alias D.
-static int lt_gemm(int64_t m, int64_t n, int64_t k, const void* a, int64_t lda, const void* b,
-                   int64_t ldb, const void* bias, cudaDataType_t bias_t, float beta,
-                   const void* c, int64_t ldc, void* d, int64_t ldd, cudaDataType_t cd_t,
-                   void* stream) {
-  if (m == 0 || n == 0) return LSRM_OK;
-  int dev = 0;
-  LSRM_CUDA(cudaGetDevice(&dev));
-  LtSlot* lt;
-  int rc = get_lt(dev, &lt);
-  if (rc) return rc;
-  cublasLtMatmulDesc_t op = nullptr;
-  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr, ld = nullptr;
-  cublasLtMatmulPreference_t pref = nullptr;
-  int status = LSRM_OK;
-  cublasOperation_t tn = CUBLAS_OP_N;
-  cublasLtEpilogue_t epi = bias ? CUBLASLT_EPILOGUE_BIAS : CUBLASLT_EPILOGUE_DEFAULT;
-  size_t wsz = kLtWorkspace;
-  cublasLtMatmulHeuristicResult_t heur = {};
-  int n_res = 0;
-  const float one = 1.f;
-  bool ok = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) == CUBLAS_STATUS_SUCCESS;
-  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tn, sizeof(tn)) == 0;
-  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tn, sizeof(tn)) == 0;
-  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi)) == 0;
-  if (bias) {
-    ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias,
-                                              sizeof(bias)) == 0;
-    ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bias_t,
-                                              sizeof(bias_t)) == 0;
-  }
-  // column-major view: D (n x m) = B^T (n x k) . A^T (k x m)
-  ok = ok && cublasLtMatrixLayoutCreate(&la, CUDA_R_16BF, n, k, ldb) == 0;
-  ok = ok && cublasLtMatrixLayoutCreate(&lb, CUDA_R_16BF, k, m, lda) == 0;
-  ok = ok && cublasLtMatrixLayoutCreate(&lc, cd_t, n, m, c ? ldc : ldd) == 0;
-  ok = ok && cublasLtMatrixLayoutCreate(&ld, cd_t, n, m, ldd) == 0;
-  ok = ok && cublasLtMatmulPreferenceCreate(&pref) == 0;
-  ok = ok && cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
-                                                  &wsz, sizeof(wsz)) == 0;
-  ok = ok && cublasLtMatmulAlgoGetHeuristic(lt->h, op, la, lb, lc, ld, pref, 1, &heur, &n_res) == 0 &&
-       n_res > 0;
-  ok = ok && cublasLtMatmul(lt->h, op, &one, b, la, a, lb, &beta, c ? c : d, lc, d, ld,
-                            &heur.algo, lt->ws, kLtWorkspace,
-                            as_stream(stream)) == CUBLAS_STATUS_SUCCESS;
-  if (!ok) status = set_error(LSRM_E_CUDA, "cublasLt GEMM failed (m=%lld n=%lld k=%lld)",
-                              (long long)m, (long long)n, (long long)k);
-  if (pref) cublasLtMatmulPreferenceDestroy(pref);
-  if (ld) cublasLtMatrixLayoutDestroy(ld);
-  if (lc) cublasLtMatrixLayoutDestroy(lc);
-  if (lb) cublasLtMatrixLayoutDestroy(lb);
-  if (la) cublasLtMatrixLayoutDestroy(la);
-  if (op) cublasLtMatmulDescDestroy(op);
-  return status;
-}
-
-// C[m,n] = A[m,k] @ B[k,n] + bias[n], bf16 in / fp32 accumulate / bf16 out.
-extern "C" int lsrm_gemm_bias_bf16(int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
-                                   const void* b, int64_t ldb, const void* bias, void* c,
-                                   int64_t ldc, void* stream) {
-  return lt_gemm(m, n, k, a, lda, b, ldb, bias, CUDA_R_16BF, 0.f, nullptr, 0, c, ldc,
-                 CUDA_R_16BF, stream);
-}
-
-// D[m,n] = A[m,k] @ B[k,n] + bias[n] + R[m,n], bf16 in, f32 bias / residual /
-// out (the FFN's second GEMM with its bias and residual in the epilogue).
-extern "C" int lsrm_gemm_bias_res_f32(int64_t m, int64_t n, int64_t k, const void* a,
-                                      int64_t lda, const void* b, int64_t ldb, const float* bias,
-                                      const float* res, int64_t ldr, float* d, int64_t ldd,
-                                      void* stream) {
-  return lt_gemm(m, n, k, a, lda, b, ldb, bias, CUDA_R_32F, res ? 1.f : 0.f, res, ldr, d, ldd,
-                 CUDA_R_32F, stream);
-}
 
 extern "C" int lsrm_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a,
                          int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc,
