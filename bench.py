@@ -342,8 +342,9 @@ def time_setup(wl_name, reps=5):
     import torch
     import paper_2604_05182_b200 as L
     from paper_2604_05182_b200 import _dev as D
-    from paper_2604_05182_b200.block_routing import (RoutingBudgets, route_image_rows,
-                                                     route_volume_rows, volume_token_coords)
+    from paper_2604_05182_b200.block_routing import (ImageSide, RoutingBudgets,
+                                                     route_image_rows, route_volume_rows,
+                                                     volume_token_coords)
     from paper_2604_05182_b200.camera_geometry import silhouettes
     from paper_2604_05182_b200.workloads import (SCENE, coarse_inputs, load_workload,
                                                  orbit_cameras, params_of)
@@ -387,7 +388,29 @@ def time_setup(wl_name, reps=5):
                                                              wl.factor_vol, wl.factor_img))
     n = x_up.count + y_up.count
     res["compaction"] = entry(t, n * (4 * d + 12) + n * 4 * d,
-                              f"{n} tokens x d={d}: features + coords written, parents read")
+                              f"{n} tokens x d={d}: features + coords written, parents read; "
+                              "public call incl. mask scans and the token-count readback")
+    # the compaction's row kernels alone (no mask scan, no host readback):
+    # N x (4d + 24) written, N x 4d parent rows read
+    from paper_2604_05182_b200.tokenizer import _compact_rows, _compact_scan
+    tv = [D.weight(t) for t in pe_v.tables]
+    ti = [D.weight(t) for t in pe_i.tables]
+    vm8, im8 = vm.to(torch.uint8), im.to(torch.uint8)
+    ws_v, nc_v, n_v = _compact_scan("volume", vm8, 1, wl.vol_mask.shape[0], wl.factor_vol)
+    ws_i, nc_i, n_i = _compact_scan("image", im8, wl.img_mask.shape[0], wl.img_mask.shape[1],
+                                    wl.factor_img)
+    cv, fv = D.empty((n_v, 3), torch.int64), D.empty((n_v, d), torch.float32)
+    ci, fi = D.empty((n_i, 3), torch.int64), D.empty((n_i, d), torch.float32)
+
+    def rows():
+        _compact_rows("volume", ws_v, nc_v, n_v, xd, d, tv, 1, wl.vol_mask.shape[0],
+                      wl.factor_vol, cv, fv)
+        _compact_rows("image", ws_i, nc_i, n_i, yd, d, ti, wl.img_mask.shape[0],
+                      wl.img_mask.shape[1], wl.factor_img, ci, fi)
+    t, _ = timed(rows)
+    res["compaction_rows"] = entry(t, (n_v + n_i) * (8 * d + 24),
+                                   "compaction row kernels alone (cell lists from the scan): "
+                                   "features + coords written, parent rows read")
     t, pv = timed(lambda: L.partition(x_up))
     _, pi = timed(lambda: L.partition(y_up))
     res["partition_volume"] = entry(t, x_up.count * 16, "N x 16 B (incl. host metadata copy)")
@@ -397,11 +420,16 @@ def time_setup(wl_name, reps=5):
     t, _ = timed(lambda: route_volume_rows(vp, pv, bud.b_v2v))
     res["route_v2v"] = entry(t, x_up.count * 24 + pv.n_occupied * 24 + x_up.count * bud.b_v2v * 4,
                              "points + centers read, rows written (bit-exact f64)")
-    t, _ = timed(lambda: route_image_rows(vp, wl.cameras, pi, ip, bud.b_i, bud.b_v2i))
-    res["route_v2i"] = entry(t, x_up.count * 24 + pi.n_occupied * 24 + y_up.count * 24 +
-                             x_up.count * bud.b_v2i * 4,
-                             "two-stage image rule: projection top-b_i + 3D min-distance "
-                             "ranking (bit-exact f64; latency/compute-bound)")
+    t, side = timed(lambda: ImageSide(pi, ip, wl.cameras))
+    res["route_image_side"] = entry(t, y_up.count * 24 * 2 + pi.n_occupied * 48,
+                                    "image-router prep, once per plan: block-major SoA token "
+                                    "points + per-block bounding boxes")
+    for name, qp, nq_, b in (("route_v2i", vp, x_up.count, bud.b_v2i),
+                             ("route_i2i", ip, y_up.count, bud.b_i2i)):
+        t, _ = timed(lambda: route_image_rows(qp, wl.cameras, pi, ip, bud.b_i, b, side))
+        res[name] = entry(t, nq_ * 24 + pi.n_occupied * 24 + y_up.count * 24 + nq_ * b * 4,
+                          "two-stage image rule: projection top-b_i + 3D min-distance "
+                          "ranking with exact box pruning (bit-exact f64; latency/compute-bound)")
     return res
 
 

@@ -87,14 +87,23 @@ int lsrm_route_volume(const double* points, int64_t nq, const double* centers,
 /* ---- K8 image router  (block_routing.py:150-230) -----------------------
  * cams: [n_views, 21] f64 rows = K(9) R(9) t(3), row-major.
  * view_row_start [n_views+1]: occupied-row range of each view.
- * block_centers [B,2] (patch units); token_points_bm [Ni,3] f64 in
- * block-major order; block_offsets [B+1]. */
+ * block_centers [B,2] (patch units); token_points_bm [3, Ni] f64 (x, y, z
+ * rows, SoA) in block-major order; block_offsets [B+1]; max_view_rows = the largest
+ * occupied-row count of any view (sizes the per-warp shared scratch). */
 int lsrm_route_image(const double* points, int64_t nq, const double* cams,
                      int n_views, const int64_t* view_row_start,
                      const double* block_centers, int64_t n_blocks,
-                     const double* token_points_bm,
+                     const double* token_points_bm, const double* block_bounds,
                      const int64_t* block_offsets, int b_i, int budget,
-                     int32_t* out_rows, int32_t* out_count, void* stream);
+                     int max_view_rows, int32_t* out_rows, int32_t* out_count,
+                     void* stream);
+/* Bounding box of every block's token points: token_points_soa [3, n_points]
+ * block-major, bounds [n_blocks, 6] = (min xyz, max xyz).  The image router
+ * prunes candidates with it (exact: the box distance is a lower bound of the
+ * rounded point distances). */
+int lsrm_block_bounds(const double* token_points_soa, int64_t n_points,
+                      const int64_t* block_offsets, int64_t n_blocks, double* bounds,
+                      void* stream);
 
 /* ---- SDF fields  (camera_geometry.py:151-205, runner.py:301-306) -------
  * kind 0 analytic: prims = n_prims rows of 8 f64 (as lsrm_voxel_mask);
@@ -218,6 +227,16 @@ int lsrm_compact_image(const uint8_t* mask, int n_views, int s_fine,
                        const float* pe_v, int64_t* coords, float* features,
                        int64_t max_out, int64_t* n_out, void* workspace,
                        size_t ws_bytes, void* stream);
+/* Second half of a two-call compaction: after lsrm_compact_volume /
+ * lsrm_compact_image ran with coords = features = NULL (mask scan, cell list
+ * left in `workspace`, count in *n_out), write the n_out tokens' coords and
+ * features from that cell list without rescanning the mask (no host sync).
+ * modality 0 = volume (pe0..pe2 the three axis tables), 1 = image (pe0 = u
+ * table, pe1 = v table, pe2 unused); n_cells = the mask's cell count. */
+int lsrm_compact_rows(int modality, const void* workspace, int64_t n_cells, int64_t n_out,
+                      int n_views, int s_fine, int factor, const float* parents, int d,
+                      const float* pe0, const float* pe1, const float* pe2, int64_t* coords,
+                      float* features, void* stream);
 
 /* ---- fp32 attention branches on CUDA cores  (nsa_attention.py:84-207) --
  * q [nq, hq, dh]; keys/values [nk, hkv, dh] f32 in BLOCK-MAJOR order of the

@@ -33,7 +33,8 @@ SIGNATURES = {
     "lsrm_compress_block": (I32, [I32, P, I64, I64, I32, P, P, P, P, P, P, I64, P,
                                   P, P]),
     "lsrm_route_volume": (I32, [P, I64, P, I64, I32, P, P, P]),
-    "lsrm_route_image": (I32, [P, I64, P, I32, P, P, I64, P, P, I32, I32, P, P, P]),
+    "lsrm_route_image": (I32, [P, I64, P, I32, P, P, I64, P, P, P, I32, I32, I32, P, P, P]),
+    "lsrm_block_bounds": (I32, [P, I64, P, I64, P, P]),
     "lsrm_build_gather_table": (I32, [P, P, I64, I32, P, I32, P, P, I64, P, P, P, P,
                                       P, P]),
     "lsrm_foreground_mask": (I32, [P, I32, I32, I32, I32, P, P]),
@@ -93,6 +94,7 @@ SIGNATURES = {
     "lsrm_voxel_sample_points": (I32, [I32, I32, I32, I32, P, P]),
     "lsrm_affine_exact": (I32, [P, I64, I64, I32, P, P, I32, I32, P, I64, P]),
     "lsrm_gemm_tc": (I32, [P, I32, P]),
+    "lsrm_compact_rows": (I32, [I32, P, I64, I64, I32, I32, I32, P, I32, P, P, P, P, P, P]),
 }
 
 _lib = None

@@ -147,8 +147,32 @@ def route_volume_rows(points, part: BlockPartition, budget: int):
     return rows, count
 
 
+class ImageSide:
+    """Per-(image partition, token points, cameras) device state of the image
+    router: block-major token points SoA [3, Ni], per-block bounding boxes
+    (`lsrm_block_bounds`), packed cameras and per-view row ranges.  Built once
+    and shared by every query set routed against the same image side (v2i and
+    i2i of a plan)."""
+
+    def __init__(self, part: BlockPartition, token_points, cameras):
+        tp = token_points.points if isinstance(token_points, TokenCoords3D) else token_points
+        cams = pack_cameras(cameras)
+        self.n_views = int(cams.shape[0])
+        vrs = np.searchsorted(part.block_views, np.arange(self.n_views + 1)).astype(np.int64)
+        self.max_view_rows = int(np.diff(vrs).max()) if vrs.size > 1 else 0
+        self.cams, self.vrs = D.dev(cams), D.dev(vrs)
+        # block-major token points, SoA [3, Ni] (coalesced loads in the kernel)
+        self.tp = _ops.gather_rows(D.dev(tp, torch.float64),
+                                   part.dev("block_token_ids")).t().contiguous()
+        self.bounds = D.empty((part.n_occupied, 6), torch.float64)
+        if part.n_occupied:
+            call("lsrm_block_bounds", self.tp.data_ptr(), int(self.tp.shape[1]),
+                 part.dev("block_offsets").data_ptr(), part.n_occupied,
+                 self.bounds.data_ptr(), D.stream())
+
+
 def route_image_rows(points, cameras, part: BlockPartition, token_points, b_i: int,
-                     budget: int):
+                     budget: int, side: ImageSide = None):
     pts = D.dev(points, torch.float64)
     nq = int(pts.shape[0])
     rows = D.empty((nq, max(budget, 1)), torch.int32)
@@ -156,19 +180,11 @@ def route_image_rows(points, cameras, part: BlockPartition, token_points, b_i: i
     if nq == 0 or part.n_occupied == 0:
         rows.fill_(-1)
         return rows, count
-    cams = pack_cameras(cameras)
-    n_views = cams.shape[0]
-    vrs = np.searchsorted(part.block_views, np.arange(n_views + 1)).astype(np.int64)
-    tp = token_points.points if isinstance(token_points, TokenCoords3D) else token_points
-    tp_bm = _ops.gather_rows(D.dev(tp, torch.float64), part.dev("block_token_ids"))
-    # keep the staging tensors referenced until the launch is enqueued: a
-    # temporary's block returns to torch's caching allocator immediately and
-    # the next H2D copy could overwrite it before the kernel reads it
-    cams_d, vrs_d = D.dev(cams), D.dev(vrs)
-    call("lsrm_route_image", pts.data_ptr(), nq, cams_d.data_ptr(), n_views,
-         vrs_d.data_ptr(), part.dev("block_centers").data_ptr(), part.n_occupied,
-         tp_bm.data_ptr(), part.dev("block_offsets").data_ptr(), b_i, budget,
-         rows.data_ptr(), count.data_ptr(), D.stream())
+    side = side or ImageSide(part, token_points, cameras)
+    call("lsrm_route_image", pts.data_ptr(), nq, side.cams.data_ptr(), side.n_views,
+         side.vrs.data_ptr(), part.dev("block_centers").data_ptr(), part.n_occupied,
+         side.tp.data_ptr(), side.bounds.data_ptr(), part.dev("block_offsets").data_ptr(), b_i,
+         budget, side.max_view_rows, rows.data_ptr(), count.data_ptr(), D.stream())
     return rows, count
 
 
@@ -202,11 +218,12 @@ def build_routing_plan(vol_coords, img_coords, part_vol, part_img, cameras,
     are kept on the plan for the fused attention path."""
     vp = vol_coords.points if isinstance(vol_coords, TokenCoords3D) else vol_coords
     ip = img_coords.points if isinstance(img_coords, TokenCoords3D) else img_coords
+    side = ImageSide(part_img, ip, cameras) if part_img.n_occupied else None
     dev_rows = {
         "v2v": route_volume_rows(vp, part_vol, budgets.b_v2v),
         "i2v": route_volume_rows(ip, part_vol, budgets.b_i2v),
-        "v2i": route_image_rows(vp, cameras, part_img, ip, budgets.b_i, budgets.b_v2i),
-        "i2i": route_image_rows(ip, cameras, part_img, ip, budgets.b_i, budgets.b_i2i),
+        "v2i": route_image_rows(vp, cameras, part_img, ip, budgets.b_i, budgets.b_v2i, side),
+        "i2i": route_image_rows(ip, cameras, part_img, ip, budgets.b_i, budgets.b_i2i, side),
     }
     parts = {"v2v": part_vol, "i2v": part_vol, "v2i": part_img, "i2i": part_img}
     tables, fallback = {}, {}

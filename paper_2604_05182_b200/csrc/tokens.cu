@@ -268,6 +268,62 @@ __global__ void compact_image_rows(const int32_t* __restrict__ cells, int64_t n_
   }
 }
 
+// Vectorised variant (d % 4 == 0, 16-byte aligned rows): one warp per output
+// token, four columns per lane per step (float4 loads and stores), the same
+// f64 add order as compact_*_rows.  kind 0 = volume (three tables), 1 = image
+// (pe0 = u table, pe1 = v table).
+template <int KIND>
+__global__ void compact_rows_vec4(const int32_t* __restrict__ cells, int64_t n_out, int s, int f,
+                                  const float4* __restrict__ par, int d4,
+                                  const float4* __restrict__ pe0, const float4* __restrict__ pe1,
+                                  const float4* __restrict__ pe2, int64_t* __restrict__ coords,
+                                  float4* __restrict__ feats) {
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= n_out) return;
+  const int64_t cell = cells[row];
+  const int sc = s / f;
+  int64_t a, b, c, parent;
+  if (KIND == 0) {
+    a = cell / ((int64_t)s * s); b = (cell / s) % s; c = cell % s;
+    parent = ((a / f) * sc + b / f) * sc + c / f;
+  } else {
+    a = cell / ((int64_t)s * s); b = (cell / s) % s; c = cell % s;   // view, row, col
+    parent = (a * sc + b / f) * sc + c / f;
+  }
+  if (lane == 0 && coords) {
+    coords[3 * row] = a;
+    coords[3 * row + 1] = KIND == 0 ? b : c;
+    coords[3 * row + 2] = KIND == 0 ? c : b;
+  }
+  if (!feats) return;
+  for (int k = lane; k < d4; k += 32) {
+    float4 x = __ldg(par + parent * d4 + k);
+    float4 o;
+    float* op = &o.x;
+    const float* xp = &x.x;
+    if (KIND == 0) {
+      const float4 t0 = __ldg(pe0 + a * d4 + k), t1 = __ldg(pe1 + b * d4 + k),
+                   t2 = __ldg(pe2 + c * d4 + k);
+      const float *p0 = &t0.x, *p1 = &t1.x, *p2 = &t2.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float pe = (float)dadd(dadd(dadd(0.0, (double)p0[e]), (double)p1[e]), (double)p2[e]);
+        op[e] = (float)dadd((double)xp[e], (double)pe);
+      }
+    } else {
+      const float4 tu = __ldg(pe0 + c * d4 + k), tv = __ldg(pe1 + b * d4 + k);
+      const float *pu = &tu.x, *pv = &tv.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float pe = (float)dadd(dadd(0.0, (double)pu[e]), (double)pv[e]);
+        op[e] = (float)dadd((double)xp[e], (double)pe);
+      }
+    }
+    feats[row * d4 + k] = o;
+  }
+}
+
 static int compact_cells(const uint8_t* mask, int64_t n_cells, void* workspace,
                          size_t ws_bytes, int32_t** cells_out, int64_t* n_out,
                          cudaStream_t st) {
@@ -411,6 +467,41 @@ int lsrm_compact_image(const uint8_t* mask, int n_views, int s_fine, int factor,
                (long long)*n_out, (long long)max_out);
   compact_image_rows<<<(unsigned)ceil_div(*n_out, 8), 256, 0, st>>>(
       cells, *n_out, s_fine, factor, y_d, d, pe_u, pe_v, coords, features);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_compact_rows(int modality, const void* workspace, int64_t n_cells, int64_t n_out,
+                      int n_views, int s_fine, int factor, const float* parents, int d,
+                      const float* pe0, const float* pe1, const float* pe2, int64_t* coords,
+                      float* features, void* stream) {
+  LSRM_REQUIRE(modality == 0 || modality == 1, "compact_rows: modality must be 0 or 1");
+  LSRM_REQUIRE(factor >= 1 && s_fine % factor == 0, "mask not divisible by factor");
+  (void)n_views;
+  if (n_out == 0) return LSRM_OK;
+  const int64_t n_chunks = ceil_div(n_cells, kScanChunk);
+  const int32_t* cells = (const int32_t*)((const char*)workspace + 16 +
+                                          ((n_chunks * sizeof(int) + 15) / 16) * 16);
+  cudaStream_t st = as_stream(stream);
+  const uintptr_t al = (uintptr_t)parents | (uintptr_t)pe0 | (uintptr_t)pe1 |
+                       (uintptr_t)(modality == 0 ? pe2 : nullptr) | (uintptr_t)features;
+  const unsigned blocks = (unsigned)ceil_div(n_out, 8);
+  if (d % 4 == 0 && (al & 15) == 0) {
+    if (modality == 0)
+      compact_rows_vec4<0><<<blocks, 256, 0, st>>>(
+          cells, n_out, s_fine, factor, (const float4*)parents, d / 4, (const float4*)pe0,
+          (const float4*)pe1, (const float4*)pe2, coords, (float4*)features);
+    else
+      compact_rows_vec4<1><<<blocks, 256, 0, st>>>(
+          cells, n_out, s_fine, factor, (const float4*)parents, d / 4, (const float4*)pe0,
+          (const float4*)pe1, nullptr, coords, (float4*)features);
+  } else if (modality == 0) {
+    compact_volume_rows<<<blocks, 256, 0, st>>>(cells, n_out, s_fine, factor, parents, d, pe0,
+                                                pe1, pe2, coords, features);
+  } else {
+    compact_image_rows<<<blocks, 256, 0, st>>>(cells, n_out, s_fine, factor, parents, d, pe0,
+                                               pe1, coords, features);
+  }
   LSRM_LAUNCHED();
   return LSRM_OK;
 }

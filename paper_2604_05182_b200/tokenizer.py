@@ -135,7 +135,9 @@ def informative_voxel_mask(field, s_vol: int, tau: float = None, t_side: int = 4
     return _ret(m.bool(), as_device)
 
 
-def _compact(kind, mask_u8, parents, d, tables, n_views, s_fine, factor):
+def _compact_scan(kind, mask_u8, n_views, s_fine, factor):
+    """Mask scan: cell list of the set cells in the returned workspace and
+    their count (one host readback: the output size is data-dependent)."""
     n_cells = mask_u8.numel()
     ws_bytes = lib().lsrm_compact_workspace(n_cells)
     ws = D.empty((ws_bytes,), torch.uint8)
@@ -143,24 +145,30 @@ def _compact(kind, mask_u8, parents, d, tables, n_views, s_fine, factor):
     nptr = n_out.ctypes.data
     st = D.stream()
     if kind == "volume":
-        call("lsrm_compact_volume", mask_u8.data_ptr(), s_fine, factor, None, d, None, None,
+        call("lsrm_compact_volume", mask_u8.data_ptr(), s_fine, factor, None, 0, None, None,
              None, None, None, 0, nptr, ws.data_ptr(), ws_bytes, st)
     else:
-        call("lsrm_compact_image", mask_u8.data_ptr(), n_views, s_fine, factor, None, d, None,
+        call("lsrm_compact_image", mask_u8.data_ptr(), n_views, s_fine, factor, None, 0, None,
              None, None, None, 0, nptr, ws.data_ptr(), ws_bytes, st)
-    n = int(n_out[0])
+    return ws, n_cells, int(n_out[0])
+
+
+def _compact_rows(kind, ws, n_cells, n, parents, d, tables, n_views, s_fine, factor,
+                  coords, feats):
+    """Coords + features of the n scanned cells (no rescan, no host sync)."""
+    if n:
+        tp = [t.data_ptr() for t in tables] + [None] * (3 - len(tables))
+        call("lsrm_compact_rows", 0 if kind == "volume" else 1, ws.data_ptr(), n_cells, n,
+             n_views, s_fine, factor, parents.data_ptr(), d, tp[0], tp[1], tp[2],
+             coords.data_ptr(), feats.data_ptr(), D.stream())
+
+
+def _compact(kind, mask_u8, parents, d, tables, n_views, s_fine, factor):
+    ws, n_cells, n = _compact_scan(kind, mask_u8, n_views, s_fine, factor)
     coords = D.empty((n, 3), torch.int64)
     feats = D.empty((n, d), torch.float32)
-    if n:
-        tp = [t.data_ptr() for t in tables]
-        if kind == "volume":
-            call("lsrm_compact_volume", mask_u8.data_ptr(), s_fine, factor, parents.data_ptr(),
-                 d, tp[0], tp[1], tp[2], coords.data_ptr(), feats.data_ptr(), n, nptr,
-                 ws.data_ptr(), ws_bytes, st)
-        else:
-            call("lsrm_compact_image", mask_u8.data_ptr(), n_views, s_fine, factor,
-                 parents.data_ptr(), d, tp[0], tp[1], coords.data_ptr(), feats.data_ptr(), n,
-                 nptr, ws.data_ptr(), ws_bytes, st)
+    _compact_rows(kind, ws, n_cells, n, parents, d, tables, n_views, s_fine, factor, coords,
+                  feats)
     return coords, feats
 
 

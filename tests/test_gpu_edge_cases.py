@@ -175,3 +175,32 @@ def test_reference_api_reads_current_weights(cuda):
     toks2 = L.TokenSet("volume", np.zeros((300, 32), np.float32), coords[::-1].copy(), (16,) * 3)
     with pytest.raises(ConfigurationError):
         L.nsa_cross_attention(x, x, L.partition(toks2), part, sel, w, params)
+
+
+@pytest.mark.parametrize("b_i", [1, 5, 16, 70, 200])
+def test_image_router_dense_views_and_ties(cuda, b_i):
+    """Image router against the oracle where views hold many occupied blocks
+    (144 per view, more than a warp) and the shortlist cut b_i falls inside
+    them, with duplicated token points so minimum distances tie (stable row
+    order decides), queries in front of and behind the cameras."""
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200.workloads import orbit_cameras
+    g = np.random.default_rng(b_i)
+    views, side = 3, 96
+    cams = orbit_cameras(views, 1.7, 20.0, (8 * side, 8 * side))
+    ic = np.argwhere(g.random((views, side, side)) < 0.6)
+    coords = np.stack([ic[:, 0], ic[:, 2], ic[:, 1]], 1)
+    y = L.TokenSet("image", np.zeros((coords.shape[0], 4), np.float32), coords,
+                   (views, side, side))
+    part = L.partition(y)
+    assert np.diff(np.searchsorted(part.block_views, np.arange(views + 1))).max() > 64
+    pts = g.random((coords.shape[0], 3))
+    pts[1::2] = pts[::2][: pts[1::2].shape[0]]          # duplicated points -> tied minima
+    queries = np.concatenate([g.random((300, 3)), g.random((20, 3)) * 6.0 - 3.0])
+    from paper_2604_05182_b200.block_routing import _route_points_to_image
+    got = _route_points_to_image(queries, cams, part, L.TokenCoords3D(pts, np.zeros(
+        pts.shape[0], bool)), b_i, 8)
+    opart = O.partition_tokens("image", coords, (views, side, side))
+    want = O.route_image(queries, [c[:3] for c in cams], opart, pts, b_i, 8)
+    for a, b in zip(got.lists, want):
+        assert np.array_equal(a, b)
