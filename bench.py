@@ -324,7 +324,9 @@ def run_gpu(args):
     # -- per-kernel breakdown (separate pass, events on the launching stream)
     brk = layer.profile_breakdown(x_bm, y_bm, reps=max(3, args.steps))
     clocks = sampler.stop()
-    # -- end to end through the public host API (pinned host buffers)
+    # -- end to end through the reference-facing call (NumPy host buffers)
+    api_ms, api_h2d, api_d2h = time_reference_api(inst, args.steps)
+    # -- and through the package's pipelined host API (pinned host buffers)
     e2e_ms, h2d, d2h = layer.time_host_path(inst.x_hat, inst.y_hat, steps=args.steps)
     pcie = pcie_bandwidth()
     # e2e roofline: the duplex copy of one step's inputs and outputs
@@ -354,6 +356,7 @@ def run_gpu(args):
     block = time_sparse_block(inst, n_tok, args.steps)
     train = time_train_step(inst) if wl_name != "c5" else None
     setup = time_setup(wl_name) if wl_name in ("c3", "c4") else None
+    c1 = time_c1_fp32(max(5, args.steps)) if wl_name == "c3" else None
     line = {
         "metric": "LSRM sparse-attn layer tokens/s", "value": n_tok / (ms * 1e-3),
         "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -377,8 +380,18 @@ def run_gpu(args):
         "sparse_block": block,
         "train_step": train,
         "setup_kernels": setup,
+        "c1_fp32": c1,
         "cpu_baseline": cpu,
-        "e2e": {"value": n_tok / (e2e_ms * 1e-3), "unit": "tokens/s",
+        "e2e": {"value": n_tok / (api_ms * 1e-3), "unit": "tokens/s",
+                "h2d_bytes_per_step": api_h2d, "d2h_bytes_per_step": api_d2h,
+                "ms_per_step": api_ms,
+                "what": "reference-API nsa_cross_attention x 4 uses (drop-in precision='bf16'), "
+                        "NumPy f32 host buffers in and out, wall clock per layer",
+                "pcie_bound_ms": max(api_h2d / (pcie["h2d_gbps"] * 1e9),
+                                     api_d2h / (pcie["d2h_gbps"] * 1e9)) * 1e3},
+        "e2e_pipelined": {"value": n_tok / (e2e_ms * 1e-3), "unit": "tokens/s",
+                "what": "package host API layer.HostPipeline: pinned f32 in/out, H2D / compute / "
+                        "D2H on separate streams, two steps in flight",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                 "roofline": {"bound": "pcie", "pcie_measured": pcie,
                              "bound_ms": e2e_bound_ms, "frac": e2e_bound_ms / e2e_ms,
@@ -389,6 +402,117 @@ def run_gpu(args):
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
+
+
+def time_c1_fp32(steps):
+    """BASELINE config 1 (C1: 4 views, desk heads 8/1/8, d = 64, fp32 fwd,
+    1 GPU): the reference-API layer on the fp32 path the C1 oracle pins
+    (≤1e-5): four `nsa_cross_attention` calls on device-resident f32 inputs
+    (fp32 projections, f64-sum compression, CUDA-core fp32 attention). Device
+    events around each layer. The bf16 engine does not take d_h = 8."""
+    import torch
+    from paper_2604_05182_b200 import _dev as D
+    from paper_2604_05182_b200.layer import build_instance
+    from paper_2604_05182_b200.nsa_attention import (GatherTable, Selection, nsa_cross_attention,
+                                                     resolve_rows)
+    from paper_2604_05182_b200.engine import SparseLayerEngine  # noqa: F401 (native lib loaded)
+    inst = build_instance("c1")
+    p = inst.params
+    parts = {"x": inst.part_vol, "y": inst.part_img}
+    feats = {"x": D.dev(inst.x_hat), "y": D.dev(inst.y_hat)}
+    geom = {"v2v": ("x", "x"), "v2i": ("x", "y"), "i2i": ("y", "y"), "i2v": ("y", "x")}
+    tables = {}
+    for use, (qs, ks) in geom.items():
+        r, c = inst.plan_rows[use]
+        own = parts[ks].block_of_token if qs == ks else None
+        rr, cc, lens, _, _ = resolve_rows(r, c, parts[ks], own, True)
+        rh, ch = D.host(r), D.host(c)
+        sel = Selection([parts[ks].occupied_ids[rh[i, :ch[i]]] for i in range(rh.shape[0])])
+        tables[use] = (GatherTable(None, None, D.host(lens), rr, cc), lens, sel)
+
+    def layer():
+        return {use: nsa_cross_attention(feats[qs], feats[ks], parts[qs], parts[ks],
+                                         tables[use][2], inst.weights[use], p,
+                                         table=tables[use][0])
+                for use, (qs, ks) in geom.items()}
+    for _ in range(3):
+        layer()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    ms = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        layer()
+        b.record(st)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = float(np.median(ms))
+    n_tok = inst.n_vol + inst.n_img
+    # algorithmic attention-core FLOPs (SURVEY §8d), useful work only
+    flops = 0.0
+    for use, (qs, ks) in geom.items():
+        pk, pq = parts[ks], parts[qs]
+        nq = pq.n_tokens
+        L_ = float(D.host(tables[use][1]).sum())
+        flops += 4.0 * p.n_q_heads * p.head_dim * (nq * pk.n_occupied + L_)
+        if qs == ks:
+            flops += 4.0 * p.n_q_heads * p.head_dim * float((pq.occupancy.astype(np.float64) ** 2).sum())
+    # fp32 FFMA peak: 148 SMs x 128 lanes x 2 flops x 1.965 GHz
+    peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    return {"workload": WORKLOAD_DESC["c1"], "n_vol": inst.n_vol, "n_img": inst.n_img,
+            "ms_per_layer": t, "tokens_per_s": n_tok / (t * 1e-3), "dtype": "fp32",
+            "attention_flops": flops, "attention_tflops_incl_projections_time": flops / (t * 1e-3) / 1e12,
+            "fp32_peak_tflops": peak,
+            "what": "reference-API nsa_cross_attention x 4 uses, fp32 path (<=1e-5 of the "
+                    "reference at C1), device-resident inputs, CUDA events, median of steps"}
+
+
+def time_reference_api(inst, steps):
+    """e2e through the reference-facing call: the drop-in's precision="bf16"
+    `nsa_cross_attention` (the reference's signature, `lsrm/nsa_attention.py:287`)
+    called for the four uses of the layer with NumPy f32 host buffers in and
+    out, as `lsrm.recon_pipeline._nsa_use` calls it (`recon_pipeline.py:451-458`).
+    Each call copies its host inputs to the device, runs the one-use bf16
+    engine (cached across calls, like a reference user's repeated calls) and
+    returns a fresh NumPy array. Returns (ms per layer, h2d B, d2h B)."""
+    import torch
+    from paper_2604_05182_b200 import _dev as D, fastpath
+    from paper_2604_05182_b200.nsa_attention import Selection, nsa_cross_attention
+    pv, pi = inst.part_vol, inst.part_img
+    parts = {"x": pv, "y": pi}
+    feats = {"x": np.ascontiguousarray(inst.x_hat, np.float32),
+             "y": np.ascontiguousarray(inst.y_hat, np.float32)}
+    geom = {"v2v": ("x", "x"), "v2i": ("x", "y"), "i2i": ("y", "y"), "i2v": ("y", "x")}
+    sels = {}
+    for use, (qs, ks) in geom.items():
+        r, c = (D.host(t) for t in inst.plan_rows[use])
+        occ = parts[ks].occupied_ids
+        sels[use] = Selection([occ[r[i, :c[i]]] for i in range(r.shape[0])])
+    fastpath.set_precision("bf16")
+    try:
+        def layer():
+            outs = {}
+            for use, (qs, ks) in geom.items():
+                outs[use] = nsa_cross_attention(feats[qs], feats[ks], parts[qs], parts[ks],
+                                                sels[use], inst.weights[use], inst.params)
+            return outs
+        layer()                            # engine build + warm-up (not timed)
+        layer()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            outs = layer()
+        torch.cuda.synchronize()
+        ms = (time.perf_counter() - t0) * 1e3 / steps
+    finally:
+        fastpath.set_precision("fp32")
+    # bytes each step moves: every call uploads its query rows and (cross
+    # uses) its key rows; self uses pass one buffer, uploaded once
+    h2d = sum(feats[qs].nbytes + (feats[ks].nbytes if qs != ks else 0)
+              for qs, ks in geom.values())
+    d2h = sum(o.nbytes for o in outs.values())
+    return ms, h2d, d2h
 
 
 def time_setup(wl_name, reps=5):
@@ -470,6 +594,29 @@ def time_setup(wl_name, reps=5):
     res["compaction_rows"] = entry(t, (n_v + n_i) * (8 * d + 24),
                                    "compaction row kernels alone (cell lists from the scan): "
                                    "features + coords written, parent rows read")
+    # BASELINE config 2 on DECODED geometry (the paper's coarse-to-fine
+    # scoring, `lsrm/runner.py:301-311`): coarse tokens -> dense feature grid
+    # -> Eq. 11 on the decoded SDF (4^3 samples per fine voxel, each a
+    # trilinear feature lookup + the SDF head, in-kernel)
+    from paper_2604_05182_b200.recon_pipeline import (decode_feature_volume, init_decode,
+                                                      init_decoder_heads)
+    from paper_2604_05182_b200.sdf import decoded_sdf_field
+    dw = init_decode(0, d, "dec_coarse")
+    t_dec, grid = timed(lambda: decode_feature_volume(xd, dw))
+    res["decode_grid"] = entry(t_dec, int(xd.numel()) * 4 + grid.numel() * 4,
+                               f"coarse tokens {tuple(xd.shape)} -> dense grid "
+                               f"{tuple(grid.shape)} f32 (f64 affine, einsum order)")
+    field = decoded_sdf_field(grid, init_decoder_heads(0))
+    t_vmd, vmd = timed(lambda: L.informative_voxel_mask(field, wl.s_vol, as_device=True))
+    res["voxel_mask_decoded"] = entry(t_vmd, grid.numel() * 4 + wl.s_vol ** 3,
+                                      f"S={wl.s_vol}: 64 decoded-SDF samples per voxel "
+                                      f"(grid read, S^3 bytes written; f64, compute-bound)")
+    res["voxel_mask_decoded"]["informative_voxels"] = int(D.host(vmd).sum())
+    coarse_ms = (t_dec + t_vmd + res["foreground_mask"]["ms"] + res["compaction"]["ms"])
+    res["coarse_stage"] = {
+        "ms": coarse_ms, "tokens": int(n), "tokens_per_s": n / (coarse_ms * 1e-3),
+        "what": "BASELINE config 2: decode grid + decoded-SDF voxel informativeness + "
+                f"foreground pruning ({v} views) + compaction (d={d}); sum of the public calls"}
     t, pv = timed(lambda: L.partition(x_up))
     _, pi = timed(lambda: L.partition(y_up))
     res["partition_volume"] = entry(t, x_up.count * 16, "N x 16 B (incl. host metadata copy)")

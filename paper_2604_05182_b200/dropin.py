@@ -10,6 +10,11 @@ reference's object, and returns the list of (module, name) pairs it changed.
 
     import lsrm, paper_2604_05182_b200.dropin as d
     patched = d.install(lsrm)     # lsrm.run_scene(...) now routes/attends on the GPU
+    d.install(lsrm, precision="bf16")   # + NSA uses / blocks / stage on the bf16 engines
+
+precision="fp32" (default) keeps the reference's float contract (fp32 CUDA
+kernels, <=1e-5); "bf16" sends `nsa_cross_attention`, `sparse_block_forward`
+and `sparse_stage_forward` to the tcgen05 engines (fastpath.py; rel-L2 <=1e-2).
 """
 
 import importlib
@@ -27,7 +32,8 @@ HOT_PATH = {
     "tokenizer": ("informative_voxel_mask", "foreground_patch_mask", "upsample_select_tokens"),
     "seq_parallel": ("shard_blocks", "all_to_all", "all_gather_kv", "naive_contiguous_shards",
                      "parallel_sparse_stage"),
-    "recon_pipeline": ("sparse_block_forward", "build_sparse_context", "ffn_forward",
+    "recon_pipeline": ("sparse_block_forward", "sparse_stage_forward", "build_sparse_context",
+                       "ffn_forward",
                        "mha_forward", "dense_block_forward", "dense_stage_forward",
                        "decode_feature_volume", "build_sparse_features", "query_field",
                        "decode_points"),
@@ -43,8 +49,10 @@ def _ours(module: str, name: str):
     return getattr(mod, name, None)
 
 
-def install(lsrm_pkg) -> list:
+def install(lsrm_pkg, precision: str = "fp32") -> list:
     """Patch the hot-path names of an imported reference `lsrm` package."""
+    from . import fastpath
+    fastpath.set_precision(precision)
     mods = {}
     for info in pkgutil.iter_modules(lsrm_pkg.__path__):
         try:
@@ -69,6 +77,8 @@ def install(lsrm_pkg) -> list:
 
 
 def uninstall() -> None:
+    from . import fastpath
+    fastpath.set_precision("fp32")
     while _saved:
         mod, name, obj = _saved.pop()
         setattr(mod, name, obj)

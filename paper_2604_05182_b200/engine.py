@@ -209,6 +209,10 @@ class SparseLayerEngine:
                  weights: dict, params: AttentionParams, shard: dict = None,
                  extra_cols: dict = None, pool: dict = None):
         require(params.head_dim in (32, 64), "bf16 engine: head_dim must be 32 or 64")
+        # the uses this engine runs: every use `weights` holds (a layer is all
+        # four; the reference-API drop-in builds one-use engines)
+        self.uses = tuple(u for u in USES if u in weights)
+        require(len(self.uses) > 0, "bf16 engine: no NSA use weights given")
         G = params.group_size
         require(128 % G == 0 and G >= 4, "bf16 engine: (n_q_heads/n_kv_heads) must be in 4..128 "
                 "and divide 128")
@@ -229,14 +233,14 @@ class SparseLayerEngine:
         wcat = {"x": [], "y": []}
         bcat = {"x": [], "y": []}
         ncol = {"x": 0, "y": 0}
-        for use in USES:
+        for use in self.uses:
             qs, _, ng = USE_GEOM[use]
             wu = weights[use]
             self.cols[(use, "q")] = ncol[qs]
             wcat[qs] += [wu.w_q, wu.gate_w]
             bcat[qs] += [np.zeros(d, np.float32), np.asarray(wu.gate_b, np.float32)]
             ncol[qs] += d + ng * d
-        for use in USES:
+        for use in self.uses:
             _, ks, _ = USE_GEOM[use]
             wu = weights[use]
             self.cols[(use, "k")] = ncol[ks]
@@ -252,15 +256,16 @@ class SparseLayerEngine:
         self.ncol = ncol
         # weights stored transposed ([n, k], K contiguous): both tcgen05 GEMM
         # operands K-major (csrc/gemm_tc.cu)
-        self.w_cat = {s: D.dev(np.concatenate(wcat[s], axis=1).T, torch.bfloat16) for s in wcat}
-        self.b_cat = {s: D.dev(np.concatenate(bcat[s]), torch.bfloat16) for s in bcat}
-        self.w_o = {u: D.dev(np.asarray(weights[u].w_o).T, torch.bfloat16) for u in USES}
-        self.gate_b = {u: D.dev(weights[u].gate_b, torch.float32) for u in USES}
+        self.w_cat = {s: D.dev(np.concatenate(wcat[s], axis=1).T, torch.bfloat16)
+                      for s in wcat if wcat[s]}
+        self.b_cat = {s: D.dev(np.concatenate(bcat[s]), torch.bfloat16) for s in bcat if bcat[s]}
+        self.w_o = {u: D.dev(np.asarray(weights[u].w_o).T, torch.bfloat16) for u in self.uses}
+        self.gate_b = {u: D.dev(weights[u].gate_b, torch.float32) for u in self.uses}
         self.cmp_w = {u: (_dev_res(weights[u].compress.for_k), _dev_res(weights[u].compress.for_v))
-                      for u in USES}
+                      for u in self.uses}
         # per-use routing (local query order) and tiles
         self.rows, self.count, self.tiles, self.kmax = {}, {}, {}, {}
-        for use in USES:
+        for use in self.uses:
             qs, ks, ng = USE_GEOM[use]
             r, c = plan_rows[use]
             rb, cb = block_major_rows(r, c, parts[qs], parts[ks], ng == 3)
@@ -285,9 +290,10 @@ class SparseLayerEngine:
                     pool[key] = t
             return t
         for s in ("x", "y"):
-            m = self.meta[s]
-            self.buf[("Y", s)] = alloc(("Y", s), (m.n_loc, ncol[s]), torch.bfloat16)
-        for use in USES:
+            if ncol[s]:     # a one-use engine reads one stream only for a self use
+                m = self.meta[s]
+                self.buf[("Y", s)] = alloc(("Y", s), (m.n_loc, ncol[s]), torch.bfloat16)
+        for use in self.uses:
             qs, ks, _ = USE_GEOM[use]
             m = self.meta[ks]
             # global KV of this use (zeroed once: padding rows, their ones
@@ -327,7 +333,7 @@ class SparseLayerEngine:
         p = self.params
         jobs, self._job_refs = [], []
         max_blocks = 0
-        for use in USES:
+        for use in self.uses:
             _, ks, _ = USE_GEOM[use]
             m = self.meta[ks]
             if not m.n_loc:
@@ -425,7 +431,7 @@ class SparseLayerEngine:
                     costs.append(c)
                     codes.append((ui << 28) | (t * hkv + h))
 
-        for use in USES:
+        for use in self.uses:
             qs, ks, ng = USE_GEOM[use]
             mq = self.meta[qs]
             rows_h = D.host(self.rows[use])
@@ -499,7 +505,7 @@ class SparseLayerEngine:
         """Both streams' fused projections (q | gate logits + bias | k | v)
         as ONE grouped tcgen05 GEMM launch."""
         probs = [_ops.gemm_problem(a, self.w_cat[s], self.buf[("Y", s)], bias=self.b_cat[s])
-                 for s, a in (("x", x_loc), ("y", y_loc)) if self.meta[s].n_loc]
+                 for s, a in (("x", x_loc), ("y", y_loc)) if self.meta[s].n_loc and self.ncol[s]]
         if probs:
             _ops.gemm_tc(probs)
 
@@ -548,7 +554,7 @@ class SparseLayerEngine:
     def output_all(self):
         """The four uses' W_o projections as ONE grouped tcgen05 GEMM launch."""
         probs = [_ops.gemm_problem(self.buf[("merged", u)], self.w_o[u], self.buf[("out", u)])
-                 for u in USES if self.buf[("merged", u)].shape[0]]
+                 for u in self.uses if self.buf[("merged", u)].shape[0]]
         if probs:
             _ops.gemm_tc(probs)
 
@@ -564,7 +570,7 @@ class SparseLayerEngine:
         self.prepare_kv()
         self.attend_all()
         self.output_all()
-        return {u: self.buf[("out", u)] for u in USES}
+        return {u: self.buf[("out", u)] for u in self.uses}
 
     def forward_local(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
         """Sharded phase 1: projections and this rank's KV shards of all uses."""
@@ -575,13 +581,13 @@ class SparseLayerEngine:
         """Sharded phase 2: launch all four All-gather-KV exchanges (in flight
         while earlier uses attend), then per use wait + place + attend."""
         require(self.exchange is not None, "sharded engine needs an exchange (seq_parallel)")
-        handles = {use: self.exchange(self, use) for use in USES}
-        for use in USES:
+        handles = {use: self.exchange(self, use) for use in self.uses}
+        for use in self.uses:
             handles[use]()          # wait + place into the canonical layout
             self.finish_kv(use)
         self.attend_all()
         self.output_all()
-        return {u: self.buf[("out", u)] for u in USES}
+        return {u: self.buf[("out", u)] for u in self.uses}
 
     def capture(self, x_bm: torch.Tensor, y_bm: torch.Tensor):
         """Record one layer (all ~30 launches) as a CUDA graph over fixed
@@ -600,7 +606,7 @@ class SparseLayerEngine:
 
     def replay(self) -> dict:
         self.graph.replay()
-        return {u: self.buf[("out", u)] for u in USES}
+        return {u: self.buf[("out", u)] for u in self.uses}
 
     # -- accounting ------------------------------------------------------------
     def attention_flops(self) -> dict:
@@ -609,7 +615,7 @@ class SparseLayerEngine:
         masked keys)."""
         p = self.params
         out = {}
-        for use in USES:
+        for use in self.uses:
             qs, ks, ng = USE_GEOM[use]
             pk = self.meta[ks].part
             mq = self.meta[qs]
@@ -628,4 +634,4 @@ class SparseLayerEngine:
 
     def projection_flops(self) -> float:
         return sum(2.0 * self.meta[s].n_loc * self.d * self.ncol[s] for s in ("x", "y")) + \
-            sum(2.0 * self.meta[USE_GEOM[u][0]].n_loc * self.d * self.d for u in USES)
+            sum(2.0 * self.meta[USE_GEOM[u][0]].n_loc * self.d * self.d for u in self.uses)

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _dev as D
-from . import _ops
+from . import _ops, fastpath
 from ._native import call
 from .block_partition import (BlockPartition, CompressWeights, compress_block_kv,
                               init_compress_weights, compress_rows)
@@ -344,6 +344,10 @@ def nsa_cross_attention(x, kv_feats, part_q: BlockPartition, part_kv: BlockParti
     """One gated sparse attention use, fp32 (`nsa_attention.py:287-327`)."""
     d = params.model_dim
     require(x.shape[1] == d, f"query width {x.shape[1]} != model dim {d}")
+    if fastpath.active() and not return_selection:
+        r = fastpath.nsa_use(x, kv_feats, part_q, part_kv, sel, w, params, table)
+        if r is not None:
+            return r
     on_dev = D.is_device(x)
     xd = D.dev(x, torch.float32)
     kvd = D.dev(kv_feats, torch.float32)

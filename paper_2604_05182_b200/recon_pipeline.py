@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _dev as D
-from . import _ops
+from . import _ops, fastpath
 from ._native import call
 from .block_partition import BlockPartition
 from .engine import USE_GEOM, USES, SparseLayerEngine
@@ -200,6 +200,10 @@ def sparse_block_forward(x, y, x_inj, y_inj, w: SparseBlockWeights, ctx: SparseC
     """One sparse residual block (`recon_pipeline.py:461-497`), reference
     float contract. NumPy in -> NumPy out; CUDA tensors stay on the device."""
     require(x.shape[0] > 0 and y.shape[0] > 0, "sparse block needs nonempty token streams")
+    if fastpath.active():
+        r = fastpath.sparse_block(x, y, x_inj, y_inj, w, ctx, params)
+        if r is not None:
+            return r
     on_dev = D.is_device(x)
     xd, yd, xi, yi = (D.dev(a, torch.float32) for a in (x, y, x_inj, y_inj))
     xe, xh = _add_ln(xd, xi, w.ln_attn_x)
@@ -222,6 +226,10 @@ def sparse_block_forward(x, y, x_inj, y_inj, w: SparseBlockWeights, ctx: SparseC
 def sparse_stage_forward(x_up, y_up, weights, ctx: SparseContext, params: AttentionParams):
     """Residual stage (`recon_pipeline.py:500-512`): zero state, per-layer
     injections of the frozen inputs, inputs added back at the end."""
+    if fastpath.active():
+        r = fastpath.sparse_stage(x_up, y_up, weights, ctx, params)
+        if r is not None:
+            return r
     xf = D.dev(x_up.features, torch.float32)
     yf = D.dev(y_up.features, torch.float32)
     x, y = torch.zeros_like(xf), torch.zeros_like(yf)
@@ -249,9 +257,12 @@ class SparseBlockEngine:
     logits."""
 
     def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
-                 w: SparseBlockWeights, params: AttentionParams, pool: dict = None):
+                 w: SparseBlockWeights, params: AttentionParams, pool: dict = None,
+                 uses: dict = None):
+        # `uses`: use -> NsaWeights, for weight objects without `.uses()` (the
+        # reference's SparseBlockWeights, via the drop-in)
         self.w, self.params = w, params
-        self.layer = SparseLayerEngine(part_vol, part_img, plan_rows, w.uses(), params,
+        self.layer = SparseLayerEngine(part_vol, part_img, plan_rows, uses or w.uses(), params,
                                        extra_cols={"x": w.gate_x_w, "y": w.gate_y_w}, pool=pool)
         # FFN weights transposed ([n, k], K contiguous) for the tcgen05 GEMM
         self.bf = {name: D.dev(np.asarray(getattr(getattr(w, f), n)).T, torch.bfloat16)
@@ -595,10 +606,11 @@ class SparseStageEngine:
     state, per-layer injection of the frozen inputs, inputs added at the end."""
 
     def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
-                 weights: list, params: AttentionParams):
+                 weights: list, params: AttentionParams, uses: list = None):
         self.pool = {}
-        self.blocks = [SparseBlockEngine(part_vol, part_img, plan_rows, w, params, pool=self.pool)
-                       for w in weights]
+        uses = uses or [None] * len(weights)
+        self.blocks = [SparseBlockEngine(part_vol, part_img, plan_rows, w, params, pool=self.pool,
+                                         uses=u) for w, u in zip(weights, uses)]
         # injection weights transposed for the tcgen05 GEMM
         self.inj = [(D.dev(np.asarray(w.inj_x).T, torch.bfloat16),
                      D.dev(np.asarray(w.inj_y).T, torch.bfloat16)) for w in weights]
