@@ -566,6 +566,36 @@ int lsrm_decode_points(const float* grid, int s_df, const int64_t* sparse_index,
                        int64_t n, const float* const* head_w, int hidden, int z_channels,
                        float* z_out, float* s_out, float* field_out, void* stream);
 
+
+/* ---- sequence-parallel exchanges over NCCL (csrc/comm.cu) -----------------
+ * Replace the reference's simulated collectives `all_gather_kv`
+ * (lsrm/seq_parallel.py:181-218) and `all_to_all` (:146-178) with real
+ * NVLink transfers. NCCL is bound at run time (libnccl.so.2, the process's
+ * copy if one is loaded); every call is enqueued on `stream`. */
+
+/* 128-byte NCCL unique id, created on one rank and shared by the host. */
+int lsrm_comm_unique_id(uint8_t* id_out);
+/* Communicator of `world` ranks (one per GPU); *comm_out is opaque. */
+int lsrm_comm_init(const uint8_t* id, int world, int rank, void** comm_out);
+int lsrm_comm_destroy(void* comm);
+
+/* All-gather-KV of one NSA use: every rank's packed shard (`shard_bytes`,
+ * [k_il | v_il | k_cmp | v_cmp]) lands in `stage` at stage_off[r] (host
+ * array [world+1]); then for each of the n_dst canonical buffers dst[i]
+ * the placement segments segs[i] (device [n_segs[i], 3] int64, see
+ * lsrm_copy_segments) are applied. Grouped ncclSend/ncclRecv (all-gather-v). */
+int lsrm_allgather_kv(void* comm, int rank, int world, const void* shard,
+                      int64_t shard_bytes, void* stage, const int64_t* stage_off,
+                      const int64_t* const* segs, const int64_t* n_segs,
+                      void* const* dst, int n_dst, void* stream);
+
+/* all-to-all-v of bytes: send_bytes[p] (host) from `send` (consecutive per
+ * peer) to peer p, recv_bytes[p] from peer p into `recv` (consecutive per
+ * peer). Token dispatch / return of the sharded stage. */
+int lsrm_all_to_all_v(void* comm, int rank, int world, const void* send,
+                      const int64_t* send_bytes, void* recv, const int64_t* recv_bytes,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

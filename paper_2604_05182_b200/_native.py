@@ -95,6 +95,11 @@ SIGNATURES = {
     "lsrm_affine_exact": (I32, [P, I64, I64, I32, P, P, I32, I32, P, I64, P]),
     "lsrm_gemm_tc": (I32, [P, I32, P]),
     "lsrm_compact_rows": (I32, [I32, P, I64, I64, I32, I32, I32, P, I32, P, P, P, P, P, P]),
+    "lsrm_comm_unique_id": (I32, [P]),
+    "lsrm_comm_init": (I32, [P, I32, I32, P]),
+    "lsrm_comm_destroy": (I32, [P]),
+    "lsrm_allgather_kv": (I32, [P, I32, I32, P, I64, P, P, P, P, P, I32, P]),
+    "lsrm_all_to_all_v": (I32, [P, I32, I32, P, P, P, P, P]),
 }
 
 _lib = None

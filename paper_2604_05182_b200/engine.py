@@ -332,6 +332,7 @@ class SparseLayerEngine:
         """Device array of `lsrm_kv_job`: K and V of every use (one launch)."""
         p = self.params
         jobs, self._job_refs = [], []
+        job_stream = []          # KV stream of each job (per-stream launches)
         max_blocks = 0
         for use in self.uses:
             _, ks, _ = USE_GEOM[use]
@@ -372,9 +373,17 @@ class SparseLayerEngine:
                                   arrive.data_ptr()))
                 self._job_refs += [src, il, blk, pad, mean, cmp_il, work_d, partial, arrive]
                 max_blocks = max(max_blocks, int(work.size))
-        raw = b"".join(C.string_at(C.addressof(j), C.sizeof(j)) for j in jobs)
-        self.kv_jobs = D.dev(np.frombuffer(raw, dtype=np.uint8).copy()) if jobs else None
-        self.n_kv_jobs, self.kv_max_blocks = len(jobs), max_blocks
+                job_stream.append((ks, int(work.size)))
+
+        def pack(sel):
+            js = [j for j, (ks, _) in zip(jobs, job_stream) if ks in sel]
+            mb = max([nb for ks, nb in job_stream if ks in sel], default=0)
+            raw = b"".join(C.string_at(C.addressof(j), C.sizeof(j)) for j in js)
+            return (D.dev(np.frombuffer(raw, dtype=np.uint8).copy()) if js else None, len(js), mb)
+        self.kv_jobs, self.n_kv_jobs, self.kv_max_blocks = pack(("x", "y"))
+        # per KV stream (sharded engines start a stream's exchanges while the
+        # other stream is still being projected)
+        self.kv_jobs_of = {s: pack((s,)) for s in ("x", "y")}
 
     def _build_attention_queue(self):
         """The four uses' attention as heaviest-first item queues. An item is
@@ -501,21 +510,25 @@ class SparseLayerEngine:
                  int(order.shape[0]), counter.data_ptr(), D.stream())
 
     # -- pieces --------------------------------------------------------------
-    def project(self, x_loc: torch.Tensor, y_loc: torch.Tensor):
-        """Both streams' fused projections (q | gate logits + bias | k | v)
+    def project(self, x_loc: torch.Tensor, y_loc: torch.Tensor, streams=("x", "y")):
+        """The streams' fused projections (q | gate logits + bias | k | v)
         as ONE grouped tcgen05 GEMM launch."""
         probs = [_ops.gemm_problem(a, self.w_cat[s], self.buf[("Y", s)], bias=self.b_cat[s])
-                 for s, a in (("x", x_loc), ("y", y_loc)) if self.meta[s].n_loc and self.ncol[s]]
+                 for s, a in (("x", x_loc), ("y", y_loc))
+                 if s in streams and self.meta[s].n_loc and self.ncol[s]]
         if probs:
             _ops.gemm_tc(probs)
 
-    def prepare_kv(self):
-        """K/V of all four uses in one launch (owned KV blocks when sharded;
-        unsharded engines write the global buffers, compressed rows included)."""
-        if self.n_kv_jobs:
+    def prepare_kv(self, stream: str = None):
+        """K/V of all four uses in one launch, or of the uses whose KV side is
+        `stream` (owned KV blocks when sharded; unsharded engines write the
+        global buffers, compressed rows included)."""
+        jobs, n, mb = (self.kv_jobs, self.n_kv_jobs, self.kv_max_blocks) if stream is None \
+            else self.kv_jobs_of[stream]
+        if n:
             p = self.params
-            call("lsrm_kv_prepare_jobs", self.kv_jobs.data_ptr(), self.n_kv_jobs,
-                 self.kv_max_blocks, p.n_kv_heads, p.head_dim, D.stream())
+            call("lsrm_kv_prepare_jobs", jobs.data_ptr(), n, mb, p.n_kv_heads, p.head_dim,
+                 D.stream())
 
     def finish_kv(self, use: str):
         """Compressed rows (global, canonical order) -> interleaved layout."""
@@ -564,8 +577,7 @@ class SparseLayerEngine:
         rank-local compact order when sharded) -> dict use -> [Nq_loc, d] bf16.
         Output buffers are reused across calls."""
         if self.sharded:
-            self.forward_local(x_loc, y_loc)
-            return self.forward_exchange()
+            return self.forward_overlapped(x_loc, y_loc)
         self.project(x_loc, y_loc)
         self.prepare_kv()
         self.attend_all()
@@ -578,16 +590,38 @@ class SparseLayerEngine:
         self.prepare_kv()
 
     def forward_exchange(self) -> dict:
-        """Sharded phase 2: launch all four All-gather-KV exchanges (in flight
-        while earlier uses attend), then per use wait + place + attend."""
+        """Sharded phase 2: launch all four All-gather-KV exchanges, then per
+        use wait + place, then attend."""
         require(self.exchange is not None, "sharded engine needs an exchange (seq_parallel)")
         handles = {use: self.exchange(self, use) for use in self.uses}
+        return self._finish_exchange(handles)
+
+    def _finish_exchange(self, handles) -> dict:
         for use in self.uses:
             handles[use]()          # wait + place into the canonical layout
             self.finish_kv(use)
         self.attend_all()
         self.output_all()
         return {u: self.buf[("out", u)] for u in self.uses}
+
+    def uses_with_kv(self, stream: str):
+        return [u for u in self.uses if USE_GEOM[u][1] == stream]
+
+    def forward_overlapped(self, x_loc: torch.Tensor, y_loc: torch.Tensor) -> dict:
+        """Sharded layer with the exchange overlapped: project + prepare the
+        x stream's KV, start the exchanges of the uses that read it (v2v,
+        i2v; the transport runs them on its own stream), then project +
+        prepare the y stream while they are in flight, start v2i / i2i, and
+        only then wait, place and attend (`lsrm/seq_parallel.py:298-311`:
+        window attention and compression are local; only KV moves)."""
+        require(self.exchange is not None, "sharded engine needs an exchange (seq_parallel)")
+        handles = {}
+        for s in ("x", "y"):
+            self.project(x_loc, y_loc, streams=(s,))
+            self.prepare_kv(s)
+            for use in self.uses_with_kv(s):
+                handles[use] = self.exchange(self, use)
+        return self._finish_exchange(handles)
 
     def capture(self, x_bm: torch.Tensor, y_bm: torch.Tensor):
         """Record one layer (all ~30 launches) as a CUDA graph over fixed

@@ -258,12 +258,15 @@ class SparseBlockEngine:
 
     def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
                  w: SparseBlockWeights, params: AttentionParams, pool: dict = None,
-                 uses: dict = None):
+                 uses: dict = None, shard: dict = None):
         # `uses`: use -> NsaWeights, for weight objects without `.uses()` (the
-        # reference's SparseBlockWeights, via the drop-in)
+        # reference's SparseBlockWeights, via the drop-in). `shard`: owned
+        # occupied rows per stream (sequence parallelism; every row-local
+        # step then runs on the owned tokens in the rank-local order)
         self.w, self.params = w, params
         self.layer = SparseLayerEngine(part_vol, part_img, plan_rows, uses or w.uses(), params,
-                                       extra_cols={"x": w.gate_x_w, "y": w.gate_y_w}, pool=pool)
+                                       extra_cols={"x": w.gate_x_w, "y": w.gate_y_w}, pool=pool,
+                                       shard=shard)
         # FFN weights transposed ([n, k], K contiguous) for the tcgen05 GEMM
         self.bf = {name: D.dev(np.asarray(getattr(getattr(w, f), n)).T, torch.bfloat16)
                    for name, f, n in (("fx1", "ffn_x", "w1"), ("fx2", "ffn_x", "w2"),
@@ -606,16 +609,18 @@ class SparseStageEngine:
     state, per-layer injection of the frozen inputs, inputs added at the end."""
 
     def __init__(self, part_vol: BlockPartition, part_img: BlockPartition, plan_rows: dict,
-                 weights: list, params: AttentionParams, uses: list = None):
+                 weights: list, params: AttentionParams, uses: list = None,
+                 shard: dict = None):
         self.pool = {}
         uses = uses or [None] * len(weights)
         self.blocks = [SparseBlockEngine(part_vol, part_img, plan_rows, w, params, pool=self.pool,
-                                         uses=u) for w, u in zip(weights, uses)]
+                                         uses=u, shard=shard) for w, u in zip(weights, uses)]
         # injection weights transposed for the tcgen05 GEMM
         self.inj = [(D.dev(np.asarray(w.inj_x).T, torch.bfloat16),
                      D.dev(np.asarray(w.inj_y).T, torch.bfloat16)) for w in weights]
 
-    def forward(self, x_up: torch.Tensor, y_up: torch.Tensor):
+    def forward(self, x_up: torch.Tensor, y_up: torch.Tensor, out=None):
+        """out: optional (x_s, y_s) f32 buffers to write the stage output to."""
         xb, yb = _ops.cast(x_up, torch.bfloat16), _ops.cast(y_up, torch.bfloat16)
         x, y = torch.zeros_like(x_up), torch.zeros_like(y_up)
         xi = D.empty(tuple(x_up.shape), torch.float32)
@@ -625,5 +630,6 @@ class SparseStageEngine:
                           if a.shape[0]])
             x, y = blk.forward(x, y, xi, yi)
         zero = torch.zeros(x_up.shape[1], dtype=torch.float32, device=x_up.device)
-        return (_bias_act(0, x, zero, 0, residual=x_up, out_dtype=torch.float32),
-                _bias_act(0, y, zero, 0, residual=y_up, out_dtype=torch.float32))
+        ox, oy = out if out is not None else (None, None)
+        return (_bias_act(0, x, zero, 0, residual=x_up, out=ox, out_dtype=torch.float32),
+                _bias_act(0, y, zero, 0, residual=y_up, out=oy, out_dtype=torch.float32))

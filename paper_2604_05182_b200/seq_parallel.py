@@ -421,6 +421,92 @@ class NcclTransport:
                 r.wait()
         return wait
 
+    def all_to_all_v(self, sends, recvs):
+        """sends[p] -> peer p, recvs[p] <- peer p (own chunk copied); grouped
+        NCCL send/recv, stream-ordered. Returns the wait callable."""
+        import torch.distributed as dist
+        if sends[self.rank].numel():
+            recvs[self.rank].copy_(sends[self.rank])
+        ops = []
+        for peer in range(self.world):
+            if peer == self.rank:
+                continue
+            if sends[peer].numel():
+                ops.append(dist.P2POp(dist.isend, sends[peer], peer, group=self.group))
+            if recvs[peer].numel():
+                ops.append(dist.P2POp(dist.irecv, recvs[peer], peer, group=self.group))
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+
+        def wait():
+            for r in reqs:
+                r.wait()
+        return wait
+
+
+class CapiNcclTransport:
+    """The same exchanges through this library's own C ABI
+    (`lsrm_allgather_kv` / `lsrm_all_to_all_v`, csrc/comm.cu): a
+    non-Python host's path. The communicator is created by the library
+    (the NCCL unique id is shared over the existing process group); the
+    transfers run on a side stream that waits for the producer, and the
+    returned wait makes the caller's stream wait for them, so they overlap
+    whatever the caller enqueues in between."""
+
+    def __init__(self, rank, world, group=None):
+        import ctypes
+        import torch.distributed as dist
+        from ._native import call
+        self.rank, self.world = rank, world
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            call("lsrm_comm_unique_id", ctypes.addressof(uid))
+        obj = [bytes(uid)]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        comm = ctypes.c_void_p()
+        call("lsrm_comm_init", ctypes.addressof(uid), world, rank, ctypes.byref(comm))
+        self.comm = comm
+        self.side = torch.cuda.Stream()
+
+    def close(self):
+        from ._native import call
+        if self.comm:
+            call("lsrm_comm_destroy", self.comm)
+            self.comm = None
+
+    def _launch(self, tensors, fn):
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        for t in tensors:
+            t.record_stream(self.side)
+        with torch.cuda.stream(self.side):
+            fn(self.side.cuda_stream)
+        side = self.side
+        return lambda: torch.cuda.current_stream().wait_stream(side)
+
+    def __call__(self, send: torch.Tensor, slots):
+        import ctypes
+        from ._native import call
+        base = slots[0].data_ptr()
+        offs = [s_.data_ptr() - base for s_ in slots] + \
+            [slots[-1].data_ptr() - base + slots[-1].numel() * slots[-1].element_size()]
+        off_arr = (ctypes.c_int64 * len(offs))(*offs)
+        nbytes = send.numel() * send.element_size()
+        return self._launch([send] + list(slots), lambda st: call(
+            "lsrm_allgather_kv", self.comm, self.rank, self.world, send.data_ptr(), nbytes,
+            base, off_arr, None, None, None, 0, st))
+
+    def all_to_all_v(self, sends, recvs):
+        import ctypes
+        from ._native import call
+        sb = (ctypes.c_int64 * self.world)(*[t.numel() * t.element_size() for t in sends])
+        rb = (ctypes.c_int64 * self.world)(*[t.numel() * t.element_size() for t in recvs])
+        s0 = next((t.data_ptr() for t in sends if t.numel()), 0)
+        r0 = next((t.data_ptr() for t in recvs if t.numel()), 0)
+        return self._launch([t for t in sends + recvs if t.numel()], lambda st: call(
+            "lsrm_all_to_all_v", self.comm, self.rank, self.world, s0, sb, r0, rb, st))
+
 
 class InProcessTransport:
     """Emulates W ranks inside one process (single-GPU tests): every
@@ -460,6 +546,27 @@ class HostStagedTransport:
             r.wait()
         for sl, h in zip(slots, recv):
             sl.copy_(h)
+        return lambda: None
+
+    def all_to_all_v(self, sends, recvs):
+        """Blocking all_to_all_v through host memory (gloo)."""
+        import torch.distributed as dist
+        hs = [t.cpu() for t in sends]
+        hr = [torch.empty(tuple(t.shape), dtype=t.dtype) for t in recvs]
+        hr[self.rank] = hs[self.rank]
+        ops = []
+        for peer in range(self.world):
+            if peer == self.rank:
+                continue
+            if hs[peer].numel():
+                ops.append(dist.P2POp(dist.isend, hs[peer], peer, group=self.group))
+            if hr[peer].numel():
+                ops.append(dist.P2POp(dist.irecv, hr[peer], peer, group=self.group))
+        for r in (dist.batch_isend_irecv(ops) if ops else []):
+            r.wait()
+        for t, h in zip(recvs, hr):
+            if t.numel():
+                t.copy_(h)
         return lambda: None
 
 
@@ -570,7 +677,8 @@ class ShardedLayer:
         self.engine.output_all()
 
     def capture(self, x_loc, y_loc):
-        """Record graphs A and B over fixed input buffers x_loc, y_loc."""
+        """Record graphs A_x, A_y (one stream's projections + KV shards
+        each) and B (placement + attention + W_o) over fixed input buffers."""
         self._gin = (x_loc, y_loc)
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
@@ -578,19 +686,25 @@ class ShardedLayer:
             self.forward(x_loc, y_loc)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
-        ga, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(ga):
-            self.engine.forward_local(x_loc, y_loc)
+        ga = {s: torch.cuda.CUDAGraph() for s in ("x", "y")}
+        gb = torch.cuda.CUDAGraph()
+        for s in ("x", "y"):
+            with torch.cuda.graph(ga[s]):
+                self.engine.project(x_loc, y_loc, streams=(s,))
+                self.engine.prepare_kv(s)
         with torch.cuda.graph(gb):
             self._phase_b()
         self.graphs = (ga, gb)
 
     def step(self) -> dict:
-        """Graph A -> four exchanges (all in flight) -> graph B."""
+        """A_x -> start the exchanges of the uses that read x as KV (v2v,
+        i2v) -> A_y (overlaps them) -> start v2i, i2i -> wait -> B."""
         from .engine import USES
         ga, gb = self.graphs
-        ga.replay()
-        waits = [self.exchange.start(u) for u in USES]
+        waits = []
+        for s in ("x", "y"):
+            ga[s].replay()
+            waits += [self.exchange.start(u) for u in self.engine.uses_with_kv(s)]
         for w in waits:
             w()
         gb.replay()
@@ -651,3 +765,209 @@ class ShardedLayer:
         h2d = (xs.numel() + ys.numel()) * 4
         d2h = sum(p.numel() * 4 for p in pinned.values())
         return a.elapsed_time(b) / steps, h2d, d2h
+
+
+# ---------------------------------------------------------------------------
+# dispatch / return (token all_to_all_v) and the sharded Stage-2 stage
+
+
+def plan_rows_lengths(part_vol, part_img, plan_rows) -> dict:
+    """Routed key count L_i per query (token order) of every use."""
+    lengths = {}
+    for use, (rows, cnt) in plan_rows.items():
+        pk = part_vol if use[2] == "v" else part_img
+        r, c = D.host(rows), D.host(cnt)
+        occ = pk.occupancy.astype(np.float64)
+        mask = np.arange(r.shape[1])[None, :] < c[:, None]
+        lengths[use] = np.where(mask, occ[np.clip(r, 0, None)], 0.0).sum(axis=1)
+    return lengths
+
+
+class TokenDispatch:
+    """The stage's two all-to-alls on the device (`lsrm/seq_parallel.py:
+    341-349` dispatch, `:431-433` return): token rows move between the naive
+    contiguous shards of the concatenated [volume; image] sequence
+    (`naive_contiguous_shards`, the layout the stage starts and ends in) and
+    the block-aligned owners of the topology.
+
+    Rank-local order on an owner = its owned volume tokens then its owned
+    image tokens, each in block-major order of the owned blocks (the order of
+    `engine.stream_meta(part, owned)`). Every message s -> d carries the
+    tokens of s's naive shard that d owns, in d's local order, so one gather
+    (sender) and one scatter (receiver) per tensor place every row.
+    `messages()` gives the (src, dst, tokens) list the reference logs."""
+
+    def __init__(self, part_vol, part_img, topology: WorkerTopology, rank: int, world: int):
+        n_x, n_y = part_vol.n_tokens, part_img.n_tokens
+        self.rank, self.world, self.n_x = rank, world, n_x
+        naive = naive_contiguous_shards(n_x + n_y, world)
+        edges = np.concatenate([[0], np.cumsum([a.size for a in naive])]).astype(np.int64)
+        self.naive = naive
+        local = []
+        for r in range(world):
+            tx = np.concatenate([part_vol.tokens_in_row(b) for b in topology.vol_rows[r]]) \
+                if len(topology.vol_rows[r]) else np.zeros(0, np.int64)
+            ty = np.concatenate([part_img.tokens_in_row(b) for b in topology.img_rows[r]]) \
+                if len(topology.img_rows[r]) else np.zeros(0, np.int64)
+            local.append((tx.astype(np.int64), ty.astype(np.int64) + n_x))
+        self.n_loc_x, self.n_loc_y = local[rank][0].size, local[rank][1].size
+        # message (src -> dst) token lists in dst's local order
+        self.msg = {}
+        for d in range(world):
+            seq = np.concatenate(local[d])
+            src = np.searchsorted(edges, seq, side="right") - 1
+            pos = np.arange(seq.size)
+            for s_ in range(world):
+                m = src == s_
+                self.msg[(s_, d)] = (seq[m], pos[m])      # tokens, dst-local positions
+        r = rank
+        self.send_counts = [self.msg[(r, d)][0].size for d in range(world)]
+        self.recv_counts = [self.msg[(s_, r)][0].size for s_ in range(world)]
+        lo = int(edges[r])
+        self.send_index = np.concatenate([self.msg[(r, d)][0] - lo for d in range(world)]
+                                         ).astype(np.int64)
+        self.recv_index = np.concatenate([self.msg[(s_, r)][1] for s_ in range(world)]
+                                         ).astype(np.int64)
+        self.n_naive = int(naive[r].size)
+        self.n_local = self.n_loc_x + self.n_loc_y
+        self.local_tokens = np.concatenate(local[r])
+        self._dev = None
+
+    def messages(self):
+        """[(src, dst, n_tokens)] for src != dst with tokens to move."""
+        return [(s_, d, int(self.msg[(s_, d)][0].size)) for s_ in range(self.world)
+                for d in range(self.world) if s_ != d and self.msg[(s_, d)][0].size]
+
+    def log(self, topology: WorkerTopology, phase: str, bytes_per_token: int, reverse=False):
+        for s_, d, n in self.messages():
+            a, b = (d, s_) if reverse else (s_, d)
+            topology.log(phase, "all_to_all", a, b, n * bytes_per_token)
+
+    @staticmethod
+    def _chunks(t, counts):
+        out, o = [], 0
+        for c in counts:
+            out.append(t[o:o + c])
+            o += c
+        return out
+
+    def _indices(self):
+        if self._dev is None:
+            self._dev = (D.dev(self.send_index), D.dev(self.recv_index))
+        return self._dev
+
+    def dispatch(self, transport, tensors, outs, gather=None, scatter=None):
+        """tensors: this rank's naive-shard rows ([n_naive, ...] each);
+        outs: [n_local, ...] buffers in the rank-local order. One gather, one
+        all_to_all_v and one scatter per tensor."""
+        from . import _ops
+        gather = gather or _ops.gather_rows
+        scatter = scatter or _ops.scatter_rows
+        si, ri = self._indices() if tensors[0].is_cuda else (torch.from_numpy(self.send_index),
+                                                            torch.from_numpy(self.recv_index))
+        waits, recvs = [], []
+        for t, o in zip(tensors, outs):
+            send = gather(t, si)
+            recv = torch.empty((int(sum(self.recv_counts)),) + tuple(t.shape[1:]), dtype=t.dtype,
+                               device=t.device)
+            waits.append(transport.all_to_all_v(self._chunks(send, self.send_counts),
+                                                self._chunks(recv, self.recv_counts)))
+            recvs.append((recv, o))
+        for w in waits:
+            w()
+        for recv, o in recvs:
+            if recv.shape[0]:
+                scatter(recv, ri, o)
+        return outs
+
+    def gather_back(self, transport, tensors, outs, gather=None, scatter=None):
+        """The return all-to-all: rank-local rows -> naive-shard rows."""
+        from . import _ops
+        gather = gather or _ops.gather_rows
+        scatter = scatter or _ops.scatter_rows
+        si, ri = self._indices() if tensors[0].is_cuda else (torch.from_numpy(self.send_index),
+                                                            torch.from_numpy(self.recv_index))
+        waits, recvs = [], []
+        for t, o in zip(tensors, outs):
+            send = gather(t, ri)          # local rows, grouped by naive owner
+            recv = torch.empty((int(sum(self.send_counts)),) + tuple(t.shape[1:]), dtype=t.dtype,
+                               device=t.device)
+            waits.append(transport.all_to_all_v(self._chunks(send, self.recv_counts),
+                                                self._chunks(recv, self.send_counts)))
+            recvs.append((recv, o))
+        for w in waits:
+            w()
+        for recv, o in recvs:
+            if recv.shape[0]:
+                scatter(recv, si, o)
+        return outs
+
+
+class ShardedStage:
+    """One rank of the block-aware sequence-parallel Stage-2 stage
+    (`lsrm/seq_parallel.py:321-434`) on the bf16 engines:
+
+      dispatch (all_to_all_v of features + coords, naive shard -> owners)
+      -> depth x sharded `SparseBlockEngine` (row-local injection / LN /
+         gates / FFN on the owned tokens; per NSA use one All-gather-KV,
+         started per KV stream while the other stream is still projected)
+      -> return (all_to_all_v, owners -> naive shard).
+
+    Every output row is computed by the same tiles from byte-identical
+    canonical KV whatever W is, so the result is bit-equal to the
+    single-GPU `SparseStageEngine` (tests/sp_stage_worker.py). The message
+    log follows the reference protocol (dispatch / layer m use / return)."""
+
+    def __init__(self, part_vol, part_img, plan_rows, weights, params, rank: int, world: int,
+                 topology: WorkerTopology = None, transport=None, by_cost: bool = True):
+        from .recon_pipeline import SparseStageEngine
+        self.rank, self.world, self.params = rank, world, params
+        if topology is None:
+            if by_cost:
+                cv, ci = block_costs(part_vol, part_img,
+                                     plan_rows_lengths(part_vol, part_img, plan_rows))
+                topology = shard_blocks_by_cost(part_vol, part_img, world, cv, ci)
+            else:
+                topology = shard_blocks(part_vol, part_img, world)
+        self.topology = topology
+        self.transport = transport or NcclTransport(rank, world)
+        shards = {"x": topology.vol_rows, "y": topology.img_rows}
+        self.stage = SparseStageEngine(part_vol, part_img, plan_rows, weights, params,
+                                       shard={"x": shards["x"][rank], "y": shards["y"][rank]})
+        for m, blk in enumerate(self.stage.blocks):
+            ex = KVExchange(blk.layer, rank, world, shards, transport=self.transport,
+                            topology=topology)
+            ex.layer_index = m
+            blk.layer.exchange = ex
+        self.tokens = TokenDispatch(part_vol, part_img, topology, rank, world)
+        d = params.model_dim
+        self.bytes_per_token = 4 * d + TOKEN_COORD_BYTES
+        tk = self.tokens
+        self.x_loc = D.empty((tk.n_loc_x, d), torch.float32)
+        self.y_loc = D.empty((tk.n_loc_y, d), torch.float32)
+        self._loc = D.empty((tk.n_local, d), torch.float32)
+        self._coords = D.empty((tk.n_local, 3), torch.int32)
+        self._out = D.empty((tk.n_local, d), torch.float32)
+
+    def forward(self, feats_naive: torch.Tensor, coords_naive: torch.Tensor) -> torch.Tensor:
+        """feats_naive [n_naive, d] f32 and coords_naive [n_naive, 3] int32:
+        this rank's naive contiguous shard of the concatenated [volume;
+        image] tokens. Returns the stage output rows of the same shard."""
+        tk, d = self.tokens, self.params.model_dim
+        tk.dispatch(self.transport, [feats_naive, coords_naive], [self._loc, self._coords])
+        tk.log(self.topology, "dispatch", self.bytes_per_token)
+        nx = tk.n_loc_x
+        self.stage.forward(self._loc[:nx], self._loc[nx:],
+                           out=(self._out[:nx], self._out[nx:]))
+        for m, blk in enumerate(self.stage.blocks):
+            self._log_window(m)
+        out = D.empty((tk.n_naive, d), torch.float32)
+        tk.gather_back(self.transport, [self._out], [out])
+        tk.log(self.topology, "return", self.bytes_per_token, reverse=True)
+        return out
+
+    def _log_window(self, m):
+        """Zero-byte window entries of the self uses (`seq_parallel.py:311`)."""
+        for name, toks in (("v2v", self.topology.vol_tokens), ("i2i", self.topology.img_tokens)):
+            if toks[self.rank].size:
+                self.topology.log(f"layer{m}/{name}/win", "window", self.rank, self.rank, 0)

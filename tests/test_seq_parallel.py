@@ -328,6 +328,96 @@ def test_gloo_world2_all_gather_kv():
 
 
 # ---------------------------------------------------------------------------
+# dispatch / return all_to_all_v (TokenDispatch): plan + gloo world 2
+
+
+def _cpu_gather(src, index, out=None):
+    return src[index]
+
+
+def _cpu_scatter(src, index, out):
+    out[index] = src
+    return out
+
+
+@pytest.mark.parametrize("W", [2, 3, 8])
+def test_token_dispatch_plan_matches_reference_accounting(c1_parts, W):
+    """The device dispatch moves exactly the reference's all_to_all messages
+    (`seq_parallel.py:146-178`, dispatch phase of `parallel_sparse_stage`)
+    and its index arrays tile the naive and local orders."""
+    pv, pi = c1_parts
+    topo = S.shard_blocks(pv, pi, W)
+    n = pv.n_tokens + pi.n_tokens
+    aligned = [np.concatenate([topo.vol_tokens[w], topo.img_tokens[w] + pv.n_tokens])
+               for w in range(W)]
+    naive = S.naive_contiguous_shards(n, W)
+    ref = S.WorkerTopology(W, [], [], [], [], np.zeros(W, np.int64))
+    S.all_to_all(naive, aligned, ref, "dispatch", 4 * 64 + 12)
+    dev = S.WorkerTopology(W, [], [], [], [], np.zeros(W, np.int64))
+    plans = [S.TokenDispatch(pv, pi, topo, r, W) for r in range(W)]
+    plans[0].log(dev, "dispatch", 4 * 64 + 12)
+    assert dev.message_log == ref.message_log
+    for r, p in enumerate(plans):
+        assert sorted(p.send_index.tolist()) == list(range(naive[r].size))
+        assert sorted(p.recv_index.tolist()) == list(range(p.n_local))
+        assert np.array_equal(np.sort(p.local_tokens), np.sort(aligned[r]))
+        assert sum(p.send_counts) == naive[r].size
+        assert [q.recv_counts[r] for q in plans] == p.send_counts
+
+
+def _dispatch_worker(rank, world, port, result):
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        from paper_2604_05182_b200.workloads import coarse_inputs
+        from fixtures import load_workload
+        wl = load_workload("c1")
+        x_d, y_d, pe_v, pe_i = coarse_inputs(wl, 64)
+        x_up, y_up = O.upsample_select_tokens(x_d, y_d, wl.vol_mask, wl.img_mask, pe_v.tables,
+                                              pe_i.tables, wl.factor_vol, wl.factor_img)
+        pv = O.partition_tokens("volume", x_up.coords, x_up.grid_res)
+        pi = O.partition_tokens("image", y_up.coords, y_up.grid_res)
+        topo = S.shard_blocks(pv, pi, world)
+        feats = torch.from_numpy(np.concatenate([x_up.features, y_up.features]))
+        coords = torch.from_numpy(np.concatenate([x_up.coords, y_up.coords]).astype(np.int32))
+        tk = S.TokenDispatch(pv, pi, topo, rank, world)
+        lo = int(np.concatenate([[0], np.cumsum([a.size for a in tk.naive])])[rank])
+        mine = slice(lo, lo + tk.n_naive)
+        loc_f = torch.zeros((tk.n_local, 64))
+        loc_c = torch.zeros((tk.n_local, 3), dtype=torch.int32)
+        tr = S.HostStagedTransport(rank, world)
+        tk.dispatch(tr, [feats[mine], coords[mine]], [loc_f, loc_c], _cpu_gather, _cpu_scatter)
+        ok = torch.equal(loc_f, feats[tk.local_tokens]) and \
+            torch.equal(loc_c, coords[tk.local_tokens])
+        back = torch.zeros((tk.n_naive, 64))
+        tk.gather_back(tr, [loc_f * 2.0], [back], _cpu_gather, _cpu_scatter)
+        ok = ok and torch.equal(back, feats[mine] * 2.0)
+        result[rank] = bool(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_token_dispatch_round_trip():
+    """dispatch -> (local op) -> return over a real gloo world of 2: every
+    rank receives exactly its owned tokens in local order and gets its naive
+    shard back."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    with ctx.Manager() as mgr:
+        result = mgr.dict()
+        procs = [ctx.Process(target=_dispatch_worker, args=(r, 2, port, result))
+                 for r in range(2)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(timeout=180)
+        assert all(p.exitcode == 0 for p in procs)
+        assert dict(result) == {0: True, 1: True}
+
+
+# ---------------------------------------------------------------------------
 # GPU: emulated ranks reproduce the single-GPU engine
 
 
@@ -392,3 +482,60 @@ def test_torchrun_ranks_share_one_gpu(cuda, W):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W", [2, 3])
+def test_torchrun_sharded_stage(cuda, W):
+    """Dispatch -> 2 sharded Stage-2 blocks (per-use All-gather-KV) -> return
+    on W torchrun ranks sharing one GPU (gloo, host-staged): bit-equal to the
+    single-GPU stage (tests/sp_stage_worker.py)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={W}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "tests", "sp_stage_worker.py"), "c1", "2"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
+
+
+@pytest.mark.gpu
+def test_capi_nccl_transport_world1(cuda):
+    """The C-ABI NCCL exchanges (`lsrm_allgather_kv`, `lsrm_all_to_all_v`)
+    through CapiNcclTransport on a one-rank communicator (this box has one
+    GPU; NCCL refuses two ranks on one device), and the sharded stage on it:
+    bit-equal to the single-GPU stage."""
+    from paper_2604_05182_b200 import _dev as D, _ops
+    from paper_2604_05182_b200.layer import build_instance
+    from paper_2604_05182_b200.recon_pipeline import SparseStageEngine, init_sparse_block
+    from paper_2604_05182_b200.tensor_core import AttentionParams
+    tr = S.CapiNcclTransport(0, 1)
+    try:
+        send = torch.arange(4096, dtype=torch.int32, device="cuda").view(torch.uint8)
+        stage = torch.zeros_like(send)
+        tr(send, [stage])()
+        assert torch.equal(stage, send)
+        recv = torch.zeros_like(send)
+        tr.all_to_all_v([send], [recv])()
+        assert torch.equal(recv, send)
+        params = AttentionParams(32, 2, 32)
+        inst = build_instance("c1", params=params)
+        ws = [init_sparse_block(0, params, m) for m in range(2)]
+        st = S.ShardedStage(inst.part_vol, inst.part_img, inst.plan_rows, ws, params, 0, 1,
+                            transport=tr)
+        feats = np.concatenate([inst.x_hat, inst.y_hat]).astype(np.float32)
+        coords = np.zeros((feats.shape[0], 3), np.int32)
+        out = D.host(st.forward(D.dev(feats), D.dev(coords)))
+        ref_eng = SparseStageEngine(inst.part_vol, inst.part_img, inst.plan_rows, ws, params)
+        tv, ti = inst.part_vol.dev("block_token_ids"), inst.part_img.dev("block_token_ids")
+        xs, ys = ref_eng.forward(_ops.gather_rows(D.dev(inst.x_hat), tv),
+                                 _ops.gather_rows(D.dev(inst.y_hat), ti))
+        xo, yo = torch.empty_like(xs), torch.empty_like(ys)
+        _ops.scatter_rows(xs, tv, xo)
+        _ops.scatter_rows(ys, ti, yo)
+        ref = np.concatenate([D.host(xo), D.host(yo)])
+        assert np.array_equal(out, ref)
+    finally:
+        tr.close()
