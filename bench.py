@@ -875,6 +875,38 @@ def run_sp(args):
     h2d_all, d2h_all = sum_all(h2d), sum_all(d2h)
     launches = int(sum_all(per_step_launches * args.steps))
     loads = np.asarray(sl.topology.loads, np.float64)
+    # NVLink bytes of the All-gather-KV: every rank sends its packed shard
+    # [k_il | v_il | k_cmp | v_cmp] of every use to every other rank
+    sent = sum(int(sl.exchange.packed[u].numel()) for u in sl.exchange.packed) * (ws - 1)
+    sent_all = sum_all(sent)
+    # the whole sequence-parallel stage (dispatch -> depth blocks -> return)
+    sp_stage = None
+    if args.sp_stage_depth > 0:
+        from paper_2604_05182_b200.recon_pipeline import init_sparse_block
+        wts = [init_sparse_block(0, inst.params, m) for m in range(args.sp_stage_depth)]
+        stg = S.ShardedStage(inst.part_vol, inst.part_img, inst.plan_rows, wts, inst.params,
+                             rank, ws, topology=sl.topology, transport=transport)
+        tk = stg.tokens
+        lo = int(np.concatenate([[0], np.cumsum([a.size for a in tk.naive])])[rank])
+        feats = np.concatenate([inst.x_hat, inst.y_hat])[lo:lo + tk.n_naive]
+        from paper_2604_05182_b200 import _dev as D
+        fn, cn = D.dev(np.ascontiguousarray(feats, np.float32)), D.zeros((tk.n_naive, 3), torch.int32)
+        for _ in range(2):
+            stg.forward(fn, cn)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(max(2, args.steps // 4)):
+            stg.forward(fn, cn)
+        b.record(st)
+        torch.cuda.synchronize()
+        stage_ms = max_all(a.elapsed_time(b) / max(2, args.steps // 4))
+        sp_stage = {"depth": args.sp_stage_depth, "ms_per_stage": stage_ms,
+                    "tokens_per_s": n_tok / (stage_ms * 1e-3),
+                    "what": "ShardedStage: dispatch all_to_all_v (features + coords) -> "
+                            f"{args.sp_stage_depth} sharded Stage-2 blocks (per-use "
+                            "All-gather-KV) -> return all_to_all_v; eager, max over ranks"}
     single = None
     if not args.no_single_compare:
         # the same workload on ONE GPU (rank 0), same timing rules: the
@@ -921,6 +953,11 @@ def run_sp(args):
                          "algorithmic_flops_per_step": total_flops,
                          "attention_ms_max_over_ranks": attn_ms},
             "single_gpu_same_workload": single,
+            "exchange": {"all_gather_kv_bytes_per_step": int(sent_all),
+                         "per_rank_sent_bytes_per_step": int(sent),
+                         "what": "packed bf16 K/V + f32 compressed rows of the 4 uses, "
+                                 "(W-1) peers per rank"},
+            "sp_stage": sp_stage,
             "cpu_baseline": None,
             "e2e": {"value": n_tok / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
@@ -948,6 +985,8 @@ def main():
                     help="default: c3 at N=1, c4 (skewed) under torchrun N>1")
     ap.add_argument("--sp-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = host-staged exchange, lets ranks share one GPU (tests)")
+    ap.add_argument("--sp-stage-depth", type=int, default=2,
+                    help="N>1: also time the sharded stage (dispatch, depth blocks, return)")
     ap.add_argument("--token-lpt", action="store_true",
                     help="shard by token counts (reference rule) instead of routed workload")
     ap.add_argument("--no-single-compare", action="store_true",

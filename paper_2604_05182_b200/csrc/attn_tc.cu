@@ -41,6 +41,8 @@
 // SWIZZLE_NONE canonical layouts (cute mma_sm100_desc.hpp):
 //   K-major  Q, K : element (row, k) at (row/8)*RS + (k/8)*64 + (row%8)*8 + k%8
 //   MN-major V    : the same storage read with N = head dim, K = keys.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -100,6 +102,11 @@ struct Params {
   int accum;      // add the gated merge to `out` instead of storing it
   const int32_t* own_rows;   // optional [nq] (tile order): each token's own kv row;
                              // the window branch then spans the tile's distinct own blocks
+  int q_tma;                 // 1: Q tiles by TMA through tmq (G % 8 == 0)
+  // Q as a 5-D tensor map {d%8, g%8, d/8, g/8, row} (strides 1, DH, 8, 8 DH,
+  // ld_q elements): the box of one token and 8k q-heads lands in shared
+  // memory directly in the UMMA K-major core-matrix layout
+  alignas(64) CUtensorMap tmq;
 };
 
 // One launch: up to kMaxUses NSA uses (same head geometry).  order == nullptr:
@@ -268,7 +275,7 @@ constexpr int tmem_alloc_cols() {
 // Shared memory of one pipeline (producer + MMA warp(s) + softmax warps that
 // stream their own items).
 template <int DH, int HP>
-struct Pipe {
+struct alignas(128) Pipe {   // 128-byte aligned: q is a TMA destination
   __nv_bfloat16 q[2][HP][kM * DH];
   __nv_bfloat16 k[kStages][HP][kNK * DH];
   __nv_bfloat16 v[kStages][HP][kNK * (DH + kOnesCols)];   // [V | ones] rows
@@ -422,6 +429,9 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const int q_first = P.tiles[4 * tile], q_cnt = P.tiles[4 * tile + 1],
                 own = P.tiles[4 * tile + 2];
       const int qb = it & 1;
+      // query row of tile token `lane` (constant over the item's chunks)
+      const int64_t my_tok =
+          lane < q_cnt ? (P.perm ? (int64_t)P.perm[q_first + lane] : (int64_t)(q_first + lane)) : 0;
       // ---- selected rows of the tile tokens (resolved rows are -1 padded)
       // (window-only items need no union of selected blocks)
       const int n_ent = P.br_first <= 1 ? T * P.kmax : 0, n_valid_ent = q_cnt * P.kmax;
@@ -431,26 +441,39 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
         S.ent[i] = r;
         if (r >= 0) atomicOr(&S.bitmap[r >> 5], 1u << (r & 31));
       }
-      // ---- Q tiles of the HP heads -> sQ[qb] (cp.async, zero-filled past the
-      //      tile), once the MMAs of item it-2 are done with the buffer
+      // ---- Q tiles of the HP heads -> sQ[qb], once the MMAs of item it-2 are
+      //      done with the buffer: TMA boxes (one per token and head-tile,
+      //      rows past the tile read out of bounds -> zeros), else cp.async
       if (it >= 2) mbar_wait(&S.q_empty[qb], ((it >> 1) - 1) & 1);
-      constexpr int kQChunks = kM * (DH / 8);
+      if (P.q_tma) {
+        if (lane == 0) mbar_expect_tx(&S.q_full[qb], (uint32_t)(HP * kM * DH * 2));
+        __syncwarp();
+        if (lane < T) {
+          const int32_t row = lane < q_cnt ? (int32_t)my_tok : (int32_t)P.nq;
+#pragma unroll
+          for (int hh = 0; hh < HP; ++hh)
+            tma_load_5d(&S.q[qb][hh][lane * G * DH], &P.tmq, 0, 0, 0, ((h0 + hh) * G) / 8, row,
+                        &S.q_full[qb]);
+        }
+      } else {
+        constexpr int kQChunks = kM * (DH / 8);
 #pragma unroll 4
-      for (int i = lane; i < HP * kQChunks; i += 32) {
-        const int hh = i / kQChunks, rem = i % kQChunks;
-        const int m = rem / (DH / 8), cc = rem % (DH / 8);
-        const int tt = m / G, gg = m % G;
-        const bool ok = tt < q_cnt;
-        const int64_t qrow = ok ? (P.perm ? P.perm[q_first + tt] : q_first + tt) : 0;
-        const __nv_bfloat16* src =
-            P.q + (ok ? qrow * P.ld_q + ((h0 + hh) * G + gg) * DH + cc * 8 : 0);
-        cp_async16(&S.q[qb][hh][(m / 8) * (8 * DH) + cc * 64 + (m % 8) * 8], src,
-                   ok ? 16u : 0u);
+        for (int i = lane; i < HP * kQChunks; i += 32) {
+          const int hh = i / kQChunks, rem = i % kQChunks;
+          const int m = rem / (DH / 8), cc = rem % (DH / 8);
+          const int tt = m / G, gg = m % G;
+          const bool ok = tt < q_cnt;
+          const int64_t qrow = __shfl_sync(0xffffffffu, my_tok, tt & 31);
+          const __nv_bfloat16* src =
+              P.q + (ok ? qrow * P.ld_q + ((h0 + hh) * G + gg) * DH + cc * 8 : 0);
+          cp_async16(&S.q[qb][hh][(m / 8) * (8 * DH) + cc * 64 + (m % 8) * 8], src,
+                     ok ? 16u : 0u);
+        }
+        cp_async_wait_all();
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.q_full[qb]);
       }
-      cp_async_wait_all();
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.q_full[qb]);
       // ---- sorted union = set bits of the bitmap in order
       const int n_words = (int)((P.n_blocks + 31) / 32);
       const int per_w = (n_words + 31) / 32;
@@ -638,13 +661,21 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
             D.qb = qb;
             D.item_seq = it;
           }
-          {   // per token: the groups it sees (padding rows of the tile see none)
+          {   // per token: the groups it sees (padding rows of the tile see none);
+              // the chunk's group table read with four 16-byte loads
+            static_assert(kGroups == 8, "tokvis: 8 groups per chunk");
+            const uint4 m0 = *reinterpret_cast<const uint4*>(&D.gmask[0]);
+            const uint4 m1 = *reinterpret_cast<const uint4*>(&D.gmask[4]);
+            const int4 n0 = *reinterpret_cast<const int4*>(&D.gnv[0]);
+            const int4 n1 = *reinterpret_cast<const int4*>(&D.gnv[4]);
+            const uint32_t gm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+            const int gn[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
             uint32_t v = 0;
-            if (lane < q_cnt)
-              for (int gi = 0; gi < n_grp; ++gi)
-                if (D.gnv[gi] > 0 && ((D.gmask[gi] >> lane) & 1u)) v |= 1u << gi;
-            D.tokvis[lane] = (uint8_t)v;
-            D.tok[lane] = lane < q_cnt ? (P.perm ? P.perm[q_first + lane] : q_first + lane) : 0;
+#pragma unroll
+            for (int gi = 0; gi < 8; ++gi)
+              v |= (gi < n_grp && gn[gi] > 0 ? (gm[gi] >> (lane & 31)) & 1u : 0u) << gi;
+            D.tokvis[lane] = (uint8_t)(lane < q_cnt ? v : 0u);
+            D.tok[lane] = (int32_t)my_tok;
           }
           __syncwarp();
           if (lane == 0)
@@ -1410,6 +1441,38 @@ using namespace lsrm;
 
 namespace lsrm {
 namespace tc {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+// Q tensor map of one use (see Params::tmq); G % 8 != 0 keeps the cp.async path.
+static int make_q_map(Params& p, int G, int dh) {
+  p.q_tma = 0;
+  if (G % 8 != 0 || p.nq == 0) return LSRM_OK;
+  auto fn = encode_fn();
+  if (!fn) return set_error(LSRM_E_CUDA, "tcgen05 attention: cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[5] = {8, 8, (cuuint64_t)(dh / 8), (cuuint64_t)(p.hq / 8), (cuuint64_t)p.nq};
+  cuuint64_t strides[4] = {(cuuint64_t)dh * 2, 16, (cuuint64_t)dh * 16, (cuuint64_t)p.ld_q * 2};
+  cuuint32_t box[5] = {8, 8, (cuuint32_t)(dh / 8), (cuuint32_t)(G / 8), 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(&p.tmq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<__nv_bfloat16*>(p.q),
+                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(LSRM_E_CUDA, "tcgen05 attention: Q tensor map encode failed (%d)", (int)r);
+  p.q_tma = 1;
+  return LSRM_OK;
+}
 // Picks the variant and grid: d_h = 32 runs two independent single-head
 // pipelines per CTA (or, with -DLSRM_HEADPAIR in static mode, one pipeline
 // whose items are kv-head pairs); d_h = 64 one pipeline (TMEM budget).
@@ -1505,6 +1568,7 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
   p.br_first = 0;
   p.accum = 0;
   p.own_rows = nullptr;
+  if (int rc = tc::make_q_map(p, G, dh)) return rc;
   tc::Launch L{};
   L.use[0] = p;
   L.n_uses = 1;
@@ -1562,6 +1626,7 @@ int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, in
     p.br_first = (int)U.branch_first;
     p.accum = (int)U.accumulate;
     p.own_rows = U.own_rows;
+    if (int rc = tc::make_q_map(p, G, dh)) return rc;
   }
   L.n_uses = n_uses;
   L.order = order;

@@ -5,17 +5,24 @@
 //
 // Job j = one K or V tensor of one NSA use: token rows [n, w = hkv*dh] bf16
 // (a column slice of the fused projection output, block-major order).
-// CTA (64-token sub-tile of a block, job j), 4 warps:
-//   1. rows -> shared memory, and -> the padded 8x8-core-matrix interleaved
-//      layout of the tcgen05 attention (plus the 16 ones columns for V);
-//   2. ResBlock r = x + W2 gelu(W1 x + b1) + b2 on the tensor cores
-//      (mma.sync m16n8k16 bf16, fp32 accumulation; warp = 16 tokens);
-//   3. per-column sums of r over the sub-tile's tokens (fixed order) -> a
-//      partial row; the block's last-arriving CTA adds its sub-tiles' partials
-//      in sub-tile order (deterministic) -> the block mean (compressed row).
+// CTA (128-token sub-tile of a block, job j), 8 warps; in the epilogues a
+// thread = (token row = TMEM lane, column half):
+//   1. rows -> shared memory (UMMA K-major core-matrix layout), and -> the
+//      padded 8x8-core-matrix interleaved layout of the tcgen05 attention
+//      (plus the 16 ones columns for V);
+//   2. ResBlock r = x + W2 gelu(W1 x + b1) + b2 on the 5th-gen tensor cores:
+//      tcgen05.mma (M = 128 tokens, N = K = w) into TMEM, x and h from shared
+//      memory, W1 / W2 from shared memory (MN-major); the bias + erf-gelu
+//      epilogue reads D1 back with tcgen05.ld and writes h (bf16) for the
+//      second MMA;
+//   3. per-column sums of r over the sub-tile's tokens (fixed order: warp
+//      shuffle tree, then the four warps) -> a partial row; the block's
+//      last-arriving CTA adds its sub-tiles' partials in sub-tile order
+//      (deterministic) -> the block mean (compressed row).
 // The compressed row goes to mean_out (f32, for the All-gather-KV shard) and/or
 // directly into the interleaved compressed layout cmp_il.
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 namespace lsrm {
 
@@ -42,31 +49,10 @@ struct KvJob {
 };
 static_assert(sizeof(KvJob) == sizeof(lsrm_kv_job), "KvJob must mirror lsrm_kv_job");
 
-constexpr int kSub = 64;   // tokens per sub-tile (4 warps x 16 rows)
+constexpr int kSub = 128;      // tokens per sub-tile = MMA M = TMEM lanes
+constexpr int kThreads = 256;  // 8 warps: TMEM lane quarter = warp % 4, column half = warp / 4
 constexpr int kSubBits = 12;   // work code = (block << kSubBits) | sub-tile
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2,
-                                        uint32_t& a3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& b0, uint32_t& b1) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
-               : "=r"(b0), "=r"(b1)
-               : "r"(addr));
-}
-__device__ __forceinline__ void mma16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2,
-                                         uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -75,17 +61,31 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 __device__ __forceinline__ int64_t il_off(int h, int64_t rows, int vw, int64_t row, int col) {
   return (int64_t)h * rows * vw + (row / 8) * (8 * vw) + (col / 8) * 64 + (row % 8) * 8 + col % 8;
 }
+// UMMA SWIZZLE_NONE core-matrix layouts of a [rows][W] bf16 tile: 8x8 core
+// matrices, (row/8, col/8) at (row/8)*8W + (col/8)*64 elements. As the A
+// operand (token rows, K = col) this is K-major (LBO 128 B between K-adjacent
+// cores, SBO 16W B between M-adjacent ones); as the B operand with rows = K
+// (W1 / W2 are [in][out]) it is MN-major (LBO 16W B, SBO 128 B).
+template <int W>
+__device__ __forceinline__ int core_off(int row, int col) {
+  return (row / 8) * (8 * W) + (col / 8) * 64 + (row % 8) * 8 + col % 8;
+}
 
 template <int W>
-__global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ jobs, int dh) {
-  constexpr int LDS = W + 8;   // padded smem row (bf16): conflict-free ldmatrix
-  constexpr int NT = W / 8;    // mma n-tiles
-  extern __shared__ __align__(16) unsigned char kv_smem[];
-  __nv_bfloat16* const xs = reinterpret_cast<__nv_bfloat16*>(kv_smem);   // [kSub][LDS]
-  __nv_bfloat16* const hs = xs + kSub * LDS;                              // [kSub][LDS]
-  __nv_bfloat16* const w1s = hs + kSub * LDS;                             // [W][LDS]
-  __nv_bfloat16* const w2s = w1s + W * LDS;                               // [W][LDS]
-  float (*csum)[W] = reinterpret_cast<float (*)[W]>(w2s + W * LDS);       // [4][W]
+__global__ void __launch_bounds__(kThreads) kv_prep_kernel(const KvJob* __restrict__ jobs, int dh) {
+  extern __shared__ __align__(128) unsigned char kv_smem[];
+  __nv_bfloat16* const xs = reinterpret_cast<__nv_bfloat16*>(kv_smem);   // [kSub][W] core
+  __nv_bfloat16* const hs = xs + kSub * W;                                // [kSub][W] core
+  __nv_bfloat16* const w1s = hs + kSub * W;                               // [W][W] core
+  __nv_bfloat16* const w2s = w1s + W * W;                                 // [W][W] core
+  float (*csum)[W] = reinterpret_cast<float (*)[W]>(w2s + W * W);       // [kThreads/W][W]
+  // [kSub][W] f32 column-sum staging, XOR-swizzled by row (conflict-free);
+  // aliases hs / w1s / w2s, which are dead once the second MMA has completed
+  float* const red = reinterpret_cast<float*>(hs);
+  static_assert(kSub * W * 4 <= (kSub * W + 2 * W * W) * 2, "red must fit hs + w1s + w2s");
+  __shared__ uint64_t s_bar;
+  __shared__ __align__(16) float s_b1[W], s_b2[W];
+  __shared__ uint32_t s_tmem;
   __shared__ int s_last;
   const KvJob& J = jobs[blockIdx.y];
   const int64_t wi = blockIdx.x;
@@ -96,123 +96,162 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
   const int hkv = W / dh, vw = dh + (int)J.ones_cols;
   const int64_t lo = J.blk_off[b], occ = J.blk_off[b + 1] - lo, prow0 = J.pad_off[b];
   const int64_t n_sub = (occ + kSub - 1) / kSub;
-  // bf16 weights -> smem (16-byte chunks; W1, W2 are [in][out]: r = x W)
-  for (int i = tid; i < W * W / 8; i += 128) {
+  if (warp == 0) tc::tmem_alloc(&s_tmem, 2 * W);   // D1 = x W1, D2 = h W2
+  if (tid == 0) {
+    tc::mbar_init(&s_bar, 1);
+    tc::fence_mbar_init();
+  }
+  // weights and the sub-tile's rows -> smem core layouts, all as async copies
+  // in flight together (rows past the block zero-filled)
+  for (int i = tid; i < W * W / 8; i += kThreads) {
     const int r = i / (W / 8), c8 = (i % (W / 8)) * 8;
-    *reinterpret_cast<uint4*>(&w1s[r * LDS + c8]) = *reinterpret_cast<const uint4*>(J.w1 + r * W + c8);
-    *reinterpret_cast<uint4*>(&w2s[r * LDS + c8]) = *reinterpret_cast<const uint4*>(J.w2 + r * W + c8);
+    tc::cp_async16(&w1s[core_off<W>(r, c8)], J.w1 + r * W + c8, 16u);
+    tc::cp_async16(&w2s[core_off<W>(r, c8)], J.w2 + r * W + c8, 16u);
   }
-  // this thread's accumulator columns: n-tile nt, cols 8nt + 2(lane%4) + {0,1}
-  const int g = lane >> 2, t4 = lane & 3;
-  float cs[NT][2];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) cs[nt][0] = cs[nt][1] = 0.f;
-  {
-    const int64_t s0 = sub * kSub;
-    const int nt_valid = (int)(occ - s0 < kSub ? occ - s0 : kSub);
-    __syncthreads();   // weights staged
-    // 1. rows -> smem + interleaved layout
-    for (int e = tid; e < kSub * (W / 8); e += 128) {
-      const int r = e / (W / 8), ch = e % (W / 8);
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < nt_valid) {
-        v = *reinterpret_cast<const uint4*>(J.src + (lo + s0 + r) * J.ld + ch * 8);
-        const int col = ch * 8, h = col / dh;
-        *reinterpret_cast<uint4*>(J.il + il_off(h, J.rows_pad, vw, prow0 + s0 + r, col - h * dh)) = v;
-      }
-      *reinterpret_cast<uint4*>(&xs[r * LDS + ch * 8]) = v;
-    }
-    if (J.ones_cols) {   // [V | ones]: 1 for a real key
-      const uint32_t one2 = 0x3F803F80u;
-      const int per = (int)J.ones_cols / 8;
-      for (int e = tid; e < nt_valid * hkv * per; e += 128) {
-        const int r = e / (hkv * per), rem = e % (hkv * per), h = rem / per, cc = rem % per;
-        *reinterpret_cast<uint4*>(J.il + il_off(h, J.rows_pad, vw, prow0 + s0 + r, dh + cc * 8)) =
-            make_uint4(one2, one2, one2, one2);
-      }
-    }
-    __syncthreads();
-    // 2. layer 1: h = gelu(x W1 + b1), rows 16*warp .. +16
-    const int r0 = 16 * warp;
-    float acc[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-#pragma unroll
-    for (int k0 = 0; k0 < W; k0 += 16) {
-      uint32_t a0, a1, a2, a3;
-      ldsm_x4(smem_addr(&xs[(r0 + (lane & 15)) * LDS + k0 + (lane >> 4) * 8]), a0, a1, a2, a3);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        uint32_t b0, b1;
-        ldsm_x2_t(smem_addr(&w1s[(k0 + (lane & 15)) * LDS + nt * 8]), b0, b1);
-        mma16816(acc[nt], a0, a1, a2, a3, b0, b1);
-      }
-    }
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      float v[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float z = acc[nt][e] + __ldg(J.b1 + 8 * nt + 2 * t4 + (e & 1));
-        v[e] = 0.5f * z * (1.f + erff(z * 0.70710678118654752f));
-      }
-      *reinterpret_cast<uint32_t*>(&hs[(r0 + g) * LDS + nt * 8 + 2 * t4]) = pack2(v[0], v[1]);
-      *reinterpret_cast<uint32_t*>(&hs[(r0 + g + 8) * LDS + nt * 8 + 2 * t4]) = pack2(v[2], v[3]);
-    }
-    __syncwarp();
-    // 3. layer 2 + residual: r = x + h W2 + b2; column sums of valid rows
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-#pragma unroll
-    for (int k0 = 0; k0 < W; k0 += 16) {
-      uint32_t a0, a1, a2, a3;
-      ldsm_x4(smem_addr(&hs[(r0 + (lane & 15)) * LDS + k0 + (lane >> 4) * 8]), a0, a1, a2, a3);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        uint32_t b0, b1;
-        ldsm_x2_t(smem_addr(&w2s[(k0 + (lane & 15)) * LDS + nt * 8]), b0, b1);
-        mma16816(acc[nt], a0, a1, a2, a3, b0, b1);
-      }
-    }
-    const bool ok_lo = r0 + g < nt_valid, ok_hi = r0 + g + 8 < nt_valid;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const __nv_bfloat162 xlo =
-          *reinterpret_cast<const __nv_bfloat162*>(&xs[(r0 + g) * LDS + nt * 8 + 2 * t4]);
-      const __nv_bfloat162 xhi =
-          *reinterpret_cast<const __nv_bfloat162*>(&xs[(r0 + g + 8) * LDS + nt * 8 + 2 * t4]);
-      const float x0 = __low2float(xlo), x1 = __high2float(xlo);
-      const float x2 = __low2float(xhi), x3 = __high2float(xhi);
-      const float c0 = __ldg(J.b2 + 8 * nt + 2 * t4), c1 = __ldg(J.b2 + 8 * nt + 2 * t4 + 1);
-      if (ok_lo) {
-        cs[nt][0] += x0 + acc[nt][0] + c0;
-        cs[nt][1] += x1 + acc[nt][1] + c1;
-      }
-      if (ok_hi) {
-        cs[nt][0] += x2 + acc[nt][2] + c0;
-        cs[nt][1] += x3 + acc[nt][3] + c1;
-      }
-    }
+  for (int i = tid; i < W; i += kThreads) {
+    s_b1[i] = J.b1[i];
+    s_b2[i] = J.b2[i];
   }
-  // 4. fixed-order reduction: lanes with equal t4 (xor 4, 8, 16), then warps
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      float v = cs[nt][e];
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
-      v += __shfl_xor_sync(0xffffffffu, v, 8);
-      v += __shfl_xor_sync(0xffffffffu, v, 16);
-      if (g == 0) csum[warp][8 * nt + 2 * t4 + e] = v;
-    }
+  const int64_t s0 = sub * kSub;
+  const int nt_valid = (int)(occ - s0 < kSub ? occ - s0 : kSub);
+  for (int e = tid; e < kSub * (W / 8); e += kThreads) {
+    const int r = e / (W / 8), ch = e % (W / 8);
+    const bool v = r < nt_valid;
+    tc::cp_async16(&xs[core_off<W>(r, ch * 8)], J.src + (v ? (lo + s0 + r) * J.ld + ch * 8 : 0),
+                   v ? 16u : 0u);
+  }
+  tc::cp_async_wait_all();
+  tc::fence_async_smem();   // smem writes -> visible to the tensor core
+  tc::tc_before_sync();
   __syncthreads();
-  for (int col = tid; col < W; col += 128)
-    J.partial[wi * W + col] = ((csum[0][col] + csum[1][col]) + csum[2][col]) + csum[3][col];
-  // 5. the block's last-arriving CTA finishes it
+  tc::tc_after_sync();
+  const uint32_t tmem = s_tmem;
+  const uint32_t d1 = tmem, d2 = tmem + W;
+  const uint32_t idesc = tc::idesc_bf16(kSub, W, 1);   // A K-major, B MN-major
+  // 2a. D1 = x W1 (K = W in steps of 16)
+  if (warp == 0 && tc::elect_one_sync()) {
+    const uint64_t a = tc::sdesc(tc::smem_u32(xs), 128, 16 * W);
+    const uint64_t bw = tc::sdesc(tc::smem_u32(w1s), 16 * W, 128);
+#pragma unroll
+    for (int kk = 0; kk < W / 16; ++kk)
+      tc::mma_bf16(d1, a + (uint64_t)(kk * 16), bw + (uint64_t)(kk * 2 * W), idesc, kk > 0);
+    tc::mma_commit(&s_bar);
+  }
+  __syncwarp();
+  // 1. (while the MMA runs) rows -> the padded interleaved layout of the
+  //    attention (plus the ones columns of [V | ones])
+  for (int e = tid; e < nt_valid * (W / 8); e += kThreads) {
+    const int r = e / (W / 8), ch = e % (W / 8);
+    const int col = ch * 8, h = col / dh;
+    *reinterpret_cast<uint4*>(J.il + il_off(h, J.rows_pad, vw, prow0 + s0 + r, col - h * dh)) =
+        *reinterpret_cast<const uint4*>(&xs[core_off<W>(r, col)]);
+  }
+  if (J.ones_cols) {   // [V | ones]: 1 for a real key
+    const uint32_t one2 = 0x3F803F80u;
+    const int per = (int)J.ones_cols / 8;
+    for (int e = tid; e < nt_valid * hkv * per; e += kThreads) {
+      const int r = e / (hkv * per), rem = e % (hkv * per), h = rem / per, cc = rem % per;
+      *reinterpret_cast<uint4*>(J.il + il_off(h, J.rows_pad, vw, prow0 + s0 + r, dh + cc * 8)) =
+          make_uint4(one2, one2, one2, one2);
+    }
+  }
+  tc::mbar_wait(&s_bar, 0);
+  tc::tc_after_sync();
+  // 2b. h = gelu(D1 + b1) -> smem (this thread's row, core layout); warps whose
+  //     rows are all past the block skip it (their D2 rows are never read)
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;                   // TMEM lane = token row
+  const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+  constexpr int kHalf = W / 2;                           // columns of this thread
+  if (quarter * 32 < nt_valid) {
+#pragma unroll
+    for (int c0 = half * kHalf; c0 < (half + 1) * kHalf; c0 += 32) {
+      uint32_t r[32];
+      tc::tmem_ld32(d1 + lane_base + c0, r);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        const float4 ba = *reinterpret_cast<const float4*>(&s_b1[c0 + j]);
+        const float4 bb = *reinterpret_cast<const float4*>(&s_b1[c0 + j + 4]);
+        const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const float z0 = __uint_as_float(r[j + e]) + bv[e];
+          const float z1 = __uint_as_float(r[j + e + 1]) + bv[e + 1];
+          w[e / 2] = pack2(0.5f * z0 * (1.f + erff(z0 * 0.70710678118654752f)),
+                           0.5f * z1 * (1.f + erff(z1 * 0.70710678118654752f)));
+        }
+        *reinterpret_cast<uint4*>(&hs[core_off<W>(row, c0 + j)]) =
+            make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+  tc::fence_async_smem();
+  tc::tc_before_sync();
+  __syncthreads();
+  tc::tc_after_sync();
+  // 2c. D2 = h W2
+  if (warp == 0 && tc::elect_one_sync()) {
+    const uint64_t a = tc::sdesc(tc::smem_u32(hs), 128, 16 * W);
+    const uint64_t bw = tc::sdesc(tc::smem_u32(w2s), 16 * W, 128);
+#pragma unroll
+    for (int kk = 0; kk < W / 16; ++kk)
+      tc::mma_bf16(d2, a + (uint64_t)(kk * 16), bw + (uint64_t)(kk * 2 * W), idesc, kk > 0);
+    tc::mma_commit(&s_bar);
+  }
+  __syncwarp();
+  tc::mbar_wait(&s_bar, 1);
+  tc::tc_after_sync();
+  // 3. r = x + D2 + b2 on valid rows -> red[row][col] (f32); then fixed-order
+  //    column sums over the 128 rows (thread = column x row slice)
+  const bool ok = row < nt_valid;
+  if (quarter * 32 < nt_valid) {
+#pragma unroll
+    for (int c0 = half * kHalf; c0 < (half + 1) * kHalf; c0 += 32) {
+      uint32_t r[32];
+      tc::tmem_ld32(d2 + lane_base + c0, r);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(&xs[core_off<W>(row, c0 + j)]);
+        const __nv_bfloat16* xh = reinterpret_cast<const __nv_bfloat16*>(&xv);
+        const float4 ba = *reinterpret_cast<const float4*>(&s_b2[c0 + j]);
+        const float4 bb = *reinterpret_cast<const float4*>(&s_b2[c0 + j + 4]);
+        const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          red[row * W + ((c0 + j + e) ^ (row & 31))] =
+              ok ? __bfloat162float(xh[e]) + __uint_as_float(r[j + e]) + bv[e] : 0.f;
+      }
+    }
+  } else {
+    for (int c = half * kHalf; c < (half + 1) * kHalf; ++c) red[row * W + c] = 0.f;
+  }
+  tc::tc_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_after_sync();
+    tc::tmem_dealloc(tmem, 2 * W);
+  }
+  {
+    constexpr int kSlices = kThreads / W;       // row slices per column (4 for W = 64)
+    constexpr int kRows = kSub / kSlices;
+    const int col = tid % W, sl = tid / W;
+    float acc = 0.f;
+    for (int i = 0; i < kRows; ++i) {
+      const int rr = sl * kRows + i;
+      acc += red[rr * W + (col ^ (rr & 31))];
+    }
+    csum[sl][col] = acc;
+  }
+  __syncthreads();
+  for (int col = tid; col < W; col += kThreads) {
+    float tot = csum[0][col];
+    for (int sl = 1; sl < kThreads / W; ++sl) tot += csum[sl][col];
+    J.partial[wi * W + col] = tot;
+  }
+  // 4. the block's last-arriving CTA finishes it
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(&J.arrive[b], 1) == (int)n_sub - 1;
@@ -225,7 +264,7 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
   // in the attention kernel
   if (!J.ones_cols) {
     const int64_t plen = J.pad_off[b + 1] - prow0;
-    for (int e = tid; e < (plen - occ) * (W / 8); e += 128) {
+    for (int e = tid; e < (plen - occ) * (W / 8); e += kThreads) {
       const int64_t r = occ + e / (W / 8);
       const int col = (e % (W / 8)) * 8, h = col / dh;
       const uint4 v = *reinterpret_cast<const uint4*>(J.src + lo * J.ld + col);
@@ -233,7 +272,7 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
     }
   }
   const float inv = 1.f / (float)occ;
-  for (int col = tid; col < W; col += 128) {
+  for (int col = tid; col < W; col += kThreads) {
     float tot = 0.f;
     for (int64_t k = 0; k < n_sub; ++k) tot += __ldcg(J.partial + (w0 + k) * W + col);
     const float mean = tot * inv;
@@ -248,7 +287,7 @@ __global__ void __launch_bounds__(128) kv_prep_kernel(const KvJob* __restrict__ 
   }
   if (tid == 0) J.arrive[b] = 0;   // ready for the next launch
   if (J.cmp_il && J.ones_cols)
-    for (int e = tid; e < hkv * (int)J.ones_cols; e += 128) {
+    for (int e = tid; e < hkv * (int)J.ones_cols; e += kThreads) {
       const int h = e / (int)J.ones_cols, cc = e % (int)J.ones_cols;
       J.cmp_il[il_off(h, J.cmp_rows_pad, vw, b, dh + cc)] = __float2bfloat16_rn(1.f);
     }
@@ -266,15 +305,15 @@ extern "C" int lsrm_kv_prepare_jobs(const lsrm_kv_job* jobs, int n_jobs, int64_t
   if (n_jobs == 0 || max_work == 0) return LSRM_OK;
   cudaStream_t st = as_stream(stream);
   const dim3 grid((unsigned)max_work, (unsigned)n_jobs);
-  const size_t smem = (size_t)(2 * kSub + 2 * w) * (w + 8) * 2 + 4 * w * sizeof(float);
+  const size_t smem = (size_t)(2 * kSub + 2 * w) * w * 2 + (size_t)kThreads * sizeof(float);
   if (w == 64) {
     LSRM_CUDA(cudaFuncSetAttribute(kv_prep_kernel<64>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kv_prep_kernel<64><<<grid, 128, smem, st>>>(reinterpret_cast<const KvJob*>(jobs), dh);
+    kv_prep_kernel<64><<<grid, kThreads, smem, st>>>(reinterpret_cast<const KvJob*>(jobs), dh);
   } else {
     LSRM_CUDA(cudaFuncSetAttribute(kv_prep_kernel<128>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kv_prep_kernel<128><<<grid, 128, smem, st>>>(reinterpret_cast<const KvJob*>(jobs), dh);
+    kv_prep_kernel<128><<<grid, kThreads, smem, st>>>(reinterpret_cast<const KvJob*>(jobs), dh);
   }
   LSRM_LAUNCHED();
   return LSRM_OK;

@@ -354,10 +354,10 @@ class SparseLayerEngine:
                     blk, pad, nb = m.kv_off, m.pad_off, m.n_blocks
                     mean, cmp_il = None, self.buf[(kind + "c_il", use)]
                 occ = np.diff(m.loc_off_host)
-                nsub = (occ + 63) // 64
-                # work code = (block << 12) | 64-token sub-tile (kv_prep.cu kSubBits)
+                nsub = (occ + 127) // 128   # 128-token sub-tiles (kv_prep.cu kSub)
+                # work code = (block << 12) | 128-token sub-tile (kv_prep.cu kSubBits)
                 require(int(nsub.max(initial=0)) <= 1 << 12 and nb < 1 << 19,
-                        f"kv_prepare: blocks of up to {64 << 12} tokens and fewer than "
+                        f"kv_prepare: blocks of up to {128 << 12} tokens and fewer than "
                         f"{1 << 19} occupied blocks are supported (got {int(occ.max(initial=0))} "
                         f"tokens, {nb} blocks)")
                 work = np.concatenate([(b << 12) + np.arange(k) for b, k in enumerate(nsub)])
