@@ -218,7 +218,18 @@ def parallel_sparse_stage(x_up, y_up, weights, ctx, params, n_workers: int):
     KV, so the W shards are computed in one pass of the fp32 stage
     (`recon_pipeline.sparse_stage_forward`) and the result is the serial one
     (the reference requires <= 1e-6; here it is identical).  The
-    multi-process NCCL path with real per-rank shards is `ShardedLayer`."""
+    multi-process NCCL path with real per-rank shards is `ShardedLayer`.
+
+    With the drop-in's precision "bf16" (`fastpath`) and a geometry the
+    bf16 engine takes, the W workers really run: one thread per worker, each
+    a `ShardedStage` (dispatch all-to-all, per-use All-gather-KV, return
+    all-to-all) exchanging device buffers through `ThreadTransport`; the
+    message log is then the bytes those exchanges moved."""
+    from . import fastpath
+    if fastpath.active():
+        r = _parallel_stage_threads(x_up, y_up, weights, ctx, params, n_workers)
+        if r is not None:
+            return r
     from .recon_pipeline import sparse_stage_forward
     part_vol, part_img = ctx.part_vol, ctx.part_img
     require(x_up.count == part_vol.n_tokens and y_up.count == part_img.n_tokens,
@@ -249,6 +260,66 @@ def parallel_sparse_stage(x_up, y_up, weights, ctx, params, n_workers: int):
                         topology.log(f"layer{m}/{name}/win", "window", w, w, 0)
     all_to_all(aligned, naive, topology, "return", 4 * d + TOKEN_COORD_BYTES)
     return x_s, y_s, topology
+
+
+def _parallel_stage_threads(x_up, y_up, weights, ctx, params, n_workers: int):
+    """bf16 `parallel_sparse_stage`: W ShardedStage workers on threads."""
+    import threading
+    from . import fastpath
+    from .nsa_attention import selection_rows
+    if not fastpath._ctx_ok(ctx, params) or len(weights) == 0:
+        return None
+    require(n_workers >= 1, "need at least one worker")
+    pv, pi = ctx.part_vol, ctx.part_img
+    require(x_up.count == pv.n_tokens and y_up.count == pi.n_tokens,
+            "token sets do not match the partitions in the context")
+    plan_rows = fastpath._ctx_rows(ctx)
+    topology = shard_blocks(pv, pi, n_workers)
+    uses = [fastpath._block_uses(w) for w in weights]
+    feats = np.concatenate([np.asarray(D.host(x_up.features) if D.is_device(x_up.features)
+                                       else x_up.features, np.float32),
+                            np.asarray(D.host(y_up.features) if D.is_device(y_up.features)
+                                       else y_up.features, np.float32)])
+    coords = np.concatenate([np.asarray(D.host(c) if D.is_device(c) else c)
+                             for c in (x_up.coords, y_up.coords)]).astype(np.int32)
+    shared, outs, errs = ThreadTransport.make_shared(n_workers), [None] * n_workers, []
+    dev = torch.cuda.current_device()
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(dev)
+            tr = ThreadTransport(r, n_workers, shared)
+            st = ShardedStage(pv, pi, plan_rows, weights, params, r, n_workers,
+                              topology=topology if r == 0 else _topology_copy(topology),
+                              transport=tr, uses=uses)
+            tk = st.tokens
+            lo = int(np.concatenate([[0], np.cumsum([a.size for a in tk.naive])])[r])
+            out = st.forward(D.dev(feats[lo:lo + tk.n_naive]), D.dev(coords[lo:lo + tk.n_naive]))
+            outs[r] = (lo, D.host(out), st.topology.message_log)
+        except BaseException as exc:   # noqa: BLE001 (re-raised on the caller's thread)
+            errs.append(exc)
+            shared["barrier"].abort()
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(n_workers)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errs:
+        raise errs[0]
+    res = np.empty_like(feats)
+    log = []
+    for lo, o, lg in outs:
+        res[lo:lo + o.shape[0]] = o
+    for r in range(n_workers):     # worker logs, in rank order
+        log += outs[r][2] if r else []
+    topology.message_log.extend(log)
+    n_x = int(x_up.count)
+    return res[:n_x], res[n_x:], topology
+
+
+def _topology_copy(t: WorkerTopology) -> WorkerTopology:
+    return WorkerTopology(t.n_workers, t.vol_rows, t.img_rows, t.vol_tokens, t.img_tokens,
+                          t.loads)
 
 
 # ---------------------------------------------------------------------------
@@ -522,6 +593,48 @@ class InProcessTransport:
             for r, slot in enumerate(slots):
                 slot.copy_(self.registry[r][use])
         return wait
+
+
+class ThreadTransport:
+    """W workers as threads of ONE process on one GPU (the reference's own
+    execution model: `_run_phase` runs the workers on a thread pool,
+    `lsrm/seq_parallel.py:68-86`). Every exchange is a rendezvous: each
+    worker publishes its send buffers, all wait at a barrier, each copies
+    what it receives (device copies on the shared stream, so stream order
+    puts them after every producer), and a second barrier keeps a sender
+    from reusing its buffer before every receiver has enqueued its copy."""
+
+    def __init__(self, rank: int, world: int, shared: dict):
+        self.rank, self.world = rank, world
+        self.shared = shared      # {"barrier": threading.Barrier(world), "slots": [None] * world}
+
+    @staticmethod
+    def make_shared(world: int) -> dict:
+        import threading
+        return {"barrier": threading.Barrier(world), "slots": [None] * world}
+
+    def _rendezvous(self, mine, take):
+        sh = self.shared
+        sh["slots"][self.rank] = mine
+        sh["barrier"].wait()
+        take(sh["slots"])
+        sh["barrier"].wait()
+
+    def __call__(self, send: torch.Tensor, slots):
+        def take(pub):
+            for r, sl in enumerate(slots):
+                if sl.numel():
+                    sl.copy_(pub[r])
+        self._rendezvous(send, take)
+        return lambda: None
+
+    def all_to_all_v(self, sends, recvs):
+        def take(pub):
+            for r, rv in enumerate(recvs):
+                if rv.numel():
+                    rv.copy_(pub[r][self.rank])
+        self._rendezvous(list(sends), take)
+        return lambda: None
 
 
 class HostStagedTransport:
@@ -838,10 +951,13 @@ class TokenDispatch:
         return [(s_, d, int(self.msg[(s_, d)][0].size)) for s_ in range(self.world)
                 for d in range(self.world) if s_ != d and self.msg[(s_, d)][0].size]
 
-    def log(self, topology: WorkerTopology, phase: str, bytes_per_token: int, reverse=False):
+    def log(self, topology: WorkerTopology, phase: str, bytes_per_token: int, reverse=False,
+            only_src: int = None):
+        """Log the messages (all pairs, or only those `only_src` sends)."""
         for s_, d, n in self.messages():
             a, b = (d, s_) if reverse else (s_, d)
-            topology.log(phase, "all_to_all", a, b, n * bytes_per_token)
+            if only_src is None or a == only_src:
+                topology.log(phase, "all_to_all", a, b, n * bytes_per_token)
 
     @staticmethod
     def _chunks(t, counts):
@@ -919,7 +1035,8 @@ class ShardedStage:
     log follows the reference protocol (dispatch / layer m use / return)."""
 
     def __init__(self, part_vol, part_img, plan_rows, weights, params, rank: int, world: int,
-                 topology: WorkerTopology = None, transport=None, by_cost: bool = True):
+                 topology: WorkerTopology = None, transport=None, by_cost: bool = True,
+                 uses: list = None):
         from .recon_pipeline import SparseStageEngine
         self.rank, self.world, self.params = rank, world, params
         if topology is None:
@@ -933,6 +1050,7 @@ class ShardedStage:
         self.transport = transport or NcclTransport(rank, world)
         shards = {"x": topology.vol_rows, "y": topology.img_rows}
         self.stage = SparseStageEngine(part_vol, part_img, plan_rows, weights, params,
+                                       uses=uses,
                                        shard={"x": shards["x"][rank], "y": shards["y"][rank]})
         for m, blk in enumerate(self.stage.blocks):
             ex = KVExchange(blk.layer, rank, world, shards, transport=self.transport,
@@ -955,7 +1073,7 @@ class ShardedStage:
         image] tokens. Returns the stage output rows of the same shard."""
         tk, d = self.tokens, self.params.model_dim
         tk.dispatch(self.transport, [feats_naive, coords_naive], [self._loc, self._coords])
-        tk.log(self.topology, "dispatch", self.bytes_per_token)
+        tk.log(self.topology, "dispatch", self.bytes_per_token, only_src=self.rank)
         nx = tk.n_loc_x
         self.stage.forward(self._loc[:nx], self._loc[nx:],
                            out=(self._out[:nx], self._out[nx:]))
@@ -963,7 +1081,7 @@ class ShardedStage:
             self._log_window(m)
         out = D.empty((tk.n_naive, d), torch.float32)
         tk.gather_back(self.transport, [self._out], [out])
-        tk.log(self.topology, "return", self.bytes_per_token, reverse=True)
+        tk.log(self.topology, "return", self.bytes_per_token, reverse=True, only_src=self.rank)
         return out
 
     def _log_window(self, m):

@@ -135,3 +135,30 @@ def test_sparse_block_and_stage_bf16(setup, bf16):
         upd = _rel(np.asarray(gg, np.float64) - base, np.asarray(ww, np.float64) - base)
         print(f"bf16 {name}: update rel-L2 vs fp32 path {upd:.2e}")
         assert upd < 2e-2, (name, upd)
+
+
+@pytest.mark.parametrize("W", [2, 3])
+def test_parallel_sparse_stage_threads_bit_equal(setup, bf16, W):
+    """precision bf16: `parallel_sparse_stage` (`lsrm/seq_parallel.py:321`)
+    really runs W workers (threads, each a ShardedStage exchanging device
+    buffers: dispatch all-to-all, per-use All-gather-KV, return all-to-all):
+    bit-equal to the single-engine stage, dispatch / return bytes equal to
+    the reference's all_to_all accounting."""
+    s = setup
+    L, R, params, ctx = s["L"], s["R"], s["params"], s["ctx"]
+    from paper_2604_05182_b200 import seq_parallel as S
+    ws = [R.init_sparse_block(0, params, m) for m in range(2)]
+    x_up, y_up = s["x_up"], s["y_up"]
+    xs, ys, topo = S.parallel_sparse_stage(x_up, y_up, ws, ctx, params, W)
+    rx, ry = R.sparse_stage_forward(x_up, y_up, ws, ctx, params)
+    assert np.array_equal(xs, rx) and np.array_equal(ys, ry)
+    ref = S.WorkerTopology(W, [], [], [], [], np.zeros(W, np.int64))
+    n = x_up.count + y_up.count
+    aligned = [np.concatenate([topo.vol_tokens[w], topo.img_tokens[w] + x_up.count])
+               for w in range(W)]
+    naive = S.naive_contiguous_shards(n, W)
+    S.all_to_all(naive, aligned, ref, "dispatch", 4 * 1024 + 12)
+    got = sorted(e for e in topo.message_log if e[0] == "dispatch")
+    assert got == sorted(ref.message_log)
+    kv = [e for e in topo.message_log if e[1] == "all_gather_kv"]
+    assert len(kv) == 2 * 4 * W * (W - 1)          # layers x uses x ordered pairs
