@@ -640,42 +640,54 @@ def time_setup(wl_name, reps=5):
 
 
 def time_train_step(inst, steps=3):
-    """Training step of the four NSA uses of one layer (SURVEY §8f rank 2,
-    BASELINE config 5's fwd+bwd): training.NsaLayerModule, fast path
-    (mma.sync bf16 branches, TF32 GEMMs), loss = sum of squares of the four
-    outputs; device events around forward and backward."""
+    """Training step of one full Stage-2 block (SURVEY §8f ranks 1-2,
+    BASELINE config 5's fwd+bwd at one layer): training.SparseBlockModule,
+    fast path (bf16 tensor-core branches, TF32 GEMMs, fp32 master weights):
+    add + LayerNorm, use gates, the four NSA uses, gated mixture +
+    LayerNorm, FFN, residuals; loss = sum of squares of both outputs; then
+    one Adam step. Device events around forward, backward and the step."""
     import torch
-    from paper_2604_05182_b200.training import NsaLayerModule, resolve_plan_rows
+    from paper_2604_05182_b200.recon_pipeline import init_sparse_block
+    from paper_2604_05182_b200.training import SparseBlockModule, resolve_plan_rows
     res = resolve_plan_rows(inst.plan_rows, inst.part_vol, inst.part_img)
-    mod = NsaLayerModule(inst.params, weights=inst.weights, fast_backward=True)
+    mod = SparseBlockModule(inst.params, weights=init_sparse_block(0, inst.params, 0),
+                            fast_backward=True)
+    opt = torch.optim.Adam(mod.parameters(), lr=1e-4)
     x = torch.tensor(inst.x_hat, device="cuda", requires_grad=True)
     y = torch.tensor(inst.y_hat, device="cuda", requires_grad=True)
+    xi, yi = (0.1 * x).detach(), (0.1 * y).detach()
 
     def fwd():
-        outs = mod(x, y, inst.part_vol, inst.part_img, res)
-        return sum((o * o).sum() for o in outs.values())
+        x2, y2 = mod(x, y, xi, yi, inst.part_vol, inst.part_img, res)
+        return (x2 * x2).sum() + (y2 * y2).sum()
     for _ in range(3):   # warm-up (lazy module loading of the sort kernels, allocator)
+        opt.zero_grad()
         fwd().backward()
+        opt.step()
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
-    fw, bw = [], []
+    fw, bw, op = [], [], []
     for _ in range(steps):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        opt.zero_grad()
         e[0].record(st)
         loss = fwd()
         e[1].record(st)
         loss.backward()
         e[2].record(st)
+        opt.step()
+        e[3].record(st)
         torch.cuda.synchronize()
         fw.append(e[0].elapsed_time(e[1]))
         bw.append(e[1].elapsed_time(e[2]))
-    f, b = float(np.mean(fw)), float(np.mean(bw))
+        op.append(e[2].elapsed_time(e[3]))
+    f, b, o = float(np.mean(fw)), float(np.mean(bw)), float(np.mean(op))
     n_tok = inst.n_vol + inst.n_img
-    return {"ms_per_step": f + b, "forward_ms": f, "backward_ms": b,
-            "tokens_per_s": n_tok / ((f + b) * 1e-3),
-            "what": "fwd+bwd of the 4 gated NSA uses of one layer incl. projections, "
-                    "compression and gates (mma.sync bf16 branches, TF32 GEMMs, fp32 master "
-                    "weights)"}
+    return {"ms_per_step": f + b + o, "forward_ms": f, "backward_ms": b, "optimizer_ms": o,
+            "tokens_per_s": n_tok / ((f + b + o) * 1e-3),
+            "what": "one full Stage-2 block (4 gated NSA uses + add/LN, use gates, gated "
+                    "mixture/LN, FFN 4d, residuals): fwd + bwd + Adam step, bf16 tensor-core "
+                    "attention branches, TF32 GEMMs, fp32 master weights"}
 
 
 def pcie_bandwidth(sizes=(64 << 20, 128 << 20, 256 << 20), reps=5):

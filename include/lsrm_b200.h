@@ -596,6 +596,31 @@ int lsrm_all_to_all_v(void* comm, int rank, int world, const void* send,
                       const int64_t* send_bytes, void* recv, const int64_t* recv_bytes,
                       void* stream);
 
+
+/* ---- backward of the Stage-2 block around the NSA uses (csrc/train_block.cu;
+ * training; forward lsrm/recon_pipeline.py:461-497).
+ * fp32, deterministic (fixed-order partial sums, no float atomics).
+ * colsum_parts(n): rows of partial sums a reduction over n rows needs
+ * (workspace `part` = 2 * parts * d floats for layer_norm_bwd, parts * d
+ * for colsum). */
+int64_t lsrm_colsum_parts(int64_t n);
+/* dx (+)= dLN(x)/dx . dy; dgamma = sum_rows dy x_hat; dbeta = sum_rows dy. */
+int lsrm_layer_norm_bwd_f32(const float* x, int64_t ld_x, int64_t n, int d, const float* gamma,
+                            float eps, const float* dy, int64_t ld_dy, float* dx, int64_t ld_dx,
+                            int accumulate, float* part, float* dgamma, float* dbeta,
+                            void* stream);
+/* out[c] = sum_rows x[r, c] (bias gradients). */
+int lsrm_colsum_f32(const float* x, int64_t ld, int64_t n, int d, float* part, float* out,
+                    void* stream);
+/* gated mixture x1 = xe + s(l_s) o_s + s(l_c) o_c (l = logits + bias [2d]):
+ * do_s, do_c [n, d] and dlogits [n, 2d] from dx1. */
+int lsrm_gate_mix_bwd_f32(const float* logits, int64_t ld_l, const float* bias, const float* o_s,
+                          const float* o_c, const float* dx1, int64_t n, int d, float* do_s,
+                          float* do_c, float* dlogits, void* stream);
+/* dt = du * gelu'(z + bias) (exact erf gelu). */
+int lsrm_gelu_bwd_f32(const float* z, const float* bias, const float* du, int64_t n, int d,
+                      float* dt, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

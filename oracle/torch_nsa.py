@@ -78,3 +78,32 @@ def nsa_use(x, kv, w, params, part_kv, sel_mask, win_mask):
     g = torch.sigmoid(x @ w["gate_w"] + w["gate_b"])
     merged = sum(g[:, b * d:(b + 1) * d] * o.reshape(n, d) for b, o in enumerate(outs))
     return merged @ w["w_o"]
+
+
+def layer_norm(x, gamma, beta, eps=1e-5):
+    """`tensor_core.py:139-146` (biased variance)."""
+    mu = x.mean(dim=1, keepdim=True)
+    var = ((x - mu) ** 2).mean(dim=1, keepdim=True)
+    return (x - mu) / torch.sqrt(var + eps) * gamma + beta
+
+
+def sparse_block(x, y, x_inj, y_inj, wb, params, parts, masks):
+    """One Stage-2 sparse block, f64 autograd (`recon_pipeline.py:461-497`).
+    wb: dict of f64 tensors: uses[v2v|v2i|i2i|i2v] (nsa_use weight dicts),
+    ln_ax/ln_ay/ln_fx/ln_fy = (gamma, beta), gate_x/gate_y = (W, b),
+    ffn_x/ffn_y = (w1, b1, w2, b2). parts[use] = the KV partition,
+    masks[use] = (sel, win)."""
+    def ffn(h, w):
+        return _gelu(h @ w[0] + w[1]) @ w[2] + w[3]
+    d = x.shape[1]
+    xe, ye = x + x_inj, y + y_inj
+    xh, yh = layer_norm(xe, *wb["ln_ax"]), layer_norm(ye, *wb["ln_ay"])
+    gx = torch.sigmoid(xh @ wb["gate_x"][0] + wb["gate_x"][1])
+    gy = torch.sigmoid(yh @ wb["gate_y"][0] + wb["gate_y"][1])
+
+    def use(name, q, kv):
+        return nsa_use(q, kv, wb["uses"][name], params, parts[name], *masks[name])
+    x1 = xe + gx[:, :d] * use("v2v", xh, xh) + gx[:, d:] * use("v2i", xh, yh)
+    y1 = ye + gy[:, :d] * use("i2i", yh, yh) + gy[:, d:] * use("i2v", yh, xh)
+    return (x1 + ffn(layer_norm(x1, *wb["ln_fx"]), wb["ffn_x"]),
+            y1 + ffn(layer_norm(y1, *wb["ln_fy"]), wb["ffn_y"]))

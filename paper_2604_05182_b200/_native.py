@@ -100,6 +100,11 @@ SIGNATURES = {
     "lsrm_comm_destroy": (I32, [P]),
     "lsrm_allgather_kv": (I32, [P, I32, I32, P, I64, P, P, P, P, P, I32, P]),
     "lsrm_all_to_all_v": (I32, [P, I32, I32, P, P, P, P, P]),
+    "lsrm_colsum_parts": (I64, [I64]),
+    "lsrm_layer_norm_bwd_f32": (I32, [P, I64, I64, I32, P, F32, P, I64, P, I64, I32, P, P, P, P]),
+    "lsrm_colsum_f32": (I32, [P, I64, I64, I32, P, P, P]),
+    "lsrm_gate_mix_bwd_f32": (I32, [P, I64, P, P, P, P, I64, I32, P, P, P, P]),
+    "lsrm_gelu_bwd_f32": (I32, [P, P, P, I64, I32, P, P]),
 }
 
 _lib = None

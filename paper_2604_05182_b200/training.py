@@ -1,4 +1,5 @@
-"""Training step of one gated NSA use.
+"""Training of the Stage-2 block: one gated NSA use, the four uses of a
+layer, and the full block.
 
 The reference is inference-only: its NSA use (`nsa_attention.py:287-327`) has
 no backward.  This module adds one on the GPU path: an fp32
@@ -12,7 +13,9 @@ and a backward built from
   * `lsrm_gemm_f32_ex`        - every projection / weight gradient (cuBLAS),
 
 wrapped in a `torch.autograd.Function` so a `torch.optim` optimizer can step
-the weights.  Gradients are checked against the float64 autograd restatement
+the weights. `SparseBlockModule` adds the block around the uses (add +
+LayerNorm, use gates, gated mixture + LayerNorm, FFN) with the row kernels of
+csrc/block.cu forward and csrc/train_block.cu backward.  Gradients are checked against the float64 autograd restatement
 `oracle/torch_nsa.py` (tests/test_training.py).
 
 Inputs and selections are fixed per call: routing (which blocks each query
@@ -111,8 +114,8 @@ def _forward(spec: _Spec, x, kv, P):
 
 
 def _colsum(t):
-    ones = torch.ones((1, t.shape[0]), dtype=torch.float32, device=t.device)
-    return _ops.gemm_ex(ones, t).view(-1)
+    """Column sums (bias gradients): deterministic fixed-order kernel."""
+    return _colsum_dev(t.contiguous())
 
 
 def _backward(spec: _Spec, P, s, dout):
@@ -341,3 +344,177 @@ class NsaLayerModule(torch.nn.Module):
         return {u: self.uses[u](streams[qs], streams[ks], parts[qs], parts[ks],
                                 table=resolved[u])
                 for u, (qs, ks, _) in USE_STREAMS.items()}
+
+
+# ---------------------------------------------------------------------------
+# the full Stage-2 block (`recon_pipeline.py:461-497`): add + LayerNorm, use
+# gates, the four NSA uses, gated mixture + LayerNorm, FFN, residuals.
+# Every piece is a torch.autograd.Function over this library's kernels
+# (forward: csrc/block.cu row kernels; backward: csrc/train_block.cu).
+
+
+def _colsum_dev(t: torch.Tensor) -> torch.Tensor:
+    n, d = t.shape
+    part = D.empty((max(int(lib().lsrm_colsum_parts(n)), 1) * d,), torch.float32)
+    out = D.empty((d,), torch.float32)
+    call("lsrm_colsum_f32", t.data_ptr(), t.stride(0), n, d, part.data_ptr(), out.data_ptr(),
+         D.stream())
+    return out
+
+
+def _ln_bwd(x, gamma, dy, dx, accumulate):
+    """dx (+)= dLN(x)/dx . dy; returns (dgamma, dbeta)."""
+    from .recon_pipeline import LN_EPS
+    n, d = x.shape
+    parts = max(int(lib().lsrm_colsum_parts(n)), 1)
+    part = D.empty((2 * parts * d,), torch.float32)
+    dg, db = D.empty((d,), torch.float32), D.empty((d,), torch.float32)
+    call("lsrm_layer_norm_bwd_f32", x.data_ptr(), x.stride(0), n, d, gamma.data_ptr(), LN_EPS,
+         dy.data_ptr(), dy.stride(0), dx.data_ptr(), dx.stride(0), int(accumulate),
+         part.data_ptr(), dg.data_ptr(), db.data_ptr(), D.stream())
+    return dg, db
+
+
+class _LinearFn(torch.autograd.Function):
+    """y = x W (fp32 out; TF32 tensor cores when `fast`)."""
+    @staticmethod
+    def forward(ctx, x, w, fast):
+        x, w = x.detach().contiguous(), w.detach().contiguous()
+        ctx.save_for_backward(x, w)
+        ctx.fast = fast
+        return _ops.gemm_ex(x, w, tf32=fast)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, w = ctx.saved_tensors
+        dy = dy.contiguous()
+        return (_ops.gemm_ex(dy, w, trans_b=True, tf32=ctx.fast),
+                _ops.gemm_ex(x, dy, trans_a=True, tf32=ctx.fast), None)
+
+
+class _AddLNFn(torch.autograd.Function):
+    """(xe, x_hat) = (a + b, LN(a + b))."""
+    @staticmethod
+    def forward(ctx, a, b, gamma, beta, exact):
+        from .recon_pipeline import NormParams, _add_ln
+        xe, xh = _add_ln(a.detach().contiguous(), b.detach().contiguous(),
+                         NormParams(gamma.detach(), beta.detach()), exact=bool(exact))
+        ctx.save_for_backward(xe, gamma)
+        return xe, xh
+
+    @staticmethod
+    def backward(ctx, dxe, dxh):
+        xe, gamma = ctx.saved_tensors
+        dx = dxe.contiguous().clone() if dxe is not None else torch.zeros_like(xe)
+        dg, db = _ln_bwd(xe, gamma.detach().contiguous(), dxh.contiguous(), dx, True)
+        return dx, dx, dg, db, None
+
+
+class _GateMixLNFn(torch.autograd.Function):
+    """x1 = xe + s(l_s + b_s) o_s + s(l_c + b_c) o_c; h = LN(x1)."""
+    @staticmethod
+    def forward(ctx, xe, logits, gate_b, o_s, o_c, gamma, beta, exact):
+        from .recon_pipeline import NormParams, _gate_mix_ln
+        xe, logits = xe.detach().contiguous(), logits.detach().contiguous()
+        o_s, o_c = o_s.detach().contiguous(), o_c.detach().contiguous()
+        x1, h = _gate_mix_ln(int(exact), xe, logits, logits.stride(0), gate_b.detach(), o_s, o_c,
+                             NormParams(gamma.detach(), beta.detach()))
+        ctx.save_for_backward(logits, gate_b, o_s, o_c, x1, gamma)
+        return x1, h
+
+    @staticmethod
+    def backward(ctx, dx1, dh):
+        logits, gate_b, o_s, o_c, x1, gamma = ctx.saved_tensors
+        n, d = x1.shape
+        dx = dx1.contiguous().clone() if dx1 is not None else torch.zeros_like(x1)
+        dg, db = _ln_bwd(x1, gamma.detach().contiguous(), dh.contiguous(), dx, True)
+        do_s, do_c = D.empty((n, d), torch.float32), D.empty((n, d), torch.float32)
+        dl = D.empty((n, 2 * d), torch.float32)
+        call("lsrm_gate_mix_bwd_f32", logits.data_ptr(), logits.stride(0),
+             gate_b.detach().contiguous().data_ptr(), o_s.data_ptr(), o_c.data_ptr(),
+             dx.data_ptr(), n, d, do_s.data_ptr(), do_c.data_ptr(), dl.data_ptr(), D.stream())
+        return dx, dl, _colsum_dev(dl), do_s, do_c, dg, db, None
+
+
+class _BiasActFn(torch.autograd.Function):
+    """out = act(z + b) (+ residual); act 0 identity, 1 exact-erf gelu."""
+    @staticmethod
+    def forward(ctx, z, b, residual, act, exact):
+        from .recon_pipeline import _bias_act
+        z = z.detach().contiguous()
+        res = residual.detach().contiguous() if residual is not None else None
+        out = _bias_act(int(exact), z, b.detach().contiguous(), act, residual=res,
+                        out_dtype=torch.float32)
+        ctx.save_for_backward(z, b)
+        ctx.act, ctx.has_res = act, residual is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        z, b = ctx.saved_tensors
+        dout = dout.contiguous()
+        if ctx.act == 1:
+            n, d = z.shape
+            dz = D.empty((n, d), torch.float32)
+            call("lsrm_gelu_bwd_f32", z.data_ptr(), b.detach().contiguous().data_ptr(),
+                 dout.data_ptr(), n, d, dz.data_ptr(), D.stream())
+        else:
+            dz = dout
+        return dz, _colsum_dev(dz), (dout if ctx.has_res else None), None, None
+
+
+BLOCK_PARAM_NAMES = ("ln_ax_g", "ln_ax_b", "ln_ay_g", "ln_ay_b", "gate_x_w", "gate_x_b",
+                     "gate_y_w", "gate_y_b", "ln_fx_g", "ln_fx_b", "ln_fy_g", "ln_fy_b",
+                     "fx_w1", "fx_b1", "fx_w2", "fx_b2", "fy_w1", "fy_b1", "fy_w2", "fy_b2")
+
+
+class SparseBlockModule(torch.nn.Module):
+    """One trainable Stage-2 sparse block (`recon_pipeline.py:461-497`): the
+    four NSA uses (`NsaLayerModule`) plus the add + LayerNorm, use gates,
+    gated mixture + LayerNorm and FFN around them, all differentiable.
+    forward(x, y, x_inj, y_inj, part_vol, part_img, resolved) -> (x2, y2),
+    token order, fp32; `fast_backward`: bf16 tensor-core attention branches
+    and TF32 GEMMs (as NsaUseModule)."""
+
+    def __init__(self, params: AttentionParams, weights=None, seed: int = 0, layer: int = 0,
+                 fast_backward: bool = False):
+        super().__init__()
+        from .recon_pipeline import init_sparse_block
+        w = weights if weights is not None else init_sparse_block(seed, params, layer)
+        self.params, self.fast = params, fast_backward
+        uses = {"v2v": w.nsa_x_self, "v2i": w.nsa_x_cross, "i2i": w.nsa_y_self,
+                "i2v": w.nsa_y_cross}
+        self.layer = NsaLayerModule(params, weights=uses, fast_backward=fast_backward,
+                                    layer=layer)
+        arrays = {"ln_ax_g": w.ln_attn_x.gamma, "ln_ax_b": w.ln_attn_x.beta,
+                  "ln_ay_g": w.ln_attn_y.gamma, "ln_ay_b": w.ln_attn_y.beta,
+                  "gate_x_w": w.gate_x_w, "gate_x_b": w.gate_x_b,
+                  "gate_y_w": w.gate_y_w, "gate_y_b": w.gate_y_b,
+                  "ln_fx_g": w.ln_ffn_x.gamma, "ln_fx_b": w.ln_ffn_x.beta,
+                  "ln_fy_g": w.ln_ffn_y.gamma, "ln_fy_b": w.ln_ffn_y.beta,
+                  "fx_w1": w.ffn_x.w1, "fx_b1": w.ffn_x.b1, "fx_w2": w.ffn_x.w2,
+                  "fx_b2": w.ffn_x.b2, "fy_w1": w.ffn_y.w1, "fy_b1": w.ffn_y.b1,
+                  "fy_w2": w.ffn_y.w2, "fy_b2": w.ffn_y.b2}
+        for name in BLOCK_PARAM_NAMES:
+            self.register_parameter(name, torch.nn.Parameter(
+                D.dev(np.asarray(arrays[name], np.float32), torch.float32).clone()))
+
+    def _stream(self, s, e, lg, o_self, o_cross):
+        exact = not self.fast
+        x1, h = _GateMixLNFn.apply(e, lg, getattr(self, f"gate_{s}_b"), o_self, o_cross,
+                                   getattr(self, f"ln_f{s}_g"), getattr(self, f"ln_f{s}_b"),
+                                   exact)
+        u = _BiasActFn.apply(_LinearFn.apply(h, getattr(self, f"f{s}_w1"), self.fast),
+                             getattr(self, f"f{s}_b1"), None, 1, exact)
+        return _BiasActFn.apply(_LinearFn.apply(u, getattr(self, f"f{s}_w2"), self.fast),
+                                getattr(self, f"f{s}_b2"), x1, 0, exact)
+
+    def forward(self, x, y, x_inj, y_inj, part_vol, part_img, resolved: dict):
+        exact = not self.fast
+        xe, xh = _AddLNFn.apply(x, x_inj, self.ln_ax_g, self.ln_ax_b, exact)
+        ye, yh = _AddLNFn.apply(y, y_inj, self.ln_ay_g, self.ln_ay_b, exact)
+        lx = _LinearFn.apply(xh, self.gate_x_w, self.fast)
+        ly = _LinearFn.apply(yh, self.gate_y_w, self.fast)
+        o = self.layer(xh, yh, part_vol, part_img, resolved)
+        return (self._stream("x", xe, lx, o["v2v"], o["v2i"]),
+                self._stream("y", ye, ly, o["i2i"], o["i2v"]))

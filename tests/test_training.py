@@ -227,3 +227,115 @@ def test_trained_weights_round_trip_to_reference_api(cuda):
     got = mod(xg, xg, part, part, sel=L.Selection(lists)).detach().cpu().numpy()
     ref = L.nsa_cross_attention(x, x, part, part, L.Selection(lists), module_weights(mod), p)
     assert np.max(np.abs(got - ref)) < 1e-5
+
+
+# ---------------------------------------------------------------------------
+# the full Stage-2 block (recon_pipeline.py:461-497)
+
+
+def _block_instance(seed, heads, wscale, side=16, keep=0.03):
+    hq, hkv, dh = heads
+    params = O.AttentionParams(hq, hkv, dh)
+    d = params.model_dim
+    cx, cy = _coords(seed, side, keep), _coords(seed + 50, side, keep)
+    px = O.partition_tokens("volume", cx, (side,) * 3)
+    py = O.partition_tokens("volume", cy, (side,) * 3)
+    g = np.random.default_rng(seed + 1)
+    f = lambda *s, sc=wscale: (g.standard_normal(s) * sc).astype(np.float32)   # noqa: E731
+    arrays = dict(x=f(cx.shape[0], d, sc=1.0), y=f(cy.shape[0], d, sc=1.0),
+                  xi=f(cx.shape[0], d, sc=0.5), yi=f(cy.shape[0], d, sc=0.5))
+    blk = {}
+    for s_ in ("x", "y"):
+        blk[f"ln_a{s_}"] = (1.0 + f(d, sc=0.2), f(d, sc=0.2))
+        blk[f"ln_f{s_}"] = (1.0 + f(d, sc=0.2), f(d, sc=0.2))
+        blk[f"gate_{s_}"] = (f(d, 2 * d), f(2 * d))
+        blk[f"ffn_{s_}"] = (f(d, 4 * d), f(4 * d), f(4 * d, d), f(d))
+    uses = {u: _weights(seed + 10 + i, hq, hkv, dh, 3 if u in ("v2v", "i2i") else 2, scale=wscale)
+            for i, u in enumerate(("v2v", "v2i", "i2i", "i2v"))}
+    kvp = {"v2v": px, "v2i": py, "i2i": py, "i2v": px}
+    qn = {"v2v": cx.shape[0], "v2i": cx.shape[0], "i2i": cy.shape[0], "i2v": cy.shape[0]}
+    lists = {u: _lists(seed + 20 + i, qn[u], kvp[u].occupied_ids)
+             for i, u in enumerate(("v2v", "v2i", "i2i", "i2v"))}
+    return params, cx, cy, px, py, arrays, blk, uses, lists
+
+
+def _block_vs_oracle(heads, wscale, fast):
+    import paper_2604_05182_b200 as L
+    from paper_2604_05182_b200 import recon_pipeline as R
+    from paper_2604_05182_b200.nsa_attention import selection_rows
+    from paper_2604_05182_b200.training import (BLOCK_PARAM_NAMES, SparseBlockModule,
+                                                resolve_plan_rows)
+    params, cx, cy, px, py, a, blk, uses, lists = _block_instance(41, heads, wscale)
+    p = L.AttentionParams(params.n_q_heads, params.n_kv_heads, params.head_dim)
+    part_x = L.partition(L.TokenSet("volume", a["x"], cx, (16,) * 3))
+    part_y = L.partition(L.TokenSet("volume", a["y"], cy, (16,) * 3))
+    kvp = {"v2v": part_x, "v2i": part_y, "i2i": part_y, "i2v": part_x}
+    plan_rows = {u: selection_rows(L.Selection(lists[u]), kvp[u]) for u in lists}
+    resolved = resolve_plan_rows(plan_rows, part_x, part_y)
+    w = R.SparseBlockWeights(
+        _our_weights(uses["v2v"], 3), _our_weights(uses["v2i"], 2), _our_weights(uses["i2i"], 3),
+        _our_weights(uses["i2v"], 2), None, None, blk["gate_x"][0], blk["gate_x"][1],
+        blk["gate_y"][0], blk["gate_y"][1], R.NormParams(*blk["ln_ax"]),
+        R.NormParams(*blk["ln_ay"]), R.NormParams(*blk["ln_fx"]), R.NormParams(*blk["ln_fy"]),
+        R.FfnWeights(*blk["ffn_x"]), R.FfnWeights(*blk["ffn_y"]))
+    mod = SparseBlockModule(p, weights=w, fast_backward=fast)
+    ins = {k: torch.tensor(v, device="cuda", requires_grad=True) for k, v in a.items()}
+    x2, y2 = mod(ins["x"], ins["y"], ins["xi"], ins["yi"], part_x, part_y, resolved)
+    g = np.random.default_rng(9)
+    dx2 = g.standard_normal(x2.shape).astype(np.float32)
+    dy2 = g.standard_normal(y2.shape).astype(np.float32)
+    torch.autograd.backward([x2, y2], [torch.tensor(dx2, device="cuda"),
+                                       torch.tensor(dy2, device="cuda")])
+    # f64 oracle
+    t = lambda v: torch.tensor(v, dtype=torch.float64, requires_grad=True)   # noqa: E731
+    tw = {"uses": {u: _t64(uses[u], requires_grad=True) for u in uses}}
+    for k, v in blk.items():
+        tw[k] = tuple(t(z) for z in v)
+    ta = {k: t(v) for k, v in a.items()}
+    okv = {"v2v": px, "v2i": py, "i2i": py, "i2v": px}
+    oq = {"v2v": px, "v2i": px, "i2i": py, "i2v": py}
+    masks = {u: TN.key_masks(oq[u], okv[u], lists[u], u in ("v2v", "i2i")) for u in lists}
+    rx, ry = TN.sparse_block(ta["x"], ta["y"], ta["xi"], ta["yi"], tw, params, okv, masks)
+    torch.autograd.backward([rx, ry], [torch.tensor(dx2, dtype=torch.float64),
+                                       torch.tensor(dy2, dtype=torch.float64)])
+    fwd = max(_rel(x2, rx), _rel(y2, ry))
+    pairs = [(k, ins[k].grad, ta[k].grad) for k in a]
+    mp = {"ln_ax_g": tw["ln_ax"][0], "ln_ax_b": tw["ln_ax"][1], "ln_ay_g": tw["ln_ay"][0],
+          "ln_ay_b": tw["ln_ay"][1], "gate_x_w": tw["gate_x"][0], "gate_x_b": tw["gate_x"][1],
+          "gate_y_w": tw["gate_y"][0], "gate_y_b": tw["gate_y"][1], "ln_fx_g": tw["ln_fx"][0],
+          "ln_fx_b": tw["ln_fx"][1], "ln_fy_g": tw["ln_fy"][0], "ln_fy_b": tw["ln_fy"][1]}
+    for s_ in ("x", "y"):
+        for i, nm in enumerate(("w1", "b1", "w2", "b2")):
+            mp[f"f{s_}_{nm}"] = tw[f"ffn_{s_}"][i]
+    for name in BLOCK_PARAM_NAMES:
+        pairs.append((name, getattr(mod, name).grad, mp[name].grad))
+    for u in lists:
+        um = mod.layer.uses[u]
+        for name in ("w_q", "w_k", "w_v", "w_o", "gate_w", "gate_b"):
+            pairs.append((f"{u}.{name}", getattr(um, name).grad, tw["uses"][u][name].grad))
+        for tag in ("ck", "cv"):
+            for i, s_ in enumerate(("w1", "b1", "w2", "b2")):
+                pairs.append((f"{u}.{tag}_{s_}", getattr(um, f"{tag}_{s_}").grad,
+                              tw["uses"][u][tag][i].grad))
+    floor = 1e-2 * max(float(b.abs().max()) for _, _, b in pairs)
+    return fwd, {n: _rel(x_, y_, floor) for n, x_, y_ in pairs}
+
+
+@pytest.mark.gpu
+def test_gpu_block_backward_matches_f64_autograd(cuda):
+    """SparseBlockModule (fp32 kernels): forward and every gradient (inputs,
+    injections, LayerNorms, use gates, FFN, the four uses' weights) within
+    GRAD_RTOL of the f64 autograd block."""
+    fwd, errs = _block_vs_oracle((4, 2, 8), 0.3, False)
+    bad = {n: e for n, e in errs.items() if e > GRAD_RTOL}
+    print(f"block fp32: fwd {fwd:.2e}, worst grad {max(errs.values()):.2e}")
+    assert fwd < 1e-5 and not bad, (fwd, bad)
+
+
+@pytest.mark.gpu
+def test_gpu_block_backward_paper_heads_fast(cuda):
+    """Paper heads, fast path (bf16 tensor-core branches, TF32 GEMMs)."""
+    fwd, errs = _block_vs_oracle((32, 2, 32), 0.03, True)
+    bad = {n: e for n, e in errs.items() if e > FAST_RTOL}
+    print(f"block fast: fwd {fwd:.2e}, worst grad {max(errs.values()):.2e}")
+    assert fwd < FAST_RTOL and not bad, (fwd, bad)
