@@ -642,7 +642,7 @@ def time_setup(wl_name, reps=5):
 def time_train_step(inst, steps=3):
     """Training step of one full Stage-2 block (SURVEY §8f ranks 1-2,
     BASELINE config 5's fwd+bwd at one layer): training.SparseBlockModule,
-    fast path (bf16 tensor-core branches, TF32 GEMMs, fp32 master weights):
+    fast path (bf16 tensor-core branches and tcgen05 GEMMs, fp32 master weights):
     add + LayerNorm, use gates, the four NSA uses, gated mixture +
     LayerNorm, FFN, residuals; loss = sum of squares of both outputs; then
     one Adam step. Device events around forward, backward and the step."""
@@ -686,8 +686,9 @@ def time_train_step(inst, steps=3):
     return {"ms_per_step": f + b + o, "forward_ms": f, "backward_ms": b, "optimizer_ms": o,
             "tokens_per_s": n_tok / ((f + b + o) * 1e-3),
             "what": "one full Stage-2 block (4 gated NSA uses + add/LN, use gates, gated "
-                    "mixture/LN, FFN 4d, residuals): fwd + bwd + Adam step, bf16 tensor-core "
-                    "attention branches, TF32 GEMMs, fp32 master weights"}
+                    "mixture/LN, FFN 4d, residuals): fwd + bwd + Adam step; bf16 mma.sync "
+                    "attention branches, bf16 tcgen05 GEMMs (fp32 accumulation), fp32 master "
+                    "weights"}
 
 
 def pcie_bandwidth(sizes=(64 << 20, 128 << 20, 256 << 20), reps=5):

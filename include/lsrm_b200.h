@@ -617,6 +617,10 @@ int lsrm_colsum_f32(const float* x, int64_t ld, int64_t n, int d, float* part, f
 int lsrm_gate_mix_bwd_f32(const float* logits, int64_t ld_l, const float* bias, const float* o_s,
                           const float* o_c, const float* dx1, int64_t n, int d, float* do_s,
                           float* do_c, float* dlogits, void* stream);
+/* dst [cols][rows_pad] bf16 = src[rows][cols]^T (f32, row stride ld), rows
+ * past `rows` zero: the K-major operands of the training GEMMs. */
+int lsrm_transpose_cast_bf16(const float* src, int64_t ld, int64_t rows, int64_t cols,
+                             void* dst, int64_t rows_pad, void* stream);
 /* dt = du * gelu'(z + bias) (exact erf gelu). */
 int lsrm_gelu_bwd_f32(const float* z, const float* bias, const float* du, int64_t n, int d,
                       float* dt, void* stream);

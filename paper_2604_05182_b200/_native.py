@@ -105,6 +105,7 @@ SIGNATURES = {
     "lsrm_colsum_f32": (I32, [P, I64, I64, I32, P, P, P]),
     "lsrm_gate_mix_bwd_f32": (I32, [P, I64, P, P, P, P, I64, I32, P, P, P, P]),
     "lsrm_gelu_bwd_f32": (I32, [P, P, P, I64, I32, P, P]),
+    "lsrm_transpose_cast_bf16": (I32, [P, I64, I64, I64, P, I64, P]),
 }
 
 _lib = None

@@ -127,3 +127,47 @@ def gemm_bf16(a: torch.Tensor, bt: torch.Tensor, out=None, out_dtype=torch.bfloa
     out = D.empty((a.shape[0], bt.shape[0]), out_dtype) if out is None else out
     gemm_tc([gemm_problem(a, bt, out, bias, res, gelu)])
     return out
+
+
+def transpose_bf16(x: torch.Tensor, pad_to: int = 8) -> torch.Tensor:
+    """[r, c] f32 -> [c, r_pad] bf16 (zero rows r..r_pad): a K-major operand."""
+    r, c = x.shape
+    rp = (r + pad_to - 1) // pad_to * pad_to
+    out = D.empty((c, rp), torch.bfloat16)
+    call("lsrm_transpose_cast_bf16", x.data_ptr(), x.stride(0), r, c, out.data_ptr(), rp,
+         D.stream())
+    return out
+
+
+def cast_pad_bf16(x: torch.Tensor, cols_pad: int) -> torch.Tensor:
+    """[r, c] f32 -> [r, cols_pad] bf16, zero columns c..cols_pad."""
+    r, c = x.shape
+    if cols_pad == c and x.is_contiguous():
+        return cast(x, torch.bfloat16)
+    out = D.empty((r, cols_pad), torch.bfloat16)
+    xt = x.t().contiguous()                 # [c, r] f32 (cold path: unaligned K)
+    call("lsrm_transpose_cast_bf16", xt.data_ptr(), xt.stride(0), c, r, out.data_ptr(),
+         cols_pad, D.stream())
+    return out
+
+
+def gemm_train(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, out=None,
+               beta=0.0) -> torch.Tensor:
+    """fp32 out (+)= op(a) @ op(b) on the tcgen05 GEMM, bf16 operands, fp32
+    accumulation (the training path's GEMMs; gemm_ex's signature). Operands
+    are cast / transposed into the K-major layouts gemm_tc takes, K padded
+    with zeros to a multiple of 8. N must be a multiple of 8 (every training
+    GEMM's N is: d, 4d, n_gates*d, h_kv*d_h)."""
+    assert a.dtype == b.dtype == torch.float32 and beta in (0.0, 1.0)
+    m, k = (a.shape[1], a.shape[0]) if trans_a else a.shape
+    k2, n = (b.shape[1], b.shape[0]) if trans_b else b.shape
+    assert k == k2 and n % 8 == 0, (k, k2, n)
+    acc = out is not None and beta == 1.0
+    dst = out if out is not None else D.empty((m, n), torch.float32)
+    if m == 0 or n == 0:
+        return dst
+    kp = (k + 7) // 8 * 8
+    am = transpose_bf16(a) if trans_a else cast_pad_bf16(a, kp)      # [m, kp]
+    bt = cast_pad_bf16(b, kp) if trans_b else transpose_bf16(b)      # [n, kp]
+    gemm_tc([gemm_problem(am, bt, dst, res=dst if acc else None)])
+    return dst

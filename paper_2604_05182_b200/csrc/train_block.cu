@@ -172,6 +172,24 @@ __global__ void gelu_bwd_kernel(const float* __restrict__ z, const float* __rest
   }
 }
 
+// dst[c][r] = bf16(src[r][c]) for r < rows, 0 for rows <= r < rows_pad:
+// 32 x 32 tiles through shared memory (coalesced both ways)
+__global__ void transpose_cast_kernel(const float* __restrict__ src, int64_t ld, int64_t rows,
+                                      int64_t cols, __nv_bfloat16* __restrict__ dst,
+                                      int64_t rows_pad) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * ld + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows_pad) dst[c * rows_pad + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+  }
+}
+
 }  // namespace tb
 }  // namespace lsrm
 
@@ -239,6 +257,17 @@ int lsrm_gate_mix_bwd_f32(const float* logits, int64_t ld_l, const float* bias, 
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
   tb::gate_mix_bwd_kernel<<<grid, 256, 0, as_stream(stream)>>>(logits, ld_l, bias, o_s, o_c, dx1,
                                                                n, d, do_s, do_c, dlogits);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
+
+int lsrm_transpose_cast_bf16(const float* src, int64_t ld, int64_t rows, int64_t cols,
+                             void* dst, int64_t rows_pad, void* stream) {
+  LSRM_REQUIRE(rows_pad >= rows && ld >= cols, "transpose_cast: bad shape");
+  if (cols == 0 || rows_pad == 0) return LSRM_OK;
+  const dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows_pad, 32));
+  tb::transpose_cast_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(
+      src, ld, rows, cols, (__nv_bfloat16*)dst, rows_pad);
   LSRM_LAUNCHED();
   return LSRM_OK;
 }

@@ -10,7 +10,10 @@ and a backward built from
                                 dQ pass and a key-major dK/dV pass, no atomics),
   * `lsrm_gate_merge_bwd_f32` - the sigmoid-gated merge,
   * `lsrm_res_block_bwd_f32`  - the compression ResBlock under the block mean,
-  * `lsrm_gemm_f32_ex`        - every projection / weight gradient (cuBLAS),
+  * every projection / weight gradient: `lsrm_gemm_f32_ex` (cuBLAS fp32) on
+                                the reference-precision path, the tcgen05
+                                GEMM (`_ops.gemm_train`, bf16 operands, fp32
+                                accumulation) on the fast path,
 
 wrapped in a `torch.autograd.Function` so a `torch.optim` optimizer can step
 the weights. `SparseBlockModule` adds the block around the uses (add +
@@ -64,7 +67,7 @@ def _forward(spec: _Spec, x, kv, P):
     width = hkv * dh
     part = spec.part_kv
     fast = _mma_ok(spec)
-    mm = lambda a, b: _ops.gemm_ex(a, b, tf32=fast)   # noqa: E731
+    mm = _ops.gemm_train if fast else _ops.gemm_ex   # fast: bf16 tcgen05 GEMMs
     q = mm(x, P["w_q"])
     k = mm(kv, P["w_k"])
     v = mm(kv, P["w_v"])
@@ -134,7 +137,7 @@ def _backward(spec: _Spec, P, s, dout):
     fast = _mma_ok(spec)
 
     def gx(a, b, **kw):
-        return _ops.gemm_ex(a, b, tf32=fast, **kw)
+        return (_ops.gemm_train if fast else _ops.gemm_ex)(a, b, **kw)
     # out = merged W_o
     dmerged = gx(dout, P["w_o"], trans_b=True)
     g["w_o"] = gx(s["merged"], dout, trans_a=True)
@@ -376,20 +379,20 @@ def _ln_bwd(x, gamma, dy, dx, accumulate):
 
 
 class _LinearFn(torch.autograd.Function):
-    """y = x W (fp32 out; TF32 tensor cores when `fast`)."""
+    """y = x W (fp32 out; `fast`: bf16 operands on the tcgen05 GEMM)."""
     @staticmethod
     def forward(ctx, x, w, fast):
         x, w = x.detach().contiguous(), w.detach().contiguous()
         ctx.save_for_backward(x, w)
         ctx.fast = fast
-        return _ops.gemm_ex(x, w, tf32=fast)
+        return (_ops.gemm_train if fast else _ops.gemm_ex)(x, w)
 
     @staticmethod
     def backward(ctx, dy):
         x, w = ctx.saved_tensors
         dy = dy.contiguous()
-        return (_ops.gemm_ex(dy, w, trans_b=True, tf32=ctx.fast),
-                _ops.gemm_ex(x, dy, trans_a=True, tf32=ctx.fast), None)
+        mm = _ops.gemm_train if ctx.fast else _ops.gemm_ex
+        return mm(dy, w, trans_b=True), mm(x, dy, trans_a=True), None
 
 
 class _AddLNFn(torch.autograd.Function):
