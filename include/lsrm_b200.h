@@ -440,6 +440,18 @@ int lsrm_gather_rows(int elem_bytes, const void* src, int64_t ld_src,
 int lsrm_scatter_rows(int elem_bytes, const void* src, int64_t ld_src,
                       const int64_t* index, int64_t n, int64_t row_elems,
                       void* dst, int64_t ld_dst, void* stream);
+/* Host rows -> device rows for the reference API's NumPy inputs
+ * (nsa_attention.py:287 `nsa_cross_attention(x, kv_feats, ...)` takes host
+ * arrays).  src is HOST f32 (pageable is fine), [*, ld_src]; row i of dst
+ * (device, [n_rows, ld_dst]) is src row row_index[i] (row_index is a HOST
+ * int64 array, NULL = identity), converted to bf16 (round-to-nearest-even,
+ * bit-identical to lsrm_cast) when to_bf16, else copied as f32.  Host
+ * threads convert into pinned staging chunks that are copied on `stream`
+ * while the next chunk is converted; returns once src has been read (the
+ * copies complete in stream order).  lsrm_host_threads(): the pool size. */
+int lsrm_host_threads(void);
+int lsrm_h2d_rows(int to_bf16, const float* src, int64_t ld_src, const int64_t* row_index,
+                  int64_t n_rows, int64_t row_elems, void* dst, int64_t ld_dst, void* stream);
 /* f32 <-> bf16 conversion, LayerNorm (tensor_core.py:139-146). */
 int lsrm_cast(int to_bf16, const void* src, void* dst, int64_t n, void* stream);
 int lsrm_layer_norm(int in_bf16, const void* x, int64_t n, int d,

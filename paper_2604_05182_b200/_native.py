@@ -106,6 +106,8 @@ SIGNATURES = {
     "lsrm_gate_mix_bwd_f32": (I32, [P, I64, P, P, P, P, I64, I32, P, P, P, P]),
     "lsrm_gelu_bwd_f32": (I32, [P, P, P, I64, I32, P, P]),
     "lsrm_transpose_cast_bf16": (I32, [P, I64, I64, I64, P, I64, P]),
+    "lsrm_host_threads": (I32, []),
+    "lsrm_h2d_rows": (I32, [I32, P, I64, P, I64, I64, P, I64, P]),
 }
 
 _lib = None

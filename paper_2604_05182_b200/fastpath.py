@@ -38,6 +38,7 @@ import torch
 
 from . import _dev as D
 from . import _ops
+from ._native import call
 from .errors import require
 
 _STATE = {"precision": "fp32"}
@@ -176,7 +177,24 @@ def _download(t: torch.Tensor) -> np.ndarray:
 
 
 def _to_block_major(a, part, dtype):
-    """token-order rows (host or device, any float) -> block-major device rows."""
+    """token-order rows (host or device, any float) -> block-major device rows.
+    Host rows go through `lsrm_h2d_rows`: the row permutation and the bf16
+    rounding happen on host threads into pinned staging chunks that are
+    copied while the next chunk is converted (csrc/hostio.cu)."""
+    if not isinstance(a, torch.Tensor):
+        a = np.asarray(a)
+        if a.dtype != np.float32 or not a.flags.c_contiguous:
+            a = np.ascontiguousarray(a, dtype=np.float32)
+        require(a.ndim == 2 and a.shape[0] == part.n_tokens,
+                "feature rows do not match the partition")
+        idx = part.block_token_ids
+        if idx.dtype != np.int64 or not idx.flags.c_contiguous:
+            idx = np.ascontiguousarray(idx, dtype=np.int64)
+        n, d = a.shape
+        out = D.empty((n, d), dtype)
+        call("lsrm_h2d_rows", int(dtype == torch.bfloat16), a.ctypes.data, d, idx.ctypes.data,
+             n, d, out.data_ptr(), d, D.stream())
+        return out
     t = _upload(a)
     g = _ops.gather_rows(t, part.dev("block_token_ids"))
     return g if dtype == torch.float32 else _ops.cast(g, dtype)

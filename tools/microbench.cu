@@ -209,6 +209,49 @@ __global__ void xu_kernel(float* out, long long* clk) {
   if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
 }
 
+// Full per-pair softmax work, register-resident: MODE 0 = 2 FFMA + 2 ex2.f32 +
+// cvt.rn.bf16x2 (the kernel today); MODE 1 = 2 FFMA + cvt.rn.f16x2.f32 +
+// ex2.approx.f16x2 (P as packed f16); MODE 2 = MODE 1 with ex2.approx.ftz.bf16x2
+// on a bf16x2 argument (not accurate enough; throughput reference only).
+template <int MODE>
+__global__ void pair_kernel(float* out, long long* clk) {
+  float s[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) s[j] = -0.01f * (threadIdx.x + j);
+  const float sl2 = 0.25f;
+  float nb = -1.f;
+  uint32_t acc = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < kIters / 8; ++it) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float a = fmaf(s[2 * j], sl2, nb), b = fmaf(s[2 * j + 1], sl2, nb);
+      uint32_t w;
+      if (MODE == 0) {
+        float ea, eb;
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(ea) : "f"(a));
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(eb) : "f"(b));
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w) : "f"(eb), "f"(ea));
+      } else if (MODE == 1) {
+        uint32_t h;
+        asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+        asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(w) : "r"(h));
+      } else {
+        uint32_t h;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));
+        asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(w) : "r"(h));
+      }
+      acc += w;
+    }
+    nb -= 1e-7f;
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)acc;
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+}
+
 int main() {
   float* out;
   long long* clk;
@@ -270,5 +313,21 @@ int main() {
       printf("exp phase %-12s warps %d: %.2f exp/clk/SM (%.0f clk per 128x128-per-warp-group chunk-equivalent)\n",
              en[mode], w, elems / h[0], (double)h[0] / 64);
     }
+  {
+    const char* pn[3] = {"f32: 2 FFMA+2 MUFU+F2FP", "f16x2: 2 FFMA+F2FP+MUFU.f16x2",
+                         "bf16x2: 2 FFMA+F2FP+MUFU.bf16x2"};
+    for (int warps = 4; warps <= 16; warps *= 2)
+      for (int mode = 0; mode < 3; ++mode) {
+        for (int rep = 0; rep < 2; ++rep) {
+          if (mode == 0) pair_kernel<0><<<148, 32 * warps>>>(out, clk);
+          if (mode == 1) pair_kernel<1><<<148, 32 * warps>>>(out, clk);
+          if (mode == 2) pair_kernel<2><<<148, 32 * warps>>>(out, clk);
+        }
+        cudaDeviceSynchronize();
+        cudaMemcpy(h, clk, sizeof(h), cudaMemcpyDeviceToHost);
+        double ex = (double)(kIters / 8) * 32 * 32 * warps;
+        printf("pair %-34s warps %2d: %.2f exp/clk/SM\n", pn[mode], warps, ex / h[0]);
+      }
+  }
   return 0;
 }
