@@ -294,6 +294,13 @@ int lsrm_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a,
 #define LSRM_GEMM_BIAS_F32 2   /* bias is f32 (else bf16) */
 #define LSRM_GEMM_RES_F32  4   /* res is f32 (else bf16) */
 #define LSRM_GEMM_GELU     8   /* act = exact-erf gelu, applied before res */
+/* MN-major operands (no transposed copy needed; e.g. weight gradients
+ * X^T . dY take X [k,m] and dY [k,n] as stored):
+ *   A_MN: `a` is A^T stored row-major, [k, m] with row stride lda >= m;
+ *   B_MN: `bt` is B stored row-major, [k, n] with row stride ldb >= n.
+ * Rows of an MN-major operand past k read as zeros. */
+#define LSRM_GEMM_A_MN    16
+#define LSRM_GEMM_B_MN    32
 typedef struct lsrm_gemm_problem {
   int64_t m, n, k;
   const void* a;  int64_t lda;
@@ -304,7 +311,9 @@ typedef struct lsrm_gemm_problem {
   int32_t flags;
   int32_t reserved;
 } lsrm_gemm_problem;
-/* problems: HOST array of n_problems descriptors. */
+/* problems: HOST array of n_problems descriptors.  With A_MN / B_MN the
+ * K-major rules above apply to the remaining K-major operand only (k % 8 == 0
+ * when one is K-major). */
 int lsrm_gemm_tc(const lsrm_gemm_problem* problems, int n_problems, void* stream);
 
 /* ---- fused bf16 three-branch NSA attention, tcgen05/TMEM  -------------
@@ -613,8 +622,8 @@ int lsrm_all_to_all_v(void* comm, int rank, int world, const void* send,
  * training; forward lsrm/recon_pipeline.py:461-497).
  * fp32, deterministic (fixed-order partial sums, no float atomics).
  * colsum_parts(n): rows of partial sums a reduction over n rows needs
- * (workspace `part` = 2 * parts * d floats for layer_norm_bwd, parts * d
- * for colsum). */
+ * (workspace `part` = 2 * parts * d + 2 * n floats for layer_norm_bwd: the
+ * partials and the rows' mean / rstd; parts * d for colsum). */
 int64_t lsrm_colsum_parts(int64_t n);
 /* dx (+)= dLN(x)/dx . dy; dgamma = sum_rows dy x_hat; dbeta = sum_rows dy. */
 int lsrm_layer_norm_bwd_f32(const float* x, int64_t ld_x, int64_t n, int d, const float* gamma,

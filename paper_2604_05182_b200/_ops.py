@@ -90,19 +90,25 @@ class GemmProblem(C.Structure):
                 ("reserved", C.c_int32)]
 
 
-GEMM_OUT_F32, GEMM_BIAS_F32, GEMM_RES_F32, GEMM_GELU = 1, 2, 4, 8
+GEMM_OUT_F32, GEMM_BIAS_F32, GEMM_RES_F32, GEMM_GELU, GEMM_A_MN, GEMM_B_MN = 1, 2, 4, 8, 16, 32
 
 
 def gemm_problem(a: torch.Tensor, bt: torch.Tensor, out: torch.Tensor, bias=None, res=None,
-                 gelu=False) -> GemmProblem:
+                 gelu=False, a_mn=False, b_mn=False, k=None) -> GemmProblem:
     """One tcgen05 GEMM problem: out = act(a @ bt^T + bias) + res, with a
-    [m,k] and bt [n,k] bf16 (K contiguous: bt is the weight transposed)."""
-    m, k = a.shape
-    n, k2 = bt.shape
-    assert k == k2 and a.dtype == bt.dtype == torch.bfloat16
+    [m,k] and bt [n,k] bf16 (K contiguous: bt is the weight transposed).
+    a_mn: `a` is A^T as stored, [k,m]; b_mn: `bt` is B as stored, [k,n]
+    (MN-major operands, no transposed copy).  k: the contraction length when
+    it is shorter than an MN-major operand's rows (rows past it read as 0
+    only past the operand's end, so pass k = rows unless padding is zero)."""
+    m, ka = (a.shape[1], a.shape[0]) if a_mn else a.shape
+    n, kb = (bt.shape[1], bt.shape[0]) if b_mn else bt.shape
+    assert ka == kb and a.dtype == bt.dtype == torch.bfloat16, (ka, kb)
+    k = ka if k is None else k
     assert a.stride(1) == 1 and bt.stride(1) == 1 and out.stride(1) == 1
     assert tuple(out.shape) == (m, n)
     flags = (GEMM_OUT_F32 if out.dtype == torch.float32 else 0) | (GEMM_GELU if gelu else 0)
+    flags |= (GEMM_A_MN if a_mn else 0) | (GEMM_B_MN if b_mn else 0)
     if bias is not None:
         flags |= GEMM_BIAS_F32 if bias.dtype == torch.float32 else 0
     if res is not None:
@@ -152,12 +158,15 @@ def cast_pad_bf16(x: torch.Tensor, cols_pad: int) -> torch.Tensor:
 
 
 def gemm_train(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, out=None,
-               beta=0.0) -> torch.Tensor:
+               beta=0.0, cache: dict = None) -> torch.Tensor:
     """fp32 out (+)= op(a) @ op(b) on the tcgen05 GEMM, bf16 operands, fp32
-    accumulation (the training path's GEMMs; gemm_ex's signature). Operands
-    are cast / transposed into the K-major layouts gemm_tc takes, K padded
-    with zeros to a multiple of 8. N must be a multiple of 8 (every training
-    GEMM's N is: d, 4d, n_gates*d, h_kv*d_h)."""
+    accumulation (the training path's GEMMs; gemm_ex's signature).  Operands
+    are only cast: a transposed operand is passed MN-major (as stored), so the
+    weight-gradient GEMMs X^T . dY need no transposed copies.  A K-major
+    operand with k % 8 != 0 is zero-padded (the MN-major one gets zero rows).
+    `cache` (optional dict) reuses the bf16 copy of a tensor cast earlier in
+    the same backward pass.  N must be a multiple of 8 (every training GEMM's
+    N is: d, 4d, n_gates*d, h_kv*d_h)."""
     assert a.dtype == b.dtype == torch.float32 and beta in (0.0, 1.0)
     m, k = (a.shape[1], a.shape[0]) if trans_a else a.shape
     k2, n = (b.shape[1], b.shape[0]) if trans_b else b.shape
@@ -166,6 +175,34 @@ def gemm_train(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, o
     dst = out if out is not None else D.empty((m, n), torch.float32)
     if m == 0 or n == 0:
         return dst
+    a_mn, b_mn = trans_a, not trans_b
+    kp = k if (a_mn and b_mn) else (k + 7) // 8 * 8
+
+    def bf(x, mn):
+        plain = kp == k and (x.is_contiguous() or not mn)   # the copy is cast(x) as stored
+        key = (x.data_ptr(), tuple(x.shape), tuple(x.stride())) + (() if plain else (mn, kp))
+        if cache is not None and key in cache:
+            return cache[key][1]
+        if not mn:                           # K-major [rows, k] -> [rows, kp]
+            y = cast_pad_bf16(x, kp)
+        elif x.shape[1] % 8:                 # MN-major, row stride padded to 8 (cold path)
+            cols = x.shape[1]
+            y = cast_pad_bf16(x, (cols + 7) // 8 * 8)
+            if kp != k:
+                y = torch.cat([y, y.new_zeros((kp - k, y.shape[1]))])
+            y = y[:, :cols]
+        elif kp == k:                        # MN-major [k, cols] as stored
+            y = cast(x.contiguous(), torch.bfloat16)
+        else:                                # MN-major with kp - k zero rows
+            y = D.empty((kp, x.shape[1]), torch.bfloat16)
+            y[k:].zero_()
+            call("lsrm_cast", 1, x.contiguous().data_ptr(), y.data_ptr(), x.numel(), D.stream())
+        if cache is not None:
+            cache[key] = (x, y)              # x kept alive: its address cannot be reused
+        return y
+    gemm_tc([gemm_problem(bf(a, a_mn), bf(b, b_mn), dst, res=dst if acc else None, a_mn=a_mn,
+                          b_mn=b_mn)])
+    return dst
     kp = (k + 7) // 8 * 8
     am = transpose_bf16(a) if trans_a else cast_pad_bf16(a, kp)      # [m, kp]
     bt = cast_pad_bf16(b, kp) if trans_b else transpose_bf16(b)      # [n, kp]

@@ -12,7 +12,11 @@
 // Problem g:  C_g[m,n] = epi(A_g[m,k] . Wt_g[n,k]^T)
 //   A   bf16 [m,k] row-major (K contiguous, row stride lda)
 //   Wt  bf16 [n,k] (the weight TRANSPOSED, K contiguous, row stride ldb):
-//       both operands are K-major, the canonical UMMA layout
+//       both K-major, the canonical UMMA layout; or, per problem, either
+//       operand MN-major (A^T [k,m] / W [k,n] as stored, flags A_MN / B_MN):
+//       TMA boxes of 64 (MN) x 64 (K) with SWIZZLE_128B, UMMA descriptors
+//       with LBO = 8 KB between 64-wide MN atoms and SBO = 1 KB between
+//       8-row K groups, the instruction descriptor's transpose bits set
 //   epi(acc) = act(acc + bias[n]) (+ res[m,n])  -> bf16 or f32
 //
 // One persistent launch runs every problem of the group: 148 CTAs (one per
@@ -69,6 +73,13 @@ struct __align__(64) Params {
 
 __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+}
+
+// MN-major SW128 operand: 64-element MN atoms 8 KB apart (one TMA box each),
+// 8-row K groups 1 KB apart; a 16-element K step advances 2 KB
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)(8192 >> 4) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
 
 __device__ __forceinline__ void locate(const Params& P, int64_t t, int& g, int64_t& mt, int& nt) {
@@ -277,25 +288,41 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         const int kb_n = (int)((P.p[g].k + BK - 1) / BK);
         const int32_t arow = (int32_t)(mt * BM * CG + rank * BM);
         const int32_t brow = (int32_t)(nt * BN + rank * C::kBRows);
+        const bool a_mn = P.p[g].flags & LSRM_GEMM_A_MN, b_mn = P.p[g].flags & LSRM_GEMM_B_MN;
+        // one box: K-major {BK, rows} at (k, row); MN-major {64, BK} at (row, k)
+        auto load = [&](uint8_t* dst, const CUtensorMap* map, int32_t x, int32_t y,
+                        uint64_t* bar_local, uint32_t bar_cluster) {
+          if constexpr (CG == 1) {
+            tma_load_2d(dst, map, x, y, bar_local);
+          } else {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+                "l"(map), "r"(x), "r"(y), "r"(bar_cluster)
+                : "memory");
+          }
+        };
         for (int kb = 0; kb < kb_n; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 1) {
             mbar_expect_tx(&full[stage], C::kStageBytes);
-            tma_load_2d(stage_a(stage), &P.ta[g], kb * BK, arow, &full[stage]);
-            tma_load_2d(stage_b(stage), &P.tb[g], kb * BK, brow, &full[stage]);
           } else {
             if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
-            const uint32_t fb = leader_addr(&full[stage]);
-            asm volatile(
-                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(stage_a(stage))),
-                "l"(&P.ta[g]), "r"(kb * BK), "r"(arow), "r"(fb)
-                : "memory");
-            asm volatile(
-                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(stage_b(stage))),
-                "l"(&P.tb[g]), "r"(kb * BK), "r"(brow), "r"(fb)
-                : "memory");
+          }
+          const uint32_t fb = CG == 1 ? 0u : leader_addr(&full[stage]);
+          if (a_mn) {
+#pragma unroll
+            for (int h = 0; h < BM / 64; ++h)
+              load(stage_a(stage) + h * 8192, &P.ta[g], arow + 64 * h, kb * BK, &full[stage], fb);
+          } else {
+            load(stage_a(stage), &P.ta[g], kb * BK, arow, &full[stage], fb);
+          }
+          if (b_mn) {
+#pragma unroll
+            for (int h = 0; h < C::kBRows / 64; ++h)
+              load(stage_b(stage) + h * 8192, &P.tb[g], brow + 64 * h, kb * BK, &full[stage], fb);
+          } else {
+            load(stage_b(stage), &P.tb[g], kb * BK, brow, &full[stage], fb);
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
@@ -303,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     }
   } else if (warp == 1 && rank == 0) {
     // ---------------- MMA issuer (leader CTA) ----------------
-    const uint32_t idesc = idesc_bf16(BM * CG, BN, 0);
+    const uint32_t idesc0 = idesc_bf16(BM * CG, BN, 0);
     uint32_t stage = 0, phase = 0;
     int it = 0;
     for (int64_t t = unit0; t < P.total_tiles; t += n_units, ++it) {
@@ -311,6 +338,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       int64_t mt;
       locate(P, t, g, mt, nt);
       const int kb_n = (int)((P.p[g].k + BK - 1) / BK);
+      const bool a_mn = P.p[g].flags & LSRM_GEMM_A_MN, b_mn = P.p[g].flags & LSRM_GEMM_B_MN;
+      // transpose bits of the instruction descriptor: 15 = A, 16 = B MN-major
+      const uint32_t idesc = idesc0 | (a_mn ? 1u << 15 : 0u) | (b_mn ? 1u << 16 : 0u);
+      // per 16-element K step, in 16-byte descriptor units: K-major +32 B, MN-major +2 KB
+      const uint64_t ka = a_mn ? 128 : 2, kbs = b_mn ? 128 : 2;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
@@ -320,17 +352,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         mbar_wait(&full[stage], phase);
         tc_after_sync();
         if (elect_one_sync()) {
-          const uint64_t da = sdesc_sw128(smem_u32(stage_a(stage)));
-          const uint64_t db = sdesc_sw128(smem_u32(stage_b(stage)));
+          const uint64_t da = a_mn ? sdesc_sw128_mn(smem_u32(stage_a(stage)))
+                                   : sdesc_sw128(smem_u32(stage_a(stage)));
+          const uint64_t db = b_mn ? sdesc_sw128_mn(smem_u32(stage_b(stage)))
+                                   : sdesc_sw128(smem_u32(stage_b(stage)));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {   // +32 bytes per 16-element K step
             if constexpr (CG == 1) {
-              mma_bf16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+              mma_bf16(d_tmem, da + ka * k, db + kbs * k, idesc, (kb | k) != 0);
             } else {
               asm volatile(
                   "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                   "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-                  "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"((uint32_t)((kb | k) != 0)));
+                  "l"(da + ka * k), "l"(db + kbs * k), "r"(idesc), "r"((uint32_t)((kb | k) != 0)));
             }
           }
           if constexpr (CG == 1) {
@@ -502,20 +536,25 @@ extern "C" int lsrm_gemm_tc(const lsrm_gemm_problem* probs, int n_problems, void
     LSRM_REQUIRE(q.m >= 0 && q.n >= 0 && q.k >= 0, "gemm_tc: negative size");
     if (q.m == 0 || q.n == 0) continue;
     LSRM_REQUIRE(q.k > 0, "gemm_tc: k must be positive");
-    LSRM_REQUIRE(q.k % 8 == 0 && q.n % 8 == 0 && q.lda % 8 == 0 && q.ldb % 8 == 0 &&
-                     q.ldc % 8 == 0 && (q.res == nullptr || q.ldr % 8 == 0),
+    const bool a_mn = q.flags & LSRM_GEMM_A_MN, b_mn = q.flags & LSRM_GEMM_B_MN;
+    LSRM_REQUIRE(((a_mn && b_mn) || q.k % 8 == 0) && q.n % 8 == 0 && q.lda % 8 == 0 &&
+                     q.ldb % 8 == 0 && q.ldc % 8 == 0 && (q.res == nullptr || q.ldr % 8 == 0),
                  "gemm_tc: k, n and every row stride must be multiples of 8 elements");
-    LSRM_REQUIRE(q.lda >= q.k && q.ldb >= q.k && q.ldc >= q.n,
+    LSRM_REQUIRE(q.lda >= (a_mn ? q.m : q.k) && q.ldb >= (b_mn ? q.n : q.k) && q.ldc >= q.n,
                  "gemm_tc: row stride smaller than the row");
     const uintptr_t al = (uintptr_t)q.a | (uintptr_t)q.bt | (uintptr_t)q.c |
                          (uintptr_t)q.bias | (uintptr_t)q.res;
     LSRM_REQUIRE((al & 15) == 0, "gemm_tc: pointers must be 16-byte aligned");
     const bool c32 = q.flags & LSRM_GEMM_OUT_F32;
-    int rc = make_map(&p.ta[n], q.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q.k, q.m, q.lda, BK, BM,
-                      CU_TENSOR_MAP_SWIZZLE_128B);
+    int rc = a_mn ? make_map(&p.ta[n], q.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q.m, q.k, q.lda,
+                             64, BK, CU_TENSOR_MAP_SWIZZLE_128B)
+                  : make_map(&p.ta[n], q.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q.k, q.m, q.lda,
+                             BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!rc)
-      rc = make_map(&p.tb[n], q.bt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q.k, q.n, q.ldb, BK,
-                    BN / cg, CU_TENSOR_MAP_SWIZZLE_128B);
+      rc = b_mn ? make_map(&p.tb[n], q.bt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q.n, q.k, q.ldb,
+                           64, BK, CU_TENSOR_MAP_SWIZZLE_128B)
+                : make_map(&p.tb[n], q.bt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, q.k, q.n, q.ldb,
+                           BK, BN / cg, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!rc)
       rc = make_map(&p.tc[n], q.c, c32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                     c32 ? 4 : 2, q.n, q.m, q.ldc, c32 ? 16 : 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);

@@ -23,6 +23,93 @@ namespace tb {
 constexpr int kRowsPerCta = 64;     // row range of one CTA's partial column sums
 constexpr int kWarps = 8;
 
+// dx (+)= rstd (g - mean(g) - x_hat mean(g x_hat)), g = dy gamma: one warp
+// per row, float4 columns (lane owns columns 4 lane + 128 j), the row's mean
+// and rstd written for the column sums below.  V4 = d / 128 float4 per lane.
+template <int V4>
+__global__ void __launch_bounds__(256) layer_norm_bwd_rows_kernel(
+    const float* __restrict__ x, int64_t ld_x, int64_t n, int d,
+    const float* __restrict__ gamma, float eps, const float* __restrict__ dy, int64_t ld_dy,
+    float* __restrict__ dx, int64_t ld_dx, int accumulate, float2* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= n) return;
+  float4 xv[V4], gv[V4];
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    xv[j] = __ldg(reinterpret_cast<const float4*>(x + r * ld_x) + lane + 32 * j);
+    s += (xv[j].x + xv[j].y) + (xv[j].z + xv[j].w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / (float)d;
+  float v = 0.f;
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const float a = xv[j].x - mean, b = xv[j].y - mean, c = xv[j].z - mean, e = xv[j].w - mean;
+    v += (a * a + b * b) + (c * c + e * e);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const float rstd = rsqrtf(v / (float)d + eps);
+  float sg = 0.f, sgx = 0.f;
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const float4 g = __ldg(reinterpret_cast<const float4*>(dy + r * ld_dy) + lane + 32 * j);
+    const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + lane + 32 * j);
+    xv[j] = make_float4((xv[j].x - mean) * rstd, (xv[j].y - mean) * rstd,
+                        (xv[j].z - mean) * rstd, (xv[j].w - mean) * rstd);
+    gv[j] = make_float4(g.x * gm.x, g.y * gm.y, g.z * gm.z, g.w * gm.w);
+    sg += (gv[j].x + gv[j].y) + (gv[j].z + gv[j].w);
+    sgx += (gv[j].x * xv[j].x + gv[j].y * xv[j].y) + (gv[j].z * xv[j].z + gv[j].w * xv[j].w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sg += __shfl_xor_sync(0xffffffffu, sg, o);
+    sgx += __shfl_xor_sync(0xffffffffu, sgx, o);
+  }
+  const float mg = sg / (float)d, mgx = sgx / (float)d;
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    float4* o = reinterpret_cast<float4*>(dx + r * ld_dx) + lane + 32 * j;
+    float4 g = make_float4(rstd * (gv[j].x - mg - xv[j].x * mgx),
+                           rstd * (gv[j].y - mg - xv[j].y * mgx),
+                           rstd * (gv[j].z - mg - xv[j].z * mgx),
+                           rstd * (gv[j].w - mg - xv[j].w * mgx));
+    if (accumulate) {
+      const float4 p = *o;
+      g = make_float4(p.x + g.x, p.y + g.y, p.z + g.z, p.w + g.w);
+    }
+    *o = g;
+  }
+  if (lane == 0) stats[r] = make_float2(mean, rstd);
+}
+
+// per-CTA partial column sums of dy x_hat (dgamma) and dy (dbeta) over rows
+// [kRowsPerCta * blockIdx.x, +kRowsPerCta), rows in order
+__global__ void layer_norm_bwd_cols_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n,
+                                           int d, const float* __restrict__ dy, int64_t ld_dy,
+                                           const float2* __restrict__ stats,
+                                           float* __restrict__ dgamma_part,
+                                           float* __restrict__ dbeta_part) {
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
+  const int64_t r1 = r0 + kRowsPerCta < n ? r0 + kRowsPerCta : n;
+  float a = 0.f, b = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    const float2 st = stats[r];
+    const float g = dy[r * ld_dy + c];
+    a += g * ((x[r * ld_x + c] - st.x) * st.y);
+    b += g;
+  }
+  dgamma_part[(int64_t)blockIdx.x * d + c] = a;
+  dbeta_part[(int64_t)blockIdx.x * d + c] = b;
+}
+
+// (the previous single-kernel form: one warp per row with per-lane column
+// partials held in registers; kept for d not a multiple of 128)
 // one warp per row (rows r0 + warp, r0 + warp + 8, ... < r0 + kRowsPerCta);
 // lane owns columns lane, lane + 32, ... (D / 32 of them, D <= 4096)
 template <int PER>
@@ -214,6 +301,26 @@ int lsrm_layer_norm_bwd_f32(const float* x, int64_t ld_x, int64_t n, int d, cons
   const size_t smem = (size_t)tb::kWarps * 2 * d * sizeof(float);
   float* pg = part;
   float* pb = part + n_part * d;
+  const bool vec = d % 128 == 0 && d <= 1024 && ((uintptr_t)x % 16) == 0 &&
+                   ((uintptr_t)dy % 16) == 0 && ((uintptr_t)dx % 16) == 0 &&
+                   ((uintptr_t)gamma % 16) == 0 && ld_x % 4 == 0 && ld_dy % 4 == 0 &&
+                   ld_dx % 4 == 0;
+  if (vec) {
+    // row pass (dx, per-row mean / rstd) then fixed-order column partials; the
+    // row stats live in the workspace after the partials (2 n floats)
+    float2* stats = reinterpret_cast<float2*>(part + 2 * n_part * d);
+#define LSRM_LNR(V)                                                                         \
+  if (d == 128 * V) {                                                                       \
+    tb::layer_norm_bwd_rows_kernel<V><<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(            \
+        x, ld_x, n, d, gamma, eps, dy, ld_dy, dx, ld_dx, accumulate, stats);                \
+  } else
+    LSRM_LNR(1) LSRM_LNR(2) LSRM_LNR(4) LSRM_LNR(8) {}
+#undef LSRM_LNR
+    LSRM_LAUNCHED();
+    tb::layer_norm_bwd_cols_kernel<<<dim3((unsigned)n_part, (unsigned)ceil_div(d, 256)), 256, 0,
+                                     st>>>(x, ld_x, n, d, dy, ld_dy, stats, pg, pb);
+    LSRM_LAUNCHED();
+  } else {
 #define LSRM_LNB(PER)                                                                       \
   if ((d + 31) / 32 <= PER) {                                                               \
     LSRM_CUDA(cudaFuncSetAttribute(tb::layer_norm_bwd_kernel<PER>,                          \
@@ -226,6 +333,7 @@ int lsrm_layer_norm_bwd_f32(const float* x, int64_t ld_x, int64_t n, int d, cons
   }
 #undef LSRM_LNB
   LSRM_LAUNCHED();
+  }
   tb::sum_parts_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(pg, n_part, d, dgamma);
   LSRM_LAUNCHED();
   tb::sum_parts_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(pb, n_part, d, dbeta);

@@ -136,8 +136,12 @@ def _backward(spec: _Spec, P, s, dout):
     g = {}
     fast = _mma_ok(spec)
 
+    bf_cache = {}   # bf16 copies of operands used by several GEMMs of this pass
+
     def gx(a, b, **kw):
-        return (_ops.gemm_train if fast else _ops.gemm_ex)(a, b, **kw)
+        if fast:
+            return _ops.gemm_train(a, b, cache=bf_cache, **kw)
+        return _ops.gemm_ex(a, b, **kw)
     # out = merged W_o
     dmerged = gx(dout, P["w_o"], trans_b=True)
     g["w_o"] = gx(s["merged"], dout, trans_a=True)
@@ -370,7 +374,7 @@ def _ln_bwd(x, gamma, dy, dx, accumulate):
     from .recon_pipeline import LN_EPS
     n, d = x.shape
     parts = max(int(lib().lsrm_colsum_parts(n)), 1)
-    part = D.empty((2 * parts * d,), torch.float32)
+    part = D.empty((2 * parts * d + 2 * n,), torch.float32)   # partials + row mean / rstd
     dg, db = D.empty((d,), torch.float32), D.empty((d,), torch.float32)
     call("lsrm_layer_norm_bwd_f32", x.data_ptr(), x.stride(0), n, d, gamma.data_ptr(), LN_EPS,
          dy.data_ptr(), dy.stride(0), dx.data_ptr(), dx.stride(0), int(accumulate),
@@ -391,8 +395,11 @@ class _LinearFn(torch.autograd.Function):
     def backward(ctx, dy):
         x, w = ctx.saved_tensors
         dy = dy.contiguous()
-        mm = _ops.gemm_train if ctx.fast else _ops.gemm_ex
-        return mm(dy, w, trans_b=True), mm(x, dy, trans_a=True), None
+        if ctx.fast:   # dy's bf16 copy serves both GEMMs
+            cache = {}
+            return (_ops.gemm_train(dy, w, trans_b=True, cache=cache),
+                    _ops.gemm_train(x, dy, trans_a=True, cache=cache), None)
+        return _ops.gemm_ex(dy, w, trans_b=True), _ops.gemm_ex(x, dy, trans_a=True), None
 
 
 class _AddLNFn(torch.autograd.Function):

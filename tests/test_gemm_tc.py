@@ -120,3 +120,63 @@ def test_gemm_rejects_bad_strides(cuda):
     bt = torch.zeros(16, 12, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ConfigurationError):
         _ops.gemm_bf16(a, bt)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (1024, 1024, 16815), (300, 264, 72),
+                                   (64, 128, 1000), (1000, 520, 137)])
+def test_gemm_mn_major_operands(cuda, a_mn, b_mn, m, n, k):
+    """A given as A^T [k,m] and/or B as W [k,n] (MN-major, no transposed copy):
+    the weight-gradient form X^T . dY of the training path."""
+    from paper_2604_05182_b200 import _ops
+    if not (a_mn and b_mn) and k % 8:
+        pytest.skip("a K-major operand needs k % 8 == 0")
+    if (a_mn and m % 8) or n % 8:
+        pytest.skip("row strides must be multiples of 8")
+    g = torch.Generator(device="cuda").manual_seed(m + 3 * n + 5 * k + 7 * a_mn + 11 * b_mn)
+    a, bt = _mk(g, m, k), _mk(g, n, k, scale=0.05)
+    a_op = a.t().contiguous() if a_mn else a
+    b_op = bt.t().contiguous() if b_mn else bt
+    for out_dtype in (torch.float32, torch.bfloat16):
+        out = torch.empty((m, n), dtype=out_dtype, device="cuda")
+        _ops.gemm_tc([_ops.gemm_problem(a_op, b_op, out, a_mn=a_mn, b_mn=b_mn)])
+        torch.cuda.synchronize()
+        _close(out, _ref(a, bt), out_dtype)
+
+
+@pytest.mark.parametrize("trans_a,trans_b", [(False, False), (False, True), (True, False),
+                                             (True, True)])
+@pytest.mark.parametrize("m,n,k", [(1000, 1024, 16815), (16815, 1024, 1024), (37, 64, 13)])
+def test_gemm_train_all_transposes(cuda, trans_a, trans_b, m, n, k):
+    """gemm_train (fp32 in/out, bf16 operands) for every op(a) / op(b)
+    combination against torch on the bf16-rounded operands, incl. k % 8 != 0
+    (zero-padded K) and beta = 1 accumulation; the cast cache returns the
+    same copy for a repeated operand."""
+    from paper_2604_05182_b200 import _ops
+    g = torch.Generator(device="cuda").manual_seed(m + n + k + 2 * trans_a + trans_b)
+    A = torch.randn(m, k, generator=g, device="cuda")
+    B = torch.randn(k, n, generator=g, device="cuda") * 0.05
+    a = A.t().contiguous() if trans_a else A
+    b = B.t().contiguous() if trans_b else B
+    want = A.bfloat16().float() @ B.bfloat16().float()
+    cache = {}
+    got = _ops.gemm_train(a, b, trans_a=trans_a, trans_b=trans_b, cache=cache)
+    n_cached = len(cache)
+    acc = _ops.gemm_train(a, b, trans_a=trans_a, trans_b=trans_b, out=got.clone(), beta=1.0,
+                          cache=cache)
+    torch.cuda.synchronize()
+    assert len(cache) == n_cached == 2
+    _close(got, want, torch.float32)
+    _close(acc, 2 * want, torch.float32)
+
+
+@pytest.mark.parametrize("n", [8 * 12345, 8 * 12345 + 3])
+def test_cast_vectorised_and_tail(cuda, n):
+    from paper_2604_05182_b200 import _ops
+    x = torch.randn(n, device="cuda") * 100
+    x[:4] = torch.tensor([float("nan"), float("inf"), -0.0, 1e-40])
+    y = _ops.cast(x, torch.bfloat16)
+    assert torch.equal(y.view(torch.int16)[4:], x.bfloat16().view(torch.int16)[4:])
+    assert torch.isnan(y[0]) and torch.isinf(y[1])
+    z = _ops.cast(y, torch.float32)
+    assert torch.equal(z[4:], y[4:].float())
