@@ -687,9 +687,10 @@ def time_train_step(inst, steps=3):
     return {"ms_per_step": f + b + o, "forward_ms": f, "backward_ms": b, "optimizer_ms": o,
             "tokens_per_s": n_tok / ((f + b + o) * 1e-3),
             "what": "one full Stage-2 block (4 gated NSA uses + add/LN, use gates, gated "
-                    "mixture/LN, FFN 4d, residuals): fwd + bwd + Adam step; bf16 mma.sync "
-                    "attention branches, bf16 tcgen05 GEMMs (fp32 accumulation), fp32 master "
-                    "weights"}
+                    "mixture/LN, FFN 4d, residuals): fwd + bwd + Adam step; attention forward "
+                    "on the fused tcgen05 kernel (branches, lse and gated merge in one launch "
+                    "per use), backward on bf16 mma.sync, bf16 tcgen05 GEMMs (fp32 "
+                    "accumulation, MN-major weight-gradient operands), fp32 master weights"}
 
 
 def pcie_bandwidth(sizes=(64 << 20, 128 << 20, 256 << 20), reps=5):

@@ -375,6 +375,11 @@ typedef struct lsrm_nsa_use {
   const int32_t* own_rows; /* optional [nq] (tile order): each token's own kv row;
                               the window branch then spans the tile's distinct own
                               blocks, so self-use tiles may cross query blocks */
+  void* branch_out;      /* optional f32 [n_gates][nq][hq*dh]: each branch's own
+                            normalized output (training forward; query-row order) */
+  void* branch_lse;      /* optional f32 [n_gates][nq][hq]: each branch's
+                            log-sum-exp of the scaled logits (natural log);
+                            set with branch_out or not at all */
 } lsrm_nsa_use;
 int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, int hkv, int dh,
                                 const int32_t* order, int64_t n_order, int32_t* counter,

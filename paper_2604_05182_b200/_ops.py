@@ -160,14 +160,16 @@ def cast_pad_bf16(x: torch.Tensor, cols_pad: int) -> torch.Tensor:
 def gemm_train(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, out=None,
                beta=0.0, cache: dict = None) -> torch.Tensor:
     """fp32 out (+)= op(a) @ op(b) on the tcgen05 GEMM, bf16 operands, fp32
-    accumulation (the training path's GEMMs; gemm_ex's signature).  Operands
-    are only cast: a transposed operand is passed MN-major (as stored), so the
+    accumulation (the training path's GEMMs; gemm_ex's signature; f32 or
+    bf16 inputs).  Operands are only cast: a transposed operand is passed MN-major (as stored), so the
     weight-gradient GEMMs X^T . dY need no transposed copies.  A K-major
     operand with k % 8 != 0 is zero-padded (the MN-major one gets zero rows).
     `cache` (optional dict) reuses the bf16 copy of a tensor cast earlier in
     the same backward pass.  N must be a multiple of 8 (every training GEMM's
     N is: d, 4d, n_gates*d, h_kv*d_h)."""
-    assert a.dtype == b.dtype == torch.float32 and beta in (0.0, 1.0)
+    assert a.dtype in (torch.float32, torch.bfloat16) and b.dtype in (torch.float32,
+                                                                     torch.bfloat16)
+    assert beta in (0.0, 1.0)
     m, k = (a.shape[1], a.shape[0]) if trans_a else a.shape
     k2, n = (b.shape[1], b.shape[0]) if trans_b else b.shape
     assert k == k2 and n % 8 == 0, (k, k2, n)
@@ -183,6 +185,10 @@ def gemm_train(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, o
         key = (x.data_ptr(), tuple(x.shape), tuple(x.stride())) + (() if plain else (mn, kp))
         if cache is not None and key in cache:
             return cache[key][1]
+        if x.dtype == torch.bfloat16 and plain and x.is_contiguous():
+            return x                         # already a bf16 operand as stored
+        if x.dtype == torch.bfloat16:
+            x = cast(x.contiguous(), torch.float32)   # cold path: re-pad through f32
         if not mn:                           # K-major [rows, k] -> [rows, kp]
             y = cast_pad_bf16(x, kp)
         elif x.shape[1] % 8:                 # MN-major, row stride padded to 8 (cold path)

@@ -103,6 +103,11 @@ struct Params {
   const int32_t* own_rows;   // optional [nq] (tile order): each token's own kv row;
                              // the window branch then spans the tile's distinct own blocks
   int q_tma;                 // 1: Q tiles by TMA through tmq (G % 8 == 0)
+  // optional (training forward): each branch's normalized output, f32
+  // [n_gates][nq][hq*DH], and its log-sum-exp of the scaled logits (natural
+  // log), f32 [n_gates][nq][hq]
+  float* o_br;
+  float* lse_br;
   // Q as a 5-D tensor map {d%8, g%8, d/8, g/8, row} (strides 1, DH, 8, 8 DH,
   // ld_q elements): the box of one token and 8k q-heads lands in shared
   // memory directly in the UMMA K-major core-matrix layout
@@ -807,6 +812,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     // finished-branch state: its epilogue runs in the next chunk, before that
     // chunk's PV overwrites O
     int br_pend = 0, head_pend = 0, use_pend = 0;
+    float m_pend = 0.f;   // the finished branch's running max (for its lse)
     // the item's first branch (items may start at the window branch); a
     // branch that is its item's first starts the merge instead of adding
     int item_br0 = 0;
@@ -851,6 +857,19 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const float inv = rowok_pend ? 1.f / __uint_as_float(eo[kOCols]) : 0.f;
       const float* bp =
           bias_all ? bias_all + ((int64_t)br_pend * P.hq + head_pend) * bias_ld : nullptr;
+      const Params& PB = L.use[use_pend];
+      if (PB.o_br && rowok_pend) {   // training forward: the branch's own output and lse
+        const int64_t brow = (int64_t)br_pend * PB.nq + tok_pend;
+        float4* ob = reinterpret_cast<float4*>(PB.o_br + brow * d_model + head_pend * DH + oc0);
+#pragma unroll
+        for (int j = 0; j < kOCols / 4; ++j)
+          ob[j] = make_float4(__uint_as_float(eo[4 * j]) * inv, __uint_as_float(eo[4 * j + 1]) * inv,
+                              __uint_as_float(eo[4 * j + 2]) * inv,
+                              __uint_as_float(eo[4 * j + 3]) * inv);
+        if (half == 0)
+          PB.lse_br[brow * P.hq + head_pend] =
+              (m_pend + __log2f(__uint_as_float(eo[kOCols]))) * 0.6931471805599453f;
+      }
 #pragma unroll
       for (int cq = 0; cq < kOCols; cq += 16) {   // 16 columns at a time (registers)
         const int c0 = oc0 + cq;
@@ -1348,6 +1367,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           for (int cq = 0; cq < kOCols; cq += 8) cp_async16(gate_s + oc0 + cq, gp + oc0 + cq, 16u);
         }
         br_pend = br;
+        m_pend = m_run;
         firstbr_pend = br == item_br0;
         use_pend = use_c;
         head_pend = head;
@@ -1568,6 +1588,8 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
   p.br_first = 0;
   p.accum = 0;
   p.own_rows = nullptr;
+  p.o_br = nullptr;
+  p.lse_br = nullptr;
   if (int rc = tc::make_q_map(p, G, dh)) return rc;
   tc::Launch L{};
   L.use[0] = p;
@@ -1626,6 +1648,11 @@ int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, in
     p.br_first = (int)U.branch_first;
     p.accum = (int)U.accumulate;
     p.own_rows = U.own_rows;
+    p.o_br = (float*)U.branch_out;
+    p.lse_br = (float*)U.branch_lse;
+    LSRM_REQUIRE((U.branch_out == nullptr) == (U.branch_lse == nullptr) &&
+                     ((uintptr_t)U.branch_out % 16) == 0,
+                 "use %d: branch_out and branch_lse go together (16-byte aligned)", u);
     if (int rc = tc::make_q_map(p, G, dh)) return rc;
   }
   L.n_uses = n_uses;

@@ -96,7 +96,8 @@ class NsaUse(C.Structure):
                 ("count", C.c_void_p), ("kmax_rows", C.c_int64), ("gate_logits", C.c_void_p),
                 ("ld_gl", C.c_int64), ("gate_col0", C.c_int64), ("n_gates", C.c_int64),
                 ("merged", C.c_void_p), ("perm", C.c_void_p), ("branch_first", C.c_int64),
-                ("accumulate", C.c_int64), ("own_rows", C.c_void_p)]
+                ("accumulate", C.c_int64), ("own_rows", C.c_void_p),
+                ("branch_out", C.c_void_p), ("branch_lse", C.c_void_p)]
 
 
 class PackedShard:

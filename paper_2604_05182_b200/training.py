@@ -27,6 +27,8 @@ attends to) is not differentiated, exactly as in NSA training.
 
 from dataclasses import dataclass
 
+import ctypes as C
+
 import numpy as np
 import torch
 
@@ -59,6 +61,109 @@ def _mma_ok(spec: _Spec) -> bool:
     return spec.fast and p.head_dim in (16, 32, 64) and p.n_q_heads // p.n_kv_heads <= 16
 
 
+def _fused_ok(spec: _Spec) -> bool:
+    """Head geometries the fused tcgen05 forward takes (engine.py / DESIGN §3)."""
+    from .fastpath import supported
+    return supported(spec.params) and int(spec.rows.shape[1]) * (128 * spec.params.n_kv_heads //
+                                                                  spec.params.n_q_heads) <= 256
+
+
+_FUSED_PLANS = {}
+
+
+def _fused_plan(spec: _Spec):
+    """Tiles / tile-order rows / LPT item queue of the fused forward for this
+    use's routing (cached per routing tensor: the plan is fixed across steps).
+    Block tiles signature-sorted inside each query block, as the engine's
+    default (engine.py `_build_attention_queue`); tile positions map to
+    token-order query rows through `perm`."""
+    from .engine import ROW_PAD, query_tiles, stream_meta
+    key = (id(spec.rows), id(spec.part_q), id(spec.part_kv), spec.n_gates)
+    hit = _FUSED_PLANS.get(key)
+    if hit is not None and hit["rows_ref"] is spec.rows:
+        return hit
+    p = spec.params
+    G = p.n_q_heads // p.n_kv_heads
+    self_use = spec.n_gates == 3
+    pq, pk = spec.part_q, spec.part_kv
+    mk = stream_meta(pk)
+    tok_q = pq.block_token_ids.astype(np.int64)
+    rows_tok = D.host(spec.rows).astype(np.int32)
+    cnt_tok = D.host(spec.count).astype(np.int32)
+    rows_bm = rows_tok[tok_q]
+    blk = np.repeat(np.arange(pq.n_occupied), pq.occupancy.astype(np.int64))
+    key_s = np.sort(np.where(rows_bm >= 0, rows_bm, np.iinfo(np.int32).max), axis=1)
+    sig = tuple(key_s[:, j] for j in reversed(range(key_s.shape[1])))
+    perm_bm = np.lexsort(sig + (blk,))
+    perm_tok = tok_q[perm_bm]
+    tiles = query_tiles(pq, G, self_use)
+    rows_t = np.ascontiguousarray(rows_tok[perm_tok])
+    cnt_t = np.ascontiguousarray(cnt_tok[perm_tok])
+    padlen = np.diff(mk.pad_off_host)
+    cmp_rows = (mk.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
+    costs = []
+    for first, tc, own, _ in tiles:
+        r = rows_t[first:first + tc].ravel()
+        c = cmp_rows + int(padlen[np.unique(r[r >= 0])].sum())
+        c += int(padlen[own]) if (own >= 0 and self_use) else 0
+        costs.append(c)
+    hkv = p.n_kv_heads
+    costs = np.repeat(np.asarray(costs, np.int64), hkv)
+    codes = np.arange(costs.size, dtype=np.int64)
+    order = codes[np.lexsort((codes, -costs))].astype(np.int32)
+    plan = {"rows_ref": spec.rows, "meta": mk, "tiles": D.dev(tiles), "rows": D.dev(rows_t),
+            "count": D.dev(cnt_t), "perm": D.dev(perm_tok.astype(np.int32)),
+            "order": D.dev(order), "counter": D.zeros((1,), torch.int32),
+            "kc_rows_pad": cmp_rows}
+    if len(_FUSED_PLANS) > 32:
+        _FUSED_PLANS.clear()
+    _FUSED_PLANS[key] = plan
+    return plan
+
+
+def _fused_attention(spec: _Spec, q_bf, k, v, kc, vc, logits):
+    """Fused tcgen05 forward of one use: per-branch outputs f32 [ng, n, d],
+    per-branch lse f32 [ng, n, hq] and the gated merge (bf16 [n, d])."""
+    from .engine import NsaUse
+    p = spec.params
+    n, d = q_bf.shape
+    hq, hkv, dh = p.n_q_heads, p.n_kv_heads, p.head_dim
+    ng = spec.n_gates
+    plan = _fused_plan(spec)
+    mk = plan["meta"]
+    pk = spec.part_kv
+    st = D.stream()
+    m = int(k.shape[0])
+    width = hkv * dh
+    k_il = D.empty((hkv, mk.n_rows_pad, dh), torch.bfloat16)
+    v_il = D.zeros((hkv, mk.n_rows_pad, dh + 16), torch.bfloat16)
+    for src, dst, ones in ((k, k_il, 0), (v, v_il, 16)):
+        call("lsrm_kv_interleave", 0, src.data_ptr(), width, m, hkv, dh, ones,
+             pk.dev("block_token_ids").data_ptr(), mk.kv_off.data_ptr(), mk.n_blocks,
+             mk.pad_off.data_ptr(), mk.n_rows_pad, dst.data_ptr(), st)
+    bp = plan["kc_rows_pad"]
+    kc_il = D.empty((hkv, bp, dh), torch.bfloat16)
+    vc_il = D.zeros((hkv, bp, dh + 16), torch.bfloat16)
+    for src, dst, ones in ((kc, kc_il, 0), (vc, vc_il, 16)):
+        call("lsrm_kv_interleave", 0, src.data_ptr(), width, mk.n_blocks, hkv, dh, ones, None,
+             None, 0, None, bp, dst.data_ptr(), st)
+    gl = _ops.cast(logits, torch.bfloat16)
+    merged = D.empty((n, d), torch.bfloat16)
+    o_all = D.empty((ng, n, d), torch.float32)
+    lse_all = D.empty((ng, n, hq), torch.float32)
+    tiles = plan["tiles"]
+    use = NsaUse(q_bf.data_ptr(), q_bf.stride(0), n, k_il.data_ptr(), v_il.data_ptr(),
+                 mk.pad_off.data_ptr(), mk.kv_off.data_ptr(), mk.n_rows_pad, kc_il.data_ptr(),
+                 vc_il.data_ptr(), mk.n_blocks, tiles.data_ptr(), int(tiles.shape[0]),
+                 plan["rows"].data_ptr(), plan["count"].data_ptr(), int(spec.rows.shape[1]),
+                 gl.data_ptr(), gl.stride(0), 0, ng, merged.data_ptr(), plan["perm"].data_ptr(),
+                 0, 0, None, o_all.data_ptr(), lse_all.data_ptr())
+    order = plan["order"]
+    call("lsrm_nsa_attention_tc_multi", C.byref(use), 1, hq, hkv, dh, order.data_ptr(),
+         int(order.shape[0]), plan["counter"].data_ptr(), st)
+    return o_all, lse_all, merged
+
+
 def _forward(spec: _Spec, x, kv, P):
     p = spec.params
     n, d = x.shape
@@ -80,6 +185,23 @@ def _forward(spec: _Spec, x, kv, P):
     B = part.n_occupied
     own = spec.part_q.dev("row_of_token") if spec.n_gates == 3 else None
     saved = dict(x=x, kv=kv, q=q, k=k, v=v, kc=kc, vc=vc, k_bm=k_bm, v_bm=v_bm, ck=ck, cv=cv)
+    if fast and _fused_ok(spec):
+        # the three branches, their gated merge and each branch's lse in ONE
+        # launch of the fused tcgen05 forward (csrc/attn_tc.cu); the bias is
+        # folded into the gate logits (so the backward sees a zero bias)
+        bf = {name: _ops.cast(saved[name], torch.bfloat16)
+              for name in ("q", "kc", "vc", "k_bm", "v_bm")}
+        logits = D.empty((n, spec.n_gates * d), torch.float32)
+        _ops.gemm_tc([_ops.gemm_problem(_ops.cast(x.contiguous(), torch.bfloat16),
+                                        _ops.cast(P["gate_w"].contiguous(), torch.bfloat16),
+                                        logits, bias=P["gate_b"], b_mn=True)])
+        o_all, lse_all, merged = _fused_attention(spec, bf["q"], k, v, kc, vc, logits)
+        outs = [o_all[b] for b in range(spec.n_gates)]
+        saved.update(bf=bf, lse=[lse_all[b] for b in range(spec.n_gates)])
+        out = mm(merged, P["w_o"])
+        o = [t.view(n, d) for t in outs] + [None] * (3 - len(outs))
+        saved.update(outs=o, logits=logits, merged=merged, gate_b_eff=torch.zeros_like(P["gate_b"]))
+        return out, saved
     if fast:
         # branches on tensor cores (bf16 operands); lse kept for the backward
         bf = {name: _ops.cast(saved[name], torch.bfloat16)
@@ -112,7 +234,7 @@ def _forward(spec: _Spec, x, kv, P):
          logits.stride(0), P["gate_b"].data_ptr(), spec.n_gates, D.ptr(o[0]), D.ptr(o[1]),
          D.ptr(o[2]), n, d, merged.data_ptr(), D.stream())
     out = mm(merged, P["w_o"])
-    saved.update(outs=o, logits=logits, merged=merged)
+    saved.update(outs=o, logits=logits, merged=merged, gate_b_eff=P["gate_b"])
     return out, saved
 
 
@@ -150,7 +272,7 @@ def _backward(spec: _Spec, P, s, dout):
     dz = D.empty((n, ng * d), torch.float32)
     o = s["outs"]
     call("lsrm_gate_merge_bwd_f32", s["logits"].data_ptr(), s["logits"].stride(0),
-         P["gate_b"].data_ptr(), ng, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]),
+         s["gate_b_eff"].data_ptr(), ng, D.ptr(o[0]), D.ptr(o[1]), D.ptr(o[2]),
          dmerged.data_ptr(), n, d, int(fast), D.ptr(do[0]), D.ptr(do[1]), D.ptr(do[2]),
          dz.data_ptr(), st)
     g["gate_w"] = gx(s["x"], dz, trans_a=True)
