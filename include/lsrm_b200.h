@@ -289,7 +289,7 @@ int lsrm_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a,
  * A bf16 [m,k] and Bt bf16 [n,k] (the weight stored TRANSPOSED) both with K
  * contiguous; fp32 accumulation in TMEM; bias/res/C dtypes per flags.
  * k, n and every row stride must be multiples of 8 elements and pointers
- * 16-byte aligned.  One persistent launch runs all problems (<= 8). */
+ * 16-byte aligned.  One persistent launch runs all problems (<= 32). */
 #define LSRM_GEMM_OUT_F32  1   /* C is f32 (else bf16) */
 #define LSRM_GEMM_BIAS_F32 2   /* bias is f32 (else bf16) */
 #define LSRM_GEMM_RES_F32  4   /* res is f32 (else bf16) */
@@ -630,6 +630,10 @@ int lsrm_all_to_all_v(void* comm, int rank, int world, const void* send,
  * (workspace `part` = 2 * parts * d + 2 * n floats for layer_norm_bwd: the
  * partials and the rows' mean / rstd; parts * d for colsum). */
 int64_t lsrm_colsum_parts(int64_t n);
+/* out[i] (+)= sum over s of parts[s * n + i], slices in order (split-K partial
+ * products of the training GEMMs; deterministic).  n % 4 == 0. */
+int lsrm_sum_slices_f32(const float* parts, int n_slices, int64_t n, float* out, int accumulate,
+                        void* stream);
 /* dx (+)= dLN(x)/dx . dy; dgamma = sum_rows dy x_hat; dbeta = sum_rows dy. */
 int lsrm_layer_norm_bwd_f32(const float* x, int64_t ld_x, int64_t n, int d, const float* gamma,
                             float eps, const float* dy, int64_t ld_dy, float* dx, int64_t ld_dx,

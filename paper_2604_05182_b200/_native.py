@@ -108,6 +108,7 @@ SIGNATURES = {
     "lsrm_transpose_cast_bf16": (I32, [P, I64, I64, I64, P, I64, P]),
     "lsrm_host_threads": (I32, []),
     "lsrm_h2d_rows": (I32, [I32, P, I64, P, I64, I64, P, I64, P]),
+    "lsrm_sum_slices_f32": (I32, [P, I32, I64, P, I32, P]),
 }
 
 _lib = None

@@ -91,6 +91,7 @@ class GemmProblem(C.Structure):
 
 
 GEMM_OUT_F32, GEMM_BIAS_F32, GEMM_RES_F32, GEMM_GELU, GEMM_A_MN, GEMM_B_MN = 1, 2, 4, 8, 16, 32
+_MAX_PROBLEMS = 32   # problems per lsrm_gemm_tc launch
 
 
 def gemm_problem(a: torch.Tensor, bt: torch.Tensor, out: torch.Tensor, bias=None, res=None,
@@ -206,8 +207,29 @@ def gemm_train(a: torch.Tensor, b: torch.Tensor, trans_a=False, trans_b=False, o
         if cache is not None:
             cache[key] = (x, y)              # x kept alive: its address cannot be reused
         return y
-    gemm_tc([gemm_problem(bf(a, a_mn), bf(b, b_mn), dst, res=dst if acc else None, a_mn=a_mn,
-                          b_mn=b_mn)])
+    A, B = bf(a, a_mn), bf(b, b_mn)
+    # split K when the output has too few 256 x 256 tiles to fill the GPU (the
+    # weight gradients: m x n = d x d, k = tokens); partial products go to a
+    # workspace and are summed in slice order (deterministic)
+    tiles = -(-m // 256) * -(-n // 256)
+    n_split = min(_MAX_PROBLEMS, -(-74 // tiles), kp // 512) if tiles < 74 else 1
+    if n_split > 1 and (m * n) % 4 == 0:
+        step = (-(-kp // n_split) + 63) // 64 * 64   # multiples of BK: 16-byte aligned slices
+        cuts = [min(kp, i * step) for i in range(n_split + 1)]
+        cuts = [c for i, c in enumerate(cuts) if i == 0 or c > cuts[i - 1]]
+        parts = D.empty((len(cuts) - 1, m, n), torch.float32)
+        probs = []
+        for s_, (k0, k1) in enumerate(zip(cuts[:-1], cuts[1:])):
+            As = A[k0:k1] if a_mn else A[:, k0:k1]
+            Bs = B[k0:k1] if b_mn else B[:, k0:k1]
+            probs.append(gemm_problem(As, Bs, parts[s_], a_mn=a_mn, b_mn=b_mn))
+        gemm_tc(probs)
+        if not dst.is_contiguous():
+            raise ValueError("gemm_train: split-K needs a contiguous output")
+        call("lsrm_sum_slices_f32", parts.data_ptr(), len(probs), m * n, dst.data_ptr(), int(acc),
+             D.stream())
+        return dst
+    gemm_tc([gemm_problem(A, B, dst, res=dst if acc else None, a_mn=a_mn, b_mn=b_mn)])
     return dst
     kp = (k + 7) // 8 * 8
     am = transpose_bf16(a) if trans_a else cast_pad_bf16(a, kp)      # [m, kp]

@@ -48,7 +48,7 @@ constexpr int BM = 128, BN = 256, BK = 64, kAccStages = 2;
 constexpr int kABytes = BM * BK * 2;
 constexpr int kEpiWarps = 8;                 // two per TMEM lane quadrant
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-constexpr int kMaxProblems = 8;
+constexpr int kMaxProblems = 32;   // ~15 KB of kernel parameters (limit 32 KB)
 
 struct Prob {
   int64_t m, n, k;

@@ -277,12 +277,41 @@ __global__ void transpose_cast_kernel(const float* __restrict__ src, int64_t ld,
   }
 }
 
+// out = (accumulate ? out : 0) + parts[0] + ... + parts[n_slices - 1]
+// (split-K partial products, summed in slice order), float4 per thread
+__global__ void sum_slices_kernel(const float4* __restrict__ parts, int n_slices, int64_t n4,
+                                  float4* __restrict__ out, int accumulate) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = accumulate ? out[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < n_slices; ++s) {
+      const float4 p = __ldcs(parts + (int64_t)s * n4 + i);
+      a.x += p.x; a.y += p.y; a.z += p.z; a.w += p.w;
+    }
+    out[i] = a;
+  }
+}
+
 }  // namespace tb
 }  // namespace lsrm
 
 using namespace lsrm;
 
 extern "C" {
+
+int lsrm_sum_slices_f32(const float* parts, int n_slices, int64_t n, float* out, int accumulate,
+                        void* stream) {
+  LSRM_REQUIRE(n_slices >= 1 && n % 4 == 0 && ((uintptr_t)parts % 16) == 0 &&
+                   ((uintptr_t)out % 16) == 0,
+               "sum_slices: n %% 4 == 0 and 16-byte aligned buffers required");
+  if (n == 0) return LSRM_OK;
+  const int64_t n4 = n / 4;
+  tb::sum_slices_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n4, 256), 148 * 8), 256, 0,
+                          as_stream(stream)>>>(reinterpret_cast<const float4*>(parts), n_slices,
+                                               n4, reinterpret_cast<float4*>(out), accumulate);
+  LSRM_LAUNCHED();
+  return LSRM_OK;
+}
 
 int64_t lsrm_colsum_parts(int64_t n) { return (n + tb::kRowsPerCta - 1) / tb::kRowsPerCta; }
 

@@ -146,12 +146,14 @@ def test_gemm_mn_major_operands(cuda, a_mn, b_mn, m, n, k):
 
 @pytest.mark.parametrize("trans_a,trans_b", [(False, False), (False, True), (True, False),
                                              (True, True)])
-@pytest.mark.parametrize("m,n,k", [(1000, 1024, 16815), (16815, 1024, 1024), (37, 64, 13)])
+@pytest.mark.parametrize("m,n,k", [(1000, 1024, 16815), (16815, 1024, 1024), (37, 64, 13),
+                                   (64, 64, 16815)])
 def test_gemm_train_all_transposes(cuda, trans_a, trans_b, m, n, k):
     """gemm_train (fp32 in/out, bf16 operands) for every op(a) / op(b)
     combination against torch on the bf16-rounded operands, incl. k % 8 != 0
-    (zero-padded K) and beta = 1 accumulation; the cast cache returns the
-    same copy for a repeated operand."""
+    (zero-padded K), split K (outputs of few tiles with long K: partial
+    products summed in slice order) and beta = 1 accumulation; the cast cache
+    returns the same copy for a repeated operand."""
     from paper_2604_05182_b200 import _ops
     g = torch.Generator(device="cuda").manual_seed(m + n + k + 2 * trans_a + trans_b)
     A = torch.randn(m, k, generator=g, device="cuda")
