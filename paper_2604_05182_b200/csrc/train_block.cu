@@ -199,14 +199,32 @@ __global__ void __launch_bounds__(kWarps * 32) layer_norm_bwd_kernel(
   }
 }
 
-// partial rows [n_part][d] -> out[d], summed in partial order
-__global__ void sum_parts_kernel(const float* __restrict__ part, int64_t n_part, int d,
-                                 float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= d) return;
-  float s = 0.f;
-  for (int64_t p = 0; p < n_part; ++p) s += part[p * d + c];
-  out[c] = s;
+// partial rows [n_part][d] -> out[d]: CTA = 32 columns x 32 warps; warp w
+// sums parts w, w + 32, ... (two accumulators, in order), then warp 0 adds
+// the 32 warp sums in warp order (a fixed order: deterministic)
+__global__ void __launch_bounds__(1024) sum_parts_kernel(const float* __restrict__ part,
+                                                         int64_t n_part, int d,
+                                                         float* __restrict__ out) {
+  __shared__ float red[32][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 32 + lane;
+  float a0 = 0.f, a1 = 0.f;
+  if (c < d) {
+    int64_t p = warp;
+    for (; p + 32 < n_part; p += 64) {
+      a0 += part[p * d + c];
+      a1 += part[(p + 32) * d + c];
+    }
+    if (p < n_part) a0 += part[p * d + c];
+  }
+  red[warp][lane] = a0 + a1;
+  __syncthreads();
+  if (warp == 0 && c < d) {
+    float t = 0.f;
+#pragma unroll 8
+    for (int w = 0; w < 32; ++w) t += red[w][lane];
+    out[c] = t;
+  }
 }
 
 // column partial sums of rows [kRowsPerCta * blockIdx.x, +kRowsPerCta)
@@ -363,9 +381,9 @@ int lsrm_layer_norm_bwd_f32(const float* x, int64_t ld_x, int64_t n, int d, cons
 #undef LSRM_LNB
   LSRM_LAUNCHED();
   }
-  tb::sum_parts_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(pg, n_part, d, dgamma);
+  tb::sum_parts_kernel<<<(unsigned)ceil_div(d, 32), 1024, 0, st>>>(pg, n_part, d, dgamma);
   LSRM_LAUNCHED();
-  tb::sum_parts_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(pb, n_part, d, dbeta);
+  tb::sum_parts_kernel<<<(unsigned)ceil_div(d, 32), 1024, 0, st>>>(pb, n_part, d, dbeta);
   LSRM_LAUNCHED();
   return LSRM_OK;
 }
@@ -381,7 +399,7 @@ int lsrm_colsum_f32(const float* x, int64_t ld, int64_t n, int d, float* part, f
   tb::colsum_part_kernel<<<dim3((unsigned)n_part, (unsigned)ceil_div(d, 256)), 256, 0, st>>>(
       x, ld, n, d, part);
   LSRM_LAUNCHED();
-  tb::sum_parts_kernel<<<(unsigned)ceil_div(d, 256), 256, 0, st>>>(part, n_part, d, out);
+  tb::sum_parts_kernel<<<(unsigned)ceil_div(d, 32), 1024, 0, st>>>(part, n_part, d, out);
   LSRM_LAUNCHED();
   return LSRM_OK;
 }

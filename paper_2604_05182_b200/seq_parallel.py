@@ -1019,6 +1019,96 @@ class TokenDispatch:
         return outs
 
 
+# ---------------------------------------------------------------------------
+# Training under block-aware sequence parallelism (BASELINE config 5): each
+# rank runs the Stage-2 block's forward and backward for the query blocks it
+# owns (training.SparseBlockModule(..., shard=...)); per NSA use the K/V rows
+# are all-gathered from their owners (All-gather-KV) and, in the backward,
+# every rank's partial dK / dV rows are summed at the owner (the adjoint);
+# parameter gradients are summed over ranks (allreduce_grads).
+
+
+class RowExchange:
+    """All-gather of one stream's rows (this rank's `loc_tok[rank]` rows, any
+    width) into token order, and its adjoint: the ranks' partial gradients
+    of every row summed, in rank order, at the rank that owns the row."""
+
+    def __init__(self, loc_tok: list, n_total: int, rank: int, transport):
+        self.loc_tok = [np.asarray(t, np.int64) for t in loc_tok]
+        self.rank, self.world, self.n_total = rank, len(loc_tok), int(n_total)
+        self.transport = transport
+        self.idx = [D.dev(t) for t in self.loc_tok]
+        self.bytes_moved = 0
+
+    @property
+    def n_local(self) -> int:
+        return int(self.loc_tok[self.rank].size)
+
+    def gather(self, t_loc: torch.Tensor) -> torch.Tensor:
+        from . import _ops
+        w = int(t_loc.shape[1])
+        recvs = [D.empty((int(t.size), w), t_loc.dtype) for t in self.loc_tok]
+        self.transport.all_to_all_v([t_loc.contiguous()] * self.world, recvs)()
+        full = D.empty((self.n_total, w), t_loc.dtype)
+        for r, buf in enumerate(recvs):
+            if buf.shape[0]:
+                _ops.scatter_rows(buf, self.idx[r], full)
+        self.bytes_moved += (self.world - 1) * t_loc.numel() * t_loc.element_size()
+        return full
+
+    def reduce_scatter(self, t_full: torch.Tensor) -> torch.Tensor:
+        from . import _ops
+        from ._native import call
+        require(t_full.dtype == torch.float32, "reduce_scatter: f32 gradients")
+        w, n = int(t_full.shape[1]), self.n_local
+        sends = [_ops.gather_rows(t_full, i) for i in self.idx]
+        stack = D.empty((self.world, n, w), torch.float32)
+        self.transport.all_to_all_v(sends, [stack[r] for r in range(self.world)])()
+        out = D.empty((n, w), torch.float32)
+        if n * w:
+            call("lsrm_sum_slices_f32", stack.data_ptr(), self.world, n * w, out.data_ptr(), 0,
+                 D.stream())
+        self.bytes_moved += sum(int(sn.numel()) * 4 for r, sn in enumerate(sends) if r != self.rank)
+        return out
+
+
+@dataclass
+class StreamShard:
+    queries: object          # training.LocalQueries of this rank
+    exchange: RowExchange
+
+
+def training_shard(part_vol, part_img, topology: WorkerTopology, rank: int, transport) -> dict:
+    """Per stream ("x" volume, "y" image): this rank's LocalQueries and the
+    RowExchange over every rank's owned rows, for
+    training.SparseBlockModule(..., shard=...)."""
+    from .training import local_queries
+    out = {}
+    for s, part, rows in (("x", part_vol, topology.vol_rows), ("y", part_img, topology.img_rows)):
+        lq = [local_queries(part, r) for r in rows]
+        out[s] = StreamShard(lq[rank], RowExchange([q.loc_tok for q in lq], part.n_tokens,
+                                                   rank, transport))
+    return out
+
+
+def allreduce_grads(params, host_staged: bool = False, group=None) -> None:
+    """Sum every parameter's gradient over the ranks (one flat buffer; through
+    host memory for a CPU backend)."""
+    import torch.distributed as dist
+    grads = [p.grad for p in params if p.grad is not None]
+    if not grads:
+        return
+    flat = torch.cat([g.reshape(-1) for g in grads])
+    buf = flat.cpu() if host_staged else flat
+    dist.all_reduce(buf, group=group)
+    if host_staged:
+        flat.copy_(buf)
+    o = 0
+    for g in grads:
+        g.copy_(flat[o:o + g.numel()].view_as(g))
+        o += g.numel()
+
+
 class ShardedStage:
     """One rank of the block-aware sequence-parallel Stage-2 stage
     (`lsrm/seq_parallel.py:321-434`) on the bf16 engines:

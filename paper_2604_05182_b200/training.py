@@ -54,6 +54,62 @@ class _Spec:
     count: torch.Tensor
     fast: bool = False    # tensor-core (bf16) attention backward
     transposed: tuple = None   # (offs, queries) per kv row, built on first use
+    # block-aware sequence parallelism (seq_parallel.py): the queries are the
+    # rows of the query blocks this rank owns, and K/V are all-gathered from
+    # their owners (their gradients reduce-scattered back) by kv_exchange
+    q_local: "LocalQueries" = None
+    kv_exchange: object = None
+
+
+@dataclass
+class LocalQueries:
+    """The queries of the query blocks one rank owns: local rows are the owned
+    blocks' tokens in block-major order (`seq_parallel.py` shards whole
+    blocks).  own_rows: each local query's block row in the (global)
+    partition; win_offs / win_ids: the local rows of every block (empty for
+    blocks other ranks own) for the window branch's key-major pass."""
+    part: BlockPartition
+    owned: np.ndarray
+    loc_tok: np.ndarray
+    own_rows: torch.Tensor
+    win_offs: torch.Tensor
+    win_ids: torch.Tensor
+
+    @property
+    def n(self) -> int:
+        return int(self.loc_tok.size)
+
+
+def local_queries(part: BlockPartition, owned) -> LocalQueries:
+    owned = np.sort(np.asarray(owned, np.int64))
+    occ = part.occupancy.astype(np.int64)
+    loc_tok = (np.concatenate([part.tokens_in_row(int(r)) for r in owned]).astype(np.int64)
+               if owned.size else np.zeros(0, np.int64))
+    own_rows = np.repeat(owned, occ[owned]).astype(np.int32)
+    counts = np.zeros(part.n_occupied, np.int64)
+    counts[owned] = occ[owned]
+    win_offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    win_ids = np.arange(loc_tok.size, dtype=np.int32)   # owned blocks in ascending order
+    return LocalQueries(part, owned, loc_tok, D.dev(own_rows), D.dev(win_offs), D.dev(win_ids))
+
+
+def q_local_rows(q_local: LocalQueries, table):
+    """The routing rows of the local queries (cached per table)."""
+    cache = q_local.__dict__.setdefault("_rows", {})
+    hit = cache.get(id(table.rows))
+    if hit is None or hit[0] is not table.rows:
+        idx = D.dev(q_local.loc_tok)
+        rows = _ops.gather_rows(table.rows, idx)
+        count = _ops.gather_rows(table.count.reshape(-1, 1), idx).reshape(-1)
+        hit = (table.rows, rows, count)
+        cache[id(table.rows)] = hit
+    return hit[1], hit[2]
+
+
+def _own_rows(spec: "_Spec"):
+    if spec.n_gates != 3:
+        return None
+    return spec.q_local.own_rows if spec.q_local is not None else spec.part_q.dev("row_of_token")
 
 
 def _mma_ok(spec: _Spec) -> bool:
@@ -78,7 +134,7 @@ def _fused_plan(spec: _Spec):
     default (engine.py `_build_attention_queue`); tile positions map to
     token-order query rows through `perm`."""
     from .engine import ROW_PAD, query_tiles, stream_meta
-    key = (id(spec.rows), id(spec.part_q), id(spec.part_kv), spec.n_gates)
+    key = (id(spec.rows), id(spec.part_q), id(spec.part_kv), spec.n_gates, id(spec.q_local))
     hit = _FUSED_PLANS.get(key)
     if hit is not None and hit["rows_ref"] is spec.rows:
         return hit
@@ -87,16 +143,21 @@ def _fused_plan(spec: _Spec):
     self_use = spec.n_gates == 3
     pq, pk = spec.part_q, spec.part_kv
     mk = stream_meta(pk)
-    tok_q = pq.block_token_ids.astype(np.int64)
     rows_tok = D.host(spec.rows).astype(np.int32)
     cnt_tok = D.host(spec.count).astype(np.int32)
+    ql = spec.q_local
+    if ql is None:
+        tok_q = pq.block_token_ids.astype(np.int64)
+        blk = np.repeat(np.arange(pq.n_occupied), pq.occupancy.astype(np.int64))
+    else:   # local rows are already block-major over the owned blocks
+        tok_q = np.arange(ql.n, dtype=np.int64)
+        blk = np.repeat(np.arange(ql.owned.size), pq.occupancy.astype(np.int64)[ql.owned])
     rows_bm = rows_tok[tok_q]
-    blk = np.repeat(np.arange(pq.n_occupied), pq.occupancy.astype(np.int64))
     key_s = np.sort(np.where(rows_bm >= 0, rows_bm, np.iinfo(np.int32).max), axis=1)
     sig = tuple(key_s[:, j] for j in reversed(range(key_s.shape[1])))
     perm_bm = np.lexsort(sig + (blk,))
     perm_tok = tok_q[perm_bm]
-    tiles = query_tiles(pq, G, self_use)
+    tiles = query_tiles(pq, G, self_use, None if ql is None else ql.owned)
     rows_t = np.ascontiguousarray(rows_tok[perm_tok])
     cnt_t = np.ascontiguousarray(cnt_tok[perm_tok])
     padlen = np.diff(mk.pad_off_host)
@@ -176,6 +237,9 @@ def _forward(spec: _Spec, x, kv, P):
     q = mm(x, P["w_q"])
     k = mm(kv, P["w_k"])
     v = mm(kv, P["w_v"])
+    if spec.kv_exchange is not None:   # All-gather-KV: every block's K/V rows
+        k, v = spec.kv_exchange.gather(k), spec.kv_exchange.gather(v)
+        m = int(k.shape[0])
     ck = [P[f"ck_{s}"] for s in ("w1", "b1", "w2", "b2")]
     cv = [P[f"cv_{s}"] for s in ("w1", "b1", "w2", "b2")]
     kc = compress_rows(k, width, m, width, ck, part)
@@ -183,7 +247,7 @@ def _forward(spec: _Spec, x, kv, P):
     tok, offs = part.dev("block_token_ids"), part.dev("block_offsets")
     k_bm, v_bm = _ops.gather_rows(k, tok), _ops.gather_rows(v, tok)
     B = part.n_occupied
-    own = spec.part_q.dev("row_of_token") if spec.n_gates == 3 else None
+    own = _own_rows(spec)
     saved = dict(x=x, kv=kv, q=q, k=k, v=v, kc=kc, vc=vc, k_bm=k_bm, v_bm=v_bm, ck=ck, cv=cv)
     if fast and _fused_ok(spec):
         # the three branches, their gated merge and each branch's lse in ONE
@@ -248,7 +312,7 @@ def _backward(spec: _Spec, P, s, dout):
     plus "x", "kv")."""
     p = spec.params
     n, d = s["x"].shape
-    m = int(s["kv"].shape[0])
+    m = int(s["k"].shape[0])   # every kv row (all-gathered under sequence parallelism)
     hq, hkv, dh = p.n_q_heads, p.n_kv_heads, p.head_dim
     width = hkv * dh
     ng = spec.n_gates
@@ -303,7 +367,9 @@ def _backward(spec: _Spec, P, s, dout):
                  t_offs.data_ptr(), t_q.data_ptr(), tws.data_ptr(), wsb, st)
             spec.transposed = (t_offs, t_q)
         lists[1] = spec.transposed
-        if ng == 3:
+        if ng == 3 and spec.q_local is not None:
+            lists[2] = (spec.q_local.win_offs, spec.q_local.win_ids)
+        elif ng == 3:
             lists[2] = (part.dev("block_offsets"), part.dev("block_token_ids").to(torch.int32))
 
     def bwd(mode, b, k, v, nk, dk, dv, rows=None, count=None, own=None):
@@ -332,7 +398,7 @@ def _backward(spec: _Spec, P, s, dout):
     bwd(0, 0, "kc", "vc", B, dkc, dvc)
     bwd(1, 1, "k_bm", "v_bm", m, dk_bm, dv_bm, rows=spec.rows, count=spec.count)
     if ng == 3:
-        bwd(2, 2, "k_bm", "v_bm", m, dk_bm, dv_bm, own=spec.part_q.dev("row_of_token"))
+        bwd(2, 2, "k_bm", "v_bm", m, dk_bm, dv_bm, own=_own_rows(spec))
     tok = part.dev("block_token_ids")
     dk = _ops.scatter_rows(dk_bm, tok, D.empty((m, width), torch.float32))
     dv = _ops.scatter_rows(dv_bm, tok, D.empty((m, width), torch.float32))
@@ -349,6 +415,8 @@ def _backward(spec: _Spec, P, s, dout):
         g[f"{tag}_b1"] = _colsum(dz1)
         g[f"{tag}_w2"] = gx(h, dr, trans_a=True)
         g[f"{tag}_b2"] = _colsum(dr)
+    if spec.kv_exchange is not None:   # every rank's partial dK / dV summed at the owners
+        dk, dv = spec.kv_exchange.reduce_scatter(dk), spec.kv_exchange.reduce_scatter(dv)
     # projections
     g["w_k"] = gx(s["kv"], dk, trans_a=True)
     g["w_v"] = gx(s["kv"], dv, trans_a=True)
@@ -394,11 +462,19 @@ class NsaUseModule(torch.nn.Module):
             self.register_parameter(name, torch.nn.Parameter(D.dev(arr, torch.float32).clone()))
 
     def forward(self, x, kv, part_q: BlockPartition, part_kv: BlockPartition, sel=None,
-                table=None):
+                table=None, q_local: LocalQueries = None, kv_exchange=None):
+        """q_local / kv_exchange: sequence-parallel call (x = this rank's
+        query rows, kv = this rank's kv-stream rows, `table` routes every
+        token of the partition)."""
         n = int(x.shape[0])
         require(x.shape[1] == self.params.model_dim, "query width != model dim")
-        require(int(kv.shape[0]) == part_kv.n_tokens, "partition does not index these tokens")
-        if getattr(table, "rows", None) is not None:
+        n_kv = kv_exchange.n_local if kv_exchange is not None else part_kv.n_tokens
+        require(int(kv.shape[0]) == n_kv, "partition does not index these tokens")
+        if q_local is not None:
+            require(getattr(table, "rows", None) is not None and n == q_local.n,
+                    "a sequence-parallel use needs a routing table and its local queries")
+            rows, count = q_local_rows(q_local, table)
+        elif getattr(table, "rows", None) is not None:
             rows, count = table.rows, table.count
         else:
             require(sel is not None and sel.n_queries == n, "a Selection covering every query "
@@ -406,7 +482,8 @@ class NsaUseModule(torch.nn.Module):
             rows, count = selection_rows(sel, part_kv)
             own = part_kv.block_of_token if self.n_gates == 3 else None
             rows, count, _, _, _ = resolve_rows(rows, count, part_kv, own, True)
-        spec = _Spec(self.params, self.n_gates, part_q, part_kv, rows, count, self.fast_backward)
+        spec = _Spec(self.params, self.n_gates, part_q, part_kv, rows, count, self.fast_backward,
+                     q_local=q_local, kv_exchange=kv_exchange)
         return _NsaUseFn.apply(spec, x, kv, *(getattr(self, nm) for nm in PARAM_NAMES))
 
 
@@ -467,11 +544,16 @@ class NsaLayerModule(torch.nn.Module):
                             fast_backward=fast_backward, tags=("train", f"layer{layer}", u))
             for u, (_, _, ng) in USE_STREAMS.items()})
 
-    def forward(self, x, y, part_vol, part_img, resolved: dict) -> dict:
+    def forward(self, x, y, part_vol, part_img, resolved: dict, shard: dict = None) -> dict:
+        """shard (sequence parallelism, `seq_parallel.training_shard`): per
+        stream its LocalQueries and RowExchange; x / y are then this rank's
+        rows of the two streams."""
         streams = {"x": x, "y": y}
         parts = {"x": part_vol, "y": part_img}
         return {u: self.uses[u](streams[qs], streams[ks], parts[qs], parts[ks],
-                                table=resolved[u])
+                                table=resolved[u],
+                                q_local=shard[qs].queries if shard else None,
+                                kv_exchange=shard[ks].exchange if shard else None)
                 for u, (qs, ks, _) in USE_STREAMS.items()}
 
 
@@ -641,12 +723,14 @@ class SparseBlockModule(torch.nn.Module):
         return _BiasActFn.apply(_LinearFn.apply(u, getattr(self, f"f{s}_w2"), self.fast),
                                 getattr(self, f"f{s}_b2"), x1, 0, exact)
 
-    def forward(self, x, y, x_inj, y_inj, part_vol, part_img, resolved: dict):
+    def forward(self, x, y, x_inj, y_inj, part_vol, part_img, resolved: dict, shard=None):
+        """shard: see NsaLayerModule.forward (x, y, x_inj, y_inj are then this
+        rank's rows; every other op of the block is row-local)."""
         exact = not self.fast
         xe, xh = _AddLNFn.apply(x, x_inj, self.ln_ax_g, self.ln_ax_b, exact)
         ye, yh = _AddLNFn.apply(y, y_inj, self.ln_ay_g, self.ln_ay_b, exact)
         lx = _LinearFn.apply(xh, self.gate_x_w, self.fast)
         ly = _LinearFn.apply(yh, self.gate_y_w, self.fast)
-        o = self.layer(xh, yh, part_vol, part_img, resolved)
+        o = self.layer(xh, yh, part_vol, part_img, resolved, shard=shard)
         return (self._stream("x", xe, lx, o["v2v"], o["v2i"]),
                 self._stream("y", ye, ly, o["i2i"], o["i2v"]))

@@ -502,6 +502,27 @@ def test_torchrun_sharded_stage(cuda, W):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("W,mode", [(2, "fp32"), (3, "fp32"), (2, "fast")])
+def test_torchrun_sharded_training(cuda, W, mode):
+    """One Stage-2 block training step under block-aware sequence parallelism
+    (BASELINE config 5's step): W torchrun ranks sharing one GPU (gloo,
+    host-staged), per-use All-gather-KV forward and its adjoint (partial
+    dK / dV summed at the owners), parameter gradients summed over ranks.
+    Outputs, input gradients and every parameter gradient match the one-GPU
+    step (tests/sp_train_worker.py): fp32 kernels within 1e-4 (summation
+    order only), the bf16 fast path within its oracle tolerance."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={W}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "tests", "sp_train_worker.py"), mode]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
+
+
+@pytest.mark.gpu
 def test_capi_nccl_transport_world1(cuda):
     """The C-ABI NCCL exchanges (`lsrm_allgather_kv`, `lsrm_all_to_all_v`)
     through CapiNcclTransport on a one-rank communicator (this box has one
