@@ -922,6 +922,50 @@ def run_sp(args):
                     "what": "ShardedStage: dispatch all_to_all_v (features + coords) -> "
                             f"{args.sp_stage_depth} sharded Stage-2 blocks (per-use "
                             "All-gather-KV) -> return all_to_all_v; eager, max over ranks"}
+    # one Stage-2 block TRAINING step under the same sharding (BASELINE
+    # config 5's step): fwd + bwd with per-use All-gather-KV and its adjoint,
+    # parameter gradients summed over ranks, Adam; max over ranks
+    sp_train = None
+    if args.sp_train_steps > 0:
+        from paper_2604_05182_b200 import _dev as D
+        from paper_2604_05182_b200.recon_pipeline import init_sparse_block
+        from paper_2604_05182_b200.training import SparseBlockModule, resolve_plan_rows
+        res = resolve_plan_rows(inst.plan_rows, inst.part_vol, inst.part_img)
+        shard = S.training_shard(inst.part_vol, inst.part_img, sl.topology, rank, transport)
+        mod = SparseBlockModule(inst.params, weights=init_sparse_block(0, inst.params, 0),
+                                fast_backward=True)
+        opt = torch.optim.Adam(mod.parameters(), lr=1e-4)
+        lx = torch.as_tensor(shard["x"].queries.loc_tok, device="cuda")
+        ly = torch.as_tensor(shard["y"].queries.loc_tok, device="cuda")
+        xl = D.dev(inst.x_hat)[lx].requires_grad_(True)
+        yl = D.dev(inst.y_hat)[ly].requires_grad_(True)
+        xi, yi = (0.1 * xl).detach(), (0.1 * yl).detach()
+
+        def train_step():
+            opt.zero_grad()
+            x2, y2 = mod(xl, yl, xi, yi, inst.part_vol, inst.part_img, res, shard=shard)
+            ((x2 * x2).sum() + (y2 * y2).sum()).backward()
+            S.allreduce_grads(list(mod.parameters()), host_staged=backend != "nccl")
+            opt.step()
+        for _ in range(2):
+            train_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        n_tr = args.sp_train_steps
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(n_tr):
+            train_step()
+        b.record(st)
+        torch.cuda.synchronize()
+        tr_ms = max_all(a.elapsed_time(b) / n_tr)
+        moved = sum_all(shard["x"].exchange.bytes_moved + shard["y"].exchange.bytes_moved)
+        sp_train = {"ms_per_step": tr_ms, "tokens_per_s": n_tok / (tr_ms * 1e-3),
+                    "exchange_bytes_per_step": moved / (n_tr + 2),
+                    "what": "one Stage-2 block training step under block-aware SP: each rank "
+                            "its own query blocks, per-use All-gather-KV of K/V rows and its "
+                            "adjoint (partial dK/dV summed at owners), gradients all-reduced, "
+                            "Adam; fused tcgen05 forward, bf16 backward; max over ranks"}
     single = None
     if not args.no_single_compare:
         # the same workload on ONE GPU (rank 0), same timing rules: the
@@ -973,6 +1017,7 @@ def run_sp(args):
                          "what": "packed bf16 K/V + f32 compressed rows of the 4 uses, "
                                  "(W-1) peers per rank"},
             "sp_stage": sp_stage,
+            "sp_train": sp_train,
             "cpu_baseline": None,
             "e2e": {"value": n_tok / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
@@ -1004,6 +1049,8 @@ def main():
                     help="N>1: also time the sharded stage (dispatch, depth blocks, return)")
     ap.add_argument("--token-lpt", action="store_true",
                     help="shard by token counts (reference rule) instead of routed workload")
+    ap.add_argument("--sp-train-steps", type=int, default=3,
+                    help="N>1: timed SP training steps of one Stage-2 block (0 = skip)")
     ap.add_argument("--no-single-compare", action="store_true",
                     help="N>1: skip timing the same workload on one GPU")
     args = ap.parse_args()
