@@ -60,7 +60,18 @@ constexpr int kM = 128;          // MMA rows per head-tile
 #endif
 // keys per chunk; double-buffered S (LSRM_DBUF) uses 96 so that two S
 // buffers (P inside) + [O | rowsum] + merge fit 256 TMEM columns per pipeline
-constexpr int kNK = LSRM_DBUF ? LSRM_DBUF_NK : 128;
+// LSRM_NK: keys per chunk of the default layout (128).  LSRM_NK = 64 with
+// LSRM_NP = 2 measured 1.13 -> 1.35 ms (chunk overhead); three pipelines
+// (which 64-key chunks would let TMEM hold: 3 x 160 columns) do not launch:
+// 18 warps put 5 on some SMSP, capping registers at 96 (spills).
+#ifndef LSRM_NK
+#define LSRM_NK 128
+#endif
+#ifndef LSRM_NP
+#define LSRM_NP 2
+#endif
+static_assert(LSRM_NP == 1 || LSRM_NP == 2, "LSRM_NP: 1 or 2 pipelines per CTA");
+constexpr int kNK = LSRM_DBUF ? LSRM_DBUF_NK : LSRM_NK;
 constexpr int kGroups = kNK / 16;
 constexpr int kMaxEnt = 256;     // tile tokens * selected rows
 
@@ -668,16 +679,19 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           }
           {   // per token: the groups it sees (padding rows of the tile see none);
               // the chunk's group table read with four 16-byte loads
-            static_assert(kGroups == 8, "tokvis: 8 groups per chunk");
-            const uint4 m0 = *reinterpret_cast<const uint4*>(&D.gmask[0]);
-            const uint4 m1 = *reinterpret_cast<const uint4*>(&D.gmask[4]);
-            const int4 n0 = *reinterpret_cast<const int4*>(&D.gnv[0]);
-            const int4 n1 = *reinterpret_cast<const int4*>(&D.gnv[4]);
-            const uint32_t gm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-            const int gn[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+            static_assert(kGroups % 4 == 0 && kGroups <= 8, "tokvis: 4 or 8 groups per chunk");
+            uint32_t gm[kGroups];
+            int gn[kGroups];
+#pragma unroll
+            for (int q = 0; q < kGroups / 4; ++q) {
+              const uint4 mq = *reinterpret_cast<const uint4*>(&D.gmask[4 * q]);
+              const int4 nq = *reinterpret_cast<const int4*>(&D.gnv[4 * q]);
+              gm[4 * q] = mq.x; gm[4 * q + 1] = mq.y; gm[4 * q + 2] = mq.z; gm[4 * q + 3] = mq.w;
+              gn[4 * q] = nq.x; gn[4 * q + 1] = nq.y; gn[4 * q + 2] = nq.z; gn[4 * q + 3] = nq.w;
+            }
             uint32_t v = 0;
 #pragma unroll
-            for (int gi = 0; gi < 8; ++gi)
+            for (int gi = 0; gi < kGroups; ++gi)
               v |= (gi < n_grp && gn[gi] > 0 ? (gm[gi] >> (lane & 31)) & 1u : 0u) << gi;
             D.tokvis[lane] = (uint8_t)(lane < q_cnt ? v : 0u);
             D.tok[lane] = (int32_t)my_tok;
@@ -1505,7 +1519,7 @@ static int launch(const Launch& L, int dh, int hkv, int64_t n_tiles_static, void
 #ifdef LSRM_HEADPAIR
   const int hp = (!dyn && dh == 32 && hkv % 2 == 0) ? 2 : 1, np_ = hp == 2 ? 1 : (dh == 32 ? 2 : 1);
 #else
-  const int hp = 1, np_ = dh == 32 ? 2 : 1;
+  const int hp = 1, np_ = dh == 32 ? LSRM_NP : 1;
 #endif
   const int64_t n_items = dyn ? L.n_order : n_tiles_static * (hkv / hp);
   if (n_items == 0) return LSRM_OK;
@@ -1519,7 +1533,7 @@ static int launch(const Launch& L, int dh, int hkv, int64_t n_tiles_static, void
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     nsa_fused_kernel<D, HP, NP><<<grid, threads_of<HP, NP>(), smem, st>>>(L);               \
   } else
-  LSRM_TC_CASE(32, 1, 2)
+  LSRM_TC_CASE(32, 1, LSRM_NP)
 #if !LSRM_DBUF
   LSRM_TC_CASE(32, 2, 1)
 #endif
