@@ -80,7 +80,10 @@ class LocalQueries:
         return int(self.loc_tok.size)
 
 
-def local_queries(part: BlockPartition, owned) -> LocalQueries:
+def local_query_arrays(part: BlockPartition, owned):
+    """Host arrays of LocalQueries: (owned rows ascending, global token id of
+    every local row, each local row's block row, per-block offsets into the
+    local rows (empty for blocks other ranks own), local row ids)."""
     owned = np.sort(np.asarray(owned, np.int64))
     occ = part.occupancy.astype(np.int64)
     loc_tok = (np.concatenate([part.tokens_in_row(int(r)) for r in owned]).astype(np.int64)
@@ -90,6 +93,11 @@ def local_queries(part: BlockPartition, owned) -> LocalQueries:
     counts[owned] = occ[owned]
     win_offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     win_ids = np.arange(loc_tok.size, dtype=np.int32)   # owned blocks in ascending order
+    return owned, loc_tok, own_rows, win_offs, win_ids
+
+
+def local_queries(part: BlockPartition, owned) -> LocalQueries:
+    owned, loc_tok, own_rows, win_offs, win_ids = local_query_arrays(part, owned)
     return LocalQueries(part, owned, loc_tok, D.dev(own_rows), D.dev(win_offs), D.dev(win_ids))
 
 

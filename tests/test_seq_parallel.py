@@ -560,3 +560,40 @@ def test_capi_nccl_transport_world1(cuda):
         assert np.array_equal(out, ref)
     finally:
         tr.close()
+
+
+# ---------------------------------------------------------------------------
+# sequence-parallel training: the host side of LocalQueries
+
+
+@pytest.mark.parametrize("W", [2, 3, 8])
+def test_local_queries_cover_owned_blocks(c1_parts, W):
+    """Every rank's local rows are exactly its owned blocks' tokens (block-
+    major, owned blocks ascending); over the ranks every token appears once;
+    own rows name each local row's block; the window lists of a block hold
+    the local rows of its tokens and are empty for blocks another rank owns."""
+    from paper_2604_05182_b200.block_partition import BlockPartition
+    from paper_2604_05182_b200.training import local_query_arrays
+    for part, rows_of in zip(c1_parts, ("vol_rows", "img_rows")):
+        bp = BlockPartition(**{f: getattr(part, f) for f in (
+            "modality", "block_size", "block_grid", "n_blocks_total", "block_of_token",
+            "occupied_ids", "block_offsets", "block_token_ids", "occupancy", "block_centers",
+            "block_views")})
+        topo = S.shard_blocks(*c1_parts, W)
+        seen = []
+        for r in range(W):
+            owned, loc_tok, own_rows, win_offs, win_ids = local_query_arrays(
+                bp, getattr(topo, rows_of)[r])
+            want = [bp.tokens_in_row(int(b)) for b in owned]
+            assert np.array_equal(loc_tok, np.concatenate(want) if want else np.zeros(0))
+            assert np.array_equal(own_rows, np.repeat(owned, bp.occupancy[owned]))
+            assert win_offs.size == bp.n_occupied + 1 and win_offs[-1] == loc_tok.size
+            for b in range(bp.n_occupied):
+                ids = win_ids[win_offs[b]:win_offs[b + 1]]
+                if b in set(owned.tolist()):
+                    assert np.array_equal(loc_tok[ids], bp.tokens_in_row(b))
+                else:
+                    assert ids.size == 0
+            seen.append(loc_tok)
+        allt = np.concatenate(seen)
+        assert np.array_equal(np.sort(allt), np.arange(bp.n_tokens))
