@@ -413,6 +413,17 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
   tc_after_sync();
   const uint32_t tmem = SM.tmem_base + (uint32_t)(pipe_id * HP * HC);   // this pipeline's columns
   long long* const trp = (blockIdx.x == 0 && pipe_id == 0) ? g_trace : nullptr;  // debug trace
+#ifdef LSRM_TRACE
+  // per-pipeline start / end (globaltimer ns) after the chunk trace: the
+  // tail of the LPT queue (tools/attn_trace.py)
+  auto gtime = []() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (g_trace && (tid & 31) == 0 && warp % kSoftPerPipe == 0 && gp < 1024)
+    g_trace[kTraceChunks * kTraceEv + 2 * gp] = gtime();
+#endif
 
   if (m_items == 0) {
     // this pipeline has no work (small launches)
@@ -1394,6 +1405,10 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       if (last_all) break;
     }
     epilogue(c - 1);
+#ifdef LSRM_TRACE
+    if (g_trace && (tid & 31) == 0 && warp % kSoftPerPipe == 0 && gp < 1024)
+      g_trace[kTraceChunks * kTraceEv + 2 * gp + 1] = gtime();
+#endif
   }
   tc_before_sync();
   __syncthreads();

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--use", default="v2v")
     ap.add_argument("--workload", default="c3")
     ap.add_argument("--time", action="store_true", help="event-time each use's attention")
+    ap.add_argument("--tail", action="store_true",
+                    help="per-pipeline end times of the merged launch (needs -DLSRM_TRACE)")
     args = ap.parse_args()
     inst = build_instance(args.workload)
     layer = SparseAttentionLayer(inst)
@@ -57,12 +59,26 @@ def main():
         b.record()
         torch.cuda.synchronize()
         print(f"attention merged launch (4 uses, LPT queue): {a.elapsed_time(b) / 10 * 1e3:8.1f} us")
-    buf = torch.zeros((256, 32), dtype=torch.int64, device="cuda")
+    buf = torch.zeros((256 * 32 + 2048,), dtype=torch.int64, device="cuda")
+    if args.tail:   # per-pipeline start / end of the merged four-use launch
+        call("lsrm_debug_set_trace", buf.data_ptr())
+        eng.attend_all()
+        torch.cuda.synchronize()
+        call("lsrm_debug_set_trace", None)
+        se = buf[256 * 32:].cpu().numpy().reshape(-1, 2).astype(np.float64)
+        se = se[se[:, 0] > 0]
+        t0 = se[:, 0].min()
+        end = (se[:, 1] - t0) / 1e3
+        print(f"merged launch: {se.shape[0]} pipelines, end us: min {end.min():.1f} "
+              f"p10 {np.percentile(end, 10):.1f} median {np.median(end):.1f} "
+              f"p90 {np.percentile(end, 90):.1f} max {end.max():.1f}; idle share "
+              f"{1 - end.mean() / end.max():.3f}")
+        buf.zero_()
     call("lsrm_debug_set_trace", buf.data_ptr())
     eng.attend(args.use)
     torch.cuda.synchronize()
     call("lsrm_debug_set_trace", None)
-    tr = buf.cpu().numpy().astype(np.float64)
+    tr = buf[:256 * 32].reshape(256, 32).cpu().numpy().astype(np.float64)
     n = int((tr[:, 3] > 0).sum())
     tr = tr[:n]
     t0 = tr[0, 0]
