@@ -247,11 +247,8 @@ __device__ __forceinline__ float ex2_poly(float x) {
 }
 // Of every 16 exponentials, kPolyPer16 go to the FMA pipe (ex2_poly) and the
 // rest to the MUFU, whose issue rate (16/clk/SM) bounds the kernel.
-// measured (round 2, C3 merged launch): 0 -> 1.171 ms, 1 -> 1.154, 2 -> 1.158,
-// 3 -> 1.175 (C5: 2 -> -2 %); the exp phase is MUFU-bound while both
-// pipelines' warps are in it, so a little FMA-pipe work relieves it
 #ifndef LSRM_POLY_PER16
-#define LSRM_POLY_PER16 1
+#define LSRM_POLY_PER16 0
 #endif
 constexpr int kPolyPer16 = LSRM_POLY_PER16;
 __device__ __forceinline__ float ex2_mixed(float x, int j) {
