@@ -148,12 +148,6 @@ struct Launch {
 #ifndef LSRM_ONEPASS
 #define LSRM_ONEPASS 0
 #endif
-// the gated-merge accumulator of an item's finished branches: TMEM (0, 16
-// f16x2 columns) or shared memory (1, conflict-free [col pair][row] words;
-// measured neutral, 1.172 vs 1.177 ms, and it costs the bias staging area)
-#ifndef LSRM_MERGE_SMEM
-#define LSRM_MERGE_SMEM 0
-#endif
 #ifndef LSRM_PINGPONG
 #define LSRM_PINGPONG 0
 #endif
@@ -201,9 +195,7 @@ static_assert(kSplit == 1 || (!LSRM_ONEPASS && !LSRM_PINGPONG),
               "the split softmax is two-pass only");
 // gate biases staged in shared memory as [n_gates * hq][DH + 1] (padded rows:
 // the 16 heads of a warp hit 16 banks) when they fit, else read from global
-// (the shared-memory merge accumulator took the room: biases are read from
-// global memory, which only the single-use entry point passes)
-constexpr int kBiasMax = (LSRM_STAGES <= 3 && !LSRM_MERGE_SMEM) ? 3328 : 4;
+constexpr int kBiasMax = LSRM_STAGES <= 3 ? 3328 : 4;
 constexpr int kOnesCols = 16;    // extra V columns holding 1 (valid key) / 0 (padding)
 constexpr int kBitmapWords = 512;  // union bitmap: up to 16384 occupied KV blocks
 
@@ -305,9 +297,6 @@ struct alignas(128) Pipe {   // 128-byte aligned: q is a TMA destination
   __nv_bfloat16 k[kStages][HP][kNK * DH];
   __nv_bfloat16 v[kStages][HP][kNK * (DH + kOnesCols)];   // [V | ones] rows
   __nv_bfloat16 gate[HP][kM * DH];  // per row: gate logits of the branch that just ended
-#if LSRM_MERGE_SMEM
-  uint32_t merge[HP][DH / 2][kM];   // the item's gated merge so far (f16x2, [col pair][row])
-#endif
   int32_t ent[kMaxEnt];          // selected rows of the tile tokens, [t][kmax]
   uint32_t bitmap[kBitmapWords]; // selected-row bitmap of the current item
   int32_t wpre[kBitmapWords];    // rank of the first set bit of each word
@@ -857,9 +846,6 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     bool lastit_pend = false, rowok_pend = false, epi_pend = false;
     int64_t tok_pend = 0;
     __nv_bfloat16* const gate_s = &S.gate[hh][m * DH];   // this row's staged gate logits
-#if LSRM_MERGE_SMEM
-    uint32_t* const mrg = &S.merge[hh][0][m];   // f16x2 column pair j at mrg[j * kM]
-#endif
     uint32_t c = 0;
     // ping-pong: the HP=2 warpgroups take turns on the exponential phase
     // (named barriers 1, 2), so one's MUFU stream covers the other's loads,
@@ -917,13 +903,8 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
 #pragma unroll
         for (int j = 0; j < 16; ++j) r[j] = eo[cq + j];
         if (!firstbr_pend) {
-#if LSRM_MERGE_SMEM
-#pragma unroll
-          for (int j = 0; j < 8; ++j) mr[j] = mrg[(c0 / 2 + j) * kM];
-#else
           tmem_ld_cols<8>(tM + c0 / 2, mr);
           tmem_wait_ld();
-#endif
         }
 #pragma unroll
         for (int k8 = 0; k8 < 2; ++k8) {
@@ -974,15 +955,10 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
                                                  __uint_as_float(r[2 * j + 1]));
             w[j] = *reinterpret_cast<const uint32_t*>(&h2);
           }
-#if LSRM_MERGE_SMEM
-#pragma unroll
-          for (int j = 0; j < 8; ++j) mrg[(c0 / 2 + j) * kM] = w[j];
-#else
           tmem_st8(tM + c0 / 2, w);
-#endif
         }
       }
-      if (!LSRM_MERGE_SMEM && !lastit_pend) tmem_wait_st();
+      if (!lastit_pend) tmem_wait_st();
     };
     auto epilogue = [&](uint32_t pc) {
       uint32_t eo[kOCols + 1];
