@@ -310,8 +310,6 @@ typedef struct lsrm_gemm_problem {
   const void* res; int64_t ldr; /* [m,n] or NULL; may alias c */
   int32_t flags;
   int32_t reserved;
-  const uint32_t* sig_mask;     /* optional DEVICE [n/32] words: bit c%32 of word c/32
-                                   set = sigmoid(column c) after bias / act (n % 32 == 0) */
 } lsrm_gemm_problem;
 /* problems: HOST array of n_problems descriptors.  With A_MN / B_MN the
  * K-major rules above apply to the remaining K-major operand only (k % 8 == 0
@@ -382,8 +380,6 @@ typedef struct lsrm_nsa_use {
   void* branch_lse;      /* optional f32 [n_gates][nq][hq]: each branch's
                             log-sum-exp of the scaled logits (natural log);
                             set with branch_out or not at all */
-  int64_t gate_prob;     /* 1: gate_logits hold the gates' sigmoid values (the
-                            projection GEMM's sigmoid columns), not logits */
 } lsrm_nsa_use;
 int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, int hkv, int dh,
                                 const int32_t* order, int64_t n_order, int32_t* counter,

@@ -87,7 +87,7 @@ class GemmProblem(C.Structure):
                 ("a", C.c_void_p), ("lda", C.c_int64), ("bt", C.c_void_p), ("ldb", C.c_int64),
                 ("c", C.c_void_p), ("ldc", C.c_int64), ("bias", C.c_void_p),
                 ("res", C.c_void_p), ("ldr", C.c_int64), ("flags", C.c_int32),
-                ("reserved", C.c_int32), ("sig_mask", C.c_void_p)]
+                ("reserved", C.c_int32)]
 
 
 GEMM_OUT_F32, GEMM_BIAS_F32, GEMM_RES_F32, GEMM_GELU, GEMM_A_MN, GEMM_B_MN = 1, 2, 4, 8, 16, 32
@@ -95,7 +95,7 @@ _MAX_PROBLEMS = 32   # problems per lsrm_gemm_tc launch
 
 
 def gemm_problem(a: torch.Tensor, bt: torch.Tensor, out: torch.Tensor, bias=None, res=None,
-                 gelu=False, a_mn=False, b_mn=False, k=None, sig_mask=None) -> GemmProblem:
+                 gelu=False, a_mn=False, b_mn=False, k=None) -> GemmProblem:
     """One tcgen05 GEMM problem: out = act(a @ bt^T + bias) + res, with a
     [m,k] and bt [n,k] bf16 (K contiguous: bt is the weight transposed).
     a_mn: `a` is A^T as stored, [k,m]; b_mn: `bt` is B as stored, [k,n]
@@ -117,8 +117,8 @@ def gemm_problem(a: torch.Tensor, bt: torch.Tensor, out: torch.Tensor, bias=None
         flags |= GEMM_RES_F32 if res.dtype == torch.float32 else 0
     prob = GemmProblem(m, n, k, a.data_ptr(), a.stride(0), bt.data_ptr(), bt.stride(0),
                        out.data_ptr(), out.stride(0), D.ptr(bias), D.ptr(res),
-                       res.stride(0) if res is not None else 0, flags, 0, D.ptr(sig_mask))
-    prob.keep = (a, bt, out, bias, res, sig_mask)   # the descriptor holds raw pointers
+                       res.stride(0) if res is not None else 0, flags, 0)
+    prob.keep = (a, bt, out, bias, res)   # the descriptor holds raw pointers
     return prob
 
 

@@ -119,7 +119,6 @@ struct Params {
   // log), f32 [n_gates][nq][hq]
   float* o_br;
   float* lse_br;
-  int gate_prob;   // 1: gl holds the gates' sigmoid values (projection GEMM epilogue)
   // Q as a 5-D tensor map {d%8, g%8, d/8, g/8, row} (strides 1, DH, 8, 8 DH,
   // ld_q elements): the box of one token and 8k q-heads lands in shared
   // memory directly in the UMMA K-major core-matrix layout
@@ -913,13 +912,11 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int cj = 8 * k8 + j;
-            // the gate: its probability as staged, or sigmoid(z) = 0.5 + 0.5
-            // tanh(z / 2) of the logit (one MUFU op)
-            const float z = __bfloat162float(hv[j]);
-            const float gt = PB.gate_prob ? z
-                                          : fmaf(0.5f, tanh_approx(0.5f * (z + (bp ? bp[c0 + cj] : 0.f))),
-                                                 0.5f);
-            float v = rowok_pend ? __uint_as_float(r[cj]) * inv * gt : 0.f;
+            const float z = __bfloat162float(hv[j]) + (bp ? bp[c0 + cj] : 0.f);
+            // sigmoid(z) = 0.5 + 0.5 tanh(z / 2): one MUFU op
+            float v = rowok_pend ? __uint_as_float(r[cj]) * inv *
+                                       fmaf(0.5f, tanh_approx(0.5f * z), 0.5f)
+                                 : 0.f;
             if (!firstbr_pend) {
               const __half2 hm = *reinterpret_cast<const __half2*>(&mr[cj / 2]);
               v += (cj & 1) ? __high2float(hm) : __low2float(hm);
@@ -1622,7 +1619,6 @@ int lsrm_nsa_attention_tc(const void* q, int64_t ld_q, int64_t nq, int hq, int h
   p.own_rows = nullptr;
   p.o_br = nullptr;
   p.lse_br = nullptr;
-  p.gate_prob = 0;
   if (int rc = tc::make_q_map(p, G, dh)) return rc;
   tc::Launch L{};
   L.use[0] = p;
@@ -1683,7 +1679,6 @@ int lsrm_nsa_attention_tc_multi(const lsrm_nsa_use* uses, int n_uses, int hq, in
     p.own_rows = U.own_rows;
     p.o_br = (float*)U.branch_out;
     p.lse_br = (float*)U.branch_lse;
-    p.gate_prob = (int)U.gate_prob;
     LSRM_REQUIRE((U.branch_out == nullptr) == (U.branch_lse == nullptr) &&
                      ((uintptr_t)U.branch_out % 16) == 0,
                  "use %d: branch_out and branch_lse go together (16-byte aligned)", u);

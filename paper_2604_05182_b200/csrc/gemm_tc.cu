@@ -60,7 +60,6 @@ struct Prob {
   int flags;
   int tiles_n;
   int64_t tile_begin;
-  const uint32_t* sig_mask;   // optional: bit c%32 of word c/32 = sigmoid column c
 };
 
 struct __align__(64) Params {
@@ -131,18 +130,6 @@ __device__ __forceinline__ void store_piece(const Prob& pb, const void* tmap_c, 
   if (pb.flags & LSRM_GEMM_GELU) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
-  }
-  if (pb.sig_mask) {   // sigmoid columns (the gate probabilities of the attention)
-    const uint32_t mk = __ldg(pb.sig_mask + col0 / 32);
-    if (mk) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if ((mk >> j) & 1u) {   // sigmoid(x) = 0.5 + 0.5 tanh(x / 2): one MUFU op
-          float t;
-          asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * v[j]));
-          v[j] = fmaf(0.5f, t, 0.5f);
-        }
-    }
   }
   if (pb.res && row < pb.m) {
     if (pb.flags & LSRM_GEMM_RES_F32) {
@@ -577,9 +564,6 @@ extern "C" int lsrm_gemm_tc(const lsrm_gemm_problem* probs, int n_problems, void
     pb.c = q.c; pb.ldc = q.ldc;
     pb.bias = q.bias; pb.res = q.res; pb.ldr = q.ldr;
     pb.flags = q.flags;
-    pb.sig_mask = q.sig_mask;
-    LSRM_REQUIRE(q.sig_mask == nullptr || q.n % 32 == 0,
-                 "gemm_tc: a sigmoid-column mask needs n %% 32 == 0");
     pb.tiles_n = (int)ceil_div(q.n, BN);
     pb.tile_begin = tiles;
     tiles += ceil_div(q.m, BM * cg) * pb.tiles_n;

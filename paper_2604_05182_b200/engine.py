@@ -68,11 +68,7 @@ SELF_GLOBAL_TILES = os.environ.get("LSRM_SELF_GLOBAL_TILES", "0") != "0"
 PACK_SELF_TAILS = os.environ.get("LSRM_PACK_SELF_TAILS", "0") != "0"
 # self uses run cmp + sel on such tiles and the window branch in a second,
 # accumulating launch (correct, measured slower: 1.23 -> 1.31 ms; off)
-SPLIT_SELF_WINDOW = os.environ.get("LSRM_SPLIT_SELF_WINDOW", "0") != "0"
-# gate sigmoids in the projection GEMM's epilogue (the attention epilogue then
-# multiplies by stored probabilities); LSRM_GATE_PROB=0: logits, sigmoid in
-# the attention epilogue
-GATE_PROB = os.environ.get("LSRM_GATE_PROB", "1") != "0"   # extra V columns (1 = real key) that make P.V also emit row sums
+SPLIT_SELF_WINDOW = os.environ.get("LSRM_SPLIT_SELF_WINDOW", "0") != "0"   # extra V columns (1 = real key) that make P.V also emit row sums
 
 
 def _padded(occ: np.ndarray) -> np.ndarray:
@@ -101,8 +97,7 @@ class NsaUse(C.Structure):
                 ("ld_gl", C.c_int64), ("gate_col0", C.c_int64), ("n_gates", C.c_int64),
                 ("merged", C.c_void_p), ("perm", C.c_void_p), ("branch_first", C.c_int64),
                 ("accumulate", C.c_int64), ("own_rows", C.c_void_p),
-                ("branch_out", C.c_void_p), ("branch_lse", C.c_void_p),
-                ("gate_prob", C.c_int64)]
+                ("branch_out", C.c_void_p), ("branch_lse", C.c_void_p)]
 
 
 class PackedShard:
@@ -260,21 +255,6 @@ class SparseLayerEngine:
             bcat[s_].append(np.zeros(int(wx.shape[1]), np.float32))
             ncol[s_] += int(wx.shape[1])
         self.ncol = ncol
-        # the gate columns leave the projection GEMM as sigmoid values (its
-        # epilogue; the attention kernel's `gate_prob` mode multiplies by them)
-        self.sig_mask = {}
-        for s_ in ("x", "y"):
-            bits = np.zeros(max(ncol[s_], 32), bool)
-            for use in self.uses:
-                qs, _, ng = USE_GEOM[use]
-                if qs == s_:
-                    c0 = self.cols[(use, "q")] + d
-                    bits[c0:c0 + ng * d] = True
-            require(ncol[s_] % 32 == 0, "projection width must be a multiple of 32")
-            words = np.packbits(bits.reshape(-1, 32)[:, ::-1], axis=1, bitorder="big")
-            words = words.view(">u4").astype(np.uint32).reshape(-1) if bits.any() else None
-            self.sig_mask[s_] = (D.dev(words.astype(np.int32))
-                                 if words is not None and GATE_PROB else None)
         # weights stored transposed ([n, k], K contiguous): both tcgen05 GEMM
         # operands K-major (csrc/gemm_tc.cu)
         self.w_cat = {s: D.dev(np.concatenate(wcat[s], axis=1).T, torch.bfloat16)
@@ -422,7 +402,6 @@ class SparseLayerEngine:
         hkv = p.n_kv_heads
         T = 128 // p.group_size
         queues = {"A": ([], [], []), "B": ([], [], [])}   # uses, costs, codes
-        solo = []   # (queue, use, NsaUse, first cost index): one-use queues for attend()
 
         def add(qname, use, tiles, rows_h, cnt_h, perm, n_gates, br_first, accum,
                 own_rows=None):
@@ -438,7 +417,7 @@ class SparseLayerEngine:
             self._job_refs += [t for t in (perm_d, rows_d, cnt_d, tiles, own_d) if t is not None]
             uses, costs, codes = queues[qname]
             ui = len(uses)
-            nu = NsaUse(
+            uses.append(NsaUse(
                 Y[:, qcol:].data_ptr(), Y.stride(0), mq.n_loc,
                 self.buf[("k_il", use)].data_ptr(), self.buf[("v_il", use)].data_ptr(),
                 mk.pad_off.data_ptr(), mk.kv_off.data_ptr(), mk.n_rows_pad,
@@ -446,9 +425,7 @@ class SparseLayerEngine:
                 mk.n_blocks, tiles.data_ptr(), int(tiles.shape[0]), rows_d.data_ptr(),
                 cnt_d.data_ptr(), self.kmax[use], Y.data_ptr(), Y.stride(0),
                 qcol + self.d, n_gates, self.buf[("merged", use)].data_ptr(), D.ptr(perm_d),
-                br_first, accum, D.ptr(own_d), None, None, int(GATE_PROB))
-            uses.append(nu)
-            solo.append((qname, use, nu, len(costs)))
+                br_first, accum, D.ptr(own_d)))
             th = D.host(tiles)
             padlen = np.diff(mk.pad_off_host)
             cmp_rows = (mk.n_blocks + ROW_PAD - 1) // ROW_PAD * ROW_PAD
@@ -513,19 +490,6 @@ class SparseLayerEngine:
             else:
                 add("A", use, self.tiles[use], rows_h, cnt_h, np.lexsort(sig + (blk,)), ng, 0, 0)
 
-        # one-use queues (attend(use): each use alone, informational timing)
-        self.use_queues = {}
-        for qname, use, nu, c0 in solo:
-            if qname != "A" or use in self.use_queues:
-                continue
-            _, costs_q, codes_q = queues[qname]
-            cs = np.asarray(costs_q[c0:], np.int64)
-            cd = np.asarray(codes_q[c0:], np.int64)
-            ui = cd[0] >> 28 if cd.size else 0
-            sel = (cd >> 28) == ui
-            cs, cd = cs[sel], cd[sel] & 0x0FFFFFFF
-            order = cd[np.lexsort((cd, -cs))].astype(np.int32)
-            self.use_queues[use] = ((NsaUse * 1)(nu), D.dev(order), D.zeros((1,), torch.int32))
         self.attn_queues = []
         for qname in ("A", "B"):
             uses, costs, codes = queues[qname]
@@ -550,8 +514,7 @@ class SparseLayerEngine:
     def project(self, x_loc: torch.Tensor, y_loc: torch.Tensor, streams=("x", "y")):
         """The streams' fused projections (q | gate logits + bias | k | v)
         as ONE grouped tcgen05 GEMM launch."""
-        probs = [_ops.gemm_problem(a, self.w_cat[s], self.buf[("Y", s)], bias=self.b_cat[s],
-                                   sig_mask=self.sig_mask[s])
+        probs = [_ops.gemm_problem(a, self.w_cat[s], self.buf[("Y", s)], bias=self.b_cat[s])
                  for s, a in (("x", x_loc), ("y", y_loc))
                  if s in streams and self.meta[s].n_loc and self.ncol[s]]
         if probs:
@@ -580,16 +543,22 @@ class SparseLayerEngine:
                  p.head_dim, ones, None, None, 0, None, int(il.shape[1]), il.data_ptr(), st)
 
     def attend(self, use: str):
-        """One use's attention alone (its own heaviest-first queue; the layer
-        runs all four uses in one launch, `attend_all`)."""
-        p = self.params
-        hit = self.use_queues.get(use)
-        if hit is None or int(hit[1].shape[0]) == 0:
+        qs, ks, ng = USE_GEOM[use]
+        mq, mk, p = self.meta[qs], self.meta[ks], self.params
+        tiles = self.tiles[use]
+        if int(tiles.shape[0]) == 0:
             return
-        uses, order, counter = hit
-        call("lsrm_nsa_attention_tc_multi", C.cast(uses, C.c_void_p), 1, p.n_q_heads,
-             p.n_kv_heads, p.head_dim, order.data_ptr(), int(order.shape[0]),
-             counter.data_ptr(), D.stream())
+        Y = self.buf[("Y", qs)]
+        qcol = self.cols[(use, "q")]
+        q = Y[:, qcol:]
+        call("lsrm_nsa_attention_tc", q.data_ptr(), Y.stride(0), mq.n_loc, p.n_q_heads,
+             p.n_kv_heads, p.head_dim, self.buf[("k_il", use)].data_ptr(),
+             self.buf[("v_il", use)].data_ptr(), mk.pad_off.data_ptr(), mk.kv_off.data_ptr(),
+             mk.n_rows_pad, self.buf[("kc_il", use)].data_ptr(),
+             self.buf[("vc_il", use)].data_ptr(), mk.n_blocks, tiles.data_ptr(),
+             int(tiles.shape[0]), self.rows[use].data_ptr(), self.count[use].data_ptr(),
+             self.kmax[use], Y.data_ptr(), Y.stride(0), qcol + self.d,
+             None, ng, self.buf[("merged", use)].data_ptr(), D.stream())   # bias: in the GEMM
 
     def output(self, use: str):
         if self.buf[("merged", use)].shape[0]:
