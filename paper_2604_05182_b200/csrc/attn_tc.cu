@@ -238,8 +238,12 @@ __device__ __forceinline__ float ex2_poly(float x) {
 }
 // Of every 16 exponentials, kPolyPer16 go to the FMA pipe (ex2_poly) and the
 // rest to the MUFU, whose issue rate (16/clk/SM) bounds the kernel.
+// same-box A/B (round 2, profiles/r2/ab_poly1_vs_default.txt): 1 of 16 on
+// the FMA pipe, attention 1.149 -> 1.132 ms, layer 1.557 -> 1.544 ms; 2/16
+// and 3/16 lose again (C3 sweep).  The exp phase is MUFU-bound while both
+// pipelines' warps are in it.
 #ifndef LSRM_POLY_PER16
-#define LSRM_POLY_PER16 0
+#define LSRM_POLY_PER16 1
 #endif
 constexpr int kPolyPer16 = LSRM_POLY_PER16;
 __device__ __forceinline__ float ex2_mixed(float x, int j) {
