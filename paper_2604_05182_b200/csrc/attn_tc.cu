@@ -249,6 +249,27 @@ constexpr int kPolyPer16 = LSRM_POLY_PER16;
 __device__ __forceinline__ float ex2_mixed(float x, int j) {
   return j >= 16 - kPolyPer16 ? ex2_poly(x) : ex2(x);
 }
+// Gate sigmoid of the branch epilogue.  Default: 0.5 + 0.5 tanh(z / 2), one
+// MUFU op.  LSRM_FMA_SIGMOID: FMA pipe only (the exp phase next door is
+// MUFU-bound): 1 / (1 + 2^(-z log2 e)) with ex2_poly and a Newton reciprocal
+// from a bit-trick seed (3 steps, rel. error < 1e-6 on the clamped range).
+#ifndef LSRM_FMA_SIGMOID
+#define LSRM_FMA_SIGMOID 0
+#endif
+__device__ __forceinline__ float sigmoid_gate(float z) {
+#if LSRM_FMA_SIGMOID
+  const float zc = fminf(fmaxf(z, -30.f), 30.f);
+  const float d = 1.f + ex2_poly(-1.4426950408889634f * zc);   // in [1, 2^44]
+  float r = __int_as_float(0x7EF311C7 - __float_as_int(d));     // ~1/d seed
+  r = r * fmaf(-d, r, 2.f);
+  r = r * fmaf(-d, r, 2.f);
+  r = r * fmaf(-d, r, 2.f);
+  return r;
+#else
+  return fmaf(0.5f, tanh_approx(0.5f * z), 0.5f);
+#endif
+}
+
 // 16 logits -> 8 words of packed bf16 exp2(s * sl2 + nb)
 __device__ __forceinline__ void exp16(const uint32_t* s, float sl2, float nb, uint32_t* w) {
 #pragma unroll
@@ -919,7 +940,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
             const float z = __bfloat162float(hv[j]) + (bp ? bp[c0 + cj] : 0.f);
             // sigmoid(z) = 0.5 + 0.5 tanh(z / 2): one MUFU op
             float v = rowok_pend ? __uint_as_float(r[cj]) * inv *
-                                       fmaf(0.5f, tanh_approx(0.5f * z), 0.5f)
+                                       sigmoid_gate(z)
                                  : 0.f;
             if (!firstbr_pend) {
               const __half2 hm = *reinterpret_cast<const __half2*>(&mr[cj / 2]);
