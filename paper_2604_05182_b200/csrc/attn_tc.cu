@@ -253,6 +253,9 @@ __device__ __forceinline__ float ex2_mixed(float x, int j) {
 // MUFU op.  LSRM_FMA_SIGMOID: FMA pipe only (the exp phase next door is
 // MUFU-bound): 1 / (1 + 2^(-z log2 e)) with ex2_poly and a Newton reciprocal
 // from a bit-trick seed (3 steps, rel. error < 1e-6 on the clamped range).
+// Measured same-box (tools/ab_bench.sh): attention 1.133 -> 1.337 ms; the
+// epilogue sits on the softmax warps' critical path and the long FMA chain
+// costs far more latency than the MUFU op it saves.  Off.
 #ifndef LSRM_FMA_SIGMOID
 #define LSRM_FMA_SIGMOID 0
 #endif
