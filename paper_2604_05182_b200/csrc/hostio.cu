@@ -30,6 +30,7 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+#include <unistd.h>
 #include <vector>
 
 namespace lsrm {
@@ -38,7 +39,16 @@ namespace {
 class HostPool {
  public:
   static HostPool& get() {
-    static HostPool* p = new HostPool();   // never destroyed: workers outlive atexit
+    // never destroyed (workers outlive atexit); a forked child gets a pool of
+    // its own (the parent's worker threads do not exist there)
+    static std::mutex m;
+    static HostPool* p = nullptr;
+    static pid_t owner = 0;
+    std::lock_guard<std::mutex> lk(m);
+    if (p == nullptr || owner != getpid()) {
+      p = new HostPool();
+      owner = getpid();
+    }
     return *p;
   }
   int parts() const { return (int)workers_.size() + 1; }

@@ -182,3 +182,16 @@ def test_cast_vectorised_and_tail(cuda, n):
     assert torch.isnan(y[0]) and torch.isinf(y[1])
     z = _ops.cast(y, torch.float32)
     assert torch.equal(z[4:], y[4:].float())
+
+
+def test_gemm_train_split_k_deterministic(cuda):
+    """Split-K partial products are summed in slice order: two runs of the
+    same weight-gradient GEMM give identical bytes."""
+    from paper_2604_05182_b200 import _ops
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(16815, 1024, generator=g, device="cuda")
+    dy = torch.randn(16815, 1024, generator=g, device="cuda")
+    a = _ops.gemm_train(x, dy, trans_a=True)
+    b = _ops.gemm_train(x, dy, trans_a=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
