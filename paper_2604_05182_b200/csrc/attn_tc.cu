@@ -280,6 +280,22 @@ __device__ __forceinline__ void exp16(const uint32_t* s, float sl2, float nb, ui
     w[j] = pack_bf16(ex2_mixed(fmaf(__uint_as_float(s[2 * j]), sl2, nb), 2 * j),
                      ex2_mixed(fmaf(__uint_as_float(s[2 * j + 1]), sl2, nb), 2 * j + 1));
 }
+#ifndef LSRM_EARLY_SFREE
+#define LSRM_EARLY_SFREE 0
+#endif
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// 16 f16 logits (8 words, already relative to a reference) -> 8 words of
+// packed bf16 exp2(x + nb)
+__device__ __forceinline__ void exp16_f16(const uint32_t* h, float nb, uint32_t* w) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[j]));
+    w[j] = pack_bf16(ex2(f.x + nb), ex2(f.y + nb));
+  }
+}
 __device__ __forceinline__ void zero8(uint32_t* w) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) w[j] = 0u;
@@ -1188,10 +1204,32 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           }
         } else {
 #else
+#if LSRM_EARLY_SFREE
+        // pieces 0,1 kept as f16 (x - ref) so S(c) can be released as soon as
+        // pieces 2,3 are loaded; ref = the running max (the chunk's max of
+        // pieces 0,1 for a branch's first chunk): the values that matter are
+        // near 0, where f16 keeps 11 bits
+        uint32_t h01[32];
+        float ref = 0.f;
+        if (hi) {
+          ref = m_run != kNegInf ? m_run : (mx == kNegInf ? 0.f : mx * sl2);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            h01[j] = pack_f16(fmaf(__uint_as_float(sa[2 * j]), sl2, -ref),
+                              fmaf(__uint_as_float(sa[2 * j + 1]), sl2, -ref));
+            h01[16 + j] = pack_f16(fmaf(__uint_as_float(sb[2 * j]), sl2, -ref),
+                                   fmaf(__uint_as_float(sb[2 * j + 1]), sl2, -ref));
+          }
+        }
+#endif
         if (hi) {
           tmem_ld32(tSc + HCols::kS + 64, sa);
           if (ncols > 96) tmem_ld32(tSc + HCols::kS + 96, sb);
           tmem_wait_ld();
+#if LSRM_EARLY_SFREE
+          tc_before_sync();
+          mbar_arrive(&S.s_free[hh]);   // S(c) in registers (0,1 as f16): QK(c+1) may go
+#endif
           if (LSRM_LIVE(2)) {
             LSRM_MAX(sa, 0, 4)
             LSRM_MAX(sa, 16, 5)
@@ -1282,6 +1320,30 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           LSRM_EXP_PIECE(sc, 2)
           if (ncols > 96) LSRM_EXP_PIECE(sd, 3)
         }
+#elif LSRM_EARLY_SFREE
+        if (hi) {
+          LSRM_EXP_PIECE(sa, 2)
+          if (ncols > 96) LSRM_EXP_PIECE(sb, 3)
+          // pieces 0,1 from their f16 copies: exp2((x - ref) + (ref - m))
+          const float nbh = m_use == kNegInf ? 0.f : ref - m_use;
+#pragma unroll
+          for (int pc = 0; pc < 2; ++pc) {
+            uint32_t w[16];
+            if ((live >> (2 * pc)) & 3u) {
+              exp16_f16(h01 + 16 * pc, ((visb >> (2 * pc)) & 1u) ? nbh : kNegInf, w);
+              exp16_f16(h01 + 16 * pc + 8, ((visb >> (2 * pc + 1)) & 1u) ? nbh : kNegInf, w + 8);
+            } else {
+              zero8(w);
+              zero8(w + 8);
+            }
+            wait_pv();
+            tmem_st16(tPc + 16 * pc, w);
+          }
+          if (tid == 0) trace(trp, c, 12);
+        } else {
+          LSRM_EXP_PIECE(sa, 0)
+          if (ncols > 32) LSRM_EXP_PIECE(sb, 1)
+        }
 #else
         if (hi) {
           LSRM_EXP_PIECE(sa, 2)
@@ -1294,8 +1356,10 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           if (tid == 0) trace(trp, c, 12);
         }
 #endif
+#if !LSRM_EARLY_SFREE
         LSRM_EXP_PIECE(sa, 0)
         if (ncols > 32) LSRM_EXP_PIECE(sb, 1)
+#endif
 #undef LSRM_EXP_PIECE
       } else {
         // ---- one pass: exponentials against m_run while the chunk max is
