@@ -280,6 +280,10 @@ __device__ __forceinline__ void exp16(const uint32_t* s, float sl2, float nb, ui
     w[j] = pack_bf16(ex2_mixed(fmaf(__uint_as_float(s[2 * j]), sl2, nb), 2 * j),
                      ex2_mixed(fmaf(__uint_as_float(s[2 * j + 1]), sl2, nb), 2 * j + 1));
 }
+// LSRM_EARLY_SFREE: pieces 0,1 packed to f16 (x - running max) after their
+// max so S(c) is released before the exp pass.  Correct, but same-box A/B
+// 1.133 -> 1.275 ms (168 registers with spills, and the f16 pack / unpack /
+// add per element in the MUFU-bound exp phase).  Off.
 #ifndef LSRM_EARLY_SFREE
 #define LSRM_EARLY_SFREE 0
 #endif
