@@ -141,6 +141,10 @@ int acquire_ring(Ring** out) {
   for (int k = 0; k < kSlots; ++k) {
     if (cudaHostAlloc(&r->slot[k], kSlotBytes, cudaHostAllocPortable) != cudaSuccess ||
         cudaEventCreateWithFlags(&r->ev[k], cudaEventDisableTiming) != cudaSuccess) {
+      for (int j = 0; j < kSlots; ++j) {   // release what was made
+        if (r->slot[j]) cudaFreeHost(r->slot[j]);
+        if (r->ev[j]) cudaEventDestroy(r->ev[j]);
+      }
       delete r;
       return set_error(LSRM_E_CUDA, "pinned staging allocation failed");
     }
