@@ -21,6 +21,12 @@
 
 #include "common.cuh"
 
+// minimum resident CTAs per SM the register allocation targets (occupancy
+// of these latency-bound per-warp passes); 1 = the compiler's choice
+#ifndef LSRM_BWD_MINBLOCKS
+#define LSRM_BWD_MINBLOCKS 1
+#endif
+
 namespace lsrm {
 namespace bwdmma {
 
@@ -214,7 +220,7 @@ __device__ __forceinline__ void walk_cmp_tiles(int64_t nk, const __nv_bfloat16* 
 
 // dQ pass: warp per (query, kv head).
 template <int DH, bool CMP>
-__global__ void __launch_bounds__(32 * kDqWarps)
+__global__ void __launch_bounds__(32 * kDqWarps, LSRM_BWD_MINBLOCKS)
 dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dob,
               const float* __restrict__ dO, const float* __restrict__ O,
               const float* __restrict__ lse_in, int64_t nq, int hq,
@@ -400,7 +406,7 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
 // softmax over the key set in 16-key tiles; writes the branch output (fp32)
 // and lse per (query, head) for the backward.
 template <int DH, bool CMP>
-__global__ void __launch_bounds__(32 * kDqWarps)
+__global__ void __launch_bounds__(32 * kDqWarps, LSRM_BWD_MINBLOCKS)
 fwd_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, int64_t nq, int hq, int hkv,
                const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                float* __restrict__ out, float* __restrict__ lse_out) {
@@ -541,7 +547,7 @@ constexpr int kKvKeys = 64;
 constexpr int kQB = LSRM_BWD_QB;   // matched queries staged per shared-memory round
 
 template <int DH>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, LSRM_BWD_MINBLOCKS)
 dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dob,
                 const float* __restrict__ lse, const float* __restrict__ dsum, int64_t nq, int hq,
                 int hkv, const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
