@@ -1,7 +1,8 @@
 #!/bin/bash
 # ncu --set full of the kernels added after the attention profile: the Stage-2
-# block's row kernels and the training path (mma.sync branch forward / dQ /
-# dK,dV, res-block backward).
+# block's row kernels and the full-block training step (fused tcgen05
+# forward, mma.sync dQ / dK,dV, res-block and LayerNorm backward, casts,
+# split-K sums, tcgen05 GEMMs).
 #   bash tools/profile_extra.sh <tag>              (GPU box; writes gpurun_out/)
 #   bash tools/profile_extra.sh <tag> --summarise  (here; writes profiles/<tag>/)
 TAG=${1:-r1}
@@ -11,9 +12,9 @@ if [ "$2" != "--summarise" ]; then
       -k "regex:gate_mix_ln_fast|add_ln_fast|bias_act_fast" --launch-count 6 \
       -o gpurun_out/block_full_$TAG -f python tools/block_profile.py > /dev/null 2>&1
   ncu --set full --import-source on --clock-control none \
-      -k "regex:fwd_mma|dq_mma|dkdv_mma|res_block_bwd" --launch-count 12 \
-      -o gpurun_out/train_full_$TAG -f \
-      python tools/train_step.py --fast --steps 1 --warmup 0 > /dev/null 2>&1
+      -k "regex:nsa_fused|dq_mma|dkdv_mma|res_block_bwd|layer_norm_bwd|cast8|sum_slices|gemm_tc" \
+      --launch-skip 400 --launch-count 24 -o gpurun_out/train_full_$TAG -f \
+      python tools/train_launches.py > /dev/null 2>&1
   exit 0
 fi
 mkdir -p profiles/$TAG
