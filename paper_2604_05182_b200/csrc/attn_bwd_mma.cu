@@ -22,11 +22,13 @@
 #include "common.cuh"
 
 // minimum resident CTAs per SM the register allocation targets (occupancy
-// of these latency-bound per-warp passes); 1 = the compiler's choice.
+// of these latency-bound per-warp passes); unset = the compiler's choice.
 // Same-box A/B (tools/ab_train.sh): 6 -> 80 registers with spills, backward
 // 13.74 -> 15.1 ms at C3.
-#ifndef LSRM_BWD_MINBLOCKS
-#define LSRM_BWD_MINBLOCKS 1
+#ifdef LSRM_BWD_MINBLOCKS
+#define LSRM_BWD_BOUNDS(t) __launch_bounds__(t, LSRM_BWD_MINBLOCKS)
+#else
+#define LSRM_BWD_BOUNDS(t) __launch_bounds__(t)
 #endif
 
 namespace lsrm {
@@ -222,7 +224,7 @@ __device__ __forceinline__ void walk_cmp_tiles(int64_t nk, const __nv_bfloat16* 
 
 // dQ pass: warp per (query, kv head).
 template <int DH, bool CMP>
-__global__ void __launch_bounds__(32 * kDqWarps, LSRM_BWD_MINBLOCKS)
+__global__ void LSRM_BWD_BOUNDS(32 * kDqWarps)
 dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dob,
               const float* __restrict__ dO, const float* __restrict__ O,
               const float* __restrict__ lse_in, int64_t nq, int hq,
@@ -408,7 +410,7 @@ dq_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat1
 // softmax over the key set in 16-key tiles; writes the branch output (fp32)
 // and lse per (query, head) for the backward.
 template <int DH, bool CMP>
-__global__ void __launch_bounds__(32 * kDqWarps, LSRM_BWD_MINBLOCKS)
+__global__ void LSRM_BWD_BOUNDS(32 * kDqWarps)
 fwd_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, int64_t nq, int hq, int hkv,
                const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                float* __restrict__ out, float* __restrict__ lse_out) {
@@ -549,7 +551,7 @@ constexpr int kKvKeys = 64;
 constexpr int kQB = LSRM_BWD_QB;   // matched queries staged per shared-memory round
 
 template <int DH>
-__global__ void __launch_bounds__(128, LSRM_BWD_MINBLOCKS)
+__global__ void LSRM_BWD_BOUNDS(128)
 dkdv_mma_kernel(KeySet ks, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dob,
                 const float* __restrict__ lse, const float* __restrict__ dsum, int64_t nq, int hq,
                 int hkv, const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
