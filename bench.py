@@ -354,7 +354,8 @@ def run_gpu(args):
                "note": "bounded sample; `bench.py --impl reference` times the full layer"}
     proj_flops = layer.engine.projection_flops()
     block = time_sparse_block(inst, n_tok, args.steps)
-    train = time_train_step(inst) if wl_name != "c5" else None
+    # (C5: ≈ 370 ms per step, 67 GB peak; a few seconds with the warm-ups)
+    train = time_train_step(inst)
     setup = time_setup(wl_name) if wl_name in ("c3", "c4") else None
     c1 = time_c1_fp32(max(5, args.steps)) if wl_name == "c3" else None
     line = {
