@@ -124,10 +124,7 @@ struct KeySet {
   }
 };
 
-#ifndef LSRM_DQ_WARPS
-#define LSRM_DQ_WARPS 4
-#endif
-constexpr int kDqWarps = LSRM_DQ_WARPS;
+constexpr int kDqWarps = 4;
 
 // Walks the 16-key tiles of query i's key set (one warp, warp-private smem
 // tiles sK / sV): the next tile's K / V rows are loaded into registers while

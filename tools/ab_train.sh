@@ -8,7 +8,7 @@ for i in 1 2 3; do
 import sys; sys.path.insert(0, '.')
 import bench
 from paper_2604_05182_b200.layer import build_instance
-r = bench.time_train_step(build_instance('${WL:-c3}'), steps=5)
+r = bench.time_train_step(build_instance('c3'), steps=5)
 print('$side', round(r['ms_per_step'], 3), 'fwd', round(r['forward_ms'], 3), 'bwd', round(r['backward_ms'], 3))" 2>/dev/null)
   done
 done
