@@ -31,11 +31,12 @@
 // mbarriers: kv_full/kv_empty (ring), s_full/s_free, p_full, o_full,
 // q_full/q_empty; phases follow a chunk counter all roles advance alike.
 //
-// Build switches (-D...), all measured against this default and recorded in
-// LSRM_SPLIT=2, LSRM_HOLD4, LSRM_DBUF (+ LSRM_DBUF_NK),
-// LSRM_SKIP_DEAD_MAX, LSRM_GROUP_SKIP, LSRM_EPI_SPLIT, LSRM_ONEPASS,
-// LSRM_PINGPONG, LSRM_POLY_PER16, LSRM_HEADPAIR, LSRM_STAGES; LSRM_TRACE for
-// tools/attn_trace.py.
+// Build switches (-D...): LSRM_POLY_PER16 (exponentials on the FMA pipe),
+// LSRM_STAGES, LSRM_NK / LSRM_NP, LSRM_HEADPAIR; LSRM_TRACE for
+// tools/attn_trace.py.  The variants measured slower over the two rounds
+// (split rows, double-buffered S, held S pieces, ping-pong, per-group skips,
+// split epilogue, one-pass streaming, early S release, FMA sigmoid, ...) are
+// recorded in DESIGN.md §4 with their numbers and removed from the code.
 //
 // SMEM operand layout: 8x8 "core matrices" of 128 contiguous bytes,
 // SWIZZLE_NONE canonical layouts (cute mma_sm100_desc.hpp):
@@ -52,14 +53,6 @@ namespace lsrm {
 namespace tc {
 
 constexpr int kM = 128;          // MMA rows per head-tile
-#ifndef LSRM_DBUF
-#define LSRM_DBUF 0
-#endif
-#ifndef LSRM_DBUF_NK
-#define LSRM_DBUF_NK 96
-#endif
-// keys per chunk; double-buffered S (LSRM_DBUF) uses 96 so that two S
-// buffers (P inside) + [O | rowsum] + merge fit 256 TMEM columns per pipeline
 // LSRM_NK: keys per chunk of the default layout (128).  LSRM_NK = 64 with
 // LSRM_NP = 2 measured 1.13 -> 1.35 ms (chunk overhead); three pipelines
 // (which 64-key chunks would let TMEM hold: 3 x 160 columns) do not launch:
@@ -71,7 +64,7 @@ constexpr int kM = 128;          // MMA rows per head-tile
 #define LSRM_NP 2
 #endif
 static_assert(LSRM_NP == 1 || LSRM_NP == 2, "LSRM_NP: 1 or 2 pipelines per CTA");
-constexpr int kNK = LSRM_DBUF ? LSRM_DBUF_NK : LSRM_NK;
+constexpr int kNK = LSRM_NK;
 constexpr int kGroups = kNK / 16;
 constexpr int kMaxEnt = 256;     // tile tokens * selected rows
 
@@ -138,60 +131,12 @@ struct Launch {
   int* counter;
 };
 
-// Build-time variants (kept switchable so they can be measured against each
-// other on the GPU): ring depth, one-pass streaming softmax, and strict
-// alternation of the two head-tiles' exponential bursts (ping-pong).
+// Build-time variants (measured against each other on the GPU; the variants
+// that lost were removed and are listed in DESIGN.md §4): the K/V ring depth.
 #ifndef LSRM_STAGES
 #define LSRM_STAGES 3
 #endif
-#ifndef LSRM_ONEPASS
-#define LSRM_ONEPASS 0
-#endif
-#ifndef LSRM_PINGPONG
-#define LSRM_PINGPONG 0
-#endif
 constexpr int kStages = LSRM_STAGES;   // K/V ring depth (each stage holds every head of the item)
-#ifndef LSRM_SPLIT
-#define LSRM_SPLIT 1
-#endif
-#ifndef LSRM_SPLIT_RELOAD
-#define LSRM_SPLIT_RELOAD 1
-#endif
-#ifndef LSRM_SKIP_DEAD_MAX
-#define LSRM_SKIP_DEAD_MAX 0
-#endif
-#ifndef LSRM_GROUP_SKIP
-#define LSRM_GROUP_SKIP 0
-#endif
-#ifndef LSRM_HOLD4
-#define LSRM_HOLD4 0
-#endif
-#ifndef LSRM_EPI_SPLIT
-#define LSRM_EPI_SPLIT 0
-#endif
-// branch epilogue: only the O read precedes the P(c) hand-over
-constexpr bool kEpiSplit = LSRM_EPI_SPLIT;
-// Double-buffered S (one pipeline per CTA): QK(c+2) is issued right after
-// PV(c) into the buffer chunk c used, so S(c+1) is ready before the softmax
-// finishes chunk c.  P(c) is written into the consumed half of S(c)'s buffer
-// (columns [kNK/2, kNK)), so a pipeline needs 2*kNK + VW + DH/2 columns.
-constexpr bool kDbuf = LSRM_DBUF;
-static_assert(!kDbuf || (LSRM_SPLIT == 1 && !LSRM_ONEPASS && !LSRM_PINGPONG),
-              "double-buffered S is two-pass, unsplit only");
-// skip exponentials per 16-key group no row of the warp sees (instead of per
-// 32-key piece)
-constexpr bool kGroupSkip = LSRM_GROUP_SKIP;
-constexpr bool kOnePass = LSRM_ONEPASS;
-constexpr bool kPingPong = LSRM_PINGPONG;
-// kSplit softmax warps per TMEM lane quadrant: warp `half` of a pair owns
-// key columns [64*half, 64*half+64) of every chunk and output columns
-// [DH/2*half, ...) of the epilogue; the pair exchanges row maxima through
-// shared memory.  Doubles the softmax warps per SMSP without more TMEM.
-constexpr int kSplit = LSRM_SPLIT;
-static_assert(kSplit == 1 || kSplit == 2, "LSRM_SPLIT must be 1 or 2");
-
-static_assert(kSplit == 1 || (!LSRM_ONEPASS && !LSRM_PINGPONG),
-              "the split softmax is two-pass only");
 // gate biases staged in shared memory as [n_gates * hq][DH + 1] (padded rows:
 // the 16 heads of a warp hit 16 banks) when they fit, else read from global
 constexpr int kBiasMax = LSRM_STAGES <= 3 ? 3328 : 4;
@@ -199,11 +144,6 @@ constexpr int kOnesCols = 16;    // extra V columns holding 1 (valid key) / 0 (p
 constexpr int kBitmapWords = 512;  // union bitmap: up to 16384 occupied KV blocks
 
 
-// in-place mask of 16 logits (keys j >= lim get -inf) and their maximum
-__device__ __forceinline__ void mask16(uint32_t* s, int lim) {
-#pragma unroll
-  for (int j = 0; j < 16; ++j) s[j] = j < lim ? s[j] : 0xff800000u;
-}
 __device__ __forceinline__ float max16(const uint32_t* s) {
   const float* x = reinterpret_cast<const float*>(s);
   float a = fmaxf(fmaxf(x[0], x[1]), x[2]), b = fmaxf(fmaxf(x[3], x[4]), x[5]);
@@ -249,28 +189,11 @@ constexpr int kPolyPer16 = LSRM_POLY_PER16;
 __device__ __forceinline__ float ex2_mixed(float x, int j) {
   return j >= 16 - kPolyPer16 ? ex2_poly(x) : ex2(x);
 }
-// Gate sigmoid of the branch epilogue.  Default: 0.5 + 0.5 tanh(z / 2), one
-// MUFU op.  LSRM_FMA_SIGMOID: FMA pipe only (the exp phase next door is
-// MUFU-bound): 1 / (1 + 2^(-z log2 e)) with ex2_poly and a Newton reciprocal
-// from a bit-trick seed (3 steps, rel. error < 1e-6 on the clamped range).
-// Measured same-box (tools/ab_bench.sh): attention 1.133 -> 1.337 ms; the
-// epilogue sits on the softmax warps' critical path and the long FMA chain
-// costs far more latency than the MUFU op it saves.  Off.
-#ifndef LSRM_FMA_SIGMOID
-#define LSRM_FMA_SIGMOID 0
-#endif
+// Gate sigmoid of the branch epilogue: 0.5 + 0.5 tanh(z / 2), one MUFU op
+// (an FMA-pipe version measured slower: the epilogue is on the softmax
+// warps' critical path).
 __device__ __forceinline__ float sigmoid_gate(float z) {
-#if LSRM_FMA_SIGMOID
-  const float zc = fminf(fmaxf(z, -30.f), 30.f);
-  const float d = 1.f + ex2_poly(-1.4426950408889634f * zc);   // in [1, 2^44]
-  float r = __int_as_float(0x7EF311C7 - __float_as_int(d));     // ~1/d seed
-  r = r * fmaf(-d, r, 2.f);
-  r = r * fmaf(-d, r, 2.f);
-  r = r * fmaf(-d, r, 2.f);
-  return r;
-#else
   return fmaf(0.5f, tanh_approx(0.5f * z), 0.5f);
-#endif
 }
 
 // 16 logits -> 8 words of packed bf16 exp2(s * sl2 + nb)
@@ -279,26 +202,6 @@ __device__ __forceinline__ void exp16(const uint32_t* s, float sl2, float nb, ui
   for (int j = 0; j < 8; ++j)
     w[j] = pack_bf16(ex2_mixed(fmaf(__uint_as_float(s[2 * j]), sl2, nb), 2 * j),
                      ex2_mixed(fmaf(__uint_as_float(s[2 * j + 1]), sl2, nb), 2 * j + 1));
-}
-// LSRM_EARLY_SFREE: pieces 0,1 packed to f16 (x - running max) after their
-// max so S(c) is released before the exp pass.  Correct, but same-box A/B
-// 1.133 -> 1.275 ms (168 registers with spills, and the f16 pack / unpack /
-// add per element in the MUFU-bound exp phase).  Off.
-#ifndef LSRM_EARLY_SFREE
-#define LSRM_EARLY_SFREE 0
-#endif
-__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
-  const __half2 h = __floats2half2_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
-// 16 f16 logits (8 words, already relative to a reference) -> 8 words of
-// packed bf16 exp2(x + nb)
-__device__ __forceinline__ void exp16_f16(const uint32_t* h, float nb, uint32_t* w) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h[j]));
-    w[j] = pack_bf16(ex2(f.x + nb), ex2(f.y + nb));
-  }
 }
 __device__ __forceinline__ void zero8(uint32_t* w) {
 #pragma unroll
@@ -324,10 +227,8 @@ constexpr int kFFirstBranch = 1, kFLastBranch = 2, kFFirstItem = 4, kFLastItem =
 template <int DH>
 struct HeadCols {
   static constexpr int VW = DH + kOnesCols;
-  // kDbuf: S buffers at 0 and kNK, P at +kNK/2 inside the chunk's S buffer
-  static constexpr uint32_t kS = 0, kP = kDbuf ? kNK / 2 : kNK,
-                            kO = kDbuf ? 2 * kNK : kNK + kNK / 2, kMerged = kO + VW;
-  static constexpr int kTotal = (kDbuf ? 2 * kNK : kNK + kNK / 2) + VW + DH / 2;
+  static constexpr uint32_t kS = 0, kP = kNK, kO = kNK + kNK / 2, kMerged = kO + VW;
+  static constexpr int kTotal = kNK + kNK / 2 + VW + DH / 2;
 };
 template <int DH, int HP, int NP>
 constexpr int tmem_alloc_cols() {
@@ -357,7 +258,6 @@ struct alignas(128) Pipe {   // 128-byte aligned: q is a TMA destination
   int32_t wseg_plen[32], wseg_occ[32], wseg_cum[32];
   uint32_t wseg_mask[32];
   ChunkDesc desc[kStages];
-  float xmax[kSplit > 1 ? 2 : 1][HP][kSplit][kM];   // split: partial row maxima, by chunk parity
   uint64_t kv_full[kStages], kv_empty[kStages], s_full[2 * HP], s_free[HP], p_full[2 * HP],
       o_full[HP],
       q_full[2], q_empty[2];
@@ -372,7 +272,7 @@ struct Smem {
 
 // per pipeline: 4 softmax warps per head-tile, 1 producer, 1 MMA warp per head-tile
 template <int HP, int NP>
-constexpr int threads_of() { return 32 * NP * (4 * kSplit * HP + HP + 1); }
+constexpr int threads_of() { return 32 * NP * (4 * HP + HP + 1); }
 
 // Work item = (query tile, group of HP kv heads).  The HP head-tiles share the
 // chunk plan (same tokens, same union of selected blocks) but not K/V, so
@@ -395,7 +295,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
   Smem<DH, HP, NP>& SM = *reinterpret_cast<Smem<DH, HP, NP>*>(smem_raw);
   using HCols = HeadCols<DH>;
   constexpr int VW = HCols::VW, HC = HCols::kTotal;
-  constexpr int kSoftPerPipe = 4 * HP * kSplit;
+  constexpr int kSoftPerPipe = 4 * HP;
   constexpr int kSoftWarps = kSoftPerPipe * NP, kProducerWarp = kSoftWarps;
   constexpr int kAlloc = tmem_alloc_cols<DH, HP, NP>();
   static_assert(kAlloc <= 512, "TMEM budget");
@@ -429,9 +329,9 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     for (int hh = 0; hh < HP; ++hh) {
       for (int b = 0; b < 2; ++b) {
         mbar_init(&S.s_full[2 * hh + b], 1);
-        mbar_init(&S.p_full[2 * hh + b], 128 * kSplit);
+        mbar_init(&S.p_full[2 * hh + b], 128);
       }
-      mbar_init(&S.s_free[hh], 128 * kSplit);
+      mbar_init(&S.s_free[hh], 128);
       mbar_init(&S.o_full[hh], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -784,11 +684,6 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     const uint32_t id_pv = idesc_bf16(kM, VW, 1);   // [O | rowsum] += P . [V | ones]
     const uint32_t t_s = tmem + hh * HC + HCols::kS, t_p = tmem + hh * HC + HCols::kP,
                    t_o = tmem + hh * HC + HCols::kO;
-    // S / P of chunk cc (kDbuf: the chunk's buffer) and its barriers
-    auto sbuf = [&](uint32_t cc) { return kDbuf ? (cc & 1u) * (uint32_t)kNK : 0u; };
-    auto sfull = [&](uint32_t cc) { return &S.s_full[kDbuf ? 2 * hh + (cc & 1) : 2 * hh]; };
-    auto pfull = [&](uint32_t cc) { return &S.p_full[kDbuf ? 2 * hh + (cc & 1) : 2 * hh]; };
-    auto bpar = [&](uint32_t cc) { return kDbuf ? (cc >> 1) & 1u : cc & 1u; };
     // S = Q K^T for chunk cc into this head-tile's S columns
     auto issue_qk = [&](uint32_t cc) {
       const int st = cc % kStages;
@@ -805,20 +700,13 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       if (elect_one_sync()) {
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(t_s + sbuf(cc), a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16), id,
-                   kk > 0);
-        mma_commit(sfull(cc));
+          mma_bf16(t_s, a0 + (uint64_t)(kk * 16), b0 + (uint64_t)(kk * 16), id, kk > 0);
+        mma_commit(&S.s_full[2 * hh]);
       }
       __syncwarp();
       if (lane == 0 && hh == 0) trace(trp, cc, 2);
     };
     issue_qk(0);
-    // kDbuf: QK(1) now; afterwards QK(c+2) right after PV(c)
-    bool next_last = (S.desc[0].flags & kFLastOverall) != 0;   // is chunk c+1 past the end?
-    if (kDbuf && !next_last) {
-      issue_qk(1);
-      next_last = (S.desc[1 % kStages].flags & kFLastOverall) != 0;
-    }
     // per chunk: S(c+1) = Q K^T as soon as the softmax has S(c) in registers
     // (s_free), then PV(c) accumulates P(c).[V|ones] into the branch's O as
     // soon as P(c) is written (p_full)
@@ -831,11 +719,11 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const uint32_t acc0 = (fl & kFFirstBranch) ? 0u : 1u;
       const int nk = D.ncols / 16;
       const int qb = D.qb;
-      if (!kDbuf && !last) {
+      if (!last) {
         mbar_wait(&S.s_free[hh], c & 1);
         issue_qk(c + 1);
       }
-      mbar_wait(pfull(c), bpar(c));
+      mbar_wait(&S.p_full[2 * hh], c & 1);
       if (lane == 0 && hh == 0) trace(trp, c, 5);
       tc_after_sync();
       const uint64_t vdesc = sdesc(smem_u32(S.v[st][hh]), 16 * VW, 128);
@@ -843,7 +731,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
 #pragma unroll
         for (int kk = 0; kk < kGroups; ++kk)
           if (kk < nk)
-            mma_bf16_ts(t_o, t_p + sbuf(c) + kk * 8, vdesc + (uint64_t)(kk * 2 * VW), id_pv,
+            mma_bf16_ts(t_o, t_p + kk * 8, vdesc + (uint64_t)(kk * 2 * VW), id_pv,
                         kk > 0 ? 1u : acc0);
         mma_commit(&S.o_full[hh]);
         if (last_in_item) mma_commit(&S.q_empty[qb]);
@@ -851,26 +739,13 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       }
       __syncwarp();
       if (lane == 0 && hh == 0) trace(trp, c, 6);
-      if (kDbuf && !last && !next_last) {
-        // chunk c+2 exists: its S goes into the buffer PV(c) just read (in
-        // issue order, so after PV(c)); the softmax released S(c) before P(c)
-        issue_qk(c + 2);
-        next_last = (S.desc[(c + 2) % kStages].flags & kFLastOverall) != 0;
-      } else if (kDbuf) {
-        next_last = true;
-      }
       ++c;
       if (last) break;
     }
     __syncwarp();
   } else {
     // ===================== softmax / epilogue (warpgroup hh = head-tile hh)
-    const int wi = warp % kSoftPerPipe;
-    const int hh = wi / (4 * kSplit), half = (wi >> 2) % kSplit, q4 = warp & 3;
-    // epilogue / rescale columns of this warp, and the pair's named barrier
-    constexpr int kOCols = DH / kSplit;
-    const int oc0 = half * kOCols;
-    const int pair_bar = 1 + (pipe_id * HP + hh) * 4 + q4;
+    const int hh = (warp % kSoftPerPipe) / 4, q4 = warp & 3;
     const int m = q4 * 32 + lane;
     const int t = m / G, g_in = m % G;
     const uint32_t tS = tmem + ((uint32_t)(q4 * 32) << 16) + hh * HC;
@@ -894,61 +769,42 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     int64_t tok_pend = 0;
     __nv_bfloat16* const gate_s = &S.gate[hh][m * DH];   // this row's staged gate logits
     uint32_t c = 0;
-    // ping-pong: the HP=2 warpgroups take turns on the exponential phase
-    // (named barriers 1, 2), so one's MUFU stream covers the other's loads,
-    // maxima and epilogue; warpgroup 1 lets warpgroup 0 go first
-    const int bar_mine = 1 + hh, bar_other = 2 - hh;
-    if (kPingPong && NP == 1 && HP == 2 && hh == 1) named_arrive(bar_other, 256);
-#ifdef LSRM_WG1_DELAY_NS
-    if (HP == 2 && hh == 1) __nanosleep(LSRM_WG1_DELAY_NS);   // start out of phase
-#endif
-    // one turn per 32-key piece: wait for ours, run the piece's exponentials,
-    // hand over (the very last hand-over of warpgroup 1 has no taker)
-    auto pp_turn = [&]() {
-      if (kPingPong && NP == 1 && HP == 2) named_sync(bar_mine, 256);
-    };
-    auto pp_pass = [&](bool last_piece) {
-      if (kPingPong && NP == 1 && HP == 2 && !(hh == 1 && last_piece)) named_arrive(bar_other, 256);
-    };
 
     // gate + merge of a finished branch (nsa_attention.py:266-284); the
-    // running merge is f16 in TMEM; at an item end the merged row is stored
-    // The epilogue in two halves: epi_load reads the branch's O (this warp's
-    // columns) and row sum into registers - the part that must precede PV(c),
-    // which overwrites O; epi_finish does the gate, the merge and the stores.
+    // running merge is f16 in TMEM; at an item end the merged row is stored.
+    // epi_load reads the branch's O and row sum (this must precede PV(c),
+    // which overwrites O); epi_finish does the gate, the merge and the stores.
     auto epi_load = [&](uint32_t pc, uint32_t* eo) {
       mbar_wait(&S.o_full[hh], pc & 1);   // PV(pc) complete
       if (tid == 0) trace(trp, pc, 7);
       tc_after_sync();
-      tmem_ld_cols<1>(tO + DH, eo + kOCols);
+      tmem_ld_cols<1>(tO + DH, eo + DH);
 #pragma unroll
-      for (int cq = 0; cq < kOCols; cq += 16) tmem_ld16_nowait(tO + oc0 + cq, eo + cq);
+      for (int cq = 0; cq < DH; cq += 16) tmem_ld16_nowait(tO + cq, eo + cq);
       tmem_wait_ld();
     };
     auto epi_finish = [&](const uint32_t* eo) {
       cp_async_wait_all();                // gate logits staged by this thread
-      const float inv = rowok_pend ? 1.f / __uint_as_float(eo[kOCols]) : 0.f;
+      const float inv = rowok_pend ? 1.f / __uint_as_float(eo[DH]) : 0.f;
       const float* bp =
           bias_all ? bias_all + ((int64_t)br_pend * P.hq + head_pend) * bias_ld : nullptr;
       const Params& PB = L.use[use_pend];
       if (PB.o_br && rowok_pend) {   // training forward: the branch's own output and lse
         const int64_t brow = (int64_t)br_pend * PB.nq + tok_pend;
-        float4* ob = reinterpret_cast<float4*>(PB.o_br + brow * d_model + head_pend * DH + oc0);
+        float4* ob = reinterpret_cast<float4*>(PB.o_br + brow * d_model + head_pend * DH);
 #pragma unroll
-        for (int j = 0; j < kOCols / 4; ++j)
+        for (int j = 0; j < DH / 4; ++j)
           ob[j] = make_float4(__uint_as_float(eo[4 * j]) * inv, __uint_as_float(eo[4 * j + 1]) * inv,
                               __uint_as_float(eo[4 * j + 2]) * inv,
                               __uint_as_float(eo[4 * j + 3]) * inv);
-        if (half == 0)
-          PB.lse_br[brow * P.hq + head_pend] =
-              (m_pend + __log2f(__uint_as_float(eo[kOCols]))) * 0.6931471805599453f;
+        PB.lse_br[brow * P.hq + head_pend] =
+            (m_pend + __log2f(__uint_as_float(eo[DH]))) * 0.6931471805599453f;
       }
 #pragma unroll
-      for (int cq = 0; cq < kOCols; cq += 16) {   // 16 columns at a time (registers)
-        const int c0 = oc0 + cq;
+      for (int c0 = 0; c0 < DH; c0 += 16) {   // 16 columns at a time (registers)
         uint32_t r[16], mr[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) r[j] = eo[cq + j];
+        for (int j = 0; j < 16; ++j) r[j] = eo[c0 + j];
         if (!firstbr_pend) {
           tmem_ld_cols<8>(tM + c0 / 2, mr);
           tmem_wait_ld();
@@ -961,10 +817,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           for (int j = 0; j < 8; ++j) {
             const int cj = 8 * k8 + j;
             const float z = __bfloat162float(hv[j]) + (bp ? bp[c0 + cj] : 0.f);
-            // sigmoid(z) = 0.5 + 0.5 tanh(z / 2): one MUFU op
-            float v = rowok_pend ? __uint_as_float(r[cj]) * inv *
-                                       sigmoid_gate(z)
-                                 : 0.f;
+            float v = rowok_pend ? __uint_as_float(r[cj]) * inv * sigmoid_gate(z) : 0.f;
             if (!firstbr_pend) {
               const __half2 hm = *reinterpret_cast<const __half2*>(&mr[cj / 2]);
               v += (cj & 1) ? __high2float(hm) : __low2float(hm);
@@ -1006,16 +859,13 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       if (!lastit_pend) tmem_wait_st();
     };
     auto epilogue = [&](uint32_t pc) {
-      uint32_t eo[kOCols + 1];
+      uint32_t eo[DH + 1];
       epi_load(pc, eo);
       epi_finish(eo);
     };
 
     for (;;) {
-      mbar_wait(&S.s_full[kDbuf ? 2 * hh + (c & 1) : 2 * hh], kDbuf ? (c >> 1) & 1 : c & 1);
-      // this chunk's S (and, kDbuf, P) columns
-      const uint32_t tSc = tS + (kDbuf ? (c & 1u) * (uint32_t)kNK : 0u);
-      const uint32_t tPc = kDbuf ? tSc + HCols::kP : tP;
+      mbar_wait(&S.s_full[2 * hh], c & 1);
       if (tid == 0) trace(trp, c, 3);
       tc_after_sync();
       // chunk plan (a few wide shared loads) and S pieces 0,1 in flight together
@@ -1025,9 +875,8 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const uint32_t visb = D.tokvis[t];
       const int ncols = hdr0.x;
       uint32_t sa[32], sb[32];
-      const int pcb = 2 * half;   // first 32-key piece of this warp (split: 0 or 2)
-      if (kSplit == 1 || ncols > 32 * pcb) tmem_ld32(tSc + HCols::kS + 32 * pcb, sa);
-      if (ncols > 32 * (pcb + 1)) tmem_ld32(tSc + HCols::kS + 32 * (pcb + 1), sb);
+      tmem_ld32(tS + HCols::kS, sa);
+      if (ncols > 32) tmem_ld32(tS + HCols::kS + 32, sb);
 #ifdef LSRM_TRACE_LD
       tmem_wait_ld();
       if (tid == 0) trace(trp, c, 1);
@@ -1046,438 +895,119 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
       const uint32_t live = __reduce_or_sync(0xffffffffu, visb);
       if (first_br) m_run = kNegInf;
       float mx = kNegInf;
-      const int n_pc = (ncols + 31) / 32;   // 32-key pieces (ping-pong turns) of this chunk
-      int pdone = 0;
       tmem_wait_ld();
       if (tid == 0) trace(trp, c, 8);
-      // Exponentials against the running max need it defined for every row
-      // that sees this chunk: the first chunk of a branch takes two passes
-      // (max, then exponentials); later chunks stream once.
-      const bool two_pass =
-          !kOnePass || __any_sync(0xffffffffu, m_run == kNegInf && visb != 0u);
-      if constexpr (kSplit == 2) {
-        // ---- split softmax: this warp's two pieces stay in registers
-        const bool has0 = ncols > 32 * pcb, has1 = ncols > 32 * (pcb + 1);
+      // pass 1: straight-line group maxima; groups this row does not see are
+      // not selected
 #define LSRM_MAX(arr, off, gi)                                  \
   {                                                             \
     const float g_ = max16(arr + (off));                        \
     mx = ((visb >> (gi)) & 1u) ? fmaxf(mx, g_) : mx;            \
   }
-        if (has0) {
-          LSRM_MAX(sa, 0, 2 * pcb)
-          LSRM_MAX(sa, 16, 2 * pcb + 1)
-        }
-        if (has1) {
-          LSRM_MAX(sb, 0, 2 * pcb + 2)
-          LSRM_MAX(sb, 16, 2 * pcb + 3)
-        }
-#undef LSRM_MAX
-#if LSRM_SPLIT_RELOAD
-        // pass 2 reloads S piece by piece (fewer live registers)
-#else
-        tc_before_sync();
-        mbar_arrive(&S.s_free[hh]);   // S(c) in registers: QK(c+1) may overwrite it
-#endif
-        // row max across the pair (double-buffered by chunk parity)
-        S.xmax[c & 1][hh][half][m] = mx;
-        named_sync(pair_bar, 64);
-        mx = fmaxf(mx, S.xmax[c & 1][hh][half ^ 1][m]);
-        if (tid == 0) trace(trp, c, 10);
-        const float m_cand = fmaxf(m_run, mx * sl2);
-        float m_use = m_run, scale = 1.f;
-        bool need = false;
-        if (m_run == kNegInf) {
-          m_use = m_cand;
-        } else if (m_cand > m_run + kHeadroom) {
-          m_use = m_cand;
-          scale = ex2(m_run - m_cand);
-          need = true;
-        }
-        bool pv_done = c == 0;
-        auto wait_pv = [&]() {
-          if (!pv_done) {
-            mbar_wait(&S.o_full[hh], (c - 1) & 1);
-            tc_after_sync();
-            pv_done = true;
-          }
-        };
-        if (__any_sync(0xffffffffu, need)) {   // the pair decides identically
-          wait_pv();
-#pragma unroll
-          for (int cq = 0; cq < kOCols; cq += 16) {
-            uint32_t r[16];
-            tmem_ld16_nowait(tO + oc0 + cq, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
-            tmem_st16(tO + oc0 + cq, r);
-          }
-          if (half == 0) {
-            uint32_t rl[1];
-            tmem_ld_cols<1>(tO + DH, rl);
-            tmem_wait_ld();
-            rl[0] = __float_as_uint(__uint_as_float(rl[0]) * scale);
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tO + DH),
-                         "r"(rl[0])
-                         : "memory");
-          }
-        }
-        m_run = m_use;
-        if (tid == 0) trace(trp, c, 11);
-        const float nbv = m_use == kNegInf ? 0.f : -m_use;
-#define LSRM_SPLIT_PIECE(arr, pc)                                              \
-  {                                                                            \
-    uint32_t w[16];                                                            \
-    if ((live >> (2 * (pc))) & 3u) {                                           \
-      exp16(arr, sl2, ((visb >> (2 * (pc))) & 1u) ? nbv : kNegInf, w);         \
-      exp16(arr + 16, sl2, ((visb >> (2 * (pc) + 1)) & 1u) ? nbv : kNegInf, w + 8); \
-    } else {                                                                   \
-      zero8(w);                                                                \
-      zero8(w + 8);                                                            \
-    }                                                                          \
-    wait_pv();                                                                 \
-    tmem_st16(tPc + 16 * (pc), w);                                              \
-  }
-#if LSRM_SPLIT_RELOAD
-        if (has0) {
-          tmem_ld32(tSc + HCols::kS + 32 * pcb, sa);
-          tmem_wait_ld();
-          if (!has1) {
-            tc_before_sync();
-            mbar_arrive(&S.s_free[hh]);
-          }
-          LSRM_SPLIT_PIECE(sa, pcb)
-        }
-        if (has1) {
-          tmem_ld32(tSc + HCols::kS + 32 * (pcb + 1), sa);
-          tmem_wait_ld();
-          tc_before_sync();
-          mbar_arrive(&S.s_free[hh]);
-          LSRM_SPLIT_PIECE(sa, pcb + 1)
-        }
-        if (!has0) {
-          tc_before_sync();
-          mbar_arrive(&S.s_free[hh]);
-        }
-#else
-        if (has0) LSRM_SPLIT_PIECE(sa, pcb)
-        if (has1) LSRM_SPLIT_PIECE(sb, pcb + 1)
-#endif
-#undef LSRM_SPLIT_PIECE
-        wait_pv();   // PV(c-1) read O before this chunk's epilogue may run
-      } else if (two_pass) {
-// straight-line group maxima; groups this row does not see are not selected
-#define LSRM_MAX(arr, off, gi)                                  \
-  {                                                             \
-    const float g_ = max16(arr + (off));                        \
-    mx = ((visb >> (gi)) & 1u) ? fmaxf(mx, g_) : mx;            \
-  }
-// pieces no row of the warp sees are skipped (warp-uniform `live` bits)
-#if LSRM_SKIP_DEAD_MAX
-#define LSRM_LIVE(pc) ((live >> (2 * (pc))) & 3u)
-#else
-#define LSRM_LIVE(pc) true
-#endif
-        if (LSRM_LIVE(0)) {
-          LSRM_MAX(sa, 0, 0)
-          LSRM_MAX(sa, 16, 1)
-        }
-        if (ncols > 32 && LSRM_LIVE(1)) {
-          LSRM_MAX(sb, 0, 2)
-          LSRM_MAX(sb, 16, 3)
-        }
-        const bool hi = ncols > 64;   // pieces 2,3 end up in registers
-        if (tid == 0) trace(trp, c, 9);
-#if LSRM_HOLD4
-        // all four pieces stay in registers: S(c) is released to QK(c+1)
-        // right after the max pass instead of after a reload mid-exp-phase
-        uint32_t sc[32], sd[32];
-        if (hi) {
-          tmem_ld32(tSc + HCols::kS + 64, sc);
-          if (ncols > 96) tmem_ld32(tSc + HCols::kS + 96, sd);
-          tmem_wait_ld();
-          tc_before_sync();
-          mbar_arrive(&S.s_free[hh]);
-          if (LSRM_LIVE(2)) {
-            LSRM_MAX(sc, 0, 4)
-            LSRM_MAX(sc, 16, 5)
-          }
-          if (ncols > 96 && LSRM_LIVE(3)) {
-            LSRM_MAX(sd, 0, 6)
-            LSRM_MAX(sd, 16, 7)
-          }
-        } else {
-#else
-#if LSRM_EARLY_SFREE
-        // pieces 0,1 kept as f16 (x - ref) so S(c) can be released as soon as
-        // pieces 2,3 are loaded; ref = the running max (the chunk's max of
-        // pieces 0,1 for a branch's first chunk): the values that matter are
-        // near 0, where f16 keeps 11 bits
-        uint32_t h01[32];
-        float ref = 0.f;
-        if (hi) {
-          ref = m_run != kNegInf ? m_run : (mx == kNegInf ? 0.f : mx * sl2);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            h01[j] = pack_f16(fmaf(__uint_as_float(sa[2 * j]), sl2, -ref),
-                              fmaf(__uint_as_float(sa[2 * j + 1]), sl2, -ref));
-            h01[16 + j] = pack_f16(fmaf(__uint_as_float(sb[2 * j]), sl2, -ref),
-                                   fmaf(__uint_as_float(sb[2 * j + 1]), sl2, -ref));
-          }
-        }
-#endif
-        if (hi) {
-          tmem_ld32(tSc + HCols::kS + 64, sa);
-          if (ncols > 96) tmem_ld32(tSc + HCols::kS + 96, sb);
-          tmem_wait_ld();
-#if LSRM_EARLY_SFREE
-          tc_before_sync();
-          mbar_arrive(&S.s_free[hh]);   // S(c) in registers (0,1 as f16): QK(c+1) may go
-#endif
-          if (LSRM_LIVE(2)) {
-            LSRM_MAX(sa, 0, 4)
-            LSRM_MAX(sa, 16, 5)
-          }
-          if (ncols > 96 && LSRM_LIVE(3)) {
-            LSRM_MAX(sb, 0, 6)
-            LSRM_MAX(sb, 16, 7)
-          }
-        } else {
-#endif
-          tc_before_sync();
-          mbar_arrive(&S.s_free[hh]);   // S(c) fully in registers: QK(c+1) may overwrite it
-        }
-#undef LSRM_MAX
-        if (tid == 0) trace(trp, c, 10);
-        // running max with headroom; rescale O (and its row sum) if it moves
-        const float m_cand = fmaxf(m_run, mx * sl2);
-        float m_use = m_run, scale = 1.f;
-        bool need = false;
-        if (m_run == kNegInf) {
-          m_use = m_cand;
-        } else if (m_cand > m_run + kHeadroom) {
-          m_use = m_cand;
-          scale = ex2(m_run - m_cand);
-          need = true;
-        }
-        // PV(c-1) must be complete before P(c) overwrites P(c-1) and before O is
-        // rescaled or read: waited for lazily, right before the first of those
-        bool pv_done = c == 0;
-        auto wait_pv = [&]() {
-          if (!pv_done) {
-            mbar_wait(&S.o_full[hh], (c - 1) & 1);
-            tc_after_sync();
-            pv_done = true;
-          }
-        };
-        if (__any_sync(0xffffffffu, need)) {
-          wait_pv();
-#pragma unroll
-          for (int c0 = 0; c0 < DH; c0 += 16) {
-            uint32_t r[16];
-            tmem_ld16_nowait(tO + c0, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
-            tmem_st16(tO + c0, r);
-          }
-          uint32_t rl[1];
-          tmem_ld_cols<1>(tO + DH, rl);
-          tmem_wait_ld();
-          rl[0] = __float_as_uint(__uint_as_float(rl[0]) * scale);
-          asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tO + DH),
-                       "r"(rl[0])
-                       : "memory");
-        }
-        m_run = m_use;
-        if (tid == 0) trace(trp, c, 11);
-        // pass 2: P = exp2(S * scale - m) as packed bf16; rows that do not see a
-        // group get a -inf bias (P = 0); fully masked rows so far use m = 0
-        const float nbv = m_use == kNegInf ? 0.f : -m_use;
-#define LSRM_EXP_PIECE(arr, pc)                                                \
-  {                                                                            \
-    uint32_t w[16];                                                            \
-    const bool lp_ = last_all && ++pdone == n_pc;                              \
-    pp_turn();                                                                 \
-    if (kGroupSkip) {   /* warp-uniform skip per 16-key group */             \
-      if ((live >> (2 * (pc))) & 1u)                                           \
-        exp16(arr, sl2, ((visb >> (2 * (pc))) & 1u) ? nbv : kNegInf, w);       \
-      else                                                                     \
-        zero8(w);                                                              \
-      if ((live >> (2 * (pc) + 1)) & 1u)                                       \
-        exp16(arr + 16, sl2, ((visb >> (2 * (pc) + 1)) & 1u) ? nbv : kNegInf, w + 8); \
-      else                                                                     \
-        zero8(w + 8);                                                          \
-    } else if ((live >> (2 * (pc))) & 3u) {                                    \
-      exp16(arr, sl2, ((visb >> (2 * (pc))) & 1u) ? nbv : kNegInf, w);         \
-      exp16(arr + 16, sl2, ((visb >> (2 * (pc) + 1)) & 1u) ? nbv : kNegInf, w + 8); \
-    } else {                                                                   \
-      zero8(w);                                                                \
-      zero8(w + 8);                                                            \
-    }                                                                          \
-    pp_pass(lp_);                                                              \
-    wait_pv();                                                                 \
-    tmem_st16(tPc + 16 * (pc), w);                                              \
-  }
-#if LSRM_HOLD4
-        if (hi) {
-          LSRM_EXP_PIECE(sc, 2)
-          if (ncols > 96) LSRM_EXP_PIECE(sd, 3)
-        }
-#elif LSRM_EARLY_SFREE
-        if (hi) {
-          LSRM_EXP_PIECE(sa, 2)
-          if (ncols > 96) LSRM_EXP_PIECE(sb, 3)
-          // pieces 0,1 from their f16 copies: exp2((x - ref) + (ref - m))
-          const float nbh = m_use == kNegInf ? 0.f : ref - m_use;
-#pragma unroll
-          for (int pc = 0; pc < 2; ++pc) {
-            uint32_t w[16];
-            if ((live >> (2 * pc)) & 3u) {
-              exp16_f16(h01 + 16 * pc, ((visb >> (2 * pc)) & 1u) ? nbh : kNegInf, w);
-              exp16_f16(h01 + 16 * pc + 8, ((visb >> (2 * pc + 1)) & 1u) ? nbh : kNegInf, w + 8);
-            } else {
-              zero8(w);
-              zero8(w + 8);
-            }
-            wait_pv();
-            tmem_st16(tPc + 16 * pc, w);
-          }
-          if (tid == 0) trace(trp, c, 12);
-        } else {
-          LSRM_EXP_PIECE(sa, 0)
-          if (ncols > 32) LSRM_EXP_PIECE(sb, 1)
-        }
-#else
-        if (hi) {
-          LSRM_EXP_PIECE(sa, 2)
-          if (ncols > 96) LSRM_EXP_PIECE(sb, 3)
-          tmem_ld32(tSc + HCols::kS, sa);   // pieces 0,1 again (both full: ncols > 64)
-          tmem_ld32(tSc + HCols::kS + 32, sb);
-          tmem_wait_ld();
-          tc_before_sync();
-          mbar_arrive(&S.s_free[hh]);
-          if (tid == 0) trace(trp, c, 12);
-        }
-#endif
-#if !LSRM_EARLY_SFREE
-        LSRM_EXP_PIECE(sa, 0)
-        if (ncols > 32) LSRM_EXP_PIECE(sb, 1)
-#endif
-#undef LSRM_EXP_PIECE
-      } else {
-        // ---- one pass: exponentials against m_run while the chunk max is
-        //      gathered; a rare fixup handles a max that leaves the headroom
-        if (c > 0) mbar_wait(&S.o_full[hh], (c - 1) & 1);   // PV(c-1) has read P(c-1)
-        tc_after_sync();
-        if (tid == 0) trace(trp, c, 11);
-        const float nbv = -m_run;
-// one 32-key piece, straight-line (no per-group branches, so the MUFU stream
-// of its 32 exponentials is scheduled back to back); groups the warp does not
-// see inside a live piece just get a -inf bias
-#define LSRM_STREAM_PIECE(arr, pc)                                            \
-  {                                                                           \
-    uint32_t w[16];                                                           \
-    if ((live >> (2 * (pc))) & 3u) {                                          \
-      const bool v0 = (visb >> (2 * (pc))) & 1u, v1 = (visb >> (2 * (pc) + 1)) & 1u; \
-      if (tid == 0) trace(trp, c, 16 + 4 * (pc));                             \
-      const float g0 = max16(arr), g1 = max16(arr + 16);                      \
-      mx = fmaxf(mx, fmaxf(v0 ? g0 : kNegInf, v1 ? g1 : kNegInf));            \
-      if (tid == 0) trace(trp, c, 17 + 4 * (pc));                             \
-      pp_turn();                                                              \
-      exp16(arr, sl2, v0 ? nbv : kNegInf, w);                                 \
-      exp16(arr + 16, sl2, v1 ? nbv : kNegInf, w + 8);                        \
-    } else {                                                                  \
-      pp_turn();                                                              \
-      zero8(w);                                                               \
-      zero8(w + 8);                                                           \
-    }                                                                         \
-    pp_pass(last_all && ++pdone == n_pc);                                     \
-    if (tid == 0) trace(trp, c, 18 + 4 * (pc));                               \
-    tmem_st16(tPc + 16 * (pc), w);                                             \
-    if (tid == 0) trace(trp, c, 19 + 4 * (pc));                               \
-  }
-        LSRM_STREAM_PIECE(sa, 0)
-        if (tid == 0) trace(trp, c, 9);
-        if (ncols > 64) tmem_ld32(tSc + HCols::kS + 64, sa);
-        if (ncols > 32) LSRM_STREAM_PIECE(sb, 1)
-        if (tid == 0) trace(trp, c, 10);
-        if (ncols > 96) tmem_ld32(tSc + HCols::kS + 96, sb);
-        if (ncols > 64) {
-          tmem_wait_ld();
-          if (tid == 0) trace(trp, c, 12);
-          LSRM_STREAM_PIECE(sa, 2)
-          if (ncols > 96) LSRM_STREAM_PIECE(sb, 3)
-        }
-#undef LSRM_STREAM_PIECE
-        const float m_cand = fmaxf(m_run, mx * sl2);
-        const bool need = m_cand > m_run + kHeadroom;
-        if (__any_sync(0xffffffffu, need)) {
-          // the chunk max left the headroom: rescale O, recompute P(c)
-          const float m_use = need ? m_cand : m_run;
-          const float scale = need ? ex2(m_run - m_cand) : 1.f;
-          tmem_wait_st();
-#pragma unroll
-          for (int c0 = 0; c0 < DH; c0 += 16) {
-            uint32_t r[16];
-            tmem_ld16_nowait(tO + c0, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
-            tmem_st16(tO + c0, r);
-          }
-          uint32_t rl[1];
-          tmem_ld_cols<1>(tO + DH, rl);
-          tmem_wait_ld();
-          rl[0] = __float_as_uint(__uint_as_float(rl[0]) * scale);
-          asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tO + DH),
-                       "r"(rl[0])
-                       : "memory");
-          const float nb2 = -m_use;
-#pragma unroll
-          for (int pc = 0; pc < kGroups / 2; ++pc) {
-            if (pc * 32 < ncols) {
-              tmem_ld32(tSc + HCols::kS + 32 * pc, sa);
-              tmem_wait_ld();
-              uint32_t w[16];
-#pragma unroll
-              for (int hf = 0; hf < 2; ++hf) {
-                const int gi = 2 * pc + hf;
-                if ((live >> gi) & 1u) {
-                  exp16(sa + 16 * hf, sl2, ((visb >> gi) & 1u) ? nb2 : kNegInf, w + 8 * hf);
-                } else {
-                  zero8(w + 8 * hf);
-                }
-              }
-              tmem_st16(tPc + 16 * pc, w);
-            }
-          }
-          m_run = m_use;
-        }
-        tc_before_sync();
-        mbar_arrive(&S.s_free[hh]);   // S(c) no longer read: QK(c+1) may overwrite it
+      LSRM_MAX(sa, 0, 0)
+      LSRM_MAX(sa, 16, 1)
+      if (ncols > 32) {
+        LSRM_MAX(sb, 0, 2)
+        LSRM_MAX(sb, 16, 3)
       }
+      const bool hi = ncols > 64;   // pieces 2,3 end up in registers
+      if (tid == 0) trace(trp, c, 9);
+      if (hi) {
+        tmem_ld32(tS + HCols::kS + 64, sa);
+        if (ncols > 96) tmem_ld32(tS + HCols::kS + 96, sb);
+        tmem_wait_ld();
+        LSRM_MAX(sa, 0, 4)
+        LSRM_MAX(sa, 16, 5)
+        if (ncols > 96) {
+          LSRM_MAX(sb, 0, 6)
+          LSRM_MAX(sb, 16, 7)
+        }
+      } else {
+        tc_before_sync();
+        mbar_arrive(&S.s_free[hh]);   // S(c) fully in registers: QK(c+1) may overwrite it
+      }
+#undef LSRM_MAX
+      if (tid == 0) trace(trp, c, 10);
+      // running max with headroom; rescale O (and its row sum) if it moves
+      const float m_cand = fmaxf(m_run, mx * sl2);
+      float m_use = m_run, scale = 1.f;
+      bool need = false;
+      if (m_run == kNegInf) {
+        m_use = m_cand;
+      } else if (m_cand > m_run + kHeadroom) {
+        m_use = m_cand;
+        scale = ex2(m_run - m_cand);
+        need = true;
+      }
+      // PV(c-1) must be complete before P(c) overwrites P(c-1) and before O is
+      // rescaled or read: waited for lazily, right before the first of those
+      bool pv_done = c == 0;
+      auto wait_pv = [&]() {
+        if (!pv_done) {
+          mbar_wait(&S.o_full[hh], (c - 1) & 1);
+          tc_after_sync();
+          pv_done = true;
+        }
+      };
+      if (__any_sync(0xffffffffu, need)) {
+        wait_pv();
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16_nowait(tO + c0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
+          tmem_st16(tO + c0, r);
+        }
+        uint32_t rl[1];
+        tmem_ld_cols<1>(tO + DH, rl);
+        tmem_wait_ld();
+        rl[0] = __float_as_uint(__uint_as_float(rl[0]) * scale);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tO + DH),
+                     "r"(rl[0])
+                     : "memory");
+      }
+      m_run = m_use;
+      if (tid == 0) trace(trp, c, 11);
+      // pass 2: P = exp2(S * scale - m) as packed bf16; rows that do not see a
+      // group get a -inf bias (P = 0); fully masked rows so far use m = 0;
+      // 32-key pieces no row of the warp sees are zero
+      const float nbv = m_use == kNegInf ? 0.f : -m_use;
+      auto exp_piece = [&](const uint32_t* arr, int pc) {
+        uint32_t w[16];
+        if ((live >> (2 * pc)) & 3u) {
+          exp16(arr, sl2, ((visb >> (2 * pc)) & 1u) ? nbv : kNegInf, w);
+          exp16(arr + 16, sl2, ((visb >> (2 * pc + 1)) & 1u) ? nbv : kNegInf, w + 8);
+        } else {
+          zero8(w);
+          zero8(w + 8);
+        }
+        wait_pv();
+        tmem_st16(tP + 16 * pc, w);
+      };
+      if (hi) {
+        exp_piece(sa, 2);
+        if (ncols > 96) exp_piece(sb, 3);
+        tmem_ld32(tS + HCols::kS, sa);   // pieces 0,1 again (both full: ncols > 64)
+        tmem_ld32(tS + HCols::kS + 32, sb);
+        tmem_wait_ld();
+        tc_before_sync();
+        mbar_arrive(&S.s_free[hh]);
+        if (tid == 0) trace(trp, c, 12);
+      }
+      exp_piece(sa, 0);
+      if (ncols > 32) exp_piece(sb, 1);
       if (tid == 0) trace(trp, c, 13);
       tmem_wait_st();
       if (tid == 0) trace(trp, c, 14);
-      if (epi_pend && kEpiSplit) {
-        // the previous branch's O into registers, release P(c) to PV(c), then
-        // gate / merge / store off the MMA's critical path
-        uint32_t eo[kOCols + 1];
-        epi_load(c - 1, eo);
-        tc_before_sync();
-        mbar_arrive(&S.p_full[kDbuf ? 2 * hh + (c & 1) : 2 * hh]);
-        epi_finish(eo);
+      if (epi_pend) {   // the previous branch's O must be read before PV(c) overwrites it
+        epilogue(c - 1);
         epi_pend = false;
-      } else {
-        if (epi_pend) {   // the previous branch's O must be read before PV(c) overwrites it
-          epilogue(c - 1);
-          epi_pend = false;
-        }
-        if (tid == 0) trace(trp, c, 15);
-        tc_before_sync();
-        mbar_arrive(&S.p_full[kDbuf ? 2 * hh + (c & 1) : 2 * hh]);
       }
+      if (tid == 0) trace(trp, c, 15);
+      tc_before_sync();
+      mbar_arrive(&S.p_full[2 * hh]);
       if (tid == 0) trace(trp, c, 4);
       if (last_br) {
         if (row_ok) {   // stage this branch's gate logits for its epilogue
@@ -1485,7 +1015,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
           const __nv_bfloat16* gp = PU.gl + tok * PU.ld_gl + PU.gcol0 + (int64_t)br * d_model +
                                     head * DH;
 #pragma unroll
-          for (int cq = 0; cq < kOCols; cq += 8) cp_async16(gate_s + oc0 + cq, gp + oc0 + cq, 16u);
+          for (int cq = 0; cq < DH; cq += 8) cp_async16(gate_s + cq, gp + cq, 16u);
         }
         br_pend = br;
         m_pend = m_run;
@@ -1645,9 +1175,7 @@ static int launch(const Launch& L, int dh, int hkv, int64_t n_tiles_static, void
     nsa_fused_kernel<D, HP, NP><<<grid, threads_of<HP, NP>(), smem, st>>>(L);               \
   } else
   LSRM_TC_CASE(32, 1, LSRM_NP)
-#if !LSRM_DBUF
   LSRM_TC_CASE(32, 2, 1)
-#endif
   LSRM_TC_CASE(32, 1, 1)
   LSRM_TC_CASE(64, 1, 1)
   return set_error(LSRM_E_CONFIG, "tcgen05 path: head_dim %d not in {32,64}", dh);
