@@ -2,21 +2,25 @@
 // and the fp32 gated merge (nsa_attention.py:266-284).
 //
 // This is the exact-precision path (BASELINE config C1 "fp32 fwd", and the
-// reference API's f32 contract): one thread per (query, q-head), keys walked
-// in block order with an fp32 online softmax (accurate expf), FFMA dot
-// products.  Keys/values are in the KV partition's block-major order so each
-// selected block is one contiguous row range.
+// reference API's f32 contract): S lanes per (query, q-head) (S a power of
+// two chosen so the launch fills the GPU), lane j walking every S-th key of
+// the query's key sequence in block order with an fp32 online softmax
+// (accurate expf) and FFMA dot products; the lanes' (max, sum, acc) states
+// are merged by a fixed xor-shuffle tree (deterministic).  Keys/values are in
+// the KV partition's block-major order so each selected block is one
+// contiguous row range.
 #include "common.cuh"
 
 namespace lsrm {
 
+// keys lo, lo+S, ... of [lo, hi) after the first `skip` (this lane's share)
 template <int DH>
 __device__ __forceinline__ void attend_range(const float* __restrict__ k,
                                              const float* __restrict__ v, int hkv,
                                              int kvh, int64_t lo, int64_t hi,
                                              const float (&q)[DH], float scale, float& m,
-                                             float& l, float (&acc)[DH]) {
-  for (int64_t j = lo; j < hi; ++j) {
+                                             float& l, float (&acc)[DH], int step = 1) {
+  for (int64_t j = lo; j < hi; j += step) {
     const float* kr = k + (j * hkv + kvh) * DH;
     const float* vr = v + (j * hkv + kvh) * DH;
     float s = 0.f;
@@ -47,38 +51,68 @@ __global__ void attention_f32_kernel(int mode, const float* __restrict__ q, int6
                                      const int32_t* __restrict__ own_row,
                                      const int64_t* __restrict__ ids,
                                      const int64_t* __restrict__ lengths, int64_t width,
-                                     float* __restrict__ out) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= nq * hq) return;
-  int64_t i = t / hq;
-  int h = (int)(t % hq);
-  int kvh = h / (hq / hkv);
+                                     float* __restrict__ out, int split) {
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = gt / split;            // (query, head) of this lane group
+  const int sl = (int)(gt % split);        // lane within the group (groups are aligned)
+  const bool valid = t < nq * hq;
+  const int64_t tt = valid ? t : 0;
+  const int64_t i = tt / hq;
+  const int h = (int)(tt % hq);
+  const int kvh = h / (hq / hkv);
   float qr[DH], acc[DH];
 #pragma unroll
-  for (int c = 0; c < DH; ++c) { qr[c] = q[t * DH + c]; acc[c] = 0.f; }
+  for (int c = 0; c < DH; ++c) { qr[c] = q[tt * DH + c]; acc[c] = 0.f; }
   const float scale = 1.0f / sqrtf((float)DH);
   float m = -__builtin_huge_valf(), l = 0.f;
-  if (mode == 0) {
-    attend_range<DH>(k, v, hkv, kvh, 0, nk, qr, scale, m, l, acc);
-  } else if (mode == 1) {
-    int c = count[i];
-    for (int s = 0; s < c; ++s) {
-      int r = rows[i * kmax + s];
-      attend_range<DH>(k, v, hkv, kvh, offs[r], offs[r + 1], qr, scale, m, l, acc);
-    }
-  } else if (mode == 2) {
-    int r = own_row[i];
-    attend_range<DH>(k, v, hkv, kvh, offs[r], offs[r + 1], qr, scale, m, l, acc);
-  } else {
-    int64_t len = lengths[i];
-    for (int64_t s = 0; s < len; ++s) {
-      int64_t j = ids[i * width + s];
-      attend_range<DH>(k, v, hkv, kvh, j, j + 1, qr, scale, m, l, acc);
+  // this lane takes the keys whose position in the query's key sequence is
+  // = sl (mod split); `seen` counts the keys of the ranges walked so far
+  int64_t seen = 0;
+  auto range = [&](int64_t lo, int64_t hi) {
+    const int64_t first = lo + ((sl - seen) % split + split) % split;
+    attend_range<DH>(k, v, hkv, kvh, first, hi, qr, scale, m, l, acc, split);
+    seen += hi - lo;
+  };
+  if (valid) {
+    if (mode == 0) {
+      range(0, nk);
+    } else if (mode == 1) {
+      const int c = count[i];
+      for (int s = 0; s < c; ++s) {
+        const int r = rows[i * kmax + s];
+        range(offs[r], offs[r + 1]);
+      }
+    } else if (mode == 2) {
+      const int r = own_row[i];
+      range(offs[r], offs[r + 1]);
+    } else {
+      const int64_t len = lengths[i];
+      for (int64_t s = 0; s < len; ++s) {
+        const int64_t j = ids[i * width + s];
+        range(j, j + 1);
+      }
     }
   }
-  float inv = 1.0f / l;
+  // merge the group's lane states (fixed xor tree: deterministic)
+  for (int o = 1; o < split; o <<= 1) {
+    const float mo = __shfl_xor_sync(0xffffffffu, m, o);
+    const float lo_ = __shfl_xor_sync(0xffffffffu, l, o);
+    const float mn = fmaxf(m, mo);
+    const float a = m == mn ? 1.f : expf(m - mn), b = mo == mn ? 1.f : expf(mo - mn);
+    l = l * a + lo_ * b;
 #pragma unroll
-  for (int c = 0; c < DH; ++c) out[t * DH + c] = acc[c] * inv;
+    for (int c = 0; c < DH; ++c) {
+      const float ao = __shfl_xor_sync(0xffffffffu, acc[c], o);
+      acc[c] = acc[c] * a + ao * b;
+    }
+    m = mn;
+  }
+  if (!valid) return;
+  const float inv = 1.0f / l;
+  // lane sl writes columns sl, sl + split, ... of the row
+#pragma unroll
+  for (int c = 0; c < DH; ++c)
+    if (c % split == sl) out[tt * DH + c] = acc[c] * inv;
 }
 
 __global__ void gated_merge_f32_kernel(const float* __restrict__ gl, int64_t ld,
@@ -228,14 +262,17 @@ int lsrm_attention_f32(int mode, const float* q, int64_t nq, int hq, int hkv, in
                "n_q_heads=%d not divisible by n_kv_heads=%d", hq, hkv);
   if (nq == 0) return LSRM_OK;
   if (nk == 0) return set_error(LSRM_E_EMPTY_CONTEXT, "attention over an empty key set");
-  unsigned blocks = (unsigned)ceil_div(nq * hq, 128);
+  // lanes per (query, head): fill ~148 SMs x 1024 threads, at most 16
+  int split = 1;
+  while (split < 16 && nq * hq * split * 2 <= 148LL * 1024) split *= 2;
+  unsigned blocks = (unsigned)ceil_div(nq * hq * split, 128);
   cudaStream_t st = as_stream(stream);
 #define LSRM_ATTN_CASE(D)                                                              \
   case D:                                                                              \
     attention_f32_kernel<D><<<blocks, 128, 0, st>>>(mode, q, nq, hq, hkv, k, v, nk,    \
                                                     block_offsets, rows, count,        \
                                                     kmax_rows, own_row, ids, lengths,  \
-                                                    width, out);                       \
+                                                    width, out, split);                \
     break;
   switch (dh) {
     LSRM_ATTN_CASE(4)
