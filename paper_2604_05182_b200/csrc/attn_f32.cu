@@ -262,9 +262,12 @@ int lsrm_attention_f32(int mode, const float* q, int64_t nq, int hq, int hkv, in
                "n_q_heads=%d not divisible by n_kv_heads=%d", hq, hkv);
   if (nq == 0) return LSRM_OK;
   if (nk == 0) return set_error(LSRM_E_EMPTY_CONTEXT, "attention over an empty key set");
-  // lanes per (query, head): fill ~148 SMs x 1024 threads, at most 16
+  // lanes per (query, head): fill ~148 SMs x LSRM_F32_FILL threads, at most 32
+#ifndef LSRM_F32_FILL
+#define LSRM_F32_FILL 1024
+#endif
   int split = 1;
-  while (split < 16 && nq * hq * split * 2 <= 148LL * 1024) split *= 2;
+  while (split < 32 && nq * hq * split * 2 <= 148LL * LSRM_F32_FILL) split *= 2;
   unsigned blocks = (unsigned)ceil_div(nq * hq * split, 128);
   cudaStream_t st = as_stream(stream);
 #define LSRM_ATTN_CASE(D)                                                              \
