@@ -28,13 +28,13 @@ __device__ __forceinline__ void attend_range(const float* __restrict__ k,
     for (int c = 0; c < DH; ++c) s = fmaf(q[c], kr[c], s);
     s *= scale;
     if (s > m) {
-      float corr = expf(m - s);  // m = -inf -> 0
+      float corr = F32_EXP(m - s);  // m = -inf -> 0
       l *= corr;
 #pragma unroll
       for (int c = 0; c < DH; ++c) acc[c] *= corr;
       m = s;
     }
-    float p = expf(s - m);
+    float p = F32_EXP(s - m);
     l += p;
 #pragma unroll
     for (int c = 0; c < DH; ++c) acc[c] = fmaf(p, vr[c], acc[c]);
