@@ -13,6 +13,13 @@
 
 namespace lsrm {
 
+// LSRM_F32_FASTEXP: __expf (ex2.approx based) instead of the accurate expf
+#ifdef LSRM_F32_FASTEXP
+#define F32_EXP(x) __expf(x)
+#else
+#define F32_EXP(x) expf(x)
+#endif
+
 // keys lo, lo+S, ... of [lo, hi) after the first `skip` (this lane's share)
 template <int DH>
 __device__ __forceinline__ void attend_range(const float* __restrict__ k,
