@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(threads_of<HP, NP>(), 1) nsa_fused_kernel(cons
     // O accumulates in TMEM over a branch relative to the running max m_run;
     // m_run only moves (and O is rescaled) when the chunk max exceeds it by
     // more than 2^kHeadroom, so P <= 2^kHeadroom and rescales are rare.
-#ifndef LSRM_HEADROOM
+#ifndef LSRM_HEADROOM   // 16 measured identical (rescales are rare either way)
 #define LSRM_HEADROOM 8
 #endif
     constexpr float kHeadroom = (float)LSRM_HEADROOM;
